@@ -1,0 +1,84 @@
+"""Pin the C oracle against golden vectors from the unmodified reference.
+
+With ``qef="lapack"`` the oracle calls the same LAPACK dsyevd numpy.linalg.eigh
+uses (dualize.py:358) and must reproduce the reference bit-for-bit, mesh
+included.  With the default Jacobi QEF (the algorithm the GPU runs) every
+stage up to the QEF is still bit-exact; QEF positions agree to ~1e-14 h and
+split decisions may differ only where the reference's own concavity predicate
+(polygonize.py:47-75) is degenerate at the last ulp.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_util import cases, field_of, index, load
+
+ALL = cases()
+
+
+def _run(tag, qef):
+    field, lo, hi, R = field_of(tag)
+    return oracle.contour_oracle(field, lo, hi, R, qef=qef)
+
+
+EXACT_UPTO_QEF = ["labels", "edge_key", "v_in", "face_key", "face_n_crossing", "cells", "instance_edges",
+                  "t1d", "pos1d", "pos2", "status", "part_cell", "part_index", "cyc_off", "cyc_edges",
+                  "cyc_insts", "normals"]
+
+
+@pytest.mark.parametrize("tag", ALL)
+def test_oracle_lapack_bit_exact(tag):
+    if oracle.numpy_dsyevd() is None:
+        pytest.skip("numpy's LAPACK not loadable")
+    g = load(tag)
+    o = _run(tag, "lapack")
+    for k in EXACT_UPTO_QEF + ["qef_pos", "qef_rank", "split_cases", "raw_vertices", "raw_triangles",
+                               "raw_kind", "raw_ref", "vertices", "triangles", "kind", "ref"]:
+        assert np.array_equal(np.asarray(g[k]), np.asarray(o[k])), k
+    assert o["eval_counts"] == g["eval_counts"]
+    assert o["n_probes"] == g["n_probes"]
+
+
+@pytest.mark.parametrize("tag", ALL)
+def test_oracle_jacobi_matches_upto_qef(tag):
+    g = load(tag)
+    o = _run(tag, "jacobi")
+    for k in EXACT_UPTO_QEF:
+        assert np.array_equal(np.asarray(g[k]), np.asarray(o[k])), k
+    h = float(np.min(o["h"]))
+    assert np.abs(g["qef_pos"] - o["qef_pos"]).max() <= 1e-12 * h
+    assert np.array_equal(g["qef_rank"], o["qef_rank"])
+    flips = int(np.sum(g["split_cases"] != o["split_cases"]))
+    # degenerate (exactly coplanar, clamped) quads only; counted, bounded
+    assert flips <= 4, flips
+    if flips == 0:
+        assert np.array_equal(g["triangles"], o["triangles"])
+
+
+def test_known_answers():
+    kat = index()["kat"]
+    from paper_2409_13418_b200.fields import PlaneField, SphereField
+
+    o = oracle.contour_oracle(SphereField((0.5, 0.5, 0.5), 0.3), (0, 0, 0), (1, 1, 1), 2)
+    assert o["labels"].tolist() == kat["sphere_R2_labels"]
+    assert int(o["labels"].sum()) == 1 and o["labels"][13] == 1
+    o = oracle.contour_oracle(SphereField((0.5, 0.5, 0.5), 0.1), (0, 0, 0), (1, 1, 1), 4)
+    assert [len(o["edge_key"]), len(o["face_key"]), len(o["cells"])] == kat["single_vertex_R4"] == [6, 12, 8]
+    o = oracle.contour_oracle(PlaneField((0, 0, 0.3), (0, 0, 1)), (0, 0, 0), (1, 1, 1), 4)
+    assert len(o["edge_key"]) == kat["halfspace_R4_edges"] == 25
+
+
+def test_eval_accounting():
+    """S^3 + 15K + F4 + 46Q."""
+    g = load("rotated_box_64")
+    ec = g["eval_counts"]
+    S3 = 65**3
+    K = len(g["edge_key"])
+    Q = len(g["instance_edges"])
+    F4 = int(g["n_probes"])
+    assert ec["labels"] == {"batches": 1, "evals": S3}
+    assert ec["search_1d"] == {"batches": 15, "evals": 15 * K}
+    assert ec["probe_face_midpoint"] == {"batches": 1, "evals": Q}
+    assert ec["search_2d"] == {"batches": 30, "evals": 45 * Q}
+    assert ec["total_evals"] == S3 + 15 * K + F4 + 46 * Q
