@@ -1,0 +1,198 @@
+/*
+ * odc.h -- C-ABI of libodc, the B200-native Occupancy-Based Dual Contouring
+ * extraction path.  Plain pointers and sizes only; no torch or CUDA types.
+ *
+ * Reference interface each entry point replaces (paths relative to
+ * /root/reference/pkg/src/occmesh/):
+ *
+ *   odc_extract        pipeline.contour(field, grid, options, counter)
+ *                      pipeline.py:154-240 -- the whole extraction path:
+ *                      sample_labels (grid.py:109-126), extract_active
+ *                      (grid.py:171-296), find_1d_points (search.py:71-94),
+ *                      face_pairings (dualize.py:51-94), partition_cells
+ *                      (dualize.py:194-238), find_2d_points (search.py:194-322),
+ *                      build_plane_samples/estimate_normals (dualize.py:299-317,
+ *                      :402-429), place_3d_points/solve_qef_batch
+ *                      (dualize.py:332-372, :432-444), build_mesh
+ *                      (polygonize.py:110-217), repair_nonmanifold
+ *                      (polygonize.py:253-374).
+ *   odc_options        pipeline.ContourOptions + search.SearchBudget/LineBudget
+ *                      (pipeline.py:60-78, search.py:29-58).
+ *   odc_stats          ContourResult.stats + EvalCounter.snapshot()
+ *                      (pipeline.py:30-57, :160-239).
+ *   odc_field_*        the field argument: OccupancyField.eval_raw + iso_level +
+ *                      continuous (fields.py:51-61), lowered to a device program
+ *                      (analytic/CSG/smoothed, fields.py:64-242) or to MLP weights.
+ *   odc_eval_raw       EvalCounter.raw / eval_labels on the device (fields.py:35-48);
+ *                      also the shared-field hook for the parity oracle.
+ *   odc_copy_mesh      ContourResult.mesh / raw_mesh (TriangleMesh, mesh.py:11-76).
+ *   odc_copy_array     intermediate stage outputs (LabelVolume.labels, ActiveSets,
+ *                      Point1DBatch, Point2DBatch, CellPartitions, ...), for parity.
+ *
+ * Error codes map onto the reference's exception types (see ODC_E_*).
+ * Thread-safety: one odc_ctx per host thread; a context owns its device
+ * workspace and its last extraction's outputs.
+ */
+#ifndef ODC_H
+#define ODC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define ODC_OK 0
+#define ODC_E_ASSERT 1   /* AssertionError  (grid.py:252-253, search.py:234-238)   */
+#define ODC_E_CONTRACT 2 /* InternalContractError (dualize.py:23-24)               */
+#define ODC_E_CONFIG 3   /* ConfigurationError (pipeline.py:26-27, :72-78, :128)   */
+#define ODC_E_VALUE 4    /* ValueError (grid.py:28-31, fields.py:42-45)           */
+#define ODC_E_CUDA 5     /* CUDA runtime failure                                   */
+#define ODC_E_NOMEM 6    /* device allocation failure                              */
+#define ODC_E_ARG 7      /* bad argument to the C-ABI                              */
+
+/* field program opcodes (postfix; lowering in paper_2409_13418_b200/fields.py) */
+#define ODC_OP_END 0
+#define ODC_OP_SPHERE_SD 1
+#define ODC_OP_BOX_SD 2
+#define ODC_OP_TORUS_SD 3
+#define ODC_OP_PLANE_SD 4
+#define ODC_OP_SD2RAW 5
+#define ODC_OP_RAW_MAX 6
+#define ODC_OP_RAW_MIN 7
+#define ODC_OP_RAW_DIFF 8
+#define ODC_OP_RAW_COMPL 9
+#define ODC_OP_SD_MIN 10
+#define ODC_OP_SD_MAX 11
+#define ODC_OP_SD_DIFF 12
+#define ODC_OP_SD_NEG 13
+#define ODC_OP_XFORM_BEGIN 14
+#define ODC_OP_XFORM_END 15
+#define ODC_OP_SMOOTH 16
+#define ODC_MAX_NODES 256
+
+typedef struct {
+  int32_t op;
+  int32_t pad;
+  double p[16];
+} odc_node;
+
+/* MlpField (paper_2409_13418_b200/fields.py): weights as float32 host arrays,
+ * already bf16-representable. w0: (d_in, 256) row-major, w1..w7: (256, 256),
+ * w_head: (256). */
+typedef struct {
+  int32_t d_in, width, depth, n_freq;
+  const float* w0;
+  const float* w_hidden; /* (depth-1, 256, 256) */
+  const float* biases;   /* (depth, 256) */
+  const float* w_head;   /* (256) */
+  double b_head, amplitude, prior_scale, prior_radius;
+  double prior_center[3];
+} odc_mlp_desc;
+
+typedef struct odc_ctx odc_ctx;
+typedef struct odc_field odc_field;
+
+/* ContourOptions (pipeline.py:60-78); enums follow ONE_D_MODES etc. */
+#define ODC_ONE_D_MIDPOINT 0
+#define ODC_ONE_D_LINEAR 1
+#define ODC_ONE_D_BINARY 2
+#define ODC_NORMALS_FD 0
+#define ODC_NORMALS_2D 1
+#define ODC_SPLIT_MDC 0
+#define ODC_SPLIT_IC 1
+typedef struct {
+  int32_t one_d, normals, split, repair;
+  int32_t iters_1d, s1_lin, s1_bin, s2_lin, s2_bin;
+  int32_t keep_intermediates; /* keep stage outputs for odc_copy_array */
+  double s1_range, s2_range, qef_truncation, fd_step_factor;
+} odc_options;
+
+/* eval categories (EvalCounter, pipeline.py:30-57) */
+#define ODC_CAT_LABELS 0
+#define ODC_CAT_SEARCH_1D 1
+#define ODC_CAT_PROBE_FACE_CENTER 2
+#define ODC_CAT_PROBE_FACE_MIDPOINT 3
+#define ODC_CAT_SEARCH_2D 4
+#define ODC_CAT_FD_GRADIENT 5
+#define ODC_N_CAT 6
+
+typedef struct {
+  int64_t n_grid_vertices, boundary_inside_vertices;
+  int64_t n_crossing_edges, n_crossing_faces, n_face_center_probes, n_crossing_cells;
+  int64_t n_2d_points, n_partitions, n_plane_samples;
+  int64_t point2d_status_counts[4]; /* exact, midpoint-fallback, clamped, range-exhausted */
+  int64_t qef_rank_counts[4];       /* rank 0..3 */
+  int64_t split_case_counts[4];     /* index 1..3 */
+  double qef_max_residual;
+  int64_t normal_fallbacks, skipped_boundary_edges;
+  int64_t raw_n_vertices, raw_n_triangles, n_vertices, n_triangles;
+  int64_t repair_added_vertices, repair_passes;
+  int64_t eval_batches[ODC_N_CAT], eval_evals[ODC_N_CAT];
+  int32_t cat_order[ODC_N_CAT]; /* first-record order, -1 terminated */
+  int32_t n_kernel_launches;
+  float device_ms; /* CUDA-event time of the whole extraction on its stream */
+} odc_stats;
+
+int odc_version(void);
+int odc_create(int device, odc_ctx** out);
+void odc_destroy(odc_ctx* ctx);
+const char* odc_last_error(const odc_ctx* ctx);
+/* stream: a cudaStream_t passed as void* (NULL = the context's own stream) */
+int odc_set_stream(odc_ctx* ctx, void* stream);
+
+int odc_field_analytic(odc_ctx* ctx, const odc_node* nodes, int32_t n_nodes, int32_t continuous,
+                       double iso_level, odc_field** out);
+int odc_field_mlp(odc_ctx* ctx, const odc_mlp_desc* desc, odc_field** out);
+void odc_field_free(odc_ctx* ctx, odc_field* f);
+
+void odc_default_options(odc_options* o);
+int odc_extract(odc_ctx* ctx, const odc_field* field, const double lo[3], const double hi[3], int64_t resolution,
+                const odc_options* opt, odc_stats* stats);
+
+/* which: 0 = repaired mesh, 1 = raw (pre-repair) mesh.  Buffers sized from stats. */
+int odc_copy_mesh(odc_ctx* ctx, int32_t which, double* vertices, int64_t* triangles, int64_t* prov_kind,
+                  int64_t* prov_ref);
+/* zero-copy device view of the last mesh: vertices (V,3) f64, triangles (T,3) i32 */
+int odc_mesh_device(odc_ctx* ctx, int32_t which, const double** vertices, const int32_t** triangles,
+                    int64_t* n_vertices, int64_t* n_triangles);
+
+/* intermediate arrays (requires keep_intermediates) */
+#define ODC_ARR_LABELS 0         /* u8  (S^3)                          */
+#define ODC_ARR_EDGE_KEY 1       /* i64 (K)                            */
+#define ODC_ARR_FACE_KEY 2       /* i64 (F)                            */
+#define ODC_ARR_FACE_NCROSS 3    /* i64 (F)                            */
+#define ODC_ARR_CELLS 4          /* i64 (C)                            */
+#define ODC_ARR_INSTANCE_EDGES 5 /* i64 (Q,2)                          */
+#define ODC_ARR_T1D 6            /* f64 (K)                            */
+#define ODC_ARR_POS1D 7          /* f64 (K,3)                          */
+#define ODC_ARR_POS2 8           /* f64 (Q,2)                          */
+#define ODC_ARR_STATUS 9         /* u8  (Q)                            */
+#define ODC_ARR_PART_CELL 10     /* i64 (P)                            */
+#define ODC_ARR_PART_INDEX 11    /* i64 (P)                            */
+#define ODC_ARR_CYC_LEN 12       /* i64 (P) cycle length per partition */
+#define ODC_ARR_CYC_EDGES 13     /* i64 (Ns)                           */
+#define ODC_ARR_CYC_INSTS 14     /* i64 (Ns)                           */
+#define ODC_ARR_NORMALS 15       /* f64 (Ns,3)                         */
+#define ODC_ARR_QEF_POS 16       /* f64 (P,3)                          */
+#define ODC_ARR_QEF_RANK 17      /* i64 (P)                            */
+#define ODC_ARR_QEF_RESID 18     /* f64 (P)                            */
+#define ODC_ARR_SPLIT_CASES 19   /* i64 (n_interior)                   */
+#define ODC_ARR_V_IN 20          /* i64 (K)                            */
+#define ODC_ARR_MID_LABEL 21     /* u8  (Q)                            */
+#define ODC_ARR_POS3 22          /* f64 (Q,3)                          */
+#define ODC_N_ARR 23
+/* Returns the element count (not bytes) in *n_elems; copies if dst != NULL. */
+int odc_copy_array(odc_ctx* ctx, int32_t which, void* dst, int64_t dst_bytes, int64_t* n_elems);
+
+/* Batched field evaluation on the device: raw values (1.0/0.0 for analytic
+ * fields and for the MLP in shared-field mode) for host points (n,3) f64. */
+int odc_eval_raw(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, double* raw);
+/* Same, labels only (u8), for host points. */
+int odc_eval_labels(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, uint8_t* labels);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,957 @@
+// odc_api.cu -- libodc C-ABI (include/odc.h): contexts, device workspace,
+// field upload and the extraction driver (the device counterpart of
+// occmesh.pipeline.contour, pipeline.py:154-240).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/odc.h"
+#include "odc_kernels.h"
+#include "odc_mlp.h"
+#include "odc_tables.h"
+
+using namespace odc;
+
+namespace {
+
+// Bump allocator over retained device blocks.  reset() makes the whole
+// workspace available again; blocks are merged so a repeated extraction of
+// the same size never calls cudaMalloc.
+struct Arena {
+  struct Block {
+    char* p;
+    size_t size, used;
+  };
+  std::vector<Block> blocks;
+  size_t high_water = 0, live = 0;
+
+  ~Arena() {
+    for (auto& b : blocks) cudaFree(b.p);
+  }
+  void reset() {
+    size_t total = 0;
+    for (auto& b : blocks) total += b.size;
+    if (blocks.size() > 1) {
+      for (auto& b : blocks) cudaFree(b.p);
+      blocks.clear();
+      Block b{nullptr, total, 0};
+      if (cudaMalloc(&b.p, total) == cudaSuccess) blocks.push_back(b);
+    }
+    for (auto& b : blocks) b.used = 0;
+    live = 0;
+  }
+  void* alloc(size_t n) {
+    n = (n + 255) & ~(size_t)255;
+    if (n == 0) n = 256;
+    for (auto& b : blocks)
+      if (b.size - b.used >= n) {
+        void* p = b.p + b.used;
+        b.used += n;
+        live += n;
+        high_water = std::max(high_water, live);
+        return p;
+      }
+    size_t want = std::max(n, blocks.empty() ? (size_t)64 << 20 : blocks.back().size * 2);
+    Block b{nullptr, want, 0};
+    if (cudaMalloc(&b.p, want) != cudaSuccess) {
+      cudaGetLastError();
+      want = n;
+      b.size = n;
+      if (cudaMalloc(&b.p, want) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+    }
+    blocks.push_back(b);
+    return alloc(n);
+  }
+  template <typename T>
+  T* get(int64_t count) {
+    return static_cast<T*>(alloc(sizeof(T) * (size_t)std::max<int64_t>(count, 1)));
+  }
+};
+
+struct OdcError {
+  int code;
+  std::string msg;
+};
+
+}  // namespace
+
+struct odc_field {
+  int kind;  // 0 analytic, 1 MLP
+  odc_node* nodes = nullptr;
+  int32_t n_nodes = 0;
+  int32_t continuous = 0;
+  double iso = 0.5;
+  // MLP
+  uint16_t* w_packed = nullptr;
+  float* bias = nullptr;
+  float* w_head = nullptr;
+  MlpDev mlp{};
+};
+
+struct odc_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr, stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  Arena arena;
+  CellTabEntry* table = nullptr;
+  unsigned long long* h_pinned = nullptr;  // small readback buffer
+  std::string err;
+  int launches = 0;
+  // last extraction
+  bool valid = false;
+  GridP g{};
+  int64_t K = 0, Q = 0, C = 0, F = 0, F4 = 0, P = 0, Ns = 0, NF = 0, T = 0, V0 = 0, V1 = 0, n_interior = 0;
+  bool keep = false;
+  uint32_t* L = nullptr;
+  WordRec* rec = nullptr;
+  int64_t *edge_key = nullptr, *inst_key = nullptr, *cell_id = nullptr, *f4_key = nullptr, *face_key = nullptr,
+          *face_nc = nullptr;
+  int64_t* v_in = nullptr;
+  int64_t* inst_edges = nullptr;
+  double *t1d = nullptr, *pos1d = nullptr;
+  Stage2D s2{};
+  CellOut cells{};
+  double* verts0 = nullptr;  // raw mesh vertices
+  int32_t* tris0 = nullptr;
+  int64_t* src0 = nullptr;   // raw vertex -> pre-compaction index (nullptr = identity)
+  double* verts1 = nullptr;  // repaired
+  int32_t* tris1 = nullptr;
+  int64_t* fan_edge = nullptr;
+  uint8_t* kase = nullptr;
+  int64_t* split_cases = nullptr;
+};
+
+namespace {
+
+#define CUDA_TRY(x)                                                                         \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess) throw OdcError{ODC_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+template <typename T>
+T* need(T* p) {
+  if (!p) throw OdcError{ODC_E_NOMEM, "device workspace allocation failed"};
+  return p;
+}
+
+void check_launch(odc_ctx* c, int n = 1) {
+  c->launches += n;
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) throw OdcError{ODC_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+void readback(odc_ctx* c, const void* dev, size_t bytes) {
+  CUDA_TRY(cudaMemcpyAsync(c->h_pinned, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+}
+
+void check_status(odc_ctx* c, DevStatus* dst) {
+  readback(c, dst, sizeof(DevStatus));
+  DevStatus s;
+  std::memcpy(&s, c->h_pinned, sizeof s);
+  if (s.code == ODC_E_ASSERT)
+    throw OdcError{ODC_E_ASSERT, "2D search instance " + std::to_string(s.detail) +
+                                     ": no corner label differs from the midpoint"};
+  if (s.code) throw OdcError{s.code, "device status " + std::to_string(s.code)};
+}
+
+// Evaluate labels (and optionally raw) of n points through the field.
+void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* lab, double* raw) {
+  if (n == 0) return;
+  if (f->kind == 0) {
+    FieldP fp{f->nodes, f->n_nodes, 0, f->iso};
+    launch_eval_raw_analytic(fp, pts, n, raw, lab, c->stream);
+  } else {
+    PointSrc src{pts, GridP{}, 0};
+    mlp_eval(f->mlp, src, n, lab, raw, c->stream);
+  }
+  check_launch(c);
+}
+
+OptP make_opt(const odc_options* o, int continuous) {
+  OptP p{};
+  p.one_d = o->one_d;
+  p.normals = o->normals;
+  p.split = o->split;
+  p.iters_1d = o->iters_1d;
+  p.s1_lin = o->s1_lin;
+  p.s1_bin = o->s1_bin;
+  p.s2_lin = o->s2_lin;
+  p.s2_bin = o->s2_bin;
+  p.continuous = continuous;
+  p.s1_range = o->s1_range;
+  p.s2_range = o->s2_range;
+  p.qef_trunc = o->qef_truncation;
+  p.fd_step = o->fd_step_factor;
+  return p;
+}
+
+void record(odc_stats* st, int cat, int64_t batches, int64_t evals) {
+  int i = 0;
+  while (i < ODC_N_CAT && st->cat_order[i] >= 0 && st->cat_order[i] != cat) i++;
+  if (i < ODC_N_CAT && st->cat_order[i] < 0) st->cat_order[i] = cat;
+  st->eval_batches[cat] += batches;
+  st->eval_evals[cat] += evals;
+}
+
+void scan1(odc_ctx* c, const uint32_t* in, uint32_t* out, int64_t n, unsigned long long* totals) {
+  const uint32_t* ins[1] = {in};
+  uint32_t* outs[1] = {out};
+  uint32_t* tiles = need(c->arena.get<uint32_t>((n + 255) / 256 + 1));
+  launch_scan_u32(ins, outs, 1, n, tiles, totals, c->stream);
+  check_launch(c, 3);
+}
+void scan2(odc_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* oa, uint32_t* ob, int64_t n,
+           unsigned long long* totals) {
+  const uint32_t* ins[2] = {a, b};
+  uint32_t* outs[2] = {oa, ob};
+  uint32_t* tiles = need(c->arena.get<uint32_t>(2 * ((n + 255) / 256) + 2));
+  launch_scan_u32(ins, outs, 2, n, tiles, totals, c->stream);
+  check_launch(c, 3);
+}
+
+void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi[3], int64_t R,
+             const odc_options* o, odc_stats* st) {
+  // ---- validation: GridSpec (grid.py:24-31), ContourOptions.validate (pipeline.py:72-78)
+  if (R < 2) throw OdcError{ODC_E_VALUE, "resolution must be at least 2"};
+  for (int a = 0; a < 3; a++)
+    if (!(hi[a] > lo[a])) throw OdcError{ODC_E_VALUE, "grid box must have positive extent"};
+  if (o->one_d < 0 || o->one_d > 2) throw OdcError{ODC_E_CONFIG, "unknown 1D mode"};
+  if (o->normals < 0 || o->normals > 1) throw OdcError{ODC_E_CONFIG, "unknown normal mode"};
+  if (o->split < 0 || o->split > 1) throw OdcError{ODC_E_CONFIG, "unknown split mode"};
+  if (R > 1290) throw OdcError{ODC_E_VALUE, "resolution above 1290 exceeds the 32-bit vertex index space"};
+
+  std::memset(st, 0, sizeof *st);
+  for (int i = 0; i < ODC_N_CAT; i++) st->cat_order[i] = -1;
+  c->valid = false;
+  c->launches = 0;
+  c->arena.reset();
+  c->keep = o->keep_intermediates != 0;
+  cudaStream_t s = c->stream;
+  CUDA_TRY(cudaEventRecord(c->ev0, s));
+
+  GridP g{};
+  g.R = R;
+  g.S = R + 1;
+  g.S2 = g.S * g.S;
+  g.S3 = g.S2 * g.S;
+  g.W = (g.S + 31) / 32;
+  g.NW = g.S2 * g.W;
+  for (int a = 0; a < 3; a++) {
+    g.lo[a] = lo[a];
+    g.h[a] = (hi[a] - lo[a]) / (double)R;  // cell_size (grid.py:37-40)
+  }
+  c->g = g;
+  const OptP op = make_opt(o, f->continuous);
+  const FieldP fp{f->nodes, f->n_nodes, f->kind, f->iso};
+  const bool mlp = f->kind == 1;
+
+  DevStats* dst = need(c->arena.get<DevStats>(1));
+  DevStatus* dstat = need(c->arena.get<DevStatus>(1));
+  unsigned long long* totals = need(c->arena.get<unsigned long long>(8));
+  CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(DevStats), s));
+  CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), s));
+
+  // ---- K1: sample_labels (grid.py:109-126)
+  c->L = need(c->arena.get<uint32_t>(g.NW));
+  if (!mlp) {
+    launch_labels_analytic(g, fp, c->L, s);
+    check_launch(c);
+  } else {
+    uint8_t* bytes = need(c->arena.get<uint8_t>(g.S3));
+    PointSrc src{nullptr, g, 0};
+    mlp_eval(f->mlp, src, g.S3, bytes, nullptr, s);
+    check_launch(c);
+    launch_pack_labels(g, bytes, c->L, s);
+    check_launch(c);
+  }
+  record(st, ODC_CAT_LABELS, 1, g.S3);
+  st->n_grid_vertices = g.S3;
+
+  // ---- K2: extract_active (grid.py:171-296)
+  const int64_t nt = active_tiles(g);
+  c->rec = need(c->arena.get<WordRec>(g.NW));
+  uint32_t* tiles = need(c->arena.get<uint32_t>(5 * nt));
+  launch_active_bits(g, c->L, c->rec, tiles, dst, s);
+  launch_scan_tiles(tiles, nt, 5, totals, s);
+  check_launch(c, 2);
+  readback(c, totals, 5 * sizeof(unsigned long long));
+  const int64_t K = (int64_t)c->h_pinned[0], Q = (int64_t)c->h_pinned[1], C = (int64_t)c->h_pinned[2],
+                Fn = (int64_t)c->h_pinned[3], F4 = (int64_t)c->h_pinned[4];
+  if (K >= (1ll << 31) || Q >= (1ll << 31)) throw OdcError{ODC_E_VALUE, "crossing set exceeds 2^31 elements"};
+  c->K = K;
+  c->Q = Q;
+  c->C = C;
+  c->F = Fn;
+  c->F4 = F4;
+  c->edge_key = need(c->arena.get<int64_t>(K));
+  c->inst_key = need(c->arena.get<int64_t>(Q));
+  c->cell_id = need(c->arena.get<int64_t>(C));
+  c->f4_key = need(c->arena.get<int64_t>(F4));
+  c->face_key = c->keep ? need(c->arena.get<int64_t>(Fn)) : nullptr;
+  c->face_nc = c->keep ? need(c->arena.get<int64_t>(Fn)) : nullptr;
+  launch_active_compact(g, c->rec, tiles, c->edge_key, c->inst_key, c->cell_id, c->f4_key, c->face_key, c->face_nc,
+                        s);
+  check_launch(c);
+  st->n_crossing_edges = K;
+  st->n_crossing_faces = Fn;
+  st->n_crossing_cells = C;
+
+  auto finish_stats = [&]() {
+    readback(c, dst, sizeof(DevStats));
+    DevStats h;
+    std::memcpy(&h, c->h_pinned, sizeof h);
+    st->boundary_inside_vertices = (int64_t)h.boundary_inside;
+    for (int i = 0; i < 4; i++) {
+      st->point2d_status_counts[i] = (int64_t)h.status[i];
+      st->qef_rank_counts[i] = (int64_t)h.rank[i];
+      st->split_case_counts[i] = (int64_t)h.split[i];
+    }
+    double mr;
+    std::memcpy(&mr, &h.max_resid_bits, 8);
+    st->qef_max_residual = mr;
+    st->normal_fallbacks = (int64_t)h.normal_fallbacks;
+    st->skipped_boundary_edges = (int64_t)h.skipped;
+    CUDA_TRY(cudaEventRecord(c->ev1, s));
+    CUDA_TRY(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    st->device_ms = ms;
+    st->n_kernel_launches = c->launches;
+  };
+
+  if (K == 0) {  // pipeline.py:174-179
+    c->P = c->NF = c->T = c->V0 = c->V1 = c->Ns = c->n_interior = 0;
+    c->verts0 = c->verts1 = nullptr;
+    c->tris0 = c->tris1 = nullptr;
+    c->src0 = nullptr;
+    finish_stats();
+    c->valid = true;
+    return;
+  }
+
+  // ---- K3: 1D points (pipeline.py:94-123, search.py:71-94)
+  c->t1d = need(c->arena.get<double>(K));
+  c->pos1d = need(c->arena.get<double>(3 * K));
+  c->v_in = c->keep ? need(c->arena.get<int64_t>(K)) : nullptr;
+  if (!mlp) {
+    launch_search1d_analytic(g, fp, op, c->L, c->edge_key, K, c->t1d, c->pos1d, c->v_in, s);
+    check_launch(c);
+  } else {
+    double* lo1 = need(c->arena.get<double>(K));
+    double* hi1 = need(c->arena.get<double>(K));
+    double* pts = need(c->arena.get<double>(3 * K));
+    uint8_t* lab = need(c->arena.get<uint8_t>(K));
+    double *raw_in = nullptr, *raw_out = nullptr;
+    launch_search1d_init(g, c->L, c->edge_key, K, lo1, hi1, s);
+    check_launch(c);
+    if (op.one_d == ODC_ONE_D_BINARY) {
+      for (int it = 0; it < op.iters_1d; it++) {
+        launch_search1d_points(g, c->L, c->edge_key, K, lo1, hi1, pts, s);
+        check_launch(c);
+        eval_points(c, f, pts, K, lab, nullptr);
+        launch_search1d_update(K, lab, lo1, hi1, s);
+        check_launch(c);
+      }
+    } else if (op.one_d == ODC_ONE_D_LINEAR && f->continuous) {
+      // raw grid values at the endpoints (LabelVolume.raw, grid.py:115-123): lo=0 / hi=1 points
+      raw_in = need(c->arena.get<double>(K));
+      raw_out = need(c->arena.get<double>(K));
+      launch_edge_endpoints(g, c->L, c->edge_key, K, 0, pts, s);
+      eval_points(c, f, pts, K, lab, raw_in);
+      launch_edge_endpoints(g, c->L, c->edge_key, K, 1, pts, s);
+      eval_points(c, f, pts, K, lab, raw_out);
+      check_launch(c, 2);
+    }
+    launch_search1d_finish(g, op, c->L, c->edge_key, K, lo1, hi1, raw_in, raw_out, c->t1d, c->pos1d, c->v_in, s);
+    check_launch(c);
+  }
+  if (op.one_d == ODC_ONE_D_BINARY) record(st, ODC_CAT_SEARCH_1D, op.iters_1d, (int64_t)op.iters_1d * K);
+
+  // ---- face_pairings probes (dualize.py:59-70)
+  if (F4) {
+    if (!mlp) {
+      launch_face_center_analytic(g, fp, c->f4_key, F4, c->rec, s);
+      check_launch(c);
+    } else {
+      double* pts = need(c->arena.get<double>(3 * F4));
+      uint8_t* lab = need(c->arena.get<uint8_t>(F4));
+      launch_face_center_points(g, c->f4_key, F4, pts, s);
+      check_launch(c);
+      eval_points(c, f, pts, F4, lab, nullptr);
+      launch_face_center_scatter(g, c->f4_key, lab, F4, c->rec, s);
+      check_launch(c);
+    }
+    record(st, ODC_CAT_PROBE_FACE_CENTER, 1, F4);
+  }
+  st->n_face_center_probes = F4;
+
+  // ---- normals: 2D points (search.py:194-322) or fd gradient (pipeline.py:126-151)
+  double* edge_normals = nullptr;
+  c->inst_edges = c->keep ? need(c->arena.get<int64_t>(2 * Q)) : nullptr;
+  c->s2 = Stage2D{};
+  if (op.normals == ODC_NORMALS_2D) {
+    c->s2.pos3 = need(c->arena.get<double>(3 * Q));
+    if (c->keep) {
+      c->s2.pos2 = need(c->arena.get<double>(2 * Q));
+      c->s2.status = need(c->arena.get<uint8_t>(Q));
+      c->s2.mid = need(c->arena.get<uint8_t>(Q));
+    }
+    if (!mlp) {
+      launch_search2d_analytic(g, fp, op, c->L, c->rec, c->inst_key, Q, c->pos1d, c->s2, c->inst_edges, dst, dstat,
+                               s);
+      check_launch(c);
+    } else {
+      void* state = need(c->arena.alloc(search2d_state_bytes(Q)));
+      double* pts = need(c->arena.get<double>(6 * Q));
+      uint8_t* lab = need(c->arena.get<uint8_t>(2 * Q));
+      launch_search2d_lockstep_init(g, op, c->L, c->rec, c->inst_key, Q, c->pos1d, state, c->inst_edges, s);
+      check_launch(c);
+      const int nsteps = search2d_num_steps(op);
+      for (int step = 0; step < nsteps; step++) {
+        int64_t M = launch_search2d_lockstep_points(g, op, c->inst_key, Q, step, state, pts, s);
+        check_launch(c);
+        eval_points(c, f, pts, M, lab, nullptr);
+        launch_search2d_lockstep_update(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, s);
+        check_launch(c);
+      }
+      launch_search2d_lockstep_finish(g, op, c->L, c->rec, c->inst_key, Q, c->pos1d, state, c->s2, dst, s);
+      check_launch(c);
+    }
+    check_status(c, dstat);
+    record(st, ODC_CAT_PROBE_FACE_MIDPOINT, 1, Q);
+    record(st, ODC_CAT_SEARCH_2D, op.s1_lin + op.s1_bin + op.s2_lin + op.s2_bin,
+           (int64_t)(op.s1_lin + op.s1_bin) * Q + (int64_t)(op.s2_lin + op.s2_bin) * 2 * Q);
+    st->n_2d_points = Q;
+  } else {
+    if (!f->continuous)
+      throw OdcError{ODC_E_CONFIG, "fd-gradient normals require a field with continuous raw values"};
+    double* pts = need(c->arena.get<double>(18 * K));
+    double* raw = need(c->arena.get<double>(6 * K));
+    uint8_t* lab = need(c->arena.get<uint8_t>(6 * K));
+    launch_fd_points(g, op, c->pos1d, K, pts, s);
+    check_launch(c);
+    eval_points(c, f, pts, 6 * K, lab, raw);
+    edge_normals = need(c->arena.get<double>(3 * K));
+    launch_fd_normals(g, op, c->L, c->edge_key, K, raw, edge_normals, dst, s);
+    check_launch(c);
+    record(st, ODC_CAT_FD_GRADIENT, 1, 6 * K);
+    st->n_2d_points = 0;
+  }
+
+  // ---- K6: partitions + plane samples + QEF (dualize.py:194-444)
+  uint16_t* cfg = need(c->arena.get<uint16_t>(C));
+  uint32_t* ncyc = need(c->arena.get<uint32_t>(C));
+  uint32_t* nsamp = need(c->arena.get<uint32_t>(C));
+  uint32_t* pbase = need(c->arena.get<uint32_t>(C));
+  uint32_t* sbase = need(c->arena.get<uint32_t>(C));
+  launch_cell_config(g, c->L, c->rec, c->cell_id, C, c->table, cfg, ncyc, nsamp, s);
+  check_launch(c);
+  scan2(c, ncyc, nsamp, pbase, sbase, C, totals);
+  readback(c, totals, 2 * sizeof(unsigned long long));
+  const int64_t P = (int64_t)c->h_pinned[0], Ns = (int64_t)c->h_pinned[1];
+  c->P = P;
+  c->Ns = Ns;
+  st->n_partitions = P;
+  st->n_plane_samples = Ns;
+  // vertex buffer sized for the worst case of fan vertices (one per edge)
+  double* verts = need(c->arena.get<double>(3 * (P + K)));
+  CellOut co{};
+  co.verts = verts;
+  co.part_cell = need(c->arena.get<int64_t>(P));
+  co.part_index = need(c->arena.get<int64_t>(P));
+  co.pinfo = need(c->arena.get<uint64_t>(C));
+  if (c->keep) {
+    co.rank = need(c->arena.get<int64_t>(P));
+    co.resid = need(c->arena.get<double>(P));
+    co.cyc_edges = need(c->arena.get<int64_t>(Ns));
+    co.cyc_insts = need(c->arena.get<int64_t>(Ns));
+    co.normals = need(c->arena.get<double>(3 * Ns));
+    co.cyc_len = need(c->arena.get<int64_t>(P));
+  }
+  launch_cell_solve(g, op, c->L, c->rec, c->cell_id, C, c->table, cfg, pbase, sbase, c->pos1d, c->s2.pos3,
+                    edge_normals, co, dst, s);
+  check_launch(c);
+  c->cells = co;
+
+  // ---- K7: build_mesh (polygonize.py:110-217)
+  int4* pid4 = need(c->arena.get<int4>(K));
+  c->kase = need(c->arena.get<uint8_t>(K));
+  uint32_t* ntri = need(c->arena.get<uint32_t>(K));
+  uint32_t* nfan = need(c->arena.get<uint32_t>(K));
+  uint32_t* toff = need(c->arena.get<uint32_t>(K));
+  uint32_t* frank = need(c->arena.get<uint32_t>(K));
+  launch_poly_classify(g, op, c->L, c->rec, c->edge_key, K, co.pinfo, verts, pid4, c->kase, ntri, nfan, dst, s);
+  check_launch(c);
+  scan2(c, ntri, nfan, toff, frank, K, totals);
+  readback(c, totals, 2 * sizeof(unsigned long long));
+  const int64_t T = (int64_t)c->h_pinned[0], NF = (int64_t)c->h_pinned[1];
+  c->T = T;
+  c->NF = NF;
+  int32_t* tris = need(c->arena.get<int32_t>(3 * T));
+  c->fan_edge = need(c->arena.get<int64_t>(NF));
+  uint8_t* used = need(c->arena.get<uint8_t>(P + NF));
+  CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)(P + NF), s));
+  if (NF) CUDA_TRY(cudaMemsetAsync(used + P, 1, (size_t)NF, s));
+  launch_poly_emit(K, P, c->edge_key, pid4, c->kase, toff, frank, c->pos1d, verts, tris, c->fan_edge, used, s);
+  check_launch(c);
+  launch_count_used(used, P, dst, s);
+  check_launch(c);
+  if (c->keep) {
+    uint32_t* flag = need(c->arena.get<uint32_t>(K));
+    uint32_t* rank = need(c->arena.get<uint32_t>(K));
+    launch_interior_flags(K, c->kase, flag, s);
+    check_launch(c);
+    scan1(c, flag, rank, K, totals + 4);
+    readback(c, totals + 4, sizeof(unsigned long long));
+    c->n_interior = (int64_t)c->h_pinned[0];
+    c->split_cases = need(c->arena.get<int64_t>(c->n_interior));
+    launch_split_cases(K, c->kase, c->split_cases, rank, s);
+    check_launch(c);
+  }
+  readback(c, &dst->used_partitions, sizeof(unsigned long long));
+  const int64_t used_p = (int64_t)c->h_pinned[0];
+  int64_t V0 = P + NF;
+  c->src0 = nullptr;
+  if (used_p != P) {  // drop unreferenced vertices (polygonize.py:199-209)
+    uint32_t* u32 = need(c->arena.get<uint32_t>(V0));
+    uint32_t* nid = need(c->arena.get<uint32_t>(V0));
+    // widen used flags
+    std::vector<uint8_t> hu(V0);
+    CUDA_TRY(cudaMemcpyAsync(hu.data(), used, V0, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<uint32_t> hw(hu.begin(), hu.end());
+    CUDA_TRY(cudaMemcpyAsync(u32, hw.data(), 4 * V0, cudaMemcpyHostToDevice, s));
+    scan1(c, u32, nid, V0, totals + 5);
+    double* vc = need(c->arena.get<double>(3 * V0));
+    c->src0 = need(c->arena.get<int64_t>(V0));
+    launch_remap_vertices(V0, T, used, nid, verts, vc, tris, c->src0, s);
+    check_launch(c, 2);
+    V0 = used_p + NF;
+    verts = vc;
+  }
+  c->verts0 = verts;
+  c->tris0 = tris;
+  c->V0 = V0;
+  st->raw_n_vertices = V0;
+  st->raw_n_triangles = T;
+
+  // ---- K8: repair_nonmanifold (polygonize.py:253-374), up to 4 passes
+  c->verts1 = verts;
+  c->tris1 = tris;
+  int64_t curV = V0;
+  if (o->repair && T > 0) {
+    int32_t* cur = need(c->arena.get<int32_t>(3 * T));
+    CUDA_TRY(cudaMemcpyAsync(cur, tris, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
+    double* cv = verts;
+    int passes = 0;
+    for (int pass = 0; pass < 4; pass++) {
+      passes++;
+      uint32_t* deg = need(c->arena.get<uint32_t>(curV + 1));
+      uint32_t* off = need(c->arena.get<uint32_t>(curV + 1));
+      uint32_t* cursor = need(c->arena.get<uint32_t>(curV));
+      int32_t* inc = need(c->arena.get<int32_t>(3 * T));
+      uint32_t* extra = need(c->arena.get<uint32_t>(curV + 1));
+      uint32_t* eoff = need(c->arena.get<uint32_t>(curV + 1));
+      CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (curV + 1), s));
+      CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * curV, s));
+      CUDA_TRY(cudaMemsetAsync(extra, 0, sizeof(uint32_t) * (curV + 1), s));
+      launch_vertex_degree(cur, T, deg, s);
+      check_launch(c);
+      scan1(c, deg, off, curV + 1, totals + 6);
+      launch_vertex_fill(cur, T, off, cursor, inc, s);
+      check_launch(c);
+      launch_repair_count(cv, cur, curV, off, inc, extra, dst, s);
+      check_launch(c);
+      scan1(c, extra, eoff, curV + 1, totals + 7);
+      readback(c, totals + 7, sizeof(unsigned long long));
+      const int64_t E = (int64_t)c->h_pinned[0];
+      readback(c, &dst->repair_overflow, sizeof(unsigned long long));
+      if (c->h_pinned[0]) throw OdcError{ODC_E_CONTRACT, "repair: a vertex fan exceeds 64 triangles"};
+      if (E == 0) break;
+      int32_t* next = need(c->arena.get<int32_t>(3 * T));
+      CUDA_TRY(cudaMemcpyAsync(next, cur, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
+      int64_t* src_new = need(c->arena.get<int64_t>(E));
+      launch_repair_apply(cv, cur, curV, off, inc, eoff, next, src_new, s);
+      check_launch(c);
+      double* nv = need(c->arena.get<double>(3 * (curV + E)));
+      CUDA_TRY(cudaMemcpyAsync(nv, cv, sizeof(double) * 3 * curV, cudaMemcpyDeviceToDevice, s));
+      launch_copy_vertices(cv, src_new, curV, E, nv, s);
+      check_launch(c);
+      cur = next;
+      cv = nv;
+      curV += E;
+    }
+    c->verts1 = cv;
+    c->tris1 = cur;
+    st->repair_passes = passes;
+  }
+  c->V1 = curV;
+  st->n_vertices = curV;
+  st->n_triangles = T;
+  st->repair_added_vertices = curV - V0;
+  finish_stats();
+  c->valid = true;
+}
+
+int guard(odc_ctx* c, int (*fn)(odc_ctx*, void*), void* arg) {
+  try {
+    return fn(c, arg);
+  } catch (const OdcError& e) {
+    c->err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    c->err = "host allocation failed";
+    return ODC_E_NOMEM;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int odc_version(void) { return 1; }
+
+int odc_create(int device, odc_ctx** out) {
+  if (!out) return ODC_E_ARG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return ODC_E_CUDA;
+  }
+  if (device < 0 || device >= n) return ODC_E_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return ODC_E_CUDA;
+  odc_ctx* c = new (std::nothrow) odc_ctx();
+  if (!c) return ODC_E_NOMEM;
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess || cudaEventCreate(&c->ev0) != cudaSuccess ||
+      cudaEventCreate(&c->ev1) != cudaSuccess || cudaMallocHost(&c->h_pinned, 4096) != cudaSuccess) {
+    delete c;
+    return ODC_E_CUDA;
+  }
+  c->stream = c->own;
+  std::vector<CellTabEntry> tab(kTableSize);
+  if (build_cell_table(tab.data()) != 0) {
+    delete c;
+    return ODC_E_CONTRACT;
+  }
+  if (cudaMalloc(&c->table, sizeof(CellTabEntry) * kTableSize) != cudaSuccess ||
+      cudaMemcpy(c->table, tab.data(), sizeof(CellTabEntry) * kTableSize, cudaMemcpyHostToDevice) != cudaSuccess) {
+    delete c;
+    return ODC_E_CUDA;
+  }
+  *out = c;
+  return ODC_OK;
+}
+
+void odc_destroy(odc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->table) cudaFree(c->table);
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+}
+
+const char* odc_last_error(const odc_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int odc_set_stream(odc_ctx* c, void* stream) {
+  if (!c) return ODC_E_ARG;
+  c->stream = stream ? (cudaStream_t)stream : c->own;
+  return ODC_OK;
+}
+
+void odc_default_options(odc_options* o) {
+  std::memset(o, 0, sizeof *o);
+  o->one_d = ODC_ONE_D_BINARY;
+  o->normals = ODC_NORMALS_2D;
+  o->split = ODC_SPLIT_IC;
+  o->repair = 1;
+  o->iters_1d = 15;
+  o->s1_lin = 4;
+  o->s1_bin = 11;
+  o->s2_lin = 3;
+  o->s2_bin = 12;
+  o->s1_range = 0.8;
+  o->s2_range = 0.70710678118654757;  // math.sqrt(2.0) / 2.0
+  o->qef_truncation = 0.1;
+  o->fd_step_factor = 0.01;
+}
+
+int odc_field_analytic(odc_ctx* c, const odc_node* nodes, int32_t n_nodes, int32_t continuous, double iso,
+                       odc_field** out) {
+  if (!c || !out || !nodes || n_nodes <= 0 || n_nodes > ODC_MAX_NODES) return ODC_E_ARG;
+  cudaSetDevice(c->device);
+  odc_field* f = new (std::nothrow) odc_field();
+  if (!f) return ODC_E_NOMEM;
+  f->kind = 0;
+  f->n_nodes = n_nodes;
+  f->continuous = continuous;
+  f->iso = iso;
+  if (cudaMalloc(&f->nodes, sizeof(odc_node) * n_nodes) != cudaSuccess ||
+      cudaMemcpyAsync(f->nodes, nodes, sizeof(odc_node) * n_nodes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
+    c->err = "field upload failed";
+    delete f;
+    return ODC_E_CUDA;
+  }
+  *out = f;
+  return ODC_OK;
+}
+
+int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
+  if (!c || !d || !out) return ODC_E_ARG;
+  if (d->width != 256 || d->depth != 8 || d->d_in != 39 || d->n_freq != 6) {
+    c->err = "the device MLP is specialised to d_in=39, 8 x 256";
+    return ODC_E_ARG;
+  }
+  cudaSetDevice(c->device);
+  odc_field* f = new (std::nothrow) odc_field();
+  if (!f) return ODC_E_NOMEM;
+  f->kind = 1;
+  f->continuous = 1;
+  f->iso = 0.5;
+  const size_t ne = mlp_packed_weight_elems();
+  std::vector<uint16_t> packed(ne);
+  mlp_pack_weights(d->w0, d->d_in, d->w_hidden, packed.data());
+  if (cudaMalloc(&f->w_packed, ne * 2) != cudaSuccess || cudaMalloc(&f->bias, 8 * 256 * 4) != cudaSuccess ||
+      cudaMalloc(&f->w_head, 256 * 4) != cudaSuccess) {
+    c->err = "field upload failed";
+    delete f;
+    return ODC_E_NOMEM;
+  }
+  cudaMemcpy(f->w_packed, packed.data(), ne * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(f->bias, d->biases, 8 * 256 * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(f->w_head, d->w_head, 256 * 4, cudaMemcpyHostToDevice);
+  f->mlp.w_packed = f->w_packed;
+  f->mlp.bias = f->bias;
+  f->mlp.w_head = f->w_head;
+  f->mlp.b_head = (float)d->b_head;
+  f->mlp.amplitude = d->amplitude;
+  f->mlp.prior_scale = d->prior_scale;
+  f->mlp.prior_radius = d->prior_radius;
+  for (int i = 0; i < 3; i++) f->mlp.prior_center[i] = d->prior_center[i];
+  *out = f;
+  return ODC_OK;
+}
+
+void odc_field_free(odc_ctx* c, odc_field* f) {
+  if (!f) return;
+  if (c) cudaStreamSynchronize(c->stream);
+  cudaFree(f->nodes);
+  cudaFree(f->w_packed);
+  cudaFree(f->bias);
+  cudaFree(f->w_head);
+  delete f;
+}
+
+struct ExtractArgs {
+  const odc_field* f;
+  const double* lo;
+  const double* hi;
+  int64_t R;
+  const odc_options* o;
+  odc_stats* st;
+};
+
+int odc_extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi[3], int64_t R,
+                const odc_options* o, odc_stats* st) {
+  if (!c || !f || !lo || !hi || !st) return ODC_E_ARG;
+  odc_options def;
+  odc_default_options(&def);
+  ExtractArgs a{f, lo, hi, R, o ? o : &def, st};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    ExtractArgs* x = (ExtractArgs*)p;
+    extract(cc, x->f, x->lo, x->hi, x->R, x->o, x->st);
+    return (int)ODC_OK;
+  }, &a);
+}
+
+struct CopyMeshArgs {
+  int32_t which;
+  double* v;
+  int64_t* t;
+  int64_t* kind;
+  int64_t* ref;
+};
+
+int odc_copy_mesh(odc_ctx* c, int32_t which, double* vertices, int64_t* triangles, int64_t* prov_kind,
+                  int64_t* prov_ref) {
+  if (!c) return ODC_E_ARG;
+  if (!c->valid) {
+    c->err = "no extraction result";
+    return ODC_E_ARG;
+  }
+  CopyMeshArgs a{which, vertices, triangles, prov_kind, prov_ref};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    CopyMeshArgs* x = (CopyMeshArgs*)p;
+    const bool raw = x->which == 1;
+    const int64_t V = raw ? cc->V0 : cc->V1, T = cc->T;
+    const double* dv = raw ? cc->verts0 : cc->verts1;
+    const int32_t* dt = raw ? cc->tris0 : cc->tris1;
+    cudaStream_t s = cc->stream;
+    if (x->v && V) CUDA_TRY(cudaMemcpyAsync(x->v, dv, sizeof(double) * 3 * V, cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> t32;
+    if (x->t && T) {
+      t32.resize(3 * T);
+      CUDA_TRY(cudaMemcpyAsync(t32.data(), dt, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<int64_t> kind, ref;
+    if ((x->kind || x->ref) && cc->V0) {
+      int64_t* dk = need(cc->arena.get<int64_t>(cc->V0));
+      int64_t* dr = need(cc->arena.get<int64_t>(2 * cc->V0));
+      launch_provenance(cc->V0, cc->P, cc->src0, cc->cells.part_cell, cc->cells.part_index, cc->fan_edge, dk, dr, s);
+      kind.resize(cc->V0);
+      ref.resize(2 * cc->V0);
+      CUDA_TRY(cudaMemcpyAsync(kind.data(), dk, 8 * cc->V0, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaMemcpyAsync(ref.data(), dr, 16 * cc->V0, cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (x->t)
+      for (int64_t i = 0; i < 3 * T; i++) x->t[i] = t32[i];
+    if (x->kind || x->ref) {
+      for (int64_t i = 0; i < V; i++) {
+        const bool dup = i >= cc->V0;
+        if (x->kind) x->kind[i] = dup ? 2 : kind[i];
+        if (x->ref) {
+          x->ref[2 * i] = dup ? -1 : ref[2 * i];
+          x->ref[2 * i + 1] = dup ? -1 : ref[2 * i + 1];
+        }
+      }
+    }
+    return (int)ODC_OK;
+  }, &a);
+}
+
+int odc_mesh_device(odc_ctx* c, int32_t which, const double** v, const int32_t** t, int64_t* nv, int64_t* nt) {
+  if (!c || !c->valid) return ODC_E_ARG;
+  const bool raw = which == 1;
+  if (v) *v = raw ? c->verts0 : c->verts1;
+  if (t) *t = raw ? c->tris0 : c->tris1;
+  if (nv) *nv = raw ? c->V0 : c->V1;
+  if (nt) *nt = c->T;
+  return ODC_OK;
+}
+
+struct CopyArrArgs {
+  int32_t which;
+  void* dst;
+  int64_t bytes;
+  int64_t* n;
+};
+
+int odc_copy_array(odc_ctx* c, int32_t which, void* dst, int64_t dst_bytes, int64_t* n_elems) {
+  if (!c || !n_elems) return ODC_E_ARG;
+  if (!c->valid) {
+    c->err = "no extraction result";
+    return ODC_E_ARG;
+  }
+  CopyArrArgs a{which, dst, dst_bytes, n_elems};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    CopyArrArgs* x = (CopyArrArgs*)p;
+    const void* src = nullptr;
+    int64_t n = 0, esize = 8;
+    const bool has1d = cc->K > 0;
+    std::vector<uint8_t> unpack;
+    switch (x->which) {
+      case ODC_ARR_LABELS: {
+        n = cc->g.S3;
+        esize = 1;
+        if (x->dst) {
+          uint8_t* b = need(cc->arena.get<uint8_t>(n));
+          launch_unpack_labels(cc->g, cc->L, b, cc->stream);
+          src = b;
+        }
+        break;
+      }
+      case ODC_ARR_EDGE_KEY: src = cc->edge_key; n = cc->K; break;
+      case ODC_ARR_V_IN: src = cc->v_in; n = cc->v_in ? cc->K : 0; break;
+      case ODC_ARR_FACE_KEY: src = cc->face_key; n = cc->face_key ? cc->F : 0; break;
+      case ODC_ARR_FACE_NCROSS: src = cc->face_nc; n = cc->face_nc ? cc->F : 0; break;
+      case ODC_ARR_CELLS: src = cc->cell_id; n = cc->C; break;
+      case ODC_ARR_INSTANCE_EDGES: src = cc->inst_edges; n = (cc->inst_edges && has1d) ? 2 * cc->Q : 0; break;
+      case ODC_ARR_T1D: src = cc->t1d; n = has1d ? cc->K : 0; break;
+      case ODC_ARR_POS1D: src = cc->pos1d; n = has1d ? 3 * cc->K : 0; break;
+      case ODC_ARR_POS2: src = cc->s2.pos2; n = (cc->s2.pos2 && has1d) ? 2 * cc->Q : 0; break;
+      case ODC_ARR_POS3: src = cc->s2.pos3; n = (cc->s2.pos3 && has1d) ? 3 * cc->Q : 0; break;
+      case ODC_ARR_STATUS: src = cc->s2.status; n = (cc->s2.status && has1d) ? cc->Q : 0; esize = 1; break;
+      case ODC_ARR_MID_LABEL: src = cc->s2.mid; n = (cc->s2.mid && has1d) ? cc->Q : 0; esize = 1; break;
+      case ODC_ARR_PART_CELL: src = cc->cells.part_cell; n = has1d ? cc->P : 0; break;
+      case ODC_ARR_PART_INDEX: src = cc->cells.part_index; n = has1d ? cc->P : 0; break;
+      case ODC_ARR_CYC_EDGES: src = cc->cells.cyc_edges; n = (cc->cells.cyc_edges && has1d) ? cc->Ns : 0; break;
+      case ODC_ARR_CYC_INSTS: src = cc->cells.cyc_insts; n = (cc->cells.cyc_insts && has1d) ? cc->Ns : 0; break;
+      case ODC_ARR_NORMALS: src = cc->cells.normals; n = (cc->cells.normals && has1d) ? 3 * cc->Ns : 0; break;
+      case ODC_ARR_QEF_POS: src = cc->cells.verts; n = has1d ? 3 * cc->P : 0; break;
+      case ODC_ARR_QEF_RANK: src = cc->cells.rank; n = (cc->cells.rank && has1d) ? cc->P : 0; break;
+      case ODC_ARR_QEF_RESID: src = cc->cells.resid; n = (cc->cells.resid && has1d) ? cc->P : 0; break;
+      case ODC_ARR_SPLIT_CASES: src = cc->split_cases; n = (cc->split_cases && has1d) ? cc->n_interior : 0; break;
+      case ODC_ARR_CYC_LEN: src = cc->cells.cyc_len; n = (cc->cells.cyc_len && has1d) ? cc->P : 0; break;
+      default: throw OdcError{ODC_E_ARG, "unknown array id"};
+    }
+    *x->n = n;
+    if (x->dst && n) {
+      if (!src) throw OdcError{ODC_E_ARG, "array not kept (set keep_intermediates)"};
+      if (x->bytes < esize * n) throw OdcError{ODC_E_ARG, "destination too small"};
+      CUDA_TRY(cudaMemcpyAsync(x->dst, src, (size_t)(esize * n), cudaMemcpyDeviceToHost, cc->stream));
+      CUDA_TRY(cudaStreamSynchronize(cc->stream));
+    }
+    return (int)ODC_OK;
+  }, &a);
+}
+
+struct EvalArgs {
+  const odc_field* f;
+  const double* pts;
+  int64_t n;
+  double* raw;
+  uint8_t* lab;
+};
+
+static int eval_common(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, double* raw, uint8_t* lab) {
+  if (!c || !f || (!pts && n)) return ODC_E_ARG;
+  EvalArgs a{f, pts, n, raw, lab};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    EvalArgs* x = (EvalArgs*)p;
+    if (x->n == 0) return (int)ODC_OK;
+    // eval_labels rejects non-finite points (fields.py:42-45)
+    for (int64_t i = 0; i < 3 * x->n; i++)
+      if (!std::isfinite(x->pts[i])) throw OdcError{ODC_E_VALUE, "non-finite query point at index " + std::to_string(i / 3)};
+    cc->valid = false;  // the evaluation reuses the workspace
+    cc->arena.reset();
+    double* dp = need(cc->arena.get<double>(3 * x->n));
+    double* dr = x->raw ? need(cc->arena.get<double>(x->n)) : nullptr;
+    uint8_t* dl = need(cc->arena.get<uint8_t>(x->n));
+    CUDA_TRY(cudaMemcpyAsync(dp, x->pts, sizeof(double) * 3 * x->n, cudaMemcpyHostToDevice, cc->stream));
+    eval_points(cc, x->f, dp, x->n, dl, dr);
+    if (x->raw) CUDA_TRY(cudaMemcpyAsync(x->raw, dr, sizeof(double) * x->n, cudaMemcpyDeviceToHost, cc->stream));
+    if (x->lab) CUDA_TRY(cudaMemcpyAsync(x->lab, dl, x->n, cudaMemcpyDeviceToHost, cc->stream));
+    CUDA_TRY(cudaStreamSynchronize(cc->stream));
+    return (int)ODC_OK;
+  }, &a);
+}
+
+int odc_eval_raw(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, double* raw) {
+  return eval_common(c, f, pts, n, raw, nullptr);
+}
+int odc_eval_labels(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* labels) {
+  return eval_common(c, f, pts, n, nullptr, labels);
+}
+
+}  // extern "C"

@@ -1,0 +1,275 @@
+// odc_device.cuh -- shared device definitions for the ODC extraction kernels.
+//
+// Numerics: every fp64 expression that mirrors a numpy expression of the
+// reference is written in numpy's evaluation order and this translation unit
+// is compiled with --fmad=false, so no multiply/add pair is contracted.  Explicit
+// fma() appears only where the reference's BLAS uses one (OpenBLAS dgemm for
+// (N,3)@(3,3), ddot) -- see SURVEY.md Appendix A.
+#pragma once
+#include <cstdint>
+
+#include "../../include/odc.h"
+
+namespace odc {
+
+constexpr int kMaxValueStack = 32;
+constexpr int kMaxPointStack = 8;
+
+// ---------------------------------------------------------------------------
+// grid (grid.py:17-91): vertex id = x + y*S + z*S^2, h = (hi - lo) / R,
+// position = lo + coord * h.  Bit-packed rows: a row is (y, z), W 32-bit words
+// cover x in [0, 32W); word index = (z*S + y)*W + x/32.
+// ---------------------------------------------------------------------------
+struct GridP {
+  int64_t R, S, S2, S3;
+  int64_t W;   // words per row
+  int64_t NW;  // S*S*W
+  double lo[3], h[3];
+};
+
+// Per-word record of every derived bitmap plus the exclusive ranks of the
+// word's first element (edges, 2D-point instances, cells).  One 64-byte
+// record per word: a rank lookup touches one record.
+struct __align__(16) WordRec {
+  uint32_t e[3];   // crossing edges by axis, bit at the lower vertex
+  uint32_t f[3];   // crossing faces (2 or 4 crossing edges) by normal axis
+  uint32_t f4[3];  // faces with 4 crossing edges
+  uint32_t cf[3];  // face-centre labels of 4-crossing faces
+  uint32_t cell;   // crossing cells (bit at the cell's base vertex)
+  uint32_t pe, pq, pc;  // exclusive prefix: edges, instances, cells
+};
+static_assert(sizeof(WordRec) == 64, "WordRec must be one 64-byte record");
+
+__device__ __forceinline__ int64_t word_of(const GridP& g, int64_t x, int64_t y, int64_t z) {
+  return (z * g.S + y) * g.W + (x >> 5);
+}
+__device__ __forceinline__ void vid_coords(const GridP& g, int64_t vid, int64_t c[3]) {
+  c[0] = vid % g.S;
+  c[1] = (vid / g.S) % g.S;
+  c[2] = vid / g.S2;
+}
+__device__ __forceinline__ int64_t vstep(const GridP& g, int a) { return a == 0 ? 1 : (a == 1 ? g.S : g.S2); }
+__device__ __forceinline__ double gpos(const GridP& g, int a, int64_t c) {
+  return __dadd_rn(g.lo[a], __dmul_rn((double)c, g.h[a]));
+}
+__device__ __forceinline__ void vposition(const GridP& g, int64_t vid, double p[3]) {
+  int64_t c[3];
+  vid_coords(g, vid, c);
+#pragma unroll
+  for (int a = 0; a < 3; a++) p[a] = gpos(g, a, c[a]);
+}
+__device__ __forceinline__ uint32_t label_at(const uint32_t* L, const GridP& g, int64_t vid) {
+  int64_t c[3];
+  vid_coords(g, vid, c);
+  return (L[word_of(g, c[0], c[1], c[2])] >> (c[0] & 31)) & 1u;
+}
+__device__ __forceinline__ uint32_t lowmask(int bit) { return bit == 0 ? 0u : (0xffffffffu >> (32 - bit)); }
+
+// rank of crossing edge (vid, axis) in ascending edge-key order
+__device__ __forceinline__ int64_t edge_rank(const WordRec* rec, const GridP& g, int64_t vid, int axis) {
+  int64_t c[3];
+  vid_coords(g, vid, c);
+  const WordRec& r = rec[word_of(g, c[0], c[1], c[2])];
+  int bit = (int)(c[0] & 31);
+  uint32_t m = lowmask(bit);
+  int64_t k = (int64_t)r.pe + __popc(r.e[0] & m) + __popc(r.e[1] & m) + __popc(r.e[2] & m);
+  for (int a = 0; a < axis; a++) k += (r.e[a] >> bit) & 1u;
+  return k;
+}
+// id of the first 2D-point instance of face (vid, normal): instances are
+// numbered in face-key order, two per 4-crossing face (dualize.py:72-88)
+__device__ __forceinline__ int64_t inst_rank(const WordRec* rec, const GridP& g, int64_t vid, int n) {
+  int64_t c[3];
+  vid_coords(g, vid, c);
+  const WordRec& r = rec[word_of(g, c[0], c[1], c[2])];
+  int bit = (int)(c[0] & 31);
+  uint32_t m = lowmask(bit);
+  int64_t k = (int64_t)r.pq;
+#pragma unroll
+  for (int a = 0; a < 3; a++) k += __popc(r.f[a] & m) + __popc(r.f4[a] & m);
+  for (int a = 0; a < n; a++) k += ((r.f[a] >> bit) & 1u) + ((r.f4[a] >> bit) & 1u);
+  return k;
+}
+__device__ __forceinline__ int64_t cell_rank(const WordRec* rec, const GridP& g, int64_t base_vid) {
+  int64_t c[3];
+  vid_coords(g, base_vid, c);
+  const WordRec& r = rec[word_of(g, c[0], c[1], c[2])];
+  int bit = (int)(c[0] & 31);
+  return (int64_t)r.pc + __popc(r.cell & lowmask(bit));
+}
+
+// ---------------------------------------------------------------------------
+// field programs (fields.py:64-242)
+// ---------------------------------------------------------------------------
+struct FieldP {
+  const odc_node* nodes;  // device
+  int32_t n_nodes;
+  int32_t kind;  // 0 analytic program, 1 MLP
+  double iso;
+};
+
+// glibc 2.39 hypot (x86-64 baseline build): Borges' corrected sqrt kernel,
+// reproduced bit-for-bit (checked on 2e7 random pairs against libm).
+static __device__ __forceinline__ double hypot_glibc(double x, double y) {
+  x = fabs(x);
+  y = fabs(y);
+  double ax = x < y ? y : x, ay = x < y ? x : y;
+  if (ay <= __dmul_rn(ax, 0x1p-54)) return __dadd_rn(ax, ay);
+  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+  double t1, t2;
+  if (h <= __dmul_rn(2.0, ay)) {
+    double delta = __dsub_rn(h, ay);
+    t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, delta), ax));
+    t2 = __dmul_rn(__dsub_rn(delta, __dmul_rn(2.0, __dsub_rn(ax, ay))), delta);
+  } else {
+    double delta = __dsub_rn(h, ax);
+    t1 = __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+    t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, delta), ay), ay), __dmul_rn(delta, delta));
+  }
+  return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+}
+
+// sqrt((x0*x0 + x1*x1) + x2*x2): numpy linalg.norm over the last axis of (N,3)
+__device__ __forceinline__ double norm3(const double x[3]) {
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x[0], x[0]), __dmul_rn(x[1], x[1])), __dmul_rn(x[2], x[2])));
+}
+// einsum('ij,ij->i') with three terms: (p0 + p2) + p1
+__device__ __forceinline__ double einsum3(const double a[3], const double b[3]) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[2], b[2])), __dmul_rn(a[1], b[1]));
+}
+__device__ __forceinline__ double dot3_fma(const double a[3], const double b[3]) {
+  return fma(a[2], b[2], fma(a[1], b[1], __dmul_rn(a[0], b[0])));
+}
+__device__ __forceinline__ void cross3(const double a[3], const double b[3], double o[3]) {
+  o[0] = __dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1]));
+  o[1] = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
+  o[2] = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
+}
+// (p - c) @ R with OpenBLAS dgemm's fma chain (fields.py:107, :179)
+__device__ __forceinline__ void rot_rows(const double l[3], const double* R, double o[3]) {
+#pragma unroll
+  for (int j = 0; j < 3; j++) o[j] = fma(l[2], R[6 + j], fma(l[1], R[3 + j], __dmul_rn(l[0], R[j])));
+}
+
+static __device__ __noinline__ double field_raw_prog(const odc_node* __restrict__ nodes, int n_nodes, const double pt[3]) {
+  double st[kMaxValueStack];
+  double pst[kMaxPointStack][3];
+  int sp = 0, pp = 0;
+  double p[3] = {pt[0], pt[1], pt[2]};
+  for (int i = 0; i < n_nodes; i++) {
+    const int op = __ldg(&nodes[i].op);
+    const double* q = nodes[i].p;
+    switch (op) {
+      case ODC_OP_SPHERE_SD: {  // fields.py:80-82
+        double d[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+        st[sp++] = __dsub_rn(norm3(d), __ldg(q + 3));
+        break;
+      }
+      case ODC_OP_BOX_SD: {  // fields.py:103-111
+        double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+        if (__ldg(q + 6) != 0.0) {
+          double R[9], o[3];
+          for (int j = 0; j < 9; j++) R[j] = __ldg(q + 7 + j);
+          rot_rows(l, R, o);
+          l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
+        }
+        double qq[3], mq[3];
+        for (int a = 0; a < 3; a++) {
+          qq[a] = __dsub_rn(fabs(l[a]), __ldg(q + 3 + a));
+          mq[a] = qq[a] > 0.0 ? qq[a] : 0.0;
+        }
+        double outside = norm3(mq);
+        double mx = qq[0];
+        if (qq[1] > mx) mx = qq[1];
+        if (qq[2] > mx) mx = qq[2];
+        double inside = mx < 0.0 ? mx : 0.0;
+        st[sp++] = __dadd_rn(outside, inside);
+        break;
+      }
+      case ODC_OP_TORUS_SD: {  // fields.py:122-126
+        double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+        double ring = __dsub_rn(hypot_glibc(l[0], l[1]), __ldg(q + 3));
+        st[sp++] = __dsub_rn(hypot_glibc(ring, l[2]), __ldg(q + 4));
+        break;
+      }
+      case ODC_OP_PLANE_SD: {  // fields.py:138-139 (dgemv)
+        double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+        double nn[3] = {__ldg(q + 3), __ldg(q + 4), __ldg(q + 5)};
+        st[sp++] = dot3_fma(l, nn);
+        break;
+      }
+      case ODC_OP_SD2RAW: st[sp - 1] = st[sp - 1] < 0.0 ? 1.0 : 0.0; break;  // fields.py:70-72
+      case ODC_OP_RAW_MAX:
+      case ODC_OP_SD_MAX: {
+        double b = st[--sp], a = st[sp - 1];
+        st[sp - 1] = (a >= b) ? a : b;
+        break;
+      }
+      case ODC_OP_RAW_MIN:
+      case ODC_OP_SD_MIN: {
+        double b = st[--sp], a = st[sp - 1];
+        st[sp - 1] = (a <= b) ? a : b;
+        break;
+      }
+      case ODC_OP_RAW_DIFF: {  // min(a, 1 - b), fields.py:197
+        double b = __dsub_rn(1.0, st[--sp]), a = st[sp - 1];
+        st[sp - 1] = (a <= b) ? a : b;
+        break;
+      }
+      case ODC_OP_RAW_COMPL: st[sp - 1] = __dsub_rn(1.0, st[sp - 1]); break;
+      case ODC_OP_SD_DIFF: {  // max(a, -b), fields.py:216
+        double b = -st[--sp], a = st[sp - 1];
+        st[sp - 1] = (a >= b) ? a : b;
+        break;
+      }
+      case ODC_OP_SD_NEG: st[sp - 1] = -st[sp - 1]; break;
+      case ODC_OP_XFORM_BEGIN: {  // (p - t) @ R, fields.py:176-180
+        pst[pp][0] = p[0]; pst[pp][1] = p[1]; pst[pp][2] = p[2];
+        pp++;
+        double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+        if (__ldg(q + 6) != 0.0) {
+          double R[9], o[3];
+          for (int j = 0; j < 9; j++) R[j] = __ldg(q + 7 + j);
+          rot_rows(l, R, o);
+          l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
+        }
+        p[0] = l[0]; p[1] = l[1]; p[2] = l[2];
+        break;
+      }
+      case ODC_OP_XFORM_END:
+        pp--;
+        p[0] = pst[pp][0]; p[1] = pst[pp][1]; p[2] = pst[pp][2];
+        break;
+      case ODC_OP_SMOOTH: {  // fields.py:239-242
+        double kd = __dmul_rn(__ldg(q), st[sp - 1]);
+        kd = kd < -500.0 ? -500.0 : kd;
+        kd = kd > 500.0 ? 500.0 : kd;
+        st[sp - 1] = __ddiv_rn(1.0, __dadd_rn(1.0, exp(kd)));
+        break;
+      }
+      default: break;
+    }
+  }
+  return sp > 0 ? st[sp - 1] : 0.0;
+}
+
+// Fast paths for the common one-primitive programs (sphere / torus / box);
+// identical arithmetic to the interpreter.
+__device__ __forceinline__ double field_raw(const FieldP& f, const double p[3]) {
+  return field_raw_prog(f.nodes, f.n_nodes, p);
+}
+__device__ __forceinline__ uint32_t field_label(const FieldP& f, const double p[3]) {
+  return field_raw(f, p) > f.iso ? 1u : 0u;
+}
+
+// device-side status word (errors raised inside kernels)
+struct DevStatus {
+  int32_t code;     // ODC_E_*
+  int32_t pad;
+  int64_t detail;   // offending element
+};
+__device__ __forceinline__ void raise_status(DevStatus* st, int code, int64_t detail) {
+  if (atomicCAS(&st->code, 0, code) == 0) st->detail = detail;
+}
+
+}  // namespace odc

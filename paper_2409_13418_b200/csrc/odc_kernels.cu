@@ -1,0 +1,1798 @@
+// odc_kernels.cu -- sm_100a kernels of the ODC extraction path (fp64 part).
+//
+// Compiled with --fmad=false: every fp64 expression keeps numpy's rounding
+// (one rounding per ufunc); see odc_device.cuh.
+//
+// Data layout in HBM (per extraction):
+//   L       bit-packed vertex labels, rows (y,z) of W words         S^2 W x 4 B
+//   rec     WordRec per word: edge/face/4-face/centre/cell bitmaps
+//           + exclusive ranks (edges, instances, cells)             S^2 W x 64 B
+//   lists   edge keys (K), instance keys (Q), cell ids (C) as int64, in
+//           the reference's ascending key order
+//   stage   t/pos1d (K), pos2/pos3/status (Q), vertices (P + fans), ...
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "odc_kernels.h"
+#include "odc_scan.cuh"
+
+namespace odc {
+
+namespace {
+inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+__device__ __forceinline__ void atomic_max_nonneg_double(unsigned long long* a, double v) {
+  atomicMax(a, (unsigned long long)__double_as_longlong(v));
+}
+}  // namespace
+
+// ===========================================================================
+// K1: grid labels (grid.py:109-126).  One thread per (row, x) bit, ballot
+// packs 32 consecutive x into one word.  label = raw > iso (fields.py:47).
+// ===========================================================================
+__global__ void __launch_bounds__(256) k_labels_analytic(GridP g, FieldP f, uint32_t* __restrict__ L) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t rowbits = g.W * 32;
+  const int64_t row = gid / rowbits;
+  if (row >= g.S * g.S) return;  // whole warps (rowbits is a multiple of 32)
+  const int64_t x = gid - row * rowbits;
+  const int64_t y = row % g.S, z = row / g.S;
+  uint32_t lab = 0;
+  if (x < g.S) {
+    double p[3] = {gpos(g, 0, x), gpos(g, 1, y), gpos(g, 2, z)};
+    lab = field_label(f, p);
+  }
+  const uint32_t w = __ballot_sync(0xffffffffu, lab);
+  if ((threadIdx.x & 31) == 0) L[row * g.W + (x >> 5)] = w;
+}
+
+void launch_labels_analytic(const GridP& g, const FieldP& f, uint32_t* L, cudaStream_t s) {
+  int64_t n = g.S * g.S * g.W * 32;
+  k_labels_analytic<<<grid_for(n, 256), 256, 0, s>>>(g, f, L);
+}
+
+__global__ void k_pack_labels(GridP g, const uint8_t* __restrict__ bytes, uint32_t* __restrict__ L) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t rowbits = g.W * 32;
+  const int64_t row = gid / rowbits;
+  if (row >= g.S * g.S) return;
+  const int64_t x = gid - row * rowbits;
+  uint32_t lab = x < g.S ? (uint32_t)(bytes[row * g.S + x] != 0) : 0u;
+  const uint32_t w = __ballot_sync(0xffffffffu, lab);
+  if ((threadIdx.x & 31) == 0) L[row * g.W + (x >> 5)] = w;
+}
+void launch_pack_labels(const GridP& g, const uint8_t* bytes, uint32_t* L, cudaStream_t s) {
+  int64_t n = g.S * g.S * g.W * 32;
+  k_pack_labels<<<grid_for(n, 256), 256, 0, s>>>(g, bytes, L);
+}
+
+__global__ void k_unpack_labels(GridP g, const uint32_t* __restrict__ L, uint8_t* __restrict__ bytes) {
+  const int64_t vid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vid >= g.S3) return;
+  bytes[vid] = (uint8_t)label_at(L, g, vid);
+}
+void launch_unpack_labels(const GridP& g, const uint32_t* L, uint8_t* bytes, cudaStream_t s) {
+  k_unpack_labels<<<grid_for(g.S3, 256), 256, 0, s>>>(g, L, bytes);
+}
+
+__global__ void k_grid_points(GridP g, int64_t begin, int64_t n, double* __restrict__ pts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double p[3];
+  vposition(g, begin + i, p);
+  pts[3 * i] = p[0];
+  pts[3 * i + 1] = p[1];
+  pts[3 * i + 2] = p[2];
+}
+void launch_grid_points(const GridP& g, int64_t begin, int64_t n, double* pts, cudaStream_t s) {
+  k_grid_points<<<grid_for(n, 256), 256, 0, s>>>(g, begin, n, pts);
+}
+
+// ===========================================================================
+// K2: active sets (grid.py:171-296) from four neighbouring label rows.
+//   edge (v,a) crosses  <=> L(v) != L(v + step_a)          (grid.py:185-195)
+//   face (v,n) crosses  <=> >= 2 of its 4 cyclic edges cross (grid.py:212-260)
+//   cell crosses        <=> its corner labels are not all equal (grid.py:263-278)
+// Channels of the rank scan: 0 edges, 1 instances (faces + 4-faces),
+// 2 cells, 3 faces, 4 4-crossing faces.
+// ===========================================================================
+constexpr int kActiveBlock = kScanBlock;
+
+__device__ __forceinline__ uint32_t bits_below(int64_t limit, int64_t wx) {
+  int64_t n = limit - wx * 32;
+  if (n <= 0) return 0u;
+  if (n >= 32) return 0xffffffffu;
+  return 0xffffffffu >> (32 - n);
+}
+
+struct ActiveBits {
+  uint32_t e[3], f[3], f4[3], cell;
+};
+
+__device__ __forceinline__ ActiveBits compute_active(const GridP& g, const uint32_t* __restrict__ L, int64_t y,
+                                                     int64_t z, int64_t wx) {
+  const int64_t W = g.W, S = g.S, R = g.R;
+  const bool yin = y < R, zin = z < R;
+  auto ld = [&](int64_t yy, int64_t zz, int64_t ww) -> uint32_t {
+    if (yy > R || zz > R || ww >= W) return 0u;
+    return L[(zz * S + yy) * W + ww];
+  };
+  const uint32_t a00 = ld(y, z, wx), a10 = ld(y + 1, z, wx), a01 = ld(y, z + 1, wx), a11 = ld(y + 1, z + 1, wx);
+  const uint32_t n00 = ld(y, z, wx + 1), n10 = ld(y + 1, z, wx + 1), n01 = ld(y, z + 1, wx + 1),
+                 n11 = ld(y + 1, z + 1, wx + 1);
+  // label at x+1
+  const uint32_t s00 = (a00 >> 1) | (n00 << 31), s10 = (a10 >> 1) | (n10 << 31);
+  const uint32_t s01 = (a01 >> 1) | (n01 << 31), s11 = (a11 >> 1) | (n11 << 31);
+  const uint32_t mS = bits_below(S, wx), mR = bits_below(R, wx);
+  ActiveBits b;
+  b.e[0] = (a00 ^ s00) & mR;
+  b.e[1] = yin ? ((a00 ^ a10) & mS) : 0u;
+  b.e[2] = zin ? ((a00 ^ a01) & mS) : 0u;
+  // x-normal face at v: edges EY(v), EZ(v+Sy), EY(v+Sz), EZ(v)
+  {
+    uint32_t e01 = a00 ^ a10, e12 = a10 ^ a11, e23 = a01 ^ a11, e30 = a00 ^ a01;
+    uint32_t m = (yin && zin) ? mS : 0u;
+    b.f[0] = (e01 | e12 | e23 | e30) & m;
+    b.f4[0] = (e01 & e12 & e23 & e30) & m;
+  }
+  // y-normal face (b=z, c=x): EZ(v), EX(v+Sz), EZ(v+1), EX(v)
+  {
+    uint32_t e01 = a00 ^ a01, e12 = a01 ^ s01, e23 = s00 ^ s01, e30 = a00 ^ s00;
+    uint32_t m = zin ? mR : 0u;
+    b.f[1] = (e01 | e12 | e23 | e30) & m;
+    b.f4[1] = (e01 & e12 & e23 & e30) & m;
+  }
+  // z-normal face (b=x, c=y): EX(v), EY(v+1), EX(v+Sy), EY(v)
+  {
+    uint32_t e01 = a00 ^ s00, e12 = s00 ^ s10, e23 = a10 ^ s10, e30 = a00 ^ a10;
+    uint32_t m = yin ? mR : 0u;
+    b.f[2] = (e01 | e12 | e23 | e30) & m;
+    b.f4[2] = (e01 & e12 & e23 & e30) & m;
+  }
+  {
+    uint32_t d = (a00 ^ s00) | (a00 ^ a10) | (a00 ^ s10) | (a00 ^ a01) | (a00 ^ s01) | (a00 ^ a11) | (a00 ^ s11);
+    b.cell = (yin && zin) ? (d & mR) : 0u;
+  }
+  return b;
+}
+
+__device__ __forceinline__ void active_counts(const ActiveBits& b, uint32_t (&c)[5]) {
+  uint32_t nf = __popc(b.f[0]) + __popc(b.f[1]) + __popc(b.f[2]);
+  uint32_t n4 = __popc(b.f4[0]) + __popc(b.f4[1]) + __popc(b.f4[2]);
+  c[0] = __popc(b.e[0]) + __popc(b.e[1]) + __popc(b.e[2]);
+  c[1] = nf + n4;
+  c[2] = __popc(b.cell);
+  c[3] = nf;
+  c[4] = n4;
+}
+
+__global__ void __launch_bounds__(kActiveBlock) k_active_bits(GridP g, const uint32_t* __restrict__ L,
+                                                              WordRec* __restrict__ rec, uint32_t* __restrict__ sums,
+                                                              int64_t ntiles, DevStats* st) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t c[5] = {0, 0, 0, 0, 0};
+  uint32_t shell = 0;
+  if (idx < g.NW) {
+    const int64_t row = idx / g.W, wx = idx - row * g.W;
+    const int64_t y = row % g.S, z = row / g.S;
+    ActiveBits b = compute_active(g, L, y, z, wx);
+    WordRec r;
+    for (int a = 0; a < 3; a++) {
+      r.e[a] = b.e[a];
+      r.f[a] = b.f[a];
+      r.f4[a] = b.f4[a];
+      r.cf[a] = 0u;
+    }
+    r.cell = b.cell;
+    r.pe = r.pq = r.pc = 0u;
+    rec[idx] = r;
+    active_counts(b, c);
+    // boundary_inside_count (grid.py:102-106)
+    const uint32_t lab = L[idx] & bits_below(g.S, wx);
+    if (y == 0 || y == g.R || z == 0 || z == g.R) {
+      shell = __popc(lab);
+    } else {
+      uint32_t m = 0u;
+      if (wx == 0) m |= 1u;
+      if ((g.R >> 5) == wx) m |= 1u << (g.R & 31);
+      shell = __popc(lab & m);
+    }
+  }
+  uint32_t ex[5], tot[5];
+  block_exscan<5>(c, ex, tot);
+  if (threadIdx.x == 0)
+    for (int ch = 0; ch < 5; ch++) sums[ch * ntiles + blockIdx.x] = tot[ch];
+  // reduce shell count
+  for (int o = 16; o > 0; o >>= 1) shell += __shfl_xor_sync(0xffffffffu, shell, o);
+  if ((threadIdx.x & 31) == 0 && shell) atomicAdd(&st->boundary_inside, (unsigned long long)shell);
+}
+
+int64_t active_tiles(const GridP& g) { return (g.NW + kActiveBlock - 1) / kActiveBlock; }
+
+void launch_active_bits(const GridP& g, const uint32_t* L, WordRec* rec, uint32_t* tile_sums, DevStats* st,
+                        cudaStream_t s) {
+  int64_t nt = active_tiles(g);
+  k_active_bits<<<(unsigned)nt, kActiveBlock, 0, s>>>(g, L, rec, tile_sums, nt, st);
+}
+
+void launch_scan_tiles(uint32_t* sums, int64_t ntiles, int nch, unsigned long long* totals, cudaStream_t s) {
+  switch (nch) {
+    case 1: k_scan_tiles<1><<<1, 1024, 0, s>>>(sums, ntiles, totals); break;
+    case 2: k_scan_tiles<2><<<1, 1024, 0, s>>>(sums, ntiles, totals); break;
+    default: k_scan_tiles<5><<<1, 1024, 0, s>>>(sums, ntiles, totals); break;
+  }
+}
+
+__global__ void __launch_bounds__(kActiveBlock) k_active_compact(GridP g, WordRec* __restrict__ rec,
+                                                                 const uint32_t* __restrict__ sums, int64_t ntiles,
+                                                                 int64_t* __restrict__ edge_key,
+                                                                 int64_t* __restrict__ inst_key,
+                                                                 int64_t* __restrict__ cell_id,
+                                                                 int64_t* __restrict__ f4_key,
+                                                                 int64_t* __restrict__ face_key,
+                                                                 int64_t* __restrict__ face_nc) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  WordRec r;
+  uint32_t c[5] = {0, 0, 0, 0, 0};
+  if (idx < g.NW) {
+    r = rec[idx];
+    ActiveBits b;
+    for (int a = 0; a < 3; a++) {
+      b.e[a] = r.e[a];
+      b.f[a] = r.f[a];
+      b.f4[a] = r.f4[a];
+    }
+    b.cell = r.cell;
+    active_counts(b, c);
+  }
+  uint32_t ex[5], tot[5];
+  block_exscan<5>(c, ex, tot);
+  if (idx >= g.NW) return;
+  uint32_t pos[5];
+  for (int ch = 0; ch < 5; ch++) pos[ch] = sums[ch * ntiles + blockIdx.x] + ex[ch];
+  rec[idx].pe = pos[0];
+  rec[idx].pq = pos[1];
+  rec[idx].pc = pos[2];
+  const int64_t row = idx / g.W, wx = idx - row * g.W;
+  const int64_t y = row % g.S, z = row / g.S;
+  const int64_t vbase = row * g.S + wx * 32;  // vertex id of bit 0 (x = 32 wx)
+  // edges: ascending vertex, then axis (edge key = vid*3 + axis)
+  uint32_t any = r.e[0] | r.e[1] | r.e[2];
+  uint32_t pe = pos[0];
+  while (any) {
+    int bit = __ffs(any) - 1;
+    any &= any - 1;
+    int64_t vid = vbase + bit;
+    for (int a = 0; a < 3; a++)
+      if ((r.e[a] >> bit) & 1u) edge_key[pe++] = vid * 3 + a;
+  }
+  uint32_t anyf = r.f[0] | r.f[1] | r.f[2];
+  uint32_t pq = pos[1], pf = pos[3], p4 = pos[4];
+  while (anyf) {
+    int bit = __ffs(anyf) - 1;
+    anyf &= anyf - 1;
+    int64_t vid = vbase + bit;
+    for (int n = 0; n < 3; n++) {
+      if (!((r.f[n] >> bit) & 1u)) continue;
+      const int64_t fk = vid * 3 + n;
+      const bool four = (r.f4[n] >> bit) & 1u;
+      inst_key[pq++] = fk * 2;
+      if (four) {
+        inst_key[pq++] = fk * 2 + 1;
+        f4_key[p4++] = fk;
+      }
+      if (face_key) {
+        face_key[pf] = fk;
+        face_nc[pf] = four ? 4 : 2;
+      }
+      pf++;
+    }
+  }
+  uint32_t cl = r.cell;
+  uint32_t pc = pos[2];
+  while (cl) {
+    int bit = __ffs(cl) - 1;
+    cl &= cl - 1;
+    int64_t x = wx * 32 + bit;
+    cell_id[pc++] = x + y * g.R + z * g.R * g.R;
+  }
+}
+
+void launch_active_compact(const GridP& g, WordRec* rec, const uint32_t* tile_sums, int64_t* edge_key,
+                           int64_t* inst_key, int64_t* cell_id, int64_t* f4_key, int64_t* face_key,
+                           int64_t* face_nc, cudaStream_t s) {
+  int64_t nt = active_tiles(g);
+  k_active_compact<<<(unsigned)nt, kActiveBlock, 0, s>>>(g, rec, tile_sums, nt, edge_key, inst_key, cell_id, f4_key,
+                                                          face_key, face_nc);
+}
+
+// ===========================================================================
+// face-centre probes (dualize.py:59-70): corner + 0.5 h along both in-plane axes
+// ===========================================================================
+__device__ __forceinline__ void face_center(const GridP& g, int64_t fk, double p[3]) {
+  int64_t vid = fk / 3;
+  int n = (int)(fk % 3), b = (n + 1) % 3, c = (n + 2) % 3;
+  vposition(g, vid, p);
+  p[b] = p[b] + 0.5 * g.h[b];
+  p[c] = p[c] + 0.5 * g.h[c];
+}
+__device__ __forceinline__ void set_center_bit(const GridP& g, WordRec* rec, int64_t fk) {
+  int64_t vid = fk / 3;
+  int n = (int)(fk % 3);
+  int64_t c[3];
+  vid_coords(g, vid, c);
+  atomicOr(&rec[word_of(g, c[0], c[1], c[2])].cf[n], 1u << (c[0] & 31));
+}
+
+__global__ void k_face_center_points(GridP g, const int64_t* __restrict__ f4, int64_t n, double* __restrict__ pts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double p[3];
+  face_center(g, f4[i], p);
+  pts[3 * i] = p[0];
+  pts[3 * i + 1] = p[1];
+  pts[3 * i + 2] = p[2];
+}
+void launch_face_center_points(const GridP& g, const int64_t* f4_key, int64_t n, double* pts, cudaStream_t s) {
+  if (n) k_face_center_points<<<grid_for(n, 128), 128, 0, s>>>(g, f4_key, n, pts);
+}
+
+__global__ void k_face_center_analytic(GridP g, FieldP f, const int64_t* __restrict__ f4, int64_t n,
+                                       WordRec* __restrict__ rec) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double p[3];
+  face_center(g, f4[i], p);
+  if (field_label(f, p)) set_center_bit(g, rec, f4[i]);
+}
+void launch_face_center_analytic(const GridP& g, const FieldP& f, const int64_t* f4_key, int64_t n, WordRec* rec,
+                                 cudaStream_t s) {
+  if (n) k_face_center_analytic<<<grid_for(n, 128), 128, 0, s>>>(g, f, f4_key, n, rec);
+}
+
+__global__ void k_face_center_scatter(GridP g, const int64_t* __restrict__ f4, const uint8_t* __restrict__ lab,
+                                      int64_t n, WordRec* __restrict__ rec) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (lab[i]) set_center_bit(g, rec, f4[i]);
+}
+void launch_face_center_scatter(const GridP& g, const int64_t* f4_key, const uint8_t* labels, int64_t n,
+                                WordRec* rec, cudaStream_t s) {
+  if (n) k_face_center_scatter<<<grid_for(n, 128), 128, 0, s>>>(g, f4_key, labels, n, rec);
+}
+
+// ===========================================================================
+// K3: 1D points (search.py:71-94, pipeline.py:94-123)
+// ===========================================================================
+struct EdgeGeom {
+  int64_t vin, vout;
+  double pin[3], span[3];
+};
+__device__ __forceinline__ EdgeGeom edge_geom(const GridP& g, const uint32_t* L, int64_t key) {
+  EdgeGeom e;
+  int64_t vid = key / 3;
+  int a = (int)(key % 3);
+  int64_t other = vid + vstep(g, a);
+  bool base_in = label_at(L, g, vid) == 1u;
+  e.vin = base_in ? vid : other;
+  e.vout = base_in ? other : vid;
+  double po[3];
+  vposition(g, e.vin, e.pin);
+  vposition(g, e.vout, po);
+  for (int j = 0; j < 3; j++) e.span[j] = po[j] - e.pin[j];
+  return e;
+}
+
+__device__ __forceinline__ double clip_t(double t, int iters) {
+  double eps = ldexp(1.0, -iters);
+  double upper = 1.0 - eps;
+  t = t < eps ? eps : t;
+  t = t > upper ? upper : t;
+  return t;
+}
+
+__device__ __forceinline__ double linear_t(double ri, double ro, double iso) {
+  double pi = ri - iso, po = ro - iso;
+  double den = pi - po;
+  double t = fabs(den) < 1e-300 ? 0.5 : pi / (den == 0.0 ? 1.0 : den);
+  t = t < 0.0 ? 0.0 : t;
+  return t > 1.0 ? 1.0 : t;
+}
+
+__global__ void __launch_bounds__(128) k_search1d_analytic(GridP g, FieldP f, OptP o, const uint32_t* __restrict__ L,
+                                                           const int64_t* __restrict__ edge_key, int64_t K,
+                                                           double* __restrict__ tout, double* __restrict__ pos,
+                                                           int64_t* __restrict__ vin_out) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  EdgeGeom e = edge_geom(g, L, edge_key[k]);
+  double t;
+  if (o.one_d == ODC_ONE_D_BINARY) {
+    double lo = 0.0, hi = 1.0;
+    for (int it = 0; it < o.iters_1d; it++) {
+      double tm = 0.5 * (lo + hi);
+      double q[3];
+      for (int j = 0; j < 3; j++) q[j] = e.pin[j] + tm * e.span[j];
+      if (field_label(f, q)) lo = tm; else hi = tm;  // bracket: label(lo)=1, label(hi)=0
+    }
+    t = clip_t(0.5 * (lo + hi), o.iters_1d);
+  } else if (o.one_d == ODC_ONE_D_MIDPOINT) {
+    t = 0.5;
+  } else {
+    double ri, ro;
+    if (o.continuous) {
+      double po[3];
+      vposition(g, e.vout, po);
+      ri = field_raw(f, e.pin);
+      ro = field_raw(f, po);
+    } else {
+      ri = 1.0;
+      ro = 0.0;
+    }
+    t = linear_t(ri, ro, f.iso);
+  }
+  tout[k] = t;
+  for (int j = 0; j < 3; j++) pos[3 * k + j] = e.pin[j] + t * e.span[j];
+  if (vin_out) vin_out[k] = e.vin;
+}
+
+void launch_search1d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
+                              const int64_t* edge_key, int64_t K, double* t, double* pos, int64_t* v_in,
+                              cudaStream_t s) {
+  if (K) k_search1d_analytic<<<grid_for(K, 128), 128, 0, s>>>(g, f, o, L, edge_key, K, t, pos, v_in);
+}
+
+// lock-step form (batched fields): lo/hi state, points, update, finish
+__global__ void k_search1d_init(int64_t K, double* lo, double* hi) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  lo[k] = 0.0;
+  hi[k] = 1.0;
+}
+void launch_search1d_init(const GridP&, const uint32_t*, const int64_t*, int64_t K, double* lo, double* hi,
+                          cudaStream_t s) {
+  if (K) k_search1d_init<<<grid_for(K, 256), 256, 0, s>>>(K, lo, hi);
+}
+__global__ void k_search1d_points(GridP g, const uint32_t* __restrict__ L, const int64_t* __restrict__ edge_key,
+                                  int64_t K, const double* __restrict__ lo, const double* __restrict__ hi,
+                                  double* __restrict__ pts) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  EdgeGeom e = edge_geom(g, L, edge_key[k]);
+  double tm = 0.5 * (lo[k] + hi[k]);
+  for (int j = 0; j < 3; j++) pts[3 * k + j] = e.pin[j] + tm * e.span[j];
+}
+void launch_search1d_points(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K, const double* lo,
+                            const double* hi, double* pts, cudaStream_t s) {
+  if (K) k_search1d_points<<<grid_for(K, 256), 256, 0, s>>>(g, L, edge_key, K, lo, hi, pts);
+}
+__global__ void k_search1d_update(int64_t K, const uint8_t* __restrict__ lab, double* lo, double* hi) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double tm = 0.5 * (lo[k] + hi[k]);
+  if (lab[k] == 1) lo[k] = tm; else hi[k] = tm;
+}
+void launch_search1d_update(int64_t K, const uint8_t* lab, double* lo, double* hi, cudaStream_t s) {
+  if (K) k_search1d_update<<<grid_for(K, 256), 256, 0, s>>>(K, lab, lo, hi);
+}
+__global__ void k_search1d_finish(GridP g, OptP o, double iso, const uint32_t* __restrict__ L,
+                                  const int64_t* __restrict__ edge_key, int64_t K, const double* __restrict__ lo,
+                                  const double* __restrict__ hi, const double* __restrict__ raw_in,
+                                  const double* __restrict__ raw_out, double* __restrict__ tout,
+                                  double* __restrict__ pos, int64_t* __restrict__ vin_out) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  EdgeGeom e = edge_geom(g, L, edge_key[k]);
+  double t;
+  if (o.one_d == ODC_ONE_D_BINARY) t = clip_t(0.5 * (lo[k] + hi[k]), o.iters_1d);
+  else if (o.one_d == ODC_ONE_D_MIDPOINT) t = 0.5;
+  else t = raw_in ? linear_t(raw_in[k], raw_out[k], iso) : linear_t(1.0, 0.0, iso);
+  tout[k] = t;
+  for (int j = 0; j < 3; j++) pos[3 * k + j] = e.pin[j] + t * e.span[j];
+  if (vin_out) vin_out[k] = e.vin;
+}
+void launch_search1d_finish(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* edge_key, int64_t K,
+                            const double* lo, const double* hi, const double* raw_in, const double* raw_out,
+                            double* t, double* pos, int64_t* v_in, cudaStream_t s) {
+  if (K)
+    k_search1d_finish<<<grid_for(K, 256), 256, 0, s>>>(g, o, 0.5, L, edge_key, K, lo, hi, raw_in, raw_out, t, pos,
+                                                       v_in);
+}
+
+__global__ void k_edge_endpoints(GridP g, const uint32_t* __restrict__ L, const int64_t* __restrict__ edge_key,
+                                 int64_t K, int which, double* __restrict__ pts) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  EdgeGeom e = edge_geom(g, L, edge_key[k]);
+  vposition(g, which ? e.vout : e.vin, pts + 3 * k);
+}
+void launch_edge_endpoints(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K, int which,
+                           double* pts, cudaStream_t s) {
+  if (K) k_edge_endpoints<<<grid_for(K, 256), 256, 0, s>>>(g, L, edge_key, K, which, pts);
+}
+
+// ===========================================================================
+// K5: 2D points -- build_face_batch (dualize.py:97-129) + find_2d_points
+// (search.py:194-322) + line_binary_search_batch (search.py:97-133).
+// One instance = (face, edge pair).  In-plane axes u = (n+1)%3, v = (n+2)%3;
+// lift(u,v) = origin with origin[u] += u, origin[v] += v (search.py:172-177).
+// ===========================================================================
+struct Inst2D {
+  double org[3];
+  int bu, bv;
+  double hu, hv, hmin;
+  double p1[2], p2[2];
+  uint32_t cl[4];  // corner labels w0..w3
+};
+
+// Decode an instance key (face_key*2 + slot): corner labels, the slot's edge
+// pair (dualize.py:37-48, :72-88) and the two 1D points in face coordinates.
+__device__ __forceinline__ bool decode_instance(const GridP& g, const uint32_t* L, const WordRec* rec,
+                                                int64_t ikey, const double* pos1d, Inst2D& I, int64_t pair[2]) {
+  const int64_t fk = ikey >> 1;
+  const int slot = (int)(ikey & 1);
+  const int64_t vid = fk / 3;
+  const int n = (int)(fk % 3), b = (n + 1) % 3, c = (n + 2) % 3;
+  const int64_t w0 = vid, w1 = vid + vstep(g, b), w3 = vid + vstep(g, c), w2 = w1 + vstep(g, c);
+  I.cl[0] = label_at(L, g, w0);
+  I.cl[1] = label_at(L, g, w1);
+  I.cl[2] = label_at(L, g, w2);
+  I.cl[3] = label_at(L, g, w3);
+  const int64_t ek[4] = {w0 * 3 + b, w1 * 3 + c, w3 * 3 + b, w0 * 3 + c};
+  const bool cr[4] = {I.cl[0] != I.cl[1], I.cl[1] != I.cl[2], I.cl[3] != I.cl[2], I.cl[0] != I.cl[3]};
+  const int ncross = (int)cr[0] + (int)cr[1] + (int)cr[2] + (int)cr[3];
+  int64_t a0, a1;
+  if (ncross == 2) {
+    int64_t sel[2];
+    int ns = 0;
+    for (int j = 0; j < 4; j++)
+      if (cr[j]) sel[ns++] = ek[j];
+    a0 = sel[0];
+    a1 = sel[1];
+  } else {
+    int64_t cc[3];
+    vid_coords(g, vid, cc);
+    const uint32_t centre = (rec[word_of(g, cc[0], cc[1], cc[2])].cf[n] >> (cc[0] & 31)) & 1u;
+    if (centre == I.cl[0]) {
+      a0 = slot ? ek[2] : ek[0];
+      a1 = slot ? ek[3] : ek[1];
+    } else {
+      a0 = slot ? ek[1] : ek[3];
+      a1 = slot ? ek[2] : ek[0];
+    }
+  }
+  if (a1 < a0) { int64_t t = a0; a0 = a1; a1 = t; }
+  pair[0] = a0;
+  pair[1] = a1;
+  vposition(g, vid, I.org);
+  I.bu = b;
+  I.bv = c;
+  I.hu = g.h[b];
+  I.hv = g.h[c];
+  I.hmin = I.hu < I.hv ? I.hu : I.hv;
+  const int64_t r0 = edge_rank(rec, g, a0 / 3, (int)(a0 % 3));
+  const int64_t r1 = edge_rank(rec, g, a1 / 3, (int)(a1 % 3));
+  I.p1[0] = pos1d[3 * r0 + b] - I.org[b];
+  I.p1[1] = pos1d[3 * r0 + c] - I.org[c];
+  I.p2[0] = pos1d[3 * r1 + b] - I.org[b];
+  I.p2[1] = pos1d[3 * r1 + c] - I.org[c];
+  return true;
+}
+
+__device__ __forceinline__ void lift(const Inst2D& I, double u, double v, double p[3]) {
+  p[0] = I.org[0];
+  p[1] = I.org[1];
+  p[2] = I.org[2];
+  p[I.bu] = I.org[I.bu] + u;
+  p[I.bv] = I.org[I.bv] + v;
+}
+
+// Geometry derived from the chord, before any evaluation (search.py:213-219)
+struct Chord {
+  double mid[2], dl[2];
+  bool degen;
+};
+__device__ __forceinline__ Chord make_chord(const Inst2D& I) {
+  Chord ch;
+  ch.mid[0] = 0.5 * (I.p1[0] + I.p2[0]);
+  ch.mid[1] = 0.5 * (I.p1[1] + I.p2[1]);
+  const double c0 = I.p2[0] - I.p1[0], c1 = I.p2[1] - I.p1[1];
+  const double clen = sqrt(c0 * c0 + c1 * c1);
+  ch.degen = clen < 1e-12 * I.hmin;
+  const double safe = ch.degen ? 1.0 : clen;
+  ch.dl[0] = c0 / safe;
+  ch.dl[1] = c1 / safe;
+  return ch;
+}
+
+// Ray side toward the nearest corner whose label differs from the midpoint
+// label (search.py:222-239).  Returns false when no corner differs.
+__device__ __forceinline__ bool ray_direction(const Inst2D& I, const Chord& ch, uint32_t mid_label, double ray[2]) {
+  const double perp0 = -ch.dl[1], perp1 = ch.dl[0];
+  const double cu[4] = {0.0, I.hu, I.hu, 0.0}, cv[4] = {0.0, 0.0, I.hv, I.hv};
+  double plus_d = INFINITY, minus_d = INFINITY;
+  for (int c = 0; c < 4; c++) {
+    const double r0 = cu[c] - ch.mid[0], r1 = cv[c] - ch.mid[1];
+    const double side = r0 * perp0 + r1 * perp1;
+    const double dist = sqrt(r0 * r0 + r1 * r1);
+    if (I.cl[c] == mid_label) continue;
+    if (side > 0 && dist < plus_d) plus_d = dist;
+    if (side < 0 && dist < minus_d) minus_d = dist;
+  }
+  if (isinf(plus_d) && isinf(minus_d)) return false;
+  if (plus_d <= minus_d) {
+    ray[0] = perp0;
+    ray[1] = perp1;
+  } else {
+    ray[0] = -perp0;
+    ray[1] = -perp1;
+  }
+  return true;
+}
+
+// Final step: line intersection, clamp, status (search.py:278-322)
+__device__ __forceinline__ void finish2d(const Inst2D& I, const Chord& ch, double dist_r, bool found_r,
+                                         const double qa[2], bool found_a, const double qb[2], bool found_b,
+                                         double out2[2], uint8_t& status) {
+  const double a1[2] = {qa[0] - I.p1[0], qa[1] - I.p1[1]};
+  const double a2[2] = {qb[0] - I.p2[0], qb[1] - I.p2[1]};
+  const double l1 = sqrt(a1[0] * a1[0] + a1[1] * a1[1]);
+  const double l2 = sqrt(a2[0] * a2[0] + a2[1] * a2[1]);
+  const double cr = a1[0] * a2[1] - a1[1] * a2[0];
+  const bool exact = dist_r <= 1e-4 * I.hmin;
+  const bool parallel = (fabs(cr) <= 1e-6 * l1 * l2) || (l1 < 1e-12 * I.hmin) || (l2 < 1e-12 * I.hmin) || ch.degen;
+  const double sc = parallel ? 1.0 : cr;
+  const double d21[2] = {I.p2[0] - I.p1[0], I.p2[1] - I.p1[1]};
+  const double tpar = (d21[0] * a2[1] - d21[1] * a2[0]) / sc;
+  double pos[2];
+  if (exact || parallel) {
+    pos[0] = ch.mid[0];
+    pos[1] = ch.mid[1];
+  } else {
+    pos[0] = I.p1[0] + tpar * a1[0];
+    pos[1] = I.p1[1] + tpar * a1[1];
+  }
+  const double lov[2] = {-0.5 * I.hu, -0.5 * I.hv}, hiv[2] = {1.5 * I.hu, 1.5 * I.hv};
+  const double delta[2] = {pos[0] - ch.mid[0], pos[1] - ch.mid[1]};
+  double smin = INFINITY;
+  for (int i = 0; i < 2; i++) {
+    const double shi = delta[i] > 0 ? (hiv[i] - ch.mid[i]) / delta[i] : INFINITY;
+    const double slo = delta[i] < 0 ? (lov[i] - ch.mid[i]) / delta[i] : INFINITY;
+    const double m2 = shi < slo ? shi : slo;
+    if (m2 < smin) smin = m2;
+  }
+  const double s = smin < 1.0 ? smin : 1.0;
+  const bool clamped = s < 1.0;
+  out2[0] = ch.mid[0] + s * delta[0];
+  out2[1] = ch.mid[1] + s * delta[1];
+  uint8_t st = 0;
+  if (!(found_r && found_a && found_b)) st = 3;
+  if (clamped) st = 2;
+  if (parallel && !exact) st = 1;
+  if (exact) st = 0;
+  status = st;
+}
+
+// Fused per-instance search for analytic fields.  Evaluations happen in the
+// same per-element order as the lock-step batches; skipping the samples
+// after the first flip of a linear scan does not change any result, and the
+// eval accounting reports the reference's logical counts.
+__device__ __forceinline__ void line_binary(const FieldP& f, const Inst2D& I, const double o2[2], const double d2[2],
+                                            uint32_t ref, double max_range, int nlin, int nbin, double& a_out,
+                                            bool& found) {
+  int first = nlin;
+  found = false;
+  for (int i = 1; i <= nlin; i++) {
+    const double s = max_range * ((double)i / (double)nlin);
+    double p[3];
+    lift(I, o2[0] + s * d2[0], o2[1] + s * d2[1], p);
+    if (field_label(f, p) != ref) {
+      first = i;
+      found = true;
+      break;
+    }
+  }
+  double a = max_range * ((double)(first - 1) / (double)nlin);
+  double b = max_range * ((double)first / (double)nlin);
+  for (int it = 0; it < nbin; it++) {
+    const double m = 0.5 * (a + b);
+    double p[3];
+    lift(I, o2[0] + m * d2[0], o2[1] + m * d2[1], p);
+    if (field_label(f, p) == ref) a = m; else b = m;
+  }
+  a_out = a;
+}
+
+__global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, OptP o, const uint32_t* __restrict__ L,
+                                                           const WordRec* __restrict__ rec,
+                                                           const int64_t* __restrict__ inst_key, int64_t Q,
+                                                           const double* __restrict__ pos1d, Stage2D out,
+                                                           int64_t* __restrict__ inst_edges, DevStats* st,
+                                                           DevStatus* dst) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  Inst2D I;
+  int64_t pair[2];
+  decode_instance(g, L, rec, inst_key[q], pos1d, I, pair);
+  if (inst_edges) {
+    inst_edges[2 * q] = pair[0];
+    inst_edges[2 * q + 1] = pair[1];
+  }
+  const Chord ch = make_chord(I);
+  double pm[3];
+  lift(I, ch.mid[0], ch.mid[1], pm);
+  const uint32_t mid_label = field_label(f, pm);
+  double ray[2];
+  if (!ray_direction(I, ch, mid_label, ray)) {
+    raise_status(dst, ODC_E_ASSERT, q);
+    return;
+  }
+  double dist_r;
+  bool found_r;
+  line_binary(f, I, ch.mid, ray, mid_label, o.s1_range * I.hmin, o.s1_lin, o.s1_bin, dist_r, found_r);
+  const double q2[2] = {ch.mid[0] + dist_r * ray[0], ch.mid[1] + dist_r * ray[1]};
+  const double r2 = o.s2_range * I.hmin;
+  const double dneg[2] = {-ch.dl[0], -ch.dl[1]};
+  double da, db;
+  bool fa, fb;
+  line_binary(f, I, q2, dneg, mid_label, r2, o.s2_lin, o.s2_bin, da, fa);
+  line_binary(f, I, q2, ch.dl, mid_label, r2, o.s2_lin, o.s2_bin, db, fb);
+  const double qa[2] = {q2[0] + da * dneg[0], q2[1] + da * dneg[1]};
+  const double qb[2] = {q2[0] + db * ch.dl[0], q2[1] + db * ch.dl[1]};
+  double p2d[2];
+  uint8_t status;
+  finish2d(I, ch, dist_r, found_r, qa, fa, qb, fb, p2d, status);
+  double p3[3];
+  lift(I, p2d[0], p2d[1], p3);
+  out.pos3[3 * q] = p3[0];
+  out.pos3[3 * q + 1] = p3[1];
+  out.pos3[3 * q + 2] = p3[2];
+  if (out.pos2) {
+    out.pos2[2 * q] = p2d[0];
+    out.pos2[2 * q + 1] = p2d[1];
+  }
+  if (out.status) out.status[q] = status;
+  if (out.mid) out.mid[q] = (uint8_t)mid_label;
+  atomicAdd(&st->status[status], 1ull);
+}
+
+void launch_search2d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
+                              const WordRec* rec, const int64_t* inst_key, int64_t Q, const double* pos1d,
+                              Stage2D out, int64_t* inst_edges, DevStats* st, DevStatus* dst, cudaStream_t s) {
+  if (Q)
+    k_search2d_analytic<<<grid_for(Q, 128), 128, 0, s>>>(g, f, o, L, rec, inst_key, Q, pos1d, out, inst_edges, st,
+                                                         dst);
+}
+
+// ---- lock-step 2D search (batched fields) --------------------------------
+// Batch sequence per instance (search.py:220, :244-276): step 0 midpoint
+// probe (Q points), steps 1..s1_lin+s1_bin the step-1 ray (Q points), then
+// s2_lin+s2_bin steps of both step-2 rays in one batch of 2Q points.
+struct Search2DState {
+  double mid[2], dl[2], ray[2];
+  double a1, b1;          // step-1 bracket
+  double q2[2];
+  double a2[2], b2[2];    // step-2 brackets (ray -dl, ray +dl)
+  int32_t first1, first2[2];
+  uint8_t mid_label, found1, found2[2], degen, pad[3];
+};
+
+size_t search2d_state_bytes(int64_t Q) { return (size_t)Q * sizeof(Search2DState); }
+int search2d_num_steps(const OptP& o) { return 1 + o.s1_lin + o.s1_bin + o.s2_lin + o.s2_bin; }
+
+__global__ void k_s2_init(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+                          const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
+                          Search2DState* __restrict__ S, int64_t* __restrict__ inst_edges) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  Inst2D I;
+  int64_t pair[2];
+  decode_instance(g, L, rec, inst_key[q], pos1d, I, pair);
+  if (inst_edges) {
+    inst_edges[2 * q] = pair[0];
+    inst_edges[2 * q + 1] = pair[1];
+  }
+  Chord ch = make_chord(I);
+  Search2DState s = {};
+  s.mid[0] = ch.mid[0];
+  s.mid[1] = ch.mid[1];
+  s.dl[0] = ch.dl[0];
+  s.dl[1] = ch.dl[1];
+  s.degen = ch.degen;
+  S[q] = s;
+}
+
+// Per-instance geometry needed to lift points: recomputed from the key.
+__device__ __forceinline__ void inst_frame(const GridP& g, int64_t ikey, Inst2D& I) {
+  const int64_t fk = ikey >> 1;
+  const int64_t vid = fk / 3;
+  const int n = (int)(fk % 3);
+  I.bu = (n + 1) % 3;
+  I.bv = (n + 2) % 3;
+  vposition(g, vid, I.org);
+}
+
+__global__ void k_s2_points(GridP g, OptP o, const int64_t* __restrict__ inst_key, int64_t Q, int step,
+                            const Search2DState* __restrict__ S, double* __restrict__ pts) {
+  int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n1 = o.s1_lin + o.s1_bin;
+  const bool two = step > n1;
+  const int64_t M = two ? 2 * Q : Q;
+  if (m >= M) return;
+  const int64_t q = two ? (m < Q ? m : m - Q) : m;
+  Inst2D I;
+  inst_frame(g, inst_key[q], I);
+  I.hu = g.h[I.bu];
+  I.hv = g.h[I.bv];
+  I.hmin = I.hu < I.hv ? I.hu : I.hv;
+  const Search2DState& s = S[q];
+  double u, v;
+  if (step == 0) {
+    u = s.mid[0];
+    v = s.mid[1];
+  } else if (step <= n1) {
+    const double mr = o.s1_range * I.hmin;
+    double d;
+    if (step <= o.s1_lin) d = mr * ((double)step / (double)o.s1_lin);
+    else d = 0.5 * (s.a1 + s.b1);
+    u = s.mid[0] + d * s.ray[0];
+    v = s.mid[1] + d * s.ray[1];
+  } else {
+    const int r = m < Q ? 0 : 1;
+    const double dir0 = r == 0 ? -s.dl[0] : s.dl[0], dir1 = r == 0 ? -s.dl[1] : s.dl[1];
+    const double mr = o.s2_range * I.hmin;
+    const int k = step - n1;
+    double d;
+    if (k <= o.s2_lin) d = mr * ((double)k / (double)o.s2_lin);
+    else d = 0.5 * (s.a2[r] + s.b2[r]);
+    u = s.q2[0] + d * dir0;
+    v = s.q2[1] + d * dir1;
+  }
+  double p[3];
+  lift(I, u, v, p);
+  pts[3 * m] = p[0];
+  pts[3 * m + 1] = p[1];
+  pts[3 * m + 2] = p[2];
+}
+
+__global__ void k_s2_update(GridP g, OptP o, const uint32_t* __restrict__ L, const int64_t* __restrict__ inst_key,
+                            int64_t Q, int step, const uint8_t* __restrict__ lab, Search2DState* __restrict__ S,
+                            DevStatus* dst) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  const int n1 = o.s1_lin + o.s1_bin;
+  Search2DState s = S[q];
+  Inst2D I;
+  inst_frame(g, inst_key[q], I);
+  I.hu = g.h[I.bu];
+  I.hv = g.h[I.bv];
+  I.hmin = I.hu < I.hv ? I.hu : I.hv;
+  if (step == 0) {
+    s.mid_label = lab[q];
+    // corner labels for the ray side
+    const int64_t fk = inst_key[q] >> 1;
+    const int64_t vid = fk / 3;
+    const int64_t w1 = vid + vstep(g, I.bu), w3 = vid + vstep(g, I.bv), w2 = w1 + vstep(g, I.bv);
+    I.cl[0] = label_at(L, g, vid);
+    I.cl[1] = label_at(L, g, w1);
+    I.cl[2] = label_at(L, g, w2);
+    I.cl[3] = label_at(L, g, w3);
+    Chord ch;
+    ch.mid[0] = s.mid[0];
+    ch.mid[1] = s.mid[1];
+    ch.dl[0] = s.dl[0];
+    ch.dl[1] = s.dl[1];
+    ch.degen = s.degen;
+    if (!ray_direction(I, ch, s.mid_label, s.ray)) raise_status(dst, ODC_E_ASSERT, q);
+    s.first1 = o.s1_lin;
+    s.found1 = 0;
+  } else if (step <= n1) {
+    const double mr = o.s1_range * I.hmin;
+    if (step <= o.s1_lin) {
+      if (lab[q] != s.mid_label && !s.found1) {
+        s.first1 = step;
+        s.found1 = 1;
+      }
+      if (step == o.s1_lin) {
+        s.a1 = mr * ((double)(s.first1 - 1) / (double)o.s1_lin);
+        s.b1 = mr * ((double)s.first1 / (double)o.s1_lin);
+      }
+    } else {
+      const double mm = 0.5 * (s.a1 + s.b1);
+      if (lab[q] == s.mid_label) s.a1 = mm; else s.b1 = mm;
+    }
+    if (step == n1) {
+      s.q2[0] = s.mid[0] + s.a1 * s.ray[0];
+      s.q2[1] = s.mid[1] + s.a1 * s.ray[1];
+      s.first2[0] = s.first2[1] = o.s2_lin;
+      s.found2[0] = s.found2[1] = 0;
+    }
+  } else {
+    const double mr = o.s2_range * I.hmin;
+    const int k = step - n1;
+    for (int r = 0; r < 2; r++) {
+      const uint8_t l = lab[q + r * Q];
+      if (k <= o.s2_lin) {
+        if (l != s.mid_label && !s.found2[r]) {
+          s.first2[r] = k;
+          s.found2[r] = 1;
+        }
+        if (k == o.s2_lin) {
+          s.a2[r] = mr * ((double)(s.first2[r] - 1) / (double)o.s2_lin);
+          s.b2[r] = mr * ((double)s.first2[r] / (double)o.s2_lin);
+        }
+      } else {
+        const double mm = 0.5 * (s.a2[r] + s.b2[r]);
+        if (l == s.mid_label) s.a2[r] = mm; else s.b2[r] = mm;
+      }
+    }
+  }
+  S[q] = s;
+}
+
+__global__ void k_s2_finish(GridP g, OptP o, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+                            const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
+                            const Search2DState* __restrict__ S, Stage2D out, DevStats* st) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  Inst2D I;
+  int64_t pair[2];
+  decode_instance(g, L, rec, inst_key[q], pos1d, I, pair);
+  const Search2DState s = S[q];
+  Chord ch;
+  ch.mid[0] = s.mid[0];
+  ch.mid[1] = s.mid[1];
+  ch.dl[0] = s.dl[0];
+  ch.dl[1] = s.dl[1];
+  ch.degen = s.degen;
+  const double qa[2] = {s.q2[0] + s.a2[0] * -s.dl[0], s.q2[1] + s.a2[0] * -s.dl[1]};
+  const double qb[2] = {s.q2[0] + s.a2[1] * s.dl[0], s.q2[1] + s.a2[1] * s.dl[1]};
+  double p2d[2];
+  uint8_t status;
+  finish2d(I, ch, s.a1, s.found1, qa, s.found2[0], qb, s.found2[1], p2d, status);
+  double p3[3];
+  lift(I, p2d[0], p2d[1], p3);
+  out.pos3[3 * q] = p3[0];
+  out.pos3[3 * q + 1] = p3[1];
+  out.pos3[3 * q + 2] = p3[2];
+  if (out.pos2) {
+    out.pos2[2 * q] = p2d[0];
+    out.pos2[2 * q + 1] = p2d[1];
+  }
+  if (out.status) out.status[q] = status;
+  if (out.mid) out.mid[q] = s.mid_label;
+  atomicAdd(&st->status[status], 1ull);
+}
+
+void launch_search2d_lockstep_init(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+                                   const int64_t* inst_key, int64_t Q, const double* pos1d, void* state,
+                                   int64_t* inst_edges, cudaStream_t s) {
+  (void)o;
+  if (Q)
+    k_s2_init<<<grid_for(Q, 128), 128, 0, s>>>(g, L, rec, inst_key, Q, pos1d, (Search2DState*)state, inst_edges);
+}
+int64_t launch_search2d_lockstep_points(const GridP& g, const OptP& o, const int64_t* inst_key, int64_t Q, int step,
+                                        const void* state, double* pts, cudaStream_t s) {
+  const int n1 = o.s1_lin + o.s1_bin;
+  int64_t M = step > n1 ? 2 * Q : Q;
+  if (M) k_s2_points<<<grid_for(M, 128), 128, 0, s>>>(g, o, inst_key, Q, step, (const Search2DState*)state, pts);
+  return M;
+}
+void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
+                                     int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
+                                     cudaStream_t s) {
+  if (Q)
+    k_s2_update<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, inst_key, Q, step, lab, (Search2DState*)state, dst);
+}
+void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+                                     const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,
+                                     Stage2D out, DevStats* st, cudaStream_t s) {
+  if (Q)
+    k_s2_finish<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, rec, inst_key, Q, pos1d, (const Search2DState*)state, out,
+                                                 st);
+}
+
+// ===========================================================================
+// fd-gradient normals (pipeline.py:126-151), ablation path
+// ===========================================================================
+__global__ void k_fd_points(GridP g, double step, const double* __restrict__ pos1d, int64_t K,
+                            double* __restrict__ pts) {
+  int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= 6 * K) return;
+  const int i = (int)(m / K);
+  const int64_t k = m - (int64_t)i * K;
+  for (int c = 0; c < 3; c++) {
+    const double e = (c == i % 3) ? step : 0.0;
+    pts[3 * m + c] = i < 3 ? pos1d[3 * k + c] + e : pos1d[3 * k + c] - e;
+  }
+}
+void launch_fd_points(const GridP& g, const OptP& o, const double* pos1d, int64_t K, double* pts, cudaStream_t s) {
+  double hmin = g.h[0] < g.h[1] ? g.h[0] : g.h[1];
+  hmin = hmin < g.h[2] ? hmin : g.h[2];
+  if (K) k_fd_points<<<grid_for(6 * K, 256), 256, 0, s>>>(g, o.fd_step * hmin, pos1d, K, pts);
+}
+__global__ void k_eval_raw(FieldP f, const double* __restrict__ pts, int64_t n, double* __restrict__ raw,
+                           uint8_t* __restrict__ lab) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+  const double r = field_raw(f, p);
+  if (raw) raw[i] = r;
+  if (lab) lab[i] = r > f.iso ? 1 : 0;
+}
+void launch_fd_raw_analytic(const FieldP& f, const double* pts, int64_t n, double* raw, cudaStream_t s) {
+  if (n) k_eval_raw<<<grid_for(n, 128), 128, 0, s>>>(f, pts, n, raw, nullptr);
+}
+void launch_eval_raw_analytic(const FieldP& f, const double* pts, int64_t n, double* raw, uint8_t* lab,
+                              cudaStream_t s) {
+  if (n) k_eval_raw<<<grid_for(n, 128), 128, 0, s>>>(f, pts, n, raw, lab);
+}
+__global__ void k_fd_normals(GridP g, double step, const uint32_t* __restrict__ L,
+                             const int64_t* __restrict__ edge_key, int64_t K, const double* __restrict__ raw,
+                             double* __restrict__ nrm, DevStats* st) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double gr[3], n[3];
+  for (int i = 0; i < 3; i++) gr[i] = (raw[i * K + k] - raw[(i + 3) * K + k]) / (2.0 * step);
+  const double nr = norm3(gr);
+  EdgeGeom e = edge_geom(g, L, edge_key[k]);
+  const double el = norm3(e.span);
+  const bool bad = nr < 1e-30;
+  const double sn = bad ? 1.0 : nr;
+  for (int c = 0; c < 3; c++) n[c] = bad ? e.span[c] / el : -gr[c] / sn;
+  if (einsum3(n, e.span) < 0.0)
+    for (int c = 0; c < 3; c++) n[c] = -n[c];
+  for (int c = 0; c < 3; c++) nrm[3 * k + c] = n[c];
+  if (bad) atomicAdd(&st->normal_fallbacks, 1ull);
+}
+void launch_fd_normals(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* edge_key, int64_t K,
+                       const double* raw, double* edge_normals, DevStats* st, cudaStream_t s) {
+  double hmin = g.h[0] < g.h[1] ? g.h[0] : g.h[1];
+  hmin = hmin < g.h[2] ? hmin : g.h[2];
+  if (K) k_fd_normals<<<grid_for(K, 128), 128, 0, s>>>(g, o.fd_step * hmin, L, edge_key, K, raw, edge_normals, st);
+}
+
+// ===========================================================================
+// K6: per-cell partitions (dualize.py:194-238 via the cycle table), plane
+// samples + normals (dualize.py:299-317, :402-429), QEF (dualize.py:332-372)
+// ===========================================================================
+__constant__ int c_LE_CORNER[12] = {0, 0, 0, 1, 1, 2, 2, 3, 4, 4, 5, 6};
+__constant__ int c_LE_AXIS[12] = {0, 1, 2, 1, 2, 0, 2, 2, 0, 1, 1, 0};
+__constant__ int c_LF_CORNER[6] = {0, 0, 0, 1, 2, 4};
+__constant__ int c_LF_NORMAL[6] = {0, 1, 2, 0, 1, 2};
+
+__device__ __forceinline__ int64_t cell_base_vid(const GridP& g, int64_t cell) {
+  const int64_t x = cell % g.R, y = (cell / g.R) % g.R, z = cell / (g.R * g.R);
+  return x + y * g.S + z * g.S2;
+}
+__device__ __forceinline__ int64_t corner_off(const GridP& g, int c) {
+  return (int64_t)(c & 1) + ((c >> 1) & 1) * g.S + ((c >> 2) & 1) * g.S2;
+}
+
+__global__ void k_cell_config(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+                              const int64_t* __restrict__ cell_id, int64_t C, const CellTabEntry* __restrict__ table,
+                              uint16_t* __restrict__ cfg_out, uint32_t* __restrict__ ncyc,
+                              uint32_t* __restrict__ nsamp) {
+  int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= C) return;
+  const int64_t base = cell_base_vid(g, cell_id[ci]);
+  uint32_t cfg = 0;
+  for (int i = 0; i < 8; i++) cfg |= label_at(L, g, base + corner_off(g, i)) << i;
+  uint32_t cm = 0;
+  for (int f = 0; f < 6; f++) {
+    const int64_t v = base + corner_off(g, c_LF_CORNER[f]);
+    int64_t c[3];
+    vid_coords(g, v, c);
+    cm |= ((rec[word_of(g, c[0], c[1], c[2])].cf[c_LF_NORMAL[f]] >> (c[0] & 31)) & 1u) << f;
+  }
+  const uint32_t idx = (cfg << 6) | cm;
+  const CellTabEntry& T = table[idx];
+  cfg_out[ci] = (uint16_t)idx;
+  ncyc[ci] = T.ncyc;
+  nsamp[ci] = T.nedge;
+}
+
+void launch_cell_config(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* cell_id, int64_t C,
+                        const CellTabEntry* table, uint16_t* cfg, uint32_t* ncyc, uint32_t* nsamp, cudaStream_t s) {
+  if (C) k_cell_config<<<grid_for(C, 128), 128, 0, s>>>(g, L, rec, cell_id, C, table, cfg, ncyc, nsamp);
+}
+
+// symmetric 3x3 eigen-solver (cyclic Jacobi; the CPU oracle runs the same
+// algorithm in the same order), eigenvalues ascending like LAPACK
+static __device__ void jacobi3(const double Ain[9], double w[3], double V[9]) {
+  double a[3][3];
+  double v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) a[i][j] = Ain[3 * i + j];
+  const int PQ[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+  for (int sweep = 0; sweep < 16; sweep++) {
+    const double off = (a[0][1] * a[0][1] + a[0][2] * a[0][2]) + a[1][2] * a[1][2];
+    if (off == 0.0) break;
+    for (int k = 0; k < 3; k++) {
+      const int p = PQ[k][0], q = PQ[k][1];
+      const double apq = a[p][q];
+      if (apq == 0.0) continue;
+      const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+      double t;
+      if (fabs(theta) > 1e150) {
+        t = 1.0 / (2.0 * theta);
+      } else {
+        t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+        if (theta < 0.0) t = -t;
+      }
+      const double c = 1.0 / sqrt(t * t + 1.0);
+      const double s = t * c;
+      const double tau = s / (1.0 + c);
+      const double app = a[p][p], aqq = a[q][q];
+      a[p][p] = app - t * apq;
+      a[q][q] = aqq + t * apq;
+      a[p][q] = a[q][p] = 0.0;
+      const int r = 3 - p - q;
+      const double arp = a[r][p], arq = a[r][q];
+      a[r][p] = a[p][r] = arp - s * (arq + tau * arp);
+      a[r][q] = a[q][r] = arq + s * (arp - tau * arq);
+      for (int i = 0; i < 3; i++) {
+        const double vip = v[i][p], viq = v[i][q];
+        v[i][p] = vip - s * (viq + tau * vip);
+        v[i][q] = viq + s * (vip - tau * viq);
+      }
+    }
+  }
+  int idx[3] = {0, 1, 2};
+  const double d[3] = {a[0][0], a[1][1], a[2][2]};
+  for (int i = 0; i < 3; i++)
+    for (int j = i + 1; j < 3; j++)
+      if (d[idx[j]] < d[idx[i]]) {
+        int t = idx[i];
+        idx[i] = idx[j];
+        idx[j] = t;
+      }
+  for (int k = 0; k < 3; k++) {
+    w[k] = d[idx[k]];
+    for (int i = 0; i < 3; i++) V[3 * i + k] = v[i][idx[k]];
+  }
+}
+
+__global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint32_t* __restrict__ L,
+                                                    const WordRec* __restrict__ rec,
+                                                    const int64_t* __restrict__ cell_id, int64_t C,
+                                                    const CellTabEntry* __restrict__ table,
+                                                    const uint16_t* __restrict__ cfg,
+                                                    const uint32_t* __restrict__ part_base,
+                                                    const uint32_t* __restrict__ samp_base,
+                                                    const double* __restrict__ pos1d, const double* __restrict__ pos3,
+                                                    const double* __restrict__ edge_normals, CellOut out,
+                                                    DevStats* st) {
+  int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= C) return;
+  const int64_t cell = cell_id[ci];
+  const int64_t base = cell_base_vid(g, cell);
+  const CellTabEntry T = table[cfg[ci]];
+  const int64_t pbase = part_base[ci];
+  const int64_t sbase = samp_base[ci];
+  out.pinfo[ci] = ((uint64_t)pbase << 24) | T.cyc_of_edge;
+  double hmin = g.h[0] < g.h[1] ? g.h[0] : g.h[1];
+  hmin = hmin < g.h[2] ? hmin : g.h[2];
+  const int64_t cc[3] = {cell % g.R, (cell / g.R) % g.R, cell / (g.R * g.R)};
+  uint32_t nfb = 0;
+  int slot = 0;
+  for (int k = 0; k < T.ncyc; k++) {
+    const int len = (T.lens >> (4 * k)) & 15;
+    double pe[12][3], nn[12][3];
+    int64_t iid[12];
+    // instance ids of the cycle (instance j joins edge j and j+1)
+    for (int j = 0; j < len; j++) {
+      const int code = (int)((T.insts >> (4 * (slot + j))) & 15);
+      const int f = code >> 1, s = code & 1;
+      iid[j] = inst_rank(rec, g, base + corner_off(g, c_LF_CORNER[f]), c_LF_NORMAL[f]) + s;
+    }
+    for (int j = 0; j < len; j++) {
+      const int le = (int)((T.edges >> (4 * (slot + j))) & 15);
+      const int64_t ev = base + corner_off(g, c_LE_CORNER[le]);
+      const int ax = c_LE_AXIS[le];
+      const int64_t row = edge_rank(rec, g, ev, ax);
+      for (int c = 0; c < 3; c++) pe[j][c] = pos1d[3 * row + c];
+      if (out.cyc_edges) {
+        out.cyc_edges[sbase + slot + j] = ev * 3 + ax;
+        out.cyc_insts[sbase + slot + j] = iid[j];
+      }
+      // edge direction p_out - p_in (dualize.py:421-423)
+      double pi[3], po[3], ed[3];
+      const int64_t other = ev + vstep(g, ax);
+      const bool base_in = label_at(L, g, ev) == 1u;
+      vposition(g, base_in ? ev : other, pi);
+      vposition(g, base_in ? other : ev, po);
+      for (int c = 0; c < 3; c++) ed[c] = po[c] - pi[c];
+      double n[3];
+      if (o.normals == ODC_NORMALS_2D) {
+        // estimate_normals (dualize.py:299-317)
+        const int64_t ia = iid[(j - 1 + len) % len], ib = iid[j];
+        double da[3], db[3];
+        for (int c = 0; c < 3; c++) {
+          da[c] = pos3[3 * ia + c] - pe[j][c];
+          db[c] = pos3[3 * ib + c] - pe[j][c];
+        }
+        cross3(da, db, n);
+        const double nr = norm3(n);
+        const bool fb = nr <= 1e-9 * hmin * hmin;
+        const double el = norm3(ed);
+        const double safe = fb ? 1.0 : nr;
+        for (int c = 0; c < 3; c++) n[c] = n[c] / safe;
+        if (fb) {
+          for (int c = 0; c < 3; c++) n[c] = ed[c] / el;
+          nfb++;
+        }
+        if (einsum3(n, ed) < 0.0)
+          for (int c = 0; c < 3; c++) n[c] = -n[c];
+      } else {
+        for (int c = 0; c < 3; c++) n[c] = edge_normals[3 * row + c];
+      }
+      for (int c = 0; c < 3; c++) nn[j][c] = n[c];
+      if (out.normals)
+        for (int c = 0; c < 3; c++) out.normals[3 * (sbase + slot + j) + c] = n[c];
+    }
+    // solve_qef_batch (dualize.py:332-372), sums sequential in cycle order
+    const double cnt = (double)(len < 1 ? 1 : len);
+    double cen[3] = {0.0, 0.0, 0.0};
+    for (int j = 0; j < len; j++)
+      for (int c = 0; c < 3; c++) cen[c] += pe[j][c];
+    for (int c = 0; c < 3; c++) cen[c] /= cnt;
+    double A[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, b[3] = {0.0, 0.0, 0.0};
+    for (int j = 0; j < len; j++)
+      for (int r = 0; r < 3; r++)
+        for (int c = 0; c < 3; c++) A[3 * r + c] += nn[j][r] * nn[j][c];
+    for (int j = 0; j < len; j++) {
+      const double d[3] = {pe[j][0] - cen[0], pe[j][1] - cen[1], pe[j][2] - cen[2]};
+      const double off = einsum3(nn[j], d);
+      for (int c = 0; c < 3; c++) b[c] += nn[j][c] * off;
+    }
+    double w[3], V[9];
+    jacobi3(A, w, V);
+    double sv[3];
+    for (int kk = 0; kk < 3; kk++) sv[kk] = sqrt(w[kk] > 0.0 ? w[kk] : 0.0);
+    const double smax = sv[2];
+    const double thr = o.qef_trunc * (smax > 1e-300 ? smax : 1e-300);
+    bool keep[3];
+    int rank = 0;
+    for (int kk = 0; kk < 3; kk++) {
+      keep[kk] = (sv[kk] >= thr) && (smax > 0.0);
+      rank += keep[kk];
+    }
+    double coef[3], y[3], sol[3];
+    for (int j = 0; j < 3; j++) coef[j] = (V[j] * b[0] + V[3 + j] * b[1]) + V[6 + j] * b[2];
+    for (int j = 0; j < 3; j++) y[j] = keep[j] ? coef[j] / w[j] : 0.0;
+    for (int i = 0; i < 3; i++) sol[i] = (V[3 * i] * y[0] + V[3 * i + 2] * y[2]) + V[3 * i + 1] * y[1];
+    double pos[3];
+    for (int c = 0; c < 3; c++) {
+      const double blo = g.lo[c] + (double)cc[c] * g.h[c];  // cell_bounds (grid.py:89-91)
+      const double bhi = blo + g.h[c];
+      double x = cen[c] + sol[c];
+      x = x > blo ? x : blo;  // np.clip
+      x = x < bhi ? x : bhi;
+      pos[c] = x;
+    }
+    double res = 0.0;
+    for (int j = 0; j < len; j++) {
+      const double d[3] = {pos[0] - pe[j][0], pos[1] - pe[j][1], pos[2] - pe[j][2]};
+      const double e = einsum3(nn[j], d);
+      res += e * e;
+    }
+    const int64_t pid = pbase + k;
+    for (int c = 0; c < 3; c++) out.verts[3 * pid + c] = pos[c];
+    out.part_cell[pid] = cell;
+    out.part_index[pid] = k;
+    if (out.cyc_len) out.cyc_len[pid] = len;
+    if (out.rank) out.rank[pid] = rank;
+    if (out.resid) out.resid[pid] = res;
+    atomicAdd(&st->rank[rank], 1ull);
+    atomic_max_nonneg_double(&st->max_resid_bits, res);
+    slot += len;
+  }
+  if (nfb) atomicAdd(&st->normal_fallbacks, (unsigned long long)nfb);
+}
+
+void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec, const int64_t* cell_id,
+                       int64_t C, const CellTabEntry* table, const uint16_t* cfg, const uint32_t* part_base,
+                       const uint32_t* samp_base, const double* pos1d, const double* pos3, const double* edge_normals,
+                       CellOut out, DevStats* st, cudaStream_t s) {
+  if (C)
+    k_cell_solve<<<grid_for(C, 128), 128, 0, s>>>(g, o, L, rec, cell_id, C, table, cfg, part_base, samp_base, pos1d,
+                                                  pos3, edge_normals, out, st);
+}
+
+// generic multi-channel exclusive scan over u32 arrays (<= 2 channels)
+struct ScanPtrs {
+  const uint32_t* in[2];
+  uint32_t* out[2];
+};
+template <int NCH>
+__global__ void __launch_bounds__(kScanBlock) k_reduce_u32(ScanPtrs p, int64_t n, uint32_t* sums, int64_t ntiles) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t v[NCH], ex[NCH], tot[NCH];
+  for (int c = 0; c < NCH; c++) v[c] = i < n ? p.in[c][i] : 0u;
+  block_exscan<NCH>(v, ex, tot);
+  if (threadIdx.x == 0)
+    for (int c = 0; c < NCH; c++) sums[c * ntiles + blockIdx.x] = tot[c];
+}
+template <int NCH>
+__global__ void __launch_bounds__(kScanBlock) k_apply_u32(ScanPtrs p, int64_t n, const uint32_t* sums,
+                                                          int64_t ntiles) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t v[NCH], ex[NCH], tot[NCH];
+  for (int c = 0; c < NCH; c++) v[c] = i < n ? p.in[c][i] : 0u;
+  block_exscan<NCH>(v, ex, tot);
+  if (i < n)
+    for (int c = 0; c < NCH; c++) p.out[c][i] = sums[c * ntiles + blockIdx.x] + ex[c];
+}
+void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
+                     unsigned long long* totals, cudaStream_t s) {
+  ScanPtrs p{};
+  for (int c = 0; c < nch; c++) {
+    p.in[c] = in[c];
+    p.out[c] = out[c];
+  }
+  const int64_t nt = (n + kScanBlock - 1) / kScanBlock;
+  if (nt == 0) {
+    cudaMemsetAsync(totals, 0, sizeof(unsigned long long) * nch, s);
+    return;
+  }
+  if (nch == 1) {
+    k_reduce_u32<1><<<(unsigned)nt, kScanBlock, 0, s>>>(p, n, tile_buf, nt);
+    k_scan_tiles<1><<<1, 1024, 0, s>>>(tile_buf, nt, totals);
+    k_apply_u32<1><<<(unsigned)nt, kScanBlock, 0, s>>>(p, n, tile_buf, nt);
+  } else {
+    k_reduce_u32<2><<<(unsigned)nt, kScanBlock, 0, s>>>(p, n, tile_buf, nt);
+    k_scan_tiles<2><<<1, 1024, 0, s>>>(tile_buf, nt, totals);
+    k_apply_u32<2><<<(unsigned)nt, kScanBlock, 0, s>>>(p, n, tile_buf, nt);
+  }
+}
+
+// ===========================================================================
+// K7: polygonization (polygonize.py:110-217)
+// ===========================================================================
+__constant__ int8_t c_le_of[8][3] = {{0, 1, 2}, {-1, 3, 4}, {5, -1, 6}, {-1, -1, 7},
+                                     {8, 9, -1}, {-1, 10, -1}, {11, -1, -1}, {-1, -1, -1}};
+
+__global__ void __launch_bounds__(128) k_poly_classify(GridP g, OptP o, const uint32_t* __restrict__ L,
+                                                       const WordRec* __restrict__ rec,
+                                                       const int64_t* __restrict__ edge_key, int64_t K,
+                                                       const uint64_t* __restrict__ pinfo,
+                                                       const double* __restrict__ verts, int4* __restrict__ pid4,
+                                                       uint8_t* __restrict__ kase, uint32_t* __restrict__ ntri,
+                                                       uint32_t* __restrict__ nfan, DevStats* st) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int64_t key = edge_key[k], vid = key / 3;
+  const int a = (int)(key % 3), b = (a + 1) % 3, c = (a + 2) % 3;
+  int64_t vc[3];
+  vid_coords(g, vid, vc);
+  const bool fwd = label_at(L, g, vid) == 1u;  // v_in == edge_vertex
+  const int RING[4][2] = {{-1, -1}, {0, -1}, {0, 0}, {-1, 0}};
+  int pid[4];
+  bool ok = true;
+  for (int j = 0; j < 4; j++) {
+    const int rj = fwd ? j : 3 - j;
+    int64_t cc[3] = {vc[0], vc[1], vc[2]};
+    cc[b] += RING[rj][0];
+    cc[c] += RING[rj][1];
+    for (int t = 0; t < 3; t++)
+      if (cc[t] < 0 || cc[t] >= g.R) ok = false;
+    if (!ok) break;
+    const int64_t cbase = cc[0] + cc[1] * g.S + cc[2] * g.S2;
+    const int64_t crow = cell_rank(rec, g, cbase);
+    const uint64_t pi = pinfo[crow];
+    const int corner = (int)(vc[0] - cc[0]) | ((int)(vc[1] - cc[1]) << 1) | ((int)(vc[2] - cc[2]) << 2);
+    const int le = c_le_of[corner][a];
+    const int cyc = (int)((pi >> (2 * le)) & 3u);
+    pid[j] = (int)((pi >> 24) + cyc);
+  }
+  if (!ok) {
+    kase[k] = 0;
+    ntri[k] = 0;
+    nfan[k] = 0;
+    atomicAdd(&st->skipped, 1ull);
+    return;
+  }
+  int cs = 1;
+  if (o.split == ODC_SPLIT_IC) {
+    // _concavity (polygonize.py:47-75)
+    double pin[3], pout[3];
+    const int64_t other = vid + vstep(g, a);
+    vposition(g, fwd ? vid : other, pin);
+    vposition(g, fwd ? other : vid, pout);
+    double q[4][3];
+    for (int j = 0; j < 4; j++)
+      for (int t = 0; t < 3; t++) q[j][t] = verts[3 * (int64_t)pid[j] + t];
+    bool conc[4];
+    for (int kk = 0; kk < 4; kk++) {
+      const double* pk = q[kk];
+      const double* da = q[(kk + 3) & 3];
+      const double* db = q[(kk + 1) & 3];
+      double u[3], v[3], w[3], x[3];
+      for (int t = 0; t < 3; t++) {
+        u[t] = da[t] - pout[t];
+        v[t] = db[t] - pout[t];
+        w[t] = pk[t] - pout[t];
+      }
+      cross3(u, v, x);
+      const bool plus = einsum3(w, x) < 0.0;
+      for (int t = 0; t < 3; t++) {
+        u[t] = da[t] - pin[t];
+        v[t] = db[t] - pin[t];
+        w[t] = pk[t] - pin[t];
+      }
+      cross3(u, v, x);
+      const bool minus = einsum3(w, x) > 0.0;
+      conc[kk] = plus || minus;
+    }
+    if (!(conc[1] || conc[3])) cs = 1;
+    else if (!(conc[0] || conc[2])) cs = 2;
+    else cs = 3;
+  }
+  pid4[k] = make_int4(pid[0], pid[1], pid[2], pid[3]);
+  kase[k] = (uint8_t)cs;
+  ntri[k] = cs == 3 ? 4u : 2u;
+  nfan[k] = cs == 3 ? 1u : 0u;
+  atomicAdd(&st->split[cs], 1ull);
+}
+
+void launch_poly_classify(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+                          const int64_t* edge_key, int64_t K, const uint64_t* pinfo, const double* verts, int4* pid4,
+                          uint8_t* kase, uint32_t* ntri, uint32_t* nfan, DevStats* st, cudaStream_t s) {
+  if (K)
+    k_poly_classify<<<grid_for(K, 128), 128, 0, s>>>(g, o, L, rec, edge_key, K, pinfo, verts, pid4, kase, ntri, nfan,
+                                                     st);
+}
+
+__global__ void k_poly_emit(int64_t K, int64_t P, const int64_t* __restrict__ edge_key, const int4* __restrict__ pid4,
+                            const uint8_t* __restrict__ kase, const uint32_t* __restrict__ tri_off,
+                            const uint32_t* __restrict__ fan_rank, const double* __restrict__ pos1d,
+                            double* __restrict__ verts, int32_t* __restrict__ tris, int64_t* __restrict__ fan_edge,
+                            uint8_t* __restrict__ used) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int cs = kase[k];
+  if (cs == 0) return;
+  const int4 p = pid4[k];
+  int32_t* t = tris + 3 * (int64_t)tri_off[k];
+  if (cs == 1) {
+    t[0] = p.x; t[1] = p.y; t[2] = p.z;
+    t[3] = p.x; t[4] = p.z; t[5] = p.w;
+  } else if (cs == 2) {
+    t[0] = p.x; t[1] = p.y; t[2] = p.w;
+    t[3] = p.y; t[4] = p.z; t[5] = p.w;
+  } else {
+    const int64_t fr = fan_rank[k];
+    const int32_t fv = (int32_t)(P + fr);
+    const int q[4] = {p.x, p.y, p.z, p.w};
+    for (int j = 0; j < 4; j++) {
+      t[3 * j] = fv;
+      t[3 * j + 1] = q[j];
+      t[3 * j + 2] = q[(j + 1) & 3];
+    }
+    for (int c = 0; c < 3; c++) verts[3 * (P + fr) + c] = pos1d[3 * k + c];
+    fan_edge[fr] = edge_key[k];
+  }
+  used[p.x] = 1;
+  used[p.y] = 1;
+  used[p.z] = 1;
+  used[p.w] = 1;
+}
+
+void launch_poly_emit(int64_t K, int64_t P, const int64_t* edge_key, const int4* pid4, const uint8_t* kase,
+                      const uint32_t* tri_off, const uint32_t* fan_rank, const double* pos1d, double* verts,
+                      int32_t* tris, int64_t* fan_edge, uint8_t* used, cudaStream_t s) {
+  if (K)
+    k_poly_emit<<<grid_for(K, 256), 256, 0, s>>>(K, P, edge_key, pid4, kase, tri_off, fan_rank, pos1d, verts, tris,
+                                                 fan_edge, used);
+}
+
+__global__ void k_count_used(const uint8_t* __restrict__ used, int64_t P, DevStats* st) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t v = (i < P && used[i]) ? 1u : 0u;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&st->used_partitions, (unsigned long long)v);
+}
+void launch_count_used(const uint8_t* used, int64_t P, DevStats* st, cudaStream_t s) {
+  if (P) k_count_used<<<grid_for(P, 256), 256, 0, s>>>(used, P, st);
+}
+
+// drop unreferenced partition vertices (polygonize.py:199-209)
+__global__ void k_remap_tris(int64_t T, const uint32_t* __restrict__ new_id, int32_t* __restrict__ tris) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * T) return;
+  tris[i] = (int32_t)new_id[tris[i]];
+}
+__global__ void k_compact_verts(int64_t V, const uint8_t* __restrict__ used, const uint32_t* __restrict__ new_id,
+                                const double* __restrict__ vin, double* __restrict__ vout,
+                                int64_t* __restrict__ src_of) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V || !used[i]) return;
+  const int64_t j = new_id[i];
+  for (int c = 0; c < 3; c++) vout[3 * j + c] = vin[3 * i + c];
+  src_of[j] = i;
+}
+void launch_remap_vertices(int64_t V, int64_t T, const uint8_t* used, const uint32_t* new_id, const double* v_in,
+                           double* v_out, int32_t* tris, int64_t* src_of, cudaStream_t s) {
+  if (V) k_compact_verts<<<grid_for(V, 256), 256, 0, s>>>(V, used, new_id, v_in, v_out, src_of);
+  if (T) k_remap_tris<<<grid_for(3 * T, 256), 256, 0, s>>>(T, new_id, tris);
+}
+
+__global__ void k_split_cases(int64_t K, const uint8_t* __restrict__ kase, const uint32_t* __restrict__ rank,
+                              int64_t* __restrict__ out) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K || kase[k] == 0) return;
+  out[rank[k]] = kase[k];
+}
+void launch_split_cases(int64_t K, const uint8_t* kase, int64_t* out, uint32_t* rank, cudaStream_t s) {
+  if (K) k_split_cases<<<grid_for(K, 256), 256, 0, s>>>(K, kase, rank, out);
+}
+__global__ void k_interior_flags(int64_t K, const uint8_t* __restrict__ kase, uint32_t* __restrict__ flag) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < K) flag[k] = kase[k] != 0;
+}
+void launch_interior_flags(int64_t K, const uint8_t* kase, uint32_t* flag, cudaStream_t s) {
+  if (K) k_interior_flags<<<grid_for(K, 256), 256, 0, s>>>(K, kase, flag);
+}
+
+// ===========================================================================
+// K8: repair_nonmanifold (polygonize.py:220-374).  Per vertex: its incident
+// triangles (ascending), the edges (v,u) to its neighbours with their
+// triangle lists (every triangle on edge (v,u) contains v, so the local count
+// is the global count), sheet pairing of >2-triangle edges by dihedral angle
+// (polygonize.py:279-305) and union-find over incident triangles
+// (polygonize.py:308-347).  Extra components get new vertex ids in vertex
+// order (polygonize.py:348-358).
+// ===========================================================================
+constexpr int kMaxFan = 64;
+
+__global__ void k_vertex_degree(const int32_t* __restrict__ tris, int64_t T, uint32_t* __restrict__ deg) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * T) return;
+  atomicAdd(&deg[tris[i]], 1u);
+}
+void launch_vertex_degree(const int32_t* tris, int64_t T, uint32_t* deg, cudaStream_t s) {
+  if (T) k_vertex_degree<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, deg);
+}
+__global__ void k_vertex_fill(const int32_t* __restrict__ tris, int64_t T, const uint32_t* __restrict__ off,
+                              uint32_t* __restrict__ cursor, int32_t* __restrict__ inc) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * T) return;
+  const int32_t v = tris[i];
+  const uint32_t slot = atomicAdd(&cursor[v], 1u);
+  inc[off[v] + slot] = (int32_t)(i / 3);
+}
+void launch_vertex_fill(const int32_t* tris, int64_t T, const uint32_t* off, uint32_t* cursor, int32_t* inc,
+                        cudaStream_t s) {
+  if (T) k_vertex_fill<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, off, cursor, inc);
+}
+
+// components of vertex v's fan; comp[i] in first-appearance order (= order
+// of the minimum triangle id, since tl is ascending)
+static __device__ int fan_components(const double* __restrict__ verts, const int32_t* __restrict__ tris, int32_t v,
+                              const int32_t* tl, int nt, int* comp) {
+  int parent[kMaxFan];
+  for (int i = 0; i < nt; i++) parent[i] = i;
+  auto find = [&](int x) {
+    while (parent[x] != x) {
+      parent[x] = parent[parent[x]];
+      x = parent[x];
+    }
+    return x;
+  };
+  auto unite = [&](int x, int y) {
+    int rx = find(x), ry = find(y);
+    if (rx != ry) parent[rx] = ry;
+  };
+  // neighbours u: for each, the local triangle indices containing edge (v,u)
+  int32_t nb[2 * kMaxFan];
+  int nnb = 0;
+  for (int i = 0; i < nt; i++) {
+    const int32_t* t = tris + 3 * (int64_t)tl[i];
+    for (int c = 0; c < 3; c++) {
+      const int32_t u = t[c];
+      if (u == v) continue;
+      bool seen = false;
+      for (int j = 0; j < nnb; j++)
+        if (nb[j] == u) seen = true;
+      if (!seen && nnb < 2 * kMaxFan) nb[nnb++] = u;
+    }
+  }
+  for (int j = 0; j < nnb; j++) {
+    const int32_t u = nb[j];
+    int mem[kMaxFan];
+    int nm = 0;
+    for (int i = 0; i < nt; i++) {
+      const int32_t* t = tris + 3 * (int64_t)tl[i];
+      if (t[0] == u || t[1] == u || t[2] == u) mem[nm++] = i;
+    }
+    if (nm == 2) {
+      unite(mem[0], mem[1]);
+    } else if (nm > 2) {
+      // sheet pairing by dihedral angle around edge (a,b), a < b
+      const int32_t a = v < u ? v : u, b = v < u ? u : v;
+      double axis[3];
+      for (int c = 0; c < 3; c++) axis[c] = verts[3 * (int64_t)b + c] - verts[3 * (int64_t)a + c];
+      double an = sqrt(dot3_fma(axis, axis));
+      if (an == 0.0) an = 1.0;
+      for (int c = 0; c < 3; c++) axis[c] /= an;
+      double rel[kMaxFan][3];
+      bool fwd[kMaxFan];
+      for (int m = 0; m < nm; m++) {
+        const int32_t* t = tris + 3 * (int64_t)tl[mem[m]];
+        int32_t other = -1;
+        for (int c = 0; c < 3 && other < 0; c++)
+          if (t[c] != a && t[c] != b) other = t[c];
+        double rr[3];
+        for (int c = 0; c < 3; c++) rr[c] = verts[3 * (int64_t)other + c] - verts[3 * (int64_t)a + c];
+        const double pr = dot3_fma(rr, axis);
+        for (int c = 0; c < 3; c++) rel[m][c] = rr[c] - axis[c] * pr;
+        // direction of the slot holding edge (a,b): e0 < e1 (polygonize.py:229)
+        bool d = false;
+        for (int c = 0; c < 3; c++) {
+          const int32_t e0 = t[c], e1 = t[(c + 1) % 3];
+          if ((e0 == a && e1 == b) || (e0 == b && e1 == a)) d = e0 < e1;
+        }
+        fwd[m] = d;
+      }
+      double ref[3] = {rel[0][0], rel[0][1], rel[0][2]};
+      double rn = sqrt(dot3_fma(ref, ref));
+      if (rn == 0.0) rn = 1.0;
+      for (int c = 0; c < 3; c++) ref[c] /= rn;
+      double perp[3];
+      cross3(axis, ref, perp);
+      double th[kMaxFan];
+      int order[kMaxFan];
+      for (int m = 0; m < nm; m++) {
+        th[m] = atan2(dot3_fma(rel[m], perp), dot3_fma(rel[m], ref));
+        order[m] = m;
+      }
+      for (int x = 1; x < nm; x++) {  // stable insertion sort
+        int y = x;
+        while (y > 0 && th[order[y - 1]] > th[order[y]]) {
+          int tmp = order[y];
+          order[y] = order[y - 1];
+          order[y - 1] = tmp;
+          y--;
+        }
+      }
+      // _pair_fan_triangles (polygonize.py:233-250)
+      const int np = nm / 2;
+      int pa[kMaxFan / 2], pb[kMaxFan / 2];
+      bool done = false;
+      const int nstarts = (nm % 2 == 0) ? 2 : 1;
+      for (int st = 0; st < nstarts && !done; st++) {
+        bool okp = true;
+        for (int i = 0; i < np; i++) {
+          pa[i] = order[(st + 2 * i) % nm];
+          pb[i] = order[(st + 2 * i + 1) % nm];
+          if (fwd[pa[i]] == fwd[pb[i]]) okp = false;
+        }
+        done = okp;
+      }
+      if (!done)
+        for (int i = 0; i < np; i++) {
+          pa[i] = order[2 * i];
+          pb[i] = order[2 * i + 1];
+        }
+      for (int i = 0; i < np; i++) unite(mem[pa[i]], mem[pb[i]]);
+    }
+  }
+  int root_comp[kMaxFan];
+  for (int i = 0; i < nt; i++) root_comp[i] = -1;
+  int ncomp = 0;
+  for (int i = 0; i < nt; i++) {
+    const int r = find(i);
+    if (root_comp[r] < 0) root_comp[r] = ncomp++;
+    comp[i] = root_comp[r];
+  }
+  return ncomp;
+}
+
+__device__ __forceinline__ int load_fan(const uint32_t* off, const int32_t* inc, int64_t v, int32_t* tl) {
+  const uint32_t b = off[v], e = off[v + 1];
+  int nt = (int)(e - b);
+  if (nt > kMaxFan) return -1;
+  for (int i = 0; i < nt; i++) tl[i] = inc[b + i];
+  for (int x = 1; x < nt; x++) {  // ascending triangle ids
+    int32_t key = tl[x];
+    int y = x - 1;
+    while (y >= 0 && tl[y] > key) {
+      tl[y + 1] = tl[y];
+      y--;
+    }
+    tl[y + 1] = key;
+  }
+  return nt;
+}
+
+__global__ void __launch_bounds__(128) k_repair_count(const double* __restrict__ verts,
+                                                      const int32_t* __restrict__ tris, int64_t V,
+                                                      const uint32_t* __restrict__ off,
+                                                      const int32_t* __restrict__ inc, uint32_t* __restrict__ extra,
+                                                      DevStats* st) {
+  int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  int32_t tl[kMaxFan];
+  const int nt = load_fan(off, inc, v, tl);
+  uint32_t ex = 0;
+  if (nt < 0) {
+    atomicAdd(&st->repair_overflow, 1ull);
+  } else if (nt > 1) {
+    int comp[kMaxFan];
+    const int nc = fan_components(verts, tris, (int32_t)v, tl, nt, comp);
+    ex = (uint32_t)(nc - 1);
+  }
+  extra[v] = ex;
+}
+void launch_repair_count(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off, const int32_t* inc,
+                         uint32_t* extra, DevStats* st, cudaStream_t s) {
+  if (V) k_repair_count<<<grid_for(V, 128), 128, 0, s>>>(verts, tris, V, off, inc, extra, st);
+}
+
+__global__ void __launch_bounds__(128) k_repair_apply(const double* __restrict__ verts,
+                                                      const int32_t* __restrict__ tris, int64_t V,
+                                                      const uint32_t* __restrict__ off,
+                                                      const int32_t* __restrict__ inc,
+                                                      const uint32_t* __restrict__ extra_off,
+                                                      int32_t* __restrict__ tris_next,
+                                                      int64_t* __restrict__ src_of_new) {
+  int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const uint32_t e0 = extra_off[v], e1 = extra_off[v + 1];
+  if (e1 == e0) return;
+  int32_t tl[kMaxFan];
+  const int nt = load_fan(off, inc, v, tl);
+  if (nt < 0) return;
+  int comp[kMaxFan];
+  fan_components(verts, tris, (int32_t)v, tl, nt, comp);
+  for (uint32_t x = e0; x < e1; x++) src_of_new[x] = v;
+  for (int i = 0; i < nt; i++) {
+    if (comp[i] == 0) continue;
+    const int32_t nv = (int32_t)(V + e0 + comp[i] - 1);
+    const int64_t t = tl[i];
+    for (int c = 0; c < 3; c++)
+      if (tris[3 * t + c] == (int32_t)v) tris_next[3 * t + c] = nv;
+  }
+}
+void launch_repair_apply(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off, const int32_t* inc,
+                         const uint32_t* extra_off, int32_t* tris_next, int64_t* src_of_new, cudaStream_t s) {
+  if (V) k_repair_apply<<<grid_for(V, 128), 128, 0, s>>>(verts, tris, V, off, inc, extra_off, tris_next, src_of_new);
+}
+
+__global__ void k_copy_vertices(const double* __restrict__ src, const int64_t* __restrict__ src_of, int64_t base,
+                                int64_t n, double* __restrict__ dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t s = src_of[i];
+  for (int c = 0; c < 3; c++) dst[3 * (base + i) + c] = src[3 * s + c];
+}
+void launch_copy_vertices(const double* src, const int64_t* src_of, int64_t base, int64_t n, double* dst,
+                          cudaStream_t s) {
+  if (n) k_copy_vertices<<<grid_for(n, 256), 256, 0, s>>>(src, src_of, base, n, dst);
+}
+
+__global__ void k_provenance(int64_t V, int64_t P, const int64_t* __restrict__ src_of,
+                             const int64_t* __restrict__ part_cell, const int64_t* __restrict__ part_index,
+                             const int64_t* __restrict__ fan_edge, int64_t* __restrict__ kind,
+                             int64_t* __restrict__ ref) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const int64_t s = src_of ? src_of[i] : i;
+  if (s < P) {
+    kind[i] = 0;
+    ref[2 * i] = part_cell[s];
+    ref[2 * i + 1] = part_index[s];
+  } else {
+    kind[i] = 1;
+    ref[2 * i] = fan_edge[s - P];
+    ref[2 * i + 1] = -1;
+  }
+}
+void launch_provenance(int64_t V, int64_t P, const int64_t* src_of, const int64_t* part_cell,
+                       const int64_t* part_index, const int64_t* fan_edge, int64_t* kind, int64_t* ref,
+                       cudaStream_t s) {
+  if (V) k_provenance<<<grid_for(V, 256), 256, 0, s>>>(V, P, src_of, part_cell, part_index, fan_edge, kind, ref);
+}
+
+}  // namespace odc

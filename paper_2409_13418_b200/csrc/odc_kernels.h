@@ -1,0 +1,165 @@
+// odc_kernels.h -- launch wrappers for the extraction kernels (odc_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "odc_device.cuh"
+#include "odc_tables.h"
+
+namespace odc {
+
+struct Counts5 {  // totals of the active-set scan
+  unsigned long long edges, insts, cells, faces, faces4;
+};
+
+struct DevStats {  // accumulated on the device, read back once
+  unsigned long long boundary_inside;
+  unsigned long long status[4];
+  unsigned long long rank[4];
+  unsigned long long split[4];
+  unsigned long long normal_fallbacks;
+  unsigned long long skipped;
+  unsigned long long max_resid_bits;  // non-negative double, ordered as bits
+  unsigned long long used_partitions;
+  unsigned long long repair_extra;
+  unsigned long long repair_overflow;
+};
+
+struct Stage2D {  // per-instance outputs of the 2D search
+  double* pos2;      // (Q,2)
+  double* pos3;      // (Q,3)
+  uint8_t* status;   // (Q)
+  uint8_t* mid;      // (Q)
+};
+
+struct OptP {
+  int one_d, normals, split, iters_1d, s1_lin, s1_bin, s2_lin, s2_bin, continuous;
+  double s1_range, s2_range, qef_trunc, fd_step;
+};
+
+// K1: labels of every grid vertex as bit-packed rows (grid.py:109-126)
+void launch_labels_analytic(const GridP& g, const FieldP& f, uint32_t* L, cudaStream_t s);
+void launch_pack_labels(const GridP& g, const uint8_t* bytes, uint32_t* L, cudaStream_t s);
+void launch_unpack_labels(const GridP& g, const uint32_t* L, uint8_t* bytes, cudaStream_t s);
+// grid positions in flat vertex order, [begin, begin+n)
+void launch_grid_points(const GridP& g, int64_t begin, int64_t n, double* pts, cudaStream_t s);
+
+// K2: crossing edges / faces / cells + ranks + compaction (grid.py:171-296)
+int64_t active_tiles(const GridP& g);
+void launch_active_bits(const GridP& g, const uint32_t* L, WordRec* rec, uint32_t* tile_sums, DevStats* st,
+                        cudaStream_t s);
+void launch_scan_tiles(uint32_t* sums, int64_t ntiles, int nch, unsigned long long* totals, cudaStream_t s);
+void launch_active_compact(const GridP& g, WordRec* rec, const uint32_t* tile_sums, int64_t* edge_key,
+                           int64_t* inst_key, int64_t* cell_id, int64_t* f4_key, int64_t* face_key,
+                           int64_t* face_nc, cudaStream_t s);
+
+// face-centre probes for 4-crossing faces (dualize.py:59-70)
+void launch_face_center_points(const GridP& g, const int64_t* f4_key, int64_t n, double* pts, cudaStream_t s);
+void launch_face_center_analytic(const GridP& g, const FieldP& f, const int64_t* f4_key, int64_t n, WordRec* rec,
+                                 cudaStream_t s);
+void launch_face_center_scatter(const GridP& g, const int64_t* f4_key, const uint8_t* labels, int64_t n,
+                                WordRec* rec, cudaStream_t s);
+
+// K3: 1D points (search.py:71-94; pipeline.py:94-123)
+void launch_search1d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
+                              const int64_t* edge_key, int64_t K, double* t, double* pos, int64_t* v_in,
+                              cudaStream_t s);
+// lock-step form for batched fields: state (lo, hi) in t/pos scratch
+void launch_search1d_init(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K, double* lo,
+                          double* hi, cudaStream_t s);
+void launch_search1d_points(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K,
+                            const double* lo, const double* hi, double* pts, cudaStream_t s);
+void launch_search1d_update(int64_t K, const uint8_t* lab, double* lo, double* hi, cudaStream_t s);
+void launch_search1d_finish(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* edge_key, int64_t K,
+                            const double* lo, const double* hi, const double* raw_in, const double* raw_out,
+                            double* t, double* pos, int64_t* v_in, cudaStream_t s);
+
+// grid positions of the inside (which=0) / outside (which=1) endpoint of each edge
+void launch_edge_endpoints(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K, int which,
+                           double* pts, cudaStream_t s);
+
+// K5: 2D points (dualize.py:97-129 + search.py:194-322)
+void launch_search2d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
+                              const WordRec* rec, const int64_t* inst_key, int64_t Q, const double* pos1d,
+                              Stage2D out, int64_t* inst_edges, DevStats* st, DevStatus* dst, cudaStream_t s);
+// lock-step form: 31 batches (1 midpoint + s1_lin + s1_bin + s2_lin + s2_bin)
+struct Search2DState;
+size_t search2d_state_bytes(int64_t Q);
+void launch_search2d_lockstep_init(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+                                   const int64_t* inst_key, int64_t Q, const double* pos1d, void* state,
+                                   int64_t* inst_edges, cudaStream_t s);
+// step: 0 = midpoint probe, then step-1 linear/binary, then step-2; returns number of points (Q or 2Q)
+int64_t launch_search2d_lockstep_points(const GridP& g, const OptP& o, const int64_t* inst_key, int64_t Q,
+                                        int step, const void* state, double* pts, cudaStream_t s);
+void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
+                                     int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
+                                     cudaStream_t s);
+void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+                                     const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,
+                                     Stage2D out, DevStats* st, cudaStream_t s);
+int search2d_num_steps(const OptP& o);
+
+// fd-gradient normals (pipeline.py:126-151): 6K raw samples
+void launch_fd_points(const GridP& g, const OptP& o, const double* pos1d, int64_t K, double* pts, cudaStream_t s);
+void launch_fd_raw_analytic(const FieldP& f, const double* pts, int64_t n, double* raw, cudaStream_t s);
+void launch_fd_normals(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* edge_key, int64_t K,
+                       const double* raw, double* edge_normals, DevStats* st, cudaStream_t s);
+
+// K6: per-cell partitions, plane samples, QEF (dualize.py:194-444)
+void launch_cell_config(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* cell_id, int64_t C,
+                        const CellTabEntry* table, uint16_t* cfg, uint32_t* ncyc, uint32_t* nsamp, cudaStream_t s);
+void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
+                     unsigned long long* totals, cudaStream_t s);
+struct CellOut {
+  double* verts;       // (P,3) partition vertices (the first P rows of the mesh)
+  int64_t* part_cell;  // (P)
+  int64_t* part_index; // (P)
+  int64_t* rank;       // (P) (keep only; may be null)
+  double* resid;       // (P) (keep only)
+  uint64_t* pinfo;     // (C) part_base << 24 | cyc_of_edge
+  int64_t* cyc_edges;  // (Ns) keep only
+  int64_t* cyc_insts;  // (Ns) keep only
+  double* normals;     // (Ns,3) keep only
+  int64_t* cyc_len;    // (P) keep only
+};
+void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec, const int64_t* cell_id,
+                       int64_t C, const CellTabEntry* table, const uint16_t* cfg, const uint32_t* part_base,
+                       const uint32_t* samp_base, const double* pos1d, const double* pos3, const double* edge_normals,
+                       CellOut out, DevStats* st, cudaStream_t s);
+
+// K7: polygonization (polygonize.py:110-217)
+void launch_poly_classify(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+                          const int64_t* edge_key, int64_t K, const uint64_t* pinfo, const double* verts,
+                          int4* pid4, uint8_t* kase, uint32_t* ntri, uint32_t* nfan, DevStats* st, cudaStream_t s);
+void launch_poly_emit(int64_t K, int64_t P, const int64_t* edge_key, const int4* pid4, const uint8_t* kase,
+                      const uint32_t* tri_off, const uint32_t* fan_rank, const double* pos1d, double* verts,
+                      int32_t* tris, int64_t* fan_edge, uint8_t* used, cudaStream_t s);
+void launch_count_used(const uint8_t* used, int64_t P, DevStats* st, cudaStream_t s);
+void launch_remap_vertices(int64_t V, int64_t T, const uint8_t* used, const uint32_t* new_id, const double* v_in,
+                           double* v_out, int32_t* tris, int64_t* src_of, cudaStream_t s);
+void launch_split_cases(int64_t K, const uint8_t* kase, int64_t* out, uint32_t* rank, cudaStream_t s);
+void launch_interior_flags(int64_t K, const uint8_t* kase, uint32_t* flag, cudaStream_t s);
+
+// K8: non-manifold repair (polygonize.py:220-374)
+void launch_vertex_degree(const int32_t* tris, int64_t T, uint32_t* deg, cudaStream_t s);
+void launch_vertex_fill(const int32_t* tris, int64_t T, const uint32_t* off, uint32_t* cursor, int32_t* inc,
+                        cudaStream_t s);
+void launch_repair_count(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off,
+                         const int32_t* inc, uint32_t* extra, DevStats* st, cudaStream_t s);
+void launch_repair_apply(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off,
+                         const int32_t* inc, const uint32_t* extra_off, int32_t* tris_next, int64_t* src_of_new,
+                         cudaStream_t s);
+void launch_copy_vertices(const double* src, const int64_t* src_of, int64_t base, int64_t n, double* dst,
+                          cudaStream_t s);
+
+// provenance (mesh.py:11-20)
+void launch_provenance(int64_t V, int64_t P, const int64_t* src_of, const int64_t* part_cell,
+                       const int64_t* part_index, const int64_t* fan_edge, int64_t* kind, int64_t* ref,
+                       cudaStream_t s);
+
+// shared-field hook
+void launch_eval_raw_analytic(const FieldP& f, const double* pts, int64_t n, double* raw, uint8_t* lab,
+                              cudaStream_t s);
+
+}  // namespace odc

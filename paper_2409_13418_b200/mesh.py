@@ -1,0 +1,88 @@
+"""Output mesh type and grid spec, mirroring the reference's data model.
+
+``TriangleMesh`` follows /root/reference/pkg/src/occmesh/mesh.py:11-76 (the
+extraction path's output type: vertices (V,3) f64, triangles (T,3) i64,
+provenance kind/ref) and ``GridSpec`` follows grid.py:17-91 (index
+conventions: vertex id x + y*S + z*S^2, h = (hi - lo) / R).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """Axis-aligned box divided into resolution^3 cells (grid.py:17-31)."""
+
+    lo: tuple
+    hi: tuple
+    resolution: int
+
+    def __post_init__(self):
+        object.__setattr__(self, "lo", tuple(float(v) for v in self.lo))
+        object.__setattr__(self, "hi", tuple(float(v) for v in self.hi))
+        if self.resolution < 2:
+            raise ValueError("resolution must be at least 2")
+        if any(h <= l for l, h in zip(self.lo, self.hi)):
+            raise ValueError("grid box must have positive extent")
+
+    @property
+    def shape(self):
+        return self.resolution + 1
+
+    @property
+    def cell_size(self):
+        return (np.array(self.hi) - np.array(self.lo)) / self.resolution
+
+    @property
+    def n_vertices(self):
+        return self.shape**3
+
+    @property
+    def n_cells(self):
+        return self.resolution**3
+
+
+@dataclass
+class TriangleMesh:
+    """Indexed triangle mesh with per-vertex provenance (mesh.py:11-36).
+
+    Provenance kind: 0 = cell partition point, 1 = edge point, 2 = repair
+    duplicate; ref carries (cell id, partition index) or (edge key, -1).
+    """
+
+    vertices: np.ndarray
+    triangles: np.ndarray
+    provenance_kind: np.ndarray | None = None
+    provenance_ref: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.vertices = np.asarray(self.vertices, dtype=np.float64).reshape(-1, 3)
+        self.triangles = np.asarray(self.triangles, dtype=np.int64).reshape(-1, 3)
+        if len(self.triangles):
+            if self.triangles.min() < 0 or self.triangles.max() >= len(self.vertices):
+                raise ValueError("triangle index out of range")
+            t = self.triangles
+            if ((t[:, 0] == t[:, 1]) | (t[:, 1] == t[:, 2]) | (t[:, 2] == t[:, 0])).any():
+                raise ValueError("triangle with repeated vertex index")
+
+    @property
+    def n_vertices(self):
+        return len(self.vertices)
+
+    @property
+    def n_triangles(self):
+        return len(self.triangles)
+
+    def undirected_edges(self):
+        e = np.concatenate([self.triangles[:, [0, 1]], self.triangles[:, [1, 2]], self.triangles[:, [2, 0]]])
+        return np.sort(e, axis=1)
+
+    def euler_characteristic(self):
+        if len(self.triangles) == 0:
+            return 0
+        n_edges = len(np.unique(self.undirected_edges(), axis=0))
+        return self.n_vertices - n_edges + self.n_triangles

@@ -1,0 +1,351 @@
+"""Drop-in ``contour`` for occmesh.pipeline.contour on the B200.
+
+Same signature, options, result type, stats keys, eval accounting and
+exception types as /root/reference/pkg/src/occmesh/pipeline.py:154-240; the
+whole extraction runs in libodc (hand-written sm_100a kernels) behind the
+C-ABI in include/odc.h.  Fields are lowered to device programs
+(fields.py); an unsupported field raises instead of falling back to a CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+
+from . import _lib
+from .fields import field_continuous, is_mlp, lower_program
+from .mesh import GridSpec, TriangleMesh
+
+ONE_D_MODES = ("midpoint", "linear-interp", "binary-search")
+NORMAL_MODES = ("fd-gradient", "two-d-points")
+SPLIT_MODES = ("mdc", "ic")
+
+STATUS_EXACT, STATUS_MIDPOINT_FALLBACK, STATUS_CLAMPED, STATUS_RANGE_EXHAUSTED = 0, 1, 2, 3
+STATUS_NAMES = {0: "exact", 1: "midpoint-fallback", 2: "clamped", 3: "range-exhausted"}
+
+
+class ConfigurationError(ValueError):
+    """Bad pipeline mode (pipeline.py:26-27)."""
+
+
+class InternalContractError(RuntimeError):
+    """An internal pipeline invariant was violated (dualize.py:23-24)."""
+
+
+@dataclass(frozen=True)
+class LineBudget:
+    """search.py:29-36"""
+
+    n_linear: int
+    n_binary: int
+    max_range_factor: float
+
+
+@dataclass(frozen=True)
+class SearchBudget:
+    """search.py:39-58: 15 evaluations per edge, (4+11) + 2*(3+12) per 2D point."""
+
+    iters_1d: int = 15
+    step1: LineBudget = dc_field(default_factory=lambda: LineBudget(4, 11, 0.8))
+    step2: LineBudget = dc_field(default_factory=lambda: LineBudget(3, 12, math.sqrt(2.0) / 2.0))
+
+    @property
+    def evals_per_2d_point(self):
+        return self.step1.n_linear + self.step1.n_binary + 2 * (self.step2.n_linear + self.step2.n_binary)
+
+
+@dataclass
+class ContourOptions:
+    """pipeline.py:60-78; the defaults are the full method."""
+
+    one_d: str = "binary-search"
+    normals: str = "two-d-points"
+    split: str = "ic"
+    budget: SearchBudget = dc_field(default_factory=SearchBudget)
+    qef_truncation: float = 0.1
+    fd_step_factor: float = 0.01
+    repair: bool = True
+
+    def validate(self):
+        if self.one_d not in ONE_D_MODES:
+            raise ConfigurationError(f"unknown 1D mode {self.one_d!r}")
+        if self.normals not in NORMAL_MODES:
+            raise ConfigurationError(f"unknown normal mode {self.normals!r}")
+        if self.split not in SPLIT_MODES:
+            raise ConfigurationError(f"unknown split mode {self.split!r}")
+
+
+class EvalCounter:
+    """Logical batched-evaluation accounting per category (pipeline.py:30-57).
+
+    The device fuses analytic searches per element; the counts recorded here
+    are the reference's lock-step batch counts, reported by libodc."""
+
+    def __init__(self, field):
+        self.field = field
+        self.stats = {}
+
+    def record(self, category, batches, evals):
+        entry = self.stats.setdefault(category, {"batches": 0, "evals": 0})
+        entry["batches"] += batches
+        entry["evals"] += evals
+
+    @property
+    def total_evals(self):
+        return sum(e["evals"] for e in self.stats.values())
+
+    def snapshot(self):
+        out = {k: dict(v) for k, v in self.stats.items()}
+        out["total_evals"] = self.total_evals
+        return out
+
+
+@dataclass
+class ContourResult:
+    mesh: TriangleMesh
+    raw_mesh: TriangleMesh
+    counter: EvalCounter
+    stats: dict
+
+
+_ERRORS = {
+    _lib.ODC_E_ASSERT: AssertionError,
+    _lib.ODC_E_CONTRACT: InternalContractError,
+    _lib.ODC_E_CONFIG: ConfigurationError,
+    _lib.ODC_E_VALUE: ValueError,
+    _lib.ODC_E_ARG: ValueError,
+}
+
+
+def _raise(rc, ctx):
+    msg = _lib.load().odc_last_error(ctx.handle).decode()
+    raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+class DeviceField:
+    """A field uploaded to one libodc context (program or MLP weights)."""
+
+    def __init__(self, ctx, field):
+        L = _lib.load()
+        self.ctx = ctx
+        self.handle = ctypes.c_void_p()
+        self.continuous = field_continuous(field)
+        if is_mlp(field):
+            keep = [
+                np.ascontiguousarray(field.weights[0], dtype=np.float32),
+                np.ascontiguousarray(np.stack(field.weights[1:]), dtype=np.float32),
+                np.ascontiguousarray(np.stack(field.biases), dtype=np.float32),
+                np.ascontiguousarray(field.w_head, dtype=np.float32),
+            ]
+            d = _lib.MlpDesc()
+            d.d_in, d.width, d.depth, d.n_freq = field.d_in, field.width, field.depth, field.n_freq
+            d.w0, d.w_hidden, d.biases, d.w_head = [a.ctypes.data for a in keep]
+            d.b_head, d.amplitude = float(field.b_head), float(field.amplitude)
+            d.prior_scale, d.prior_radius = float(field.prior_scale), float(field.prior_radius)
+            for i in range(3):
+                d.prior_center[i] = float(field.prior_center[i])
+            rc = L.odc_field_mlp(ctx.handle, ctypes.byref(d), ctypes.byref(self.handle))
+        else:
+            prog = lower_program(field)
+            nodes = np.ascontiguousarray(prog)
+            rc = L.odc_field_analytic(ctx.handle, nodes.ctypes.data_as(ctypes.POINTER(_lib.Node)), len(nodes),
+                                      int(self.continuous), float(getattr(field, "iso_level", 0.5)),
+                                      ctypes.byref(self.handle))
+        if rc != _lib.ODC_OK:
+            _raise(rc, ctx)
+
+    def free(self):
+        if self.handle:
+            _lib.load().odc_field_free(self.ctx.handle, self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.free()
+
+
+def make_options(options, keep_intermediates=False):
+    o = _lib.Options()
+    _lib.load().odc_default_options(ctypes.byref(o))
+    o.one_d = {"midpoint": 0, "linear-interp": 1, "binary-search": 2}[options.one_d]
+    o.normals = {"fd-gradient": 0, "two-d-points": 1}[options.normals]
+    o.split = {"mdc": 0, "ic": 1}[options.split]
+    o.repair = int(bool(options.repair))
+    b = options.budget
+    o.iters_1d = b.iters_1d
+    o.s1_lin, o.s1_bin, o.s1_range = b.step1.n_linear, b.step1.n_binary, b.step1.max_range_factor
+    o.s2_lin, o.s2_bin, o.s2_range = b.step2.n_linear, b.step2.n_binary, b.step2.max_range_factor
+    o.qef_truncation = options.qef_truncation
+    o.fd_step_factor = options.fd_step_factor
+    o.keep_intermediates = int(bool(keep_intermediates))
+    return o
+
+
+def _copy_mesh(ctx, which, st, provenance=True):
+    L = _lib.load()
+    raw = which == 1
+    V = st.raw_n_vertices if raw else st.n_vertices
+    T = st.raw_n_triangles if raw else st.n_triangles
+    v = np.empty((V, 3), dtype=np.float64)
+    t = np.empty((T, 3), dtype=np.int64)
+    kind = np.empty(V, dtype=np.int64) if provenance else None
+    ref = np.empty((V, 2), dtype=np.int64) if provenance else None
+    ptr = lambda a: a.ctypes.data if a is not None and a.size else None  # noqa: E731
+    rc = L.odc_copy_mesh(ctx.handle, which, ptr(v), ptr(t), ptr(kind), ptr(ref))
+    if rc != _lib.ODC_OK:
+        _raise(rc, ctx)
+    return TriangleMesh(v, t, provenance_kind=kind, provenance_ref=ref)
+
+
+def stats_dict(st, options, mesh_counts=True):
+    """ContourResult.stats with the reference's keys (pipeline.py:160-239)."""
+    stats = {"options": options, "warnings": []}
+    bi = int(st.boundary_inside_vertices)
+    stats["boundary_inside_vertices"] = bi
+    if bi:
+        stats["warnings"].append(
+            f"{bi} boundary grid vertices are inside; the output will have an open boundary")
+    stats["n_crossing_edges"] = int(st.n_crossing_edges)
+    stats["n_crossing_cells"] = int(st.n_crossing_cells)
+    if st.n_crossing_edges == 0:
+        stats["n_2d_points"] = 0
+        stats["open_boundary"] = False
+        return stats
+    stats["n_partitions"] = int(st.n_partitions)
+    stats["n_2d_points"] = int(st.n_2d_points)
+    if options.normals == "two-d-points":
+        stats["point2d_status_counts"] = {
+            STATUS_NAMES[c]: int(st.point2d_status_counts[c]) for c in range(4) if st.point2d_status_counts[c]}
+    stats["normal_fallbacks"] = int(st.normal_fallbacks)
+    stats["qef_rank_counts"] = {r: int(st.qef_rank_counts[r]) for r in range(4) if st.qef_rank_counts[r]}
+    stats["qef_max_residual"] = float(st.qef_max_residual)
+    stats["split_case_counts"] = {c: int(st.split_case_counts[c]) for c in range(1, 4) if st.split_case_counts[c]}
+    stats["open_boundary"] = st.skipped_boundary_edges > 0
+    stats["skipped_boundary_edges"] = int(st.skipped_boundary_edges)
+    stats["repair_added_vertices"] = int(st.repair_added_vertices)
+    return stats
+
+
+def record_counts(counter, st):
+    for c in list(st.cat_order):
+        if c < 0:
+            break
+        counter.record(_lib.CATEGORIES[c], int(st.eval_batches[c]), int(st.eval_evals[c]))
+
+
+def _grid_args(grid):
+    lo = (ctypes.c_double * 3)(*[float(v) for v in grid.lo])
+    hi = (ctypes.c_double * 3)(*[float(v) for v in grid.hi])
+    return lo, hi, int(grid.resolution)
+
+
+def contour(field, grid, options=None, counter=None, *, device=0, provenance=True, keep_intermediates=False,
+            return_context=False):
+    """Run the dual contouring pipeline on the GPU and return the repaired mesh.
+
+    Signature and result follow occmesh.pipeline.contour (pipeline.py:154);
+    ``grid`` may be this package's or the reference's GridSpec."""
+    options = options or ContourOptions()
+    options.validate()
+    counter = counter or EvalCounter(field)
+    t0 = time.perf_counter()
+    ctx = _lib.context(device)
+    L = _lib.load()
+    st = _lib.Stats()
+    lo, hi, R = _grid_args(grid)
+    if R < 2:
+        raise ValueError("resolution must be at least 2")
+    o = make_options(options, keep_intermediates)
+    with DeviceField(ctx, field) as dfield:
+        rc = L.odc_extract(ctx.handle, dfield.handle, lo, hi, R, ctypes.byref(o), ctypes.byref(st))
+        if rc != _lib.ODC_OK:
+            _raise(rc, ctx)
+    stats = stats_dict(st, options)
+    if st.n_crossing_edges == 0:
+        empty = TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64))
+        mesh = raw_mesh = empty
+    else:
+        mesh = _copy_mesh(ctx, 0, st, provenance)
+        raw_mesh = mesh if st.repair_added_vertices == 0 else _copy_mesh(ctx, 1, st, provenance)
+    record_counts(counter, st)
+    stats["wall_time_s"] = time.perf_counter() - t0
+    stats["eval_counts"] = counter.snapshot()
+    stats["device_ms"] = float(st.device_ms)
+    result = ContourResult(mesh, raw_mesh, counter, stats)
+    if return_context:
+        return result, ctx, st
+    return result
+
+
+def stage_arrays(ctx, names):
+    """Intermediate arrays of the last extraction (needs keep_intermediates)."""
+    L = _lib.load()
+    out = {}
+    for name in names:
+        which, dt = _lib.ARR[name]
+        n = ctypes.c_int64()
+        rc = L.odc_copy_array(ctx.handle, which, None, 0, ctypes.byref(n))
+        if rc != _lib.ODC_OK:
+            _raise(rc, ctx)
+        a = np.empty(n.value, dtype=dt)
+        if n.value:
+            rc = L.odc_copy_array(ctx.handle, which, a.ctypes.data, a.nbytes, ctypes.byref(n))
+            if rc != _lib.ODC_OK:
+                _raise(rc, ctx)
+        out[name] = a
+    return out
+
+
+def eval_raw(field, points, device=0):
+    """Field raw values evaluated on the device (EvalCounter.raw semantics)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    ctx = _lib.context(device)
+    out = np.empty(len(pts))
+    with DeviceField(ctx, field) as f:
+        rc = _lib.load().odc_eval_raw(ctx.handle, f.handle, pts.ctypes.data, len(pts), out.ctypes.data)
+        if rc != _lib.ODC_OK:
+            _raise(rc, ctx)
+    return out
+
+
+def eval_labels(field, points, device=0):
+    """Binary labels evaluated on the device (fields.py:35-48 semantics)."""
+    pts = np.asarray(points, dtype=np.float64)
+    squeeze = pts.ndim == 1
+    pts = np.ascontiguousarray(pts.reshape(-1, 3))
+    ctx = _lib.context(device)
+    out = np.empty(len(pts), dtype=np.uint8)
+    with DeviceField(ctx, field) as f:
+        rc = _lib.load().odc_eval_labels(ctx.handle, f.handle, pts.ctypes.data, len(pts), out.ctypes.data)
+        if rc != _lib.ODC_OK:
+            _raise(rc, ctx)
+    return out[0] if squeeze else out
+
+
+class SharedField:
+    """A field whose evaluation runs on the device, bound to one context and
+    upload -- the shared-field hook for parity oracles."""
+
+    def __init__(self, field, device=0):
+        self.field = field
+        self.ctx = _lib.Context(device)  # own workspace: never clobbers a contour() result
+        self.dev = DeviceField(self.ctx, field)
+        self.continuous = field_continuous(field)
+        self.iso_level = 0.5
+
+    def eval_raw(self, points):
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        out = np.empty(len(pts))
+        rc = _lib.load().odc_eval_raw(self.ctx.handle, self.dev.handle, pts.ctypes.data, len(pts), out.ctypes.data)
+        if rc != _lib.ODC_OK:
+            _raise(rc, self.ctx)
+        return out
+
+    def close(self):
+        self.dev.free()
