@@ -1,0 +1,361 @@
+"""ODC extraction benchmark (BASELINE.json metric: extraction ms and grid
+cells/s at 512^3, vs the CPU reference).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload mlp_512]
+    python bench.py --impl reference ...     # the CPU reference arm
+
+A step is one full extraction (occmesh.pipeline.contour semantics) of the
+workload's grid.  ``value`` = grid cells (R^3) processed by all ranks per
+second with the field already resident on the device; ``e2e`` = the same
+through the public ``contour()`` call with the field uploaded from the host
+and the mesh (+ provenance) copied back every step.  Under torchrun every
+rank extracts its own full-size grid (replicas of the workload: per-GPU work
+is fixed, scaling "weak"); the step time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = json.loads((REPO / "BASELINE.json").read_text())["metric"]
+
+
+def workload(name):
+    from paper_2409_13418_b200 import MlpField, scenes
+
+    if name.startswith("mlp_"):
+        R = int(name.split("_")[1])
+        return MlpField(seed=0, amplitude=1.0), (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), R, \
+            f"MlpField(seed=0, L=6 PE, 8x256 ReLU, He-normal bf16 weights, amplitude=1) at {R}^3 (config 3)"
+    scene, R = name.rsplit("_", 1)
+    R = int(R)
+    sc = scenes.thin_shell(R) if scene == "thin_shell" else scenes.SCENES[scene]
+    field, lo, hi = scenes.resolve(sc, R)
+    return field, lo, hi, R, f"scene {scene} at {R}^3"
+
+
+def load_peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: the oracle port (C lock-step restatement of
+# occmesh.pipeline.contour + numpy MlpField) on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_sample(field, lo, hi, R_full, full_evals, sample_R=None):
+    import oracle
+    from paper_2409_13418_b200.fields import is_mlp
+
+    cores = len(os.sched_getaffinity(0))
+    if is_mlp(field):
+        sR = sample_R or 40
+        t0 = time.perf_counter()
+        o = oracle.contour_oracle(field, lo, hi, sR)
+        dt = time.perf_counter() - t0
+        ev = o["eval_counts"]["total_evals"]
+        t_full = dt * full_evals / ev
+        sample = (f"oracle pipeline (C, 1 thread) + numpy fp32 MlpField (OpenBLAS, {cores} threads) at {sR}^3: "
+                  f"{ev} evals in {dt:.2f} s; scaled by the eval count of the {R_full}^3 run ({full_evals} evals)")
+    else:
+        sR = sample_R or R_full
+        t0 = time.perf_counter()
+        oracle.contour_oracle(field, lo, hi, sR)
+        dt = time.perf_counter() - t0
+        t_full = dt * (R_full / sR) ** 3
+        sample = f"oracle pipeline (C, 1 thread) at {sR}^3 in {dt:.2f} s" + (
+            "" if sR == R_full else f", scaled by cells to {R_full}^3")
+        cores = 1
+    return R_full**3 / t_full, t_full, cores, sample, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    field, lo, hi, R, desc = workload(args.workload)
+    from paper_2409_13418_b200.fields import is_mlp
+
+    full_evals = None
+    if is_mlp(field):
+        # eval count of the full-size run (S^3 + 15K + F4 + 46Q) from the oracle's
+        # accounting formula on a CPU-cheap estimate is not possible without the
+        # surface; use the recorded count of the device run when available.
+        full_evals = args.full_evals or estimate_mlp_evals(R)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, t_full, cores, sample, dt = cpu_sample(field, lo, hi, R, full_evals, args.cpu_sample_r)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.mean(vals))
+    line = {
+        "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": R**3 / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32+f64" if is_mlp(field) else "f64", "data": "synthetic",
+        "config": {"workload": desc, "R": R, "cells": R**3},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def estimate_mlp_evals(R):
+    """S^3 + 15K + F4 + 46Q for the config-3 field, K ~ 2.27 R^2 (measured
+    surface density of this field), Q ~ 2K."""
+    S3 = (R + 1) ** 3
+    K = int(2.27 * R * R)
+    return S3 + 15 * K + 46 * 2 * K
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_gpu(args, rank, world, dist):
+    import torch
+
+    from paper_2409_13418_b200 import GridSpec, _lib, contour
+    from paper_2409_13418_b200.fields import is_mlp
+    from paper_2409_13418_b200.pipeline import DeviceField, make_options, ContourOptions
+
+    device = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(device)
+    field, lo, hi, R, desc = workload(args.workload)
+    L = _lib.load()
+    ctx = _lib.context(device)
+    opts = make_options(ContourOptions())
+    lo_c = (ctypes.c_double * 3)(*lo)
+    hi_c = (ctypes.c_double * 3)(*hi)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # > 126 MB L2
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    dfield = DeviceField(ctx, field)
+    st = _lib.Stats()
+
+    def step():
+        rc = L.odc_extract(ctx.handle, dfield.handle, lo_c, hi_c, R, ctypes.byref(opts), ctypes.byref(st))
+        if rc:
+            raise RuntimeError(L.odc_last_error(ctx.handle).decode())
+        return st.device_ms, list(st.stage_ms), st.n_kernel_launches
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    # ---- device-resident timed region
+    dev_ms, stage, launches = [], [], 0
+    barrier()
+    with ClockSampler(device) as clocks:
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush, outside the step's event pair
+            torch.cuda.synchronize()
+            ms, sms, nl = step()
+            dev_ms.append(ms)
+            stage.append(sms)
+            launches += nl
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+    clock = clocks.summary()
+    tot_ms = float(sum(dev_ms))
+    if dist is not None:
+        t = torch.tensor([tot_ms], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_step = tot_ms / args.steps
+    value = world * R**3 / (ms_step / 1e3)
+    stats_snapshot = {k: getattr(st, k) for k in ("n_crossing_edges", "n_crossing_cells", "n_partitions",
+                                                  "n_2d_points", "n_vertices", "n_triangles",
+                                                  "repair_added_vertices")}
+    total_evals = int(sum(st.eval_evals))
+    dfield.free()
+
+    # ---- end to end through the public API (host field in, host mesh out)
+    e2e_ms = []
+    grid = GridSpec(lo, hi, R)
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        barrier()
+        t0 = time.perf_counter()
+        res = contour(field, grid)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_ms.append((t1 - t0) * 1e3)
+    e2e_step = float(np.mean(e2e_ms))
+    if dist is not None:
+        t = torch.tensor([e2e_step], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item())
+    V, T = res.mesh.n_vertices, res.mesh.n_triangles
+    if is_mlp(field):
+        h2d = (64 * 256 + 7 * 256 * 256) * 2 + 8 * 256 * 4 + 256 * 4
+    else:
+        from paper_2409_13418_b200.fields import lower_program
+
+        h2d = 136 * len(lower_program(field))
+    d2h = V * 24 + T * 12 + V * 24  # vertices f64, triangles i32 (widened on the host), provenance
+    if res.raw_mesh is not res.mesh:
+        d2h += res.raw_mesh.n_vertices * 48 + T * 12
+
+    # ---- roofline of the dominant kernel (grid labels)
+    peaks, peak_kind = load_peaks()
+    k1_ms = float(np.mean([s[7] for s in stage]))
+    S3 = (R + 1) ** 3
+    if is_mlp(field):
+        flops = float(field.flops_per_eval) * S3
+        achieved = flops / (k1_ms / 1e3) / 1e12
+        peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "kernel": "grid occupancy MLP (labels of all S^3 vertices)",
+                "algorithmic": f"937984 FLOP/eval x {S3} evals per launch"}
+    else:
+        W = (R + 1 + 31) // 32
+        nbytes = (R + 1) ** 2 * W * 4
+        achieved = nbytes / (k1_ms / 1e3) / 1e9
+        peak = float(peaks["hbm_gbs"])
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "kernel": "k_labels_analytic (fp64 field program per vertex, bit-packed labels)",
+                "algorithmic": f"{nbytes} label-bitmap bytes written per launch"}
+    roof["peak_source"] = f"{peak_kind} (MEASURED_PEAKS.json)" if peak_kind == "measured" else "fallback"
+    roof["kernel_ms"] = k1_ms
+    prof = REPO / "profiles" / "ncu_traffic.json"
+    roof["traffic"] = None
+    if prof.exists():
+        try:
+            roof["traffic"] = json.loads(prof.read_text()).get(args.workload)
+        except Exception:
+            pass
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, t_full, cores, sample, dt = cpu_sample(field, lo, hi, R, total_evals, args.cpu_sample_r)
+        cpu = {"value": v, "unit": "cells/s", "cores": cores, "kind": "port", "sample": sample}
+    stage_names = ["labels", "active_sets", "points_1d", "normals_2d", "cells_qef", "polygonize", "repair",
+                   "labels_kernel"]
+    line = {
+        "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16+f64" if is_mlp(field) else "f64", "data": "synthetic",
+        "config": {"workload": desc, "R": R, "cells": R**3, "parallelism": f"replicas x{world}",
+                   "l2": "flushed (512 MiB write) before every step, outside its CUDA-event pair",
+                   "evals_per_step": total_evals},
+        "e2e": {"value": world * R**3 / (e2e_step / 1e3), "unit": "cells/s", "ms_per_step": e2e_step,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "api": "paper_2409_13418_b200.contour(field, GridSpec) -> TriangleMesh (numpy)"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "clocks": clock,
+        "stage_ms": {n: float(np.mean([s[i] for s in stage])) for i, n in enumerate(stage_names)},
+        "wall_s_timed_region": t_wall,
+        "mesh": stats_snapshot,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="mlp_512")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-r", type=int, default=None)
+    ap.add_argument("--full-evals", type=int, default=None)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        backend = "nccl" if args.impl == "b200" else "gloo"
+        tdist.init_process_group(backend=backend)
+        dist = tdist
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_gpu(args, rank, world, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

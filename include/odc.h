@@ -133,6 +133,10 @@ typedef struct {
   int32_t cat_order[ODC_N_CAT]; /* first-record order, -1 terminated */
   int32_t n_kernel_launches;
   float device_ms; /* CUDA-event time of the whole extraction on its stream */
+  /* CUDA-event time per stage: 0 labels, 1 active sets, 2 1D points + face
+   * probes, 3 normals (2D points / fd), 4 cells + QEF, 5 polygonize, 6 repair,
+   * 7 the grid-label evaluation kernel alone (the dominant kernel). */
+  float stage_ms[8];
 } odc_stats;
 
 int odc_version(void);

@@ -63,7 +63,7 @@ class Stats(ctypes.Structure):
         ("repair_added_vertices", ctypes.c_int64), ("repair_passes", ctypes.c_int64),
         ("eval_batches", ctypes.c_int64 * ODC_N_CAT), ("eval_evals", ctypes.c_int64 * ODC_N_CAT),
         ("cat_order", ctypes.c_int32 * ODC_N_CAT), ("n_kernel_launches", ctypes.c_int32),
-        ("device_ms", ctypes.c_float),
+        ("device_ms", ctypes.c_float), ("stage_ms", ctypes.c_float * 8),
     ]
 
 

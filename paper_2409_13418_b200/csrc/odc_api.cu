@@ -101,6 +101,7 @@ struct odc_ctx {
   int device = 0;
   cudaStream_t own = nullptr, stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evs[9] = {};  // stage boundaries
   Arena arena;
   CellTabEntry* table = nullptr;
   unsigned long long* h_pinned = nullptr;  // small readback buffer
@@ -262,16 +263,24 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(DevStats), s));
   CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), s));
 
+  int marks = 0;
+  auto mark = [&](int i) {
+    CUDA_TRY(cudaEventRecord(c->evs[i], s));
+    marks = i + 1;
+  };
   // ---- K1: sample_labels (grid.py:109-126)
+  mark(0);
   c->L = need(c->arena.get<uint32_t>(g.NW));
   if (!mlp) {
     launch_labels_analytic(g, fp, c->L, s);
     check_launch(c);
+    mark(8);
   } else {
     uint8_t* bytes = need(c->arena.get<uint8_t>(g.S3));
     PointSrc src{nullptr, g, 0};
     mlp_eval(f->mlp, src, g.S3, bytes, nullptr, s);
     check_launch(c);
+    mark(8);
     launch_pack_labels(g, bytes, c->L, s);
     check_launch(c);
   }
@@ -279,6 +288,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   st->n_grid_vertices = g.S3;
 
   // ---- K2: extract_active (grid.py:171-296)
+  mark(1);
   const int64_t nt = active_tiles(g);
   c->rec = need(c->arena.get<WordRec>(g.NW));
   uint32_t* tiles = need(c->arena.get<uint32_t>(5 * nt));
@@ -327,6 +337,16 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     st->device_ms = ms;
+    // stage i spans mark i -> mark i+1 (or the end event)
+    for (int i = 0; i < 7; i++) {
+      float x = 0.f;
+      if (i + 1 < marks) cudaEventElapsedTime(&x, c->evs[i], c->evs[i + 1]);
+      else if (i < marks) cudaEventElapsedTime(&x, c->evs[i], c->ev1);
+      st->stage_ms[i] = x;
+    }
+    float k1 = 0.f;
+    cudaEventElapsedTime(&k1, c->evs[0], c->evs[8]);
+    st->stage_ms[7] = k1;
     st->n_kernel_launches = c->launches;
   };
 
@@ -341,6 +361,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   }
 
   // ---- K3: 1D points (pipeline.py:94-123, search.py:71-94)
+  mark(2);
   c->t1d = need(c->arena.get<double>(K));
   c->pos1d = need(c->arena.get<double>(3 * K));
   c->v_in = c->keep ? need(c->arena.get<int64_t>(K)) : nullptr;
@@ -397,6 +418,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   st->n_face_center_probes = F4;
 
   // ---- normals: 2D points (search.py:194-322) or fd gradient (pipeline.py:126-151)
+  mark(3);
   double* edge_normals = nullptr;
   c->inst_edges = c->keep ? need(c->arena.get<int64_t>(2 * Q)) : nullptr;
   c->s2 = Stage2D{};
@@ -450,6 +472,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   }
 
   // ---- K6: partitions + plane samples + QEF (dualize.py:194-444)
+  mark(4);
   uint16_t* cfg = need(c->arena.get<uint16_t>(C));
   uint32_t* ncyc = need(c->arena.get<uint32_t>(C));
   uint32_t* nsamp = need(c->arena.get<uint32_t>(C));
@@ -485,6 +508,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   c->cells = co;
 
   // ---- K7: build_mesh (polygonize.py:110-217)
+  mark(5);
   int4* pid4 = need(c->arena.get<int4>(K));
   c->kase = need(c->arena.get<uint8_t>(K));
   uint32_t* ntri = need(c->arena.get<uint32_t>(K));
@@ -547,6 +571,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   st->raw_n_triangles = T;
 
   // ---- K8: repair_nonmanifold (polygonize.py:253-374), up to 4 passes
+  mark(6);
   c->verts1 = verts;
   c->tris1 = tris;
   int64_t curV = V0;
@@ -596,6 +621,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     c->tris1 = cur;
     st->repair_passes = passes;
   }
+  mark(7);
   c->V1 = curV;
   st->n_vertices = curV;
   st->n_triangles = T;
@@ -641,6 +667,11 @@ int odc_create(int device, odc_ctx** out) {
     return ODC_E_CUDA;
   }
   c->stream = c->own;
+  for (auto& e : c->evs)
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      delete c;
+      return ODC_E_CUDA;
+    }
   std::vector<CellTabEntry> tab(kTableSize);
   if (build_cell_table(tab.data()) != 0) {
     delete c;
@@ -663,6 +694,8 @@ void odc_destroy(odc_ctx* c) {
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (auto& e : c->evs)
+    if (e) cudaEventDestroy(e);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }

@@ -42,8 +42,17 @@ def oracle_run(field, lo, hi, R, options=None):
     return oracle.contour_oracle(field, lo, hi, R, options=options)
 
 
-def compare(res, arrs, o, exact_positions=True):
+def _close(a, b, atol):
+    a, b = np.asarray(a), np.asarray(b).reshape(np.shape(a))
+    return a.shape == b.shape and (a.size == 0 or np.abs(a - b).max() <= atol)
+
+
+def compare(res, arrs, o, exact_positions=True, tol=None):
+    """Discrete outputs bit-exact; with ``tol`` (in units of h) continuous
+    outputs are compared with that tolerance instead of bit-for-bit (used
+    where raw values come from the device exp(), which is not glibc's)."""
     h = float(np.min(o["h"]))
+    eq = (lambda a, b: _close(a, b, tol * h)) if tol is not None else (lambda a, b: np.array_equal(a, np.reshape(b, np.shape(a))))
     assert np.array_equal(arrs["labels"], o["labels"])
     for k in ("edge_key", "v_in", "face_key", "face_n_crossing", "cells"):
         assert np.array_equal(arrs[k], o[k]), k
@@ -51,19 +60,20 @@ def compare(res, arrs, o, exact_positions=True):
         assert res.mesh.n_triangles == 0
         return
     assert np.array_equal(arrs["instance_edges"].reshape(-1, 2), o["instance_edges"])
-    assert np.array_equal(arrs["t1d"], o["t1d"])
-    assert np.array_equal(arrs["pos1d"].reshape(-1, 3), o["pos1d"])
-    assert np.array_equal(arrs["pos2"].reshape(-1, 2), o["pos2"])
+    assert eq(arrs["t1d"], o["t1d"]) if tol is None else _close(arrs["t1d"], o["t1d"], tol)
+    assert eq(arrs["pos1d"].reshape(-1, 3), o["pos1d"])
+    assert eq(arrs["pos2"].reshape(-1, 2), o["pos2"])
     assert np.array_equal(arrs["status"], o["status"])
     assert np.array_equal(arrs["part_cell"], o["part_cell"])
     assert np.array_equal(arrs["part_index"], o["part_index"])
     assert np.array_equal(np.concatenate([[0], np.cumsum(arrs["cyc_len"])]), o["cyc_off"])
     assert np.array_equal(arrs["cyc_edges"], o["cyc_edges"])
     assert np.array_equal(arrs["cyc_insts"], o["cyc_insts"])
-    assert np.array_equal(arrs["normals"].reshape(-1, 3), o["normals"])
+    assert eq(arrs["normals"].reshape(-1, 3), o["normals"]) if tol is None else _close(
+        arrs["normals"].reshape(-1, 3), o["normals"], tol)
     qp = arrs["qef_pos"].reshape(-1, 3)
     assert np.abs(qp - o["qef_pos"]).max() <= 1e-4 * h
-    if exact_positions:
+    if exact_positions and tol is None:
         assert np.array_equal(qp, o["qef_pos"])
     assert np.array_equal(arrs["qef_rank"], o["qef_rank"])
     assert np.array_equal(arrs["split_cases"], o["split_cases"])
@@ -116,7 +126,9 @@ def test_gpu_ablation_modes(opts):
         field, lo, hi, R = field_of(tag)
         res, arrs = gpu_run(field, lo, hi, R, opts)
         o = oracle_run(field, lo, hi, R, opts)
-        compare(res, arrs, o)
+        # linear-interp on a smoothed field interpolates exp()-based raw values
+        smooth_raw = opts.one_d == "linear-interp" and tag.startswith("smooth")
+        compare(res, arrs, o, tol=1e-9 if smooth_raw else None)
 
 
 def test_gpu_fd_gradient_normals():
