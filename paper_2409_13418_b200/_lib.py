@@ -70,7 +70,7 @@ class Stats(ctypes.Structure):
 EXPORTS = (
     "odc_version", "odc_create", "odc_destroy", "odc_last_error", "odc_set_stream", "odc_field_analytic",
     "odc_field_mlp", "odc_field_free", "odc_default_options", "odc_extract", "odc_copy_mesh", "odc_mesh_device",
-    "odc_copy_array", "odc_eval_raw", "odc_eval_labels",
+    "odc_copy_array", "odc_eval_raw", "odc_eval_labels", "odc_set_param",
 )
 
 _lib = None
@@ -95,6 +95,7 @@ def load():
         L.odc_last_error.argtypes = [vp]
         L.odc_last_error.restype = ctypes.c_char_p
         L.odc_set_stream.argtypes = [vp, vp]
+        L.odc_set_param.argtypes = [vp, ctypes.c_char_p, i64]
         L.odc_field_analytic.argtypes = [vp, P(Node), i32, i32, dbl, P(vp)]
         L.odc_field_mlp.argtypes = [vp, P(MlpDesc), P(vp)]
         L.odc_field_free.argtypes = [vp, vp]

@@ -92,6 +92,7 @@ struct odc_field {
   double iso = 0.5;
   // MLP
   uint16_t* w_packed = nullptr;
+  uint16_t* w_tc = nullptr;
   float* bias = nullptr;
   float* w_head = nullptr;
   MlpDev mlp{};
@@ -107,6 +108,7 @@ struct odc_ctx {
   unsigned long long* h_pinned = nullptr;  // small readback buffer
   std::string err;
   int launches = 0;
+  int mlp_impl = 0;  // odc_set_param("mlp_impl"): 0 tcgen05, 1 SIMT reference
   // last extraction
   bool valid = false;
   GridP g{};
@@ -174,7 +176,9 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
     launch_eval_raw_analytic(fp, pts, n, raw, lab, c->stream);
   } else {
     PointSrc src{pts, GridP{}, 0};
-    mlp_eval(f->mlp, src, n, lab, raw, c->stream);
+    MlpDev md = f->mlp;
+    md.impl = c->mlp_impl;
+    mlp_eval(md, src, n, lab, raw, c->stream);
   }
   check_launch(c);
 }
@@ -278,7 +282,9 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   } else {
     uint8_t* bytes = need(c->arena.get<uint8_t>(g.S3));
     PointSrc src{nullptr, g, 0};
-    mlp_eval(f->mlp, src, g.S3, bytes, nullptr, s);
+    MlpDev md = f->mlp;
+    md.impl = c->mlp_impl;
+    mlp_eval(md, src, g.S3, bytes, nullptr, s);
     check_launch(c);
     mark(8);
     launch_pack_labels(g, bytes, c->L, s);
@@ -702,6 +708,16 @@ void odc_destroy(odc_ctx* c) {
 
 const char* odc_last_error(const odc_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+int odc_set_param(odc_ctx* c, const char* name, int64_t value) {
+  if (!c || !name) return ODC_E_ARG;
+  if (std::strcmp(name, "mlp_impl") == 0 && (value == 0 || value == 1)) {
+    c->mlp_impl = (int)value;
+    return ODC_OK;
+  }
+  c->err = std::string("unknown parameter ") + name;
+  return ODC_E_ARG;
+}
+
 int odc_set_stream(odc_ctx* c, void* stream) {
   if (!c) return ODC_E_ARG;
   c->stream = stream ? (cudaStream_t)stream : c->own;
@@ -759,17 +775,23 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
   f->iso = 0.5;
   const size_t ne = mlp_packed_weight_elems();
   std::vector<uint16_t> packed(ne);
+  const size_t nt = mlp_tc_weight_elems();
+  std::vector<uint16_t> packed_tc(nt);
+  mlp_pack_weights_tc(d->w0, d->d_in, d->w_hidden, packed_tc.data());
   mlp_pack_weights(d->w0, d->d_in, d->w_hidden, packed.data());
-  if (cudaMalloc(&f->w_packed, ne * 2) != cudaSuccess || cudaMalloc(&f->bias, 8 * 256 * 4) != cudaSuccess ||
+  if (cudaMalloc(&f->w_packed, ne * 2) != cudaSuccess || cudaMalloc(&f->w_tc, nt * 2) != cudaSuccess ||
+      cudaMalloc(&f->bias, 8 * 256 * 4) != cudaSuccess ||
       cudaMalloc(&f->w_head, 256 * 4) != cudaSuccess) {
     c->err = "field upload failed";
     delete f;
     return ODC_E_NOMEM;
   }
   cudaMemcpy(f->w_packed, packed.data(), ne * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(f->w_tc, packed_tc.data(), nt * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(f->bias, d->biases, 8 * 256 * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(f->w_head, d->w_head, 256 * 4, cudaMemcpyHostToDevice);
   f->mlp.w_packed = f->w_packed;
+  f->mlp.w_tc = f->w_tc;
   f->mlp.bias = f->bias;
   f->mlp.w_head = f->w_head;
   f->mlp.b_head = (float)d->b_head;
@@ -786,6 +808,7 @@ void odc_field_free(odc_ctx* c, odc_field* f) {
   if (c) cudaStreamSynchronize(c->stream);
   cudaFree(f->nodes);
   cudaFree(f->w_packed);
+  cudaFree(f->w_tc);
   cudaFree(f->bias);
   cudaFree(f->w_head);
   delete f;

@@ -8,6 +8,7 @@
 #include <cstring>
 
 #include "odc_mlp.h"
+#include "odc_mlp_tc.cuh"
 
 namespace odc {
 
@@ -116,13 +117,274 @@ __global__ void __launch_bounds__(kWidth) k_mlp_simt(MlpDev m, PointSrc src, int
   }
 }
 
+// ===========================================================================
+// tcgen05 / TMEM evaluator (see odc_mlp_tc.cuh for the structure)
+// ===========================================================================
+size_t mlp_tc_weight_elems() { return (size_t)tc::kChunksPerPair * 128 * 64; }
+
+// chunk order = MMA consumption order: for l: for nh: for kc.  Each chunk is
+// the smem image of B rows n = 128 nh + r (K-major), k = 64 kc + j, swizzled.
+void mlp_pack_weights_tc(const float* w0, int d_in, const float* w_hidden, uint16_t* out) {
+  size_t ci = 0;
+  for (int l = 0; l < kDepth; l++) {
+    const int nkc = l == 0 ? 1 : 4;
+    for (int nh = 0; nh < 2; nh++)
+      for (int kc = 0; kc < nkc; kc++, ci++) {
+        uint16_t* img = out + ci * 128 * 64;
+        for (int r = 0; r < 128; r++)
+          for (int j = 0; j < 64; j++) {
+            const int n = 128 * nh + r, k = 64 * kc + j;
+            float v;
+            if (l == 0) v = k < d_in ? w0[(size_t)k * kWidth + n] : 0.f;
+            else v = w_hidden[((size_t)(l - 1) * kWidth + k) * kWidth + n];
+            const size_t byte = (size_t)((r >> 3) * 1024 + (r & 7) * 128 + (((j >> 3) ^ (r & 7)) << 4) + (j & 7) * 2);
+            img[byte / 2] = f2bf(v);
+          }
+      }
+  }
+}
+
+__device__ __forceinline__ void write_pe_row(const PointSrc& src, int64_t n, int64_t p, uint32_t a_atom0, int r) {
+  float f[64];
+  if (p < n) {
+    double pt[3];
+    point_of(src, p, pt);
+#pragma unroll
+    for (int j = 0; j < 64; j++) f[j] = pe_feature(pt, j);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 64; j++) f[j] = 0.f;
+  }
+#pragma unroll
+  for (int c = 0; c < 8; c++)
+    tc::st_shared_v4(a_atom0 + tc::sw128_off(r, c), tc::pack_bf16x2(f[8 * c], f[8 * c + 1]),
+                     tc::pack_bf16x2(f[8 * c + 2], f[8 * c + 3]), tc::pack_bf16x2(f[8 * c + 4], f[8 * c + 5]),
+                     tc::pack_bf16x2(f[8 * c + 6], f[8 * c + 7]));
+}
+
+__device__ __forceinline__ float relu_bias(uint32_t bits, float b) {
+  const float v = __uint_as_float(bits) + b;
+  return v > 0.f ? v : 0.f;
+}
+
+__global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc src, int64_t n,
+                                                           uint8_t* __restrict__ labels, double* __restrict__ raw) {
+  using namespace tc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* A0 = smem;
+  uint8_t* Wst = smem + 2 * kTileABytes;
+  uint64_t* bars = (uint64_t*)(Wst + kStages * kChunkBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* acc_full = bars + 2 * kStages;
+  uint64_t* a_ready = acc_full + 2;
+  uint32_t* tmem_slot = (uint32_t*)(a_ready + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t npairs = (n + 255) / 256;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&acc_full[0], 1);
+    mbar_init(&acc_full[1], 1);
+    mbar_init(&a_ready[0], 256);
+    mbar_init(&a_ready[1], 256);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- weight producer
+      uint32_t g = 0;
+      for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x)
+        for (int i = 0; i < kChunksPerPair; i++, g++) {
+          const uint32_t s = g % kStages, ph = (g / kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], kChunkBytes);
+          bulk_g2s(Wst + s * kChunkBytes, m.w_tc + (size_t)i * 128 * 64, kChunkBytes, &full[s]);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      uint32_t g = 0, ra0 = 0, ra1 = 0;
+      const uint32_t a_base[2] = {smem_u32(A0), smem_u32(A0 + kTileABytes)};
+      for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
+        for (int l = 0; l < kDepth; l++) {
+          const int nkc = l == 0 ? 1 : 4;
+          for (int nh = 0; nh < 2; nh++) {
+            for (int kc = 0; kc < nkc; kc++, g++) {
+              if (nh == 0 && kc == 0) {
+                mbar_wait(&a_ready[0], ra0 & 1);
+                ra0++;
+                tc_fence_after();
+              }
+              if (l > 0 && nh == 0 && kc == 2) {
+                mbar_wait(&a_ready[1], ra1 & 1);
+                ra1++;
+                tc_fence_after();
+              }
+              const uint32_t s = g % kStages, ph = (g / kStages) & 1;
+              mbar_wait(&full[s], ph);
+              tc_fence_after();
+              const uint32_t b_base = smem_u32(Wst + s * kChunkBytes);
+#pragma unroll
+              for (int t = 0; t < 2; t++) {
+                const uint32_t d = tmem + t * 256 + nh * 128;
+#pragma unroll
+                for (int ks = 0; ks < 4; ks++)
+                  umma_bf16(d, sw128_desc(a_base[t] + kc * 16384 + ks * 32), sw128_desc(b_base + ks * 32),
+                            (kc | ks) != 0);
+              }
+              umma_commit(&empty[s]);
+            }
+            umma_commit(&acc_full[nh]);
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---- epilogue: 2 tiles x 128 rows
+    const int et = threadIdx.x - 128;
+    const int t = et >> 7;
+    const int q = warp & 3;
+    const int r = 32 * q + lane;
+    const uint32_t a_t = smem_u32(A0 + t * kTileABytes);
+    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + t * 256;
+    uint32_t af0 = 0, af1 = 0;
+    if ((int64_t)blockIdx.x < npairs) {
+      write_pe_row(src, n, (int64_t)blockIdx.x * 256 + t * 128 + r, a_t, r);
+      fence_proxy_async();
+      mbar_arrive(&a_ready[0]);
+    }
+    for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
+      float dot = 0.f;
+      for (int l = 0; l < kDepth; l++) {
+        const float* bl = m.bias + l * kWidth;
+        mbar_wait(&acc_full[0], af0 & 1);
+        af0++;
+        tc_fence_after();
+        uint32_t pk[64];
+        if (l < kDepth - 1) {
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            uint32_t v[32];
+            ODC_TMEM_LD32(trow + 32 * i, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+              pk[16 * i + j] = pack_bf16x2(relu_bias(v[2 * j], __ldg(bl + 32 * i + 2 * j)),
+                                           relu_bias(v[2 * j + 1], __ldg(bl + 32 * i + 2 * j + 1)));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            uint32_t v[32];
+            ODC_TMEM_LD32(trow + 32 * i, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; j++) dot = fmaf(relu_bias(v[j], __ldg(bl + 32 * i + j)), __ldg(m.w_head + 32 * i + j), dot);
+          }
+        }
+        mbar_wait(&acc_full[1], af1 & 1);
+        af1++;
+        tc_fence_after();
+        if (l < kDepth - 1) {
+          // half 0 -> A columns 0..127 (K-atoms 0, 1); the layer's MMAs are done
+#pragma unroll
+          for (int c = 0; c < 16; c++)
+            st_shared_v4(a_t + (c >> 3) * 16384 + sw128_off(r, c & 7), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                         pk[4 * c + 3]);
+          fence_proxy_async();
+          mbar_arrive(&a_ready[0]);
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            uint32_t v[32];
+            ODC_TMEM_LD32(trow + 128 + 32 * i, v);
+            tmem_ld_wait();
+            uint32_t w[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+              w[j] = pack_bf16x2(relu_bias(v[2 * j], __ldg(bl + 128 + 32 * i + 2 * j)),
+                                 relu_bias(v[2 * j + 1], __ldg(bl + 128 + 32 * i + 2 * j + 1)));
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+              const int cc = 4 * i + c;  // chunk within columns 128..255
+              st_shared_v4(a_t + (2 + (cc >> 3)) * 16384 + sw128_off(r, cc & 7), w[4 * c], w[4 * c + 1],
+                           w[4 * c + 2], w[4 * c + 3]);
+            }
+          }
+          fence_proxy_async();
+          mbar_arrive(&a_ready[1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            uint32_t v[32];
+            ODC_TMEM_LD32(trow + 128 + 32 * i, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; j++)
+              dot = fmaf(relu_bias(v[j], __ldg(bl + 128 + 32 * i + j)), __ldg(m.w_head + 128 + 32 * i + j), dot);
+          }
+        }
+      }
+      const int64_t p = pair * 256 + t * 128 + r;
+      if (p < n) {
+        const double mlp = (double)(dot + m.b_head);
+        double pt[3];
+        point_of(src, p, pt);
+        const double d[3] = {pt[0] - m.prior_center[0], pt[1] - m.prior_center[1], pt[2] - m.prior_center[2]};
+        const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+        const double logit = m.amplitude * mlp - m.prior_scale * (dist - m.prior_radius);
+        const double rv = 1.0 / (1.0 + exp(-logit));
+        labels[p] = rv > 0.5 ? 1 : 0;
+        if (raw) raw[p] = rv;
+      }
+      const int64_t next = pair + gridDim.x;
+      if (next < npairs) {
+        write_pe_row(src, n, next * 256 + t * 128 + r, a_t, r);
+        fence_proxy_async();
+        mbar_arrive(&a_ready[0]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+static int g_num_sms = 0;
+
 int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s) {
   if (n <= 0) return 0;
-  const int64_t blocks = (n + kPts - 1) / kPts;
-  k_mlp_simt<<<(unsigned)blocks, kWidth, 0, s>>>(m, src, n, labels, raw);
+  if (m.impl == 1 || m.w_tc == nullptr) {
+    const int64_t blocks = (n + kPts - 1) / kPts;
+    k_mlp_simt<<<(unsigned)blocks, kWidth, 0, s>>>(m, src, n, labels, raw);
+    return 0;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    attr = true;
+  }
+  const int64_t npairs = (n + 255) / 256;
+  const int64_t grid = npairs < g_num_sms ? npairs : g_num_sms;
+  k_mlp_tc<<<(unsigned)grid, tc::kThreads, tc::kSmemBytes, s>>>(m, src, n, labels, raw);
   return 0;
 }
 
-const char* mlp_kernel_name() { return "k_mlp_simt"; }
+const char* mlp_kernel_name() { return "k_mlp_tc"; }
 
 }  // namespace odc

@@ -18,8 +18,9 @@
 namespace odc {
 
 struct MlpDev {
-  // tensor-core layout (UMMA canonical K-major, see odc_mlp.cu)
-  const uint16_t* w_packed;  // 8 layers of bf16 weights, each N=256 x K (K=64 for layer 0, 256 after)
+  const uint16_t* w_packed;  // row-major bf16 W[k][n] per layer (layer 0 padded to K=64): SIMT evaluator
+  const uint16_t* w_tc;      // 58 chunks of 128x64 bf16 in the UMMA SWIZZLE_128B smem image (odc_mlp_tc.cuh)
+  int impl;                  // 0 = tcgen05 (default), 1 = SIMT reference evaluator
   const float* bias;         // (8, 256)
   const float* w_head;       // (256)
   float b_head;
@@ -35,6 +36,8 @@ struct PointSrc {
 };
 
 size_t mlp_packed_weight_elems();
+size_t mlp_tc_weight_elems();
+void mlp_pack_weights_tc(const float* w0, int d_in, const float* w_hidden, uint16_t* out);
 // host: pack float32 weights (already bf16-representable) into the device layout
 void mlp_pack_weights(const float* w0, int d_in, const float* w_hidden, uint16_t* out);
 

@@ -1,0 +1,65 @@
+"""tcgen05 MLP evaluator (K9) against the SIMT reference evaluator (same bf16
+operands, fp32 accumulation on CUDA cores) and against numpy fp32."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2409_13418_b200 import MlpField, _lib
+from paper_2409_13418_b200.pipeline import DeviceField
+
+pytestmark = pytest.mark.gpu
+
+
+def device_raw(field, pts, impl):
+    ctx = _lib.Context(0)
+    L = _lib.load()
+    assert L.odc_set_param(ctx.handle, b"mlp_impl", impl) == 0
+    pts = np.ascontiguousarray(pts, dtype=np.float64)
+    out = np.empty(len(pts))
+    with DeviceField(ctx, field) as f:
+        rc = L.odc_eval_raw(ctx.handle, f.handle, pts.ctypes.data, len(pts), out.ctypes.data)
+        assert rc == 0, L.odc_last_error(ctx.handle)
+    return out
+
+
+def logit(raw):
+    raw = np.clip(raw, 1e-300, 1 - 1e-16)
+    return np.log(raw / (1 - raw))
+
+
+@pytest.mark.parametrize("n", [1, 255, 256, 1000, 70001])
+def test_tc_matches_simt(n):
+    field = MlpField(seed=0, amplitude=1.0)
+    rng = np.random.default_rng(n)
+    pts = rng.uniform(0, 1, size=(n, 3))
+    a = device_raw(field, pts, 0)
+    b = device_raw(field, pts, 1)
+    la, lb = logit(a), logit(b)
+    ok = np.isfinite(la) & np.isfinite(lb)
+    # only the fp32 summation order differs
+    assert np.abs(la - lb)[ok].max() < 2e-2
+    sure = np.abs(lb) > 0.05
+    assert np.array_equal(a[sure] > 0.5, b[sure] > 0.5)
+
+
+def test_tc_vs_numpy_fp32_label_agreement():
+    field = MlpField(seed=0, amplitude=1.0)
+    rng = np.random.default_rng(7)
+    pts = rng.uniform(0.1, 0.9, size=(20000, 3))
+    a = device_raw(field, pts, 0) > 0.5
+    c = oracle.mlp_raw_numpy(field, pts) > 0.5
+    assert np.mean(a == c) > 0.995
+
+
+def test_tc_batch_invariance():
+    field = MlpField(seed=3, amplitude=2.0)
+    rng = np.random.default_rng(1)
+    pts = rng.uniform(0, 1, size=(5000, 3))
+    full = device_raw(field, pts, 0)
+    part = np.concatenate([device_raw(field, pts[:1234], 0), device_raw(field, pts[1234:], 0)])
+    assert np.array_equal(full, part)
+    rev = device_raw(field, pts[::-1].copy(), 0)[::-1]
+    assert np.array_equal(full, rev)
