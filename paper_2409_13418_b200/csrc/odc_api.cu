@@ -792,6 +792,9 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
   cudaMemcpy(f->w_head, d->w_head, 256 * 4, cudaMemcpyHostToDevice);
   f->mlp.w_packed = f->w_packed;
   f->mlp.w_tc = f->w_tc;
+  f->mlp.has_bias = 0;
+  for (int i = 0; i < 8 * 256; i++)
+    if (d->biases[i] != 0.f) f->mlp.has_bias = 1;
   f->mlp.bias = f->bias;
   f->mlp.w_head = f->w_head;
   f->mlp.b_head = (float)d->b_head;

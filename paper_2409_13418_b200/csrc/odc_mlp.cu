@@ -144,29 +144,59 @@ void mlp_pack_weights_tc(const float* w0, int d_in, const float* w_hidden, uint1
   }
 }
 
-__device__ __forceinline__ void write_pe_row(const PointSrc& src, int64_t n, int64_t p, uint32_t a_atom0, int r) {
-  float f[64];
-  if (p < n) {
-    double pt[3];
-    point_of(src, p, pt);
+// Positional encoding of point p packed to 32 bf16x2 words (features 0..63,
+// 39..63 zero); computed ahead of time, stored when the A tile is free.
+__device__ __forceinline__ void pe_row_packed(const PointSrc& src, int64_t n, int64_t p, uint32_t (&pk)[32]) {
+  double pt[3] = {0.5, 0.5, 0.5};
+  const bool ok = p < n;
+  if (ok) point_of(src, p, pt);
 #pragma unroll
-    for (int j = 0; j < 64; j++) f[j] = pe_feature(pt, j);
-  } else {
-#pragma unroll
-    for (int j = 0; j < 64; j++) f[j] = 0.f;
+  for (int c = 0; c < 32; c++) {
+    const float lo = ok ? pe_feature(pt, 2 * c) : 0.f;
+    const float hi = ok ? pe_feature(pt, 2 * c + 1) : 0.f;
+    pk[c] = tc::pack_bf16x2(lo, hi);
   }
+}
+__device__ __forceinline__ void store_pe_row(const uint32_t (&pk)[32], uint32_t a_atom0, int r) {
 #pragma unroll
   for (int c = 0; c < 8; c++)
-    tc::st_shared_v4(a_atom0 + tc::sw128_off(r, c), tc::pack_bf16x2(f[8 * c], f[8 * c + 1]),
-                     tc::pack_bf16x2(f[8 * c + 2], f[8 * c + 3]), tc::pack_bf16x2(f[8 * c + 4], f[8 * c + 5]),
-                     tc::pack_bf16x2(f[8 * c + 6], f[8 * c + 7]));
+    tc::st_shared_v4(a_atom0 + tc::sw128_off(r, c), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
 }
 
-__device__ __forceinline__ float relu_bias(uint32_t bits, float b) {
-  const float v = __uint_as_float(bits) + b;
-  return v > 0.f ? v : 0.f;
+// relu(a + b), relu(c + d) -> bf16x2 in one conversion
+__device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
 }
 
+// 32 accumulator columns -> 16 packed bf16x2 words of relu(acc + bias)
+template <bool kBias>
+__device__ __forceinline__ void relu_pack32(const uint32_t (&v)[32], const float* __restrict__ sb, uint32_t* out) {
+#pragma unroll
+  for (int j = 0; j < 16; j++) {
+    float a = __uint_as_float(v[2 * j]), b = __uint_as_float(v[2 * j + 1]);
+    if (kBias) {
+      a += sb[2 * j];
+      b += sb[2 * j + 1];
+    }
+    out[j] = relu_pack(a, b);
+  }
+}
+template <bool kBias>
+__device__ __forceinline__ float head32(const uint32_t (&v)[32], const float* __restrict__ sb,
+                                        const float* __restrict__ sw, float dot) {
+#pragma unroll
+  for (int j = 0; j < 32; j++) {
+    float a = __uint_as_float(v[j]);
+    if (kBias) a += sb[j];
+    a = a > 0.f ? a : 0.f;
+    dot = fmaf(a, sw[j], dot);
+  }
+  return dot;
+}
+
+template <bool kBias>
 __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc src, int64_t n,
                                                            uint8_t* __restrict__ labels, double* __restrict__ raw) {
   using namespace tc;
@@ -180,6 +210,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
   uint64_t* acc_full = bars + 2 * kStages;
   uint64_t* a_ready = acc_full + 2;
   uint32_t* tmem_slot = (uint32_t*)(a_ready + 2);
+  float* s_bias = (float*)(Wst + kStages * kChunkBytes + 256);  // (8, 256)
+  float* s_head = s_bias + kDepth * kWidth;                      // (256)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t npairs = (n + 255) / 256;
 
@@ -194,6 +226,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
     mbar_init(&a_ready[1], 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = threadIdx.x; i < kDepth * kWidth; i += blockDim.x) s_bias[i] = m.bias[i];
+  for (int i = threadIdx.x; i < kWidth; i += blockDim.x) s_head[i] = m.w_head[i];
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -260,15 +294,20 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
     const uint32_t a_t = smem_u32(A0 + t * kTileABytes);
     const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + t * 256;
     uint32_t af0 = 0, af1 = 0;
+    uint32_t pe[32];
     if ((int64_t)blockIdx.x < npairs) {
-      write_pe_row(src, n, (int64_t)blockIdx.x * 256 + t * 128 + r, a_t, r);
+      pe_row_packed(src, n, (int64_t)blockIdx.x * 256 + t * 128 + r, pe);
+      store_pe_row(pe, a_t, r);
       fence_proxy_async();
       mbar_arrive(&a_ready[0]);
     }
     for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
       float dot = 0.f;
+      const int64_t next = pair + gridDim.x;
       for (int l = 0; l < kDepth; l++) {
-        const float* bl = m.bias + l * kWidth;
+        const float* bl = s_bias + l * kWidth;
+        if (l == kDepth - 1 && next < npairs)  // hide the next tile's encoding behind layer 7's MMAs
+          pe_row_packed(src, n, next * 256 + t * 128 + r, pe);
         mbar_wait(&acc_full[0], af0 & 1);
         af0++;
         tc_fence_after();
@@ -279,10 +318,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
             uint32_t v[32];
             ODC_TMEM_LD32(trow + 32 * i, v);
             tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; j++)
-              pk[16 * i + j] = pack_bf16x2(relu_bias(v[2 * j], __ldg(bl + 32 * i + 2 * j)),
-                                           relu_bias(v[2 * j + 1], __ldg(bl + 32 * i + 2 * j + 1)));
+            relu_pack32<kBias>(v, bl + 32 * i, pk + 16 * i);
           }
         } else {
 #pragma unroll
@@ -290,8 +326,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
             uint32_t v[32];
             ODC_TMEM_LD32(trow + 32 * i, v);
             tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; j++) dot = fmaf(relu_bias(v[j], __ldg(bl + 32 * i + j)), __ldg(m.w_head + 32 * i + j), dot);
+            dot = head32<kBias>(v, bl + 32 * i, s_head + 32 * i, dot);
           }
         }
         mbar_wait(&acc_full[1], af1 & 1);
@@ -311,10 +346,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
             ODC_TMEM_LD32(trow + 128 + 32 * i, v);
             tmem_ld_wait();
             uint32_t w[16];
-#pragma unroll
-            for (int j = 0; j < 16; j++)
-              w[j] = pack_bf16x2(relu_bias(v[2 * j], __ldg(bl + 128 + 32 * i + 2 * j)),
-                                 relu_bias(v[2 * j + 1], __ldg(bl + 128 + 32 * i + 2 * j + 1)));
+            relu_pack32<kBias>(v, bl + 128 + 32 * i, w);
 #pragma unroll
             for (int c = 0; c < 4; c++) {
               const int cc = 4 * i + c;  // chunk within columns 128..255
@@ -330,11 +362,14 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
             uint32_t v[32];
             ODC_TMEM_LD32(trow + 128 + 32 * i, v);
             tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; j++)
-              dot = fmaf(relu_bias(v[j], __ldg(bl + 128 + 32 * i + j)), __ldg(m.w_head + 128 + 32 * i + j), dot);
+            dot = head32<kBias>(v, bl + 128 + 32 * i, s_head + 128 + 32 * i, dot);
           }
         }
+      }
+      if (next < npairs) {  // A is free: the next tile pair can start while this one finishes
+        store_pe_row(pe, a_t, r);
+        fence_proxy_async();
+        mbar_arrive(&a_ready[0]);
       }
       const int64_t p = pair * 256 + t * 128 + r;
       if (p < n) {
@@ -347,12 +382,6 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
         const double rv = 1.0 / (1.0 + exp(-logit));
         labels[p] = rv > 0.5 ? 1 : 0;
         if (raw) raw[p] = rv;
-      }
-      const int64_t next = pair + gridDim.x;
-      if (next < npairs) {
-        write_pe_row(src, n, next * 256 + t * 128 + r, a_t, r);
-        fence_proxy_async();
-        mbar_arrive(&a_ready[0]);
       }
     }
   }
@@ -373,7 +402,8 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+    cudaFuncSetAttribute(k_mlp_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+    cudaFuncSetAttribute(k_mlp_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -381,7 +411,10 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
   }
   const int64_t npairs = (n + 255) / 256;
   const int64_t grid = npairs < g_num_sms ? npairs : g_num_sms;
-  k_mlp_tc<<<(unsigned)grid, tc::kThreads, tc::kSmemBytes, s>>>(m, src, n, labels, raw);
+  if (m.has_bias)
+    k_mlp_tc<true><<<(unsigned)grid, tc::kThreads, tc::kSmemBytes, s>>>(m, src, n, labels, raw);
+  else
+    k_mlp_tc<false><<<(unsigned)grid, tc::kThreads, tc::kSmemBytes, s>>>(m, src, n, labels, raw);
   return 0;
 }
 

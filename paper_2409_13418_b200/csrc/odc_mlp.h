@@ -21,6 +21,7 @@ struct MlpDev {
   const uint16_t* w_packed;  // row-major bf16 W[k][n] per layer (layer 0 padded to K=64): SIMT evaluator
   const uint16_t* w_tc;      // 58 chunks of 128x64 bf16 in the UMMA SWIZZLE_128B smem image (odc_mlp_tc.cuh)
   int impl;                  // 0 = tcgen05 (default), 1 = SIMT reference evaluator
+  int has_bias;              // any non-zero bias (selects the bias-add epilogue)
   const float* bias;         // (8, 256)
   const float* w_head;       // (256)
   float b_head;

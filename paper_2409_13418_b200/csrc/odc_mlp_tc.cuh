@@ -36,7 +36,7 @@ constexpr uint32_t kIdesc = (1u << 4)      // D f32
                             | (1u << 10)   // B bf16
                             | (16u << 17)  // N = 128
                             | (8u << 24);  // M = 128
-constexpr size_t kSmemBytes = 1024 + 2 * kTileABytes + kStages * kChunkBytes + 256;
+constexpr size_t kSmemBytes = 1024 + 2 * kTileABytes + kStages * kChunkBytes + 256 + (8 * 256 + 256) * 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
