@@ -119,7 +119,7 @@ def cpu_sample(field, lo, hi, R_full, full_evals, sample_R=None):
 
     cores = len(os.sched_getaffinity(0))
     if is_mlp(field):
-        sR = sample_R or 40
+        sR = sample_R or 64
         t0 = time.perf_counter()
         o = oracle.contour_oracle(field, lo, hi, sR)
         dt = time.perf_counter() - t0
@@ -267,7 +267,7 @@ def run_gpu(args, rank, world, dist):
         h2d = 136 * len(lower_program(field))
     d2h = V * 24 + T * 12 + V * 24  # vertices f64, triangles i32 (widened on the host), provenance
     if res.raw_mesh is not res.mesh:
-        d2h += res.raw_mesh.n_vertices * 48 + T * 12
+        d2h += 8 * (res.mesh.n_vertices - res.raw_mesh.n_vertices)  # duplicate -> source map
 
     # ---- roofline of the dominant kernel (grid labels)
     peaks, peak_kind = load_peaks()

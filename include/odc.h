@@ -189,7 +189,8 @@ int odc_mesh_device(odc_ctx* ctx, int32_t which, const double** vertices, const 
 #define ODC_ARR_V_IN 20          /* i64 (K)                            */
 #define ODC_ARR_MID_LABEL 21     /* u8  (Q)                            */
 #define ODC_ARR_POS3 22          /* f64 (Q,3)                          */
-#define ODC_N_ARR 23
+#define ODC_ARR_DUP_SOURCE 23    /* i64 (V-V_raw): raw vertex of each repair duplicate */
+#define ODC_N_ARR 24
 /* Returns the element count (not bytes) in *n_elems; copies if dst != NULL. */
 int odc_copy_array(odc_ctx* ctx, int32_t which, void* dst, int64_t dst_bytes, int64_t* n_elems);
 

@@ -22,7 +22,7 @@ ARR = dict(
     pos2=(8, np.float64), status=(9, np.uint8), part_cell=(10, np.int64), part_index=(11, np.int64),
     cyc_len=(12, np.int64), cyc_edges=(13, np.int64), cyc_insts=(14, np.int64), normals=(15, np.float64),
     qef_pos=(16, np.float64), qef_rank=(17, np.int64), qef_resid=(18, np.float64), split_cases=(19, np.int64),
-    v_in=(20, np.int64), mid_label=(21, np.uint8), pos3=(22, np.float64),
+    v_in=(20, np.int64), mid_label=(21, np.uint8), pos3=(22, np.float64), dup_source=(23, np.int64),
 )
 
 

@@ -131,6 +131,11 @@ struct odc_ctx {
   int64_t* fan_edge = nullptr;
   uint8_t* kase = nullptr;
   int64_t* split_cases = nullptr;
+  struct DupPass {
+    const int64_t* src;  // device: source vertex of each new vertex of the pass
+    int64_t base, n;
+  };
+  std::vector<DupPass> dup_passes;  // repair passes (polygonize.py:348-358)
 };
 
 namespace {
@@ -579,6 +584,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   // ---- K8: repair_nonmanifold (polygonize.py:253-374), up to 4 passes
   mark(6);
   c->verts1 = verts;
+  c->dup_passes.clear();
   c->tris1 = tris;
   int64_t curV = V0;
   if (o->repair && T > 0) {
@@ -613,6 +619,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       int32_t* next = need(c->arena.get<int32_t>(3 * T));
       CUDA_TRY(cudaMemcpyAsync(next, cur, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
       int64_t* src_new = need(c->arena.get<int64_t>(E));
+      c->dup_passes.push_back({src_new, curV, E});
       launch_repair_apply(cv, cur, curV, off, inc, eoff, next, src_new, s);
       check_launch(c);
       double* nv = need(c->arena.get<double>(3 * (curV + E)));
@@ -960,6 +967,25 @@ int odc_copy_array(odc_ctx* c, int32_t which, void* dst, int64_t dst_bytes, int6
       case ODC_ARR_QEF_RANK: src = cc->cells.rank; n = (cc->cells.rank && has1d) ? cc->P : 0; break;
       case ODC_ARR_QEF_RESID: src = cc->cells.resid; n = (cc->cells.resid && has1d) ? cc->P : 0; break;
       case ODC_ARR_SPLIT_CASES: src = cc->split_cases; n = (cc->split_cases && has1d) ? cc->n_interior : 0; break;
+      case ODC_ARR_DUP_SOURCE: {
+        // original (raw-mesh) vertex of every repair duplicate, resolved across passes
+        n = cc->V1 - cc->V0;
+        if (x->dst && n) {
+          if (x->bytes < 8 * n) throw OdcError{ODC_E_ARG, "destination too small"};
+          int64_t* out = (int64_t*)x->dst;
+          for (const auto& dp : cc->dup_passes) {
+            std::vector<int64_t> s(dp.n);
+            CUDA_TRY(cudaMemcpyAsync(s.data(), dp.src, 8 * dp.n, cudaMemcpyDeviceToHost, cc->stream));
+            CUDA_TRY(cudaStreamSynchronize(cc->stream));
+            for (int64_t i = 0; i < dp.n; i++) {
+              int64_t v = s[i];
+              out[dp.base - cc->V0 + i] = v >= cc->V0 ? out[v - cc->V0] : v;
+            }
+          }
+        }
+        *x->n = n;
+        return (int)ODC_OK;
+      }
       case ODC_ARR_CYC_LEN: src = cc->cells.cyc_len; n = (cc->cells.cyc_len && has1d) ? cc->P : 0; break;
       default: throw OdcError{ODC_E_ARG, "unknown array id"};
     }

@@ -69,6 +69,15 @@ class TriangleMesh:
             if ((t[:, 0] == t[:, 1]) | (t[:, 1] == t[:, 2]) | (t[:, 2] == t[:, 0])).any():
                 raise ValueError("triangle with repeated vertex index")
 
+    @classmethod
+    def trusted(cls, vertices, triangles, provenance_kind=None, provenance_ref=None):
+        """Wrap arrays produced by libodc (already f64/i64, in range, no repeated
+        index) without re-running the O(T) validation of __post_init__."""
+        m = object.__new__(cls)
+        m.vertices, m.triangles = vertices, triangles
+        m.provenance_kind, m.provenance_ref = provenance_kind, provenance_ref
+        return m
+
     @property
     def n_vertices(self):
         return len(self.vertices)

@@ -200,7 +200,22 @@ def _copy_mesh(ctx, which, st, provenance=True):
     rc = L.odc_copy_mesh(ctx.handle, which, ptr(v), ptr(t), ptr(kind), ptr(ref))
     if rc != _lib.ODC_OK:
         _raise(rc, ctx)
-    return TriangleMesh(v, t, provenance_kind=kind, provenance_ref=ref)
+    return TriangleMesh.trusted(v, t, kind, ref)
+
+
+def _raw_from_repaired(ctx, mesh, st):
+    """The pre-repair mesh from the repaired one: repair only appends
+    duplicates of existing vertices and renames triangle corners to them
+    (polygonize.py:348-373), so mapping every duplicate back to its source
+    restores the raw triangles exactly."""
+    V0 = int(st.raw_n_vertices)
+    src = stage_arrays(ctx, ["dup_source"])["dup_source"]
+    t = mesh.triangles.copy()
+    m = t >= V0
+    t[m] = src[t[m] - V0]
+    kind = mesh.provenance_kind[:V0].copy() if mesh.provenance_kind is not None else None
+    ref = mesh.provenance_ref[:V0].copy() if mesh.provenance_ref is not None else None
+    return TriangleMesh.trusted(mesh.vertices[:V0].copy(), t, kind, ref)
 
 
 def stats_dict(st, options, mesh_counts=True):
@@ -272,7 +287,7 @@ def contour(field, grid, options=None, counter=None, *, device=0, provenance=Tru
         mesh = raw_mesh = empty
     else:
         mesh = _copy_mesh(ctx, 0, st, provenance)
-        raw_mesh = mesh if st.repair_added_vertices == 0 else _copy_mesh(ctx, 1, st, provenance)
+        raw_mesh = mesh if st.repair_added_vertices == 0 else _raw_from_repaired(ctx, mesh, st)
     record_counts(counter, st)
     stats["wall_time_s"] = time.perf_counter() - t0
     stats["eval_counts"] = counter.snapshot()
