@@ -158,6 +158,38 @@ void odc_default_options(odc_options* o);
 int odc_extract(odc_ctx* ctx, const odc_field* field, const double lo[3], const double hi[3], int64_t resolution,
                 const odc_options* opt, odc_stats* stats);
 
+/* ---- z-slab mode (multi-GPU) --------------------------------
+ * A rank extracts the owned cell layers [cell_z0, cell_z1) of the global grid
+ * plus a recomputed one-layer halo below (no halo data exchange).  Local
+ * vertex ids: [0, n_halo) halo-layer partitions (owned by the rank below),
+ * [n_halo, n_window) owned partitions, [n_window, n_window + n_fans) fan
+ * vertices of owned edges.  After an all-gather of (n_partitions, n_fans)
+ * the host calls odc_slab_globalize with the rank's global offsets; rank 0
+ * concatenates every rank's owned vertices/triangles in rank order (which is
+ * the reference's global order) and calls odc_mesh_finish, which drops
+ * unreferenced vertices and repairs (polygonize.py:199-209, :253-374).
+ * Device pointers stay valid until the next call on the context. */
+typedef struct {
+  int64_t n_halo_partitions, n_partitions, n_window_partitions, n_fans, n_triangles;
+  const double* partition_vertices; /* device (n_partitions,3) owned partition vertices */
+  const double* fan_vertices;       /* device (n_fans,3) */
+  const int32_t* triangles;         /* device (n_triangles,3), local ids */
+  const int64_t* partition_cell;    /* device (n_partitions) provenance ref[0] */
+  const int64_t* partition_index;   /* device (n_partitions) provenance ref[1] */
+  const int64_t* fan_edge;          /* device (n_fans) provenance ref[0] of fan vertices */
+} odc_slab_info;
+int odc_extract_slab(odc_ctx* ctx, const odc_field* field, const double lo[3], const double hi[3],
+                     int64_t resolution, const odc_options* opt, int64_t cell_z0, int64_t cell_z1,
+                     odc_stats* stats, odc_slab_info* info);
+/* rewrite the last slab's local triangle ids to global ids (device int32 (T,3)) */
+int odc_slab_globalize(odc_ctx* ctx, int64_t part_base, int64_t n_partitions_total, int64_t fan_base,
+                       int32_t* triangles_out);
+/* finish an assembled mesh (device or host pointers): unused-vertex removal +
+ * repair; the result is read back with odc_copy_mesh / odc_mesh_device. */
+int odc_mesh_finish(odc_ctx* ctx, const double* vertices, int64_t n_vertices, const int32_t* triangles,
+                    int64_t n_triangles, int64_t n_partitions, const int64_t* prov_kind, const int64_t* prov_ref,
+                    int32_t repair, odc_stats* stats);
+
 /* which: 0 = repaired mesh, 1 = raw (pre-repair) mesh.  Buffers sized from stats. */
 int odc_copy_mesh(odc_ctx* ctx, int32_t which, double* vertices, int64_t* triangles, int64_t* prov_kind,
                   int64_t* prov_ref);

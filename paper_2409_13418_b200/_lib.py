@@ -67,10 +67,20 @@ class Stats(ctypes.Structure):
     ]
 
 
+class SlabInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_halo_partitions", ctypes.c_int64), ("n_partitions", ctypes.c_int64),
+        ("n_window_partitions", ctypes.c_int64), ("n_fans", ctypes.c_int64), ("n_triangles", ctypes.c_int64),
+        ("partition_vertices", ctypes.c_void_p), ("fan_vertices", ctypes.c_void_p), ("triangles", ctypes.c_void_p),
+        ("partition_cell", ctypes.c_void_p), ("partition_index", ctypes.c_void_p), ("fan_edge", ctypes.c_void_p),
+    ]
+
+
 EXPORTS = (
     "odc_version", "odc_create", "odc_destroy", "odc_last_error", "odc_set_stream", "odc_field_analytic",
     "odc_field_mlp", "odc_field_free", "odc_default_options", "odc_extract", "odc_copy_mesh", "odc_mesh_device",
-    "odc_copy_array", "odc_eval_raw", "odc_eval_labels", "odc_set_param",
+    "odc_copy_array", "odc_eval_raw", "odc_eval_labels", "odc_set_param", "odc_extract_slab",
+    "odc_slab_globalize", "odc_mesh_finish",
 )
 
 _lib = None
@@ -108,6 +118,9 @@ def load():
         L.odc_copy_array.argtypes = [vp, i32, vp, i64, P(i64)]
         L.odc_eval_raw.argtypes = [vp, vp, vp, i64, vp]
         L.odc_eval_labels.argtypes = [vp, vp, vp, i64, vp]
+        L.odc_extract_slab.argtypes = [vp, vp, P(dbl), P(dbl), i64, P(Options), i64, i64, P(Stats), P(SlabInfo)]
+        L.odc_slab_globalize.argtypes = [vp, i64, i64, i64, vp]
+        L.odc_mesh_finish.argtypes = [vp, vp, i64, vp, i64, i64, vp, vp, i32, P(Stats)]
         _lib = L
         return L
 

@@ -131,6 +131,14 @@ struct odc_ctx {
   int64_t* fan_edge = nullptr;
   uint8_t* kase = nullptr;
   int64_t* split_cases = nullptr;
+  // slab mode (z-slab extraction)
+  bool slab_mode = false;
+  int64_t e_lo = 0, e_hi = 0, c_lo = 0, c_hi = 0, P_halo = 0, P_own = 0;
+  double* slab_verts = nullptr;
+  int32_t* slab_tris = nullptr;
+  // mesh assembled by odc_mesh_finish: provenance supplied by the caller
+  int64_t* prov_kind_in = nullptr;
+  int64_t* prov_ref_in = nullptr;
   struct DupPass {
     const int64_t* src;  // device: source vertex of each new vertex of the pass
     int64_t base, n;
@@ -230,343 +238,23 @@ void scan2(odc_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* oa, uint3
   check_launch(c, 3);
 }
 
-void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi[3], int64_t R,
-             const odc_options* o, odc_stats* st) {
-  // ---- validation: GridSpec (grid.py:24-31), ContourOptions.validate (pipeline.py:72-78)
-  if (R < 2) throw OdcError{ODC_E_VALUE, "resolution must be at least 2"};
-  for (int a = 0; a < 3; a++)
-    if (!(hi[a] > lo[a])) throw OdcError{ODC_E_VALUE, "grid box must have positive extent"};
-  if (o->one_d < 0 || o->one_d > 2) throw OdcError{ODC_E_CONFIG, "unknown 1D mode"};
-  if (o->normals < 0 || o->normals > 1) throw OdcError{ODC_E_CONFIG, "unknown normal mode"};
-  if (o->split < 0 || o->split > 1) throw OdcError{ODC_E_CONFIG, "unknown split mode"};
-  if (R > 1290) throw OdcError{ODC_E_VALUE, "resolution above 1290 exceeds the 32-bit vertex index space"};
-
-  std::memset(st, 0, sizeof *st);
-  for (int i = 0; i < ODC_N_CAT; i++) st->cat_order[i] = -1;
-  c->valid = false;
-  c->launches = 0;
-  c->arena.reset();
-  c->keep = o->keep_intermediates != 0;
+// Drop unreferenced partition vertices (polygonize.py:199-209), then repair
+// non-manifold fans (polygonize.py:253-374, up to 4 passes).  verts holds P
+// partition vertices followed by NF fan vertices; used marks referenced ones.
+void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris, int64_t T, uint8_t* used,
+                 bool repair, odc_stats* st, DevStats* dst, unsigned long long* totals) {
   cudaStream_t s = c->stream;
-  CUDA_TRY(cudaEventRecord(c->ev0, s));
-
-  GridP g{};
-  g.R = R;
-  g.S = R + 1;
-  g.S2 = g.S * g.S;
-  g.S3 = g.S2 * g.S;
-  g.W = (g.S + 31) / 32;
-  g.NW = g.S2 * g.W;
-  for (int a = 0; a < 3; a++) {
-    g.lo[a] = lo[a];
-    g.h[a] = (hi[a] - lo[a]) / (double)R;  // cell_size (grid.py:37-40)
-  }
-  c->g = g;
-  const OptP op = make_opt(o, f->continuous);
-  const FieldP fp{f->nodes, f->n_nodes, f->kind, f->iso};
-  const bool mlp = f->kind == 1;
-
-  DevStats* dst = need(c->arena.get<DevStats>(1));
-  DevStatus* dstat = need(c->arena.get<DevStatus>(1));
-  unsigned long long* totals = need(c->arena.get<unsigned long long>(8));
-  CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(DevStats), s));
-  CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), s));
-
-  int marks = 0;
-  auto mark = [&](int i) {
-    CUDA_TRY(cudaEventRecord(c->evs[i], s));
-    marks = i + 1;
-  };
-  // ---- K1: sample_labels (grid.py:109-126)
-  mark(0);
-  c->L = need(c->arena.get<uint32_t>(g.NW));
-  if (!mlp) {
-    launch_labels_analytic(g, fp, c->L, s);
-    check_launch(c);
-    mark(8);
-  } else {
-    uint8_t* bytes = need(c->arena.get<uint8_t>(g.S3));
-    PointSrc src{nullptr, g, 0};
-    MlpDev md = f->mlp;
-    md.impl = c->mlp_impl;
-    mlp_eval(md, src, g.S3, bytes, nullptr, s);
-    check_launch(c);
-    mark(8);
-    launch_pack_labels(g, bytes, c->L, s);
-    check_launch(c);
-  }
-  record(st, ODC_CAT_LABELS, 1, g.S3);
-  st->n_grid_vertices = g.S3;
-
-  // ---- K2: extract_active (grid.py:171-296)
-  mark(1);
-  const int64_t nt = active_tiles(g);
-  c->rec = need(c->arena.get<WordRec>(g.NW));
-  uint32_t* tiles = need(c->arena.get<uint32_t>(5 * nt));
-  launch_active_bits(g, c->L, c->rec, tiles, dst, s);
-  launch_scan_tiles(tiles, nt, 5, totals, s);
-  check_launch(c, 2);
-  readback(c, totals, 5 * sizeof(unsigned long long));
-  const int64_t K = (int64_t)c->h_pinned[0], Q = (int64_t)c->h_pinned[1], C = (int64_t)c->h_pinned[2],
-                Fn = (int64_t)c->h_pinned[3], F4 = (int64_t)c->h_pinned[4];
-  if (K >= (1ll << 31) || Q >= (1ll << 31)) throw OdcError{ODC_E_VALUE, "crossing set exceeds 2^31 elements"};
-  c->K = K;
-  c->Q = Q;
-  c->C = C;
-  c->F = Fn;
-  c->F4 = F4;
-  c->edge_key = need(c->arena.get<int64_t>(K));
-  c->inst_key = need(c->arena.get<int64_t>(Q));
-  c->cell_id = need(c->arena.get<int64_t>(C));
-  c->f4_key = need(c->arena.get<int64_t>(F4));
-  c->face_key = c->keep ? need(c->arena.get<int64_t>(Fn)) : nullptr;
-  c->face_nc = c->keep ? need(c->arena.get<int64_t>(Fn)) : nullptr;
-  launch_active_compact(g, c->rec, tiles, c->edge_key, c->inst_key, c->cell_id, c->f4_key, c->face_key, c->face_nc,
-                        s);
-  check_launch(c);
-  st->n_crossing_edges = K;
-  st->n_crossing_faces = Fn;
-  st->n_crossing_cells = C;
-
-  auto finish_stats = [&]() {
-    readback(c, dst, sizeof(DevStats));
-    DevStats h;
-    std::memcpy(&h, c->h_pinned, sizeof h);
-    st->boundary_inside_vertices = (int64_t)h.boundary_inside;
-    for (int i = 0; i < 4; i++) {
-      st->point2d_status_counts[i] = (int64_t)h.status[i];
-      st->qef_rank_counts[i] = (int64_t)h.rank[i];
-      st->split_case_counts[i] = (int64_t)h.split[i];
-    }
-    double mr;
-    std::memcpy(&mr, &h.max_resid_bits, 8);
-    st->qef_max_residual = mr;
-    st->normal_fallbacks = (int64_t)h.normal_fallbacks;
-    st->skipped_boundary_edges = (int64_t)h.skipped;
-    CUDA_TRY(cudaEventRecord(c->ev1, s));
-    CUDA_TRY(cudaEventSynchronize(c->ev1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
-    st->device_ms = ms;
-    // stage i spans mark i -> mark i+1 (or the end event)
-    for (int i = 0; i < 7; i++) {
-      float x = 0.f;
-      if (i + 1 < marks) cudaEventElapsedTime(&x, c->evs[i], c->evs[i + 1]);
-      else if (i < marks) cudaEventElapsedTime(&x, c->evs[i], c->ev1);
-      st->stage_ms[i] = x;
-    }
-    float k1 = 0.f;
-    cudaEventElapsedTime(&k1, c->evs[0], c->evs[8]);
-    st->stage_ms[7] = k1;
-    st->n_kernel_launches = c->launches;
-  };
-
-  if (K == 0) {  // pipeline.py:174-179
-    c->P = c->NF = c->T = c->V0 = c->V1 = c->Ns = c->n_interior = 0;
-    c->verts0 = c->verts1 = nullptr;
-    c->tris0 = c->tris1 = nullptr;
-    c->src0 = nullptr;
-    finish_stats();
-    c->valid = true;
-    return;
-  }
-
-  // ---- K3: 1D points (pipeline.py:94-123, search.py:71-94)
-  mark(2);
-  c->t1d = need(c->arena.get<double>(K));
-  c->pos1d = need(c->arena.get<double>(3 * K));
-  c->v_in = c->keep ? need(c->arena.get<int64_t>(K)) : nullptr;
-  if (!mlp) {
-    launch_search1d_analytic(g, fp, op, c->L, c->edge_key, K, c->t1d, c->pos1d, c->v_in, s);
-    check_launch(c);
-  } else {
-    double* lo1 = need(c->arena.get<double>(K));
-    double* hi1 = need(c->arena.get<double>(K));
-    double* pts = need(c->arena.get<double>(3 * K));
-    uint8_t* lab = need(c->arena.get<uint8_t>(K));
-    double *raw_in = nullptr, *raw_out = nullptr;
-    launch_search1d_init(g, c->L, c->edge_key, K, lo1, hi1, s);
-    check_launch(c);
-    if (op.one_d == ODC_ONE_D_BINARY) {
-      for (int it = 0; it < op.iters_1d; it++) {
-        launch_search1d_points(g, c->L, c->edge_key, K, lo1, hi1, pts, s);
-        check_launch(c);
-        eval_points(c, f, pts, K, lab, nullptr);
-        launch_search1d_update(K, lab, lo1, hi1, s);
-        check_launch(c);
-      }
-    } else if (op.one_d == ODC_ONE_D_LINEAR && f->continuous) {
-      // raw grid values at the endpoints (LabelVolume.raw, grid.py:115-123): lo=0 / hi=1 points
-      raw_in = need(c->arena.get<double>(K));
-      raw_out = need(c->arena.get<double>(K));
-      launch_edge_endpoints(g, c->L, c->edge_key, K, 0, pts, s);
-      eval_points(c, f, pts, K, lab, raw_in);
-      launch_edge_endpoints(g, c->L, c->edge_key, K, 1, pts, s);
-      eval_points(c, f, pts, K, lab, raw_out);
-      check_launch(c, 2);
-    }
-    launch_search1d_finish(g, op, c->L, c->edge_key, K, lo1, hi1, raw_in, raw_out, c->t1d, c->pos1d, c->v_in, s);
-    check_launch(c);
-  }
-  if (op.one_d == ODC_ONE_D_BINARY) record(st, ODC_CAT_SEARCH_1D, op.iters_1d, (int64_t)op.iters_1d * K);
-
-  // ---- face_pairings probes (dualize.py:59-70)
-  if (F4) {
-    if (!mlp) {
-      launch_face_center_analytic(g, fp, c->f4_key, F4, c->rec, s);
-      check_launch(c);
-    } else {
-      double* pts = need(c->arena.get<double>(3 * F4));
-      uint8_t* lab = need(c->arena.get<uint8_t>(F4));
-      launch_face_center_points(g, c->f4_key, F4, pts, s);
-      check_launch(c);
-      eval_points(c, f, pts, F4, lab, nullptr);
-      launch_face_center_scatter(g, c->f4_key, lab, F4, c->rec, s);
-      check_launch(c);
-    }
-    record(st, ODC_CAT_PROBE_FACE_CENTER, 1, F4);
-  }
-  st->n_face_center_probes = F4;
-
-  // ---- normals: 2D points (search.py:194-322) or fd gradient (pipeline.py:126-151)
-  mark(3);
-  double* edge_normals = nullptr;
-  c->inst_edges = c->keep ? need(c->arena.get<int64_t>(2 * Q)) : nullptr;
-  c->s2 = Stage2D{};
-  if (op.normals == ODC_NORMALS_2D) {
-    c->s2.pos3 = need(c->arena.get<double>(3 * Q));
-    if (c->keep) {
-      c->s2.pos2 = need(c->arena.get<double>(2 * Q));
-      c->s2.status = need(c->arena.get<uint8_t>(Q));
-      c->s2.mid = need(c->arena.get<uint8_t>(Q));
-    }
-    if (!mlp) {
-      launch_search2d_analytic(g, fp, op, c->L, c->rec, c->inst_key, Q, c->pos1d, c->s2, c->inst_edges, dst, dstat,
-                               s);
-      check_launch(c);
-    } else {
-      void* state = need(c->arena.alloc(search2d_state_bytes(Q)));
-      double* pts = need(c->arena.get<double>(6 * Q));
-      uint8_t* lab = need(c->arena.get<uint8_t>(2 * Q));
-      launch_search2d_lockstep_init(g, op, c->L, c->rec, c->inst_key, Q, c->pos1d, state, c->inst_edges, s);
-      check_launch(c);
-      const int nsteps = search2d_num_steps(op);
-      for (int step = 0; step < nsteps; step++) {
-        int64_t M = launch_search2d_lockstep_points(g, op, c->inst_key, Q, step, state, pts, s);
-        check_launch(c);
-        eval_points(c, f, pts, M, lab, nullptr);
-        launch_search2d_lockstep_update(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, s);
-        check_launch(c);
-      }
-      launch_search2d_lockstep_finish(g, op, c->L, c->rec, c->inst_key, Q, c->pos1d, state, c->s2, dst, s);
-      check_launch(c);
-    }
-    check_status(c, dstat);
-    record(st, ODC_CAT_PROBE_FACE_MIDPOINT, 1, Q);
-    record(st, ODC_CAT_SEARCH_2D, op.s1_lin + op.s1_bin + op.s2_lin + op.s2_bin,
-           (int64_t)(op.s1_lin + op.s1_bin) * Q + (int64_t)(op.s2_lin + op.s2_bin) * 2 * Q);
-    st->n_2d_points = Q;
-  } else {
-    if (!f->continuous)
-      throw OdcError{ODC_E_CONFIG, "fd-gradient normals require a field with continuous raw values"};
-    double* pts = need(c->arena.get<double>(18 * K));
-    double* raw = need(c->arena.get<double>(6 * K));
-    uint8_t* lab = need(c->arena.get<uint8_t>(6 * K));
-    launch_fd_points(g, op, c->pos1d, K, pts, s);
-    check_launch(c);
-    eval_points(c, f, pts, 6 * K, lab, raw);
-    edge_normals = need(c->arena.get<double>(3 * K));
-    launch_fd_normals(g, op, c->L, c->edge_key, K, raw, edge_normals, dst, s);
-    check_launch(c);
-    record(st, ODC_CAT_FD_GRADIENT, 1, 6 * K);
-    st->n_2d_points = 0;
-  }
-
-  // ---- K6: partitions + plane samples + QEF (dualize.py:194-444)
-  mark(4);
-  uint16_t* cfg = need(c->arena.get<uint16_t>(C));
-  uint32_t* ncyc = need(c->arena.get<uint32_t>(C));
-  uint32_t* nsamp = need(c->arena.get<uint32_t>(C));
-  uint32_t* pbase = need(c->arena.get<uint32_t>(C));
-  uint32_t* sbase = need(c->arena.get<uint32_t>(C));
-  launch_cell_config(g, c->L, c->rec, c->cell_id, C, c->table, cfg, ncyc, nsamp, s);
-  check_launch(c);
-  scan2(c, ncyc, nsamp, pbase, sbase, C, totals);
-  readback(c, totals, 2 * sizeof(unsigned long long));
-  const int64_t P = (int64_t)c->h_pinned[0], Ns = (int64_t)c->h_pinned[1];
-  c->P = P;
-  c->Ns = Ns;
-  st->n_partitions = P;
-  st->n_plane_samples = Ns;
-  // vertex buffer sized for the worst case of fan vertices (one per edge)
-  double* verts = need(c->arena.get<double>(3 * (P + K)));
-  CellOut co{};
-  co.verts = verts;
-  co.part_cell = need(c->arena.get<int64_t>(P));
-  co.part_index = need(c->arena.get<int64_t>(P));
-  co.pinfo = need(c->arena.get<uint64_t>(C));
-  if (c->keep) {
-    co.rank = need(c->arena.get<int64_t>(P));
-    co.resid = need(c->arena.get<double>(P));
-    co.cyc_edges = need(c->arena.get<int64_t>(Ns));
-    co.cyc_insts = need(c->arena.get<int64_t>(Ns));
-    co.normals = need(c->arena.get<double>(3 * Ns));
-    co.cyc_len = need(c->arena.get<int64_t>(P));
-  }
-  launch_cell_solve(g, op, c->L, c->rec, c->cell_id, C, c->table, cfg, pbase, sbase, c->pos1d, c->s2.pos3,
-                    edge_normals, co, dst, s);
-  check_launch(c);
-  c->cells = co;
-
-  // ---- K7: build_mesh (polygonize.py:110-217)
-  mark(5);
-  int4* pid4 = need(c->arena.get<int4>(K));
-  c->kase = need(c->arena.get<uint8_t>(K));
-  uint32_t* ntri = need(c->arena.get<uint32_t>(K));
-  uint32_t* nfan = need(c->arena.get<uint32_t>(K));
-  uint32_t* toff = need(c->arena.get<uint32_t>(K));
-  uint32_t* frank = need(c->arena.get<uint32_t>(K));
-  launch_poly_classify(g, op, c->L, c->rec, c->edge_key, K, co.pinfo, verts, pid4, c->kase, ntri, nfan, dst, s);
-  check_launch(c);
-  scan2(c, ntri, nfan, toff, frank, K, totals);
-  readback(c, totals, 2 * sizeof(unsigned long long));
-  const int64_t T = (int64_t)c->h_pinned[0], NF = (int64_t)c->h_pinned[1];
-  c->T = T;
-  c->NF = NF;
-  int32_t* tris = need(c->arena.get<int32_t>(3 * T));
-  c->fan_edge = need(c->arena.get<int64_t>(NF));
-  uint8_t* used = need(c->arena.get<uint8_t>(P + NF));
-  CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)(P + NF), s));
-  if (NF) CUDA_TRY(cudaMemsetAsync(used + P, 1, (size_t)NF, s));
-  launch_poly_emit(K, P, c->edge_key, pid4, c->kase, toff, frank, c->pos1d, verts, tris, c->fan_edge, used, s);
-  check_launch(c);
   launch_count_used(used, P, dst, s);
   check_launch(c);
-  if (c->keep) {
-    uint32_t* flag = need(c->arena.get<uint32_t>(K));
-    uint32_t* rank = need(c->arena.get<uint32_t>(K));
-    launch_interior_flags(K, c->kase, flag, s);
-    check_launch(c);
-    scan1(c, flag, rank, K, totals + 4);
-    readback(c, totals + 4, sizeof(unsigned long long));
-    c->n_interior = (int64_t)c->h_pinned[0];
-    c->split_cases = need(c->arena.get<int64_t>(c->n_interior));
-    launch_split_cases(K, c->kase, c->split_cases, rank, s);
-    check_launch(c);
-  }
   readback(c, &dst->used_partitions, sizeof(unsigned long long));
   const int64_t used_p = (int64_t)c->h_pinned[0];
   int64_t V0 = P + NF;
   c->src0 = nullptr;
-  if (used_p != P) {  // drop unreferenced vertices (polygonize.py:199-209)
+  if (used_p != P) {
     uint32_t* u32 = need(c->arena.get<uint32_t>(V0));
     uint32_t* nid = need(c->arena.get<uint32_t>(V0));
-    // widen used flags
-    std::vector<uint8_t> hu(V0);
-    CUDA_TRY(cudaMemcpyAsync(hu.data(), used, V0, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    std::vector<uint32_t> hw(hu.begin(), hu.end());
-    CUDA_TRY(cudaMemcpyAsync(u32, hw.data(), 4 * V0, cudaMemcpyHostToDevice, s));
+    launch_widen_flags(used, V0, u32, s);
+    check_launch(c);
     scan1(c, u32, nid, V0, totals + 5);
     double* vc = need(c->arena.get<double>(3 * V0));
     c->src0 = need(c->arena.get<int64_t>(V0));
@@ -580,14 +268,11 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   c->V0 = V0;
   st->raw_n_vertices = V0;
   st->raw_n_triangles = T;
-
-  // ---- K8: repair_nonmanifold (polygonize.py:253-374), up to 4 passes
-  mark(6);
   c->verts1 = verts;
   c->dup_passes.clear();
   c->tris1 = tris;
   int64_t curV = V0;
-  if (o->repair && T > 0) {
+  if (repair && T > 0) {
     int32_t* cur = need(c->arena.get<int32_t>(3 * T));
     CUDA_TRY(cudaMemcpyAsync(cur, tris, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
     double* cv = verts;
@@ -634,11 +319,411 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     c->tris1 = cur;
     st->repair_passes = passes;
   }
-  mark(7);
   c->V1 = curV;
   st->n_vertices = curV;
   st->n_triangles = T;
   st->repair_added_vertices = curV - V0;
+}
+
+// z-window of one extraction: owned cell layers [c0, c1) plus a one-layer
+// halo below; the full grid is c0 = 0, c1 = R.
+struct Window {
+  int64_t c0, c1;
+  bool slab;  // stop after polygonization (offsets are assigned across ranks)
+};
+
+void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi[3], int64_t R,
+             const odc_options* o, odc_stats* st, const Window& win) {
+  // ---- validation: GridSpec (grid.py:24-31), ContourOptions.validate (pipeline.py:72-78)
+  if (R < 2) throw OdcError{ODC_E_VALUE, "resolution must be at least 2"};
+  for (int a = 0; a < 3; a++)
+    if (!(hi[a] > lo[a])) throw OdcError{ODC_E_VALUE, "grid box must have positive extent"};
+  if (o->one_d < 0 || o->one_d > 2) throw OdcError{ODC_E_CONFIG, "unknown 1D mode"};
+  if (o->normals < 0 || o->normals > 1) throw OdcError{ODC_E_CONFIG, "unknown normal mode"};
+  if (o->split < 0 || o->split > 1) throw OdcError{ODC_E_CONFIG, "unknown split mode"};
+  if (R > 1290) throw OdcError{ODC_E_VALUE, "resolution above 1290 exceeds the 32-bit vertex index space"};
+  if (win.c0 < 0 || win.c1 > R || win.c0 >= win.c1) throw OdcError{ODC_E_ARG, "bad slab range"};
+
+  std::memset(st, 0, sizeof *st);
+  for (int i = 0; i < ODC_N_CAT; i++) st->cat_order[i] = -1;
+  c->valid = false;
+  c->launches = 0;
+  c->arena.reset();
+  c->keep = o->keep_intermediates != 0;
+  cudaStream_t s = c->stream;
+  CUDA_TRY(cudaEventRecord(c->ev0, s));
+
+  GridP g{};
+  g.R = R;
+  g.S = R + 1;
+  g.S2 = g.S * g.S;
+  g.S3 = g.S2 * g.S;
+  g.W = (g.S + 31) / 32;
+  g.z0 = win.c0 > 0 ? win.c0 - 1 : 0;  // one halo layer below the owned cells
+  g.nz = win.c1 - g.z0 + 1;            // through the top vertex layer of the owned cells
+  g.own0 = win.c0;
+  g.own1 = win.c1 == R ? g.S : win.c1;  // the last slab owns the top vertex layer
+  g.NW = g.nz * g.S * g.W;
+  c->slab_mode = win.slab;
+  for (int a = 0; a < 3; a++) {
+    g.lo[a] = lo[a];
+    g.h[a] = (hi[a] - lo[a]) / (double)R;  // cell_size (grid.py:37-40)
+  }
+  c->g = g;
+  const OptP op = make_opt(o, f->continuous);
+  const FieldP fp{f->nodes, f->n_nodes, f->kind, f->iso};
+  const bool mlp = f->kind == 1;
+
+  DevStats* dst = need(c->arena.get<DevStats>(1));
+  DevStatus* dstat = need(c->arena.get<DevStatus>(1));
+  unsigned long long* totals = need(c->arena.get<unsigned long long>(8));
+  CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(DevStats), s));
+  CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), s));
+
+  int marks = 0;
+  auto mark = [&](int i) {
+    CUDA_TRY(cudaEventRecord(c->evs[i], s));
+    marks = i + 1;
+  };
+  // ---- K1: sample_labels (grid.py:109-126)
+  mark(0);
+  c->L = need(c->arena.get<uint32_t>(g.NW));
+  if (!mlp) {
+    launch_labels_analytic(g, fp, c->L, s);
+    check_launch(c);
+    mark(8);
+  } else {
+    uint8_t* bytes = need(c->arena.get<uint8_t>(g.nz * g.S2));
+    PointSrc src{nullptr, g, g.z0 * g.S2};
+    MlpDev md = f->mlp;
+    md.impl = c->mlp_impl;
+    mlp_eval(md, src, g.nz * g.S2, bytes, nullptr, s);
+    check_launch(c);
+    mark(8);
+    launch_pack_labels(g, bytes, c->L, s);
+    check_launch(c);
+  }
+  record(st, ODC_CAT_LABELS, 1, (g.own1 - g.own0) * g.S2);
+  st->n_grid_vertices = (g.own1 - g.own0) * g.S2;
+
+  // ---- K2: extract_active (grid.py:171-296)
+  mark(1);
+  const int64_t nt = active_tiles(g);
+  c->rec = need(c->arena.get<WordRec>(g.NW));
+  uint32_t* tiles = need(c->arena.get<uint32_t>(5 * nt));
+  launch_active_bits(g, c->L, c->rec, tiles, dst, s);
+  launch_scan_tiles(tiles, nt, 5, totals, s);
+  check_launch(c, 2);
+  readback(c, totals, 5 * sizeof(unsigned long long));
+  const int64_t K = (int64_t)c->h_pinned[0], Q = (int64_t)c->h_pinned[1], C = (int64_t)c->h_pinned[2],
+                Fn = (int64_t)c->h_pinned[3], F4 = (int64_t)c->h_pinned[4];
+  if (K >= (1ll << 31) || Q >= (1ll << 31)) throw OdcError{ODC_E_VALUE, "crossing set exceeds 2^31 elements"};
+  c->K = K;
+  c->Q = Q;
+  c->C = C;
+  c->F = Fn;
+  c->F4 = F4;
+  c->edge_key = need(c->arena.get<int64_t>(K));
+  c->inst_key = need(c->arena.get<int64_t>(Q));
+  c->cell_id = need(c->arena.get<int64_t>(C));
+  c->f4_key = need(c->arena.get<int64_t>(F4));
+  c->face_key = c->keep ? need(c->arena.get<int64_t>(Fn)) : nullptr;
+  c->face_nc = c->keep ? need(c->arena.get<int64_t>(Fn)) : nullptr;
+  launch_active_compact(g, c->rec, tiles, c->edge_key, c->inst_key, c->cell_id, c->f4_key, c->face_key, c->face_nc,
+                        s);
+  check_launch(c);
+  // owned element ranges: rows are in key order, so ownership by base layer
+  // is a contiguous row range [lo, hi) read from the word ranks
+  int64_t e_lo = 0, e_hi = K, q_lo = 0, q_hi = Q, c_lo = 0, c_hi = C, f_own = Fn, f4_own = F4;
+  if (win.slab || g.z0 != 0 || g.nz != g.S) {
+    const int64_t ztop = g.z0 + g.nz - 1;
+    WordRec* h = reinterpret_cast<WordRec*>(c->h_pinned);
+    CUDA_TRY(cudaMemcpyAsync(&h[0], c->rec + (g.own0 - g.z0) * g.S * g.W, sizeof(WordRec), cudaMemcpyDeviceToHost, s));
+    if (g.own1 <= ztop)
+      CUDA_TRY(cudaMemcpyAsync(&h[1], c->rec + (g.own1 - g.z0) * g.S * g.W, sizeof(WordRec), cudaMemcpyDeviceToHost,
+                               s));
+    launch_count_owned_faces(g, c->rec, dst, s);
+    check_launch(c);
+    CUDA_TRY(cudaMemcpyAsync(&h[2], &dst->faces_own, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    e_lo = h[0].pe;
+    q_lo = h[0].pq;
+    c_lo = h[0].pc;
+    if (g.own1 <= ztop) {
+      e_hi = h[1].pe;
+      q_hi = h[1].pq;
+      c_hi = h[1].pc;
+    }
+    const unsigned long long* fc = reinterpret_cast<const unsigned long long*>(&h[2]);
+    f_own = (int64_t)fc[0];
+    f4_own = (int64_t)fc[1];
+  }
+  c->e_lo = e_lo;
+  c->e_hi = e_hi;
+  c->c_lo = c_lo;
+  c->c_hi = c_hi;
+  const int64_t K_own = e_hi - e_lo, Q_own = q_hi - q_lo;
+  st->n_crossing_edges = K_own;
+  st->n_crossing_faces = f_own;
+  st->n_crossing_cells = c_hi - c_lo;
+
+  auto finish_stats = [&]() {
+    readback(c, dst, sizeof(DevStats));
+    DevStats h;
+    std::memcpy(&h, c->h_pinned, sizeof h);
+    st->boundary_inside_vertices = (int64_t)h.boundary_inside;
+    for (int i = 0; i < 4; i++) {
+      st->point2d_status_counts[i] = (int64_t)h.status[i];
+      st->qef_rank_counts[i] = (int64_t)h.rank[i];
+      st->split_case_counts[i] = (int64_t)h.split[i];
+    }
+    double mr;
+    std::memcpy(&mr, &h.max_resid_bits, 8);
+    st->qef_max_residual = mr;
+    st->normal_fallbacks = (int64_t)h.normal_fallbacks;
+    st->skipped_boundary_edges = (int64_t)h.skipped;
+    CUDA_TRY(cudaEventRecord(c->ev1, s));
+    CUDA_TRY(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    st->device_ms = ms;
+    // stage i spans mark i -> mark i+1 (or the end event)
+    for (int i = 0; i < 7; i++) {
+      float x = 0.f;
+      if (i + 1 < marks) cudaEventElapsedTime(&x, c->evs[i], c->evs[i + 1]);
+      else if (i < marks) cudaEventElapsedTime(&x, c->evs[i], c->ev1);
+      st->stage_ms[i] = x;
+    }
+    float k1 = 0.f;
+    cudaEventElapsedTime(&k1, c->evs[0], c->evs[8]);
+    st->stage_ms[7] = k1;
+    st->n_kernel_launches = c->launches;
+  };
+
+  if (K == 0) {  // pipeline.py:174-179
+    c->P = c->NF = c->T = c->V0 = c->V1 = c->Ns = c->n_interior = 0;
+    c->P_halo = c->P_own = 0;
+    c->prov_kind_in = c->prov_ref_in = nullptr;
+    c->verts0 = c->verts1 = nullptr;
+    c->tris0 = c->tris1 = nullptr;
+    c->src0 = nullptr;
+    finish_stats();
+    c->valid = true;
+    return;
+  }
+
+  // ---- K3: 1D points (pipeline.py:94-123, search.py:71-94)
+  mark(2);
+  c->t1d = need(c->arena.get<double>(K));
+  c->pos1d = need(c->arena.get<double>(3 * K));
+  c->v_in = c->keep ? need(c->arena.get<int64_t>(K)) : nullptr;
+  if (!mlp) {
+    launch_search1d_analytic(g, fp, op, c->L, c->edge_key, K, c->t1d, c->pos1d, c->v_in, s);
+    check_launch(c);
+  } else {
+    double* lo1 = need(c->arena.get<double>(K));
+    double* hi1 = need(c->arena.get<double>(K));
+    double* pts = need(c->arena.get<double>(3 * K));
+    uint8_t* lab = need(c->arena.get<uint8_t>(K));
+    double *raw_in = nullptr, *raw_out = nullptr;
+    launch_search1d_init(g, c->L, c->edge_key, K, lo1, hi1, s);
+    check_launch(c);
+    if (op.one_d == ODC_ONE_D_BINARY) {
+      for (int it = 0; it < op.iters_1d; it++) {
+        launch_search1d_points(g, c->L, c->edge_key, K, lo1, hi1, pts, s);
+        check_launch(c);
+        eval_points(c, f, pts, K, lab, nullptr);
+        launch_search1d_update(K, lab, lo1, hi1, s);
+        check_launch(c);
+      }
+    } else if (op.one_d == ODC_ONE_D_LINEAR && f->continuous) {
+      // raw grid values at the endpoints (LabelVolume.raw, grid.py:115-123): lo=0 / hi=1 points
+      raw_in = need(c->arena.get<double>(K));
+      raw_out = need(c->arena.get<double>(K));
+      launch_edge_endpoints(g, c->L, c->edge_key, K, 0, pts, s);
+      eval_points(c, f, pts, K, lab, raw_in);
+      launch_edge_endpoints(g, c->L, c->edge_key, K, 1, pts, s);
+      eval_points(c, f, pts, K, lab, raw_out);
+      check_launch(c, 2);
+    }
+    launch_search1d_finish(g, op, c->L, c->edge_key, K, lo1, hi1, raw_in, raw_out, c->t1d, c->pos1d, c->v_in, s);
+    check_launch(c);
+  }
+  if (op.one_d == ODC_ONE_D_BINARY) record(st, ODC_CAT_SEARCH_1D, op.iters_1d, (int64_t)op.iters_1d * K_own);
+
+  // ---- face_pairings probes (dualize.py:59-70)
+  if (F4) {
+    if (!mlp) {
+      launch_face_center_analytic(g, fp, c->f4_key, F4, c->rec, s);
+      check_launch(c);
+    } else {
+      double* pts = need(c->arena.get<double>(3 * F4));
+      uint8_t* lab = need(c->arena.get<uint8_t>(F4));
+      launch_face_center_points(g, c->f4_key, F4, pts, s);
+      check_launch(c);
+      eval_points(c, f, pts, F4, lab, nullptr);
+      launch_face_center_scatter(g, c->f4_key, lab, F4, c->rec, s);
+      check_launch(c);
+    }
+  }
+  if (f4_own) record(st, ODC_CAT_PROBE_FACE_CENTER, 1, f4_own);
+  st->n_face_center_probes = f4_own;
+
+  // ---- normals: 2D points (search.py:194-322) or fd gradient (pipeline.py:126-151)
+  mark(3);
+  double* edge_normals = nullptr;
+  c->inst_edges = c->keep ? need(c->arena.get<int64_t>(2 * Q)) : nullptr;
+  c->s2 = Stage2D{};
+  if (op.normals == ODC_NORMALS_2D) {
+    c->s2.pos3 = need(c->arena.get<double>(3 * Q));
+    if (c->keep) {
+      c->s2.pos2 = need(c->arena.get<double>(2 * Q));
+      c->s2.status = need(c->arena.get<uint8_t>(Q));
+      c->s2.mid = need(c->arena.get<uint8_t>(Q));
+    }
+    if (!mlp) {
+      launch_search2d_analytic(g, fp, op, c->L, c->rec, c->inst_key, Q, c->pos1d, c->s2, c->inst_edges, dst, dstat,
+                               q_lo, q_hi, s);
+      check_launch(c);
+    } else {
+      void* state = need(c->arena.alloc(search2d_state_bytes(Q)));
+      double* pts = need(c->arena.get<double>(6 * Q));
+      uint8_t* lab = need(c->arena.get<uint8_t>(2 * Q));
+      launch_search2d_lockstep_init(g, op, c->L, c->rec, c->inst_key, Q, c->pos1d, state, c->inst_edges, s);
+      check_launch(c);
+      const int nsteps = search2d_num_steps(op);
+      for (int step = 0; step < nsteps; step++) {
+        int64_t M = launch_search2d_lockstep_points(g, op, c->inst_key, Q, step, state, pts, s);
+        check_launch(c);
+        eval_points(c, f, pts, M, lab, nullptr);
+        launch_search2d_lockstep_update(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, s);
+        check_launch(c);
+      }
+      launch_search2d_lockstep_finish(g, op, c->L, c->rec, c->inst_key, Q, c->pos1d, state, c->s2, dst, q_lo, q_hi,
+                                      s);
+      check_launch(c);
+    }
+    check_status(c, dstat);
+    record(st, ODC_CAT_PROBE_FACE_MIDPOINT, 1, Q_own);
+    record(st, ODC_CAT_SEARCH_2D, op.s1_lin + op.s1_bin + op.s2_lin + op.s2_bin,
+           (int64_t)(op.s1_lin + op.s1_bin) * Q_own + (int64_t)(op.s2_lin + op.s2_bin) * 2 * Q_own);
+    st->n_2d_points = Q_own;
+  } else {
+    if (!f->continuous)
+      throw OdcError{ODC_E_CONFIG, "fd-gradient normals require a field with continuous raw values"};
+    double* pts = need(c->arena.get<double>(18 * K));
+    double* raw = need(c->arena.get<double>(6 * K));
+    uint8_t* lab = need(c->arena.get<uint8_t>(6 * K));
+    launch_fd_points(g, op, c->pos1d, K, pts, s);
+    check_launch(c);
+    eval_points(c, f, pts, 6 * K, lab, raw);
+    edge_normals = need(c->arena.get<double>(3 * K));
+    launch_fd_normals(g, op, c->L, c->edge_key, K, raw, edge_normals, dst, e_lo, e_hi, s);
+    check_launch(c);
+    record(st, ODC_CAT_FD_GRADIENT, 1, 6 * K_own);
+    st->n_2d_points = 0;
+  }
+
+  // ---- K6: partitions + plane samples + QEF (dualize.py:194-444)
+  mark(4);
+  uint16_t* cfg = need(c->arena.get<uint16_t>(C));
+  uint32_t* ncyc = need(c->arena.get<uint32_t>(C));
+  uint32_t* nsamp = need(c->arena.get<uint32_t>(C));
+  uint32_t* pbase = need(c->arena.get<uint32_t>(C + 1));
+  uint32_t* sbase = need(c->arena.get<uint32_t>(C + 1));
+  launch_cell_config(g, c->L, c->rec, c->cell_id, C, c->table, cfg, ncyc, nsamp, s);
+  check_launch(c);
+  scan2(c, ncyc, nsamp, pbase, sbase, C, totals);
+  readback(c, totals, 2 * sizeof(unsigned long long));
+  const int64_t P = (int64_t)c->h_pinned[0], Ns = (int64_t)c->h_pinned[1];
+  int64_t P_halo = 0, P_end = P;  // partitions of the halo cell layer come first
+  if (c_lo > 0 || c_hi < C) {
+    uint32_t* hp = reinterpret_cast<uint32_t*>(c->h_pinned);
+    hp[0] = hp[1] = 0;
+    if (c_lo > 0 && c_lo < C) CUDA_TRY(cudaMemcpyAsync(&hp[0], pbase + c_lo, 4, cudaMemcpyDeviceToHost, s));
+    if (c_hi < C) CUDA_TRY(cudaMemcpyAsync(&hp[1], pbase + c_hi, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    P_halo = c_lo >= C ? P : (int64_t)hp[0];
+    P_end = c_hi < C ? (int64_t)hp[1] : P;
+  }
+  c->P = P;
+  c->Ns = Ns;
+  c->P_halo = P_halo;
+  st->n_partitions = P_end - P_halo;
+  st->n_plane_samples = Ns;
+  // vertex buffer sized for the worst case of fan vertices (one per owned edge)
+  double* verts = need(c->arena.get<double>(3 * (P + K_own)));
+  CellOut co{};
+  co.verts = verts;
+  co.part_cell = need(c->arena.get<int64_t>(P));
+  co.part_index = need(c->arena.get<int64_t>(P));
+  co.pinfo = need(c->arena.get<uint64_t>(C));
+  if (c->keep) {
+    co.rank = need(c->arena.get<int64_t>(P));
+    co.resid = need(c->arena.get<double>(P));
+    co.cyc_edges = need(c->arena.get<int64_t>(Ns));
+    co.cyc_insts = need(c->arena.get<int64_t>(Ns));
+    co.normals = need(c->arena.get<double>(3 * Ns));
+    co.cyc_len = need(c->arena.get<int64_t>(P));
+  }
+  launch_cell_solve(g, op, c->L, c->rec, c->cell_id, C, c->table, cfg, pbase, sbase, c->pos1d, c->s2.pos3,
+                    edge_normals, co, dst, c_lo, c_hi, s);
+  check_launch(c);
+  c->cells = co;
+
+  // ---- K7: build_mesh (polygonize.py:110-217) over the owned edges
+  mark(5);
+  const int64_t* ekey = c->edge_key + e_lo;
+  const double* epos = c->pos1d + 3 * e_lo;
+  int4* pid4 = need(c->arena.get<int4>(K_own));
+  c->kase = need(c->arena.get<uint8_t>(K_own));
+  uint32_t* ntri = need(c->arena.get<uint32_t>(K_own));
+  uint32_t* nfan = need(c->arena.get<uint32_t>(K_own));
+  uint32_t* toff = need(c->arena.get<uint32_t>(K_own));
+  uint32_t* frank = need(c->arena.get<uint32_t>(K_own));
+  launch_poly_classify(g, op, c->L, c->rec, ekey, K_own, co.pinfo, verts, pid4, c->kase, ntri, nfan, dst, s);
+  check_launch(c);
+  scan2(c, ntri, nfan, toff, frank, K_own, totals);
+  readback(c, totals, 2 * sizeof(unsigned long long));
+  const int64_t T = (int64_t)c->h_pinned[0], NF = (int64_t)c->h_pinned[1];
+  c->T = T;
+  c->NF = NF;
+  int32_t* tris = need(c->arena.get<int32_t>(3 * T));
+  c->fan_edge = need(c->arena.get<int64_t>(NF));
+  uint8_t* used = need(c->arena.get<uint8_t>(P + NF));
+  CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)(P + NF), s));
+  if (NF) CUDA_TRY(cudaMemsetAsync(used + P, 1, (size_t)NF, s));
+  launch_poly_emit(K_own, P, ekey, pid4, c->kase, toff, frank, epos, verts, tris, c->fan_edge, used, s);
+  check_launch(c);
+  if (c->keep) {
+    uint32_t* flag = need(c->arena.get<uint32_t>(K_own));
+    uint32_t* rank = need(c->arena.get<uint32_t>(K_own));
+    launch_interior_flags(K_own, c->kase, flag, s);
+    check_launch(c);
+    scan1(c, flag, rank, K_own, totals + 4);
+    readback(c, totals + 4, sizeof(unsigned long long));
+    c->n_interior = (int64_t)c->h_pinned[0];
+    c->split_cases = need(c->arena.get<int64_t>(c->n_interior));
+    launch_split_cases(K_own, c->kase, c->split_cases, rank, s);
+    check_launch(c);
+  }
+  c->prov_kind_in = c->prov_ref_in = nullptr;
+  if (win.slab) {  // offsets across slabs are assigned by the host (odc_slab_globalize)
+    c->slab_verts = verts;
+    c->slab_tris = tris;
+    c->P_own = P_end - P_halo;
+    mark(6);
+    mark(7);
+    c->V0 = c->V1 = 0;
+    st->raw_n_triangles = st->n_triangles = T;
+    finish_stats();
+    c->valid = true;
+    return;
+  }
+  // ---- unused-vertex removal + K8 repair (polygonize.py:199-209, :253-374)
+  mark(6);
+  finish_mesh(c, verts, P, NF, tris, T, used, o->repair != 0, st, dst, totals);
+  mark(7);
   finish_stats();
   c->valid = true;
 }
@@ -842,7 +927,115 @@ int odc_extract(odc_ctx* c, const odc_field* f, const double lo[3], const double
   cudaSetDevice(c->device);
   return guard(c, [](odc_ctx* cc, void* p) {
     ExtractArgs* x = (ExtractArgs*)p;
-    extract(cc, x->f, x->lo, x->hi, x->R, x->o, x->st);
+    extract(cc, x->f, x->lo, x->hi, x->R, x->o, x->st, Window{0, x->R, false});
+    return (int)ODC_OK;
+  }, &a);
+}
+
+struct SlabArgs {
+  const odc_field* f;
+  const double* lo;
+  const double* hi;
+  int64_t R, z0, z1;
+  const odc_options* o;
+  odc_stats* st;
+  odc_slab_info* info;
+};
+
+int odc_extract_slab(odc_ctx* c, const odc_field* f, const double lo[3], const double hi[3], int64_t R,
+                     const odc_options* o, int64_t cell_z0, int64_t cell_z1, odc_stats* st, odc_slab_info* info) {
+  if (!c || !f || !lo || !hi || !st || !info) return ODC_E_ARG;
+  odc_options def;
+  odc_default_options(&def);
+  SlabArgs a{f, lo, hi, R, cell_z0, cell_z1, o ? o : &def, st, info};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    SlabArgs* x = (SlabArgs*)p;
+    extract(cc, x->f, x->lo, x->hi, x->R, x->o, x->st, Window{x->z0, x->z1, true});
+    odc_slab_info& I = *x->info;
+    std::memset(&I, 0, sizeof I);
+    I.n_halo_partitions = cc->P_halo;
+    I.n_partitions = cc->P_own;
+    I.n_window_partitions = cc->P;
+    I.n_fans = cc->NF;
+    I.n_triangles = cc->T;
+    if (cc->K > 0) {
+      I.partition_vertices = cc->slab_verts + 3 * cc->P_halo;
+      I.fan_vertices = cc->slab_verts + 3 * cc->P;
+      I.triangles = cc->slab_tris;
+      I.partition_cell = cc->cells.part_cell + cc->P_halo;
+      I.partition_index = cc->cells.part_index + cc->P_halo;
+      I.fan_edge = cc->fan_edge;
+    }
+    return (int)ODC_OK;
+  }, &a);
+}
+
+int odc_slab_globalize(odc_ctx* c, int64_t part_base, int64_t n_partitions_total, int64_t fan_base,
+                       int32_t* triangles_out) {
+  if (!c || !c->valid || !c->slab_mode) return ODC_E_ARG;
+  if (c->T == 0) return ODC_OK;
+  if (!triangles_out) return ODC_E_ARG;
+  cudaSetDevice(c->device);
+  launch_globalize_tris(c->slab_tris, c->T, c->P_halo, c->P, part_base, n_partitions_total, fan_base, triangles_out,
+                        c->stream);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    c->err = "slab globalize failed";
+    return ODC_E_CUDA;
+  }
+  return ODC_OK;
+}
+
+struct FinishArgs {
+  const double* v;
+  int64_t V;
+  const int32_t* t;
+  int64_t T, P;
+  const int64_t* kind;
+  const int64_t* ref;
+  int32_t repair;
+  odc_stats* st;
+};
+
+int odc_mesh_finish(odc_ctx* c, const double* vertices, int64_t V, const int32_t* triangles, int64_t T,
+                    int64_t n_partitions, const int64_t* prov_kind, const int64_t* prov_ref, int32_t repair,
+                    odc_stats* st) {
+  if (!c || !st || V < n_partitions || (T && !triangles) || (V && !vertices)) return ODC_E_ARG;
+  FinishArgs a{vertices, V, triangles, T, n_partitions, prov_kind, prov_ref, repair, st};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    FinishArgs* x = (FinishArgs*)p;
+    cudaStream_t s = cc->stream;
+    std::memset(x->st, 0, sizeof *x->st);
+    for (int i = 0; i < ODC_N_CAT; i++) x->st->cat_order[i] = -1;
+    cc->valid = false;
+    cc->launches = 0;
+    cc->arena.reset();
+    cc->slab_mode = false;
+    DevStats* dst = need(cc->arena.get<DevStats>(1));
+    unsigned long long* totals = need(cc->arena.get<unsigned long long>(8));
+    CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(DevStats), s));
+    double* v = need(cc->arena.get<double>(3 * x->V));
+    int32_t* t = need(cc->arena.get<int32_t>(3 * x->T));
+    if (x->V) CUDA_TRY(cudaMemcpyAsync(v, x->v, sizeof(double) * 3 * x->V, cudaMemcpyDefault, s));
+    if (x->T) CUDA_TRY(cudaMemcpyAsync(t, x->t, sizeof(int32_t) * 3 * x->T, cudaMemcpyDefault, s));
+    cc->prov_kind_in = cc->prov_ref_in = nullptr;
+    if (x->kind && x->ref && x->V) {
+      cc->prov_kind_in = need(cc->arena.get<int64_t>(x->V));
+      cc->prov_ref_in = need(cc->arena.get<int64_t>(2 * x->V));
+      CUDA_TRY(cudaMemcpyAsync(cc->prov_kind_in, x->kind, 8 * x->V, cudaMemcpyDefault, s));
+      CUDA_TRY(cudaMemcpyAsync(cc->prov_ref_in, x->ref, 16 * x->V, cudaMemcpyDefault, s));
+    }
+    uint8_t* used = need(cc->arena.get<uint8_t>(x->V));
+    CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)x->V, s));
+    launch_mark_used(t, x->T, used, s);
+    check_launch(cc);
+    cc->T = x->T;
+    cc->P = x->P;
+    cc->K = 1;  // a mesh exists
+    finish_mesh(cc, v, x->P, x->V - x->P, t, x->T, used, x->repair != 0, x->st, dst, totals);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    cc->valid = true;
     return (int)ODC_OK;
   }, &a);
 }
@@ -881,7 +1074,11 @@ int odc_copy_mesh(odc_ctx* c, int32_t which, double* vertices, int64_t* triangle
     if ((x->kind || x->ref) && cc->V0) {
       int64_t* dk = need(cc->arena.get<int64_t>(cc->V0));
       int64_t* dr = need(cc->arena.get<int64_t>(2 * cc->V0));
-      launch_provenance(cc->V0, cc->P, cc->src0, cc->cells.part_cell, cc->cells.part_index, cc->fan_edge, dk, dr, s);
+      if (cc->prov_kind_in)
+        launch_gather_provenance(cc->V0, cc->src0, cc->prov_kind_in, cc->prov_ref_in, dk, dr, s);
+      else
+        launch_provenance(cc->V0, cc->P, cc->src0, cc->cells.part_cell, cc->cells.part_index, cc->fan_edge, dk, dr,
+                          s);
       kind.resize(cc->V0);
       ref.resize(2 * cc->V0);
       CUDA_TRY(cudaMemcpyAsync(kind.data(), dk, 8 * cc->V0, cudaMemcpyDeviceToHost, s));

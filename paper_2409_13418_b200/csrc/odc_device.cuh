@@ -20,10 +20,15 @@ constexpr int kMaxPointStack = 8;
 // position = lo + coord * h.  Bit-packed rows: a row is (y, z), W 32-bit words
 // cover x in [0, 32W); word index = (z*S + y)*W + x/32.
 // ---------------------------------------------------------------------------
+// z-window (slab mode): the device holds vertex layers
+// [z0, z0 + nz) of the global grid; ids, keys and positions stay global.
+// Edges/faces/vertices with base layer in [own0, own1) are owned by this
+// extraction (the full grid: z0 = 0, nz = S, own = [0, S)).
 struct GridP {
   int64_t R, S, S2, S3;
   int64_t W;   // words per row
-  int64_t NW;  // S*S*W
+  int64_t NW;  // nz*S*W words held
+  int64_t z0, nz, own0, own1;
   double lo[3], h[3];
 };
 
@@ -41,7 +46,7 @@ struct __align__(16) WordRec {
 static_assert(sizeof(WordRec) == 64, "WordRec must be one 64-byte record");
 
 __device__ __forceinline__ int64_t word_of(const GridP& g, int64_t x, int64_t y, int64_t z) {
-  return (z * g.S + y) * g.W + (x >> 5);
+  return ((z - g.z0) * g.S + y) * g.W + (x >> 5);
 }
 __device__ __forceinline__ void vid_coords(const GridP& g, int64_t vid, int64_t c[3]) {
   c[0] = vid % g.S;

@@ -33,10 +33,10 @@ __device__ __forceinline__ void atomic_max_nonneg_double(unsigned long long* a, 
 __global__ void __launch_bounds__(256) k_labels_analytic(GridP g, FieldP f, uint32_t* __restrict__ L) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t rowbits = g.W * 32;
-  const int64_t row = gid / rowbits;
-  if (row >= g.S * g.S) return;  // whole warps (rowbits is a multiple of 32)
+  const int64_t row = gid / rowbits;  // window-local row
+  if (row >= g.nz * g.S) return;      // whole warps (rowbits is a multiple of 32)
   const int64_t x = gid - row * rowbits;
-  const int64_t y = row % g.S, z = row / g.S;
+  const int64_t y = row % g.S, z = g.z0 + row / g.S;
   uint32_t lab = 0;
   if (x < g.S) {
     double p[3] = {gpos(g, 0, x), gpos(g, 1, y), gpos(g, 2, z)};
@@ -47,32 +47,32 @@ __global__ void __launch_bounds__(256) k_labels_analytic(GridP g, FieldP f, uint
 }
 
 void launch_labels_analytic(const GridP& g, const FieldP& f, uint32_t* L, cudaStream_t s) {
-  int64_t n = g.S * g.S * g.W * 32;
+  int64_t n = g.nz * g.S * g.W * 32;
   k_labels_analytic<<<grid_for(n, 256), 256, 0, s>>>(g, f, L);
 }
 
 __global__ void k_pack_labels(GridP g, const uint8_t* __restrict__ bytes, uint32_t* __restrict__ L) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t rowbits = g.W * 32;
-  const int64_t row = gid / rowbits;
-  if (row >= g.S * g.S) return;
+  const int64_t row = gid / rowbits;  // window-local row; bytes are window-local flat
+  if (row >= g.nz * g.S) return;
   const int64_t x = gid - row * rowbits;
   uint32_t lab = x < g.S ? (uint32_t)(bytes[row * g.S + x] != 0) : 0u;
   const uint32_t w = __ballot_sync(0xffffffffu, lab);
   if ((threadIdx.x & 31) == 0) L[row * g.W + (x >> 5)] = w;
 }
 void launch_pack_labels(const GridP& g, const uint8_t* bytes, uint32_t* L, cudaStream_t s) {
-  int64_t n = g.S * g.S * g.W * 32;
+  int64_t n = g.nz * g.S * g.W * 32;
   k_pack_labels<<<grid_for(n, 256), 256, 0, s>>>(g, bytes, L);
 }
 
 __global__ void k_unpack_labels(GridP g, const uint32_t* __restrict__ L, uint8_t* __restrict__ bytes) {
-  const int64_t vid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (vid >= g.S3) return;
-  bytes[vid] = (uint8_t)label_at(L, g, vid);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.nz * g.S2) return;
+  bytes[i] = (uint8_t)label_at(L, g, g.z0 * g.S2 + i);
 }
 void launch_unpack_labels(const GridP& g, const uint32_t* L, uint8_t* bytes, cudaStream_t s) {
-  k_unpack_labels<<<grid_for(g.S3, 256), 256, 0, s>>>(g, L, bytes);
+  k_unpack_labels<<<grid_for(g.nz * g.S2, 256), 256, 0, s>>>(g, L, bytes);
 }
 
 __global__ void k_grid_points(GridP g, int64_t begin, int64_t n, double* __restrict__ pts) {
@@ -112,10 +112,11 @@ struct ActiveBits {
 __device__ __forceinline__ ActiveBits compute_active(const GridP& g, const uint32_t* __restrict__ L, int64_t y,
                                                      int64_t z, int64_t wx) {
   const int64_t W = g.W, S = g.S, R = g.R;
-  const bool yin = y < R, zin = z < R;
+  const int64_t ztop = g.z0 + g.nz - 1;  // last layer held
+  const bool yin = y < R, zin = z < R && z < ztop;
   auto ld = [&](int64_t yy, int64_t zz, int64_t ww) -> uint32_t {
-    if (yy > R || zz > R || ww >= W) return 0u;
-    return L[(zz * S + yy) * W + ww];
+    if (yy > R || zz > ztop || ww >= W) return 0u;
+    return L[((zz - g.z0) * S + yy) * W + ww];
   };
   const uint32_t a00 = ld(y, z, wx), a10 = ld(y + 1, z, wx), a01 = ld(y, z + 1, wx), a11 = ld(y + 1, z + 1, wx);
   const uint32_t n00 = ld(y, z, wx + 1), n10 = ld(y + 1, z, wx + 1), n01 = ld(y, z + 1, wx + 1),
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kActiveBlock) k_active_bits(GridP g, const uin
   uint32_t shell = 0;
   if (idx < g.NW) {
     const int64_t row = idx / g.W, wx = idx - row * g.W;
-    const int64_t y = row % g.S, z = row / g.S;
+    const int64_t y = row % g.S, z = g.z0 + row / g.S;
     ActiveBits b = compute_active(g, L, y, z, wx);
     WordRec r;
     for (int a = 0; a < 3; a++) {
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kActiveBlock) k_active_bits(GridP g, const uin
     rec[idx] = r;
     active_counts(b, c);
     // boundary_inside_count (grid.py:102-106)
-    const uint32_t lab = L[idx] & bits_below(g.S, wx);
+    const uint32_t lab = (z >= g.own0 && z < g.own1) ? (L[idx] & bits_below(g.S, wx)) : 0u;
     if (y == 0 || y == g.R || z == 0 || z == g.R) {
       shell = __popc(lab);
     } else {
@@ -254,8 +255,8 @@ __global__ void __launch_bounds__(kActiveBlock) k_active_compact(GridP g, WordRe
   rec[idx].pq = pos[1];
   rec[idx].pc = pos[2];
   const int64_t row = idx / g.W, wx = idx - row * g.W;
-  const int64_t y = row % g.S, z = row / g.S;
-  const int64_t vbase = row * g.S + wx * 32;  // vertex id of bit 0 (x = 32 wx)
+  const int64_t y = row % g.S, z = g.z0 + row / g.S;
+  const int64_t vbase = (z * g.S + y) * g.S + wx * 32;  // global vertex id of bit 0 (x = 32 wx)
   // edges: ascending vertex, then axis (edge key = vid*3 + axis)
   uint32_t any = r.e[0] | r.e[1] | r.e[2];
   uint32_t pe = pos[0];
@@ -708,7 +709,7 @@ __global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, Op
                                                            const int64_t* __restrict__ inst_key, int64_t Q,
                                                            const double* __restrict__ pos1d, Stage2D out,
                                                            int64_t* __restrict__ inst_edges, DevStats* st,
-                                                           DevStatus* dst) {
+                                                           DevStatus* dst, int64_t st_lo, int64_t st_hi) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= Q) return;
   Inst2D I;
@@ -753,15 +754,16 @@ __global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, Op
   }
   if (out.status) out.status[q] = status;
   if (out.mid) out.mid[q] = (uint8_t)mid_label;
-  atomicAdd(&st->status[status], 1ull);
+  if (q >= st_lo && q < st_hi) atomicAdd(&st->status[status], 1ull);
 }
 
 void launch_search2d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
                               const WordRec* rec, const int64_t* inst_key, int64_t Q, const double* pos1d,
-                              Stage2D out, int64_t* inst_edges, DevStats* st, DevStatus* dst, cudaStream_t s) {
+                              Stage2D out, int64_t* inst_edges, DevStats* st, DevStatus* dst, int64_t st_lo,
+                              int64_t st_hi, cudaStream_t s) {
   if (Q)
     k_search2d_analytic<<<grid_for(Q, 128), 128, 0, s>>>(g, f, o, L, rec, inst_key, Q, pos1d, out, inst_edges, st,
-                                                         dst);
+                                                         dst, st_lo, st_hi);
 }
 
 // ---- lock-step 2D search (batched fields) --------------------------------
@@ -932,7 +934,8 @@ __global__ void k_s2_update(GridP g, OptP o, const uint32_t* __restrict__ L, con
 
 __global__ void k_s2_finish(GridP g, OptP o, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
                             const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
-                            const Search2DState* __restrict__ S, Stage2D out, DevStats* st) {
+                            const Search2DState* __restrict__ S, Stage2D out, DevStats* st, int64_t st_lo,
+                            int64_t st_hi) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= Q) return;
   Inst2D I;
@@ -961,7 +964,7 @@ __global__ void k_s2_finish(GridP g, OptP o, const uint32_t* __restrict__ L, con
   }
   if (out.status) out.status[q] = status;
   if (out.mid) out.mid[q] = s.mid_label;
-  atomicAdd(&st->status[status], 1ull);
+  if (q >= st_lo && q < st_hi) atomicAdd(&st->status[status], 1ull);
 }
 
 void launch_search2d_lockstep_init(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
@@ -986,10 +989,10 @@ void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32
 }
 void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
                                      const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,
-                                     Stage2D out, DevStats* st, cudaStream_t s) {
+                                     Stage2D out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s) {
   if (Q)
     k_s2_finish<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, rec, inst_key, Q, pos1d, (const Search2DState*)state, out,
-                                                 st);
+                                                 st, st_lo, st_hi);
 }
 
 // ===========================================================================
@@ -1029,7 +1032,7 @@ void launch_eval_raw_analytic(const FieldP& f, const double* pts, int64_t n, dou
 }
 __global__ void k_fd_normals(GridP g, double step, const uint32_t* __restrict__ L,
                              const int64_t* __restrict__ edge_key, int64_t K, const double* __restrict__ raw,
-                             double* __restrict__ nrm, DevStats* st) {
+                             double* __restrict__ nrm, DevStats* st, int64_t st_lo, int64_t st_hi) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   double gr[3], n[3];
@@ -1043,13 +1046,15 @@ __global__ void k_fd_normals(GridP g, double step, const uint32_t* __restrict__ 
   if (einsum3(n, e.span) < 0.0)
     for (int c = 0; c < 3; c++) n[c] = -n[c];
   for (int c = 0; c < 3; c++) nrm[3 * k + c] = n[c];
-  if (bad) atomicAdd(&st->normal_fallbacks, 1ull);
+  if (bad && k >= st_lo && k < st_hi) atomicAdd(&st->normal_fallbacks, 1ull);
 }
 void launch_fd_normals(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* edge_key, int64_t K,
-                       const double* raw, double* edge_normals, DevStats* st, cudaStream_t s) {
+                       const double* raw, double* edge_normals, DevStats* st, int64_t st_lo, int64_t st_hi,
+                       cudaStream_t s) {
   double hmin = g.h[0] < g.h[1] ? g.h[0] : g.h[1];
   hmin = hmin < g.h[2] ? hmin : g.h[2];
-  if (K) k_fd_normals<<<grid_for(K, 128), 128, 0, s>>>(g, o.fd_step * hmin, L, edge_key, K, raw, edge_normals, st);
+  if (K) k_fd_normals<<<grid_for(K, 128), 128, 0, s>>>(g, o.fd_step * hmin, L, edge_key, K, raw, edge_normals, st,
+                                                           st_lo, st_hi);
 }
 
 // ===========================================================================
@@ -1162,7 +1167,7 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
                                                     const uint32_t* __restrict__ samp_base,
                                                     const double* __restrict__ pos1d, const double* __restrict__ pos3,
                                                     const double* __restrict__ edge_normals, CellOut out,
-                                                    DevStats* st) {
+                                                    DevStats* st, int64_t st_lo, int64_t st_hi) {
   int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (ci >= C) return;
   const int64_t cell = cell_id[ci];
@@ -1284,20 +1289,22 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
     if (out.cyc_len) out.cyc_len[pid] = len;
     if (out.rank) out.rank[pid] = rank;
     if (out.resid) out.resid[pid] = res;
-    atomicAdd(&st->rank[rank], 1ull);
-    atomic_max_nonneg_double(&st->max_resid_bits, res);
+    if (ci >= st_lo && ci < st_hi) {
+      atomicAdd(&st->rank[rank], 1ull);
+      atomic_max_nonneg_double(&st->max_resid_bits, res);
+    }
     slot += len;
   }
-  if (nfb) atomicAdd(&st->normal_fallbacks, (unsigned long long)nfb);
+  if (nfb && ci >= st_lo && ci < st_hi) atomicAdd(&st->normal_fallbacks, (unsigned long long)nfb);
 }
 
 void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec, const int64_t* cell_id,
                        int64_t C, const CellTabEntry* table, const uint16_t* cfg, const uint32_t* part_base,
                        const uint32_t* samp_base, const double* pos1d, const double* pos3, const double* edge_normals,
-                       CellOut out, DevStats* st, cudaStream_t s) {
+                       CellOut out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s) {
   if (C)
     k_cell_solve<<<grid_for(C, 128), 128, 0, s>>>(g, o, L, rec, cell_id, C, table, cfg, part_base, samp_base, pos1d,
-                                                  pos3, edge_normals, out, st);
+                                                  pos3, edge_normals, out, st, st_lo, st_hi);
 }
 
 // generic multi-channel exclusive scan over u32 arrays (<= 2 channels)
@@ -1770,6 +1777,82 @@ __global__ void k_copy_vertices(const double* __restrict__ src, const int64_t* _
 void launch_copy_vertices(const double* src, const int64_t* src_of, int64_t base, int64_t n, double* dst,
                           cudaStream_t s) {
   if (n) k_copy_vertices<<<grid_for(n, 256), 256, 0, s>>>(src, src_of, base, n, dst);
+}
+
+// ===========================================================================
+// slab mode helpers
+// ===========================================================================
+__global__ void k_count_owned_faces(GridP g, const WordRec* __restrict__ rec, DevStats* st) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t nf = 0, n4 = 0;
+  if (idx < g.NW) {
+    const int64_t z = g.z0 + (idx / g.W) / g.S;
+    if (z >= g.own0 && z < g.own1) {
+      const WordRec& r = rec[idx];
+      for (int a = 0; a < 3; a++) {
+        nf += __popc(r.f[a]);
+        n4 += __popc(r.f4[a]);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    nf += __shfl_xor_sync(0xffffffffu, nf, o);
+    n4 += __shfl_xor_sync(0xffffffffu, n4, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (nf) atomicAdd(&st->faces_own, (unsigned long long)nf);
+    if (n4) atomicAdd(&st->faces4_own, (unsigned long long)n4);
+  }
+}
+void launch_count_owned_faces(const GridP& g, const WordRec* rec, DevStats* st, cudaStream_t s) {
+  k_count_owned_faces<<<grid_for(g.NW, 256), 256, 0, s>>>(g, rec, st);
+}
+
+// local ids: [0, P_halo) halo partitions (owned by the rank below, which
+// numbers them last), [P_halo, P_window) owned partitions, then fans
+__global__ void k_globalize_tris(const int32_t* __restrict__ tris, int64_t n, int64_t P_halo, int64_t P_window,
+                                 int64_t part_base, int64_t P_total, int64_t fan_base, int32_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t v = tris[i];
+  int64_t gv;
+  if (v < P_halo) gv = part_base - P_halo + v;
+  else if (v < P_window) gv = part_base + (v - P_halo);
+  else gv = P_total + fan_base + (v - P_window);
+  out[i] = (int32_t)gv;
+}
+void launch_globalize_tris(const int32_t* tris, int64_t T, int64_t P_halo, int64_t P_window, int64_t part_base,
+                           int64_t P_total, int64_t fan_base, int32_t* out, cudaStream_t s) {
+  if (T) k_globalize_tris<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, 3 * T, P_halo, P_window, part_base, P_total,
+                                                                fan_base, out);
+}
+__global__ void k_mark_used(const int32_t* __restrict__ tris, int64_t n, uint8_t* __restrict__ used) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) used[tris[i]] = 1;
+}
+void launch_mark_used(const int32_t* tris, int64_t T, uint8_t* used, cudaStream_t s) {
+  if (T) k_mark_used<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, 3 * T, used);
+}
+__global__ void k_widen_flags(const uint8_t* __restrict__ f, int64_t n, uint32_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = f[i] ? 1u : 0u;
+}
+void launch_widen_flags(const uint8_t* f, int64_t n, uint32_t* out, cudaStream_t s) {
+  if (n) k_widen_flags<<<grid_for(n, 256), 256, 0, s>>>(f, n, out);
+}
+__global__ void k_gather_provenance(int64_t V, const int64_t* __restrict__ src_of, const int64_t* __restrict__ kin,
+                                    const int64_t* __restrict__ rin, int64_t* __restrict__ kind,
+                                    int64_t* __restrict__ ref) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const int64_t s = src_of ? src_of[i] : i;
+  kind[i] = kin[s];
+  ref[2 * i] = rin[2 * s];
+  ref[2 * i + 1] = rin[2 * s + 1];
+}
+void launch_gather_provenance(int64_t V, const int64_t* src_of, const int64_t* kind_in, const int64_t* ref_in,
+                              int64_t* kind, int64_t* ref, cudaStream_t s) {
+  if (V) k_gather_provenance<<<grid_for(V, 256), 256, 0, s>>>(V, src_of, kind_in, ref_in, kind, ref);
 }
 
 __global__ void k_provenance(int64_t V, int64_t P, const int64_t* __restrict__ src_of,

@@ -24,6 +24,7 @@ struct DevStats {  // accumulated on the device, read back once
   unsigned long long used_partitions;
   unsigned long long repair_extra;
   unsigned long long repair_overflow;
+  unsigned long long faces_own, faces4_own;  // slab mode: faces with base layer owned
 };
 
 struct Stage2D {  // per-instance outputs of the 2D search
@@ -82,7 +83,8 @@ void launch_edge_endpoints(const GridP& g, const uint32_t* L, const int64_t* edg
 // K5: 2D points (dualize.py:97-129 + search.py:194-322)
 void launch_search2d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
                               const WordRec* rec, const int64_t* inst_key, int64_t Q, const double* pos1d,
-                              Stage2D out, int64_t* inst_edges, DevStats* st, DevStatus* dst, cudaStream_t s);
+                              Stage2D out, int64_t* inst_edges, DevStats* st, DevStatus* dst, int64_t st_lo,
+                              int64_t st_hi, cudaStream_t s);
 // lock-step form: 31 batches (1 midpoint + s1_lin + s1_bin + s2_lin + s2_bin)
 struct Search2DState;
 size_t search2d_state_bytes(int64_t Q);
@@ -97,14 +99,15 @@ void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32
                                      cudaStream_t s);
 void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
                                      const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,
-                                     Stage2D out, DevStats* st, cudaStream_t s);
+                                     Stage2D out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s);
 int search2d_num_steps(const OptP& o);
 
 // fd-gradient normals (pipeline.py:126-151): 6K raw samples
 void launch_fd_points(const GridP& g, const OptP& o, const double* pos1d, int64_t K, double* pts, cudaStream_t s);
 void launch_fd_raw_analytic(const FieldP& f, const double* pts, int64_t n, double* raw, cudaStream_t s);
 void launch_fd_normals(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* edge_key, int64_t K,
-                       const double* raw, double* edge_normals, DevStats* st, cudaStream_t s);
+                       const double* raw, double* edge_normals, DevStats* st, int64_t st_lo, int64_t st_hi,
+                       cudaStream_t s);
 
 // K6: per-cell partitions, plane samples, QEF (dualize.py:194-444)
 void launch_cell_config(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* cell_id, int64_t C,
@@ -126,7 +129,7 @@ struct CellOut {
 void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec, const int64_t* cell_id,
                        int64_t C, const CellTabEntry* table, const uint16_t* cfg, const uint32_t* part_base,
                        const uint32_t* samp_base, const double* pos1d, const double* pos3, const double* edge_normals,
-                       CellOut out, DevStats* st, cudaStream_t s);
+                       CellOut out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s);
 
 // K7: polygonization (polygonize.py:110-217)
 void launch_poly_classify(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
@@ -152,6 +155,15 @@ void launch_repair_apply(const double* verts, const int32_t* tris, int64_t V, co
                          cudaStream_t s);
 void launch_copy_vertices(const double* src, const int64_t* src_of, int64_t base, int64_t n, double* dst,
                           cudaStream_t s);
+
+// slab mode
+void launch_count_owned_faces(const GridP& g, const WordRec* rec, DevStats* st, cudaStream_t s);
+void launch_globalize_tris(const int32_t* tris, int64_t T, int64_t P_halo, int64_t P_window, int64_t part_base,
+                           int64_t P_total, int64_t fan_base, int32_t* out, cudaStream_t s);
+void launch_mark_used(const int32_t* tris, int64_t T, uint8_t* used, cudaStream_t s);
+void launch_widen_flags(const uint8_t* f, int64_t n, uint32_t* out, cudaStream_t s);
+void launch_gather_provenance(int64_t V, const int64_t* src_of, const int64_t* kind_in, const int64_t* ref_in,
+                              int64_t* kind, int64_t* ref, cudaStream_t s);
 
 // provenance (mesh.py:11-20)
 void launch_provenance(int64_t V, int64_t P, const int64_t* src_of, const int64_t* part_cell,

@@ -1,0 +1,316 @@
+"""z-slab multi-GPU extraction.
+
+The grid's cells are numbered z-major (grid.py:84-87), edges and faces by
+their lower vertex (grid.py:1-8), so the reference's global output order --
+partition vertices in (cell, cycle) order, fan vertices and triangles in
+edge-key order (polygonize.py:162-214) -- is exactly the concatenation of
+per-slab outputs in slab order.  Rank k owns cell layers [c_k, c_{k+1}) and
+the edges/faces whose lower vertex lies in those layers (the last rank also
+owns the top vertex layer).  It recomputes the halo cell layer c_k - 1
+(labels, searches, partitions and QEF are deterministic, hence identical to
+the owner's result) so it can polygonize its seam edges without exchanging
+any geometry.  The only collectives are
+
+  1. an all-gather of the per-rank counts (owned partitions, fan vertices,
+     triangles) from which every rank derives its global id offsets; a halo
+     partition j of rank k is global id  part_base_k - n_halo_k + j;
+  2. point-to-point sends of each rank's owned vertices / triangles /
+     provenance to rank 0 (NCCL over NVLink on the GPU path),
+
+after which rank 0 drops unreferenced vertices and runs the non-manifold
+repair on the assembled mesh (polygonize.py:199-209, :253-374; a seam
+vertex's fan spans two slabs).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .mesh import TriangleMesh
+
+STAT_KEYS = ("n_grid_vertices", "boundary_inside_vertices", "n_crossing_edges", "n_crossing_cells",
+             "n_face_center_probes", "n_2d_points", "n_partitions", "normal_fallbacks", "skipped_boundary_edges")
+
+
+def slab_ranges(R, world):
+    """Owned cell layers [c0, c1) of every rank (balanced split of R layers)."""
+    if world < 1 or world > R:
+        raise ValueError(f"cannot split {R} cell layers over {world} ranks")
+    b = [R * k // world for k in range(world + 1)]
+    return [(b[k], b[k + 1]) for k in range(world)]
+
+
+def global_offsets(counts, rank):
+    """counts: (world, 3) [n_partitions, n_fans, n_triangles] of every rank.
+    Returns (part_base, n_partitions_total, fan_base) of ``rank``."""
+    counts = np.asarray(counts, dtype=np.int64)
+    return int(counts[:rank, 0].sum()), int(counts[:, 0].sum()), int(counts[:rank, 1].sum())
+
+
+def globalize_ids(local, n_halo, n_window, part_base, n_total, fan_base):
+    """Host-side restatement of k_globalize_tris (odc_kernels.cu) for the
+    CPU (gloo) path and tests: local -> global vertex ids."""
+    local = np.asarray(local, dtype=np.int64)
+    out = np.where(local < n_halo, part_base - n_halo + local,
+                   np.where(local < n_window, part_base + (local - n_halo), n_total + fan_base + (local - n_window)))
+    return out
+
+
+@dataclass
+class SlabPiece:
+    """What one rank contributes (arrays are torch tensors on the rank's device)."""
+
+    n_halo: int
+    n_window: int
+    part_vertices: object   # (P, 3) f64
+    fan_vertices: object    # (NF, 3) f64
+    triangles: object       # (T, 3) int32 local ids
+    part_cell: object       # (P,) i64
+    part_index: object      # (P,) i64
+    fan_edge: object        # (NF,) i64
+    stats: np.ndarray       # STAT_KEYS + eval counts
+
+
+class _CudaArray:
+    """Zero-copy view of a libodc device buffer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _dev(torch, ptr, shape, typestr, device):
+    n = int(np.prod(shape))
+    dt = {"<f8": torch.float64, "<i4": torch.int32, "<i8": torch.int64}[typestr]
+    if n == 0 or not ptr:
+        return torch.zeros(shape, dtype=dt, device=device)
+    return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=device).clone()
+
+
+def extract_piece(field, grid, options, c0, c1, device=0):
+    """Run libodc's slab extraction for owned cell layers [c0, c1)."""
+    import torch
+
+    from .pipeline import DeviceField, _grid_args, _raise, make_options
+
+    ctx = _lib.context(device)
+    L = _lib.load()
+    st = _lib.Stats()
+    info = _lib.SlabInfo()
+    lo, hi, R = _grid_args(grid)
+    o = make_options(options)
+    with DeviceField(ctx, field) as df:
+        rc = L.odc_extract_slab(ctx.handle, df.handle, lo, hi, R, ctypes.byref(o), int(c0), int(c1), ctypes.byref(st),
+                                ctypes.byref(info))
+        if rc != _lib.ODC_OK:
+            _raise(rc, ctx)
+    dev = torch.device("cuda", device)
+    P, NF, T = info.n_partitions, info.n_fans, info.n_triangles
+    piece = SlabPiece(
+        n_halo=int(info.n_halo_partitions), n_window=int(info.n_window_partitions),
+        part_vertices=_dev(torch, info.partition_vertices, (P, 3), "<f8", dev),
+        fan_vertices=_dev(torch, info.fan_vertices, (NF, 3), "<f8", dev),
+        triangles=_dev(torch, info.triangles, (T, 3), "<i4", dev),
+        part_cell=_dev(torch, info.partition_cell, (P,), "<i8", dev),
+        part_index=_dev(torch, info.partition_index, (P,), "<i8", dev),
+        fan_edge=_dev(torch, info.fan_edge, (NF,), "<i8", dev),
+        stats=stats_vector(st),
+    )
+    return piece, ctx
+
+
+def stats_vector(st):
+    v = [getattr(st, k) for k in STAT_KEYS]
+    v += list(st.point2d_status_counts) + list(st.qef_rank_counts) + list(st.split_case_counts)
+    v += list(st.eval_batches) + list(st.eval_evals)
+    v.append(int(np.array([st.qef_max_residual]).view(np.int64)[0]))  # >= 0 doubles order like their bits
+    return np.asarray(v, dtype=np.int64)
+
+
+def stitch(piece, rank, world, dist, device):
+    """Collectives + assembly.  Returns the assembled arrays on rank 0
+    (vertices, triangles (global int32), kind, ref, n_partitions_total,
+    per-rank stats) and None elsewhere."""
+    import torch
+
+    P, NF, T = piece.part_vertices.shape[0], piece.fan_vertices.shape[0], piece.triangles.shape[0]
+    counts = torch.tensor([P, NF, T], dtype=torch.int64, device=device)
+    gathered = [torch.zeros_like(counts) for _ in range(world)]
+    dist.all_gather(gathered, counts)
+    allc = torch.stack(gathered).cpu().numpy()
+    part_base, P_tot, fan_base = global_offsets(allc, rank)
+    tris = globalize(piece, part_base, P_tot, fan_base, device)
+    sv = torch.as_tensor(piece.stats, device=device)
+    gst = [torch.zeros_like(sv) for _ in range(world)]
+    dist.all_gather(gst, sv)
+    payload = [piece.part_vertices.contiguous(), piece.fan_vertices.contiguous(), tris.contiguous(),
+               piece.part_cell.contiguous(), piece.part_index.contiguous(), piece.fan_edge.contiguous()]
+    if rank != 0:
+        for t in payload:
+            if t.numel():
+                dist.send(t, dst=0)
+        return None
+    parts = [[p] for p in payload]
+    for r in range(1, world):
+        Pr, NFr, Tr = (int(x) for x in allc[r])
+        bufs = [torch.empty((Pr, 3), dtype=torch.float64, device=device),
+                torch.empty((NFr, 3), dtype=torch.float64, device=device),
+                torch.empty((Tr, 3), dtype=torch.int32, device=device),
+                torch.empty((Pr,), dtype=torch.int64, device=device),
+                torch.empty((Pr,), dtype=torch.int64, device=device),
+                torch.empty((NFr,), dtype=torch.int64, device=device)]
+        for b in bufs:
+            if b.numel():
+                dist.recv(b, src=r)
+        for i, b in enumerate(bufs):
+            parts[i].append(b)
+    verts, tr, kind, ref = assemble([[p[r] for p in parts] for r in range(world)], device)
+    return verts, tr, kind, ref, P_tot, torch.stack(gst).cpu().numpy()
+
+
+def globalize(piece, part_base, P_tot, fan_base, device):
+    import torch
+
+    T = piece.triangles.shape[0]
+    out = torch.empty((T, 3), dtype=torch.int32, device=device)
+    if T == 0:
+        return out
+    if piece.triangles.is_cuda:
+        ctx = _lib.context(piece.triangles.device.index or 0)
+        rc = _lib.load().odc_slab_globalize(ctx.handle, part_base, P_tot, fan_base, out.data_ptr())
+        if rc != _lib.ODC_OK:
+            raise RuntimeError(_lib.load().odc_last_error(ctx.handle).decode())
+        return out
+    g = globalize_ids(piece.triangles.numpy(), piece.n_halo, piece.n_window, part_base, P_tot, fan_base)
+    return torch.as_tensor(g.astype(np.int32))
+
+
+def aggregate_stats(rows, options):
+    """Sum per-rank stats vectors into the reference's stats dict."""
+    from .pipeline import STATUS_NAMES
+
+    rows = np.asarray(rows)
+    nk = len(STAT_KEYS)
+    tot = rows[:, :nk].sum(axis=0)
+    d = dict(zip(STAT_KEYS, (int(x) for x in tot)))
+    status = rows[:, nk:nk + 4].sum(axis=0)
+    ranks = rows[:, nk + 4:nk + 8].sum(axis=0)
+    split = rows[:, nk + 8:nk + 12].sum(axis=0)
+    batches = rows[:, nk + 12:nk + 18].max(axis=0)
+    evals = rows[:, nk + 18:nk + 24].sum(axis=0)
+    resid = float(np.array([rows[:, nk + 24].max()], dtype=np.int64).view(np.float64)[0])
+    return d, status, ranks, split, batches, evals, resid
+
+
+def contour_slab(field, grid, options=None, *, rank, world, dist, device=0):
+    """One rank of a z-slab extraction over ``world`` ranks (one per GPU).
+    Returns the ContourResult on rank 0 and None on the other ranks."""
+    import torch
+
+    from .pipeline import ContourOptions, ContourResult, EvalCounter, _copy_mesh, _raise, _raw_from_repaired
+
+    options = options or ContourOptions()
+    options.validate()
+    t0 = time.perf_counter()
+    c0, c1 = slab_ranges(grid.resolution, world)[rank]
+    piece, ctx = extract_piece(field, grid, options, c0, c1, device)
+    out = stitch(piece, rank, world, dist, torch.device("cuda", device))
+    if out is None:
+        return None
+    verts, tris, kind, ref, P_tot, rows = out
+    L = _lib.load()
+    st = _lib.Stats()
+    rc = L.odc_mesh_finish(ctx.handle, verts.data_ptr(), verts.shape[0], tris.data_ptr(), tris.shape[0], P_tot,
+                           kind.data_ptr(), ref.data_ptr(), int(bool(options.repair)), ctypes.byref(st))
+    if rc != _lib.ODC_OK:
+        _raise(rc, ctx)
+    mesh = _copy_mesh(ctx, 0, st) if st.n_triangles else TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), np.int64))
+    raw = mesh if st.repair_added_vertices == 0 else _raw_from_repaired(ctx, mesh, st)
+    stats = slab_stats(rows, options, st)
+    counter = EvalCounter(field)
+    _, _, _, _, batches, evals, _ = aggregate_stats(rows, options)
+    for c, name in enumerate(_lib.CATEGORIES):
+        if evals[c] or (batches[c] and c == 0):
+            counter.record(name, int(batches[c]), int(evals[c]))
+    stats["wall_time_s"] = time.perf_counter() - t0
+    stats["eval_counts"] = counter.snapshot()
+    stats["slabs"] = world
+    return ContourResult(mesh, raw, counter, stats)
+
+
+def assemble(pieces_global, device):
+    """Concatenate per-rank (part_vertices, fan_vertices, triangles_global,
+    part_cell, part_index, fan_edge) in rank order: partitions of all ranks,
+    then fans of all ranks (the reference's vertex order)."""
+    import torch
+
+    pv, fv, tr, pc, pi, fe = (torch.cat([p[i] for p in pieces_global]) for i in range(6))
+    verts = torch.cat([pv, fv])
+    kind = torch.cat([torch.zeros(pv.shape[0], dtype=torch.int64, device=device),
+                      torch.ones(fv.shape[0], dtype=torch.int64, device=device)])
+    ref = torch.cat([torch.stack([pc, pi], dim=1), torch.stack([fe, torch.full_like(fe, -1)], dim=1)])
+    return verts, tr, kind, ref
+
+
+def contour_slabs_serial(field, grid, n_slabs, options=None, device=0):
+    """All slabs of an n-way decomposition run one after another on one GPU
+    (the same kernels and id arithmetic as the multi-GPU path, without the
+    collectives) and finished into one mesh -- used to check that slab
+    decomposition reproduces the single-extraction result exactly."""
+    import torch
+
+    from .pipeline import ContourOptions, _copy_mesh, _raise
+
+    options = options or ContourOptions()
+    dev = torch.device("cuda", device)
+    pieces = [extract_piece(field, grid, options, c0, c1, device)[0] for c0, c1 in slab_ranges(grid.resolution, n_slabs)]
+    counts = np.array([[p.part_vertices.shape[0], p.fan_vertices.shape[0], p.triangles.shape[0]] for p in pieces])
+    glob = []
+    for k, p in enumerate(pieces):
+        part_base, P_tot, fan_base = global_offsets(counts, k)
+        t = globalize_ids(p.triangles.cpu().numpy(), p.n_halo, p.n_window, part_base, P_tot, fan_base)
+        glob.append([p.part_vertices, p.fan_vertices, torch.as_tensor(t.astype(np.int32), device=dev), p.part_cell,
+                     p.part_index, p.fan_edge])
+    verts, tris, kind, ref = assemble(glob, dev)
+    ctx = _lib.context(device)
+    st = _lib.Stats()
+    rc = _lib.load().odc_mesh_finish(ctx.handle, verts.data_ptr(), verts.shape[0], tris.data_ptr(), tris.shape[0],
+                                     int(counts[:, 0].sum()), kind.data_ptr(), ref.data_ptr(),
+                                     int(bool(options.repair)), ctypes.byref(st))
+    if rc != _lib.ODC_OK:
+        _raise(rc, ctx)
+    return _copy_mesh(ctx, 0, st), pieces, np.stack([p.stats for p in pieces])
+
+
+def slab_stats(rows, options, st_finish):
+    from .pipeline import STATUS_NAMES
+
+    d, status, ranks, split, batches, evals, resid = aggregate_stats(rows, options)
+    stats = {"options": options, "warnings": []}
+    bi = d["boundary_inside_vertices"]
+    stats["boundary_inside_vertices"] = bi
+    if bi:
+        stats["warnings"].append(f"{bi} boundary grid vertices are inside; the output will have an open boundary")
+    stats["n_crossing_edges"] = d["n_crossing_edges"]
+    stats["n_crossing_cells"] = d["n_crossing_cells"]
+    if d["n_crossing_edges"] == 0:
+        stats["n_2d_points"] = 0
+        stats["open_boundary"] = False
+        return stats
+    stats["n_partitions"] = d["n_partitions"]
+    stats["n_2d_points"] = d["n_2d_points"]
+    if options.normals == "two-d-points":
+        stats["point2d_status_counts"] = {STATUS_NAMES[c]: int(status[c]) for c in range(4) if status[c]}
+    stats["normal_fallbacks"] = d["normal_fallbacks"]
+    stats["qef_rank_counts"] = {r: int(ranks[r]) for r in range(4) if ranks[r]}
+    stats["qef_max_residual"] = float(resid)
+    stats["split_case_counts"] = {c: int(split[c]) for c in range(1, 4) if split[c]}
+    stats["open_boundary"] = d["skipped_boundary_edges"] > 0
+    stats["skipped_boundary_edges"] = d["skipped_boundary_edges"]
+    stats["repair_added_vertices"] = int(st_finish.repair_added_vertices)
+    return stats
