@@ -8,9 +8,9 @@ A step is one full extraction (occmesh.pipeline.contour semantics) of the
 workload's grid.  ``value`` = grid cells (R^3) processed by all ranks per
 second with the field already resident on the device; ``e2e`` = the same
 through the public ``contour()`` call with the field uploaded from the host
-and the mesh (+ provenance) copied back every step.  Under torchrun every
-rank extracts its own full-size grid (replicas of the workload: per-GPU work
-is fixed, scaling "weak"); the step time is the max over ranks.
+and the mesh (+ provenance) copied back every step.  Under torchrun the
+grid is split into z-slabs, one per GPU (paper_2409_13418_b200.slab: total
+work fixed, scaling "strong"); the step time is the max over ranks.
 """
 
 from __future__ import annotations
@@ -41,6 +41,10 @@ def workload(name):
         R = int(name.split("_")[1])
         return MlpField(seed=0, amplitude=1.0), (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), R, \
             f"MlpField(seed=0, L=6 PE, 8x256 ReLU, He-normal bf16 weights, amplitude=1) at {R}^3 (config 3)"
+    if name.startswith("batch"):  # the reference arm samples shape 0 of the batch
+        n, R = (int(x) for x in name[len("batch"):].split("_"))
+        field, lo, hi = scenes.resolve(scenes.batch_shape(0), R)
+        return field, lo, hi, R, f"batch of {n} analytic shapes at {R}^3 (config 5); CPU arm: shape 0"
     scene, R = name.rsplit("_", 1)
     R = int(R)
     sc = scenes.thin_shell(R) if scene == "thin_shell" else scenes.SCENES[scene]
@@ -159,7 +163,7 @@ def run_reference(args, rank, world):
     value = float(np.mean(vals))
     line = {
         "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": R**3 / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": R**3 / value * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32+f64" if is_mlp(field) else "f64", "data": "synthetic",
         "config": {"workload": desc, "R": R, "cells": R**3},
         "impl": "reference",
@@ -308,7 +312,7 @@ def run_gpu(args, rank, world, dist):
                    "labels_kernel"]
     line = {
         "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16+f64" if is_mlp(field) else "f64", "data": "synthetic",
         "config": {"workload": desc, "R": R, "cells": R**3, "parallelism": f"replicas x{world}",
                    "l2": "flushed (512 MiB write) before every step, outside its CUDA-event pair",
@@ -327,6 +331,168 @@ def run_gpu(args, rank, world, dist):
     print(json.dumps(line), flush=True)
 
 
+def run_gpu_batch(args, rank, world, dist):
+    """Config 5: 64 analytic shapes at 256^3 extracted concurrently (worker
+    threads, one libodc context + stream each).  value = cells of all grids /
+    wall time between device-wide synchronizations (fields resident);
+    e2e = the same through contour_batch (field upload + mesh copy-back)."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
+    from paper_2409_13418_b200 import GridSpec, _lib, scenes
+    from paper_2409_13418_b200.batch import contour_batch
+    from paper_2409_13418_b200.pipeline import ContourOptions, DeviceField, make_options
+
+    device = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(device)
+    n, R = (int(x) for x in args.workload[len("batch"):].split("_"))
+    shapes = scenes.batch_shapes(n)
+    jobs = []
+    for sc in shapes:
+        f, lo, hi = scenes.resolve(sc, R)
+        jobs.append((f, GridSpec(lo, hi, R)))
+    mine = jobs[rank::world]
+    workers = args.batch_workers
+    L = _lib.load()
+    opts = make_options(ContourOptions())
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
+
+    def worker(idx):
+        ctx = _lib.context(device)
+        out = []
+        for j in idx:
+            f, g = mine[j]
+            with DeviceField(ctx, f) as df:
+                st = _lib.Stats()
+                lo = (C.c_double * 3)(*g.lo)
+                hi = (C.c_double * 3)(*g.hi)
+                rc = L.odc_extract(ctx.handle, df.handle, lo, hi, R, C.byref(opts), C.byref(st))
+                if rc:
+                    raise RuntimeError(L.odc_last_error(ctx.handle).decode())
+                out.append(st.n_kernel_launches)
+        return out
+
+    parts = [list(range(w, len(mine), workers)) for w in range(workers)]
+
+    def run_all():
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            return sum(sum(x) for x in pool.map(worker, parts))
+
+    for _ in range(args.warmup):
+        run_all()
+    times, launches = [], 0
+    with ClockSampler(device) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            launches += run_all()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+    clock = clocks.summary()
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = contour_batch(mine, workers=workers, device=device)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e.append(t1 - t0)
+    step = float(np.mean(times))
+    e2e_step = float(np.mean(e2e))
+    if dist is not None:
+        t = torch.tensor([step, e2e_step], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step, e2e_step = (float(x) for x in t.tolist())
+    if rank != 0:
+        return
+    cells = n * R**3
+    d2h = sum(r.mesh.n_vertices * 48 + r.mesh.n_triangles * 12 for r in res)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        f, g = jobs[0]
+        v, t_full, cores, sample, dt = cpu_sample(f, g.lo, g.hi, R, None, args.cpu_sample_r)
+        cpu = {"value": v, "unit": "cells/s", "cores": cores, "kind": "port",
+               "sample": sample + " (shape 0 of the batch; per-shape throughput)"}
+    line = {
+        "metric": METRIC, "value": cells / step, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"batch of {n} analytic shapes (scenes.batch_shapes) at {R}^3 (config 5)", "R": R,
+                   "cells": cells, "parallelism": f"{workers} concurrent contexts/streams per GPU x{world}",
+                   "l2": "flushed before every step; step timed between device-wide synchronizations"},
+        "e2e": {"value": cells / e2e_step, "unit": "cells/s", "ms_per_step": e2e_step * 1e3,
+                "h2d_bytes_per_step": None, "d2h_bytes_per_step": int(d2h),
+                "api": "paper_2409_13418_b200.batch.contour_batch(jobs) -> [ContourResult]"},
+        "roofline": None, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clock,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu_slabs(args, rank, world, dist):
+    """N > 1: the workload's grid is split into N z-slabs, one per GPU
+    (paper_2409_13418_b200.slab): total work fixed (strong scaling); the step
+    covers the slab extraction, the count all-gather, the NCCL gather of
+    every slab's vertices/triangles to rank 0 and the finish (unused-vertex
+    removal + repair) there.  Time = max over ranks of CUDA-event time."""
+    import torch
+
+    from paper_2409_13418_b200 import GridSpec
+    from paper_2409_13418_b200.fields import is_mlp
+    from paper_2409_13418_b200.slab import contour_slab, slab_ranges
+
+    device = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(device)
+    field, lo, hi, R, desc = workload(args.workload)
+    grid = GridSpec(lo, hi, R)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
+
+    def timed(n, to_host):
+        ms = []
+        for _ in range(n):
+            flush.zero_()
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            contour_slab(field, grid, rank=rank, world=world, dist=dist, device=device, to_host=to_host)
+            torch.cuda.synchronize()
+            e1.record()
+            e1.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{device}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms.append(float(t.item()))
+        return ms
+
+    timed(args.warmup, False)
+    with ClockSampler(device) as clocks:
+        dev_ms = timed(args.steps, False)
+    clock = clocks.summary()
+    timed(args.warmup, True)
+    e2e_ms = timed(args.steps, True)
+    ms_step = float(np.mean(dev_ms))
+    e2e_step = float(np.mean(e2e_ms))
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": R**3 / (ms_step / 1e3), "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16+f64" if is_mlp(field) else "f64", "data": "synthetic",
+        "config": {"workload": desc, "R": R, "cells": R**3, "parallelism": f"z-slabs x{world}",
+                   "slabs": slab_ranges(R, world),
+                   "l2": "flushed (512 MiB write) before every step, outside its CUDA-event pair"},
+        "e2e": {"value": R**3 / (e2e_step / 1e3), "unit": "cells/s", "ms_per_step": e2e_step,
+                "api": "paper_2409_13418_b200.slab.contour_slab(field, GridSpec, rank, world) -> TriangleMesh on rank 0",
+                "h2d_bytes_per_step": None, "d2h_bytes_per_step": None},
+        "roofline": None, "cpu_baseline": None, "gpu_launches": None, "clocks": clock,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -337,6 +503,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-r", type=int, default=None)
     ap.add_argument("--full-evals", type=int, default=None)
+    ap.add_argument("--batch-workers", type=int, default=8)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -350,6 +517,10 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)
+        elif args.workload.startswith("batch"):
+            run_gpu_batch(args, rank, world, dist)
+        elif world > 1:
+            run_gpu_slabs(args, rank, world, dist)
         else:
             run_gpu(args, rank, world, dist)
     finally:

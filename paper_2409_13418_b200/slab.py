@@ -207,9 +207,11 @@ def aggregate_stats(rows, options):
     return d, status, ranks, split, batches, evals, resid
 
 
-def contour_slab(field, grid, options=None, *, rank, world, dist, device=0):
+def contour_slab(field, grid, options=None, *, rank, world, dist, device=0, to_host=True):
     """One rank of a z-slab extraction over ``world`` ranks (one per GPU).
-    Returns the ContourResult on rank 0 and None on the other ranks."""
+    Returns the ContourResult on rank 0 and None on the other ranks; with
+    ``to_host=False`` the finished mesh stays on rank 0's device (read it with
+    odc_mesh_device) and only the stats are returned."""
     import torch
 
     from .pipeline import ContourOptions, ContourResult, EvalCounter, _copy_mesh, _raise, _raw_from_repaired
@@ -229,6 +231,8 @@ def contour_slab(field, grid, options=None, *, rank, world, dist, device=0):
                            kind.data_ptr(), ref.data_ptr(), int(bool(options.repair)), ctypes.byref(st))
     if rc != _lib.ODC_OK:
         _raise(rc, ctx)
+    if not to_host:
+        return st
     mesh = _copy_mesh(ctx, 0, st) if st.n_triangles else TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), np.int64))
     raw = mesh if st.repair_added_vertices == 0 else _raw_from_repaired(ctx, mesh, st)
     stats = slab_stats(rows, options, st)
