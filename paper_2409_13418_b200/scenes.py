@@ -70,11 +70,11 @@ def batch_shape(s):
 
     def prim(k):
         if k == "sphere":
-            r = float(rng.uniform(0.12, 0.3).round(6))
+            r = round(float(rng.uniform(0.12, 0.3)), 6)
             return {"type": "sphere", "center": center(r), "radius": r}
         if k == "torus":
-            R_ = float(rng.uniform(0.14, 0.22).round(6))
-            r_ = float(rng.uniform(0.04, 0.1).round(6))
+            R_ = round(float(rng.uniform(0.14, 0.22)), 6)
+            r_ = round(float(rng.uniform(0.04, 0.1)), 6)
             return {"type": "torus", "center": center(R_ + r_), "major_radius": R_, "minor_radius": r_}
         half = rng.uniform(0.08, 0.2, size=3).round(6)
         ang = rng.uniform(0, 60, size=3).round(3).tolist()
