@@ -93,6 +93,7 @@ struct odc_field {
   // MLP
   uint16_t* w_packed = nullptr;
   uint16_t* w_tc = nullptr;
+  uint16_t* w_tc2 = nullptr;
   float* bias = nullptr;
   float* w_head = nullptr;
   MlpDev mlp{};
@@ -802,7 +803,7 @@ const char* odc_last_error(const odc_ctx* c) { return c ? c->err.c_str() : "null
 
 int odc_set_param(odc_ctx* c, const char* name, int64_t value) {
   if (!c || !name) return ODC_E_ARG;
-  if (std::strcmp(name, "mlp_impl") == 0 && (value == 0 || value == 1)) {
+  if (std::strcmp(name, "mlp_impl") == 0 && value >= 0 && value <= 2) {
     c->mlp_impl = (int)value;
     return ODC_OK;
   }
@@ -870,8 +871,12 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
   const size_t nt = mlp_tc_weight_elems();
   std::vector<uint16_t> packed_tc(nt);
   mlp_pack_weights_tc(d->w0, d->d_in, d->w_hidden, packed_tc.data());
+  const size_t nt2 = mlp_tc2_weight_elems();
+  std::vector<uint16_t> packed_tc2(nt2);
+  mlp_pack_weights_tc2(d->w0, d->d_in, d->w_hidden, packed_tc2.data());
   mlp_pack_weights(d->w0, d->d_in, d->w_hidden, packed.data());
   if (cudaMalloc(&f->w_packed, ne * 2) != cudaSuccess || cudaMalloc(&f->w_tc, nt * 2) != cudaSuccess ||
+      cudaMalloc(&f->w_tc2, nt2 * 2) != cudaSuccess ||
       cudaMalloc(&f->bias, 8 * 256 * 4) != cudaSuccess ||
       cudaMalloc(&f->w_head, 256 * 4) != cudaSuccess) {
     c->err = "field upload failed";
@@ -880,10 +885,12 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
   }
   cudaMemcpy(f->w_packed, packed.data(), ne * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(f->w_tc, packed_tc.data(), nt * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(f->w_tc2, packed_tc2.data(), nt2 * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(f->bias, d->biases, 8 * 256 * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(f->w_head, d->w_head, 256 * 4, cudaMemcpyHostToDevice);
   f->mlp.w_packed = f->w_packed;
   f->mlp.w_tc = f->w_tc;
+  f->mlp.w_tc2 = f->w_tc2;
   f->mlp.has_bias = 0;
   for (int i = 0; i < 8 * 256; i++)
     if (d->biases[i] != 0.f) f->mlp.has_bias = 1;
@@ -904,6 +911,7 @@ void odc_field_free(odc_ctx* c, odc_field* f) {
   cudaFree(f->nodes);
   cudaFree(f->w_packed);
   cudaFree(f->w_tc);
+  cudaFree(f->w_tc2);
   cudaFree(f->bias);
   cudaFree(f->w_head);
   delete f;

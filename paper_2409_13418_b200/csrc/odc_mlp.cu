@@ -9,6 +9,7 @@
 
 #include "odc_mlp.h"
 #include "odc_mlp_tc.cuh"
+#include "odc_mlp_tc2.cuh"
 
 namespace odc {
 
@@ -391,8 +392,255 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ===========================================================================
+// CTA-pair tcgen05 evaluator (see odc_mlp_tc2.cuh)
+// ===========================================================================
+size_t mlp_tc2_weight_elems() { return (size_t)tc::kChunksPerPair * 2 * 64 * 64; }
+
+// chunk c = (l, nh, kc) in consumption order; half r holds B rows
+// n = 128 nh + 64 r + i, k = 64 kc + j in the SWIZZLE_128B K-major image
+void mlp_pack_weights_tc2(const float* w0, int d_in, const float* w_hidden, uint16_t* out) {
+  size_t ci = 0;
+  for (int l = 0; l < kDepth; l++) {
+    const int nkc = l == 0 ? 1 : 4;
+    for (int nh = 0; nh < 2; nh++)
+      for (int kc = 0; kc < nkc; kc++, ci++)
+        for (int r = 0; r < 2; r++) {
+          uint16_t* img = out + (ci * 2 + r) * 64 * 64;
+          for (int i = 0; i < 64; i++)
+            for (int j = 0; j < 64; j++) {
+              const int n = 128 * nh + 64 * r + i, k = 64 * kc + j;
+              float v;
+              if (l == 0) v = k < d_in ? w0[(size_t)k * kWidth + n] : 0.f;
+              else v = w_hidden[((size_t)(l - 1) * kWidth + k) * kWidth + n];
+              const size_t byte = (size_t)((i >> 3) * 1024 + (i & 7) * 128 + (((j >> 3) ^ (i & 7)) << 4) + (j & 7) * 2);
+              img[byte / 2] = f2bf(v);
+            }
+        }
+  }
+}
+
+template <bool kBias>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
+    k_mlp_tc2(MlpDev m, PointSrc src, int64_t n, uint8_t* __restrict__ labels, double* __restrict__ raw) {
+  using namespace tc;
+  using namespace tc2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* Wst = smem;
+  uint64_t* bars = (uint64_t*)(Wst + tc2::kStages * kHalfChunkBytes);
+  uint64_t* full = bars;                         // [kStages] local weight half landed
+  uint64_t* empty = full + tc2::kStages;         // [kStages] stage consumed (commit, both CTAs)
+  uint64_t* fullp = empty + tc2::kStages;        // [kStages] leader: peer half landed (relay)
+  uint64_t* acc_full = fullp + tc2::kStages;     // [2] accumulator half ready (commit, both CTAs)
+  uint64_t* a_ready = acc_full + 2;              // [2] leader: A half written (8 warps: 4 per CTA)
+  uint64_t* pe_ready = a_ready + 2;              // leader: next tile's encoding written (4 nh0 warps x 2)
+  uint64_t* pe_free = pe_ready + 1;              // layer 6 done: A buffer 0 may take the next encoding
+  uint32_t* tmem_slot = (uint32_t*)(pe_free + 1);
+  float* s_bias = (float*)(bars + 128);           // (8, 256)
+  float* s_head = s_bias + kDepth * kWidth;       // (256)
+  float* s_part = s_head + kWidth;                // (128) head partial sums of columns 128..255
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int64_t ntiles = (n + 255) / 256;
+  const int64_t cluster_id = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < tc2::kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&fullp[s], 1);
+    }
+    mbar_init(&acc_full[0], 1);
+    mbar_init(&acc_full[1], 1);
+    mbar_init(&a_ready[0], 8);
+    mbar_init(&a_ready[1], 8);
+    mbar_init(pe_ready, 8);
+    mbar_init(pe_free, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < kDepth * kWidth; i += blockDim.x) s_bias[i] = m.bias[i];
+  for (int i = threadIdx.x; i < kWidth; i += blockDim.x) s_head[i] = m.w_head[i];
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- weight producer (own half)
+      uint32_t g = 0;
+      for (int64_t t = cluster_id; t < ntiles; t += nclusters)
+        for (int i = 0; i < kChunksPerPair; i++, g++) {
+          const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], kHalfChunkBytes);
+          bulk_g2s(Wst + s * kHalfChunkBytes, m.w_tc2 + ((size_t)i * 2 + crank) * 64 * 64, kHalfChunkBytes, &full[s]);
+        }
+    }
+  } else if (warp == 3) {
+    if (lane == 0 && !leader) {  // ---- relay: peer half landed -> leader's fullp[s]
+      uint32_t g = 0;
+      for (int64_t t = cluster_id; t < ntiles; t += nclusters)
+        for (int i = 0; i < kChunksPerPair; i++, g++) {
+          const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
+          mbar_wait(&full[s], ph);
+          mbar_arrive_cluster(mapa(smem_u32(&fullp[s]), 0));
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---- MMA issuer
+      uint32_t g = 0, ra0 = 0, ra1 = 0, rpe = 0;
+      bool first = true;
+      for (int64_t t = cluster_id; t < ntiles; t += nclusters) {
+        for (int l = 0; l < kDepth; l++) {
+          const int nkc = l == 0 ? 1 : 4;
+          const uint32_t a_buf = tmem + 256 + (l & 1) * 128;
+          for (int nh = 0; nh < 2; nh++) {
+            for (int kc = 0; kc < nkc; kc++, g++) {
+              if (l == 0 && nh == 0) {  // encoding of this tile written (A buffer 0, D half 0 drained)
+                mbar_wait(pe_ready, rpe & 1);
+                rpe++;
+                tc_fence_after();
+              }
+              if (l == 0 && nh == 1 && !first) {  // D half 1 drained by the previous tile's layer 7
+                mbar_wait(&a_ready[1], ra1 & 1);
+                ra1++;
+                tc_fence_after();
+              }
+              if (l > 0 && nh == 0 && kc == 0) {
+                mbar_wait(&a_ready[0], ra0 & 1);
+                ra0++;
+                tc_fence_after();
+              }
+              if (l > 0 && nh == 0 && kc == 2) {
+                mbar_wait(&a_ready[1], ra1 & 1);
+                ra1++;
+                tc_fence_after();
+              }
+              const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
+              mbar_wait(&full[s], ph);
+              mbar_wait(&fullp[s], ph);
+              tc_fence_after();
+              const uint32_t b_base = smem_u32(Wst + s * kHalfChunkBytes);
+              const uint32_t d = tmem + nh * 128;
+#pragma unroll
+              for (int ks = 0; ks < 4; ks++)
+                umma_ts(d, a_buf + kc * 32 + ks * 8, sw128_desc(b_base + ks * 32), (kc | ks) != 0);
+              umma_commit_pair(&empty[s]);
+            }
+            umma_commit_pair(&acc_full[nh]);
+            if (l == kDepth - 2 && nh == 1) umma_commit_pair(pe_free);
+          }
+        }
+        first = false;
+      }
+    }
+  } else if (warp >= 4) {  // ---- epilogue
+    const int half = (warp - 4) >> 2;  // 0: columns 0..127, 1: columns 128..255
+    const int q = warp & 3;
+    const int r = 32 * q + lane;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    const uint32_t dcol = tmem + lane_base + half * 128;
+    const uint32_t leader_a_ready = mapa(smem_u32(&a_ready[half]), 0);
+    const uint32_t leader_pe_ready = mapa(smem_u32(pe_ready), 0);
+    uint32_t af = 0, pf = 0;
+    uint32_t pe[32];
+    const int64_t t0 = cluster_id;
+    if (half == 0 && t0 < ntiles) {
+      pe_row_packed(src, n, t0 * 256 + crank * 128 + r, pe);
+      ODC_TMEM_ST32(tmem + lane_base + 256, pe);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_pe_ready);
+    }
+    for (int64_t t = t0; t < ntiles; t += nclusters) {
+      const int64_t next = t + nclusters;
+      float dot = 0.f;
+      for (int l = 0; l < kDepth; l++) {
+        const float* bl = s_bias + l * kWidth + half * 128;
+        if (half == 0 && l == kDepth - 1 && next < ntiles) pe_row_packed(src, n, next * 256 + crank * 128 + r, pe);
+        mbar_wait(&acc_full[half], af & 1);
+        af++;
+        tc_fence_after();
+        if (l < kDepth - 1) {
+          const uint32_t a_out = tmem + lane_base + 256 + ((l + 1) & 1) * 128 + half * 64;
+#pragma unroll
+          for (int i = 0; i < 4; i += 2) {
+            uint32_t v0[32], v1[32], w[32];
+            ODC_TMEM_LD32(dcol + 32 * i, v0);
+            ODC_TMEM_LD32(dcol + 32 * i + 32, v1);
+            tmem_ld_wait();
+            relu_pack32<kBias>(v0, bl + 32 * i, w);
+            relu_pack32<kBias>(v1, bl + 32 * i + 32, w + 16);
+            ODC_TMEM_ST32(a_out + 16 * i, w);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_a_ready);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            uint32_t v[32];
+            ODC_TMEM_LD32(dcol + 32 * i, v);
+            tmem_ld_wait();
+            dot = head32<kBias>(v, bl + 32 * i, s_head + half * 128 + 32 * i, dot);
+          }
+          if (half == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader_a_ready);  // D half 1 drained
+            s_part[r] = dot;
+          } else if (next < ntiles) {
+            mbar_wait(pe_free, pf & 1);  // layer 6's MMAs (readers of A buffer 0) are done
+            pf++;
+            tc_fence_after();
+            ODC_TMEM_ST32(tmem + lane_base + 256, pe);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader_pe_ready);
+          }
+        }
+      }
+      if (half == 0 && next >= ntiles) {  // keep pe_free's phase in step on the last tile
+        mbar_wait(pe_free, pf & 1);
+        pf++;
+      }
+      named_bar_sync(1, 256);  // head partials of columns 128..255 visible
+      if (half == 0) {
+        dot += s_part[r];
+        const int64_t p = t * 256 + crank * 128 + r;
+        if (p < n) {
+          const double mlp = (double)(dot + m.b_head);
+          double pt[3];
+          point_of(src, p, pt);
+          const double d[3] = {pt[0] - m.prior_center[0], pt[1] - m.prior_center[1], pt[2] - m.prior_center[2]};
+          const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+          const double logit = m.amplitude * mlp - m.prior_scale * (dist - m.prior_radius);
+          const double rv = 1.0 / (1.0 + exp(-logit));
+          labels[p] = rv > 0.5 ? 1 : 0;
+          if (raw) raw[p] = rv;
+        }
+      }
+      named_bar_sync(1, 256);  // s_part reusable
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 static int g_num_sms = 0;
 
+// impl: 0 = CTA-pair tcgen05 (default), 1 = SIMT reference, 2 = single-CTA tcgen05
 int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s) {
   if (n <= 0) return 0;
   if (m.impl == 1 || m.w_tc == nullptr) {
@@ -404,13 +652,23 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
   if (!attr) {
     cudaFuncSetAttribute(k_mlp_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+    cudaFuncSetAttribute(k_mlp_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc2::kSmemBytes);
+    cudaFuncSetAttribute(k_mlp_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc2::kSmemBytes);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     attr = true;
   }
-  const int64_t npairs = (n + 255) / 256;
-  const int64_t grid = npairs < g_num_sms ? npairs : g_num_sms;
+  const int64_t ntiles = (n + 255) / 256;
+  if (m.impl == 0 && m.w_tc2 != nullptr) {
+    const int64_t pairs = (g_num_sms / 2) < ntiles ? (g_num_sms / 2) : ntiles;
+    if (m.has_bias)
+      k_mlp_tc2<true><<<(unsigned)(2 * pairs), tc2::kThreads, tc2::kSmemBytes, s>>>(m, src, n, labels, raw);
+    else
+      k_mlp_tc2<false><<<(unsigned)(2 * pairs), tc2::kThreads, tc2::kSmemBytes, s>>>(m, src, n, labels, raw);
+    return 0;
+  }
+  const int64_t grid = ntiles < g_num_sms ? ntiles : g_num_sms;
   if (m.has_bias)
     k_mlp_tc<true><<<(unsigned)grid, tc::kThreads, tc::kSmemBytes, s>>>(m, src, n, labels, raw);
   else
@@ -418,6 +676,6 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
   return 0;
 }
 
-const char* mlp_kernel_name() { return "k_mlp_tc"; }
+const char* mlp_kernel_name() { return "k_mlp_tc2"; }
 
 }  // namespace odc

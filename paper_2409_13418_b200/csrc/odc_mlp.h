@@ -20,7 +20,8 @@ namespace odc {
 struct MlpDev {
   const uint16_t* w_packed;  // row-major bf16 W[k][n] per layer (layer 0 padded to K=64): SIMT evaluator
   const uint16_t* w_tc;      // 58 chunks of 128x64 bf16 in the UMMA SWIZZLE_128B smem image (odc_mlp_tc.cuh)
-  int impl;                  // 0 = tcgen05 (default), 1 = SIMT reference evaluator
+  const uint16_t* w_tc2;     // the same chunks split into two 64-row halves (odc_mlp_tc2.cuh)
+  int impl;                  // 0 = CTA-pair tcgen05 (default), 1 = SIMT reference, 2 = single-CTA tcgen05
   int has_bias;              // any non-zero bias (selects the bias-add epilogue)
   const float* bias;         // (8, 256)
   const float* w_head;       // (256)
@@ -39,6 +40,8 @@ struct PointSrc {
 size_t mlp_packed_weight_elems();
 size_t mlp_tc_weight_elems();
 void mlp_pack_weights_tc(const float* w0, int d_in, const float* w_hidden, uint16_t* out);
+size_t mlp_tc2_weight_elems();
+void mlp_pack_weights_tc2(const float* w0, int d_in, const float* w_hidden, uint16_t* out);
 // host: pack float32 weights (already bf16-representable) into the device layout
 void mlp_pack_weights(const float* w0, int d_in, const float* w_hidden, uint16_t* out);
 
