@@ -395,18 +395,19 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
 // ===========================================================================
 // CTA-pair tcgen05 evaluator (see odc_mlp_tc2.cuh)
 // ===========================================================================
-size_t mlp_tc2_weight_elems() { return (size_t)tc::kChunksPerPair * 2 * 64 * 64; }
+size_t mlp_tc2_weight_elems() { return (size_t)tc2::kStagesPerTile * 2 * tc2::kStageBytes / 2; }
 
-// chunk c = (l, nh, kc) in consumption order; half r holds B rows
-// n = 128 nh + 64 r + i, k = 64 kc + j in the SWIZZLE_128B K-major image
+// stage (l, nh) in consumption order; CTA half r holds B rows
+// n = 128 nh + 64 r + i, k = 64 kc + j: K-atom kc (8 KB SWIZZLE_128B K-major
+// image) at byte 8192 kc of the half's 32 KB slot (layer 0: one atom)
 void mlp_pack_weights_tc2(const float* w0, int d_in, const float* w_hidden, uint16_t* out) {
-  size_t ci = 0;
+  std::memset(out, 0, mlp_tc2_weight_elems() * 2);
   for (int l = 0; l < kDepth; l++) {
     const int nkc = l == 0 ? 1 : 4;
     for (int nh = 0; nh < 2; nh++)
-      for (int kc = 0; kc < nkc; kc++, ci++)
+      for (int kc = 0; kc < nkc; kc++)
         for (int r = 0; r < 2; r++) {
-          uint16_t* img = out + (ci * 2 + r) * 64 * 64;
+          uint16_t* img = out + ((size_t)((l * 2 + nh) * 2 + r) * tc2::kStageBytes + kc * 8192) / 2;
           for (int i = 0; i < 64; i++)
             for (int j = 0; j < 64; j++) {
               const int n = 128 * nh + 64 * r + i, k = 64 * kc + j;
@@ -428,7 +429,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* Wst = smem;
-  uint64_t* bars = (uint64_t*)(Wst + tc2::kStages * kHalfChunkBytes);
+  uint64_t* bars = (uint64_t*)(Wst + tc2::kStages * tc2::kStageBytes);
   uint64_t* full = bars;                         // [kStages] local weight half landed
   uint64_t* empty = full + tc2::kStages;         // [kStages] stage consumed (commit, both CTAs)
   uint64_t* fullp = empty + tc2::kStages;        // [kStages] leader: peer half landed (relay)
@@ -475,18 +476,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
     if (lane == 0) {  // ---- weight producer (own half)
       uint32_t g = 0;
       for (int64_t t = cluster_id; t < ntiles; t += nclusters)
-        for (int i = 0; i < kChunksPerPair; i++, g++) {
+        for (int i = 0; i < tc2::kStagesPerTile; i++, g++) {
           const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
+          const uint32_t bytes = i < 2 ? 8192u : (uint32_t)tc2::kStageBytes;  // layer 0: K = 64
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], kHalfChunkBytes);
-          bulk_g2s(Wst + s * kHalfChunkBytes, m.w_tc2 + ((size_t)i * 2 + crank) * 64 * 64, kHalfChunkBytes, &full[s]);
+          mbar_expect_tx(&full[s], bytes);
+          bulk_g2s(Wst + s * tc2::kStageBytes, m.w_tc2 + ((size_t)i * 2 + crank) * (tc2::kStageBytes / 2), bytes,
+                   &full[s]);
         }
     }
   } else if (warp == 3) {
     if (lane == 0 && !leader) {  // ---- relay: peer half landed -> leader's fullp[s]
       uint32_t g = 0;
       for (int64_t t = cluster_id; t < ntiles; t += nclusters)
-        for (int i = 0; i < kChunksPerPair; i++, g++) {
+        for (int i = 0; i < tc2::kStagesPerTile; i++, g++) {
           const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
           mbar_wait(&full[s], ph);
           mbar_arrive_cluster(mapa(smem_u32(&fullp[s]), 0));
@@ -500,8 +503,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
         for (int l = 0; l < kDepth; l++) {
           const int nkc = l == 0 ? 1 : 4;
           const uint32_t a_buf = tmem + 256 + (l & 1) * 128;
-          for (int nh = 0; nh < 2; nh++) {
-            for (int kc = 0; kc < nkc; kc++, g++) {
+          for (int nh = 0; nh < 2; nh++, g++) {
+            const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
+            mbar_wait(&full[s], ph);
+            mbar_wait(&fullp[s], ph);
+            const uint32_t b_stage = smem_u32(Wst + s * tc2::kStageBytes);
+            for (int kc = 0; kc < nkc; kc++) {
               if (l == 0 && nh == 0) {  // encoding of this tile written (A buffer 0, D half 0 drained)
                 mbar_wait(pe_ready, rpe & 1);
                 rpe++;
@@ -522,17 +529,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
                 ra1++;
                 tc_fence_after();
               }
-              const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
-              mbar_wait(&full[s], ph);
-              mbar_wait(&fullp[s], ph);
               tc_fence_after();
-              const uint32_t b_base = smem_u32(Wst + s * kHalfChunkBytes);
+              const uint32_t b_base = b_stage + kc * 8192;
               const uint32_t d = tmem + nh * 128;
 #pragma unroll
               for (int ks = 0; ks < 4; ks++)
                 umma_ts(d, a_buf + kc * 32 + ks * 8, sw128_desc(b_base + ks * 32), (kc | ks) != 0);
-              umma_commit_pair(&empty[s]);
             }
+            umma_commit_pair(&empty[s]);
             umma_commit_pair(&acc_full[nh]);
             if (l == kDepth - 2 && nh == 1) umma_commit_pair(pe_free);
           }

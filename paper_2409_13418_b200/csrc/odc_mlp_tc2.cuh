@@ -7,8 +7,8 @@
 //     layer's bf16 activations with tcgen05.st, double-buffered, so shared
 //     memory carries only weights;
 //   * B (weights) is split along N: each CTA streams its 64-row half of every
-//     16 KB weight chunk (8 KB) into its own ring with cp.async.bulk; the
-//     leader's MMA reads both halves;
+//     half-layer (l, N half) of the weights (32 KB, 4 K-atoms) into its own
+//     4-stage ring with cp.async.bulk; the leader's MMA reads both halves;
 //   * D (fp32 accumulators) per CTA: its 128 rows x N, in TMEM.
 // Per SM and layer that is 64 KB of weights through shared memory per 2048
 // MMA cycles (32 B/clk), against 128 B/clk for the single-CTA SS version.
@@ -31,14 +31,15 @@ namespace odc {
 namespace tc2 {
 
 constexpr int kThreads = 384;
-constexpr int kStages = 16;
-constexpr int kHalfChunkBytes = 8192;  // 64 rows x 128 B
+constexpr int kStages = 4;            // ring of half-layer stages
+constexpr int kStageBytes = 32768;    // per CTA: 64 rows x K 256 (4 K-atoms of 8 KB)
+constexpr int kStagesPerTile = 16;    // (layer, N half)
 constexpr uint32_t kIdesc = (1u << 4)      // D f32
                             | (1u << 7)    // A bf16
                             | (1u << 10)   // B bf16
                             | (16u << 17)  // N = 128
                             | (16u << 24); // M = 256 (CTA pair)
-constexpr size_t kSmemBytes = 1024 + kStages * kHalfChunkBytes + 1024 + (8 * 256 + 256 + 256) * 4;
+constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 1024 + (8 * 256 + 256 + 256) * 4;
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
