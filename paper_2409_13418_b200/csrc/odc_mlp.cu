@@ -397,9 +397,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
 // ===========================================================================
 size_t mlp_tc2_weight_elems() { return (size_t)tc2::kStagesPerTile * 2 * tc2::kStageBytes / 2; }
 
-// stage (l, nh) in consumption order; CTA half r holds B rows
-// n = 128 nh + 64 r + i, k = 64 kc + j: K-atom kc (8 KB SWIZZLE_128B K-major
-// image) at byte 8192 kc of the half's 32 KB slot (layer 0: one atom)
+// stages (l, nh, kh) in consumption order (layer 0: kh = 0 only, K = 64);
+// CTA half r of a stage holds B rows n = 128 nh + 64 r + i and K-atoms
+// kc = 2 kh, 2 kh + 1 (k = 64 kc + j), each an 8 KB SWIZZLE_128B K-major image
+__host__ __device__ inline int tc2_stage_index(int l, int nh, int kh) { return l == 0 ? nh : 2 + (l - 1) * 4 + nh * 2 + kh; }
 void mlp_pack_weights_tc2(const float* w0, int d_in, const float* w_hidden, uint16_t* out) {
   std::memset(out, 0, mlp_tc2_weight_elems() * 2);
   for (int l = 0; l < kDepth; l++) {
@@ -407,7 +408,8 @@ void mlp_pack_weights_tc2(const float* w0, int d_in, const float* w_hidden, uint
     for (int nh = 0; nh < 2; nh++)
       for (int kc = 0; kc < nkc; kc++)
         for (int r = 0; r < 2; r++) {
-          uint16_t* img = out + ((size_t)((l * 2 + nh) * 2 + r) * tc2::kStageBytes + kc * 8192) / 2;
+          const int si = tc2_stage_index(l, nh, kc >> 1);
+          uint16_t* img = out + ((size_t)(si * 2 + r) * tc2::kStageBytes + (kc & 1) * 8192) / 2;
           for (int i = 0; i < 64; i++)
             for (int j = 0; j < 64; j++) {
               const int n = 128 * nh + 64 * r + i, k = 64 * kc + j;
@@ -478,7 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
       for (int64_t t = cluster_id; t < ntiles; t += nclusters)
         for (int i = 0; i < tc2::kStagesPerTile; i++, g++) {
           const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
-          const uint32_t bytes = i < 2 ? 8192u : (uint32_t)tc2::kStageBytes;  // layer 0: K = 64
+          const uint32_t bytes = i < 2 ? 8192u : (uint32_t)tc2::kStageBytes;  // layer 0 stages: K = 64
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], bytes);
           bulk_g2s(Wst + s * tc2::kStageBytes, m.w_tc2 + ((size_t)i * 2 + crank) * (tc2::kStageBytes / 2), bytes,
@@ -503,12 +505,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
         for (int l = 0; l < kDepth; l++) {
           const int nkc = l == 0 ? 1 : 4;
           const uint32_t a_buf = tmem + 256 + (l & 1) * 128;
-          for (int nh = 0; nh < 2; nh++, g++) {
-            const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
-            mbar_wait(&full[s], ph);
-            mbar_wait(&fullp[s], ph);
-            const uint32_t b_stage = smem_u32(Wst + s * tc2::kStageBytes);
+          for (int nh = 0; nh < 2; nh++) {
+            uint32_t s = 0, b_stage = 0;
             for (int kc = 0; kc < nkc; kc++) {
+              if ((kc & 1) == 0) {  // a new stage holds K-atoms kc, kc + 1
+                s = g % tc2::kStages;
+                const uint32_t ph = (g / tc2::kStages) & 1;
+                mbar_wait(&full[s], ph);
+                mbar_wait(&fullp[s], ph);
+                b_stage = smem_u32(Wst + s * tc2::kStageBytes);
+              }
               if (l == 0 && nh == 0) {  // encoding of this tile written (A buffer 0, D half 0 drained)
                 mbar_wait(pe_ready, rpe & 1);
                 rpe++;
@@ -530,13 +536,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
                 tc_fence_after();
               }
               tc_fence_after();
-              const uint32_t b_base = b_stage + kc * 8192;
+              const uint32_t b_base = b_stage + (kc & 1) * 8192;
               const uint32_t d = tmem + nh * 128;
 #pragma unroll
               for (int ks = 0; ks < 4; ks++)
                 umma_ts(d, a_buf + kc * 32 + ks * 8, sw128_desc(b_base + ks * 32), (kc | ks) != 0);
+              if ((kc & 1) == 1 || kc == nkc - 1) {
+                umma_commit_pair(&empty[s]);
+                g++;
+              }
             }
-            umma_commit_pair(&empty[s]);
             umma_commit_pair(&acc_full[nh]);
             if (l == kDepth - 2 && nh == 1) umma_commit_pair(pe_free);
           }

@@ -7,8 +7,8 @@
 //     layer's bf16 activations with tcgen05.st, double-buffered, so shared
 //     memory carries only weights;
 //   * B (weights) is split along N: each CTA streams its 64-row half of every
-//     half-layer (l, N half) of the weights (32 KB, 4 K-atoms) into its own
-//     4-stage ring with cp.async.bulk; the leader's MMA reads both halves;
+//     (layer, N half, K half) block of the weights (16 KB, 2 K-atoms) into a
+//     12-stage ring with cp.async.bulk; the leader's MMA reads both halves;
 //   * D (fp32 accumulators) per CTA: its 128 rows x N, in TMEM.
 // Per SM and layer that is 64 KB of weights through shared memory per 2048
 // MMA cycles (32 B/clk), against 128 B/clk for the single-CTA SS version.
@@ -31,9 +31,9 @@ namespace odc {
 namespace tc2 {
 
 constexpr int kThreads = 384;
-constexpr int kStages = 4;            // ring of half-layer stages
-constexpr int kStageBytes = 32768;    // per CTA: 64 rows x K 256 (4 K-atoms of 8 KB)
-constexpr int kStagesPerTile = 16;    // (layer, N half)
+constexpr int kStages = 12;           // ring of weight stages
+constexpr int kStageBytes = 16384;    // per CTA: 64 rows x K 128 (2 K-atoms of 8 KB)
+constexpr int kStagesPerTile = 30;    // (layer, N half, K half); layer 0 has one K half
 constexpr uint32_t kIdesc = (1u << 4)      // D f32
                             | (1u << 7)    // A bf16
                             | (1u << 10)   // B bf16
