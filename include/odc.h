@@ -229,6 +229,9 @@ int odc_copy_array(odc_ctx* ctx, int32_t which, void* dst, int64_t dst_bytes, in
 /* Batched field evaluation on the device: raw values (1.0/0.0 for analytic
  * fields and for the MLP in shared-field mode) for host points (n,3) f64. */
 int odc_eval_raw(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, double* raw);
+/* Profiling hook (tracing): run the MLP evaluator over n grid points
+ * and return CTA 0's clock64 event timeline (trace_len >= 256 int64 slots). */
+int odc_profile_mlp(odc_ctx* ctx, const odc_field* field, int64_t n, int64_t* trace, int64_t trace_len);
 /* Same, labels only (u8), for host points. */
 int odc_eval_labels(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, uint8_t* labels);
 

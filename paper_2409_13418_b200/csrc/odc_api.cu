@@ -1237,6 +1237,41 @@ static int eval_common(odc_ctx* c, const odc_field* f, const double* pts, int64_
   }, &a);
 }
 
+int odc_profile_mlp(odc_ctx* c, const odc_field* f, int64_t n, int64_t* trace, int64_t trace_len) {
+  if (!c || !f || f->kind != 1 || !trace || trace_len < 256) return ODC_E_ARG;
+  cudaSetDevice(c->device);
+  c->valid = false;
+  c->arena.reset();
+  unsigned long long* dt = c->arena.get<unsigned long long>(trace_len);
+  uint8_t* lab = c->arena.get<uint8_t>(n);
+  if (!dt || !lab) return ODC_E_NOMEM;
+  cudaMemsetAsync(dt, 0, 8 * trace_len, c->stream);
+  GridP g{};
+  const int64_t S = 1 + (int64_t)std::ceil(std::cbrt((double)n));
+  g.R = S - 1;
+  g.S = S;
+  g.S2 = S * S;
+  g.S3 = S * S * S;
+  g.W = (S + 31) / 32;
+  g.z0 = 0;
+  g.nz = S;
+  for (int a = 0; a < 3; a++) {
+    g.lo[a] = 0.0;
+    g.h[a] = 1.0 / (double)g.R;
+  }
+  MlpDev md = f->mlp;
+  md.impl = c->mlp_impl;
+  md.trace = dt;
+  PointSrc src{nullptr, g, 0};
+  mlp_eval(md, src, n < g.S3 ? n : g.S3, lab, nullptr, c->stream);
+  if (cudaMemcpyAsync(trace, dt, 8 * trace_len, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    c->err = "profile run failed";
+    return ODC_E_CUDA;
+  }
+  return ODC_OK;
+}
+
 int odc_eval_raw(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, double* raw) {
   return eval_common(c, f, pts, n, raw, nullptr);
 }

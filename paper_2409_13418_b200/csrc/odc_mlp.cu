@@ -13,6 +13,13 @@
 
 namespace odc {
 
+// Timeline trace of CTA 0 (profiling hook, odc_profile_mlp): clock64 at
+// pipeline events of the first two tiles; slot = ((tile*8 + layer)*16 + event).
+#define ODC_TRACE(t, l, e)                                                                   \
+  do {                                                                                       \
+    if (m.trace && blockIdx.x == 0 && (t) < 2) m.trace[((t) * 8 + (l)) * 16 + (e)] = clock64(); \
+  } while (0)
+
 constexpr int kWidth = 256;
 constexpr int kDepth = 8;
 constexpr int kDin = 39;
@@ -501,10 +508,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
     if (lane == 0 && leader) {  // ---- MMA issuer
       uint32_t g = 0, ra0 = 0, ra1 = 0, rpe = 0;
       bool first = true;
-      for (int64_t t = cluster_id; t < ntiles; t += nclusters) {
+      int ti = 0;
+      for (int64_t t = cluster_id; t < ntiles; t += nclusters, ti++) {
         for (int l = 0; l < kDepth; l++) {
           const int nkc = l == 0 ? 1 : 4;
           const uint32_t a_buf = tmem + 256 + (l & 1) * 128;
+          ODC_TRACE(ti, l, 0);
           for (int nh = 0; nh < 2; nh++) {
             uint32_t s = 0, b_stage = 0;
             for (int kc = 0; kc < nkc; kc++) {
@@ -529,11 +538,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
                 mbar_wait(&a_ready[0], ra0 & 1);
                 ra0++;
                 tc_fence_after();
+                ODC_TRACE(ti, l, 1);
               }
               if (l > 0 && nh == 0 && kc == 2) {
+                ODC_TRACE(ti, l, 2);
                 mbar_wait(&a_ready[1], ra1 & 1);
                 ra1++;
                 tc_fence_after();
+                ODC_TRACE(ti, l, 3);
               }
               tc_fence_after();
               const uint32_t b_base = b_stage + (kc & 1) * 8192;
@@ -547,6 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
               }
             }
             umma_commit_pair(&acc_full[nh]);
+            ODC_TRACE(ti, l, 4 + nh);
             if (l == kDepth - 2 && nh == 1) umma_commit_pair(pe_free);
           }
         }
@@ -572,15 +585,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_pe_ready);
     }
-    for (int64_t t = t0; t < ntiles; t += nclusters) {
+    int ti = 0;
+    for (int64_t t = t0; t < ntiles; t += nclusters, ti++) {
       const int64_t next = t + nclusters;
       float dot = 0.f;
       for (int l = 0; l < kDepth; l++) {
         const float* bl = s_bias + l * kWidth + half * 128;
         if (half == 0 && l == kDepth - 1 && next < ntiles) pe_row_packed(src, n, next * 256 + crank * 128 + r, pe);
+        if (r == 0 && crank == 0) ODC_TRACE(ti, l, 6 + half);
         mbar_wait(&acc_full[half], af & 1);
         af++;
         tc_fence_after();
+        if (r == 0 && crank == 0) ODC_TRACE(ti, l, 8 + half);
         if (l < kDepth - 1) {
           const uint32_t a_out = tmem + lane_base + 256 + ((l + 1) & 1) * 128 + half * 64;
 #pragma unroll
@@ -597,6 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(leader_a_ready);
+          if (r == 0 && crank == 0) ODC_TRACE(ti, l, 10 + half);
         } else {
 #pragma unroll
           for (int i = 0; i < 4; i++) {

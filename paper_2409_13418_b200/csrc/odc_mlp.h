@@ -23,6 +23,7 @@ struct MlpDev {
   const uint16_t* w_tc2;     // the same chunks split into two 64-row halves (odc_mlp_tc2.cuh)
   int impl;                  // 0 = CTA-pair tcgen05 (default), 1 = SIMT reference, 2 = single-CTA tcgen05
   int has_bias;              // any non-zero bias (selects the bias-add epilogue)
+  unsigned long long* trace; // profiling: event timeline of CTA 0 (nullptr = off)
   const float* bias;         // (8, 256)
   const float* w_head;       // (256)
   float b_head;
