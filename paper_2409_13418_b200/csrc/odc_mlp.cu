@@ -246,18 +246,21 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- weight producer
+    {  // ---- weight producer (whole warp, one elected lane issues)
       uint32_t g = 0;
       for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x)
         for (int i = 0; i < kChunksPerPair; i++, g++) {
           const uint32_t s = g % kStages, ph = (g / kStages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], kChunkBytes);
-          bulk_g2s(Wst + s * kChunkBytes, m.w_tc + (size_t)i * 128 * 64, kChunkBytes, &full[s]);
+          if (elect_one()) {
+            mbar_expect_tx(&full[s], kChunkBytes);
+            bulk_g2s(Wst + s * kChunkBytes, m.w_tc + (size_t)i * 128 * 64, kChunkBytes, &full[s]);
+          }
+          __syncwarp();
         }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
+    {  // ---- MMA issuer (whole warp keeps operands uniform; one elected lane issues)
       uint32_t g = 0, ra0 = 0, ra1 = 0;
       const uint32_t a_base[2] = {smem_u32(A0), smem_u32(A0 + kTileABytes)};
       for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
@@ -279,17 +282,21 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
               mbar_wait(&full[s], ph);
               tc_fence_after();
               const uint32_t b_base = smem_u32(Wst + s * kChunkBytes);
+              if (elect_one()) {
 #pragma unroll
-              for (int t = 0; t < 2; t++) {
-                const uint32_t d = tmem + t * 256 + nh * 128;
+                for (int t = 0; t < 2; t++) {
+                  const uint32_t d = tmem + t * 256 + nh * 128;
 #pragma unroll
-                for (int ks = 0; ks < 4; ks++)
-                  umma_bf16(d, sw128_desc(a_base[t] + kc * 16384 + ks * 32), sw128_desc(b_base + ks * 32),
-                            (kc | ks) != 0);
+                  for (int ks = 0; ks < 4; ks++)
+                    umma_bf16(d, sw128_desc(a_base[t] + kc * 16384 + ks * 32), sw128_desc(b_base + ks * 32),
+                              (kc | ks) != 0);
+                }
+                umma_commit(&empty[s]);
               }
-              umma_commit(&empty[s]);
+              __syncwarp();
             }
-            umma_commit(&acc_full[nh]);
+            if (elect_one()) umma_commit(&acc_full[nh]);
+            __syncwarp();
           }
         }
       }
@@ -482,30 +489,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- weight producer (own half)
+    {  // ---- weight producer (own half; whole warp, one elected lane issues)
       uint32_t g = 0;
       for (int64_t t = cluster_id; t < ntiles; t += nclusters)
         for (int i = 0; i < tc2::kStagesPerTile; i++, g++) {
           const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
           const uint32_t bytes = i < 2 ? 8192u : (uint32_t)tc2::kStageBytes;  // layer 0 stages: K = 64
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], bytes);
-          bulk_g2s(Wst + s * tc2::kStageBytes, m.w_tc2 + ((size_t)i * 2 + crank) * (tc2::kStageBytes / 2), bytes,
-                   &full[s]);
+          if (elect_one()) {
+            mbar_expect_tx(&full[s], bytes);
+            bulk_g2s(Wst + s * tc2::kStageBytes, m.w_tc2 + ((size_t)i * 2 + crank) * (tc2::kStageBytes / 2), bytes,
+                     &full[s]);
+          }
+          __syncwarp();
         }
     }
   } else if (warp == 3) {
-    if (lane == 0 && !leader) {  // ---- relay: peer half landed -> leader's fullp[s]
+    if (!leader) {  // ---- relay: peer half landed -> leader's fullp[s]
       uint32_t g = 0;
       for (int64_t t = cluster_id; t < ntiles; t += nclusters)
         for (int i = 0; i < tc2::kStagesPerTile; i++, g++) {
           const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
           mbar_wait(&full[s], ph);
-          mbar_arrive_cluster(mapa(smem_u32(&fullp[s]), 0));
+          if (elect_one()) mbar_arrive_cluster(mapa(smem_u32(&fullp[s]), 0));
+          __syncwarp();
         }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ---- MMA issuer
+    if (leader) {  // ---- MMA issuer (whole warp keeps operands uniform; one elected lane issues)
       uint32_t g = 0, ra0 = 0, ra1 = 0, rpe = 0;
       bool first = true;
       int ti = 0;
@@ -550,17 +561,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
               tc_fence_after();
               const uint32_t b_base = b_stage + (kc & 1) * 8192;
               const uint32_t d = tmem + nh * 128;
+              const bool last_of_stage = (kc & 1) == 1 || kc == nkc - 1;
+              if (elect_one()) {
 #pragma unroll
-              for (int ks = 0; ks < 4; ks++)
-                umma_ts(d, a_buf + kc * 32 + ks * 8, sw128_desc(b_base + ks * 32), (kc | ks) != 0);
-              if ((kc & 1) == 1 || kc == nkc - 1) {
-                umma_commit_pair(&empty[s]);
-                g++;
+                for (int ks = 0; ks < 4; ks++)
+                  umma_ts(d, a_buf + kc * 32 + ks * 8, sw128_desc(b_base + ks * 32), (kc | ks) != 0);
+                if (last_of_stage) umma_commit_pair(&empty[s]);
               }
+              __syncwarp();
+              if (last_of_stage) g++;
             }
-            umma_commit_pair(&acc_full[nh]);
+            if (elect_one()) {
+              umma_commit_pair(&acc_full[nh]);
+              if (l == kDepth - 2 && nh == 1) umma_commit_pair(pe_free);
+            }
+            __syncwarp();
             ODC_TRACE(ti, l, 4 + nh);
-            if (l == kDepth - 2 && nh == 1) umma_commit_pair(pe_free);
           }
         }
         first = false;

@@ -19,7 +19,7 @@ with DeviceField(ctx, MlpField()) as f:
     for _ in range(2):
         rc = L.odc_profile_mlp(ctx.handle, f.handle, n, tr.ctypes.data, len(tr))
         assert rc == 0, L.odc_last_error(ctx.handle)
-t = tr.reshape(2, 8, 16).astype(np.float64)
+t = tr[:256].reshape(2, 8, 16).astype(np.float64)
 base = t[0, 0, 0]
 names = ["mma_start", "a0_ok", "wait_a1", "a1_ok", "iss_nh0", "iss_nh1", "e0_wait", "e1_wait", "e0_acc", "e1_acc",
          "e0_done", "e1_done"]
