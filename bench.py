@@ -132,7 +132,7 @@ def cpu_sample(field, lo, hi, R_full, full_evals, sample_R=None):
         sample = (f"oracle pipeline (C, 1 thread) + numpy fp32 MlpField (OpenBLAS, {cores} threads) at {sR}^3: "
                   f"{ev} evals in {dt:.2f} s; scaled by the eval count of the {R_full}^3 run ({full_evals} evals)")
     else:
-        sR = sample_R or R_full
+        sR = sample_R or min(R_full, 384)  # ~10 s of C oracle work; 1024^3 would take minutes
         t0 = time.perf_counter()
         oracle.contour_oracle(field, lo, hi, sR)
         dt = time.perf_counter() - t0
@@ -206,7 +206,7 @@ def run_gpu(args, rank, world, dist):
             dist.barrier()
         torch.cuda.synchronize()
 
-    if os.environ.get("ODC_MLP_IMPL"):  # evaluator selection for experiments (default: CTA-pair tcgen05)
+    if os.environ.get("ODC_MLP_IMPL"):  # evaluator selection for experiments (default: single-CTA tcgen05)
         L.odc_set_param(ctx.handle, b"mlp_impl", int(os.environ["ODC_MLP_IMPL"]))
     dfield = DeviceField(ctx, field)
     st = _lib.Stats()

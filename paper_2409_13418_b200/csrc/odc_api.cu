@@ -109,7 +109,9 @@ struct odc_ctx {
   unsigned long long* h_pinned = nullptr;  // small readback buffer
   std::string err;
   int launches = 0;
-  int mlp_impl = 0;  // odc_set_param("mlp_impl"): 0 tcgen05, 1 SIMT reference
+  // odc_set_param("mlp_impl"): 2 single-CTA tcgen05 (default, fastest measured),
+  // 0 CTA-pair tcgen05, 1 SIMT reference
+  int mlp_impl = 2;
   // last extraction
   bool valid = false;
   GridP g{};
