@@ -9,6 +9,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/odc.h"
@@ -107,6 +108,8 @@ struct odc_ctx {
   Arena arena;
   CellTabEntry* table = nullptr;
   unsigned long long* h_pinned = nullptr;  // small readback buffer
+  char* h_stage = nullptr;  // grow-only pinned staging for mesh copy-back
+  size_t h_stage_bytes = 0;
   std::string err;
   int launches = 0;
   // odc_set_param("mlp_impl"): 2 single-CTA tcgen05 (default, fastest measured),
@@ -793,6 +796,7 @@ void odc_destroy(odc_ctx* c) {
   cudaStreamSynchronize(c->stream);
   if (c->table) cudaFree(c->table);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (auto& e : c->evs)
@@ -1074,38 +1078,75 @@ int odc_copy_mesh(odc_ctx* c, int32_t which, double* vertices, int64_t* triangle
     const double* dv = raw ? cc->verts0 : cc->verts1;
     const int32_t* dt = raw ? cc->tris0 : cc->tris1;
     cudaStream_t s = cc->stream;
-    if (x->v && V) CUDA_TRY(cudaMemcpyAsync(x->v, dv, sizeof(double) * 3 * V, cudaMemcpyDeviceToHost, s));
-    std::vector<int32_t> t32;
+    // Everything is produced in its final host type on the device (triangles
+    // widened to int64, duplicate provenance filled in), copied with one D2H
+    // per array into pinned staging at full link speed, then spread into the
+    // caller's (pageable, first-touch) buffers by several host threads.
+    struct Seg {
+      const void* dev;
+      void* host;
+      size_t bytes;
+      size_t off;
+    };
+    std::vector<Seg> segs;
+    size_t total = 0;
+    auto add = [&](const void* dev, void* host, size_t bytes) {
+      if (!host || !bytes) return;
+      segs.push_back({dev, host, bytes, total});
+      total += (bytes + 255) & ~(size_t)255;
+    };
+    add(dv, x->v, sizeof(double) * 3 * V);
     if (x->t && T) {
-      t32.resize(3 * T);
-      CUDA_TRY(cudaMemcpyAsync(t32.data(), dt, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToHost, s));
+      int64_t* t64 = need(cc->arena.get<int64_t>(3 * T));
+      launch_widen_i32(dt, t64, 3 * T, s);
+      add(t64, x->t, sizeof(int64_t) * 3 * T);
     }
-    std::vector<int64_t> kind, ref;
-    if ((x->kind || x->ref) && cc->V0) {
-      int64_t* dk = need(cc->arena.get<int64_t>(cc->V0));
-      int64_t* dr = need(cc->arena.get<int64_t>(2 * cc->V0));
+    if ((x->kind || x->ref) && V) {
+      int64_t* dk = need(cc->arena.get<int64_t>(V));
+      int64_t* dr = need(cc->arena.get<int64_t>(2 * V));
+      const int64_t V0 = cc->V0;
       if (cc->prov_kind_in)
-        launch_gather_provenance(cc->V0, cc->src0, cc->prov_kind_in, cc->prov_ref_in, dk, dr, s);
+        launch_gather_provenance(V0, cc->src0, cc->prov_kind_in, cc->prov_ref_in, dk, dr, s);
       else
-        launch_provenance(cc->V0, cc->P, cc->src0, cc->cells.part_cell, cc->cells.part_index, cc->fan_edge, dk, dr,
-                          s);
-      kind.resize(cc->V0);
-      ref.resize(2 * cc->V0);
-      CUDA_TRY(cudaMemcpyAsync(kind.data(), dk, 8 * cc->V0, cudaMemcpyDeviceToHost, s));
-      CUDA_TRY(cudaMemcpyAsync(ref.data(), dr, 16 * cc->V0, cudaMemcpyDeviceToHost, s));
+        launch_provenance(V0, cc->P, cc->src0, cc->cells.part_cell, cc->cells.part_index, cc->fan_edge, dk, dr, s);
+      launch_dup_provenance(V0, V, dk, dr, s);
+      add(dk, x->kind, sizeof(int64_t) * V);
+      add(dr, x->ref, sizeof(int64_t) * 2 * V);
     }
+    CUDA_TRY(cudaGetLastError());
+    if (total > cc->h_stage_bytes) {
+      if (cc->h_stage) cudaFreeHost(cc->h_stage);
+      cc->h_stage = nullptr;
+      cc->h_stage_bytes = 0;
+      const size_t want = total + total / 4;
+      CUDA_TRY(cudaHostAlloc((void**)&cc->h_stage, want, cudaHostAllocDefault));
+      cc->h_stage_bytes = want;
+    }
+    for (const Seg& g : segs)
+      CUDA_TRY(cudaMemcpyAsync(cc->h_stage + g.off, g.dev, g.bytes, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    if (x->t)
-      for (int64_t i = 0; i < 3 * T; i++) x->t[i] = t32[i];
-    if (x->kind || x->ref) {
-      for (int64_t i = 0; i < V; i++) {
-        const bool dup = i >= cc->V0;
-        if (x->kind) x->kind[i] = dup ? 2 : kind[i];
-        if (x->ref) {
-          x->ref[2 * i] = dup ? -1 : ref[2 * i];
-          x->ref[2 * i + 1] = dup ? -1 : ref[2 * i + 1];
-        }
-      }
+    // parallel spread: chunks of ~4 MB over up to 8 threads
+    const size_t chunk = 4u << 20;
+    struct Piece {
+      const char* src;
+      char* dst;
+      size_t n;
+    };
+    std::vector<Piece> pieces;
+    for (const Seg& g : segs)
+      for (size_t o = 0; o < g.bytes; o += chunk)
+        pieces.push_back({cc->h_stage + g.off + o, (char*)g.host + o, std::min(chunk, g.bytes - o)});
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nthr = std::min<size_t>({(size_t)8, (size_t)hw, pieces.size()});
+    if (nthr <= 1) {
+      for (const Piece& q : pieces) std::memcpy(q.dst, q.src, q.n);
+    } else {
+      std::vector<std::thread> pool;
+      for (size_t t = 0; t < nthr; t++)
+        pool.emplace_back([&pieces, t, nthr]() {
+          for (size_t i = t; i < pieces.size(); i += nthr) std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].n);
+        });
+      for (auto& th : pool) th.join();
     }
     return (int)ODC_OK;
   }, &a);

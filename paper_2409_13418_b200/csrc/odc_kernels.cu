@@ -1878,4 +1878,25 @@ void launch_provenance(int64_t V, int64_t P, const int64_t* src_of, const int64_
   if (V) k_provenance<<<grid_for(V, 256), 256, 0, s>>>(V, P, src_of, part_cell, part_index, fan_edge, kind, ref);
 }
 
+__global__ void k_widen_i32(const int32_t* __restrict__ src, int64_t* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+void launch_widen_i32(const int32_t* src, int64_t* dst, int64_t n, cudaStream_t s) {
+  if (n) k_widen_i32<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n);
+}
+
+__global__ void k_dup_provenance(int64_t V0, int64_t V, int64_t* __restrict__ kind, int64_t* __restrict__ ref) {
+  const int64_t i = V0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  if (kind) kind[i] = 2;
+  if (ref) {
+    ref[2 * i] = -1;
+    ref[2 * i + 1] = -1;
+  }
+}
+void launch_dup_provenance(int64_t V0, int64_t V, int64_t* kind, int64_t* ref, cudaStream_t s) {
+  if (V > V0) k_dup_provenance<<<grid_for(V - V0, 256), 256, 0, s>>>(V0, V, kind, ref);
+}
+
 }  // namespace odc

@@ -165,6 +165,11 @@ void launch_widen_flags(const uint8_t* f, int64_t n, uint32_t* out, cudaStream_t
 void launch_gather_provenance(int64_t V, const int64_t* src_of, const int64_t* kind_in, const int64_t* ref_in,
                               int64_t* kind, int64_t* ref, cudaStream_t s);
 
+// mesh copy-back: int32 triangles widened to the reference's int64 (mesh.py:28)
+void launch_widen_i32(const int32_t* src, int64_t* dst, int64_t n, cudaStream_t s);
+// provenance of repair duplicates [V0, V): kind 2, ref (-1, -1) (polygonize.py:348-373)
+void launch_dup_provenance(int64_t V0, int64_t V, int64_t* kind, int64_t* ref, cudaStream_t s);
+
 // provenance (mesh.py:11-20)
 void launch_provenance(int64_t V, int64_t P, const int64_t* src_of, const int64_t* part_cell,
                        const int64_t* part_index, const int64_t* fan_edge, int64_t* kind, int64_t* ref,

@@ -204,18 +204,18 @@ def _copy_mesh(ctx, which, st, provenance=True):
 
 
 def _raw_from_repaired(ctx, mesh, st):
-    """The pre-repair mesh from the repaired one: repair only appends
-    duplicates of existing vertices and renames triangle corners to them
-    (polygonize.py:348-373), so mapping every duplicate back to its source
-    restores the raw triangles exactly."""
-    V0 = int(st.raw_n_vertices)
-    src = stage_arrays(ctx, ["dup_source"])["dup_source"]
-    t = mesh.triangles.copy()
-    m = t >= V0
-    t[m] = src[t[m] - V0]
-    kind = mesh.provenance_kind[:V0].copy() if mesh.provenance_kind is not None else None
-    ref = mesh.provenance_ref[:V0].copy() if mesh.provenance_ref is not None else None
-    return TriangleMesh.trusted(mesh.vertices[:V0].copy(), t, kind, ref)
+    """The pre-repair mesh: repair only appends duplicates of existing
+    vertices and renames triangle corners to them (polygonize.py:348-373), so
+    its vertices and provenance are the first V0 rows of the repaired mesh
+    (views, no copy) and its triangles are the device's pre-repair buffer."""
+    V0, T = int(st.raw_n_vertices), int(st.raw_n_triangles)
+    t = np.empty((T, 3), dtype=np.int64)
+    rc = _lib.load().odc_copy_mesh(ctx.handle, 1, None, t.ctypes.data if T else None, None, None)
+    if rc != _lib.ODC_OK:
+        _raise(rc, ctx)
+    kind = mesh.provenance_kind[:V0] if mesh.provenance_kind is not None else None
+    ref = mesh.provenance_ref[:V0] if mesh.provenance_ref is not None else None
+    return TriangleMesh.trusted(mesh.vertices[:V0], t, kind, ref)
 
 
 def stats_dict(st, options, mesh_counts=True):
