@@ -115,6 +115,7 @@ struct odc_ctx {
   // odc_set_param("mlp_impl"): 2 single-CTA tcgen05 (default, fastest measured),
   // 0 CTA-pair tcgen05, 1 SIMT reference
   int mlp_impl = 2;
+  int mlp_debug = 0;  // odc_set_param("mlp_debug"): profiling experiments, odc_profile_mlp only
   // last extraction
   bool valid = false;
   GridP g{};
@@ -809,6 +810,10 @@ const char* odc_last_error(const odc_ctx* c) { return c ? c->err.c_str() : "null
 
 int odc_set_param(odc_ctx* c, const char* name, int64_t value) {
   if (!c || !name) return ODC_E_ARG;
+  if (std::strcmp(name, "mlp_debug") == 0 && value >= 0 && value <= 127) {
+    c->mlp_debug = (int)value;
+    return ODC_OK;
+  }
   if (std::strcmp(name, "mlp_impl") == 0 && value >= 0 && value <= 2) {
     c->mlp_impl = (int)value;
     return ODC_OK;
@@ -1304,14 +1309,20 @@ int odc_profile_mlp(odc_ctx* c, const odc_field* f, int64_t n, int64_t* trace, i
   }
   MlpDev md = f->mlp;
   md.impl = c->mlp_impl;
-  md.trace = dt;
+  md.debug = c->mlp_debug & 63;
+  md.trace = (c->mlp_debug & 64) ? nullptr : dt;  // 64: time the kernel without the trace hooks
   PointSrc src{nullptr, g, 0};
+  cudaEventRecord(c->ev0, c->stream);
   mlp_eval(md, src, n < g.S3 ? n : g.S3, lab, nullptr, c->stream);
+  cudaEventRecord(c->ev1, c->stream);
   if (cudaMemcpyAsync(trace, dt, 8 * trace_len, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
       cudaStreamSynchronize(c->stream) != cudaSuccess) {
     c->err = "profile run failed";
     return ODC_E_CUDA;
   }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  trace[trace_len - 1] = (int64_t)(ms * 1e6f);  // kernel time, ns
   return ODC_OK;
 }
 

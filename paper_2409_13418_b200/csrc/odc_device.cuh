@@ -49,6 +49,14 @@ __device__ __forceinline__ int64_t word_of(const GridP& g, int64_t x, int64_t y,
   return ((z - g.z0) * g.S + y) * g.W + (x >> 5);
 }
 __device__ __forceinline__ void vid_coords(const GridP& g, int64_t vid, int64_t c[3]) {
+  if ((uint64_t)vid <= 0xffffffffull && g.S <= 0xffff) {  // 32-bit divisions (every grid up to 2^32 vertices)
+    const uint32_t v = (uint32_t)vid, S = (uint32_t)g.S;
+    const uint32_t q = v / S;
+    c[0] = v - q * S;
+    c[1] = q % S;
+    c[2] = q / S;
+    return;
+  }
   c[0] = vid % g.S;
   c[1] = (vid / g.S) % g.S;
   c[2] = vid / g.S2;

@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 #include "odc_mlp.h"
 #include "odc_mlp_tc.cuh"
@@ -153,17 +154,30 @@ void mlp_pack_weights_tc(const float* w0, int d_in, const float* w_hidden, uint1
 }
 
 // Positional encoding of point p packed to 32 bf16x2 words (features 0..63,
-// 39..63 zero); computed ahead of time, stored when the A tile is free.
+// 39..63 zero); one sincospif per (frequency, coordinate) feeds both the sin
+// and the cos feature.  Same values as pe_feature().
 __device__ __forceinline__ void pe_row_packed(const PointSrc& src, int64_t n, int64_t p, uint32_t (&pk)[32]) {
   double pt[3] = {0.5, 0.5, 0.5};
   const bool ok = p < n;
   if (ok) point_of(src, p, pt);
+  float f[40];
+  const float x[3] = {(float)(pt[0] - 0.5), (float)(pt[1] - 0.5), (float)(pt[2] - 0.5)};
 #pragma unroll
-  for (int c = 0; c < 32; c++) {
-    const float lo = ok ? pe_feature(pt, 2 * c) : 0.f;
-    const float hi = ok ? pe_feature(pt, 2 * c + 1) : 0.f;
-    pk[c] = tc::pack_bf16x2(lo, hi);
-  }
+  for (int c = 0; c < 3; c++) f[c] = x[c];
+#pragma unroll
+  for (int k = 0; k < 6; k++)
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      float sv, cv;
+      sincospif(x[c] * (float)(1 << k), &sv, &cv);
+      f[3 + 6 * k + c] = sv;
+      f[3 + 6 * k + 3 + c] = cv;
+    }
+  f[39] = 0.f;
+#pragma unroll
+  for (int c = 0; c < 20; c++) pk[c] = ok ? tc::pack_bf16x2(f[2 * c], f[2 * c + 1]) : 0u;
+#pragma unroll
+  for (int c = 20; c < 32; c++) pk[c] = 0u;
 }
 __device__ __forceinline__ void store_pe_row(const uint32_t (&pk)[32], uint32_t a_atom0, int r) {
 #pragma unroll
@@ -204,7 +218,41 @@ __device__ __forceinline__ float head32(const uint32_t (&v)[32], const float* __
   return dot;
 }
 
-template <bool kBias>
+// fp64 prior + logistic of one point from its fp32 head dot product
+// (paper_2409_13418_b200/fields.py MlpField); p < 0 or p >= n: nothing to do
+__device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& src, int64_t n, int64_t p, float dot,
+                                             uint8_t* __restrict__ labels, double* __restrict__ raw) {
+  if (p < 0 || p >= n) return;
+  if (!raw && !src.pts) {
+    // labels only: the sign of the logit in fp32 (FP64 is a narrow pipe here).
+    // Its error is < 1e-4 for these magnitudes, so a margin of 1e-3 decides
+    // exactly; anything closer takes the fp64 path below.
+    int64_t c[3];
+    vid_coords(src.grid, src.begin + p, c);
+    float d2 = 0.f;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      const float x = fmaf((float)c[a], (float)src.grid.h[a], (float)src.grid.lo[a]) - (float)m.prior_center[a];
+      d2 = fmaf(x, x, d2);
+    }
+    const float lg = (float)m.amplitude * (dot + m.b_head) - (float)m.prior_scale * (sqrtf(d2) - (float)m.prior_radius);
+    if (fabsf(lg) > 1e-3f) {
+      labels[p] = lg > 0.f ? 1 : 0;
+      return;
+    }
+  }
+  const double mlp = (double)(dot + m.b_head);
+  double pt[3];
+  point_of(src, p, pt);
+  const double d[3] = {pt[0] - m.prior_center[0], pt[1] - m.prior_center[1], pt[2] - m.prior_center[2]};
+  const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+  const double logit = m.amplitude * mlp - m.prior_scale * (dist - m.prior_radius);
+  const double rv = 1.0 / (1.0 + exp(-logit));
+  labels[p] = rv > 0.5 ? 1 : 0;
+  if (raw) raw[p] = rv;
+}
+
+template <bool kBias, bool kTrace>
 __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc src, int64_t n,
                                                            uint8_t* __restrict__ labels, double* __restrict__ raw) {
   using namespace tc;
@@ -216,12 +264,14 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* acc_full = bars + 2 * kStages;
-  uint64_t* a_ready = acc_full + 2;
-  uint32_t* tmem_slot = (uint32_t*)(a_ready + 2);
+  uint64_t* a_ready = acc_full + 2;  // [0]: K-atom 0 of A written, D half 0 drained; [1]: K-atoms 2-3, D half 1
+  uint64_t* a_rk1 = a_ready + 2;     // K-atom 1 of A written
+  uint32_t* tmem_slot = (uint32_t*)(a_rk1 + 1);
   float* s_bias = (float*)(Wst + kStages * kChunkBytes + 256);  // (8, 256)
   float* s_head = s_bias + kDepth * kWidth;                      // (256)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t npairs = (n + 255) / 256;
+  const int dbg = kTrace ? m.debug : 0;  // profiling experiments only
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; s++) {
@@ -232,6 +282,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
     mbar_init(&acc_full[1], 1);
     mbar_init(&a_ready[0], 256);
     mbar_init(&a_ready[1], 256);
+    mbar_init(a_rk1, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < kDepth * kWidth; i += blockDim.x) s_bias[i] = m.bias[i];
@@ -245,7 +296,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 && !(dbg & 16)) {
     {  // ---- weight producer (whole warp, one elected lane issues)
       uint32_t g = 0;
       for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x)
@@ -253,55 +304,86 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
           const uint32_t s = g % kStages, ph = (g / kStages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           if (elect_one()) {
-            mbar_expect_tx(&full[s], kChunkBytes);
-            bulk_g2s(Wst + s * kChunkBytes, m.w_tc + (size_t)i * 128 * 64, kChunkBytes, &full[s]);
+            if ((dbg & 1) && g >= (uint32_t)kStages) {
+              mbar_arrive(&full[s]);  // experiment: stale weights, no L2 traffic
+            } else {
+              mbar_expect_tx(&full[s], kChunkBytes);
+              bulk_g2s(Wst + s * kChunkBytes, m.w_tc + (size_t)i * 128 * 64, kChunkBytes, &full[s]);
+            }
           }
           __syncwarp();
         }
     }
   } else if (warp == 1) {
-    {  // ---- MMA issuer (whole warp keeps operands uniform; one elected lane issues)
-      uint32_t g = 0, ra0 = 0, ra1 = 0;
-      const uint32_t a_base[2] = {smem_u32(A0), smem_u32(A0 + kTileABytes)};
-      for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
-        for (int l = 0; l < kDepth; l++) {
-          const int nkc = l == 0 ? 1 : 4;
-          for (int nh = 0; nh < 2; nh++) {
-            for (int kc = 0; kc < nkc; kc++, g++) {
-              if (nh == 0 && kc == 0) {
-                mbar_wait(&a_ready[0], ra0 & 1);
-                ra0++;
-                tc_fence_after();
-              }
-              if (l > 0 && nh == 0 && kc == 2) {
-                mbar_wait(&a_ready[1], ra1 & 1);
-                ra1++;
-                tc_fence_after();
-              }
-              const uint32_t s = g % kStages, ph = (g / kStages) & 1;
-              mbar_wait(&full[s], ph);
-              tc_fence_after();
-              const uint32_t b_base = smem_u32(Wst + s * kChunkBytes);
-              if (elect_one()) {
+    // ---- MMA issuer.  The whole warp walks the loop (operands stay in uniform
+    // registers); one elected lane issues.  Descriptors are built from a base
+    // low word plus compile-time offsets, so a chunk of 8 MMAs costs a handful
+    // of uniform adds -- the issue path must stay well under the 512 cycles
+    // the tensor pipe spends on a chunk.
+    const uint32_t a_lo = desc_lo(smem_u32(A0));
+    const uint32_t w_lo = desc_lo(smem_u32(Wst));
+    uint32_t s = 0, ph = 0, ra0 = 0, ra1 = 0, rk1 = 0;
+    int ti = 0;
+    auto wait_a = [&](uint64_t* bar, uint32_t& cnt) {
+      if (!(dbg & 8)) mbar_wait(bar, cnt & 1);
+      cnt++;
+      tc_fence_after();
+    };
+    // one weight chunk: 2 tiles x 4 K-steps of M128 N128 K16
+    auto chunk = [&](int nh, auto kc_c, long long& wfull) {
+      constexpr int kc = decltype(kc_c)::value;
+      const long long w0 = kTrace ? clock64() : 0;
+      if (!(dbg & 16)) mbar_wait(&full[s], ph);
+      if (kTrace) wfull += clock64() - w0;
+      const uint32_t b_lo = w_lo + s * (kChunkBytes >> 4);
+      if (elect_one()) {
 #pragma unroll
-                for (int t = 0; t < 2; t++) {
-                  const uint32_t d = tmem + t * 256 + nh * 128;
+        for (int t = 0; t < 2; t++) {
+          const uint32_t d = tmem + t * 256 + nh * 128;
 #pragma unroll
-                  for (int ks = 0; ks < 4; ks++)
-                    umma_bf16(d, sw128_desc(a_base[t] + kc * 16384 + ks * 32), sw128_desc(b_base + ks * 32),
-                              (kc | ks) != 0);
-                }
-                umma_commit(&empty[s]);
-              }
-              __syncwarp();
-            }
-            if (elect_one()) umma_commit(&acc_full[nh]);
-            __syncwarp();
-          }
+          for (int ks = 0; ks < 4; ks++)
+            umma_bf16(d, make_desc(a_lo + ((t * kTileABytes + kc * 16384 + ks * 32) >> 4)),
+                      make_desc(b_lo + ((ks * 32) >> 4)), (kc | ks) != 0);
         }
+        umma_commit(&empty[s]);
+      }
+      __syncwarp();
+      if (++s == kStages) {
+        s = 0;
+        ph ^= 1;
+      }
+    };
+    for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x, ti++) {
+      for (int l = 0; l < kDepth; l++) {
+        long long wfull = 0;
+#pragma unroll
+        for (int nh = 0; nh < 2; nh++) {
+          if (nh == 0) {
+            if (kTrace && lane == 0) ODC_TRACE(ti, l, 0);
+            wait_a(&a_ready[0], ra0);
+            if (kTrace && lane == 0) ODC_TRACE(ti, l, 1);
+          }
+          if (l == 0 && nh == 1 && ti > 0) wait_a(&a_ready[1], ra1);  // D half 1 drained by layer 7
+          chunk(nh, std::integral_constant<int, 0>{}, wfull);
+          if (l > 0) {
+            if (nh == 0) wait_a(a_rk1, rk1);
+            chunk(nh, std::integral_constant<int, 1>{}, wfull);
+            if (nh == 0) {
+              if (kTrace && lane == 0) ODC_TRACE(ti, l, 2);
+              wait_a(&a_ready[1], ra1);
+              if (kTrace && lane == 0) ODC_TRACE(ti, l, 3);
+            }
+            chunk(nh, std::integral_constant<int, 2>{}, wfull);
+            chunk(nh, std::integral_constant<int, 3>{}, wfull);
+          }
+          if (elect_one()) umma_commit(&acc_full[nh]);
+          __syncwarp();
+          if (kTrace && lane == 0) ODC_TRACE(ti, l, 4 + nh);
+        }
+        if (kTrace && lane == 0 && blockIdx.x == 0 && ti < 2) m.trace[(ti * 8 + l) * 16 + 12] = wfull;
       }
     }
-  } else if (warp >= 4) {  // ---- epilogue: 2 tiles x 128 rows
+  } else if (warp >= 4 && !(dbg & 32)) {  // ---- epilogue: 2 tiles x 128 rows
     const int et = threadIdx.x - 128;
     const int t = et >> 7;
     const int q = warp & 3;
@@ -316,89 +398,137 @@ __global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc s
       fence_proxy_async();
       mbar_arrive(&a_ready[0]);
     }
-    for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
+    int ti = 0;
+    const bool tr = kTrace && et == 0;
+    int64_t p_prev = -1;
+    float dot_prev = 0.f;
+    for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x, ti++) {
       float dot = 0.f;
       const int64_t next = pair + gridDim.x;
       for (int l = 0; l < kDepth; l++) {
         const float* bl = s_bias + l * kWidth;
         if (l == kDepth - 1 && next < npairs)  // hide the next tile's encoding behind layer 7's MMAs
           pe_row_packed(src, n, next * 256 + t * 128 + r, pe);
-        mbar_wait(&acc_full[0], af0 & 1);
+        if (l == 1) {
+          if (tr) ODC_TRACE(ti, l, 13);
+          finish_label(m, src, n, p_prev, dot_prev, labels, raw);
+          p_prev = -1;
+          if (tr) ODC_TRACE(ti, l, 14);
+        }
+        if (tr) ODC_TRACE(ti, l, 6);
+        if (!(dbg & 8)) mbar_wait(&acc_full[0], af0 & 1);
         af0++;
         tc_fence_after();
+        if (tr) ODC_TRACE(ti, l, 8);
         uint32_t pk[64];
         if (l < kDepth - 1) {
 #pragma unroll
           for (int i = 0; i < 4; i++) {
             uint32_t v[32];
-            ODC_TMEM_LD32(trow + 32 * i, v);
-            tmem_ld_wait();
+            if (dbg & 4) {
+#pragma unroll
+              for (int j = 0; j < 32; j++) v[j] = j;
+            } else {
+              ODC_TMEM_LD32(trow + 32 * i, v);
+              tmem_ld_wait();
+            }
             relu_pack32<kBias>(v, bl + 32 * i, pk + 16 * i);
           }
         } else {
 #pragma unroll
           for (int i = 0; i < 4; i++) {
             uint32_t v[32];
-            ODC_TMEM_LD32(trow + 32 * i, v);
-            tmem_ld_wait();
+            if (dbg & 4) {
+#pragma unroll
+              for (int j = 0; j < 32; j++) v[j] = j;
+            } else {
+              ODC_TMEM_LD32(trow + 32 * i, v);
+              tmem_ld_wait();
+            }
             dot = head32<kBias>(v, bl + 32 * i, s_head + 32 * i, dot);
           }
         }
-        mbar_wait(&acc_full[1], af1 & 1);
+        if (tr) ODC_TRACE(ti, l, 7);
+        if (!(dbg & 8)) mbar_wait(&acc_full[1], af1 & 1);
         af1++;
         tc_fence_after();
+        if (tr) ODC_TRACE(ti, l, 9);
         if (l < kDepth - 1) {
           // half 0 -> A columns 0..127 (K-atoms 0, 1); the layer's MMAs are done
+          // half 0 -> A K-atom 0 (the next layer's first chunk), release, then K-atom 1
+          if (!(dbg & 2)) {
 #pragma unroll
-          for (int c = 0; c < 16; c++)
-            st_shared_v4(a_t + (c >> 3) * 16384 + sw128_off(r, c & 7), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
-                         pk[4 * c + 3]);
+            for (int c = 0; c < 8; c++)
+              st_shared_v4(a_t + sw128_off(r, c), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          }
           fence_proxy_async();
+          tc_fence_before();
           mbar_arrive(&a_ready[0]);
+          if (!(dbg & 2)) {
+#pragma unroll
+            for (int c = 8; c < 16; c++)
+              st_shared_v4(a_t + 16384 + sw128_off(r, c & 7), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          }
+          fence_proxy_async();
+          mbar_arrive(a_rk1);
+          if (tr) ODC_TRACE(ti, l, 10);
 #pragma unroll
           for (int i = 0; i < 4; i++) {
             uint32_t v[32];
-            ODC_TMEM_LD32(trow + 128 + 32 * i, v);
-            tmem_ld_wait();
+            if (dbg & 4) {
+#pragma unroll
+              for (int j = 0; j < 32; j++) v[j] = j;
+            } else {
+              ODC_TMEM_LD32(trow + 128 + 32 * i, v);
+              tmem_ld_wait();
+            }
             uint32_t w[16];
             relu_pack32<kBias>(v, bl + 128 + 32 * i, w);
 #pragma unroll
             for (int c = 0; c < 4; c++) {
               const int cc = 4 * i + c;  // chunk within columns 128..255
-              st_shared_v4(a_t + (2 + (cc >> 3)) * 16384 + sw128_off(r, cc & 7), w[4 * c], w[4 * c + 1],
+              if (!(dbg & 2)) st_shared_v4(a_t + (2 + (cc >> 3)) * 16384 + sw128_off(r, cc & 7), w[4 * c], w[4 * c + 1],
                            w[4 * c + 2], w[4 * c + 3]);
             }
           }
           fence_proxy_async();
+          tc_fence_before();
           mbar_arrive(&a_ready[1]);
+          if (tr) ODC_TRACE(ti, l, 11);
         } else {
+          // layer 7: the MMAs are done with A -> the next tile pair's encoding
+          // goes in now, before the half-1 head, so its layer 0 starts at once
+          if (next < npairs) {
+            store_pe_row(pe, a_t, r);
+            fence_proxy_async();
+            tc_fence_before();
+            mbar_arrive(&a_ready[0]);
+          }
 #pragma unroll
           for (int i = 0; i < 4; i++) {
             uint32_t v[32];
-            ODC_TMEM_LD32(trow + 128 + 32 * i, v);
-            tmem_ld_wait();
+            if (dbg & 4) {
+#pragma unroll
+              for (int j = 0; j < 32; j++) v[j] = j;
+            } else {
+              ODC_TMEM_LD32(trow + 128 + 32 * i, v);
+              tmem_ld_wait();
+            }
             dot = head32<kBias>(v, bl + 128 + 32 * i, s_head + 128 + 32 * i, dot);
+          }
+          if (next < npairs) {  // D half 1 drained: the next pair's layer 0 may overwrite it
+            tc_fence_before();
+            mbar_arrive(&a_ready[1]);
           }
         }
       }
-      if (next < npairs) {  // A is free: the next tile pair can start while this one finishes
-        store_pe_row(pe, a_t, r);
-        fence_proxy_async();
-        mbar_arrive(&a_ready[0]);
-      }
-      const int64_t p = pair * 256 + t * 128 + r;
-      if (p < n) {
-        const double mlp = (double)(dot + m.b_head);
-        double pt[3];
-        point_of(src, p, pt);
-        const double d[3] = {pt[0] - m.prior_center[0], pt[1] - m.prior_center[1], pt[2] - m.prior_center[2]};
-        const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
-        const double logit = m.amplitude * mlp - m.prior_scale * (dist - m.prior_radius);
-        const double rv = 1.0 / (1.0 + exp(-logit));
-        labels[p] = rv > 0.5 ? 1 : 0;
-        if (raw) raw[p] = rv;
-      }
+      // the label of this point is finished during the next pair's layer 1
+      // (the epilogue idles there while the MMAs run), keeping this pair's
+      // tail off the critical path into the next pair's layer 0
+      p_prev = pair * 256 + t * 128 + r;
+      dot_prev = dot;
     }
+    finish_label(m, src, n, p_prev, dot_prev, labels, raw);
   }
   tc_fence_before();
   __syncthreads();
@@ -558,7 +688,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
                 tc_fence_after();
                 ODC_TRACE(ti, l, 3);
               }
-              tc_fence_after();
               const uint32_t b_base = b_stage + (kc & 1) * 8192;
               const uint32_t d = tmem + nh * 128;
               const bool last_of_stage = (kc & 1) == 1 || kc == nkc - 1;
@@ -696,8 +825,10 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_mlp_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
-    cudaFuncSetAttribute(k_mlp_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+    cudaFuncSetAttribute(k_mlp_tc<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+    cudaFuncSetAttribute(k_mlp_tc<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+    cudaFuncSetAttribute(k_mlp_tc<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+    cudaFuncSetAttribute(k_mlp_tc<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc2::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc2::kSmemBytes);
     int dev = 0;
@@ -715,13 +846,12 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
     return 0;
   }
   const int64_t grid = ntiles < g_num_sms ? ntiles : g_num_sms;
-  if (m.has_bias)
-    k_mlp_tc<true><<<(unsigned)grid, tc::kThreads, tc::kSmemBytes, s>>>(m, src, n, labels, raw);
-  else
-    k_mlp_tc<false><<<(unsigned)grid, tc::kThreads, tc::kSmemBytes, s>>>(m, src, n, labels, raw);
+  auto k = m.trace ? (m.has_bias ? k_mlp_tc<true, true> : k_mlp_tc<false, true>)
+                   : (m.has_bias ? k_mlp_tc<true, false> : k_mlp_tc<false, false>);
+  k<<<(unsigned)grid, tc::kThreads, tc::kSmemBytes, s>>>(m, src, n, labels, raw);
   return 0;
 }
 
-const char* mlp_kernel_name() { return "k_mlp_tc2"; }
+const char* mlp_kernel_name() { return "k_mlp_tc"; }
 
 }  // namespace odc
