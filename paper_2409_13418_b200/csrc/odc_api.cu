@@ -772,6 +772,13 @@ int odc_create(int device, odc_ctx** out) {
     return ODC_E_CUDA;
   }
   c->stream = c->own;
+  {  // field buffers come from the stream-ordered pool; keep freed blocks cached
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   for (auto& e : c->evs)
     if (cudaEventCreate(&e) != cudaSuccess) {
       delete c;
@@ -855,8 +862,9 @@ int odc_field_analytic(odc_ctx* c, const odc_node* nodes, int32_t n_nodes, int32
   f->n_nodes = n_nodes;
   f->continuous = continuous;
   f->iso = iso;
-  if (cudaMalloc(&f->nodes, sizeof(odc_node) * n_nodes) != cudaSuccess ||
-      cudaMemcpyAsync(f->nodes, nodes, sizeof(odc_node) * n_nodes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
+  if (cudaMallocAsync((void**)&f->nodes, sizeof(odc_node) * n_nodes, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(f->nodes, nodes, sizeof(odc_node) * n_nodes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess) {
     c->err = "field upload failed";
     delete f;
     return ODC_E_CUDA;
@@ -886,19 +894,27 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
   std::vector<uint16_t> packed_tc2(nt2);
   mlp_pack_weights_tc2(d->w0, d->d_in, d->w_hidden, packed_tc2.data());
   mlp_pack_weights(d->w0, d->d_in, d->w_hidden, packed.data());
-  if (cudaMalloc(&f->w_packed, ne * 2) != cudaSuccess || cudaMalloc(&f->w_tc, nt * 2) != cudaSuccess ||
-      cudaMalloc(&f->w_tc2, nt2 * 2) != cudaSuccess ||
-      cudaMalloc(&f->bias, 8 * 256 * 4) != cudaSuccess ||
-      cudaMalloc(&f->w_head, 256 * 4) != cudaSuccess) {
+  // stream-ordered pool allocations: no driver round trip per field
+  cudaStream_t s = c->stream;
+  if (cudaMallocAsync((void**)&f->w_packed, ne * 2, s) != cudaSuccess ||
+      cudaMallocAsync((void**)&f->w_tc, nt * 2, s) != cudaSuccess ||
+      cudaMallocAsync((void**)&f->w_tc2, nt2 * 2, s) != cudaSuccess ||
+      cudaMallocAsync((void**)&f->bias, 8 * 256 * 4, s) != cudaSuccess ||
+      cudaMallocAsync((void**)&f->w_head, 256 * 4, s) != cudaSuccess) {
     c->err = "field upload failed";
     delete f;
     return ODC_E_NOMEM;
   }
-  cudaMemcpy(f->w_packed, packed.data(), ne * 2, cudaMemcpyHostToDevice);
-  cudaMemcpy(f->w_tc, packed_tc.data(), nt * 2, cudaMemcpyHostToDevice);
-  cudaMemcpy(f->w_tc2, packed_tc2.data(), nt2 * 2, cudaMemcpyHostToDevice);
-  cudaMemcpy(f->bias, d->biases, 8 * 256 * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(f->w_head, d->w_head, 256 * 4, cudaMemcpyHostToDevice);
+  cudaMemcpyAsync(f->w_packed, packed.data(), ne * 2, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(f->w_tc, packed_tc.data(), nt * 2, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(f->w_tc2, packed_tc2.data(), nt2 * 2, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(f->bias, d->biases, 8 * 256 * 4, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(f->w_head, d->w_head, 256 * 4, cudaMemcpyHostToDevice, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) {  // usable from any stream once created
+    c->err = "field upload failed";
+    delete f;
+    return ODC_E_CUDA;
+  }
   f->mlp.w_packed = f->w_packed;
   f->mlp.w_tc = f->w_tc;
   f->mlp.w_tc2 = f->w_tc2;
@@ -918,13 +934,18 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
 
 void odc_field_free(odc_ctx* c, odc_field* f) {
   if (!f) return;
-  if (c) cudaStreamSynchronize(c->stream);
-  cudaFree(f->nodes);
-  cudaFree(f->w_packed);
-  cudaFree(f->w_tc);
-  cudaFree(f->w_tc2);
-  cudaFree(f->bias);
-  cudaFree(f->w_head);
+  if (c) {
+    cudaStreamSynchronize(c->stream);
+    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head};
+    for (void* b : bufs)
+      if (b) cudaFreeAsync(b, c->stream);  // back to the pool, no device-wide sync
+  } else {
+    cudaDeviceSynchronize();
+    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head};
+    for (void* b : bufs)
+      if (b) cudaFreeAsync(b, 0);
+    cudaDeviceSynchronize();
+  }
   delete f;
 }
 
