@@ -235,6 +235,16 @@ int odc_profile_mlp(odc_ctx* ctx, const odc_field* field, int64_t n, int64_t* tr
 /* Same, labels only (u8), for host points. */
 int odc_eval_labels(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, uint8_t* labels);
 
+/* Mesh output formats (replaces occmesh.meshio.export_obj / export_ply,
+ * meshio.py:22-28 and :79-98).  Host-only, no context needed; vertices
+ * (n_vertices, 3) f64 and triangles (n_triangles, 3) int64, as in
+ * TriangleMesh.  OBJ bytes are identical to the reference writer (%.17g,
+ * 1-based faces); PLY is binary little-endian float32 / uchar+3 int32. */
+int odc_export_obj(const char* path, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                   int64_t n_triangles);
+int odc_export_ply(const char* path, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                   int64_t n_triangles);
+
 #ifdef __cplusplus
 }
 #endif
