@@ -235,6 +235,22 @@ int odc_profile_mlp(odc_ctx* ctx, const odc_field* field, int64_t n, int64_t* tr
 /* Same, labels only (u8), for host points. */
 int odc_eval_labels(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, uint8_t* labels);
 
+/* Mesh validation on the device (replaces occmesh.mesh.validate_manifold,
+ * mesh.py:91-150).  Triangles are host int64 (n_triangles, 3) indexing
+ * n_vertices vertices.  Counts come back in the report; the lists
+ * (non-manifold edges (a, b) a < b by key, pinched and isolated vertex ids,
+ * all ascending) are then copied with odc_validate_copy into caller buffers
+ * of those sizes.  Uses its own workspace: the context's last extraction
+ * stays readable. */
+typedef struct {
+  int32_t manifold, pad;
+  int64_t n_nonmanifold_edges, n_pinched_vertices, n_boundary_edges, n_isolated_vertices;
+} odc_manifold_report;
+int odc_validate_manifold(odc_ctx* ctx, const int64_t* triangles, int64_t n_triangles, int64_t n_vertices,
+                          odc_manifold_report* report);
+int odc_validate_copy(odc_ctx* ctx, int64_t* nonmanifold_edges, int64_t* pinched_vertices,
+                      int64_t* isolated_vertices);
+
 /* Mesh output formats (replaces occmesh.meshio.export_obj / export_ply,
  * meshio.py:22-28 and :79-98).  Host-only, no context needed; vertices
  * (n_vertices, 3) f64 and triangles (n_triangles, 3) int64, as in

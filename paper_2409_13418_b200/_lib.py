@@ -76,11 +76,18 @@ class SlabInfo(ctypes.Structure):
     ]
 
 
+class ManifoldReport(ctypes.Structure):
+    _fields_ = [("manifold", ctypes.c_int32), ("pad", ctypes.c_int32), ("n_nonmanifold_edges", ctypes.c_int64),
+                ("n_pinched_vertices", ctypes.c_int64), ("n_boundary_edges", ctypes.c_int64),
+                ("n_isolated_vertices", ctypes.c_int64)]
+
+
 EXPORTS = (
     "odc_version", "odc_create", "odc_destroy", "odc_last_error", "odc_set_stream", "odc_field_analytic",
     "odc_field_mlp", "odc_field_free", "odc_default_options", "odc_extract", "odc_copy_mesh", "odc_mesh_device",
     "odc_copy_array", "odc_eval_raw", "odc_eval_labels", "odc_set_param", "odc_extract_slab",
     "odc_slab_globalize", "odc_mesh_finish", "odc_profile_mlp", "odc_export_obj", "odc_export_ply",
+    "odc_validate_manifold", "odc_validate_copy",
 )
 
 _lib = None
@@ -122,6 +129,8 @@ def load():
         L.odc_slab_globalize.argtypes = [vp, i64, i64, i64, vp]
         L.odc_mesh_finish.argtypes = [vp, vp, i64, vp, i64, i64, vp, vp, i32, P(Stats)]
         L.odc_profile_mlp.argtypes = [vp, vp, i64, vp, i64]
+        L.odc_validate_manifold.argtypes = [vp, vp, i64, i64, P(ManifoldReport)]
+        L.odc_validate_copy.argtypes = [vp, vp, vp, vp]
         L.odc_export_obj.argtypes = [ctypes.c_char_p, vp, i64, vp, i64]
         L.odc_export_ply.argtypes = [ctypes.c_char_p, vp, i64, vp, i64]
         _lib = L

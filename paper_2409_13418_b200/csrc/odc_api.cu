@@ -109,6 +109,9 @@ struct odc_ctx {
   CellTabEntry* table = nullptr;
   unsigned long long* h_pinned = nullptr;  // small readback buffer
   char* h_stage = nullptr;  // grow-only pinned staging for mesh copy-back
+  // mesh validation (its own workspace: the last extraction stays valid)
+  Arena varena;
+  std::vector<int64_t> v_edges, v_pinched, v_isolated;
   size_t h_stage_bytes = 0;
   std::string err;
   int launches = 0;
@@ -1176,6 +1179,117 @@ int odc_copy_mesh(odc_ctx* c, int32_t which, double* vertices, int64_t* triangle
     }
     return (int)ODC_OK;
   }, &a);
+}
+
+struct ValidateArgs {
+  const int64_t* tris;
+  int64_t T, V;
+  odc_manifold_report* out;
+};
+
+int odc_validate_manifold(odc_ctx* c, const int64_t* triangles, int64_t n_triangles, int64_t n_vertices,
+                          odc_manifold_report* out) {
+  if (!c || !out || n_triangles < 0 || n_vertices < 0 || (n_triangles && !triangles)) return ODC_E_ARG;
+  if (n_vertices >= INT32_MAX || 3 * n_triangles >= INT32_MAX) {
+    c->err = "validate_manifold: mesh too large for 32-bit fans";
+    return ODC_E_ARG;
+  }
+  ValidateArgs a{triangles, n_triangles, n_vertices, out};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    ValidateArgs* x = (ValidateArgs*)p;
+    std::memset(x->out, 0, sizeof *x->out);
+    cc->v_edges.clear();
+    cc->v_pinched.clear();
+    cc->v_isolated.clear();
+    if (x->T == 0) {  // mesh.py:97-98: an empty mesh is reported manifold, nothing else
+      x->out->manifold = 1;
+      return (int)ODC_OK;
+    }
+    Arena& A = cc->varena;
+    A.reset();
+    cudaStream_t s = cc->stream;
+    const int64_t T = x->T, V = x->V, n3 = 3 * T;
+    int64_t* t64 = need(A.get<int64_t>(n3));
+    int32_t* t = need(A.get<int32_t>(n3));
+    uint32_t* bad = need(A.get<uint32_t>(2));
+    unsigned long long* totals = need(A.get<unsigned long long>(8));
+    CUDA_TRY(cudaMemcpyAsync(t64, x->tris, 8 * n3, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(bad, 0, 8, s));
+    launch_narrow_tris(t64, n3, t, V, bad, s);
+    check_launch(cc);
+    readback(cc, bad, 4);
+    if (((uint32_t*)cc->h_pinned)[0]) throw OdcError{ODC_E_VALUE, "triangle index out of range"};
+    uint32_t* deg = need(A.get<uint32_t>(V + 1));
+    uint32_t* off = need(A.get<uint32_t>(V + 1));
+    uint32_t* cursor = need(A.get<uint32_t>(V));
+    int32_t* inc = need(A.get<int32_t>(n3));
+    CUDA_TRY(cudaMemsetAsync(deg, 0, 4 * (V + 1), s));
+    CUDA_TRY(cudaMemsetAsync(cursor, 0, 4 * V, s));
+    launch_vertex_degree(t, T, deg, s);
+    check_launch(cc);
+    auto scan = [&](const uint32_t* in, uint32_t* o, int64_t n, unsigned long long* tot) {
+      const uint32_t* ins[1] = {in};
+      uint32_t* outs[1] = {o};
+      uint32_t* tiles = need(A.get<uint32_t>((n + 255) / 256 + 1));
+      launch_scan_u32(ins, outs, 1, n, tiles, tot, s);
+      check_launch(cc, 3);
+    };
+    scan(deg, off, V + 1, totals + 0);
+    launch_vertex_fill(t, T, off, cursor, inc, s);
+    check_launch(cc);
+    int32_t* nbv = need(A.get<int32_t>(2 * n3));
+    uint32_t* nbc = need(A.get<uint32_t>(2 * n3));
+    uint32_t* nbt = need(A.get<uint32_t>(2 * n3));
+    uint32_t* uf = need(A.get<uint32_t>(n3));
+    uint32_t* per[5];
+    for (auto& q : per) q = need(A.get<uint32_t>(V + 1));
+    uint32_t *n_nb = per[0], *n_nm = per[1], *n_bd = per[2], *pin = per[3], *iso = per[4];
+    launch_manifold_vertex(V, t, off, inc, nbv, nbc, nbt, uf, n_nb, n_nm, n_bd, pin, iso, s);
+    check_launch(cc);
+    uint32_t* nm_off = need(A.get<uint32_t>(V + 1));
+    uint32_t* bd_off = need(A.get<uint32_t>(V + 1));
+    uint32_t* pin_off = need(A.get<uint32_t>(V + 1));
+    uint32_t* iso_off = need(A.get<uint32_t>(V + 1));
+    scan(n_nm, nm_off, V, totals + 1);
+    scan(n_bd, bd_off, V, totals + 2);
+    scan(pin, pin_off, V, totals + 3);
+    scan(iso, iso_off, V, totals + 4);
+    readback(cc, totals + 1, 4 * sizeof(unsigned long long));
+    const int64_t n_nm_t = (int64_t)cc->h_pinned[0], n_bd_t = (int64_t)cc->h_pinned[1],
+                  n_pin_t = (int64_t)cc->h_pinned[2], n_iso_t = (int64_t)cc->h_pinned[3];
+    int64_t* e_out = need(A.get<int64_t>(2 * n_nm_t + 1));
+    int64_t* p_out = need(A.get<int64_t>(n_pin_t + 1));
+    int64_t* i_out = need(A.get<int64_t>(n_iso_t + 1));
+    launch_manifold_emit(V, off, nbv, nbc, n_nb, n_nm, nm_off, e_out, s);
+    launch_emit_flagged(V, pin, pin_off, p_out, s);
+    launch_emit_flagged(V, iso, iso_off, i_out, s);
+    check_launch(cc, 3);
+    cc->v_edges.resize(2 * n_nm_t);
+    cc->v_pinched.resize(n_pin_t);
+    cc->v_isolated.resize(n_iso_t);
+    if (n_nm_t) CUDA_TRY(cudaMemcpyAsync(cc->v_edges.data(), e_out, 16 * n_nm_t, cudaMemcpyDeviceToHost, s));
+    if (n_pin_t) CUDA_TRY(cudaMemcpyAsync(cc->v_pinched.data(), p_out, 8 * n_pin_t, cudaMemcpyDeviceToHost, s));
+    if (n_iso_t) CUDA_TRY(cudaMemcpyAsync(cc->v_isolated.data(), i_out, 8 * n_iso_t, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    x->out->manifold = n_nm_t == 0 && n_pin_t == 0;
+    x->out->n_nonmanifold_edges = n_nm_t;
+    x->out->n_pinched_vertices = n_pin_t;
+    x->out->n_boundary_edges = n_bd_t;
+    x->out->n_isolated_vertices = n_iso_t;
+    return (int)ODC_OK;
+  }, &a);
+}
+
+int odc_validate_copy(odc_ctx* c, int64_t* nonmanifold_edges, int64_t* pinched_vertices, int64_t* isolated_vertices) {
+  if (!c) return ODC_E_ARG;
+  if (nonmanifold_edges && !c->v_edges.empty())
+    std::memcpy(nonmanifold_edges, c->v_edges.data(), 8 * c->v_edges.size());
+  if (pinched_vertices && !c->v_pinched.empty())
+    std::memcpy(pinched_vertices, c->v_pinched.data(), 8 * c->v_pinched.size());
+  if (isolated_vertices && !c->v_isolated.empty())
+    std::memcpy(isolated_vertices, c->v_isolated.data(), 8 * c->v_isolated.size());
+  return ODC_OK;
 }
 
 int odc_mesh_device(odc_ctx* c, int32_t which, const double** v, const int32_t** t, int64_t* nv, int64_t* nt) {

@@ -170,6 +170,16 @@ void launch_widen_i32(const int32_t* src, int64_t* dst, int64_t n, cudaStream_t 
 // provenance of repair duplicates [V0, V): kind 2, ref (-1, -1) (polygonize.py:348-373)
 void launch_dup_provenance(int64_t V0, int64_t V, int64_t* kind, int64_t* ref, cudaStream_t s);
 
+// mesh validation (odc_validate.cu; mesh.py:91-150)
+void launch_manifold_vertex(int64_t V, const int32_t* tris, const uint32_t* off, const int32_t* inc, int32_t* nbv,
+                            uint32_t* nbc, uint32_t* nbt, uint32_t* uf, uint32_t* n_nb, uint32_t* n_nm,
+                            uint32_t* n_bd, uint32_t* pinched, uint32_t* isolated, cudaStream_t s);
+void launch_manifold_emit(int64_t V, const uint32_t* off, const int32_t* nbv, const uint32_t* nbc,
+                          const uint32_t* n_nb, const uint32_t* n_nm, const uint32_t* nm_off, int64_t* edges,
+                          cudaStream_t s);
+void launch_emit_flagged(int64_t V, const uint32_t* flag, const uint32_t* pos, int64_t* out, cudaStream_t s);
+void launch_narrow_tris(const int64_t* in, int64_t n, int32_t* out, int64_t V, uint32_t* bad, cudaStream_t s);
+
 // provenance (mesh.py:11-20)
 void launch_provenance(int64_t V, int64_t P, const int64_t* src_of, const int64_t* part_cell,
                        const int64_t* part_index, const int64_t* fan_edge, int64_t* kind, int64_t* ref,

@@ -8,6 +8,7 @@ conventions: vertex id x + y*S + z*S^2, h = (hi - lo) / R).
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -95,3 +96,43 @@ class TriangleMesh:
             return 0
         n_edges = len(np.unique(self.undirected_edges(), axis=0))
         return self.n_vertices - n_edges + self.n_triangles
+
+
+@dataclass
+class ManifoldReport:
+    """validate_manifold's result (mesh.py:79-88 of the reference)."""
+
+    manifold: bool
+    nonmanifold_edges: list
+    pinched_vertices: list
+    boundary_edges: int
+    isolated_vertices: list
+
+    def __bool__(self):
+        return self.manifold
+
+
+def validate_manifold(mesh, device=0):
+    """Edge incidence (at most two triangles per edge) and fan connectivity,
+    computed on the GPU (libodc ``odc_validate_manifold``); same report as
+    occmesh.mesh.validate_manifold (mesh.py:91-150): non-manifold edges as
+    (a, b) with a < b in key order, pinched and isolated vertex ids ascending,
+    the boundary-edge count."""
+    from . import _lib
+
+    ctx = _lib.context(device)
+    L = _lib.load()
+    t = np.ascontiguousarray(mesh.triangles, dtype=np.int64).reshape(-1, 3)
+    rep = _lib.ManifoldReport()
+    rc = L.odc_validate_manifold(ctx.handle, t.ctypes.data if len(t) else None, len(t), int(len(mesh.vertices)),
+                                 ctypes.byref(rep))
+    if rc != _lib.ODC_OK:
+        msg = L.odc_last_error(ctx.handle).decode()
+        raise (ValueError(msg) if rc == _lib.ODC_E_VALUE else RuntimeError(msg))
+    e = np.empty((rep.n_nonmanifold_edges, 2), dtype=np.int64)
+    p = np.empty(rep.n_pinched_vertices, dtype=np.int64)
+    iso = np.empty(rep.n_isolated_vertices, dtype=np.int64)
+    ptr = lambda a: a.ctypes.data if a.size else None  # noqa: E731
+    L.odc_validate_copy(ctx.handle, ptr(e), ptr(p), ptr(iso))
+    return ManifoldReport(bool(rep.manifold), [(int(a), int(b)) for a, b in e.tolist()], p.tolist(),
+                          int(rep.n_boundary_edges), iso.tolist())

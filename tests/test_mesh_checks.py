@@ -1,0 +1,96 @@
+"""Mesh validation (occmesh.mesh.validate_manifold, mesh.py:91-150): the CPU
+oracle is pinned to the reference's outputs (tests/golden/checks.json); the
+GPU implementation must match both exactly."""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import mesh_checks
+from paper_2409_13418_b200 import TriangleMesh
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+CHECKS = json.loads((GOLDEN / "checks.json").read_text())
+
+
+def golden_mesh(name):
+    syn = np.load(GOLDEN / "checks_meshes.npz")
+    if f"{name}_v" in syn:
+        return syn[f"{name}_v"], syn[f"{name}_t"]
+    raw = name.endswith("_raw")
+    d = np.load(GOLDEN / f"{name[:-4] if raw else name}.npz")
+    return (d["raw_vertices"], d["raw_triangles"]) if raw else (d["vertices"], d["triangles"])
+
+
+def as_tuple(r):
+    return (bool(r.manifold), [list(e) for e in r.nonmanifold_edges], list(r.pinched_vertices),
+            int(r.boundary_edges), list(r.isolated_vertices))
+
+
+def golden_tuple(g):
+    return (g["manifold"], g["nonmanifold_edges"], g["pinched_vertices"], g["boundary_edges"],
+            g["isolated_vertices"])
+
+
+@pytest.mark.parametrize("name", sorted(CHECKS))
+def test_oracle_validate_manifold_matches_reference(name):
+    v, t = golden_mesh(name)
+    assert mesh_checks.validate_manifold(v, t) == golden_tuple(CHECKS[name])
+
+
+def random_soup(seed, nv=300, nt=900):
+    """Triangles over few vertices: many shared edges (multiplicity > 2),
+    pinched fans, boundary edges and isolated vertices."""
+    rng = np.random.default_rng(seed)
+    t = rng.integers(0, nv - 20, size=(nt, 3))
+    t = t[(t[:, 0] != t[:, 1]) & (t[:, 1] != t[:, 2]) & (t[:, 0] != t[:, 2])]
+    return rng.random((nv, 3)), t
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(CHECKS))
+def test_gpu_validate_manifold_matches_reference(name):
+    from paper_2409_13418_b200.mesh import validate_manifold
+
+    v, t = golden_mesh(name)
+    assert as_tuple(validate_manifold(TriangleMesh.trusted(v, t))) == golden_tuple(CHECKS[name])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_gpu_validate_manifold_random_soups(seed):
+    from paper_2409_13418_b200.mesh import validate_manifold
+
+    v, t = random_soup(seed, nv=60 + 200 * seed, nt=200 + 3000 * seed)
+    assert as_tuple(validate_manifold(TriangleMesh.trusted(v, t))) == mesh_checks.validate_manifold(v, t)
+
+
+@pytest.mark.gpu
+def test_gpu_validate_manifold_edge_cases():
+    from paper_2409_13418_b200.mesh import validate_manifold
+
+    empty = TriangleMesh(np.zeros((5, 3)), np.zeros((0, 3), dtype=np.int64))
+    assert as_tuple(validate_manifold(empty)) == (True, [], [], 0, [])
+    bad = TriangleMesh.trusted(np.zeros((3, 3)), np.array([[0, 1, 3]]))
+    with pytest.raises(ValueError):
+        validate_manifold(bad)
+    # one vertex with a 400-triangle fan (a fan-triangulated disk)
+    n = 400
+    ang = np.linspace(0, 2 * np.pi, n, endpoint=False)
+    v = np.concatenate([[[0, 0, 0]], np.stack([np.cos(ang), np.sin(ang), 0 * ang], 1)])
+    t = np.stack([np.zeros(n, int), 1 + np.arange(n), 1 + (np.arange(n) + 1) % n], 1)
+    assert as_tuple(validate_manifold(TriangleMesh.trusted(v, t))) == mesh_checks.validate_manifold(v, t)
+
+
+@pytest.mark.gpu
+def test_gpu_validate_extraction_mesh_keeps_context_result():
+    """Validation runs in its own workspace: the last extraction stays readable."""
+    from paper_2409_13418_b200 import GridSpec, SphereField, contour
+    from paper_2409_13418_b200.mesh import validate_manifold
+
+    res = contour(SphereField((0.5, 0.5, 0.5), 0.3), GridSpec((0, 0, 0), (1, 1, 1), 96))
+    rep = validate_manifold(res.mesh)
+    assert rep.manifold and rep.boundary_edges == 0 and not rep.isolated_vertices
+    assert as_tuple(rep) == mesh_checks.validate_manifold(res.mesh.vertices, res.mesh.triangles)
