@@ -251,6 +251,16 @@ int odc_validate_manifold(odc_ctx* ctx, const int64_t* triangles, int64_t n_tria
 int odc_validate_copy(odc_ctx* ctx, int64_t* nonmanifold_edges, int64_t* pinched_vertices,
                       int64_t* isolated_vertices);
 
+/* Self-intersection count on the device (replaces
+ * occmesh.mesh.count_self_intersections(mesh, tolerance, return_pairs),
+ * mesh.py:395-487): triangle pairs with positive-measure intersection, pairs
+ * sharing a vertex or involving a degenerate triangle excluded, decided in
+ * the reference's fp64 arithmetic order.  The sorted (a, b) pairs of the last
+ * call are copied with odc_self_intersection_pairs into a (count, 2) buffer. */
+int odc_count_self_intersections(odc_ctx* ctx, const double* vertices, int64_t n_vertices,
+                                 const int64_t* triangles, int64_t n_triangles, double tolerance, int64_t* count);
+int odc_self_intersection_pairs(odc_ctx* ctx, int64_t* pairs);
+
 /* Mesh output formats (replaces occmesh.meshio.export_obj / export_ply,
  * meshio.py:22-28 and :79-98).  Host-only, no context needed; vertices
  * (n_vertices, 3) f64 and triangles (n_triangles, 3) int64, as in

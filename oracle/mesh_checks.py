@@ -11,6 +11,11 @@ tests/golden/make_checks_golden.py).
   per-vertex union of incident triangles through shared neighbour vertices
   (more than one component = pinched), unused vertices = isolated; an empty
   triangle list is reported manifold with empty lists.
+* count_self_intersections -- mesh.py:395-487 with _tri_tri_cross
+  (:300-349) and _coplanar_overlap_area (:368-392): unit-box normalisation,
+  uniform-hash broad phase (cell = 1.0001 x the largest triangle box side),
+  vertex-sharing / degenerate / box rejects, exact interval test in numpy
+  fp64 (same expression order), coplanar pairs by clipped overlap area.
 """
 
 from __future__ import annotations
@@ -68,3 +73,139 @@ def validate_manifold(vertices, triangles):
     used[t.reshape(-1)] = True
     isolated = np.nonzero(~used)[0].tolist()
     return (not nonmanifold and not pinched), [list(e) for e in nonmanifold], pinched, boundary, isolated
+
+
+def _cross(a, b):
+    return np.stack([a[:, 1] * b[:, 2] - a[:, 2] * b[:, 1],
+                     a[:, 2] * b[:, 0] - a[:, 0] * b[:, 2],
+                     a[:, 0] * b[:, 1] - a[:, 1] * b[:, 0]], axis=1)
+
+
+def _dot(a, b):  # numpy's 3-term einsum('ij,ij->i') order: (p0 + p2) + p1
+    return (a[:, 0] * b[:, 0] + a[:, 2] * b[:, 2]) + a[:, 1] * b[:, 1]
+
+
+def _norm(a):  # np.linalg.norm(axis=1) order: (x0^2 + x1^2) + x2^2
+    return np.sqrt((a[:, 0] * a[:, 0] + a[:, 1] * a[:, 1]) + a[:, 2] * a[:, 2])
+
+
+def _pair_test(P, Q, tol):
+    """(crossing, coplanar) per pair, arrays of (n, 3, 3) corners."""
+    n1 = _cross(P[:, 1] - P[:, 0], P[:, 2] - P[:, 0])
+    n2 = _cross(Q[:, 1] - Q[:, 0], Q[:, 2] - Q[:, 0])
+    dq = np.stack([_dot(Q[:, k] - P[:, 0], n1) for k in range(3)], axis=1)
+    dp = np.stack([_dot(P[:, k] - Q[:, 0], n2) for k in range(3)], axis=1)
+    tq = tol * np.maximum(_norm(n1), 1e-300)[:, None]
+    tp = tol * np.maximum(_norm(n2), 1e-300)[:, None]
+    sep = (dq > tq).all(1) | (dq < -tq).all(1) | (dp > tp).all(1) | (dp < -tp).all(1)
+    cop = (np.abs(dq) <= tq).all(1) & (np.abs(dp) <= tp).all(1)
+    d = _cross(n1, n2)
+    ax = np.argmax(np.abs(d), axis=1)
+
+    def span(T, dist, tl):
+        pr = T[np.arange(len(T)), :, ax]
+        sg = np.where(dist > tl, 1, -1)
+        lo = np.full(len(T), np.inf)
+        hi = np.full(len(T), -np.inf)
+        for i in range(3):
+            j = (i + 1) % 3
+            m = sg[:, i] * sg[:, j] < 0
+            df = dist[:, i] - dist[:, j]
+            with np.errstate(divide="ignore", invalid="ignore"):
+                tt = pr[:, i] + (pr[:, j] - pr[:, i]) * (dist[:, i] / np.where(np.abs(df) < 1e-300, 1.0, df))
+            lo = np.where(m, np.minimum(lo, tt), lo)
+            hi = np.where(m, np.maximum(hi, tt), hi)
+        return lo, hi
+
+    with np.errstate(invalid="ignore"):
+        l1, h1 = span(Q, dq, tq)
+        l2, h2 = span(P, dp, tp)
+        ov = np.minimum(h1, h2) - np.maximum(l1, l2)
+        crossing = ~sep & ~cop & (ov > tol) & np.isfinite(ov)
+    return crossing, cop & ~sep
+
+
+def _clip_left(poly, a, b):
+    out = []
+    for i in range(len(poly)):
+        c, n = poly[i], poly[(i + 1) % len(poly)]
+        sc = (b[0] - a[0]) * (c[1] - a[1]) - (b[1] - a[1]) * (c[0] - a[0])
+        sn = (b[0] - a[0]) * (n[1] - a[1]) - (b[1] - a[1]) * (n[0] - a[0])
+        if sc >= 0:
+            out.append(c)
+        if sc * sn < 0:
+            tt = sc / (sc - sn)
+            out.append((c[0] + tt * (n[0] - c[0]), c[1] + tt * (n[1] - c[1])))
+    return out
+
+
+def _coplanar_area(P, Q):
+    p = [np.float64(x) for x in P.reshape(-1)]
+    u = [p[3] - p[0], p[4] - p[1], p[5] - p[2]]
+    w = [p[6] - p[0], p[7] - p[1], p[8] - p[2]]
+    n = [u[1] * w[2] - u[2] * w[1], u[2] * w[0] - u[0] * w[2], u[0] * w[1] - u[1] * w[0]]
+    ax = int(np.argmax(np.abs(n)))
+    k0, k1 = [k for k in range(3) if k != ax]
+    A = [(P[i, k0], P[i, k1]) for i in range(3)]
+    B = [(Q[i, k0], Q[i, k1]) for i in range(3)]
+    if n[ax] < 0:
+        A = A[::-1]
+    nb = (B[1][0] - B[0][0]) * (B[2][1] - B[0][1]) - (B[1][1] - B[0][1]) * (B[2][0] - B[0][0])
+    if nb < 0:
+        B = B[::-1]
+    poly = B
+    for i in range(3):
+        poly = _clip_left(poly, A[i], A[(i + 1) % 3])
+        if len(poly) < 3:
+            return 0.0
+    area = 0.0
+    for i in range(1, len(poly) - 1):
+        area += 0.5 * abs((poly[i][0] - poly[0][0]) * (poly[i + 1][1] - poly[0][1])
+                          - (poly[i + 1][0] - poly[0][0]) * (poly[i][1] - poly[0][1]))
+    return area
+
+
+def count_self_intersections(vertices, triangles, tolerance=1e-12):
+    """Sorted list of intersecting (a, b) triangle pairs, a < b."""
+    V = np.asarray(vertices, dtype=np.float64).reshape(-1, 3)
+    T = np.asarray(triangles, dtype=np.int64).reshape(-1, 3)
+    nt = len(T)
+    if nt < 2:
+        return []
+    lo = V.min(axis=0)
+    ext = float((V.max(axis=0) - lo).max()) or 1.0
+    C = ((V - lo) / ext)[T]
+    degen = 0.5 * _norm(_cross(C[:, 1] - C[:, 0], C[:, 2] - C[:, 0])) < 1e-20
+    blo, bhi = C.min(axis=1), C.max(axis=1)
+    cell = max(float((bhi - blo).max()) * 1.0001, 1e-9)
+    ns = int(1.0 / cell) + 3
+    ilo = np.floor(blo / cell).astype(np.int64)
+    ihi = np.floor(bhi / cell).astype(np.int64)
+    cells = {}
+    for c in range(8):
+        ix = ihi[:, 0] if c & 4 else ilo[:, 0]
+        iy = ihi[:, 1] if c & 2 else ilo[:, 1]
+        iz = ihi[:, 2] if c & 1 else ilo[:, 2]
+        for tri, key in enumerate(((ix * ns + iy) * ns + iz).tolist()):
+            cells.setdefault(key, set()).add(tri)
+    cand = set()
+    for members in cells.values():
+        m = sorted(members)
+        for i in range(len(m)):
+            for j in range(i + 1, len(m)):
+                cand.add((m[i], m[j]))
+    if not cand:
+        return []
+    pa, pb = np.array(sorted(cand), dtype=np.int64).T
+    share = (T[pa][:, :, None] == T[pb][:, None, :]).any(axis=(1, 2))
+    keep = ~share & ~degen[pa] & ~degen[pb]
+    keep &= ((blo[pa] <= bhi[pb] + tolerance) & (blo[pb] <= bhi[pa] + tolerance)).all(axis=1)
+    pa, pb = pa[keep], pb[keep]
+    if len(pa) == 0:
+        return []
+    crossing, cop = _pair_test(C[pa], C[pb], tolerance)
+    hits = [(int(a), int(b)) for a, b in zip(pa[crossing], pb[crossing])]
+    for i in np.nonzero(cop)[0]:
+        if _coplanar_area(C[pa[i]], C[pb[i]]) > tolerance:
+            hits.append((int(pa[i]), int(pb[i])))
+    return sorted(hits)

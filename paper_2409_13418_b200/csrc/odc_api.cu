@@ -112,6 +112,7 @@ struct odc_ctx {
   // mesh validation (its own workspace: the last extraction stays valid)
   Arena varena;
   std::vector<int64_t> v_edges, v_pinched, v_isolated;
+  std::vector<int64_t> v_si_pairs;
   size_t h_stage_bytes = 0;
   std::string err;
   int launches = 0;
@@ -1289,6 +1290,81 @@ int odc_validate_copy(odc_ctx* c, int64_t* nonmanifold_edges, int64_t* pinched_v
     std::memcpy(pinched_vertices, c->v_pinched.data(), 8 * c->v_pinched.size());
   if (isolated_vertices && !c->v_isolated.empty())
     std::memcpy(isolated_vertices, c->v_isolated.data(), 8 * c->v_isolated.size());
+  return ODC_OK;
+}
+
+struct SelfxArgs {
+  const double* v;
+  int64_t nv;
+  const int64_t* t;
+  int64_t nt;
+  double tol;
+  int64_t* count;
+};
+
+int odc_count_self_intersections(odc_ctx* c, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                                 int64_t n_triangles, double tolerance, int64_t* count) {
+  if (!c || !count || n_vertices < 0 || n_triangles < 0 || (n_vertices && !vertices) || (n_triangles && !triangles))
+    return ODC_E_ARG;
+  if (n_vertices >= INT32_MAX || n_triangles >= INT32_MAX / 8) {
+    c->err = "count_self_intersections: mesh too large";
+    return ODC_E_ARG;
+  }
+  SelfxArgs a{vertices, n_vertices, triangles, n_triangles, tolerance, count};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    SelfxArgs* x = (SelfxArgs*)p;
+    *x->count = 0;
+    cc->v_si_pairs.clear();
+    if (x->nt < 2) return (int)ODC_OK;  // mesh.py:423-424
+    Arena& A = cc->varena;
+    cudaStream_t s = cc->stream;
+    const int64_t n3 = 3 * x->nt;
+    double* dv = nullptr;
+    int32_t* t = nullptr;
+    auto upload = [&]() {
+      A.reset();
+      dv = need(A.get<double>(3 * x->nv));
+      int64_t* t64 = need(A.get<int64_t>(n3));
+      t = need(A.get<int32_t>(n3));
+      uint32_t* bad = need(A.get<uint32_t>(2));
+      CUDA_TRY(cudaMemcpyAsync(dv, x->v, 24 * x->nv, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(t64, x->t, 8 * n3, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemsetAsync(bad, 0, 8, s));
+      launch_narrow_tris(t64, n3, t, x->nv, bad, s);
+      check_launch(cc);
+      readback(cc, bad, 4);
+      if (((uint32_t*)cc->h_pinned)[0]) throw OdcError{ODC_E_VALUE, "triangle index out of range"};
+    };
+    auto alloc = [](void* ar, size_t n) -> void* { return ((Arena*)ar)->alloc(n); };
+    int64_t cap = 1 << 20, n_hits = 0;
+    for (;;) {
+      upload();
+      int64_t* hits = need(A.get<int64_t>(cap));
+      const int rc = self_intersections(dv, x->nv, t, x->nt, x->tol, alloc, &A, s, hits, cap, &n_hits);
+      if (rc != ODC_OK) throw OdcError{rc, "count_self_intersections failed"};
+      if (n_hits > cap) {  // rerun with room for every hit
+        cap = n_hits;
+        continue;
+      }
+      cc->v_si_pairs.resize(2 * n_hits);
+      std::vector<int64_t> keys(n_hits);
+      if (n_hits) CUDA_TRY(cudaMemcpyAsync(keys.data(), hits, 8 * n_hits, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      for (int64_t i = 0; i < n_hits; i++) {
+        cc->v_si_pairs[2 * i] = keys[i] / x->nt;
+        cc->v_si_pairs[2 * i + 1] = keys[i] % x->nt;
+      }
+      break;
+    }
+    *x->count = n_hits;
+    return (int)ODC_OK;
+  }, &a);
+}
+
+int odc_self_intersection_pairs(odc_ctx* c, int64_t* pairs) {
+  if (!c) return ODC_E_ARG;
+  if (pairs && !c->v_si_pairs.empty()) std::memcpy(pairs, c->v_si_pairs.data(), 8 * c->v_si_pairs.size());
   return ODC_OK;
 }
 

@@ -179,6 +179,11 @@ void launch_manifold_emit(int64_t V, const uint32_t* off, const int32_t* nbv, co
                           cudaStream_t s);
 void launch_emit_flagged(int64_t V, const uint32_t* flag, const uint32_t* pos, int64_t* out, cudaStream_t s);
 void launch_narrow_tris(const int64_t* in, int64_t n, int32_t* out, int64_t V, uint32_t* bad, cudaStream_t s);
+// count_self_intersections (odc_selfx.cu; mesh.py:395-487): hit keys a*nt+b
+// sorted into d_out_hits when their number fits cap; *n_hits always set
+int self_intersections(const double* d_v, int64_t nv, const int32_t* d_t, int64_t nt, double tol,
+                       void* (*alloc)(void*, size_t), void* actx, cudaStream_t s, int64_t* d_out_hits,
+                       int64_t cap, int64_t* n_hits);
 
 // provenance (mesh.py:11-20)
 void launch_provenance(int64_t V, int64_t P, const int64_t* src_of, const int64_t* part_cell,

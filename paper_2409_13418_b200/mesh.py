@@ -136,3 +136,29 @@ def validate_manifold(mesh, device=0):
     L.odc_validate_copy(ctx.handle, ptr(e), ptr(p), ptr(iso))
     return ManifoldReport(bool(rep.manifold), [(int(a), int(b)) for a, b in e.tolist()], p.tolist(),
                           int(rep.n_boundary_edges), iso.tolist())
+
+
+def count_self_intersections(mesh, tolerance=1e-12, return_pairs=False, device=0):
+    """Triangle pairs with positive-measure intersection, on the GPU (libodc
+    ``odc_count_self_intersections``); same contract as
+    occmesh.mesh.count_self_intersections (mesh.py:395-487): pairs sharing a
+    vertex or involving a degenerate triangle are excluded; with
+    ``return_pairs`` also the sorted list of (a, b) pairs."""
+    from . import _lib
+
+    ctx = _lib.context(device)
+    L = _lib.load()
+    v = np.ascontiguousarray(mesh.vertices, dtype=np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(mesh.triangles, dtype=np.int64).reshape(-1, 3)
+    n = ctypes.c_int64()
+    rc = L.odc_count_self_intersections(ctx.handle, v.ctypes.data if len(v) else None, len(v),
+                                        t.ctypes.data if len(t) else None, len(t), float(tolerance),
+                                        ctypes.byref(n))
+    if rc != _lib.ODC_OK:
+        msg = L.odc_last_error(ctx.handle).decode()
+        raise (ValueError(msg) if rc == _lib.ODC_E_VALUE else RuntimeError(msg))
+    if not return_pairs:
+        return int(n.value)
+    pairs = np.empty((n.value, 2), dtype=np.int64)
+    L.odc_self_intersection_pairs(ctx.handle, pairs.ctypes.data if n.value else None)
+    return int(n.value), [(int(a), int(b)) for a, b in pairs.tolist()]

@@ -94,3 +94,62 @@ def test_gpu_validate_extraction_mesh_keeps_context_result():
     rep = validate_manifold(res.mesh)
     assert rep.manifold and rep.boundary_edges == 0 and not rep.isolated_vertices
     assert as_tuple(rep) == mesh_checks.validate_manifold(res.mesh.vertices, res.mesh.triangles)
+
+
+# ---- count_self_intersections (mesh.py:395-487) ----------------------------
+@pytest.mark.parametrize("name", sorted(CHECKS))
+def test_oracle_self_intersections_match_reference(name):
+    v, t = golden_mesh(name)
+    assert [list(p) for p in mesh_checks.count_self_intersections(v, t)] == CHECKS[name]["si_pairs"]
+
+
+def crossing_soup(seed, n=400):
+    """Small random triangles in the unit box: many crossing pairs, a few
+    coplanar overlaps (copies shifted in-plane), shared-vertex pairs."""
+    rng = np.random.default_rng(seed)
+    c = rng.random((n, 3))
+    v = (c[:, None, :] + rng.normal(scale=0.04, size=(n, 3, 3))).reshape(-1, 3)
+    t = np.arange(3 * n).reshape(-1, 3)
+    k = n // 10  # coplanar partners: same plane, shifted inside it
+    base = v[: 3 * k].reshape(k, 3, 3)
+    shift = 0.3 * (base[:, 1] - base[:, 0]) + 0.2 * (base[:, 2] - base[:, 0])
+    cop = (base + shift[:, None, :]).reshape(-1, 3)
+    v = np.concatenate([v, cop])
+    t = np.concatenate([t, 3 * n + np.arange(3 * k).reshape(-1, 3)])
+    t[5] = [t[4][0], t[4][1], t[5][2]]  # two triangles sharing an edge
+    return v, t
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(CHECKS))
+def test_gpu_self_intersections_match_reference(name):
+    from paper_2409_13418_b200.mesh import count_self_intersections
+
+    v, t = golden_mesh(name)
+    n, pairs = count_self_intersections(TriangleMesh.trusted(v, t), return_pairs=True)
+    assert n == CHECKS[name]["si_count"] and [list(p) for p in pairs] == CHECKS[name]["si_pairs"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(4))
+def test_gpu_self_intersections_random(seed):
+    from paper_2409_13418_b200.mesh import count_self_intersections
+
+    v, t = crossing_soup(seed, n=200 + 300 * seed)
+    n, pairs = count_self_intersections(TriangleMesh.trusted(v, t), return_pairs=True)
+    want = mesh_checks.count_self_intersections(v, t)
+    assert n > 0 and pairs == want
+    assert count_self_intersections(TriangleMesh.trusted(v, t), tolerance=1e-3) == len(
+        mesh_checks.count_self_intersections(v, t, tolerance=1e-3))
+
+
+@pytest.mark.gpu
+def test_gpu_self_intersections_mlp_extraction():
+    from paper_2409_13418_b200 import GridSpec, MlpField, contour
+    from paper_2409_13418_b200.mesh import count_self_intersections
+
+    res = contour(MlpField(seed=0, amplitude=4.0), GridSpec((0, 0, 0), (1, 1, 1), 48))
+    m = res.mesh
+    n, pairs = count_self_intersections(m, return_pairs=True)
+    assert pairs == mesh_checks.count_self_intersections(m.vertices, m.triangles)
+    assert count_self_intersections(TriangleMesh(np.zeros((3, 3)), np.array([[0, 1, 2]]))) == 0
