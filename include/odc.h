@@ -261,6 +261,15 @@ int odc_count_self_intersections(odc_ctx* ctx, const double* vertices, int64_t n
                                  const int64_t* triangles, int64_t n_triangles, double tolerance, int64_t* count);
 int odc_self_intersection_pairs(odc_ctx* ctx, int64_t* pairs);
 
+/* Exact point-to-mesh distances on the device (replaces
+ * occmesh.mesh.MeshDistanceIndex(mesh).query(points), mesh.py:202-270):
+ * per point the distance, the closest triangle (smallest index on exact
+ * ties) and the closest point (n_points, 3); tri / closest may be NULL.
+ * The building block of the MD2 / HDD / NIC metrics (metrics.py:26-70). */
+int odc_mesh_distance(odc_ctx* ctx, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                      int64_t n_triangles, const double* points, int64_t n_points, double* dist, int64_t* tri,
+                      double* closest);
+
 /* Mesh output formats (replaces occmesh.meshio.export_obj / export_ply,
  * meshio.py:22-28 and :79-98).  Host-only, no context needed; vertices
  * (n_vertices, 3) f64 and triangles (n_triangles, 3) int64, as in

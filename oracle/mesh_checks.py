@@ -16,6 +16,11 @@ tests/golden/make_checks_golden.py).
   uniform-hash broad phase (cell = 1.0001 x the largest triangle box side),
   vertex-sharing / degenerate / box rejects, exact interval test in numpy
   fp64 (same expression order), coplanar pairs by clipped overlap area.
+* mesh_distance -- MeshDistanceIndex.query (mesh.py:202-270) by brute force:
+  Ericson's closest point (_closest_point_on_triangles, mesh.py:153-199) to
+  every triangle and the minimum distance; on exact ties the winner is the
+  first of the 8 nearest centroids attaining it (the reference's KD-tree
+  pass; equal centroid distances by index), else the smallest index.
 """
 
 from __future__ import annotations
@@ -209,3 +214,64 @@ def count_self_intersections(vertices, triangles, tolerance=1e-12):
         if _coplanar_area(C[pa[i]], C[pb[i]]) > tolerance:
             hits.append((int(pa[i]), int(pb[i])))
     return sorted(hits)
+
+
+def _closest(p, a, b, c):
+    """Ericson's region walk, vectorised, first matching region wins."""
+    ab, ac = b - a, c - a
+    ap, bp, cp = p - a, p - b, p - c
+    d1, d2 = _dot(ab, ap), _dot(ac, ap)
+    d3, d4 = _dot(ab, bp), _dot(ac, bp)
+    d5, d6 = _dot(ab, cp), _dot(ac, cp)
+    vc = d1 * d4 - d3 * d2
+    vb = d5 * d2 - d1 * d6
+    va = d3 * d6 - d5 * d4
+
+    def safe(x):
+        return np.where(np.abs(x) < 1e-300, 1.0, x)
+
+    with np.errstate(divide="ignore", invalid="ignore"):
+        e43, e56 = d4 - d3, d5 - d6
+        den = safe((va + vb) + vc)
+        choices = [
+            ((d1 <= 0) & (d2 <= 0), a),
+            ((d3 >= 0) & (d4 <= d3), b),
+            ((vc <= 0) & (d1 >= 0) & (d3 <= 0), a + ab * np.clip(d1 / safe(d1 - d3), 0, 1)[:, None]),
+            ((d6 >= 0) & (d5 <= d6), c),
+            ((vb <= 0) & (d2 >= 0) & (d6 <= 0), a + ac * np.clip(d2 / safe(d2 - d6), 0, 1)[:, None]),
+            ((va <= 0) & (e43 >= 0) & (e56 >= 0), b + (c - b) * np.clip(e43 / safe(e43 + e56), 0, 1)[:, None]),
+        ]
+        out = a + ab * (vb / den)[:, None] + ac * (vc / den)[:, None]
+    for m, val in reversed(choices):
+        out = np.where(m[:, None], val, out)
+    return out
+
+
+def mesh_distance(vertices, triangles, points, chunk=256):
+    """(distance, triangle, closest point) per query point, exact."""
+    V = np.asarray(vertices, dtype=np.float64)
+    T = np.asarray(triangles, dtype=np.int64)
+    P = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    A, B, C = V[T[:, 0]], V[T[:, 1]], V[T[:, 2]]
+    nt = len(T)
+    dist = np.empty(len(P))
+    tri = np.empty(len(P), dtype=np.int64)
+    cpo = np.empty((len(P), 3))
+    for s in range(0, len(P), chunk):
+        q = P[s:s + chunk]
+        qq = np.repeat(q, nt, axis=0)
+        cp = _closest(qq, np.tile(A, (len(q), 1)), np.tile(B, (len(q), 1)), np.tile(C, (len(q), 1)))
+        d = _norm(cp - qq).reshape(len(q), nt)
+        k = np.argmin(d, axis=1)  # first minimum = smallest index on ties
+        cen = (((A + B) + C) / 3.0)
+        for r in range(len(q)):
+            e = cen - q[r]
+            d2 = (e[:, 0] * e[:, 0] + e[:, 1] * e[:, 1]) + e[:, 2] * e[:, 2]
+            near = np.argsort(d2, kind="stable")[: min(8, nt)]
+            hit = near[d[r, near] == d[r, k[r]]]
+            if len(hit):
+                k[r] = hit[0]
+        dist[s:s + chunk] = d[np.arange(len(q)), k]
+        tri[s:s + chunk] = k
+        cpo[s:s + chunk] = cp.reshape(len(q), nt, 3)[np.arange(len(q)), k]
+    return dist, tri, cpo

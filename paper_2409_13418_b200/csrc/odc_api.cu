@@ -1362,6 +1362,67 @@ int odc_count_self_intersections(odc_ctx* c, const double* vertices, int64_t n_v
   }, &a);
 }
 
+struct DistArgs {
+  const double* v;
+  int64_t nv;
+  const int64_t* t;
+  int64_t nt;
+  const double* q;
+  int64_t nq;
+  double* dist;
+  int64_t* tri;
+  double* cp;
+};
+
+int odc_mesh_distance(odc_ctx* c, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                      int64_t n_triangles, const double* points, int64_t n_points, double* dist, int64_t* tri,
+                      double* closest) {
+  if (!c || n_vertices < 0 || n_triangles < 0 || n_points < 0 || (n_points && (!points || !dist))) return ODC_E_ARG;
+  if (n_triangles == 0 || !vertices || !triangles) {
+    c->err = "distance index needs a non-empty mesh";
+    return ODC_E_VALUE;
+  }
+  if (n_vertices >= INT32_MAX || 3 * n_triangles >= INT32_MAX) {
+    c->err = "mesh_distance: mesh too large";
+    return ODC_E_ARG;
+  }
+  DistArgs a{vertices, n_vertices, triangles, n_triangles, points, n_points, dist, tri, closest};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    DistArgs* x = (DistArgs*)p;
+    if (x->nq == 0) return (int)ODC_OK;
+    Arena& A = cc->varena;
+    A.reset();
+    cudaStream_t s = cc->stream;
+    const int64_t n3 = 3 * x->nt;
+    double* dv = need(A.get<double>(3 * x->nv));
+    int64_t* t64 = need(A.get<int64_t>(n3));
+    int32_t* t = need(A.get<int32_t>(n3));
+    uint32_t* bad = need(A.get<uint32_t>(2));
+    double* dq = need(A.get<double>(3 * x->nq));
+    double* dd = need(A.get<double>(x->nq));
+    int64_t* dt = need(A.get<int64_t>(x->nq));
+    double* dc = need(A.get<double>(3 * x->nq));
+    CUDA_TRY(cudaMemcpyAsync(dv, x->v, 24 * x->nv, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(t64, x->t, 8 * n3, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(dq, x->q, 24 * x->nq, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(bad, 0, 8, s));
+    launch_narrow_tris(t64, n3, t, x->nv, bad, s);
+    check_launch(cc);
+    readback(cc, bad, 4);
+    if (((uint32_t*)cc->h_pinned)[0]) throw OdcError{ODC_E_VALUE, "triangle index out of range"};
+    auto alloc = [](void* ar, size_t n) -> void* { return ((Arena*)ar)->alloc(n); };
+    const int rc = mesh_distance(dv, t, x->nt, dq, x->nq, alloc, &A, s, dd, dt, dc);
+    if (rc != ODC_OK) throw OdcError{rc, "mesh_distance failed"};
+    cc->launches += 5;
+    CUDA_TRY(cudaMemcpyAsync(x->dist, dd, 8 * x->nq, cudaMemcpyDeviceToHost, s));
+    if (x->tri) CUDA_TRY(cudaMemcpyAsync(x->tri, dt, 8 * x->nq, cudaMemcpyDeviceToHost, s));
+    if (x->cp) CUDA_TRY(cudaMemcpyAsync(x->cp, dc, 24 * x->nq, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return (int)ODC_OK;
+  }, &a);
+}
+
 int odc_self_intersection_pairs(odc_ctx* c, int64_t* pairs) {
   if (!c) return ODC_E_ARG;
   if (pairs && !c->v_si_pairs.empty()) std::memcpy(pairs, c->v_si_pairs.data(), 8 * c->v_si_pairs.size());

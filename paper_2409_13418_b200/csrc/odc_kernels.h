@@ -179,6 +179,10 @@ void launch_manifold_emit(int64_t V, const uint32_t* off, const int32_t* nbv, co
                           cudaStream_t s);
 void launch_emit_flagged(int64_t V, const uint32_t* flag, const uint32_t* pos, int64_t* out, cudaStream_t s);
 void launch_narrow_tris(const int64_t* in, int64_t n, int32_t* out, int64_t V, uint32_t* bad, cudaStream_t s);
+// exact point-to-mesh distance (odc_distance.cu; mesh.py:153-270)
+int mesh_distance(const double* d_v, const int32_t* d_t, int64_t nt, const double* d_q, int64_t nq,
+                  void* (*alloc)(void*, size_t), void* actx, cudaStream_t s, double* d_dist, int64_t* d_tri,
+                  double* d_cp);
 // count_self_intersections (odc_selfx.cu; mesh.py:395-487): hit keys a*nt+b
 // sorted into d_out_hits when their number fits cap; *n_hits always set
 int self_intersections(const double* d_v, int64_t nv, const int32_t* d_t, int64_t nt, double tol,

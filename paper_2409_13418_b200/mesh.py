@@ -83,6 +83,25 @@ class TriangleMesh:
     def n_vertices(self):
         return len(self.vertices)
 
+    def corners(self):
+        """(T, 3, 3) triangle corner positions (mesh.py:46-47)."""
+        return self.vertices[self.triangles]
+
+    def face_normals(self, normalized=True):
+        """Per-triangle cross((c1 - c0), (c2 - c0)), unit length unless
+        degenerate (zero) when ``normalized`` (mesh.py:49-55)."""
+        c = self.corners()
+        n = np.cross(c[:, 1] - c[:, 0], c[:, 2] - c[:, 0])
+        if normalized:
+            lens = np.linalg.norm(n, axis=1, keepdims=True)
+            n = np.divide(n, lens, out=np.zeros_like(n), where=lens > 0)
+        return n
+
+    def areas(self):
+        """Triangle areas (mesh.py:57-61)."""
+        c = self.corners()
+        return 0.5 * np.linalg.norm(np.cross(c[:, 1] - c[:, 0], c[:, 2] - c[:, 0]), axis=1)
+
     @property
     def n_triangles(self):
         return len(self.triangles)
