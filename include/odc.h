@@ -270,6 +270,11 @@ int odc_mesh_distance(odc_ctx* ctx, const double* vertices, int64_t n_vertices, 
                       int64_t n_triangles, const double* points, int64_t n_points, double* dist, int64_t* tri,
                       double* closest);
 
+/* Triangle areas (TriangleMesh.areas, mesh.py:57-61), bit-identical to numpy;
+ * feeds surface sampling for the metrics. */
+int odc_triangle_areas(odc_ctx* ctx, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                       int64_t n_triangles, double* areas);
+
 /* Mesh output formats (replaces occmesh.meshio.export_obj / export_ply,
  * meshio.py:22-28 and :79-98).  Host-only, no context needed; vertices
  * (n_vertices, 3) f64 and triangles (n_triangles, 3) int64, as in

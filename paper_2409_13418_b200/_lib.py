@@ -88,7 +88,7 @@ EXPORTS = (
     "odc_copy_array", "odc_eval_raw", "odc_eval_labels", "odc_set_param", "odc_extract_slab",
     "odc_slab_globalize", "odc_mesh_finish", "odc_profile_mlp", "odc_export_obj", "odc_export_ply",
     "odc_validate_manifold", "odc_validate_copy", "odc_count_self_intersections", "odc_self_intersection_pairs",
-    "odc_mesh_distance",
+    "odc_mesh_distance", "odc_triangle_areas",
 )
 
 _lib = None
@@ -135,6 +135,7 @@ def load():
         L.odc_count_self_intersections.argtypes = [vp, vp, i64, vp, i64, dbl, P(i64)]
         L.odc_self_intersection_pairs.argtypes = [vp, vp]
         L.odc_mesh_distance.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, vp, vp]
+        L.odc_triangle_areas.argtypes = [vp, vp, i64, vp, i64, vp]
         L.odc_export_obj.argtypes = [ctypes.c_char_p, vp, i64, vp, i64]
         L.odc_export_ply.argtypes = [ctypes.c_char_p, vp, i64, vp, i64]
         _lib = L

@@ -1423,6 +1423,39 @@ int odc_mesh_distance(odc_ctx* c, const double* vertices, int64_t n_vertices, co
   }, &a);
 }
 
+int odc_triangle_areas(odc_ctx* c, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                       int64_t n_triangles, double* areas) {
+  if (!c || n_vertices < 0 || n_triangles < 0 || (n_triangles && (!triangles || !areas || !vertices)))
+    return ODC_E_ARG;
+  if (n_vertices >= INT32_MAX || 3 * n_triangles >= INT32_MAX) return ODC_E_ARG;
+  DistArgs a{vertices, n_vertices, triangles, n_triangles, nullptr, 0, areas, nullptr, nullptr};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    DistArgs* x = (DistArgs*)p;
+    if (x->nt == 0) return (int)ODC_OK;
+    Arena& A = cc->varena;
+    A.reset();
+    cudaStream_t s = cc->stream;
+    const int64_t n3 = 3 * x->nt;
+    double* dv = need(A.get<double>(3 * x->nv));
+    int64_t* t64 = need(A.get<int64_t>(n3));
+    int32_t* t = need(A.get<int32_t>(n3));
+    uint32_t* bad = need(A.get<uint32_t>(2));
+    double* da = need(A.get<double>(x->nt));
+    CUDA_TRY(cudaMemcpyAsync(dv, x->v, 24 * x->nv, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(t64, x->t, 8 * n3, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(bad, 0, 8, s));
+    launch_narrow_tris(t64, n3, t, x->nv, bad, s);
+    launch_tri_areas(dv, t, x->nt, da, s);
+    check_launch(cc, 2);
+    readback(cc, bad, 4);
+    if (((uint32_t*)cc->h_pinned)[0]) throw OdcError{ODC_E_VALUE, "triangle index out of range"};
+    CUDA_TRY(cudaMemcpyAsync(x->dist, da, 8 * x->nt, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return (int)ODC_OK;
+  }, &a);
+}
+
 int odc_self_intersection_pairs(odc_ctx* c, int64_t* pairs) {
   if (!c) return ODC_E_ARG;
   if (pairs && !c->v_si_pairs.empty()) std::memcpy(pairs, c->v_si_pairs.data(), 8 * c->v_si_pairs.size());

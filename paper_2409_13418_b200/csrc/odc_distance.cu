@@ -241,6 +241,21 @@ __global__ void k_dist_query(const double* __restrict__ v, const int32_t* __rest
   cpo[3 * i + 2] = cp.z;
 }
 
+// TriangleMesh.areas (mesh.py:57-61): 0.5 * norm(cross(c1 - c0, c2 - c0)),
+// numpy's arithmetic order, so the values equal numpy's bit for bit
+__global__ void k_tri_areas(const double* __restrict__ v, const int32_t* __restrict__ t, int64_t nt,
+                            double* __restrict__ area) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const D3 a = corner(v, t, (int32_t)i, 0), b = corner(v, t, (int32_t)i, 1), c = corner(v, t, (int32_t)i, 2);
+  const D3 u = b - a, w = c - a;
+  const D3 n{u.y * w.z - u.z * w.y, u.z * w.x - u.x * w.z, u.x * w.y - u.y * w.x};
+  area[i] = 0.5 * sqrt((n.x * n.x + n.y * n.y) + n.z * n.z);
+}
+void launch_tri_areas(const double* v, const int32_t* t, int64_t nt, double* area, cudaStream_t s) {
+  if (nt) k_tri_areas<<<grid_for(nt, 256), 256, 0, s>>>(v, t, nt, area);
+}
+
 int mesh_distance(const double* d_v, const int32_t* d_t, int64_t nt, const double* d_q, int64_t nq,
                   void* (*alloc)(void*, size_t), void* actx, cudaStream_t s, double* d_dist, int64_t* d_tri,
                   double* d_cp) {

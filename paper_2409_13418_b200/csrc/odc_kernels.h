@@ -183,6 +183,7 @@ void launch_narrow_tris(const int64_t* in, int64_t n, int32_t* out, int64_t V, u
 int mesh_distance(const double* d_v, const int32_t* d_t, int64_t nt, const double* d_q, int64_t nq,
                   void* (*alloc)(void*, size_t), void* actx, cudaStream_t s, double* d_dist, int64_t* d_tri,
                   double* d_cp);
+void launch_tri_areas(const double* v, const int32_t* t, int64_t nt, double* area, cudaStream_t s);
 // count_self_intersections (odc_selfx.cu; mesh.py:395-487): hit keys a*nt+b
 // sorted into d_out_hits when their number fits cap; *n_hits always set
 int self_intersections(const double* d_v, int64_t nv, const int32_t* d_t, int64_t nt, double tol,

@@ -16,6 +16,20 @@ import numpy as np
 from . import _lib
 
 
+def triangle_areas(mesh, device=0):
+    """TriangleMesh.areas() computed on the GPU (same values as numpy)."""
+    v = np.ascontiguousarray(mesh.vertices, dtype=np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(mesh.triangles, dtype=np.int64).reshape(-1, 3)
+    out = np.empty(len(t))
+    if len(t):
+        ctx = _lib.context(device)
+        L = _lib.load()
+        rc = L.odc_triangle_areas(ctx.handle, v.ctypes.data, len(v), t.ctypes.data, len(t), out.ctypes.data)
+        if rc != _lib.ODC_OK:
+            raise ValueError(L.odc_last_error(ctx.handle).decode())
+    return out
+
+
 def sample_surface(mesh, n, seed=0, rng=None):
     """Area-weighted uniform surface samples with their face normals and
     triangle indices; the reference's generator sequence (mesh.py:273-297)."""
@@ -24,7 +38,7 @@ def sample_surface(mesh, n, seed=0, rng=None):
     if n < 1:
         raise ValueError("sample count must be at least 1")
     rng = rng or np.random.default_rng(seed)
-    areas = mesh.areas()
+    areas = triangle_areas(mesh)
     total = areas.sum()
     if total <= 0:
         raise ValueError("mesh has zero total area")
@@ -35,9 +49,17 @@ def sample_surface(mesh, n, seed=0, rng=None):
     over = u + v > 1.0
     u[over] = 1.0 - u[over]
     v[over] = 1.0 - v[over]
-    c = mesh.corners()[idx]
+    # only the sampled triangles' corners and normals (row-wise identical to
+    # indexing the full arrays, without materialising them)
+    c = mesh.vertices[mesh.triangles[idx]]
     pts = c[:, 0] + u[:, None] * (c[:, 1] - c[:, 0]) + v[:, None] * (c[:, 2] - c[:, 0])
-    return pts, mesh.face_normals()[idx], idx
+    return pts, _normals(c), idx
+
+
+def _normals(c):
+    n = np.cross(c[:, 1] - c[:, 0], c[:, 2] - c[:, 0])
+    lens = np.linalg.norm(n, axis=1, keepdims=True)
+    return np.divide(n, lens, out=np.zeros_like(n), where=lens > 0)
 
 
 class MeshDistanceIndex:
@@ -98,8 +120,8 @@ def metric_nic(mesh_gt, mesh_out, n=100_000, seed=0, return_directions=False, de
     po, no, _ = sample_surface(mesh_out, n, seed=seed + 1)
     _, t_go, _ = MeshDistanceIndex(mesh_out, device).query(pg)
     _, t_og, _ = MeshDistanceIndex(mesh_gt, device).query(po)
-    n_out = mesh_out.face_normals()[t_go]
-    n_gt = mesh_gt.face_normals()[t_og]
+    n_out = _normals(mesh_out.vertices[mesh_out.triangles[t_go]])
+    n_gt = _normals(mesh_gt.vertices[mesh_gt.triangles[t_og]])
     fwd = float(np.mean(np.arccos(np.clip(np.einsum("ij,ij->i", ng, n_out), -1.0, 1.0))))
     bwd = float(np.mean(np.arccos(np.clip(np.einsum("ij,ij->i", no, n_gt), -1.0, 1.0))))
     mean = 0.5 * (fwd + bwd)

@@ -88,3 +88,12 @@ def test_gpu_metric_fit_and_errors():
     assert 0.0 <= fit < 0.2
     with pytest.raises(ValueError):
         MeshDistanceIndex(TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", NAMES)
+def test_gpu_triangle_areas_equal_numpy(name):
+    from paper_2409_13418_b200.metrics import triangle_areas
+
+    m = golden_mesh(name)
+    assert np.array_equal(triangle_areas(m), m.areas())
