@@ -106,6 +106,8 @@ typedef struct {
   int32_t one_d, normals, split, repair;
   int32_t iters_1d, s1_lin, s1_bin, s2_lin, s2_bin;
   int32_t keep_intermediates; /* keep stage outputs for odc_copy_array */
+  int32_t method;             /* 0 dual contouring (contour); marching-cubes baseline
+                                 (baseline.marching_cubes, baseline.py:48-127): 1 binary, 2 continuous */
   double s1_range, s2_range, qef_truncation, fd_step_factor;
 } odc_options;
 

@@ -44,7 +44,7 @@ class Options(ctypes.Structure):
         ("one_d", ctypes.c_int32), ("normals", ctypes.c_int32), ("split", ctypes.c_int32), ("repair", ctypes.c_int32),
         ("iters_1d", ctypes.c_int32), ("s1_lin", ctypes.c_int32), ("s1_bin", ctypes.c_int32),
         ("s2_lin", ctypes.c_int32), ("s2_bin", ctypes.c_int32), ("keep_intermediates", ctypes.c_int32),
-        ("s1_range", ctypes.c_double), ("s2_range", ctypes.c_double), ("qef_truncation", ctypes.c_double),
+        ("method", ctypes.c_int32), ("s1_range", ctypes.c_double), ("s2_range", ctypes.c_double), ("qef_truncation", ctypes.c_double),
         ("fd_step_factor", ctypes.c_double),
     ]
 

@@ -354,6 +354,9 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   if (o->split < 0 || o->split > 1) throw OdcError{ODC_E_CONFIG, "unknown split mode"};
   if (R > 1290) throw OdcError{ODC_E_VALUE, "resolution above 1290 exceeds the 32-bit vertex index space"};
   if (win.c0 < 0 || win.c1 > R || win.c0 >= win.c1) throw OdcError{ODC_E_ARG, "bad slab range"};
+  if (o->method < 0 || o->method > 2) throw OdcError{ODC_E_CONFIG, "unknown marching-cubes mode"};
+  if (o->method && (win.slab || win.c0 != 0 || win.c1 != R))
+    throw OdcError{ODC_E_ARG, "marching cubes runs on the whole grid only"};
 
   std::memset(st, 0, sizeof *st);
   for (int i = 0; i < ODC_N_CAT; i++) st->cat_order[i] = -1;
@@ -523,6 +526,84 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     return;
   }
 
+  // ---- face_pairings probes (dualize.py:59-70)
+  auto face_probes = [&]() {
+    if (F4) {
+      if (!mlp) {
+        launch_face_center_analytic(g, fp, c->f4_key, F4, c->rec, s);
+        check_launch(c);
+      } else {
+        double* pts = need(c->arena.get<double>(3 * F4));
+        uint8_t* lab = need(c->arena.get<uint8_t>(F4));
+        launch_face_center_points(g, c->f4_key, F4, pts, s);
+        check_launch(c);
+        eval_points(c, f, pts, F4, lab, nullptr);
+        launch_face_center_scatter(g, c->f4_key, lab, F4, c->rec, s);
+        check_launch(c);
+      }
+    }
+    if (f4_own) record(st, ODC_CAT_PROBE_FACE_CENTER, 1, f4_own);
+    st->n_face_center_probes = f4_own;
+  };
+
+  if (o->method) {  // ---- marching-cubes baseline (baseline.py:48-127)
+    mark(2);
+    double* mcpos = need(c->arena.get<double>(3 * K));
+    double *raw_in = nullptr, *raw_out = nullptr;
+    if (o->method == 2) {  // continuous: inverse lerp of the raw grid values (baseline.py:82-89)
+      if (!f->continuous)
+        throw OdcError{ODC_E_CONFIG, "continuous marching cubes requires a field with raw values"};
+      raw_in = need(c->arena.get<double>(K));
+      raw_out = need(c->arena.get<double>(K));
+      double* pts = need(c->arena.get<double>(3 * K));
+      uint8_t* lab = need(c->arena.get<uint8_t>(K));
+      launch_edge_endpoints(g, c->L, c->edge_key, K, 0, pts, s);
+      eval_points(c, f, pts, K, lab, raw_in);
+      launch_edge_endpoints(g, c->L, c->edge_key, K, 1, pts, s);
+      eval_points(c, f, pts, K, lab, raw_out);
+      check_launch(c, 2);
+    }
+    launch_mc_points(g, c->L, c->edge_key, K, raw_in, raw_out, f->iso, mcpos, s);
+    check_launch(c);
+    c->t1d = nullptr;
+    c->pos1d = mcpos;
+    face_probes();
+    mark(3);
+    mark(4);
+    uint16_t* cfg = need(c->arena.get<uint16_t>(C));
+    uint32_t* ncyc = need(c->arena.get<uint32_t>(C));
+    uint32_t* nsamp = need(c->arena.get<uint32_t>(C));
+    uint32_t* ntri = need(c->arena.get<uint32_t>(C));
+    uint32_t* toff = need(c->arena.get<uint32_t>(C + 1));
+    launch_cell_config(g, c->L, c->rec, c->cell_id, C, c->table, cfg, ncyc, nsamp, s);
+    launch_mc_count(C, ncyc, nsamp, ntri, s);
+    check_launch(c, 2);
+    scan1(c, ntri, toff, C, totals);
+    readback(c, totals, sizeof(unsigned long long));
+    const int64_t T = (int64_t)c->h_pinned[0];
+    st->n_partitions = 0;
+    mark(5);
+    int32_t* tris = need(c->arena.get<int32_t>(3 * T));
+    uint8_t* used = need(c->arena.get<uint8_t>(K));
+    CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)K, s));
+    launch_mc_fans(g, c->L, c->rec, c->cell_id, C, c->table, cfg, toff, mcpos, tris, used, s);
+    check_launch(c);
+    c->P = K;
+    c->NF = 0;
+    c->T = T;
+    c->Ns = 0;
+    c->n_interior = 0;
+    c->prov_kind_in = c->prov_ref_in = nullptr;
+    c->cells = CellOut{};
+    c->fan_edge = nullptr;
+    mark(6);
+    finish_mesh(c, mcpos, K, 0, tris, T, used, false, st, dst, totals);
+    mark(7);
+    finish_stats();
+    c->valid = true;
+    return;
+  }
+
   // ---- K3: 1D points (pipeline.py:94-123, search.py:71-94)
   mark(2);
   c->t1d = need(c->arena.get<double>(K));
@@ -562,23 +643,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   }
   if (op.one_d == ODC_ONE_D_BINARY) record(st, ODC_CAT_SEARCH_1D, op.iters_1d, (int64_t)op.iters_1d * K_own);
 
-  // ---- face_pairings probes (dualize.py:59-70)
-  if (F4) {
-    if (!mlp) {
-      launch_face_center_analytic(g, fp, c->f4_key, F4, c->rec, s);
-      check_launch(c);
-    } else {
-      double* pts = need(c->arena.get<double>(3 * F4));
-      uint8_t* lab = need(c->arena.get<uint8_t>(F4));
-      launch_face_center_points(g, c->f4_key, F4, pts, s);
-      check_launch(c);
-      eval_points(c, f, pts, F4, lab, nullptr);
-      launch_face_center_scatter(g, c->f4_key, lab, F4, c->rec, s);
-      check_launch(c);
-    }
-  }
-  if (f4_own) record(st, ODC_CAT_PROBE_FACE_CENTER, 1, f4_own);
-  st->n_face_center_probes = f4_own;
+  face_probes();
 
   // ---- normals: 2D points (search.py:194-322) or fd gradient (pipeline.py:126-151)
   mark(3);

@@ -1899,4 +1899,94 @@ void launch_dup_provenance(int64_t V0, int64_t V, int64_t* kind, int64_t* ref, c
   if (V > V0) k_dup_provenance<<<grid_for(V - V0, 256), 256, 0, s>>>(V0, V, kind, ref);
 }
 
+
+// ===========================================================================
+// Marching-cubes baseline (baseline.py:48-127): one vertex per crossing edge,
+// each partition cycle fanned from its first edge and oriented outward.
+// ===========================================================================
+// vertex of crossing edge k: binary = midpoint, continuous = inverse lerp of
+// the raw grid values (baseline.py:78-89)
+__global__ void k_mc_points(GridP g, const uint32_t* __restrict__ L, const int64_t* __restrict__ edge_key, int64_t K,
+                            const double* __restrict__ raw_in, const double* __restrict__ raw_out, double iso,
+                            double* __restrict__ pos) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const EdgeGeom e = edge_geom(g, L, edge_key[k]);
+  double t = 0.5;
+  if (raw_in) {
+    const double pin = raw_in[k] - iso, pout = raw_out[k] - iso;
+    const double den = pin - pout;
+    t = pin / (fabs(den) < 1e-300 ? 1.0 : den);
+    if (!isnan(t)) t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  }
+  for (int c = 0; c < 3; c++) pos[3 * k + c] = e.pin[c] + t * e.span[c];
+}
+void launch_mc_points(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K, const double* raw_in,
+                      const double* raw_out, double iso, double* pos, cudaStream_t s) {
+  if (K) k_mc_points<<<grid_for(K, 256), 256, 0, s>>>(g, L, edge_key, K, raw_in, raw_out, iso, pos);
+}
+
+// triangles per cell: sum over its cycles of (len - 2) = edges - 2 * cycles
+__global__ void k_mc_count(int64_t C, const uint32_t* __restrict__ ncyc, const uint32_t* __restrict__ nedge,
+                           uint32_t* __restrict__ ntri) {
+  const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci < C) ntri[ci] = nedge[ci] - 2 * ncyc[ci];
+}
+void launch_mc_count(int64_t C, const uint32_t* ncyc, const uint32_t* nedge, uint32_t* ntri, cudaStream_t s) {
+  if (C) k_mc_count<<<grid_for(C, 256), 256, 0, s>>>(C, ncyc, nedge, ntri);
+}
+
+__global__ void k_mc_fans(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+                          const int64_t* __restrict__ cell_id, int64_t C, const CellTabEntry* __restrict__ table,
+                          const uint16_t* __restrict__ cfg, const uint32_t* __restrict__ tri_off,
+                          const double* __restrict__ pos, int32_t* __restrict__ tris, uint8_t* __restrict__ used) {
+  const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= C) return;
+  const int64_t base = cell_base_vid(g, cell_id[ci]);
+  const CellTabEntry T = table[cfg[ci]];
+  int64_t out = tri_off[ci];
+  int slot = 0;
+  for (int k = 0; k < T.ncyc; k++) {
+    const int len = (T.lens >> (4 * k)) & 15;
+    int64_t rows[12];
+    double outward[3] = {0.0, 0.0, 0.0};
+    for (int j = 0; j < len; j++) {
+      const int le = (int)((T.edges >> (4 * (slot + j))) & 15);
+      const int64_t ev = base + corner_off(g, c_LE_CORNER[le]);
+      const int ax = c_LE_AXIS[le];
+      rows[j] = edge_rank(rec, g, ev, ax);
+      const EdgeGeom e = edge_geom(g, L, ev * 3 + ax);
+      for (int c = 0; c < 3; c++) outward[c] = j == 0 ? e.span[c] : outward[c] + e.span[c];
+    }
+    slot += len;
+    if (len < 3) continue;
+    // normal = sum of the fan triangles' cross products, in fan order
+    double nrm[3] = {0.0, 0.0, 0.0};
+    const double* a = pos + 3 * rows[0];
+    for (int j = 1; j + 1 < len; j++) {
+      const double* b = pos + 3 * rows[j];
+      const double* c = pos + 3 * rows[j + 1];
+      const double u[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+      const double w[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+      double x[3];
+      cross3(u, w, x);
+      for (int q = 0; q < 3; q++) nrm[q] = nrm[q] + x[q];
+    }
+    // normal @ outward: numpy's 1-D matmul is an fma chain (BLAS ddot)
+    const double dot = __fma_rn(nrm[2], outward[2], __fma_rn(nrm[1], outward[1], nrm[0] * outward[0]));
+    const bool flip = dot < 0.0;
+    for (int j = 1; j + 1 < len; j++, out++) {
+      tris[3 * out] = (int32_t)rows[0];
+      tris[3 * out + 1] = (int32_t)(flip ? rows[j + 1] : rows[j]);
+      tris[3 * out + 2] = (int32_t)(flip ? rows[j] : rows[j + 1]);
+    }
+    for (int j = 0; j < len; j++) used[rows[j]] = 1;
+  }
+}
+void launch_mc_fans(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* cell_id, int64_t C,
+                    const CellTabEntry* table, const uint16_t* cfg, const uint32_t* tri_off, const double* pos,
+                    int32_t* tris, uint8_t* used, cudaStream_t s) {
+  if (C) k_mc_fans<<<grid_for(C, 128), 128, 0, s>>>(g, L, rec, cell_id, C, table, cfg, tri_off, pos, tris, used);
+}
+
 }  // namespace odc

@@ -170,6 +170,14 @@ void launch_widen_i32(const int32_t* src, int64_t* dst, int64_t n, cudaStream_t 
 // provenance of repair duplicates [V0, V): kind 2, ref (-1, -1) (polygonize.py:348-373)
 void launch_dup_provenance(int64_t V0, int64_t V, int64_t* kind, int64_t* ref, cudaStream_t s);
 
+// marching-cubes baseline (baseline.py:48-127)
+void launch_mc_points(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K, const double* raw_in,
+                      const double* raw_out, double iso, double* pos, cudaStream_t s);
+void launch_mc_count(int64_t C, const uint32_t* ncyc, const uint32_t* nedge, uint32_t* ntri, cudaStream_t s);
+void launch_mc_fans(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* cell_id, int64_t C,
+                    const CellTabEntry* table, const uint16_t* cfg, const uint32_t* tri_off, const double* pos,
+                    int32_t* tris, uint8_t* used, cudaStream_t s);
+
 // mesh validation (odc_validate.cu; mesh.py:91-150)
 void launch_manifold_vertex(int64_t V, const int32_t* tris, const uint32_t* off, const int32_t* inc, int32_t* nbv,
                             uint32_t* nbc, uint32_t* nbt, uint32_t* uf, uint32_t* n_nb, uint32_t* n_nm,
