@@ -32,7 +32,7 @@ def test_struct_layouts_match_header():
     from paper_2409_13418_b200 import _lib
 
     assert ctypes.sizeof(_lib.Node) == 136
-    assert ctypes.sizeof(_lib.Options) == 4 * 10 + 8 * 4
+    assert ctypes.sizeof(_lib.Options) == 4 * 11 + 4 + 8 * 4  # 11 int32 (+4 padding), 4 doubles
     L = _lib.load()
     o = _lib.Options()
     L.odc_default_options(ctypes.byref(o))
