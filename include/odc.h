@@ -154,6 +154,11 @@ int odc_set_param(odc_ctx* ctx, const char* name, int64_t value);
 int odc_field_analytic(odc_ctx* ctx, const odc_node* nodes, int32_t n_nodes, int32_t continuous,
                        double iso_level, odc_field** out);
 int odc_field_mlp(odc_ctx* ctx, const odc_mlp_desc* desc, odc_field** out);
+/* MeshWindingField (fields.py:281-386): occupancy from a triangle mesh,
+ * raw = generalized winding number (continuous), label = raw > 1/2; queries
+ * on the surface are perturbed like the reference's "perturb" mode. */
+int odc_field_mesh(odc_ctx* ctx, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                   int64_t n_triangles, odc_field** out);
 void odc_field_free(odc_ctx* ctx, odc_field* f);
 
 void odc_default_options(odc_options* o);

@@ -10,12 +10,14 @@ sm_100a kernels in libodc.so behind the C-ABI of include/odc.h.
 from .fields import (  # noqa: F401
     BoxField,
     CsgField,
+    MeshWindingField,
     MlpField,
     OccupancyField,
     PlaneField,
     Scene,
     SmoothedOccupancy,
     SphereField,
+    SurfaceCoincidenceError,
     TorusField,
     field_from_dict,
     load_scene,

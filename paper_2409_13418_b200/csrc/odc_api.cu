@@ -98,6 +98,9 @@ struct odc_field {
   float* bias = nullptr;
   float* w_head = nullptr;
   MlpDev mlp{};
+  // mesh winding-number field (kind 2)
+  WindDev wind{};
+  void* wind_buf = nullptr;
 };
 
 struct odc_ctx {
@@ -108,6 +111,7 @@ struct odc_ctx {
   Arena arena;
   CellTabEntry* table = nullptr;
   unsigned long long* h_pinned = nullptr;  // small readback buffer
+  unsigned int* d_fail = nullptr;          // device flag: a winding query stayed on the surface
   char* h_stage = nullptr;  // grow-only pinned staging for mesh copy-back
   // mesh validation (its own workspace: the last extraction stays valid)
   Arena varena;
@@ -198,6 +202,9 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
   if (f->kind == 0) {
     FieldP fp{f->nodes, f->n_nodes, 0, f->iso};
     launch_eval_raw_analytic(fp, pts, n, raw, lab, c->stream);
+  } else if (f->kind == 2) {
+    PointSrc src{pts, GridP{}, 0};
+    winding_eval(f->wind, src, n, lab, raw, c->d_fail, c->stream);
   } else {
     PointSrc src{pts, GridP{}, 0};
     MlpDev md = f->mlp;
@@ -205,6 +212,16 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
     mlp_eval(md, src, n, lab, raw, c->stream);
   }
   check_launch(c);
+}
+
+// MeshWindingField "perturb" mode gave up on a query (fields.py:354-355)
+void check_surface(odc_ctx* c) {
+  if (!c->d_fail) return;
+  readback(c, c->d_fail, 4);
+  if (((unsigned int*)c->h_pinned)[0]) {
+    CUDA_TRY(cudaMemsetAsync(c->d_fail, 0, 4, c->stream));
+    throw OdcError{ODC_E_VALUE, "could not perturb queries off the surface"};
+  }
 }
 
 OptP make_opt(const odc_options* o, int continuous) {
@@ -386,7 +403,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   c->g = g;
   const OptP op = make_opt(o, f->continuous);
   const FieldP fp{f->nodes, f->n_nodes, f->kind, f->iso};
-  const bool mlp = f->kind == 1;
+  const bool mlp = f->kind != 0;  // fields evaluated in lock-step batches (MLP, mesh winding)
 
   DevStats* dst = need(c->arena.get<DevStats>(1));
   DevStatus* dstat = need(c->arena.get<DevStatus>(1));
@@ -409,9 +426,13 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   } else {
     uint8_t* bytes = need(c->arena.get<uint8_t>(g.nz * g.S2));
     PointSrc src{nullptr, g, g.z0 * g.S2};
-    MlpDev md = f->mlp;
-    md.impl = c->mlp_impl;
-    mlp_eval(md, src, g.nz * g.S2, bytes, nullptr, s);
+    if (f->kind == 2) {
+      winding_eval(f->wind, src, g.nz * g.S2, bytes, nullptr, c->d_fail, s);
+    } else {
+      MlpDev md = f->mlp;
+      md.impl = c->mlp_impl;
+      mlp_eval(md, src, g.nz * g.S2, bytes, nullptr, s);
+    }
     check_launch(c);
     mark(8);
     launch_pack_labels(g, bytes, c->L, s);
@@ -482,6 +503,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   st->n_crossing_cells = c_hi - c_lo;
 
   auto finish_stats = [&]() {
+    check_surface(c);
     readback(c, dst, sizeof(DevStats));
     DevStats h;
     std::memcpy(&h, c->h_pinned, sizeof h);
@@ -836,7 +858,8 @@ int odc_create(int device, odc_ctx** out) {
   if (!c) return ODC_E_NOMEM;
   c->device = device;
   if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess || cudaEventCreate(&c->ev0) != cudaSuccess ||
-      cudaEventCreate(&c->ev1) != cudaSuccess || cudaMallocHost(&c->h_pinned, 4096) != cudaSuccess) {
+      cudaEventCreate(&c->ev1) != cudaSuccess || cudaMallocHost(&c->h_pinned, 4096) != cudaSuccess ||
+      cudaMalloc(&c->d_fail, 4) != cudaSuccess || cudaMemset(c->d_fail, 0, 4) != cudaSuccess) {
     delete c;
     return ODC_E_CUDA;
   }
@@ -874,6 +897,7 @@ void odc_destroy(odc_ctx* c) {
   if (c->table) cudaFree(c->table);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->d_fail) cudaFree(c->d_fail);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (auto& e : c->evs)
@@ -1001,16 +1025,87 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
   return ODC_OK;
 }
 
+int odc_field_mesh(odc_ctx* c, const double* vertices, int64_t n_vertices, const int64_t* triangles,
+                   int64_t n_triangles, odc_field** out) {
+  if (!c || !out || n_vertices < 0 || n_triangles < 0 || (n_vertices && !vertices)) return ODC_E_ARG;
+  if (n_triangles == 0 || !triangles) {
+    c->err = "mesh field needs at least one triangle";
+    return ODC_E_VALUE;
+  }
+  for (int64_t i = 0; i < 3 * n_triangles; i++)
+    if (triangles[i] < 0 || triangles[i] >= n_vertices) {
+      c->err = "triangle index out of range";
+      return ODC_E_VALUE;
+    }
+  cudaSetDevice(c->device);
+  odc_field* f = new (std::nothrow) odc_field();
+  if (!f) return ODC_E_NOMEM;
+  f->kind = 2;
+  f->continuous = 1;
+  f->iso = 0.5;
+  // nudge = 1e-9 * max(ptp(vertices, axis=0)) / sqrt(3) (fields.py:311-312)
+  double scale = 0.0;
+  for (int a = 0; a < 3; a++) {
+    double lo = vertices[a], hi = vertices[a];
+    for (int64_t i = 1; i < n_vertices; i++) {
+      lo = std::min(lo, vertices[3 * i + a]);
+      hi = std::max(hi, vertices[3 * i + a]);
+    }
+    scale = std::max(scale, hi - lo);
+  }
+  if (scale == 0.0) scale = 1.0;
+  const int64_t T = n_triangles;
+  const size_t bytes = sizeof(double) * (18 * T + 4 * T) + (size_t)T + sizeof(double) * 3 * n_vertices + 24 * T;
+  cudaStream_t s = c->stream;
+  char* buf = nullptr;
+  if (cudaMallocAsync((void**)&buf, bytes + 512, s) != cudaSuccess) {
+    delete f;
+    c->err = "field upload failed";
+    return ODC_E_NOMEM;
+  }
+  double* d = (double*)buf;
+  WindDev& w = f->wind;
+  w.ta = d;
+  w.tb = d + 3 * T;
+  w.tc = d + 6 * T;
+  w.nhat = d + 9 * T;
+  w.eab = d + 12 * T;
+  w.eac = d + 15 * T;
+  w.d00 = d + 18 * T;
+  w.d01 = d + 19 * T;
+  w.d11 = d + 20 * T;
+  w.denb = d + 21 * T;
+  double* dv = d + 22 * T;
+  int64_t* dt = (int64_t*)(dv + 3 * n_vertices);
+  w.ok = (uint8_t*)(dt + 3 * T);
+  w.nt = T;
+  w.nudge = 1e-9 * scale * 1.0 / std::sqrt(3.0);
+  f->wind_buf = buf;
+  if (cudaMemcpyAsync(dv, vertices, 24 * n_vertices, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(dt, triangles, 24 * T, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    odc_field_free(c, f);
+    return ODC_E_CUDA;
+  }
+  launch_winding_prep(dv, dt, T, w, s);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) {
+    odc_field_free(c, f);
+    c->err = "mesh field setup failed";
+    return ODC_E_CUDA;
+  }
+  *out = f;
+  return ODC_OK;
+}
+
 void odc_field_free(odc_ctx* c, odc_field* f) {
   if (!f) return;
   if (c) {
     cudaStreamSynchronize(c->stream);
-    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head};
+    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head, f->wind_buf};
     for (void* b : bufs)
       if (b) cudaFreeAsync(b, c->stream);  // back to the pool, no device-wide sync
   } else {
     cudaDeviceSynchronize();
-    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head};
+    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head, f->wind_buf};
     for (void* b : bufs)
       if (b) cudaFreeAsync(b, 0);
     cudaDeviceSynchronize();
@@ -1648,6 +1743,7 @@ static int eval_common(odc_ctx* c, const odc_field* f, const double* pts, int64_
     uint8_t* dl = need(cc->arena.get<uint8_t>(x->n));
     CUDA_TRY(cudaMemcpyAsync(dp, x->pts, sizeof(double) * 3 * x->n, cudaMemcpyHostToDevice, cc->stream));
     eval_points(cc, x->f, dp, x->n, dl, dr);
+    check_surface(cc);
     if (x->raw) CUDA_TRY(cudaMemcpyAsync(x->raw, dr, sizeof(double) * x->n, cudaMemcpyDeviceToHost, cc->stream));
     if (x->lab) CUDA_TRY(cudaMemcpyAsync(x->lab, dl, x->n, cudaMemcpyDeviceToHost, cc->stream));
     CUDA_TRY(cudaStreamSynchronize(cc->stream));

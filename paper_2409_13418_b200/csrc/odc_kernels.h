@@ -170,6 +170,21 @@ void launch_widen_i32(const int32_t* src, int64_t* dst, int64_t n, cudaStream_t 
 // provenance of repair duplicates [V0, V): kind 2, ref (-1, -1) (polygonize.py:348-373)
 void launch_dup_provenance(int64_t V0, int64_t V, int64_t* kind, int64_t* ref, cudaStream_t s);
 
+// MeshWindingField (odc_winding.cu; fields.py:281-386): per-triangle terms
+struct WindDev {
+  double *ta, *tb, *tc, *nhat, *eab, *eac;  // (T,3)
+  double *d00, *d01, *d11, *denb;           // (T)
+  uint8_t* ok;                              // (T) non-degenerate normal
+  int64_t nt;
+  double nudge;  // 1e-9 * scale / sqrt(3)
+};
+void launch_winding_prep(const double* v, const int64_t* t, int64_t nt, const WindDev& w, cudaStream_t s);
+struct PointSrc;
+// labels (raw > 0.5) and/or raw winding numbers of n query points; sets
+// *failed when a query could not be moved off the surface in 8 attempts
+void winding_eval(const WindDev& w, const PointSrc& src, int64_t n, uint8_t* labels, double* raw,
+                  unsigned int* failed, cudaStream_t s);
+
 // marching-cubes baseline (baseline.py:48-127)
 void launch_mc_points(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K, const double* raw_in,
                       const double* raw_out, double iso, double* pos, cudaStream_t s);

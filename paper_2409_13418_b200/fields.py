@@ -238,6 +238,28 @@ class LoweringError(TypeError):
     pass
 
 
+class SurfaceCoincidenceError(ValueError):
+    """A winding-number query could not be moved off the surface (fields.py:21-22)."""
+
+
+class MeshWindingField(OccupancyField):
+    """Occupancy from a triangle mesh (fields.py:370-386): raw = generalized
+    winding number, inside where raw > 1/2; queries exactly on the surface are
+    perturbed deterministically.  Evaluated on the GPU (csrc/odc_winding.cu)."""
+
+    continuous = True
+
+    def __init__(self, vertices, triangles):
+        self.vertices = np.asarray(vertices, dtype=np.float64)
+        self.triangles = np.asarray(triangles, dtype=np.int64)
+        if len(self.triangles) == 0:
+            raise ValueError("mesh field needs at least one triangle")
+
+
+def is_mesh_winding(field):
+    return _kind(field) == "MeshWindingField"
+
+
 def _node(op, params=()):
     n = np.zeros((), dtype=NODE_DTYPE)
     n["op"] = op
@@ -376,7 +398,17 @@ def field_from_dict(spec, base_dir=None):
         return CsgField(spec["op"], children, rotation=rot, translation=spec.get("translation"))
     if kind == "mlp":
         return MlpField(**{k: v for k, v in spec.items() if k != "type"})
-    raise ValueError(f"unknown field type {kind!r} (mesh/voxel fields are not on the device path)")
+    if kind == "mesh":  # fields.py:424-431
+        from pathlib import Path
+
+        from .meshio import import_obj
+
+        path = Path(spec["path"])
+        if base_dir is not None and not path.is_absolute():
+            path = Path(base_dir) / path
+        mesh = import_obj(path)
+        return MeshWindingField(mesh.vertices, mesh.triangles)
+    raise ValueError(f"unknown field type {kind!r} (voxel fields are not on the device path)")
 
 
 class Scene:

@@ -17,7 +17,7 @@ from dataclasses import dataclass, field as dc_field
 import numpy as np
 
 from . import _lib
-from .fields import field_continuous, is_mlp, lower_program
+from .fields import SurfaceCoincidenceError, field_continuous, is_mesh_winding, is_mlp, lower_program
 from .mesh import GridSpec, TriangleMesh
 
 ONE_D_MODES = ("midpoint", "linear-interp", "binary-search")
@@ -123,6 +123,8 @@ _ERRORS = {
 
 def _raise(rc, ctx):
     msg = _lib.load().odc_last_error(ctx.handle).decode()
+    if rc == _lib.ODC_E_VALUE and "off the surface" in msg:
+        raise SurfaceCoincidenceError(msg)
     raise _ERRORS.get(rc, RuntimeError)(msg)
 
 
@@ -149,6 +151,11 @@ class DeviceField:
             for i in range(3):
                 d.prior_center[i] = float(field.prior_center[i])
             rc = L.odc_field_mlp(ctx.handle, ctypes.byref(d), ctypes.byref(self.handle))
+        elif is_mesh_winding(field):
+            v = np.ascontiguousarray(field.vertices, dtype=np.float64).reshape(-1, 3)
+            t = np.ascontiguousarray(field.triangles, dtype=np.int64).reshape(-1, 3)
+            rc = L.odc_field_mesh(ctx.handle, v.ctypes.data if len(v) else None, len(v),
+                                  t.ctypes.data if len(t) else None, len(t), ctypes.byref(self.handle))
         else:
             prog = lower_program(field)
             nodes = np.ascontiguousarray(prog)
