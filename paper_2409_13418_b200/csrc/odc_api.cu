@@ -914,7 +914,7 @@ int odc_set_param(odc_ctx* c, const char* name, int64_t value) {
     c->mlp_debug = (int)value;
     return ODC_OK;
   }
-  if (std::strcmp(name, "mlp_impl") == 0 && value >= 0 && value <= 2) {
+  if (std::strcmp(name, "mlp_impl") == 0 && value >= 0 && value <= 3) {
     c->mlp_impl = (int)value;
     return ODC_OK;
   }

@@ -816,6 +816,255 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
 static int g_num_sms = 0;
 
 // impl: 0 = CTA-pair tcgen05 (default), 1 = SIMT reference, 2 = single-CTA tcgen05
+// ===========================================================================
+// CTA-pair, N = 256, tile ping-pong evaluator (odc_mlp_tc4: mlp_impl 3)
+//
+// A cluster of two CTAs (one TPC) runs 2 x 256 points through the layers.
+// Each CTA holds two 128-row activation tiles in shared memory (A, bf16,
+// 128 KB) and its 128-row half of every weight K-atom (B split along N:
+// CTA r owns output columns 128r .. 128r+127 -- exactly tc1's chunk
+// (l, nh = r, kc), so w_tc is reused).  The leader issues
+// tcgen05.mma.cta_group::2 M256 N256 K16 (128 cycles): A from each CTA's own
+// tile, B from both CTAs' halves, fp32 D of tile t in TMEM columns 256t ..
+// 256t+255 of each CTA (its 128 rows).  Tiles alternate: (t0, l), (t1, l),
+// (t0, l+1), ... so tile t's epilogue (TMEM -> bias + ReLU -> bf16 -> A(t))
+// runs while the other tile's MMAs run, and a weight stage serves both
+// tiles of a layer before it is released.  Per SM and layer: A reads 128 KB,
+// B reads 128 KB, weight copies 64 KB, activation stores 128 KB of shared
+// memory traffic for 4,096 MMA cycles (tc1: 768 KB), so the tensor pipe,
+// not shared memory, sets the pace.
+// ===========================================================================
+namespace tc4 {
+constexpr int kThreads = 384;
+constexpr int kStages = 6;
+constexpr int kStageBytes = 16384;   // per CTA: 128 N rows x K 64 (one K-atom)
+constexpr int kTileABytes = 65536;   // 128 rows x 256 bf16
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (32u << 17) | (16u << 24);  // M256 N256
+constexpr size_t kSmemBytes = 1024 + 2 * kTileABytes + kStages * kStageBytes + 256 + 384 * 4;
+__device__ __forceinline__ void umma_ss2(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+}  // namespace tc4
+
+template <bool kBias>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
+    k_mlp_tc4(MlpDev m, PointSrc src, int64_t n, uint8_t* __restrict__ labels, double* __restrict__ raw) {
+  using namespace tc;
+  using tc2::cluster_ctarank;
+  using tc2::cluster_sync;
+  using tc2::mapa;
+  using tc2::mbar_arrive_cluster;
+  using tc2::named_bar_sync;
+  using tc2::umma_commit_pair;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* A0 = smem;
+  uint8_t* Wst = smem + 2 * tc4::kTileABytes;
+  uint64_t* bars = (uint64_t*)(Wst + tc4::kStages * tc4::kStageBytes);
+  uint64_t* full = bars;                       // [S] local weight half landed
+  uint64_t* empty = full + tc4::kStages;       // [S] both tiles done with the stage (commit, both CTAs)
+  uint64_t* fullp = empty + tc4::kStages;      // [S] leader: the peer's half landed (relay)
+  uint64_t* acc_full = fullp + tc4::kStages;   // [2] tile t's layer done (commit, both CTAs)
+  uint64_t* a_ready = acc_full + 2;            // [2] leader: A(t) written and D(t) drained, 8 warps
+  uint32_t* tmem_slot = (uint32_t*)(a_ready + 2);
+  float* s_head = (float*)(bars + 32);         // (256)
+  float* s_part = s_head + kWidth;             // (128) head partials of columns 128..255
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int64_t npairs = (n + 511) / 512;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < tc4::kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&fullp[s], 1);
+    }
+    for (int t = 0; t < 2; t++) {
+      mbar_init(&acc_full[t], 1);
+      mbar_init(&a_ready[t], 16);  // 8 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < kWidth; i += blockDim.x) s_head[i] = m.w_head[i];
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {  // ---- weight producer: this CTA's N half of every K-atom
+    uint32_t g = 0;
+    for (int64_t pr = cid; pr < npairs; pr += ncl)
+      for (int l = 0; l < kDepth; l++)
+        for (int kc = 0; kc < (l == 0 ? 1 : 4); kc++, g++) {
+          const uint32_t s = g % tc4::kStages, ph = (g / tc4::kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one()) {
+            const int ci = l == 0 ? (int)crank : 2 + (l - 1) * 8 + (int)crank * 4 + kc;
+            mbar_expect_tx(&full[s], tc4::kStageBytes);
+            bulk_g2s(Wst + s * tc4::kStageBytes, m.w_tc + (size_t)ci * 128 * 64, tc4::kStageBytes, &full[s]);
+          }
+          __syncwarp();
+        }
+  } else if (warp == 3) {
+    if (!leader) {  // ---- relay: the peer's half landed -> leader's fullp[s]
+      uint32_t g = 0;
+      for (int64_t pr = cid; pr < npairs; pr += ncl)
+        for (int l = 0; l < kDepth; l++)
+          for (int kc = 0; kc < (l == 0 ? 1 : 4); kc++, g++) {
+            const uint32_t s = g % tc4::kStages, ph = (g / tc4::kStages) & 1;
+            mbar_wait(&full[s], ph);
+            if (elect_one()) mbar_arrive_cluster(mapa(smem_u32(&fullp[s]), 0));
+            __syncwarp();
+          }
+    }
+  } else if (warp == 1) {
+    if (leader) {  // ---- MMA issuer (whole warp walks; one elected lane issues)
+      const uint32_t a_lo = desc_lo(smem_u32(A0));
+      const uint32_t w_lo = desc_lo(smem_u32(Wst));
+      uint32_t g0 = 0, ra[2] = {0, 0};
+      int ti = 0;
+      for (int64_t pr = cid; pr < npairs; pr += ncl, ti++) {
+        for (int l = 0; l < kDepth; l++) {
+          const int nst = l == 0 ? 1 : 4;
+#pragma unroll
+          for (int t = 0; t < 2; t++) {
+            if (lane == 0) ODC_TRACE(ti, l, 2 * t);
+            mbar_wait(&a_ready[t], ra[t] & 1);
+            ra[t]++;
+            tc_fence_after();
+            if (lane == 0) ODC_TRACE(ti, l, 2 * t + 1);
+            for (int k = 0; k < nst; k++) {
+              const uint32_t g = g0 + k, s = g % tc4::kStages, ph = (g / tc4::kStages) & 1;
+              if (t == 0) {
+                mbar_wait(&full[s], ph);
+                mbar_wait(&fullp[s], ph);
+              }
+              const uint32_t b_lo = w_lo + s * (tc4::kStageBytes >> 4);
+              const uint32_t a_k = a_lo + (uint32_t)((t * tc4::kTileABytes + k * 16384) >> 4);
+              if (elect_one()) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ks++)
+                  tc4::umma_ss2(tmem + t * 256, make_desc(a_k + ks * 2), make_desc(b_lo + ks * 2), (k | ks) != 0);
+                if (t == 1) umma_commit_pair(&empty[s]);
+              }
+              __syncwarp();
+            }
+            if (elect_one()) umma_commit_pair(&acc_full[t]);
+            __syncwarp();
+            if (lane == 0) ODC_TRACE(ti, l, 4 + t);
+          }
+          g0 += nst;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: all 8 warps work on one tile at a time (tiles alternate),
+    // warp%4 = TMEM lane quarter, (warp-4)/4 = column half of the 256 outputs
+    const int q = warp & 3;
+    const int hc = (warp - 4) >> 2;
+    const int r = 32 * q + lane;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    uint32_t leader_ready[2] = {mapa(smem_u32(&a_ready[0]), 0), mapa(smem_u32(&a_ready[1]), 0)};
+    auto release = [&](int t) {  // A(t) written / D(t) drained -> the leader's a_ready[t]
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_ready[t]);
+    };
+    // this warp's encoding row: tile hc, row r (column half 0 stores tile 0, half 1 tile 1)
+    const uint32_t a_pe = smem_u32(A0 + hc * tc4::kTileABytes);
+    uint32_t af[2] = {0, 0};
+    uint32_t pe[32];
+    int64_t p_prev = -1;
+    float dot_prev[2] = {0.f, 0.f};
+    const bool tr = r == 0 && crank == 0 && hc == 0;
+    if (cid < npairs) {
+      pe_row_packed(src, n, cid * 512 + hc * 256 + crank * 128 + r, pe);
+      store_pe_row(pe, a_pe, r);
+      release(0);
+      release(1);
+    }
+    int ti = 0;
+    for (int64_t pr = cid; pr < npairs; pr += ncl, ti++) {
+      const int64_t next = pr + ncl;
+      float dot[2] = {0.f, 0.f};
+      for (int l = 0; l < kDepth; l++) {
+        const float* bl = m.bias + l * kWidth + hc * 128;
+        if (l == 1 && hc == 0) {  // the previous pair's labels, in this layer's slack
+          finish_label(m, src, n, p_prev, dot_prev[0], labels, raw);
+          if (p_prev >= 0) finish_label(m, src, n, p_prev + 256, dot_prev[1], labels, raw);
+          p_prev = -1;
+        }
+        if (l == kDepth - 1 && next < npairs) pe_row_packed(src, n, next * 512 + hc * 256 + crank * 128 + r, pe);
+#pragma unroll
+        for (int t = 0; t < 2; t++) {
+          const uint32_t a_t = smem_u32(A0 + t * tc4::kTileABytes);
+          const uint32_t dcol = tmem + lane_base + t * 256 + hc * 128;
+          if (tr) ODC_TRACE(ti, l, 6 + t);
+          mbar_wait(&acc_full[t], af[t] & 1);
+          af[t]++;
+          tc_fence_after();
+          if (tr) ODC_TRACE(ti, l, 8 + t);
+          if (l < kDepth - 1) {
+#pragma unroll
+            for (int gk = 0; gk < 2; gk++) {  // 64 columns = one K-atom of the next layer's A
+              uint32_t v0[32], v1[32], w[32];
+              ODC_TMEM_LD32(dcol + 64 * gk, v0);
+              ODC_TMEM_LD32(dcol + 64 * gk + 32, v1);
+              tmem_ld_wait();
+              relu_pack32<kBias>(v0, bl + 64 * gk, w);
+              relu_pack32<kBias>(v1, bl + 64 * gk + 32, w + 16);
+              const uint32_t atom = a_t + (2 * hc + gk) * 16384;
+#pragma unroll
+              for (int c = 0; c < 8; c++)
+                st_shared_v4(atom + sw128_off(r, c), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+            }
+            release(t);
+            if (tr) ODC_TRACE(ti, l, 10 + t);
+          } else {
+            float d = 0.f;
+#pragma unroll
+            for (int gk = 0; gk < 4; gk++) {
+              uint32_t v[32];
+              ODC_TMEM_LD32(dcol + 32 * gk, v);
+              tmem_ld_wait();
+              d = head32<kBias>(v, bl + 32 * gk, s_head + hc * 128 + 32 * gk, d);
+            }
+            // halves meet in shared memory (the 8 warps are on the same tile)
+            if (hc == 1) s_part[r] = d;
+            named_bar_sync(1, 256);
+            if (hc == 0) dot[t] = d + s_part[r];
+            named_bar_sync(1, 256);
+            // D(t) drained; the next pair's encoding of tile t goes in (half t's rows)
+            if (next < npairs && hc == t) store_pe_row(pe, a_pe, r);
+            release(t);
+          }
+        }
+      }
+      p_prev = pr * 512 + crank * 128 + r;  // tile 0 row; tile 1 row = +256
+      dot_prev[0] = dot[0];
+      dot_prev[1] = dot[1];
+    }
+    if (hc == 0 && p_prev >= 0) {
+      finish_label(m, src, n, p_prev, dot_prev[0], labels, raw);
+      finish_label(m, src, n, p_prev + 256, dot_prev[1], labels, raw);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s) {
   if (n <= 0) return 0;
   if (m.impl == 1 || m.w_tc == nullptr) {
@@ -837,6 +1086,21 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
     attr = true;
   }
   const int64_t ntiles = (n + 255) / 256;
+  if (m.impl == 3) {
+    static bool attr4 = false;
+    if (!attr4) {
+      cudaFuncSetAttribute(k_mlp_tc4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc4::kSmemBytes);
+      cudaFuncSetAttribute(k_mlp_tc4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc4::kSmemBytes);
+      attr4 = true;
+    }
+    const int64_t np4 = (n + 511) / 512;
+    const int64_t pairs = (g_num_sms / 2) < np4 ? (g_num_sms / 2) : np4;
+    if (m.has_bias)
+      k_mlp_tc4<true><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, src, n, labels, raw);
+    else
+      k_mlp_tc4<false><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, src, n, labels, raw);
+    return 0;
+  }
   if (m.impl == 0 && m.w_tc2 != nullptr) {
     const int64_t pairs = (g_num_sms / 2) < ntiles ? (g_num_sms / 2) : ntiles;
     if (m.has_bias)

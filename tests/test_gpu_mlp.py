@@ -30,10 +30,10 @@ def logit(raw):
     return np.log(raw / (1 - raw))
 
 
-@pytest.mark.parametrize("impl", [0, 2])
+@pytest.mark.parametrize("impl", [0, 2, 3])
 @pytest.mark.parametrize("n", [1, 255, 256, 1000, 70001])
 def test_tc_matches_simt(n, impl):
-    """impl 0: CTA-pair tcgen05 (TMEM A operand); impl 2: single-CTA tcgen05."""
+    """impl 0: CTA-pair tcgen05 (TMEM A operand); impl 2: single-CTA tcgen05; impl 3: CTA-pair N=256 ping-pong."""
     field = MlpField(seed=0, amplitude=1.0)
     rng = np.random.default_rng(n)
     pts = rng.uniform(0, 1, size=(n, 3))
