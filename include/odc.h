@@ -147,8 +147,9 @@ void odc_destroy(odc_ctx* ctx);
 const char* odc_last_error(const odc_ctx* ctx);
 /* stream: a cudaStream_t passed as void* (NULL = the context's own stream) */
 int odc_set_stream(odc_ctx* ctx, void* stream);
-/* tuning/testing knobs: "mlp_impl" = 2 single-CTA tcgen05 evaluator (default),
- * 0 CTA-pair tcgen05 evaluator, 1 SIMT reference evaluator (same math, CUDA cores) */
+/* tuning/testing knobs: "mlp_impl" = 3 CTA-pair N=256 tile ping-pong tcgen05
+ * evaluator (default), 2 single-CTA tcgen05, 0 CTA-pair with A in TMEM, 1 SIMT
+ * reference evaluator (same math, CUDA cores) */
 int odc_set_param(odc_ctx* ctx, const char* name, int64_t value);
 
 int odc_field_analytic(odc_ctx* ctx, const odc_node* nodes, int32_t n_nodes, int32_t continuous,

@@ -120,9 +120,10 @@ struct odc_ctx {
   size_t h_stage_bytes = 0;
   std::string err;
   int launches = 0;
-  // odc_set_param("mlp_impl"): 2 single-CTA tcgen05 (default, fastest measured),
-  // 0 CTA-pair tcgen05, 1 SIMT reference
-  int mlp_impl = 2;
+  // odc_set_param("mlp_impl"): 3 CTA-pair N=256 ping-pong tcgen05 (default,
+  // fastest measured), 2 single-CTA tcgen05, 0 CTA-pair with A in TMEM,
+  // 1 SIMT reference
+  int mlp_impl = 3;
   int mlp_debug = 0;  // odc_set_param("mlp_debug"): profiling experiments, odc_profile_mlp only
   // last extraction
   bool valid = false;

@@ -1116,6 +1116,6 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
   return 0;
 }
 
-const char* mlp_kernel_name() { return "k_mlp_tc"; }
+const char* mlp_kernel_name() { return "k_mlp_tc4"; }
 
 }  // namespace odc
