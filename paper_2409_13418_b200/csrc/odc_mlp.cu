@@ -218,6 +218,15 @@ __device__ __forceinline__ float head32(const uint32_t (&v)[32], const float* __
   return dot;
 }
 
+// grid vertex -> (x, y, z) with the precomputed divisor by S (vids < 2^31)
+__device__ __forceinline__ void grid_coords_fast(const PointSrc& src, int64_t p, uint32_t c[3]) {
+  const uint32_t S = (uint32_t)src.grid.S;
+  const uint32_t v = (uint32_t)(src.begin + p);
+  const uint32_t q = __umulhi(v, src.fd_m) >> src.fd_s;
+  c[0] = v - q * S;
+  c[2] = __umulhi(q, src.fd_m) >> src.fd_s;
+  c[1] = q - c[2] * S;
+}
 // fp64 prior + logistic of one point from its fp32 head dot product
 // (paper_2409_13418_b200/fields.py MlpField); p < 0 or p >= n: nothing to do
 __device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& src, int64_t n, int64_t p, float dot,
@@ -228,7 +237,15 @@ __device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& sr
     // Its error is < 1e-4 for these magnitudes, so a margin of 1e-3 decides
     // exactly; anything closer takes the fp64 path below.
     int64_t c[3];
-    vid_coords(src.grid, src.begin + p, c);
+    if (src.fd_m) {
+      uint32_t cf[3];
+      grid_coords_fast(src, p, cf);
+      c[0] = cf[0];
+      c[1] = cf[1];
+      c[2] = cf[2];
+    } else {
+      vid_coords(src.grid, src.begin + p, c);
+    }
     float d2 = 0.f;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
@@ -816,6 +833,115 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
 static int g_num_sms = 0;
 
 // impl: 0 = CTA-pair tcgen05 (default), 1 = SIMT reference, 2 = single-CTA tcgen05
+// Positional encoding built in pieces across the layers of the current tile
+// pair (the epilogue's slack after each layer): piece 0 = the fp64 point and
+// frequency 0, piece k = frequency k.  The packed words equal
+// pe_row_packed's: word c = (feature 2c, feature 2c + 1), features
+// [x(3), sin_k(3), cos_k(3), ...]; frequency k's first feature 3 + 6k is the
+// high half of word 1 + 3k, whose low half (``pend``) is the previous one.
+struct PePiece {
+  float x[3];
+  float pend;
+  bool ok;
+};
+// encoding row of grid point p from the per-axis table: the same values as
+// pe_row_packed (the table holds exactly its per-coordinate features)
+__device__ __forceinline__ void pe_from_table(const PointSrc& src, int64_t n, int64_t p, uint32_t (&pk)[32]) {
+#pragma unroll
+  for (int c = 20; c < 32; c++) pk[c] = 0u;
+  if (p >= n) {
+#pragma unroll
+    for (int c = 0; c < 20; c++) pk[c] = 0u;
+    return;
+  }
+  uint32_t ci[3];
+  grid_coords_fast(src, p, ci);
+  float T[3][16];
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    const float4* row = reinterpret_cast<const float4*>(src.petab + ((size_t)a * src.grid.S + ci[a]) * 16);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const float4 q = __ldg(row + j);
+      T[a][4 * j] = q.x;
+      T[a][4 * j + 1] = q.y;
+      T[a][4 * j + 2] = q.z;
+      T[a][4 * j + 3] = q.w;
+    }
+  }
+  float f[40];
+#pragma unroll
+  for (int a = 0; a < 3; a++) f[a] = T[a][0];
+#pragma unroll
+  for (int k = 0; k < 6; k++)
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      f[3 + 6 * k + a] = T[a][1 + k];
+      f[6 + 6 * k + a] = T[a][7 + k];
+    }
+  f[39] = 0.f;
+#pragma unroll
+  for (int c = 0; c < 20; c++) pk[c] = tc::pack_bf16x2(f[2 * c], f[2 * c + 1]);
+}
+
+// table rows: [x, sin_0..sin_5, cos_0..cos_5, 0, 0, 0] per (axis, coordinate index)
+__global__ void k_pe_table(GridP g, float* __restrict__ tab) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * g.S) return;
+  const int a = (int)(i / g.S);
+  const int64_t c = i % g.S;
+  const float x = (float)(gpos(g, a, c) - 0.5);
+  float* row = tab + i * 16;
+  row[0] = x;
+  for (int k = 0; k < 6; k++) {
+    float sv, cv;
+    sincospif(x * (float)(1 << k), &sv, &cv);
+    row[1 + k] = sv;
+    row[7 + k] = cv;
+  }
+  row[13] = row[14] = row[15] = 0.f;
+}
+
+template <int K>
+__device__ __forceinline__ void pe_piece_k(const PointSrc& src, int64_t n, int64_t p, PePiece& st,
+                                           uint32_t (&pk)[32]) {
+  if (K == 0) {
+    double pt[3] = {0.5, 0.5, 0.5};
+    st.ok = p < n;
+    if (st.ok) point_of(src, p, pt);
+#pragma unroll
+    for (int c = 0; c < 3; c++) st.x[c] = (float)(pt[c] - 0.5);
+    pk[0] = tc::pack_bf16x2(st.x[0], st.x[1]);
+    st.pend = st.x[2];
+  }
+  float sv[3], cv[3];
+#pragma unroll
+  for (int c = 0; c < 3; c++) sincospif(st.x[c] * (float)(1 << K), &sv[c], &cv[c]);
+  pk[1 + 3 * K] = tc::pack_bf16x2(st.pend, sv[0]);
+  pk[2 + 3 * K] = tc::pack_bf16x2(sv[1], sv[2]);
+  pk[3 + 3 * K] = tc::pack_bf16x2(cv[0], cv[1]);
+  st.pend = cv[2];
+  if (K == 5) {
+    pk[19] = tc::pack_bf16x2(st.pend, 0.f);
+#pragma unroll
+    for (int c = 0; c < 20; c++) pk[c] = st.ok ? pk[c] : 0u;
+#pragma unroll
+    for (int c = 20; c < 32; c++) pk[c] = 0u;
+  }
+}
+// runtime piece index -> compile-time register indices (no local-memory array)
+__device__ __forceinline__ void pe_piece(const PointSrc& src, int64_t n, int64_t p, int k, PePiece& st,
+                                         uint32_t (&pk)[32]) {
+  switch (k) {
+    case 0: pe_piece_k<0>(src, n, p, st, pk); break;
+    case 1: pe_piece_k<1>(src, n, p, st, pk); break;
+    case 2: pe_piece_k<2>(src, n, p, st, pk); break;
+    case 3: pe_piece_k<3>(src, n, p, st, pk); break;
+    case 4: pe_piece_k<4>(src, n, p, st, pk); break;
+    default: pe_piece_k<5>(src, n, p, st, pk); break;
+  }
+}
+
 // ===========================================================================
 // CTA-pair, N = 256, tile ping-pong evaluator (odc_mlp_tc4: mlp_impl 3)
 //
@@ -984,11 +1110,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
     const uint32_t a_pe = smem_u32(A0 + hc * tc4::kTileABytes);
     uint32_t af[2] = {0, 0};
     uint32_t pe[32];
+    PePiece pes;
     int64_t p_prev = -1;
     float dot_prev[2] = {0.f, 0.f};
     const bool tr = r == 0 && crank == 0 && hc == 0;
     if (cid < npairs) {
-      pe_row_packed(src, n, cid * 512 + hc * 256 + crank * 128 + r, pe);
+      if (src.petab) pe_from_table(src, n, cid * 512 + hc * 256 + crank * 128 + r, pe);
+      else pe_row_packed(src, n, cid * 512 + hc * 256 + crank * 128 + r, pe);
       store_pe_row(pe, a_pe, r);
       release(0);
       release(1);
@@ -1004,7 +1132,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
           if (p_prev >= 0) finish_label(m, src, n, p_prev + 256, dot_prev[1], labels, raw);
           p_prev = -1;
         }
-        if (l == kDepth - 1 && next < npairs) pe_row_packed(src, n, next * 512 + hc * 256 + crank * 128 + r, pe);
 #pragma unroll
         for (int t = 0; t < 2; t++) {
           const uint32_t a_t = smem_u32(A0 + t * tc4::kTileABytes);
@@ -1030,6 +1157,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
             }
             release(t);
             if (tr) ODC_TRACE(ti, l, 10 + t);
+            // slack until the next layer: one piece of the next pair's encoding
+            if (t == 1 && next < npairs) {
+              const int64_t pn = next * 512 + hc * 256 + crank * 128 + r;
+              if (src.petab) {  // grid points: table lookups, in one layer's slack
+                if (l == kDepth - 2) pe_from_table(src, n, pn, pe);
+              } else if (l >= 1) {  // explicit points: one frequency per layer
+                pe_piece(src, n, pn, l - 1, pes, pe);
+              }
+              if (tr) ODC_TRACE(ti, l, 14);
+            }
           } else {
             float d = 0.f;
 #pragma unroll
@@ -1095,10 +1232,30 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
     }
     const int64_t np4 = (n + 511) / 512;
     const int64_t pairs = (g_num_sms / 2) < np4 ? (g_num_sms / 2) : np4;
+    PointSrc sp = src;
+    sp.petab = nullptr;
+    sp.fd_m = sp.fd_s = 0;
+    float* tab = nullptr;
+    if (!src.pts && src.begin + n <= INT32_MAX && src.grid.S >= 2) {
+      // grid points: per-axis encoding table + divisor by S (CUTLASS-style
+      // round-up multiplier, exact for dividends < 2^31)
+      uint32_t l2 = 0;
+      while ((1u << l2) < (uint32_t)src.grid.S) l2++;
+      const uint32_t pw = 31 + l2;
+      sp.fd_m = (uint32_t)(((1ull << pw) + (uint64_t)src.grid.S - 1) / (uint64_t)src.grid.S);
+      sp.fd_s = pw - 32;
+      if (cudaMallocAsync((void**)&tab, sizeof(float) * 16 * 3 * src.grid.S, s) == cudaSuccess) {
+        k_pe_table<<<(unsigned)((3 * src.grid.S + 127) / 128), 128, 0, s>>>(src.grid, tab);
+        sp.petab = tab;
+      } else {
+        cudaGetLastError();
+      }
+    }
     if (m.has_bias)
-      k_mlp_tc4<true><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, src, n, labels, raw);
+      k_mlp_tc4<true><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, sp, n, labels, raw);
     else
-      k_mlp_tc4<false><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, src, n, labels, raw);
+      k_mlp_tc4<false><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, sp, n, labels, raw);
+    if (tab) cudaFreeAsync(tab, s);
     return 0;
   }
   if (m.impl == 0 && m.w_tc2 != nullptr) {

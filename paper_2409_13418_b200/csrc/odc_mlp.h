@@ -37,6 +37,10 @@ struct PointSrc {
   const double* pts;
   GridP grid;
   int64_t begin;
+  // grid sources, filled in by mlp_eval: per-axis encoding table (x, sin_k,
+  // cos_k of every coordinate index, 16 floats per row) and a fast divisor by S
+  const float* petab;
+  uint32_t fd_m, fd_s;
 };
 
 size_t mlp_packed_weight_elems();

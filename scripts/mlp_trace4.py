@@ -25,5 +25,7 @@ for ti in range(2):
     for l in range(8):
         row = [(t[ti, l, e] - base) if t[ti, l, e] else float("nan") for e in range(12)]
         print(f"{ti:4d} {l:5d} " + " ".join(f"{x:8.0f}" for x in row))
+print("point_of alone:", [t[i, 0, 13] - t[i, 0, 12] for i in range(2)])
+print("piece ends:", [[t[i, l, 14] - (t[i, l, 11]) for l in range(1, 7)] for i in range(2)])
 per = [t[0, l + 1, 0] - t[0, l, 0] for l in range(1, 6)]
 print(f"mean layer period {np.mean(per):.0f} cycles; pair {t[1, 0, 0] - t[0, 0, 0]:.0f}; kernel {tr[-1] / 1e6:.3f} ms")
