@@ -48,6 +48,15 @@ static_assert(sizeof(WordRec) == 64, "WordRec must be one 64-byte record");
 __device__ __forceinline__ int64_t word_of(const GridP& g, int64_t x, int64_t y, int64_t z) {
   return ((z - g.z0) * g.S + y) * g.W + (x >> 5);
 }
+// non-negative a / b and a % b with the 32-bit divider when both fit (the
+// 64-bit one is a long software routine)
+__device__ __forceinline__ int64_t idiv(int64_t a, int64_t b) {
+  return ((uint64_t)a <= 0xffffffffull && (uint64_t)b <= 0xffffffffull) ? (int64_t)((uint32_t)a / (uint32_t)b) : a / b;
+}
+__device__ __forceinline__ int64_t imod(int64_t a, int64_t b) {
+  return ((uint64_t)a <= 0xffffffffull && (uint64_t)b <= 0xffffffffull) ? (int64_t)((uint32_t)a % (uint32_t)b) : a % b;
+}
+
 __device__ __forceinline__ void vid_coords(const GridP& g, int64_t vid, int64_t c[3]) {
   if ((uint64_t)vid <= 0xffffffffull && g.S <= 0xffff) {  // 32-bit divisions (every grid up to 2^32 vertices)
     const uint32_t v = (uint32_t)vid, S = (uint32_t)g.S;

@@ -33,10 +33,10 @@ __device__ __forceinline__ void atomic_max_nonneg_double(unsigned long long* a, 
 __global__ void __launch_bounds__(256) k_labels_analytic(GridP g, FieldP f, uint32_t* __restrict__ L) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t rowbits = g.W * 32;
-  const int64_t row = gid / rowbits;  // window-local row
+  const int64_t row = idiv(gid, rowbits);  // window-local row
   if (row >= g.nz * g.S) return;      // whole warps (rowbits is a multiple of 32)
   const int64_t x = gid - row * rowbits;
-  const int64_t y = row % g.S, z = g.z0 + row / g.S;
+  const int64_t y = imod(row, g.S), z = g.z0 + idiv(row, g.S);
   uint32_t lab = 0;
   if (x < g.S) {
     double p[3] = {gpos(g, 0, x), gpos(g, 1, y), gpos(g, 2, z)};
@@ -54,7 +54,7 @@ void launch_labels_analytic(const GridP& g, const FieldP& f, uint32_t* L, cudaSt
 __global__ void k_pack_labels(GridP g, const uint8_t* __restrict__ bytes, uint32_t* __restrict__ L) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t rowbits = g.W * 32;
-  const int64_t row = gid / rowbits;  // window-local row; bytes are window-local flat
+  const int64_t row = idiv(gid, rowbits);  // window-local row; bytes are window-local flat
   if (row >= g.nz * g.S) return;
   const int64_t x = gid - row * rowbits;
   uint32_t lab = x < g.S ? (uint32_t)(bytes[row * g.S + x] != 0) : 0u;
@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(kActiveBlock) k_active_bits(GridP g, const uin
   uint32_t c[5] = {0, 0, 0, 0, 0};
   uint32_t shell = 0;
   if (idx < g.NW) {
-    const int64_t row = idx / g.W, wx = idx - row * g.W;
-    const int64_t y = row % g.S, z = g.z0 + row / g.S;
+    const int64_t row = idiv(idx, g.W), wx = idx - row * g.W;
+    const int64_t y = imod(row, g.S), z = g.z0 + idiv(row, g.S);
     ActiveBits b = compute_active(g, L, y, z, wx);
     WordRec r;
     for (int a = 0; a < 3; a++) {
@@ -254,8 +254,8 @@ __global__ void __launch_bounds__(kActiveBlock) k_active_compact(GridP g, WordRe
   rec[idx].pe = pos[0];
   rec[idx].pq = pos[1];
   rec[idx].pc = pos[2];
-  const int64_t row = idx / g.W, wx = idx - row * g.W;
-  const int64_t y = row % g.S, z = g.z0 + row / g.S;
+  const int64_t row = idiv(idx, g.W), wx = idx - row * g.W;
+  const int64_t y = imod(row, g.S), z = g.z0 + idiv(row, g.S);
   const int64_t vbase = (z * g.S + y) * g.S + wx * 32;  // global vertex id of bit 0 (x = 32 wx)
   // edges: ascending vertex, then axis (edge key = vid*3 + axis)
   uint32_t any = r.e[0] | r.e[1] | r.e[2];
@@ -1067,7 +1067,7 @@ __constant__ int c_LF_CORNER[6] = {0, 0, 0, 1, 2, 4};
 __constant__ int c_LF_NORMAL[6] = {0, 1, 2, 0, 1, 2};
 
 __device__ __forceinline__ int64_t cell_base_vid(const GridP& g, int64_t cell) {
-  const int64_t x = cell % g.R, y = (cell / g.R) % g.R, z = cell / (g.R * g.R);
+  const int64_t x = imod(cell, g.R), y = imod(idiv(cell, g.R), g.R), z = idiv(cell, g.R * g.R);
   return x + y * g.S + z * g.S2;
 }
 __device__ __forceinline__ int64_t corner_off(const GridP& g, int c) {
@@ -1178,7 +1178,7 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
   out.pinfo[ci] = ((uint64_t)pbase << 24) | T.cyc_of_edge;
   double hmin = g.h[0] < g.h[1] ? g.h[0] : g.h[1];
   hmin = hmin < g.h[2] ? hmin : g.h[2];
-  const int64_t cc[3] = {cell % g.R, (cell / g.R) % g.R, cell / (g.R * g.R)};
+  const int64_t cc[3] = {imod(cell, g.R), imod(idiv(cell, g.R), g.R), idiv(cell, g.R * g.R)};
   uint32_t nfb = 0;
   int slot = 0;
   for (int k = 0; k < T.ncyc; k++) {
@@ -1786,7 +1786,7 @@ __global__ void k_count_owned_faces(GridP g, const WordRec* __restrict__ rec, De
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t nf = 0, n4 = 0;
   if (idx < g.NW) {
-    const int64_t z = g.z0 + (idx / g.W) / g.S;
+    const int64_t z = g.z0 + idiv(idiv(idx, g.W), g.S);
     if (z >= g.own0 && z < g.own1) {
       const WordRec& r = rec[idx];
       for (int a = 0; a < 3; a++) {
