@@ -173,6 +173,70 @@ __device__ __forceinline__ void rot_rows(const double l[3], const double* R, dou
   for (int j = 0; j < 3; j++) o[j] = fma(l[2], R[6 + j], fma(l[1], R[3 + j], __dmul_rn(l[0], R[j])));
 }
 
+// signed distance of one primitive node at p (fields.py:75-139); shared by
+// the interpreter and the fast paths so both give identical bits
+__device__ __forceinline__ double prim_sd(int op, const double* __restrict__ q, const double p[3]) {
+  if (op == ODC_OP_SPHERE_SD) {  // fields.py:80-82
+    double d[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+    return __dsub_rn(norm3(d), __ldg(q + 3));
+  }
+  if (op == ODC_OP_BOX_SD) {  // fields.py:103-111
+    double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+    if (__ldg(q + 6) != 0.0) {
+      double R[9], o[3];
+      for (int j = 0; j < 9; j++) R[j] = __ldg(q + 7 + j);
+      rot_rows(l, R, o);
+      l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
+    }
+    double qq[3], mq[3];
+    for (int a = 0; a < 3; a++) {
+      qq[a] = __dsub_rn(fabs(l[a]), __ldg(q + 3 + a));
+      mq[a] = qq[a] > 0.0 ? qq[a] : 0.0;
+    }
+    const double outside = norm3(mq);
+    double mx = qq[0];
+    if (qq[1] > mx) mx = qq[1];
+    if (qq[2] > mx) mx = qq[2];
+    const double inside = mx < 0.0 ? mx : 0.0;
+    return __dadd_rn(outside, inside);
+  }
+  if (op == ODC_OP_TORUS_SD) {  // fields.py:122-126
+    double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+    const double ring = __dsub_rn(hypot_glibc(l[0], l[1]), __ldg(q + 3));
+    return __dsub_rn(hypot_glibc(ring, l[2]), __ldg(q + 4));
+  }
+  // ODC_OP_PLANE_SD, fields.py:138-139 (dgemv)
+  double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+  double nn[3] = {__ldg(q + 3), __ldg(q + 4), __ldg(q + 5)};
+  return dot3_fma(l, nn);
+}
+// sd < 0 for one primitive.  For a box, sd = |max(q, 0)| + min(max_i q_i, 0)
+// is negative exactly when every q_i < 0 (otherwise the min term is 0 and
+// the norm is >= 0), so the label needs neither the norm nor its sqrt.
+__device__ __forceinline__ bool prim_inside(int op, const double* __restrict__ q, const double p[3]) {
+  if (op != ODC_OP_BOX_SD) return prim_sd(op, q, p) < 0.0;
+  double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+  if (__ldg(q + 6) != 0.0) {
+    double R[9], o[3];
+    for (int j = 0; j < 9; j++) R[j] = __ldg(q + 7 + j);
+    rot_rows(l, R, o);
+    l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
+  }
+  bool in = true;
+  for (int a = 0; a < 3; a++) in &= __dsub_rn(fabs(l[a]), __ldg(q + 3 + a)) < 0.0;
+  return in;
+}
+__device__ __forceinline__ bool is_prim(int op) {
+  return op == ODC_OP_SPHERE_SD || op == ODC_OP_BOX_SD || op == ODC_OP_TORUS_SD || op == ODC_OP_PLANE_SD;
+}
+// fields.py:239-242
+__device__ __forceinline__ double smooth_raw(double k, double sd) {
+  double kd = __dmul_rn(k, sd);
+  kd = kd < -500.0 ? -500.0 : kd;
+  kd = kd > 500.0 ? 500.0 : kd;
+  return __ddiv_rn(1.0, __dadd_rn(1.0, exp(kd)));
+}
+
 static __device__ __noinline__ double field_raw_prog(const odc_node* __restrict__ nodes, int n_nodes, const double pt[3]) {
   double st[kMaxValueStack];
   double pst[kMaxPointStack][3];
@@ -182,44 +246,10 @@ static __device__ __noinline__ double field_raw_prog(const odc_node* __restrict_
     const int op = __ldg(&nodes[i].op);
     const double* q = nodes[i].p;
     switch (op) {
-      case ODC_OP_SPHERE_SD: {  // fields.py:80-82
-        double d[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
-        st[sp++] = __dsub_rn(norm3(d), __ldg(q + 3));
-        break;
-      }
-      case ODC_OP_BOX_SD: {  // fields.py:103-111
-        double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
-        if (__ldg(q + 6) != 0.0) {
-          double R[9], o[3];
-          for (int j = 0; j < 9; j++) R[j] = __ldg(q + 7 + j);
-          rot_rows(l, R, o);
-          l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
-        }
-        double qq[3], mq[3];
-        for (int a = 0; a < 3; a++) {
-          qq[a] = __dsub_rn(fabs(l[a]), __ldg(q + 3 + a));
-          mq[a] = qq[a] > 0.0 ? qq[a] : 0.0;
-        }
-        double outside = norm3(mq);
-        double mx = qq[0];
-        if (qq[1] > mx) mx = qq[1];
-        if (qq[2] > mx) mx = qq[2];
-        double inside = mx < 0.0 ? mx : 0.0;
-        st[sp++] = __dadd_rn(outside, inside);
-        break;
-      }
-      case ODC_OP_TORUS_SD: {  // fields.py:122-126
-        double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
-        double ring = __dsub_rn(hypot_glibc(l[0], l[1]), __ldg(q + 3));
-        st[sp++] = __dsub_rn(hypot_glibc(ring, l[2]), __ldg(q + 4));
-        break;
-      }
-      case ODC_OP_PLANE_SD: {  // fields.py:138-139 (dgemv)
-        double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
-        double nn[3] = {__ldg(q + 3), __ldg(q + 4), __ldg(q + 5)};
-        st[sp++] = dot3_fma(l, nn);
-        break;
-      }
+      case ODC_OP_SPHERE_SD:
+      case ODC_OP_BOX_SD:
+      case ODC_OP_TORUS_SD:
+      case ODC_OP_PLANE_SD: st[sp++] = prim_sd(op, q, p); break;
       case ODC_OP_SD2RAW: st[sp - 1] = st[sp - 1] < 0.0 ? 1.0 : 0.0; break;  // fields.py:70-72
       case ODC_OP_RAW_MAX:
       case ODC_OP_SD_MAX: {
@@ -262,22 +292,37 @@ static __device__ __noinline__ double field_raw_prog(const odc_node* __restrict_
         pp--;
         p[0] = pst[pp][0]; p[1] = pst[pp][1]; p[2] = pst[pp][2];
         break;
-      case ODC_OP_SMOOTH: {  // fields.py:239-242
-        double kd = __dmul_rn(__ldg(q), st[sp - 1]);
-        kd = kd < -500.0 ? -500.0 : kd;
-        kd = kd > 500.0 ? 500.0 : kd;
-        st[sp - 1] = __ddiv_rn(1.0, __dadd_rn(1.0, exp(kd)));
-        break;
-      }
+      case ODC_OP_SMOOTH: st[sp - 1] = smooth_raw(__ldg(q), st[sp - 1]); break;
       default: break;
     }
   }
   return sp > 0 ? st[sp - 1] : 0.0;
 }
 
-// Fast paths for the common one-primitive programs (sphere / torus / box);
-// identical arithmetic to the interpreter.
+// Fast paths (registers only, no stack) for the program shapes of the
+// scenes: one primitive -> raw or smoothed, and a CSG pair of primitives
+// (union / intersection / difference of their binary raws).  Same node
+// arithmetic as the interpreter, so identical bits; anything else runs the
+// interpreter.
 __device__ __forceinline__ double field_raw(const FieldP& f, const double p[3]) {
+  const odc_node* nd = f.nodes;
+  if (f.n_nodes == 2) {
+    const int op0 = __ldg(&nd[0].op), op1 = __ldg(&nd[1].op);
+    if (is_prim(op0) && op1 == ODC_OP_SD2RAW) return prim_inside(op0, nd[0].p, p) ? 1.0 : 0.0;
+    if (is_prim(op0) && op1 == ODC_OP_SMOOTH) return smooth_raw(__ldg(nd[1].p), prim_sd(op0, nd[0].p, p));
+  } else if (f.n_nodes == 5) {
+    const int op0 = __ldg(&nd[0].op), op1 = __ldg(&nd[1].op), op2 = __ldg(&nd[2].op), op3 = __ldg(&nd[3].op),
+              op4 = __ldg(&nd[4].op);
+    if (is_prim(op0) && op1 == ODC_OP_SD2RAW && is_prim(op2) && op3 == ODC_OP_SD2RAW &&
+        (op4 == ODC_OP_RAW_MAX || op4 == ODC_OP_RAW_MIN || op4 == ODC_OP_RAW_DIFF)) {
+      const double a = prim_inside(op0, nd[0].p, p) ? 1.0 : 0.0;
+      double b = prim_inside(op2, nd[2].p, p) ? 1.0 : 0.0;
+      if (op4 == ODC_OP_RAW_MAX) return (a >= b) ? a : b;
+      if (op4 == ODC_OP_RAW_MIN) return (a <= b) ? a : b;
+      b = __dsub_rn(1.0, b);
+      return (a <= b) ? a : b;
+    }
+  }
   return field_raw_prog(f.nodes, f.n_nodes, p);
 }
 __device__ __forceinline__ uint32_t field_label(const FieldP& f, const double p[3]) {
