@@ -267,6 +267,12 @@ def run_gpu(args, rank, world, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_step = float(t.item())
     V, T = res.mesh.n_vertices, res.mesh.n_triangles
+    # mesh checks of the last end-to-end result, on the GPU, outside the timed region
+    from paper_2409_13418_b200.mesh import count_self_intersections, validate_manifold
+
+    rep = validate_manifold(res.mesh)
+    stats_checks = {"manifold": rep.manifold, "nonmanifold_edges": len(rep.nonmanifold_edges),
+                    "boundary_edges": rep.boundary_edges, "self_intersections": count_self_intersections(res.mesh)}
     if is_mlp(field):
         h2d = (64 * 256 + 7 * 256 * 256) * 2 + 8 * 256 * 4 + 256 * 4
     else:
@@ -331,7 +337,7 @@ def run_gpu(args, rank, world, dist):
         "clocks": clock,
         "stage_ms": {n: float(np.mean([s[i] for s in stage])) for i, n in enumerate(stage_names)},
         "wall_s_timed_region": t_wall,
-        "mesh": stats_snapshot,
+        "mesh": {**stats_snapshot, **stats_checks},
     }
     print(json.dumps(line), flush=True)
 

@@ -97,3 +97,24 @@ def test_gpu_triangle_areas_equal_numpy(name):
 
     m = golden_mesh(name)
     assert np.array_equal(triangle_areas(m), m.areas())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["sphere_64", "torus_64", "rotated_box_64", "csg_union_64", "csg_difference_64",
+                                 "smooth_sphere_64", "thin_shell_64"])
+def test_gpu_chamfer_to_reference_mesh(tag):
+    """north_star's tolerance check: the GPU mesh against the reference's own
+    mesh (golden) -- symmetric mean squared surface distance (metric_md2,
+    metrics.py:26-32) and the sampled Hausdorff distance, both far below
+    (1e-4 h)."""
+    from golden_util import field_of, load
+    from paper_2409_13418_b200 import GridSpec, contour
+    from paper_2409_13418_b200.metrics import metric_hdd, metric_md2
+
+    f, lo, hi, R = field_of(tag)
+    ref = load(tag)
+    ours = contour(f, GridSpec(lo, hi, R)).mesh
+    theirs = TriangleMesh.trusted(ref["vertices"], ref["triangles"])
+    h = 1.0 / R
+    assert metric_md2(ours, theirs, n=20000) <= (1e-4 * h) ** 2
+    assert metric_hdd(ours, theirs, n=20000) <= 1e-4 * h
