@@ -160,6 +160,11 @@ int odc_field_mlp(odc_ctx* ctx, const odc_mlp_desc* desc, odc_field** out);
  * on the surface are perturbed like the reference's "perturb" mode. */
 int odc_field_mesh(odc_ctx* ctx, const double* vertices, int64_t n_vertices, const int64_t* triangles,
                    int64_t n_triangles, odc_field** out);
+/* VoxelField (fields.py:245-278): trilinear interpolation of a dense
+ * (nx, ny, nz) C-order f64 grid at origin + index * spacing, zero outside;
+ * continuous, label = raw > 1/2. */
+int odc_field_voxels(odc_ctx* ctx, const double origin[3], const double spacing[3], const double* values, int64_t nx,
+                     int64_t ny, int64_t nz, odc_field** out);
 void odc_field_free(odc_ctx* ctx, odc_field* f);
 
 void odc_default_options(odc_options* o);

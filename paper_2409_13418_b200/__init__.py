@@ -19,6 +19,7 @@ from .fields import (  # noqa: F401
     SphereField,
     SurfaceCoincidenceError,
     TorusField,
+    VoxelField,
     field_from_dict,
     load_scene,
     rotation_from_euler,

@@ -88,7 +88,7 @@ EXPORTS = (
     "odc_copy_array", "odc_eval_raw", "odc_eval_labels", "odc_set_param", "odc_extract_slab",
     "odc_slab_globalize", "odc_mesh_finish", "odc_profile_mlp", "odc_export_obj", "odc_export_ply",
     "odc_validate_manifold", "odc_validate_copy", "odc_count_self_intersections", "odc_self_intersection_pairs",
-    "odc_mesh_distance", "odc_triangle_areas", "odc_field_mesh",
+    "odc_mesh_distance", "odc_triangle_areas", "odc_field_mesh", "odc_field_voxels",
 )
 
 _lib = None
@@ -117,6 +117,7 @@ def load():
         L.odc_field_analytic.argtypes = [vp, P(Node), i32, i32, dbl, P(vp)]
         L.odc_field_mlp.argtypes = [vp, P(MlpDesc), P(vp)]
         L.odc_field_mesh.argtypes = [vp, vp, i64, vp, i64, P(vp)]
+        L.odc_field_voxels.argtypes = [vp, P(dbl), P(dbl), vp, i64, i64, i64, P(vp)]
         L.odc_field_free.argtypes = [vp, vp]
         L.odc_field_free.restype = None
         L.odc_default_options.argtypes = [P(Options)]

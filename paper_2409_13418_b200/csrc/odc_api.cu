@@ -101,6 +101,8 @@ struct odc_field {
   // mesh winding-number field (kind 2)
   WindDev wind{};
   void* wind_buf = nullptr;
+  // voxel field (kind 3)
+  VoxDev vox{};
 };
 
 struct odc_ctx {
@@ -206,6 +208,9 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
   } else if (f->kind == 2) {
     PointSrc src{pts, GridP{}, 0};
     winding_eval(f->wind, src, n, lab, raw, c->d_fail, c->stream);
+  } else if (f->kind == 3) {
+    PointSrc src{pts, GridP{}, 0};
+    voxel_eval(f->vox, src, n, lab, raw, c->stream);
   } else {
     PointSrc src{pts, GridP{}, 0};
     MlpDev md = f->mlp;
@@ -429,6 +434,8 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     PointSrc src{nullptr, g, g.z0 * g.S2};
     if (f->kind == 2) {
       winding_eval(f->wind, src, g.nz * g.S2, bytes, nullptr, c->d_fail, s);
+    } else if (f->kind == 3) {
+      voxel_eval(f->vox, src, g.nz * g.S2, bytes, nullptr, s);
     } else {
       MlpDev md = f->mlp;
       md.impl = c->mlp_impl;
@@ -710,6 +717,10 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   } else {
     if (!f->continuous)
       throw OdcError{ODC_E_CONFIG, "fd-gradient normals require a field with continuous raw values"};
+    if (c->inst_edges) {  // kept stage output: the instance pairs exist in this mode too
+      launch_instance_edges(g, c->L, c->rec, c->inst_key, Q, c->pos1d, c->inst_edges, s);
+      check_launch(c);
+    }
     double* pts = need(c->arena.get<double>(18 * K));
     double* raw = need(c->arena.get<double>(6 * K));
     uint8_t* lab = need(c->arena.get<uint8_t>(6 * K));
@@ -1097,16 +1108,53 @@ int odc_field_mesh(odc_ctx* c, const double* vertices, int64_t n_vertices, const
   return ODC_OK;
 }
 
+int odc_field_voxels(odc_ctx* c, const double origin[3], const double spacing[3], const double* values, int64_t nx,
+                     int64_t ny, int64_t nz, odc_field** out) {
+  if (!c || !out || !origin || !spacing || !values) return ODC_E_ARG;
+  if (nx < 2 || ny < 2 || nz < 2) {
+    c->err = "voxel values must be at least 2 x 2 x 2";
+    return ODC_E_VALUE;
+  }
+  cudaSetDevice(c->device);
+  odc_field* f = new (std::nothrow) odc_field();
+  if (!f) return ODC_E_NOMEM;
+  f->kind = 3;
+  f->continuous = 1;
+  f->iso = 0.5;
+  const size_t bytes = sizeof(double) * (size_t)nx * ny * nz;
+  double* d = nullptr;
+  if (cudaMallocAsync((void**)&d, bytes, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(d, values, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    if (d) cudaFreeAsync(d, c->stream);
+    delete f;
+    c->err = "field upload failed";
+    return ODC_E_NOMEM;
+  }
+  f->vox.values = d;
+  f->vox.nx = nx;
+  f->vox.ny = ny;
+  f->vox.nz = nz;
+  for (int a = 0; a < 3; a++) {
+    f->vox.origin[a] = origin[a];
+    f->vox.spacing[a] = spacing[a];
+  }
+  *out = f;
+  return ODC_OK;
+}
+
 void odc_field_free(odc_ctx* c, odc_field* f) {
   if (!f) return;
   if (c) {
     cudaStreamSynchronize(c->stream);
-    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head, f->wind_buf};
+    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head, f->wind_buf,
+                    (void*)f->vox.values};
     for (void* b : bufs)
       if (b) cudaFreeAsync(b, c->stream);  // back to the pool, no device-wide sync
   } else {
     cudaDeviceSynchronize();
-    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head, f->wind_buf};
+    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head, f->wind_buf,
+                    (void*)f->vox.values};
     for (void* b : bufs)
       if (b) cudaFreeAsync(b, 0);
     cudaDeviceSynchronize();

@@ -782,6 +782,24 @@ struct Search2DState {
 size_t search2d_state_bytes(int64_t Q) { return (size_t)Q * sizeof(Search2DState); }
 int search2d_num_steps(const OptP& o) { return 1 + o.s1_lin + o.s1_bin + o.s2_lin + o.s2_bin; }
 
+// instance pairs only (face_pairings, dualize.py:72-88) -- the fd-gradient
+// mode has no 2D search to write them
+__global__ void k_instance_edges(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+                                 const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
+                                 int64_t* __restrict__ inst_edges) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  Inst2D I;
+  int64_t pair[2];
+  decode_instance(g, L, rec, inst_key[q], pos1d, I, pair);
+  inst_edges[2 * q] = pair[0];
+  inst_edges[2 * q + 1] = pair[1];
+}
+void launch_instance_edges(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* inst_key, int64_t Q,
+                           const double* pos1d, int64_t* inst_edges, cudaStream_t s) {
+  if (Q) k_instance_edges<<<grid_for(Q, 128), 128, 0, s>>>(g, L, rec, inst_key, Q, pos1d, inst_edges);
+}
+
 __global__ void k_s2_init(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
                           const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
                           Search2DState* __restrict__ S, int64_t* __restrict__ inst_edges) {

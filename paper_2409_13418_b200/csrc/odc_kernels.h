@@ -185,6 +185,17 @@ struct PointSrc;
 void winding_eval(const WindDev& w, const PointSrc& src, int64_t n, uint8_t* labels, double* raw,
                   unsigned int* failed, cudaStream_t s);
 
+// VoxelField (odc_voxel.cu; fields.py:245-278): dense (nx, ny, nz) f64 values
+struct VoxDev {
+  const double* values;
+  int64_t nx, ny, nz;
+  double origin[3], spacing[3];
+};
+void voxel_eval(const VoxDev& w, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s);
+
+void launch_instance_edges(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* inst_key, int64_t Q,
+                           const double* pos1d, int64_t* inst_edges, cudaStream_t s);
+
 // marching-cubes baseline (baseline.py:48-127)
 void launch_mc_points(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K, const double* raw_in,
                       const double* raw_out, double iso, double* pos, cudaStream_t s);

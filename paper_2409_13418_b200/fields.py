@@ -260,6 +260,24 @@ def is_mesh_winding(field):
     return _kind(field) == "MeshWindingField"
 
 
+class VoxelField(OccupancyField):
+    """Trilinear interpolation of a dense value grid, zero outside
+    (fields.py:245-278).  Evaluated on the GPU (csrc/odc_voxel.cu)."""
+
+    continuous = True
+
+    def __init__(self, origin, spacing, values):
+        self.origin = np.asarray(origin, dtype=np.float64)
+        self.spacing = np.asarray(spacing, dtype=np.float64)
+        self.values = np.asarray(values, dtype=np.float64)
+        if self.values.ndim != 3:
+            raise ValueError("voxel values must be a 3D array")
+
+
+def is_voxels(field):
+    return _kind(field) == "VoxelField"
+
+
 def _node(op, params=()):
     n = np.zeros((), dtype=NODE_DTYPE)
     n["op"] = op
@@ -408,7 +426,18 @@ def field_from_dict(spec, base_dir=None):
             path = Path(base_dir) / path
         mesh = import_obj(path)
         return MeshWindingField(mesh.vertices, mesh.triangles)
-    raise ValueError(f"unknown field type {kind!r} (voxel fields are not on the device path)")
+    if kind == "voxels":  # fields.py:432-440
+        from pathlib import Path
+
+        if "path" in spec:
+            path = Path(spec["path"])
+            if base_dir is not None and not path.is_absolute():
+                path = Path(base_dir) / path
+            values = np.load(path)
+        else:
+            values = np.asarray(spec["values"], dtype=np.float64)
+        return VoxelField(spec.get("origin", (0, 0, 0)), spec.get("spacing", (1, 1, 1)), values)
+    raise ValueError(f"unknown field type {kind!r}")
 
 
 class Scene:

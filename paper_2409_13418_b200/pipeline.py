@@ -17,7 +17,7 @@ from dataclasses import dataclass, field as dc_field
 import numpy as np
 
 from . import _lib
-from .fields import SurfaceCoincidenceError, field_continuous, is_mesh_winding, is_mlp, lower_program
+from .fields import SurfaceCoincidenceError, field_continuous, is_mesh_winding, is_mlp, is_voxels, lower_program
 from .mesh import GridSpec, TriangleMesh
 
 ONE_D_MODES = ("midpoint", "linear-interp", "binary-search")
@@ -151,6 +151,12 @@ class DeviceField:
             for i in range(3):
                 d.prior_center[i] = float(field.prior_center[i])
             rc = L.odc_field_mlp(ctx.handle, ctypes.byref(d), ctypes.byref(self.handle))
+        elif is_voxels(field):
+            vals = np.ascontiguousarray(field.values, dtype=np.float64)
+            o = (ctypes.c_double * 3)(*[float(x) for x in field.origin])
+            sp = (ctypes.c_double * 3)(*[float(x) for x in field.spacing])
+            nx, ny, nz = vals.shape
+            rc = L.odc_field_voxels(ctx.handle, o, sp, vals.ctypes.data, nx, ny, nz, ctypes.byref(self.handle))
         elif is_mesh_winding(field):
             v = np.ascontiguousarray(field.vertices, dtype=np.float64).reshape(-1, 3)
             t = np.ascontiguousarray(field.triangles, dtype=np.int64).reshape(-1, 3)
