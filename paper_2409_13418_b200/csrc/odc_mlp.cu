@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <type_traits>
 
 #include "odc_mlp.h"
@@ -830,7 +831,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-static int g_num_sms = 0;
 
 // impl: 0 = CTA-pair tcgen05 (default), 1 = SIMT reference, 2 = single-CTA tcgen05
 // Positional encoding built in pieces across the layers of the current tile
@@ -1209,27 +1209,27 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
     k_mlp_simt<<<(unsigned)blocks, kWidth, 0, s>>>(m, src, n, labels, raw);
     return 0;
   }
-  static bool attr = false;
-  if (!attr) {
+  // kernel attributes and the SM count, once per device (thread-safe: the
+  // batch mode drives one context per host thread)
+  static std::once_flag once[64];
+  static int num_sms[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  std::call_once(once[dev], [dev]() {
     cudaFuncSetAttribute(k_mlp_tc<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc2::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc2::kSmemBytes);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    attr = true;
-  }
+    cudaFuncSetAttribute(k_mlp_tc4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc4::kSmemBytes);
+    cudaFuncSetAttribute(k_mlp_tc4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc4::kSmemBytes);
+    cudaDeviceGetAttribute(&num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  });
+  const int g_num_sms = num_sms[dev];
   const int64_t ntiles = (n + 255) / 256;
   if (m.impl == 3) {
-    static bool attr4 = false;
-    if (!attr4) {
-      cudaFuncSetAttribute(k_mlp_tc4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc4::kSmemBytes);
-      cudaFuncSetAttribute(k_mlp_tc4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc4::kSmemBytes);
-      attr4 = true;
-    }
     const int64_t np4 = (n + 511) / 512;
     const int64_t pairs = (g_num_sms / 2) < np4 ? (g_num_sms / 2) : np4;
     PointSrc sp = src;
