@@ -698,11 +698,15 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       launch_search2d_lockstep_init(g, op, c->L, c->rec, c->inst_key, Q, c->pos1d, state, c->inst_edges, s);
       check_launch(c);
       const int nsteps = search2d_num_steps(op);
+      int64_t M = launch_search2d_lockstep_points(g, op, c->inst_key, Q, 0, state, pts, s);
+      check_launch(c);
       for (int step = 0; step < nsteps; step++) {
-        int64_t M = launch_search2d_lockstep_points(g, op, c->inst_key, Q, step, state, pts, s);
-        check_launch(c);
         eval_points(c, f, pts, M, lab, nullptr);
-        launch_search2d_lockstep_update(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, s);
+        if (step + 1 < nsteps) {  // update + the next step's points in one pass
+          M = launch_search2d_lockstep_step(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, pts, s);
+        } else {
+          launch_search2d_lockstep_update(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, s);
+        }
         check_launch(c);
       }
       launch_search2d_lockstep_finish(g, op, c->L, c->rec, c->inst_key, Q, c->pos1d, state, c->s2, dst, q_lo, q_hi,

@@ -832,21 +832,11 @@ __device__ __forceinline__ void inst_frame(const GridP& g, int64_t ikey, Inst2D&
   vposition(g, vid, I.org);
 }
 
-__global__ void k_s2_points(GridP g, OptP o, const int64_t* __restrict__ inst_key, int64_t Q, int step,
-                            const Search2DState* __restrict__ S, double* __restrict__ pts) {
-  int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// query point of instance (I, s) at lock-step ``step`` (ray r of the two
+// step-2 rays), in face coordinates (search.py:244-276)
+__device__ __forceinline__ void s2_point_uv(const OptP& o, const Inst2D& I, const Search2DState& s, int step, int r,
+                                            double& u, double& v) {
   const int n1 = o.s1_lin + o.s1_bin;
-  const bool two = step > n1;
-  const int64_t M = two ? 2 * Q : Q;
-  if (m >= M) return;
-  const int64_t q = two ? (m < Q ? m : m - Q) : m;
-  Inst2D I;
-  inst_frame(g, inst_key[q], I);
-  I.hu = g.h[I.bu];
-  I.hv = g.h[I.bv];
-  I.hmin = I.hu < I.hv ? I.hu : I.hv;
-  const Search2DState& s = S[q];
-  double u, v;
   if (step == 0) {
     u = s.mid[0];
     v = s.mid[1];
@@ -858,7 +848,6 @@ __global__ void k_s2_points(GridP g, OptP o, const int64_t* __restrict__ inst_ke
     u = s.mid[0] + d * s.ray[0];
     v = s.mid[1] + d * s.ray[1];
   } else {
-    const int r = m < Q ? 0 : 1;
     const double dir0 = r == 0 ? -s.dl[0] : s.dl[0], dir1 = r == 0 ? -s.dl[1] : s.dl[1];
     const double mr = o.s2_range * I.hmin;
     const int k = step - n1;
@@ -868,25 +857,38 @@ __global__ void k_s2_points(GridP g, OptP o, const int64_t* __restrict__ inst_ke
     u = s.q2[0] + d * dir0;
     v = s.q2[1] + d * dir1;
   }
-  double p[3];
+}
+__device__ __forceinline__ void s2_frame(const GridP& g, int64_t ikey, Inst2D& I) {
+  inst_frame(g, ikey, I);
+  I.hu = g.h[I.bu];
+  I.hv = g.h[I.bv];
+  I.hmin = I.hu < I.hv ? I.hu : I.hv;
+}
+
+__global__ void k_s2_points(GridP g, OptP o, const int64_t* __restrict__ inst_key, int64_t Q, int step,
+                            const Search2DState* __restrict__ S, double* __restrict__ pts) {
+  int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n1 = o.s1_lin + o.s1_bin;
+  const bool two = step > n1;
+  const int64_t M = two ? 2 * Q : Q;
+  if (m >= M) return;
+  const int64_t q = two ? (m < Q ? m : m - Q) : m;
+  Inst2D I;
+  s2_frame(g, inst_key[q], I);
+  double u, v, p[3];
+  s2_point_uv(o, I, S[q], step, m < Q ? 0 : 1, u, v);
   lift(I, u, v, p);
   pts[3 * m] = p[0];
   pts[3 * m + 1] = p[1];
   pts[3 * m + 2] = p[2];
 }
 
-__global__ void k_s2_update(GridP g, OptP o, const uint32_t* __restrict__ L, const int64_t* __restrict__ inst_key,
-                            int64_t Q, int step, const uint8_t* __restrict__ lab, Search2DState* __restrict__ S,
-                            DevStatus* dst) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= Q) return;
+// fold the labels of lock-step ``step`` into the search state (search.py:220-276)
+__device__ __forceinline__ void s2_apply(const GridP& g, const OptP& o, const uint32_t* __restrict__ L,
+                                         const int64_t* __restrict__ inst_key, int64_t Q, int64_t q, int step,
+                                         const uint8_t* __restrict__ lab, Inst2D& I, Search2DState& s,
+                                         DevStatus* dst) {
   const int n1 = o.s1_lin + o.s1_bin;
-  Search2DState s = S[q];
-  Inst2D I;
-  inst_frame(g, inst_key[q], I);
-  I.hu = g.h[I.bu];
-  I.hv = g.h[I.bv];
-  I.hmin = I.hu < I.hv ? I.hu : I.hv;
   if (step == 0) {
     s.mid_label = lab[q];
     // corner labels for the ray side
@@ -947,7 +949,44 @@ __global__ void k_s2_update(GridP g, OptP o, const uint32_t* __restrict__ L, con
       }
     }
   }
+}
+
+__global__ void k_s2_update(GridP g, OptP o, const uint32_t* __restrict__ L, const int64_t* __restrict__ inst_key,
+                            int64_t Q, int step, const uint8_t* __restrict__ lab, Search2DState* __restrict__ S,
+                            DevStatus* dst) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  Search2DState s = S[q];
+  Inst2D I;
+  s2_frame(g, inst_key[q], I);
+  s2_apply(g, o, L, inst_key, Q, q, step, lab, I, s, dst);
   S[q] = s;
+}
+
+// update with the labels of ``step`` and emit the query points of step + 1
+// (one thread per instance, both rays in step 2): one pass over the state
+// per lock-step instead of two
+__global__ void k_s2_step(GridP g, OptP o, const uint32_t* __restrict__ L, const int64_t* __restrict__ inst_key,
+                          int64_t Q, int step, const uint8_t* __restrict__ lab, Search2DState* __restrict__ S,
+                          DevStatus* dst, double* __restrict__ pts) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  Search2DState s = S[q];
+  Inst2D I;
+  s2_frame(g, inst_key[q], I);
+  s2_apply(g, o, L, inst_key, Q, q, step, lab, I, s, dst);
+  S[q] = s;
+  const int next = step + 1;
+  const int nr = next > o.s1_lin + o.s1_bin ? 2 : 1;
+  for (int r = 0; r < nr; r++) {
+    double u, v, p[3];
+    s2_point_uv(o, I, s, next, r, u, v);
+    lift(I, u, v, p);
+    const int64_t m = q + r * Q;
+    pts[3 * m] = p[0];
+    pts[3 * m + 1] = p[1];
+    pts[3 * m + 2] = p[2];
+  }
 }
 
 __global__ void k_s2_finish(GridP g, OptP o, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
@@ -1004,6 +1043,13 @@ void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32
                                      cudaStream_t s) {
   if (Q)
     k_s2_update<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, inst_key, Q, step, lab, (Search2DState*)state, dst);
+}
+int64_t launch_search2d_lockstep_step(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
+                                      int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
+                                      double* pts, cudaStream_t s) {
+  if (Q)
+    k_s2_step<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, inst_key, Q, step, lab, (Search2DState*)state, dst, pts);
+  return step + 1 > o.s1_lin + o.s1_bin ? 2 * Q : Q;
 }
 void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
                                      const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,

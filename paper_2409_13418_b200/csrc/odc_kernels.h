@@ -100,6 +100,10 @@ void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32
 void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
                                      const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,
                                      Stage2D out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s);
+// fused: fold the labels of ``step`` in and write the points of step + 1; returns their count
+int64_t launch_search2d_lockstep_step(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
+                                      int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
+                                      double* pts, cudaStream_t s);
 int search2d_num_steps(const OptP& o);
 
 // fd-gradient normals (pipeline.py:126-151): 6K raw samples

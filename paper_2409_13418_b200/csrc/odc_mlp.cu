@@ -233,24 +233,33 @@ __device__ __forceinline__ void grid_coords_fast(const PointSrc& src, int64_t p,
 __device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& src, int64_t n, int64_t p, float dot,
                                              uint8_t* __restrict__ labels, double* __restrict__ raw) {
   if (p < 0 || p >= n) return;
-  if (!raw && !src.pts) {
-    // labels only: the sign of the logit in fp32 (FP64 is a narrow pipe here).
-    // Its error is < 1e-4 for these magnitudes, so a margin of 1e-3 decides
-    // exactly; anything closer takes the fp64 path below.
-    int64_t c[3];
-    if (src.fd_m) {
-      uint32_t cf[3];
-      grid_coords_fast(src, p, cf);
-      c[0] = cf[0];
-      c[1] = cf[1];
-      c[2] = cf[2];
+  if (!raw) {
+    // labels only: the sign of the logit in fp32 (short dependent chains
+    // instead of fp64 divide / sqrt / exp).  Its error is < 1e-4 for these
+    // magnitudes, so a margin of 1e-3 decides exactly; anything closer takes
+    // the fp64 path below.
+    float xf[3];
+    if (src.pts) {
+#pragma unroll
+      for (int a = 0; a < 3; a++) xf[a] = (float)src.pts[3 * p + a];
     } else {
-      vid_coords(src.grid, src.begin + p, c);
+      int64_t c[3];
+      if (src.fd_m) {
+        uint32_t cf[3];
+        grid_coords_fast(src, p, cf);
+        c[0] = cf[0];
+        c[1] = cf[1];
+        c[2] = cf[2];
+      } else {
+        vid_coords(src.grid, src.begin + p, c);
+      }
+#pragma unroll
+      for (int a = 0; a < 3; a++) xf[a] = fmaf((float)c[a], (float)src.grid.h[a], (float)src.grid.lo[a]);
     }
     float d2 = 0.f;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-      const float x = fmaf((float)c[a], (float)src.grid.h[a], (float)src.grid.lo[a]) - (float)m.prior_center[a];
+      const float x = xf[a] - (float)m.prior_center[a];
       d2 = fmaf(x, x, d2);
     }
     const float lg = (float)m.amplitude * (dot + m.b_head) - (float)m.prior_scale * (sqrtf(d2) - (float)m.prior_radius);
