@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -98,6 +99,10 @@ struct odc_field {
   float* bias = nullptr;
   float* w_head = nullptr;
   MlpDev mlp{};
+  // host weights for the formats packed on first use (CTA-pair TS and SIMT evaluators)
+  std::vector<float> h_w0, h_wh;
+  int32_t h_din = 0;
+  std::mutex lazy;
   // mesh winding-number field (kind 2)
   WindDev wind{};
   void* wind_buf = nullptr;
@@ -200,6 +205,36 @@ void check_status(odc_ctx* c, DevStatus* dst) {
 }
 
 // Evaluate labels (and optionally raw) of n points through the field.
+// The CTA-pair TS (mlp_impl 0) and SIMT (1) evaluators read their own weight
+// layouts; those are packed and uploaded the first time a context selects
+// them (the default layout is uploaded with the field).
+void ensure_mlp_format(odc_ctx* c, const odc_field* fc) {
+  odc_field* f = const_cast<odc_field*>(fc);
+  if (f->kind != 1 || (c->mlp_impl != 0 && c->mlp_impl != 1)) return;
+  std::lock_guard<std::mutex> lock(f->lazy);
+  cudaStream_t s = c->stream;
+  if (c->mlp_impl == 0 && !f->w_tc2) {
+    std::vector<uint16_t> h(mlp_tc2_weight_elems());
+    mlp_pack_weights_tc2(f->h_w0.data(), f->h_din, f->h_wh.data(), h.data());
+    uint16_t* d = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d, h.size() * 2, s));
+    CUDA_TRY(cudaMemcpyAsync(d, h.data(), h.size() * 2, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    f->w_tc2 = d;
+    f->mlp.w_tc2 = d;
+  }
+  if (c->mlp_impl == 1 && !f->w_packed) {
+    std::vector<uint16_t> h(mlp_packed_weight_elems());
+    mlp_pack_weights(f->h_w0.data(), f->h_din, f->h_wh.data(), h.data());
+    uint16_t* d = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d, h.size() * 2, s));
+    CUDA_TRY(cudaMemcpyAsync(d, h.data(), h.size() * 2, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    f->w_packed = d;
+    f->mlp.w_packed = d;
+  }
+}
+
 void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* lab, double* raw) {
   if (n == 0) return;
   if (f->kind == 0) {
@@ -212,6 +247,7 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
     PointSrc src{pts, GridP{}, 0};
     voxel_eval(f->vox, src, n, lab, raw, c->stream);
   } else {
+    ensure_mlp_format(c, f);
     PointSrc src{pts, GridP{}, 0};
     MlpDev md = f->mlp;
     md.impl = c->mlp_impl;
@@ -437,6 +473,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     } else if (f->kind == 3) {
       voxel_eval(f->vox, src, g.nz * g.S2, bytes, nullptr, s);
     } else {
+      ensure_mlp_format(c, f);
       MlpDev md = f->mlp;
       md.impl = c->mlp_impl;
       mlp_eval(md, src, g.nz * g.S2, bytes, nullptr, s);
@@ -994,29 +1031,23 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
   f->kind = 1;
   f->continuous = 1;
   f->iso = 0.5;
-  const size_t ne = mlp_packed_weight_elems();
-  std::vector<uint16_t> packed(ne);
+  // only the default evaluator's layout now; the others are packed on first use
   const size_t nt = mlp_tc_weight_elems();
   std::vector<uint16_t> packed_tc(nt);
   mlp_pack_weights_tc(d->w0, d->d_in, d->w_hidden, packed_tc.data());
-  const size_t nt2 = mlp_tc2_weight_elems();
-  std::vector<uint16_t> packed_tc2(nt2);
-  mlp_pack_weights_tc2(d->w0, d->d_in, d->w_hidden, packed_tc2.data());
-  mlp_pack_weights(d->w0, d->d_in, d->w_hidden, packed.data());
+  f->h_w0.assign(d->w0, d->w0 + (size_t)d->d_in * 256);
+  f->h_wh.assign(d->w_hidden, d->w_hidden + (size_t)7 * 256 * 256);
+  f->h_din = d->d_in;
   // stream-ordered pool allocations: no driver round trip per field
   cudaStream_t s = c->stream;
-  if (cudaMallocAsync((void**)&f->w_packed, ne * 2, s) != cudaSuccess ||
-      cudaMallocAsync((void**)&f->w_tc, nt * 2, s) != cudaSuccess ||
-      cudaMallocAsync((void**)&f->w_tc2, nt2 * 2, s) != cudaSuccess ||
+  if (cudaMallocAsync((void**)&f->w_tc, nt * 2, s) != cudaSuccess ||
       cudaMallocAsync((void**)&f->bias, 8 * 256 * 4, s) != cudaSuccess ||
       cudaMallocAsync((void**)&f->w_head, 256 * 4, s) != cudaSuccess) {
     c->err = "field upload failed";
     delete f;
     return ODC_E_NOMEM;
   }
-  cudaMemcpyAsync(f->w_packed, packed.data(), ne * 2, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(f->w_tc, packed_tc.data(), nt * 2, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(f->w_tc2, packed_tc2.data(), nt2 * 2, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(f->bias, d->biases, 8 * 256 * 4, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(f->w_head, d->w_head, 256 * 4, cudaMemcpyHostToDevice, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) {  // usable from any stream once created
@@ -1825,6 +1856,12 @@ int odc_profile_mlp(odc_ctx* c, const odc_field* f, int64_t n, int64_t* trace, i
   for (int a = 0; a < 3; a++) {
     g.lo[a] = 0.0;
     g.h[a] = 1.0 / (double)g.R;
+  }
+  try {
+    ensure_mlp_format(c, f);
+  } catch (const OdcError& e) {
+    c->err = e.msg;
+    return e.code;
   }
   MlpDev md = f->mlp;
   md.impl = c->mlp_impl;
