@@ -462,6 +462,8 @@ def run_gpu_slabs(args, rank, world, dist):
     grid = GridSpec(lo, hi, R)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
 
+    last = {}
+
     def timed(n, to_host):
         ms = []
         for _ in range(n):
@@ -470,18 +472,26 @@ def run_gpu_slabs(args, rank, world, dist):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            contour_slab(field, grid, rank=rank, world=world, dist=dist, device=device, to_host=to_host)
+            out = contour_slab(field, grid, rank=rank, world=world, dist=dist, device=device, to_host=to_host)
             torch.cuda.synchronize()
             e1.record()
             e1.synchronize()
             t = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{device}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms.append(float(t.item()))
+            last["out"] = out
         return ms
 
     timed(args.warmup, False)
+    launches = 0
+    k_ms = []
     with ClockSampler(device) as clocks:
-        dev_ms = timed(args.steps, False)
+        dev_ms = []
+        for _ in range(args.steps):
+            dev_ms += timed(1, False)
+            if last["out"] is not None:  # rank 0: launches summed over ranks, slowest grid pass
+                launches += last["out"]["n_kernel_launches"]
+                k_ms.append(last["out"]["labels_kernel_ms"])
     clock = clocks.summary()
     timed(args.warmup, True)
     e2e_ms = timed(args.steps, True)
@@ -489,6 +499,34 @@ def run_gpu_slabs(args, rank, world, dist):
     e2e_step = float(np.mean(e2e_ms))
     if rank != 0:
         return
+    res = last["out"]
+    V, T = res.mesh.n_vertices, res.mesh.n_triangles
+    if is_mlp(field):
+        h2d = world * ((64 * 256 + 7 * 256 * 256) * 2 + 8 * 256 * 4 + 256 * 4)
+    else:
+        from paper_2409_13418_b200.fields import lower_program
+
+        h2d = world * 136 * len(lower_program(field))
+    d2h = V * 24 + T * 24 + V * 24 + (T * 24 if res.raw_mesh is not res.mesh else 0)
+    roof = None
+    if k_ms:
+        peaks, peak_kind = load_peaks()
+        km = float(np.mean(k_ms))
+        S3 = (R + 1) ** 3 / world  # the slowest rank's share of the grid, approximately
+        if is_mlp(field):
+            peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+            ach = float(field.flops_per_eval) * S3 / (km / 1e3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "kernel": "grid occupancy MLP of one slab (slowest rank)", "kernel_ms": km}
+        else:
+            W = (R + 1 + 31) // 32
+            nbytes = (R + 1) ** 2 * W * 4 / world
+            peak = float(peaks["hbm_gbs"])
+            ach = nbytes / (km / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "kernel": "k_labels_analytic of one slab (slowest rank)", "kernel_ms": km}
+        roof["peak_source"] = f"{peak_kind} (MEASURED_PEAKS.json)" if peak_kind == "measured" else "fallback"
+        roof["traffic"] = None
     line = {
         "metric": METRIC, "value": R**3 / (ms_step / 1e3), "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
@@ -498,8 +536,8 @@ def run_gpu_slabs(args, rank, world, dist):
                    "l2": "flushed (512 MiB write) before every step, outside its CUDA-event pair"},
         "e2e": {"value": R**3 / (e2e_step / 1e3), "unit": "cells/s", "ms_per_step": e2e_step,
                 "api": "paper_2409_13418_b200.slab.contour_slab(field, GridSpec, rank, world) -> TriangleMesh on rank 0",
-                "h2d_bytes_per_step": None, "d2h_bytes_per_step": None},
-        "roofline": None, "cpu_baseline": None, "gpu_launches": None, "clocks": clock,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "roofline": roof, "cpu_baseline": None, "gpu_launches": launches, "clocks": clock,
     }
     print(json.dumps(line), flush=True)
 
@@ -515,22 +553,30 @@ def main():
     ap.add_argument("--cpu-sample-r", type=int, default=None)
     ap.add_argument("--full-evals", type=int, default=None)
     ap.add_argument("--batch-workers", type=int, default=8)
+    ap.add_argument("--slabs", action="store_true", help="use the z-slab path even on one rank (testing)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist = None
-    if world > 1:
+    if world > 1 or args.slabs:
         import torch.distributed as tdist
 
         backend = "nccl" if args.impl == "b200" else "gloo"
-        tdist.init_process_group(backend=backend)
+        if backend == "nccl":
+            import torch
+
+            local = int(os.environ.get("LOCAL_RANK", "0"))
+            torch.cuda.set_device(local)
+            tdist.init_process_group(backend=backend, device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend=backend)
         dist = tdist
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)
         elif args.workload.startswith("batch"):
             run_gpu_batch(args, rank, world, dist)
-        elif world > 1:
+        elif world > 1 or args.slabs:
             run_gpu_slabs(args, rank, world, dist)
         else:
             run_gpu(args, rank, world, dist)

@@ -129,7 +129,16 @@ def stats_vector(st):
     v += list(st.point2d_status_counts) + list(st.qef_rank_counts) + list(st.split_case_counts)
     v += list(st.eval_batches) + list(st.eval_evals)
     v.append(int(np.array([st.qef_max_residual]).view(np.int64)[0]))  # >= 0 doubles order like their bits
+    # extras for the benchmark: kernel launches, grid-label kernel time (ns)
+    v.append(int(st.n_kernel_launches))
+    v.append(int(round(float(st.stage_ms[7]) * 1e6)))
     return np.asarray(v, dtype=np.int64)
+
+
+def run_extras(rows):
+    """(kernel launches summed over ranks, slowest rank's grid-label kernel ms)."""
+    rows = np.asarray(rows)
+    return int(rows[:, -2].sum()), float(rows[:, -1].max()) / 1e6
 
 
 def stitch(piece, rank, world, dist, device):
@@ -232,7 +241,8 @@ def contour_slab(field, grid, options=None, *, rank, world, dist, device=0, to_h
     if rc != _lib.ODC_OK:
         _raise(rc, ctx)
     if not to_host:
-        return st
+        launches, k_ms = run_extras(rows)
+        return {"finish": st, "n_kernel_launches": launches + int(st.n_kernel_launches), "labels_kernel_ms": k_ms}
     mesh = _copy_mesh(ctx, 0, st) if st.n_triangles else TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), np.int64))
     raw = mesh if st.repair_added_vertices == 0 else _raw_from_repaired(ctx, mesh, st)
     stats = slab_stats(rows, options, st)
@@ -244,6 +254,9 @@ def contour_slab(field, grid, options=None, *, rank, world, dist, device=0, to_h
     stats["wall_time_s"] = time.perf_counter() - t0
     stats["eval_counts"] = counter.snapshot()
     stats["slabs"] = world
+    launches, k_ms = run_extras(rows)
+    stats["n_kernel_launches"] = launches + int(st.n_kernel_launches)
+    stats["labels_kernel_ms"] = k_ms
     return ContourResult(mesh, raw, counter, stats)
 
 
