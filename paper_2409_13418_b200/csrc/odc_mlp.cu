@@ -26,6 +26,7 @@ constexpr int kWidth = 256;
 constexpr int kDepth = 8;
 constexpr int kDin = 39;
 constexpr int kDinPad = 64;
+static_assert(kDin <= 48, "tc4 skips layer-0 K-step 3 (features 48..63 are padding)");
 constexpr int kPts = 32;  // points per block (SIMT evaluator)
 
 size_t mlp_packed_weight_elems() { return (size_t)kDinPad * kWidth + (size_t)(kDepth - 1) * kWidth * kWidth; }
@@ -1085,9 +1086,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
               }
               const uint32_t b_lo = w_lo + s * (tc4::kStageBytes >> 4);
               const uint32_t a_k = a_lo + (uint32_t)((t * tc4::kTileABytes + k * 16384) >> 4);
+              // layer 0: the encoding has 39 features, so K-step 3 (features
+              // 48..63, all zero) is skipped -- the sum is unchanged
+              const int nks = l == 0 ? 3 : 4;
               if (elect_one()) {
-#pragma unroll
-                for (int ks = 0; ks < 4; ks++)
+                for (int ks = 0; ks < nks; ks++)
                   tc4::umma_ss2(tmem + t * 256, make_desc(a_k + ks * 2), make_desc(b_lo + ks * 2), (k | ks) != 0);
                 if (t == 1) umma_commit_pair(&empty[s]);
               }
