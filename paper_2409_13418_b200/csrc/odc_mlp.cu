@@ -977,6 +977,9 @@ constexpr int kStageBytes = 16384;   // per CTA: 128 N rows x K 64 (one K-atom)
 constexpr int kTileABytes = 65536;   // 128 rows x 256 bf16
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (32u << 17) | (16u << 24);  // M256 N256
 constexpr size_t kSmemBytes = 1024 + 2 * kTileABytes + kStages * kStageBytes + 256 + 384 * 4;
+constexpr uint32_t kBarW = 2;              // named barriers 2..7: weight stage s ready
+constexpr uint32_t kBarA = kBarW + kStages;  // 8..9: A(t) ready
+static_assert(kBarA + 2 <= 16, "named barriers");
 __device__ __forceinline__ void umma_ss2(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -993,6 +996,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   using tc2::cluster_sync;
   using tc2::mapa;
   using tc2::mbar_arrive_cluster;
+  using tc2::named_bar_arrive;
   using tc2::named_bar_sync;
   using tc2::umma_commit_pair;
   extern __shared__ uint8_t smem_raw[];
@@ -1044,63 +1048,98 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
           const uint32_t s = g % tc4::kStages, ph = (g / tc4::kStages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           if (elect_one()) {
-            const int ci = l == 0 ? (int)crank : 2 + (l - 1) * 8 + (int)crank * 4 + kc;
-            mbar_expect_tx(&full[s], tc4::kStageBytes);
-            bulk_g2s(Wst + s * tc4::kStageBytes, m.w_tc + (size_t)ci * 128 * 64, tc4::kStageBytes, &full[s]);
+            if ((m.debug & 1) && g >= (uint32_t)tc4::kStages) {
+              mbar_arrive(&full[s]);  // experiment (odc_profile_mlp only): stale weights, no L2 traffic
+            } else {
+              const int ci = l == 0 ? (int)crank : 2 + (l - 1) * 8 + (int)crank * 4 + kc;
+              mbar_expect_tx(&full[s], tc4::kStageBytes);
+              bulk_g2s(Wst + s * tc4::kStageBytes, m.w_tc + (size_t)ci * 128 * 64, tc4::kStageBytes, &full[s]);
+            }
           }
           __syncwarp();
         }
   } else if (warp == 3) {
-    if (!leader) {  // ---- relay: the peer's half landed -> leader's fullp[s]
-      uint32_t g = 0;
-      for (int64_t pr = cid; pr < npairs; pr += ncl)
-        for (int l = 0; l < kDepth; l++)
-          for (int kc = 0; kc < (l == 0 ? 1 : 4); kc++, g++) {
-            const uint32_t s = g % tc4::kStages, ph = (g / tc4::kStages) & 1;
-            mbar_wait(&full[s], ph);
+    // peer: its half landed -> the leader's fullp[s].  leader: both halves
+    // landed -> named barrier kBarW + s for the MMA warp (a bar.sync is cheap
+    // for the issuer; an mbarrier poll costs it ~180 cycles of tensor-pipe
+    // bubble with shared memory saturated by operand reads)
+    uint32_t g = 0;
+    for (int64_t pr = cid; pr < npairs; pr += ncl)
+      for (int l = 0; l < kDepth; l++)
+        for (int kc = 0; kc < (l == 0 ? 1 : 4); kc++, g++) {
+          const uint32_t s = g % tc4::kStages, ph = (g / tc4::kStages) & 1;
+          mbar_wait(&full[s], ph);
+          if (leader) {
+            mbar_wait(&fullp[s], ph);
+            named_bar_arrive(tc4::kBarW + s, 64);
+          } else {
             if (elect_one()) mbar_arrive_cluster(mapa(smem_u32(&fullp[s]), 0));
             __syncwarp();
+          }
+        }
+  } else if (warp == 2) {
+    if (leader) {  // ---- relay: a_ready[t] -> named barrier kBarA + t for the MMA warp
+      uint32_t ra[2] = {0, 0};
+      for (int64_t pr = cid; pr < npairs; pr += ncl)
+        for (int l = 0; l < kDepth; l++)
+          for (int t = 0; t < 2; t++) {
+            mbar_wait(&a_ready[t], ra[t] & 1);
+            ra[t]++;
+            named_bar_arrive(tc4::kBarA + t, 64);
           }
     }
   } else if (warp == 1) {
     if (leader) {  // ---- MMA issuer (whole warp walks; one elected lane issues)
       const uint32_t a_lo = desc_lo(smem_u32(A0));
       const uint32_t w_lo = desc_lo(smem_u32(Wst));
-      uint32_t g0 = 0, ra[2] = {0, 0};
+      // one tile's layer: NST K-atoms of NKS K-steps each, fully unrolled so
+      // that each MMA is two immediate adds on the descriptor words (the
+      // issue rate is what keeps the tensor pipe fed between tiles)
+      auto tile = [&](auto tc, auto nstc, auto nksc, int ti, int l, uint32_t s0) {
+        constexpr int t = decltype(tc)::value, NST = decltype(nstc)::value, NKS = decltype(nksc)::value;
+        if (lane == 0) ODC_TRACE(ti, l, 2 * t);
+        named_bar_sync(tc4::kBarA + t, 64);  // a_ready[t] (relayed by warp 2)
+        tc_fence_after();
+        if (lane == 0) ODC_TRACE(ti, l, 2 * t + 1);
+        const uint32_t a_t = a_lo + (uint32_t)((t * tc4::kTileABytes) >> 4);
+        uint32_t s = s0;
+#pragma unroll
+        for (int k = 0; k < NST; k++) {
+          if (t == 0) {  // both weight halves of stage s landed (relayed by warp 3)
+            const long long w0 = m.trace ? clock64() : 0;
+            named_bar_sync(tc4::kBarW + s, 64);
+            if (m.trace && lane == 0 && blockIdx.x == 0 && ti < 2)
+              m.trace[256 + (ti * 8 + l) * 4 + k] = (unsigned long long)(clock64() - w0);
+          }
+          const uint32_t b_lo = w_lo + s * (tc4::kStageBytes >> 4);
+          if (elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < NKS; ks++)
+              tc4::umma_ss2(tmem + t * 256, make_desc(a_t + (uint32_t)((k * 16384) >> 4) + ks * 2),
+                            make_desc(b_lo + ks * 2), (k | ks) != 0);
+            if (t == 1) umma_commit_pair(&empty[s]);
+          }
+          __syncwarp();
+          s = s + 1 == (uint32_t)tc4::kStages ? 0 : s + 1;
+        }
+        if (elect_one()) umma_commit_pair(&acc_full[t]);
+        __syncwarp();
+        if (lane == 0) ODC_TRACE(ti, l, 4 + t);
+      };
+      using I0 = std::integral_constant<int, 0>;
+      using I1 = std::integral_constant<int, 1>;
+      uint32_t s0 = 0;
       int ti = 0;
       for (int64_t pr = cid; pr < npairs; pr += ncl, ti++) {
-        for (int l = 0; l < kDepth; l++) {
-          const int nst = l == 0 ? 1 : 4;
-#pragma unroll
-          for (int t = 0; t < 2; t++) {
-            if (lane == 0) ODC_TRACE(ti, l, 2 * t);
-            mbar_wait(&a_ready[t], ra[t] & 1);
-            ra[t]++;
-            tc_fence_after();
-            if (lane == 0) ODC_TRACE(ti, l, 2 * t + 1);
-            for (int k = 0; k < nst; k++) {
-              const uint32_t g = g0 + k, s = g % tc4::kStages, ph = (g / tc4::kStages) & 1;
-              if (t == 0) {
-                mbar_wait(&full[s], ph);
-                mbar_wait(&fullp[s], ph);
-              }
-              const uint32_t b_lo = w_lo + s * (tc4::kStageBytes >> 4);
-              const uint32_t a_k = a_lo + (uint32_t)((t * tc4::kTileABytes + k * 16384) >> 4);
-              // layer 0: the encoding has 39 features, so K-step 3 (features
-              // 48..63, all zero) is skipped -- the sum is unchanged
-              const int nks = l == 0 ? 3 : 4;
-              if (elect_one()) {
-                for (int ks = 0; ks < nks; ks++)
-                  tc4::umma_ss2(tmem + t * 256, make_desc(a_k + ks * 2), make_desc(b_lo + ks * 2), (k | ks) != 0);
-                if (t == 1) umma_commit_pair(&empty[s]);
-              }
-              __syncwarp();
-            }
-            if (elect_one()) umma_commit_pair(&acc_full[t]);
-            __syncwarp();
-            if (lane == 0) ODC_TRACE(ti, l, 4 + t);
-          }
-          g0 += nst;
+        // layer 0: one K-atom; the encoding has 39 features, so K-step 3
+        // (features 48..63, all zero) is skipped -- the sum is unchanged
+        tile(I0{}, I1{}, std::integral_constant<int, 3>{}, ti, 0, s0);
+        tile(I1{}, I1{}, std::integral_constant<int, 3>{}, ti, 0, s0);
+        s0 = s0 + 1 == (uint32_t)tc4::kStages ? 0 : s0 + 1;
+        for (int l = 1; l < kDepth; l++) {
+          tile(I0{}, std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}, ti, l, s0);
+          tile(I1{}, std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}, ti, l, s0);
+          s0 = (s0 + 4) % tc4::kStages;
         }
       }
     }

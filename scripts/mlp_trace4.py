@@ -12,6 +12,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
 ctx = _lib.Context(0)
 L = _lib.load()
 L.odc_set_param(ctx.handle, b"mlp_impl", 3)
+L.odc_set_param(ctx.handle, b"mlp_debug", int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 tr = np.zeros(256 * 4, dtype=np.int64)
 with DeviceField(ctx, MlpField()) as f:
     for _ in range(2):
@@ -25,7 +26,8 @@ for ti in range(2):
     for l in range(8):
         row = [(t[ti, l, e] - base) if t[ti, l, e] else float("nan") for e in range(12)]
         print(f"{ti:4d} {l:5d} " + " ".join(f"{x:8.0f}" for x in row))
-print("point_of alone:", [t[i, 0, 13] - t[i, 0, 12] for i in range(2)])
+ww = tr[256:320].reshape(2, 8, 4)
+print("weight waits [pair][layer][k]:", ww.tolist())
 print("piece ends:", [[t[i, l, 14] - (t[i, l, 11]) for l in range(1, 7)] for i in range(2)])
 per = [t[0, l + 1, 0] - t[0, l, 0] for l in range(1, 6)]
 print(f"mean layer period {np.mean(per):.0f} cycles; pair {t[1, 0, 0] - t[0, 0, 0]:.0f}; kernel {tr[-1] / 1e6:.3f} ms")
