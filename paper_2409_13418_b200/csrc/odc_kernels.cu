@@ -581,11 +581,11 @@ __device__ __forceinline__ bool decode_instance(const GridP& g, const uint32_t* 
 }
 
 __device__ __forceinline__ void lift(const Inst2D& I, double u, double v, double p[3]) {
-  p[0] = I.org[0];
-  p[1] = I.org[1];
-  p[2] = I.org[2];
-  p[I.bu] = I.org[I.bu] + u;
-  p[I.bv] = I.org[I.bv] + v;
+  // the addend is selected, not the slot (p[I.bu] = ... is a dynamic index
+  // and puts p in local memory).  org + 0.0 == org: grid positions are
+  // lo + c*h rounded to nearest, never -0.0.
+#pragma unroll
+  for (int a = 0; a < 3; a++) p[a] = I.org[a] + (a == I.bu ? u : a == I.bv ? v : 0.0);
 }
 
 // Geometry derived from the chord, before any evaluation (search.py:213-219)
@@ -612,6 +612,7 @@ __device__ __forceinline__ bool ray_direction(const Inst2D& I, const Chord& ch, 
   const double perp0 = -ch.dl[1], perp1 = ch.dl[0];
   const double cu[4] = {0.0, I.hu, I.hu, 0.0}, cv[4] = {0.0, 0.0, I.hv, I.hv};
   double plus_d = INFINITY, minus_d = INFINITY;
+#pragma unroll
   for (int c = 0; c < 4; c++) {
     const double r0 = cu[c] - ch.mid[0], r1 = cv[c] - ch.mid[1];
     const double side = r0 * perp0 + r1 * perp1;
@@ -776,10 +777,96 @@ struct Search2DState {
   double q2[2];
   double a2[2], b2[2];    // step-2 brackets (ray -dl, ray +dl)
   int32_t first1, first2[2];
-  uint8_t mid_label, found1, found2[2], degen, pad[3];
+  uint8_t mid_label, found1, found2[2], degen;
 };
 
-size_t search2d_state_bytes(int64_t Q) { return (size_t)Q * sizeof(Search2DState); }
+// In HBM the state is structure-of-arrays (14 double fields, then 4 int32
+// fields, each Q long) so that every field access of a warp is one coalesced
+// 256-/128-byte line; the step kernels load and store only the fields their
+// phase touches.
+namespace {
+enum { F_MID = 0, F_DL = 2, F_RAY = 4, F_A1 = 6, F_B1 = 7, F_Q2 = 8, F_A2 = 10, F_B2 = 12, F_N = 14 };
+enum { I_FIRST1 = 0, I_FIRST2 = 1, I_FLAGS = 3, I_N = 4 };
+// store masks
+enum : unsigned { W_GEOM = 1, W_RAY = 2, W_S1 = 4, W_Q2 = 8, W_S2 = 16, W_INT = 32, W_ALL = 63 };
+struct S2View {
+  double* d;
+  int32_t* i;
+  int64_t Q;
+};
+__host__ __device__ __forceinline__ S2View s2_view(void* base, int64_t Q) {
+  return {(double*)base, (int32_t*)((double*)base + F_N * Q), Q};
+}
+__device__ __forceinline__ Search2DState s2_load(const S2View& v, int64_t q) {
+  Search2DState s;
+  const double* __restrict__ d = v.d;
+  const int32_t* __restrict__ iw = v.i;
+  const int64_t Q = v.Q;
+  s.mid[0] = d[(F_MID + 0) * Q + q];
+  s.mid[1] = d[(F_MID + 1) * Q + q];
+  s.dl[0] = d[(F_DL + 0) * Q + q];
+  s.dl[1] = d[(F_DL + 1) * Q + q];
+  s.ray[0] = d[(F_RAY + 0) * Q + q];
+  s.ray[1] = d[(F_RAY + 1) * Q + q];
+  s.a1 = d[F_A1 * Q + q];
+  s.b1 = d[F_B1 * Q + q];
+  s.q2[0] = d[(F_Q2 + 0) * Q + q];
+  s.q2[1] = d[(F_Q2 + 1) * Q + q];
+  s.a2[0] = d[(F_A2 + 0) * Q + q];
+  s.a2[1] = d[(F_A2 + 1) * Q + q];
+  s.b2[0] = d[(F_B2 + 0) * Q + q];
+  s.b2[1] = d[(F_B2 + 1) * Q + q];
+  s.first1 = iw[I_FIRST1 * Q + q];
+  s.first2[0] = iw[(I_FIRST2 + 0) * Q + q];
+  s.first2[1] = iw[(I_FIRST2 + 1) * Q + q];
+  const uint32_t f = (uint32_t)iw[I_FLAGS * Q + q];
+  s.mid_label = (uint8_t)(f & 255u);
+  s.found1 = (uint8_t)((f >> 8) & 1u);
+  s.found2[0] = (uint8_t)((f >> 9) & 1u);
+  s.found2[1] = (uint8_t)((f >> 10) & 1u);
+  s.degen = (uint8_t)((f >> 16) & 255u);
+  return s;
+}
+__device__ __forceinline__ void s2_store(const S2View& v, int64_t q, const Search2DState& s, unsigned w) {
+  double* __restrict__ d = v.d;
+  int32_t* __restrict__ iw = v.i;
+  const int64_t Q = v.Q;
+  if (w & W_GEOM) {
+    d[(F_MID + 0) * Q + q] = s.mid[0];
+    d[(F_MID + 1) * Q + q] = s.mid[1];
+    d[(F_DL + 0) * Q + q] = s.dl[0];
+    d[(F_DL + 1) * Q + q] = s.dl[1];
+  }
+  if (w & W_RAY) {
+    d[(F_RAY + 0) * Q + q] = s.ray[0];
+    d[(F_RAY + 1) * Q + q] = s.ray[1];
+  }
+  if (w & W_S1) {
+    d[F_A1 * Q + q] = s.a1;
+    d[F_B1 * Q + q] = s.b1;
+  }
+  if (w & W_Q2) {
+    d[(F_Q2 + 0) * Q + q] = s.q2[0];
+    d[(F_Q2 + 1) * Q + q] = s.q2[1];
+  }
+  if (w & W_S2) {
+    d[(F_A2 + 0) * Q + q] = s.a2[0];
+    d[(F_A2 + 1) * Q + q] = s.a2[1];
+    d[(F_B2 + 0) * Q + q] = s.b2[0];
+    d[(F_B2 + 1) * Q + q] = s.b2[1];
+  }
+  if (w & W_INT) {
+    iw[I_FIRST1 * Q + q] = s.first1;
+    iw[(I_FIRST2 + 0) * Q + q] = s.first2[0];
+    iw[(I_FIRST2 + 1) * Q + q] = s.first2[1];
+    iw[I_FLAGS * Q + q] = (int32_t)((uint32_t)s.mid_label | ((uint32_t)s.found1 << 8) |
+                                    ((uint32_t)s.found2[0] << 9) | ((uint32_t)s.found2[1] << 10) |
+                                    ((uint32_t)s.degen << 16));
+  }
+}
+}  // namespace
+
+size_t search2d_state_bytes(int64_t Q) { return (size_t)Q * (F_N * sizeof(double) + I_N * sizeof(int32_t)); }
 int search2d_num_steps(const OptP& o) { return 1 + o.s1_lin + o.s1_bin + o.s2_lin + o.s2_bin; }
 
 // instance pairs only (face_pairings, dualize.py:72-88) -- the fd-gradient
@@ -802,7 +889,7 @@ void launch_instance_edges(const GridP& g, const uint32_t* L, const WordRec* rec
 
 __global__ void k_s2_init(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
                           const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
-                          Search2DState* __restrict__ S, int64_t* __restrict__ inst_edges) {
+                          S2View S, int64_t* __restrict__ inst_edges) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= Q) return;
   Inst2D I;
@@ -819,16 +906,16 @@ __global__ void k_s2_init(GridP g, const uint32_t* __restrict__ L, const WordRec
   s.dl[0] = ch.dl[0];
   s.dl[1] = ch.dl[1];
   s.degen = ch.degen;
-  S[q] = s;
+  s2_store(S, q, s, W_ALL);
 }
 
 // Per-instance geometry needed to lift points: recomputed from the key.
 __device__ __forceinline__ void inst_frame(const GridP& g, int64_t ikey, Inst2D& I) {
   const int64_t fk = ikey >> 1;
   const int64_t vid = fk / 3;
-  const int n = (int)(fk % 3);
-  I.bu = (n + 1) % 3;
-  I.bv = (n + 2) % 3;
+  const int n = (int)(fk - 3 * vid);
+  I.bu = n == 2 ? 0 : n + 1;
+  I.bv = n == 0 ? 2 : n - 1;
   vposition(g, vid, I.org);
 }
 
@@ -853,20 +940,20 @@ __device__ __forceinline__ void s2_point_uv(const OptP& o, const Inst2D& I, cons
     const int k = step - n1;
     double d;
     if (k <= o.s2_lin) d = mr * ((double)k / (double)o.s2_lin);
-    else d = 0.5 * (s.a2[r] + s.b2[r]);
+    else d = 0.5 * (r == 0 ? s.a2[0] + s.b2[0] : s.a2[1] + s.b2[1]);
     u = s.q2[0] + d * dir0;
     v = s.q2[1] + d * dir1;
   }
 }
 __device__ __forceinline__ void s2_frame(const GridP& g, int64_t ikey, Inst2D& I) {
   inst_frame(g, ikey, I);
-  I.hu = g.h[I.bu];
-  I.hv = g.h[I.bv];
+  I.hu = I.bu == 0 ? g.h[0] : I.bu == 1 ? g.h[1] : g.h[2];
+  I.hv = I.bv == 0 ? g.h[0] : I.bv == 1 ? g.h[1] : g.h[2];
   I.hmin = I.hu < I.hv ? I.hu : I.hv;
 }
 
-__global__ void k_s2_points(GridP g, OptP o, const int64_t* __restrict__ inst_key, int64_t Q, int step,
-                            const Search2DState* __restrict__ S, double* __restrict__ pts) {
+__global__ void k_s2_points(GridP g, OptP o, const int64_t* __restrict__ inst_key, int64_t Q, int step, S2View S,
+                            double* __restrict__ pts) {
   int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int n1 = o.s1_lin + o.s1_bin;
   const bool two = step > n1;
@@ -876,20 +963,23 @@ __global__ void k_s2_points(GridP g, OptP o, const int64_t* __restrict__ inst_ke
   Inst2D I;
   s2_frame(g, inst_key[q], I);
   double u, v, p[3];
-  s2_point_uv(o, I, S[q], step, m < Q ? 0 : 1, u, v);
+  s2_point_uv(o, I, s2_load(S, q), step, m < Q ? 0 : 1, u, v);
   lift(I, u, v, p);
   pts[3 * m] = p[0];
   pts[3 * m + 1] = p[1];
   pts[3 * m + 2] = p[2];
 }
 
-// fold the labels of lock-step ``step`` into the search state (search.py:220-276)
-__device__ __forceinline__ void s2_apply(const GridP& g, const OptP& o, const uint32_t* __restrict__ L,
-                                         const int64_t* __restrict__ inst_key, int64_t Q, int64_t q, int step,
-                                         const uint8_t* __restrict__ lab, Inst2D& I, Search2DState& s,
-                                         DevStatus* dst) {
+// fold the labels of lock-step ``step`` into the search state (search.py:220-276);
+// returns the store mask of the fields it changed.  PH: the phase of
+// ``step`` when known at compile time (0, 1, 2), -1 to branch at run time.
+template <int PH>
+__device__ __forceinline__ unsigned s2_apply(const GridP& g, const OptP& o, const uint32_t* __restrict__ L,
+                                             const int64_t* __restrict__ inst_key, int64_t Q, int64_t q, int step,
+                                             const uint8_t* __restrict__ lab, Inst2D& I, Search2DState& s,
+                                             DevStatus* dst) {
   const int n1 = o.s1_lin + o.s1_bin;
-  if (step == 0) {
+  if (PH == 0 || (PH < 0 && step == 0)) {
     s.mid_label = lab[q];
     // corner labels for the ray side
     const int64_t fk = inst_key[q] >> 1;
@@ -908,7 +998,9 @@ __device__ __forceinline__ void s2_apply(const GridP& g, const OptP& o, const ui
     if (!ray_direction(I, ch, s.mid_label, s.ray)) raise_status(dst, ODC_E_ASSERT, q);
     s.first1 = o.s1_lin;
     s.found1 = 0;
-  } else if (step <= n1) {
+    return W_RAY | W_INT;
+  } else if (PH == 1 || (PH < 0 && step <= n1)) {
+    unsigned w = W_INT;
     const double mr = o.s1_range * I.hmin;
     if (step <= o.s1_lin) {
       if (lab[q] != s.mid_label && !s.found1) {
@@ -918,20 +1010,25 @@ __device__ __forceinline__ void s2_apply(const GridP& g, const OptP& o, const ui
       if (step == o.s1_lin) {
         s.a1 = mr * ((double)(s.first1 - 1) / (double)o.s1_lin);
         s.b1 = mr * ((double)s.first1 / (double)o.s1_lin);
+        w |= W_S1;
       }
     } else {
       const double mm = 0.5 * (s.a1 + s.b1);
       if (lab[q] == s.mid_label) s.a1 = mm; else s.b1 = mm;
+      w |= W_S1;
     }
     if (step == n1) {
       s.q2[0] = s.mid[0] + s.a1 * s.ray[0];
       s.q2[1] = s.mid[1] + s.a1 * s.ray[1];
       s.first2[0] = s.first2[1] = o.s2_lin;
       s.found2[0] = s.found2[1] = 0;
+      w |= W_Q2;
     }
+    return w;
   } else {
     const double mr = o.s2_range * I.hmin;
     const int k = step - n1;
+#pragma unroll
     for (int r = 0; r < 2; r++) {
       const uint8_t l = lab[q + r * Q];
       if (k <= o.s2_lin) {
@@ -948,57 +1045,68 @@ __device__ __forceinline__ void s2_apply(const GridP& g, const OptP& o, const ui
         if (l == s.mid_label) s.a2[r] = mm; else s.b2[r] = mm;
       }
     }
+    return (k >= o.s2_lin ? W_S2 : 0u) | (k <= o.s2_lin ? W_INT : 0u);
   }
 }
 
 __global__ void k_s2_update(GridP g, OptP o, const uint32_t* __restrict__ L, const int64_t* __restrict__ inst_key,
-                            int64_t Q, int step, const uint8_t* __restrict__ lab, Search2DState* __restrict__ S,
-                            DevStatus* dst) {
+                            int64_t Q, int step, const uint8_t* __restrict__ lab, S2View S, DevStatus* dst) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= Q) return;
-  Search2DState s = S[q];
+  Search2DState s = s2_load(S, q);
   Inst2D I;
   s2_frame(g, inst_key[q], I);
-  s2_apply(g, o, L, inst_key, Q, q, step, lab, I, s, dst);
-  S[q] = s;
+  s2_store(S, q, s, s2_apply<-1>(g, o, L, inst_key, Q, q, step, lab, I, s, dst));
 }
 
 // update with the labels of ``step`` and emit the query points of step + 1
 // (one thread per instance, both rays in step 2): one pass over the state
-// per lock-step instead of two
-__global__ void k_s2_step(GridP g, OptP o, const uint32_t* __restrict__ L, const int64_t* __restrict__ inst_key,
-                          int64_t Q, int step, const uint8_t* __restrict__ lab, Search2DState* __restrict__ S,
-                          DevStatus* dst, double* __restrict__ pts) {
+// per lock-step instead of two.  PH = phase of ``step`` (0 midpoint probe,
+// 1 step-1 ray, 2 step-2 rays), so the loads of fields the phase never reads
+// compile away.
+template <int PH>
+__global__ void __launch_bounds__(256) k_s2_step(GridP g, OptP o, const uint32_t* __restrict__ L,
+                                                 const int64_t* __restrict__ inst_key, int64_t Q, int step,
+                                                 const uint8_t* __restrict__ lab, S2View S, DevStatus* dst,
+                                                 double* __restrict__ pts) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= Q) return;
-  Search2DState s = S[q];
+  Search2DState s = s2_load(S, q);
+  if (PH == 0) {  // fields not yet written (init leaves them zero); keep them out of the load
+    s.ray[0] = s.ray[1] = s.a1 = s.b1 = s.q2[0] = s.q2[1] = 0.0;
+    s.a2[0] = s.a2[1] = s.b2[0] = s.b2[1] = 0.0;
+  } else if (PH == 2) {  // step-1 state is final
+    s.ray[0] = s.ray[1] = s.a1 = s.b1 = 0.0;
+    s.mid[0] = s.mid[1] = 0.0;
+  }
   Inst2D I;
   s2_frame(g, inst_key[q], I);
-  s2_apply(g, o, L, inst_key, Q, q, step, lab, I, s, dst);
-  S[q] = s;
+  s2_store(S, q, s, s2_apply<PH>(g, o, L, inst_key, Q, q, step, lab, I, s, dst));
   const int next = step + 1;
   const int nr = next > o.s1_lin + o.s1_bin ? 2 : 1;
-  for (int r = 0; r < nr; r++) {
-    double u, v, p[3];
-    s2_point_uv(o, I, s, next, r, u, v);
-    lift(I, u, v, p);
-    const int64_t m = q + r * Q;
-    pts[3 * m] = p[0];
-    pts[3 * m + 1] = p[1];
-    pts[3 * m + 2] = p[2];
+#pragma unroll
+  for (int r = 0; r < 2; r++) {
+    if (r < nr) {
+      double u, v, p[3];
+      s2_point_uv(o, I, s, next, r, u, v);
+      lift(I, u, v, p);
+      const int64_t m = q + r * Q;
+      pts[3 * m] = p[0];
+      pts[3 * m + 1] = p[1];
+      pts[3 * m + 2] = p[2];
+    }
   }
 }
 
 __global__ void k_s2_finish(GridP g, OptP o, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
                             const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
-                            const Search2DState* __restrict__ S, Stage2D out, DevStats* st, int64_t st_lo,
-                            int64_t st_hi) {
+                            S2View S, Stage2D out, DevStats* st, int64_t st_lo, int64_t st_hi) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= Q) return;
   Inst2D I;
   int64_t pair[2];
   decode_instance(g, L, rec, inst_key[q], pos1d, I, pair);
-  const Search2DState s = S[q];
+  const Search2DState s = s2_load(S, q);
   Chord ch;
   ch.mid[0] = s.mid[0];
   ch.mid[1] = s.mid[1];
@@ -1028,34 +1136,37 @@ void launch_search2d_lockstep_init(const GridP& g, const OptP& o, const uint32_t
                                    const int64_t* inst_key, int64_t Q, const double* pos1d, void* state,
                                    int64_t* inst_edges, cudaStream_t s) {
   (void)o;
-  if (Q)
-    k_s2_init<<<grid_for(Q, 128), 128, 0, s>>>(g, L, rec, inst_key, Q, pos1d, (Search2DState*)state, inst_edges);
+  if (Q) k_s2_init<<<grid_for(Q, 128), 128, 0, s>>>(g, L, rec, inst_key, Q, pos1d, s2_view(state, Q), inst_edges);
 }
 int64_t launch_search2d_lockstep_points(const GridP& g, const OptP& o, const int64_t* inst_key, int64_t Q, int step,
                                         const void* state, double* pts, cudaStream_t s) {
   const int n1 = o.s1_lin + o.s1_bin;
   int64_t M = step > n1 ? 2 * Q : Q;
-  if (M) k_s2_points<<<grid_for(M, 128), 128, 0, s>>>(g, o, inst_key, Q, step, (const Search2DState*)state, pts);
+  if (M) k_s2_points<<<grid_for(M, 128), 128, 0, s>>>(g, o, inst_key, Q, step, s2_view((void*)state, Q), pts);
   return M;
 }
 void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
                                      int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
                                      cudaStream_t s) {
-  if (Q)
-    k_s2_update<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, inst_key, Q, step, lab, (Search2DState*)state, dst);
+  if (Q) k_s2_update<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, inst_key, Q, step, lab, s2_view(state, Q), dst);
 }
 int64_t launch_search2d_lockstep_step(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
                                       int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
                                       double* pts, cudaStream_t s) {
-  if (Q)
-    k_s2_step<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, inst_key, Q, step, lab, (Search2DState*)state, dst, pts);
+  if (Q) {
+    const int ph = step == 0 ? 0 : step <= o.s1_lin + o.s1_bin ? 1 : 2;
+    const S2View v = s2_view(state, Q);
+    if (ph == 0) k_s2_step<0><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts);
+    else if (ph == 1) k_s2_step<1><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts);
+    else k_s2_step<2><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts);
+  }
   return step + 1 > o.s1_lin + o.s1_bin ? 2 * Q : Q;
 }
 void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
                                      const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,
                                      Stage2D out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s) {
   if (Q)
-    k_s2_finish<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, rec, inst_key, Q, pos1d, (const Search2DState*)state, out,
+    k_s2_finish<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, rec, inst_key, Q, pos1d, s2_view((void*)state, Q), out,
                                                  st, st_lo, st_hi);
 }
 
