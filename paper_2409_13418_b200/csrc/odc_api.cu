@@ -119,6 +119,8 @@ struct odc_ctx {
   CellTabEntry* table = nullptr;
   unsigned long long* h_pinned = nullptr;  // small readback buffer
   unsigned int* d_fail = nullptr;          // device flag: a winding query stayed on the surface
+  unsigned long long* d_sched = nullptr;   // MLP evaluator's pair counter (only grows)
+  unsigned long long sched_next = 0;       // its value when the next launch starts
   char* h_stage = nullptr;  // grow-only pinned staging for mesh copy-back
   // mesh validation (its own workspace: the last extraction stays valid)
   Arena varena;
@@ -204,6 +206,16 @@ void check_status(odc_ctx* c, DevStatus* dst) {
   if (s.code) throw OdcError{s.code, "device status " + std::to_string(s.code)};
 }
 
+// One MLP evaluator launch on this context's stream and pair counter.
+void run_mlp(odc_ctx* c, const odc_field* f, const PointSrc& src, int64_t n, uint8_t* lab, double* raw,
+             cudaStream_t s, const MlpDev* override_md = nullptr) {
+  MlpDev md = override_md ? *override_md : f->mlp;
+  if (!override_md) md.impl = c->mlp_impl;
+  md.sched = c->d_sched;
+  if (mlp_eval(md, src, n, lab, raw, s, &c->sched_next) != 0)
+    throw OdcError{ODC_E_CUDA, "MLP evaluator: no pair counter on this context"};
+}
+
 // Evaluate labels (and optionally raw) of n points through the field.
 // The CTA-pair TS (mlp_impl 0) and SIMT (1) evaluators read their own weight
 // layouts; those are packed and uploaded the first time a context selects
@@ -249,9 +261,7 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
   } else {
     ensure_mlp_format(c, f);
     PointSrc src{pts, GridP{}, 0};
-    MlpDev md = f->mlp;
-    md.impl = c->mlp_impl;
-    mlp_eval(md, src, n, lab, raw, c->stream);
+    run_mlp(c, f, src, n, lab, raw, c->stream);
   }
   check_launch(c);
 }
@@ -474,9 +484,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       voxel_eval(f->vox, src, g.nz * g.S2, bytes, nullptr, s);
     } else {
       ensure_mlp_format(c, f);
-      MlpDev md = f->mlp;
-      md.impl = c->mlp_impl;
-      mlp_eval(md, src, g.nz * g.S2, bytes, nullptr, s);
+      run_mlp(c, f, src, g.nz * g.S2, bytes, nullptr, s);
     }
     check_launch(c);
     mark(8);
@@ -912,7 +920,8 @@ int odc_create(int device, odc_ctx** out) {
   c->device = device;
   if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess || cudaEventCreate(&c->ev0) != cudaSuccess ||
       cudaEventCreate(&c->ev1) != cudaSuccess || cudaMallocHost(&c->h_pinned, 4096) != cudaSuccess ||
-      cudaMalloc(&c->d_fail, 4) != cudaSuccess || cudaMemset(c->d_fail, 0, 4) != cudaSuccess) {
+      cudaMalloc(&c->d_fail, 4) != cudaSuccess || cudaMemset(c->d_fail, 0, 4) != cudaSuccess ||
+      cudaMalloc(&c->d_sched, 8) != cudaSuccess || cudaMemset(c->d_sched, 0, 8) != cudaSuccess) {
     delete c;
     return ODC_E_CUDA;
   }
@@ -951,6 +960,7 @@ void odc_destroy(odc_ctx* c) {
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->d_fail) cudaFree(c->d_fail);
+  if (c->d_sched) cudaFree(c->d_sched);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (auto& e : c->evs)
@@ -963,7 +973,7 @@ const char* odc_last_error(const odc_ctx* c) { return c ? c->err.c_str() : "null
 
 int odc_set_param(odc_ctx* c, const char* name, int64_t value) {
   if (!c || !name) return ODC_E_ARG;
-  if (std::strcmp(name, "mlp_debug") == 0 && value >= 0 && value <= 127) {
+  if (std::strcmp(name, "mlp_debug") == 0 && value >= 0 && value <= 255) {
     c->mlp_debug = (int)value;
     return ODC_OK;
   }
@@ -977,6 +987,9 @@ int odc_set_param(odc_ctx* c, const char* name, int64_t value) {
 
 int odc_set_stream(odc_ctx* c, void* stream) {
   if (!c) return ODC_E_ARG;
+  // the context's launches must stay ordered (the MLP pair counter is per
+  // context): drain the old stream before switching
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return ODC_E_CUDA;
   c->stream = stream ? (cudaStream_t)stream : c->own;
   return ODC_OK;
 }
@@ -1867,9 +1880,21 @@ int odc_profile_mlp(odc_ctx* c, const odc_field* f, int64_t n, int64_t* trace, i
   md.impl = c->mlp_impl;
   md.debug = c->mlp_debug & 63;
   md.trace = (c->mlp_debug & 64) ? nullptr : dt;  // 64: time the kernel without the trace hooks
+  const int64_t np = n < g.S3 ? n : g.S3;
   PointSrc src{nullptr, g, 0};
+  if (c->mlp_debug & 128) {  // 128: the same vertices as explicit points (the search batches' path)
+    double* pts = c->arena.get<double>(3 * np);
+    if (!pts) return ODC_E_NOMEM;
+    launch_grid_points(g, 0, np, pts, c->stream);
+    src.pts = pts;
+  }
   cudaEventRecord(c->ev0, c->stream);
-  mlp_eval(md, src, n < g.S3 ? n : g.S3, lab, nullptr, c->stream);
+  try {
+    run_mlp(c, f, src, np, lab, nullptr, c->stream, &md);
+  } catch (const OdcError& e) {
+    c->err = e.msg;
+    return e.code;
+  }
   cudaEventRecord(c->ev1, c->stream);
   if (cudaMemcpyAsync(trace, dt, 8 * trace_len, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
       cudaStreamSynchronize(c->stream) != cudaSuccess) {

@@ -543,13 +543,18 @@ __device__ __forceinline__ bool decode_instance(const GridP& g, const uint32_t* 
   const bool cr[4] = {I.cl[0] != I.cl[1], I.cl[1] != I.cl[2], I.cl[3] != I.cl[2], I.cl[0] != I.cl[3]};
   const int ncross = (int)cr[0] + (int)cr[1] + (int)cr[2] + (int)cr[3];
   int64_t a0, a1;
-  if (ncross == 2) {
-    int64_t sel[2];
-    int ns = 0;
-    for (int j = 0; j < 4; j++)
-      if (cr[j]) sel[ns++] = ek[j];
-    a0 = sel[0];
-    a1 = sel[1];
+  if (ncross == 2) {  // the two crossing edges in j order (no dynamic index: registers)
+    bool have = false;
+    a0 = a1 = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (cr[j] && !have) {
+        a0 = ek[j];
+        have = true;
+      } else if (cr[j]) {
+        a1 = ek[j];
+      }
+    }
   } else {
     int64_t cc[3];
     vid_coords(g, vid, cc);
@@ -568,15 +573,17 @@ __device__ __forceinline__ bool decode_instance(const GridP& g, const uint32_t* 
   vposition(g, vid, I.org);
   I.bu = b;
   I.bv = c;
-  I.hu = g.h[b];
-  I.hv = g.h[c];
+  I.hu = b == 0 ? g.h[0] : b == 1 ? g.h[1] : g.h[2];
+  I.hv = c == 0 ? g.h[0] : c == 1 ? g.h[1] : g.h[2];
   I.hmin = I.hu < I.hv ? I.hu : I.hv;
+  const double ob = b == 0 ? I.org[0] : b == 1 ? I.org[1] : I.org[2];
+  const double oc = c == 0 ? I.org[0] : c == 1 ? I.org[1] : I.org[2];
   const int64_t r0 = edge_rank(rec, g, a0 / 3, (int)(a0 % 3));
   const int64_t r1 = edge_rank(rec, g, a1 / 3, (int)(a1 % 3));
-  I.p1[0] = pos1d[3 * r0 + b] - I.org[b];
-  I.p1[1] = pos1d[3 * r0 + c] - I.org[c];
-  I.p2[0] = pos1d[3 * r1 + b] - I.org[b];
-  I.p2[1] = pos1d[3 * r1 + c] - I.org[c];
+  I.p1[0] = pos1d[3 * r0 + b] - ob;
+  I.p1[1] = pos1d[3 * r0 + c] - oc;
+  I.p2[0] = pos1d[3 * r1 + b] - ob;
+  I.p2[1] = pos1d[3 * r1 + c] - oc;
   return true;
 }
 
@@ -657,6 +664,7 @@ __device__ __forceinline__ void finish2d(const Inst2D& I, const Chord& ch, doubl
   const double lov[2] = {-0.5 * I.hu, -0.5 * I.hv}, hiv[2] = {1.5 * I.hu, 1.5 * I.hv};
   const double delta[2] = {pos[0] - ch.mid[0], pos[1] - ch.mid[1]};
   double smin = INFINITY;
+#pragma unroll
   for (int i = 0; i < 2; i++) {
     const double shi = delta[i] > 0 ? (hiv[i] - ch.mid[i]) / delta[i] : INFINITY;
     const double slo = delta[i] < 0 ? (lov[i] - ch.mid[i]) / delta[i] : INFINITY;

@@ -976,7 +976,9 @@ constexpr int kStages = 6;
 constexpr int kStageBytes = 16384;   // per CTA: 128 N rows x K 64 (one K-atom)
 constexpr int kTileABytes = 65536;   // 128 rows x 256 bf16
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (32u << 17) | (16u << 24);  // M256 N256
-constexpr size_t kSmemBytes = 1024 + 2 * kTileABytes + kStages * kStageBytes + 256 + 384 * 4;
+constexpr size_t kSmemBytes = 1024 + 2 * kTileABytes + kStages * kStageBytes + 48 * 8 + 384 * 4;
+constexpr int kSched = 4;  // pair-index ring depth (dynamic schedule)
+constexpr uint32_t kSchedReaders = 22;  // warps that read each slot: 12 in the leader, 10 in the peer
 constexpr uint32_t kBarW = 2;              // named barriers 2..7: weight stage s ready
 constexpr uint32_t kBarA = kBarW + kStages;  // 8..9: A(t) ready
 static_assert(kBarA + 2 <= 16, "named barriers");
@@ -1010,14 +1012,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   uint64_t* acc_full = fullp + tc4::kStages;   // [2] tile t's layer done (commit, both CTAs)
   uint64_t* a_ready = acc_full + 2;            // [2] leader: A(t) written and D(t) drained, 8 warps
   uint32_t* tmem_slot = (uint32_t*)(a_ready + 2);
-  float* s_head = (float*)(bars + 32);         // (256)
+  uint64_t* sched_full = bars + 24;            // [4] pair index of slot s written (scheduler, both CTAs)
+  uint64_t* sched_empty = bars + 28;           // [4] peer: all 22 reader warps took slot s
+  int64_t* sched_pr = (int64_t*)(bars + 32);   // [4] ring of pair indices (>= npairs: no more work)
+  float* s_head = (float*)(bars + 48);         // (256)
   float* s_part = s_head + kWidth;             // (128) head partials of columns 128..255
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
   const int64_t npairs = (n + 511) / 512;
-  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
+  if (m.trace && threadIdx.x == 0 && blockIdx.x < 300) m.trace[400 + 2 * blockIdx.x] = globaltimer_ns();
   if (threadIdx.x == 0) {
     for (int s = 0; s < tc4::kStages; s++) {
       mbar_init(&full[s], 1);
@@ -1027,6 +1032,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
     for (int t = 0; t < 2; t++) {
       mbar_init(&acc_full[t], 1);
       mbar_init(&a_ready[t], 16);  // 8 epilogue warps x 2 CTAs
+    }
+    for (int i = 0; i < tc4::kSched; i++) {
+      mbar_init(&sched_full[i], 1);
+      mbar_init(&sched_empty[i], tc4::kSchedReaders);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1040,9 +1049,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // Dynamic schedule: the peer's warp 2 takes pair indices from a global
+  // counter (m.sched, minus this launch's base) into a 4-slot ring in both
+  // CTAs; every role walks the ring, so clusters that run faster take more
+  // pairs and all clusters finish within about one pair of each other
+  // (static round-robin left a ~4 % spread of cluster end times).
+  // Whole-warp call; slot i's reader count is tc4::kSchedReaders.
+  auto sched_get = [&](uint32_t i) -> int64_t {
+    const uint32_t sl = i % tc4::kSched, ph = (i / tc4::kSched) & 1;
+    mbar_wait_cluster(&sched_full[sl], ph);
+    const int64_t pr = *(volatile int64_t*)&sched_pr[sl];
+    __syncwarp();
+    if (lane == 0) {
+      if (crank == 1) mbar_arrive(&sched_empty[sl]);
+      else mbar_arrive_cluster(mapa(smem_u32(&sched_empty[sl]), 1));
+    }
+    return pr;
+  };
+
   if (warp == 0) {  // ---- weight producer: this CTA's N half of every K-atom
     uint32_t g = 0;
-    for (int64_t pr = cid; pr < npairs; pr += ncl)
+    for (uint32_t i = 0; sched_get(i) < npairs; i++)
       for (int l = 0; l < kDepth; l++)
         for (int kc = 0; kc < (l == 0 ? 1 : 4); kc++, g++) {
           const uint32_t s = g % tc4::kStages, ph = (g / tc4::kStages) & 1;
@@ -1064,7 +1091,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
     // for the issuer; an mbarrier poll costs it ~180 cycles of tensor-pipe
     // bubble with shared memory saturated by operand reads)
     uint32_t g = 0;
-    for (int64_t pr = cid; pr < npairs; pr += ncl)
+    for (uint32_t i = 0; sched_get(i) < npairs; i++)
       for (int l = 0; l < kDepth; l++)
         for (int kc = 0; kc < (l == 0 ? 1 : 4); kc++, g++) {
           const uint32_t s = g % tc4::kStages, ph = (g / tc4::kStages) & 1;
@@ -1080,13 +1107,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   } else if (warp == 2) {
     if (leader) {  // ---- relay: a_ready[t] -> named barrier kBarA + t for the MMA warp
       uint32_t ra[2] = {0, 0};
-      for (int64_t pr = cid; pr < npairs; pr += ncl)
+      for (uint32_t i = 0; sched_get(i) < npairs; i++)
         for (int l = 0; l < kDepth; l++)
           for (int t = 0; t < 2; t++) {
             mbar_wait(&a_ready[t], ra[t] & 1);
             ra[t]++;
             named_bar_arrive(tc4::kBarA + t, 64);
           }
+    } else if (lane == 0) {  // ---- scheduler: pair indices into both CTAs' rings
+      const uint32_t peer_pr = mapa(smem_u32(sched_pr), 0);
+      const uint32_t peer_full = mapa(smem_u32(sched_full), 0);
+      for (uint32_t i = 0;; i++) {
+        const uint32_t sl = i % tc4::kSched, ph = (i / tc4::kSched) & 1;
+        mbar_wait(&sched_empty[sl], ph ^ 1);
+        int64_t pr = (int64_t)(atomicAdd(m.sched, 1ull) - m.sched_base);
+        if (m.debug & 8) {  // experiment (odc_profile_mlp only): static round-robin order
+          const int64_t st = (int64_t)(blockIdx.x >> 1) + (int64_t)i * (int64_t)(gridDim.x >> 1);
+          pr = st < npairs ? st : npairs;
+        }
+        *(volatile int64_t*)&sched_pr[sl] = pr;
+        asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(peer_pr + 8 * sl), "l"(pr) : "memory");
+        mbar_arrive(&sched_full[sl]);
+        mbar_arrive_cluster(peer_full + 8 * sl);  // release.cluster: orders the store above
+        if (pr >= npairs) break;
+      }
     }
   } else if (warp == 1) {
     if (leader) {  // ---- MMA issuer (whole warp walks; one elected lane issues)
@@ -1129,8 +1173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
       using I0 = std::integral_constant<int, 0>;
       using I1 = std::integral_constant<int, 1>;
       uint32_t s0 = 0;
-      int ti = 0;
-      for (int64_t pr = cid; pr < npairs; pr += ncl, ti++) {
+      for (int ti = 0; sched_get((uint32_t)ti) < npairs; ti++) {
         // layer 0: one K-atom; the encoding has 39 features, so K-step 3
         // (features 48..63, all zero) is skipped -- the sum is unchanged
         tile(I0{}, I1{}, std::integral_constant<int, 3>{}, ti, 0, s0);
@@ -1165,16 +1208,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
     int64_t p_prev = -1;
     float dot_prev[2] = {0.f, 0.f};
     const bool tr = r == 0 && crank == 0 && hc == 0;
-    if (cid < npairs) {
-      if (src.petab) pe_from_table(src, n, cid * 512 + hc * 256 + crank * 128 + r, pe);
-      else pe_row_packed(src, n, cid * 512 + hc * 256 + crank * 128 + r, pe);
+    int64_t pr = sched_get(0);
+    if (pr < npairs) {
+      if (src.petab) pe_from_table(src, n, pr * 512 + hc * 256 + crank * 128 + r, pe);
+      else pe_row_packed(src, n, pr * 512 + hc * 256 + crank * 128 + r, pe);
       store_pe_row(pe, a_pe, r);
       release(0);
       release(1);
     }
-    int ti = 0;
-    for (int64_t pr = cid; pr < npairs; pr += ncl, ti++) {
-      const int64_t next = pr + ncl;
+    for (int ti = 0; pr < npairs; ti++) {
+      const int64_t next = sched_get((uint32_t)ti + 1);  // its encoding goes in during this pair
       float dot[2] = {0.f, 0.f};
       for (int l = 0; l < kDepth; l++) {
         const float* bl = m.bias + l * kWidth + hc * 128;
@@ -1241,6 +1284,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
       p_prev = pr * 512 + crank * 128 + r;  // tile 0 row; tile 1 row = +256
       dot_prev[0] = dot[0];
       dot_prev[1] = dot[1];
+      pr = next;
     }
     if (hc == 0 && p_prev >= 0) {
       finish_label(m, src, n, p_prev, dot_prev[0], labels, raw);
@@ -1251,9 +1295,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   cluster_sync();
   tc_fence_after();
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (m.trace && threadIdx.x == 0 && blockIdx.x < 300) m.trace[401 + 2 * blockIdx.x] = globaltimer_ns();
 }
 
-int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s) {
+int mlp_eval(const MlpDev& m_in, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s,
+             unsigned long long* sched_next) {
+  MlpDev m = m_in;
   if (n <= 0) return 0;
   if (m.impl == 1 || m.w_tc == nullptr) {
     const int64_t blocks = (n + kPts - 1) / kPts;
@@ -1283,6 +1330,10 @@ int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, d
   if (m.impl == 3) {
     const int64_t np4 = (n + 511) / 512;
     const int64_t pairs = (g_num_sms / 2) < np4 ? (g_num_sms / 2) : np4;
+    if (!m.sched || !sched_next) return -1;  // the dynamic schedule needs the context's counter
+    // every cluster takes indices until one is >= np4: np4 + clusters fetches
+    m.sched_base = *sched_next;
+    *sched_next += (unsigned long long)(np4 + pairs);
     PointSrc sp = src;
     sp.petab = nullptr;
     sp.fd_m = sp.fd_s = 0;

@@ -25,6 +25,10 @@ struct MlpDev {
   int debug;                 // profiling only (odc_profile_mlp): 1 no weight refills, 2 no A stores, 4 no TMEM loads
   int has_bias;              // any non-zero bias (selects the bias-add epilogue)
   unsigned long long* trace; // profiling: event timeline of CTA 0 (nullptr = off)
+  // impl 3 dynamic pair schedule: a per-context device counter that only
+  // grows; mlp_eval() sets sched_base from *sched_next and advances it
+  unsigned long long* sched;
+  unsigned long long sched_base;
   const float* bias;         // (8, 256)
   const float* w_head;       // (256)
   float b_head;
@@ -52,7 +56,10 @@ void mlp_pack_weights_tc2(const float* w0, int d_in, const float* w_hidden, uint
 void mlp_pack_weights(const float* w0, int d_in, const float* w_hidden, uint16_t* out);
 
 // labels (u8) and optionally raw = sigmoid(logit) (f64) for n points
-int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s);
+// impl 3 needs m.sched and sched_next (the host copy of the counter's value
+// at the next launch, advanced here); returns nonzero when they are missing
+int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s,
+             unsigned long long* sched_next = nullptr);
 const char* mlp_kernel_name();
 
 }  // namespace odc
