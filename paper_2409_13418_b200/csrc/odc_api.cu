@@ -1853,10 +1853,12 @@ int odc_profile_mlp(odc_ctx* c, const odc_field* f, int64_t n, int64_t* trace, i
   cudaSetDevice(c->device);
   c->valid = false;
   c->arena.reset();
-  unsigned long long* dt = c->arena.get<unsigned long long>(trace_len);
+  // the kernels' trace slots reach index ~1,200: the device buffer is at
+  // least 2,048 entries whatever the caller reads back
+  unsigned long long* dt = c->arena.get<unsigned long long>(trace_len > 2048 ? trace_len : 2048);
   uint8_t* lab = c->arena.get<uint8_t>(n);
   if (!dt || !lab) return ODC_E_NOMEM;
-  cudaMemsetAsync(dt, 0, 8 * trace_len, c->stream);
+  cudaMemsetAsync(dt, 0, 8 * (trace_len > 2048 ? trace_len : 2048), c->stream);
   GridP g{};
   const int64_t S = 1 + (int64_t)std::ceil(std::cbrt((double)n));
   g.R = S - 1;

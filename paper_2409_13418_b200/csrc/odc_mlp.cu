@@ -978,7 +978,7 @@ constexpr int kTileABytes = 65536;   // 128 rows x 256 bf16
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (32u << 17) | (16u << 24);  // M256 N256
 constexpr size_t kSmemBytes = 1024 + 2 * kTileABytes + kStages * kStageBytes + 48 * 8 + 384 * 4;
 constexpr int kSched = 4;  // pair-index ring depth (dynamic schedule)
-constexpr uint32_t kSchedReaders = 22;  // warps that read each slot: 12 in the leader, 10 in the peer
+constexpr uint32_t kSchedReaders = 23;  // warps that read each slot: 12 in the leader, 11 in the peer
 constexpr uint32_t kBarW = 2;              // named barriers 2..7: weight stage s ready
 constexpr uint32_t kBarA = kBarW + kStages;  // 8..9: A(t) ready
 static_assert(kBarA + 2 <= 16, "named barriers");
@@ -998,6 +998,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   using tc2::cluster_sync;
   using tc2::mapa;
   using tc2::mbar_arrive_cluster;
+  using tc2::mbar_arrive_cluster_relaxed;
   using tc2::named_bar_arrive;
   using tc2::named_bar_sync;
   using tc2::umma_commit_pair;
@@ -1015,6 +1016,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   uint64_t* sched_full = bars + 24;            // [4] pair index of slot s written (scheduler, both CTAs)
   uint64_t* sched_empty = bars + 28;           // [4] peer: all 22 reader warps took slot s
   int64_t* sched_pr = (int64_t*)(bars + 32);   // [4] ring of pair indices (>= npairs: no more work)
+  uint64_t* a_loc = bars + 36;                 // [2] peer: its 8 epilogue warps released A(t)
   float* s_head = (float*)(bars + 48);         // (256)
   float* s_part = s_head + kWidth;             // (128) head partials of columns 128..255
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1031,7 +1033,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
     }
     for (int t = 0; t < 2; t++) {
       mbar_init(&acc_full[t], 1);
-      mbar_init(&a_ready[t], 16);  // 8 epilogue warps x 2 CTAs
+      mbar_init(&a_ready[t], 9);  // leader: its 8 epilogue warps + the peer's relay
+      mbar_init(&a_loc[t], 8);
     }
     for (int i = 0; i < tc4::kSched; i++) {
       mbar_init(&sched_full[i], 1);
@@ -1057,12 +1060,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   // Whole-warp call; slot i's reader count is tc4::kSchedReaders.
   auto sched_get = [&](uint32_t i) -> int64_t {
     const uint32_t sl = i % tc4::kSched, ph = (i / tc4::kSched) & 1;
-    mbar_wait_cluster(&sched_full[sl], ph);
+    mbar_wait(&sched_full[sl], ph);  // leader: the slot came by st.async (async proxy, complete_tx)
     const int64_t pr = *(volatile int64_t*)&sched_pr[sl];
     __syncwarp();
     if (lane == 0) {
-      if (crank == 1) mbar_arrive(&sched_empty[sl]);
-      else mbar_arrive_cluster(mapa(smem_u32(&sched_empty[sl]), 1));
+      if (crank == 1) {
+        mbar_arrive(&sched_empty[sl]);
+      } else {
+        // relaxed: a release.cluster arrive would first drain this thread's
+        // outstanding stores (~1,000 cycles); the slot's value is already in
+        // a register and the scheduler refills it only kSched pairs later
+        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                         mapa(smem_u32(&sched_empty[sl]), 1))
+                     : "memory");
+      }
     }
     return pr;
   };
@@ -1100,7 +1111,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
             mbar_wait(&fullp[s], ph);
             named_bar_arrive(tc4::kBarW + s, 64);
           } else {
-            if (elect_one()) mbar_arrive_cluster(mapa(smem_u32(&fullp[s]), 0));
+            if (elect_one()) mbar_arrive_cluster_relaxed(mapa(smem_u32(&fullp[s]), 0));
             __syncwarp();
           }
         }
@@ -1111,6 +1122,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
         for (int l = 0; l < kDepth; l++)
           for (int t = 0; t < 2; t++) {
             mbar_wait(&a_ready[t], ra[t] & 1);
+            if (m.trace && blockIdx.x == 0 && lane == 0 && ra[t] < 24) m.trace[750 + 24 * t + ra[t]] = globaltimer_ns();
             ra[t]++;
             named_bar_arrive(tc4::kBarA + t, 64);
           }
@@ -1126,14 +1138,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
           pr = st < npairs ? st : npairs;
         }
         *(volatile int64_t*)&sched_pr[sl] = pr;
-        asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(peer_pr + 8 * sl), "l"(pr) : "memory");
         mbar_arrive(&sched_full[sl]);
-        mbar_arrive_cluster(peer_full + 8 * sl);  // release.cluster: orders the store above
+        // the leader's copy: an async-proxy store that completes the leader's
+        // barrier transaction (like a bulk copy), so its readers need no
+        // cluster-scope acquire (that wait cost ~1,300 cycles per pair)
+        asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], 8;" ::"r"(
+                         peer_full + 8 * sl)
+                     : "memory");
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(peer_pr + 8 * sl),
+                     "l"(pr), "r"(peer_full + 8 * sl)
+                     : "memory");
         if (pr >= npairs) break;
       }
     }
+  } else if (warp == 1 && !leader) {
+    // ---- peer relay: its 8 epilogue warps released A(t) (CTA-scope arrives,
+    // after fence.proxy.async) -> one relaxed remote arrive on the leader's
+    // a_ready[t] (see mbar_arrive_cluster_relaxed: a release.cluster arrive
+    // costs ~600 ns of MEMBAR.GPU on this path)
+    const uint32_t leader_ready[2] = {mapa(smem_u32(&a_ready[0]), 0), mapa(smem_u32(&a_ready[1]), 0)};
+    uint32_t ra[2] = {0, 0};
+    auto forward = [&](int t) {
+      mbar_wait(&a_loc[t], ra[t] & 1);
+      if (m.trace && blockIdx.x == 1 && lane == 0 && ra[t] < 24) m.trace[700 + 24 * t + ra[t]] = globaltimer_ns();
+      ra[t]++;
+      if (elect_one()) mbar_arrive_cluster_relaxed(leader_ready[t]);
+      __syncwarp();
+    };
+    int64_t pr = sched_get(0);
+    if (pr < npairs) {
+      forward(0);
+      forward(1);
+    }
+    for (uint32_t i = 0; pr < npairs; i++) {
+      const int64_t next = sched_get(i + 1);
+      for (int l = 0; l < kDepth; l++) {
+        forward(0);
+        forward(1);
+      }
+      pr = next;
+    }
   } else if (warp == 1) {
-    if (leader) {  // ---- MMA issuer (whole warp walks; one elected lane issues)
+    {  // ---- MMA issuer (leader; whole warp walks, one elected lane issues)
       const uint32_t a_lo = desc_lo(smem_u32(A0));
       const uint32_t w_lo = desc_lo(smem_u32(Wst));
       // one tile's layer: NST K-atoms of NKS K-steps each, fully unrolled so
@@ -1193,12 +1239,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
     const int hc = (warp - 4) >> 2;
     const int r = 32 * q + lane;
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-    uint32_t leader_ready[2] = {mapa(smem_u32(&a_ready[0]), 0), mapa(smem_u32(&a_ready[1]), 0)};
+    int nrel = 0;
     auto release = [&](int t) {  // A(t) written / D(t) drained -> the leader's a_ready[t]
       fence_proxy_async();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(leader_ready[t]);
+      // CTA-scope releases only: the leader's MMA warp acquires a_ready[t]
+      // directly; the peer's a_loc[t] is forwarded at cluster scope by its
+      // warp 1 (release -> acquire -> release.cluster -> acquire.cluster)
+      if (lane == 0) mbar_arrive(leader ? &a_ready[t] : &a_loc[t]);
+      if (m.trace && blockIdx.x < 2 && lane == 0 && t == 0 && nrel < 24)
+        m.trace[800 + blockIdx.x * 200 + (warp - 4) * 24 + nrel] = globaltimer_ns();
+      if (t == 0) nrel++;
     };
     // this warp's encoding row: tile hc, row r (column half 0 stores tile 0, half 1 tile 1)
     const uint32_t a_pe = smem_u32(A0 + hc * tc4::kTileABytes);
@@ -1217,7 +1269,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
       release(1);
     }
     for (int ti = 0; pr < npairs; ti++) {
+      const long long sg0 = m.trace ? clock64() : 0;
       const int64_t next = sched_get((uint32_t)ti + 1);  // its encoding goes in during this pair
+      if (m.trace && tr && ti < 8) m.trace[320 + ti] = (unsigned long long)(clock64() - sg0);
       float dot[2] = {0.f, 0.f};
       for (int l = 0; l < kDepth; l++) {
         const float* bl = m.bias + l * kWidth + hc * 128;
@@ -1270,6 +1324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
               tmem_ld_wait();
               d = head32<kBias>(v, bl + 32 * gk, s_head + hc * 128 + 32 * gk, d);
             }
+            if (tr) ODC_TRACE(ti, l, 12 + t);
             // halves meet in shared memory (the 8 warps are on the same tile)
             if (hc == 1) s_part[r] = d;
             named_bar_sync(1, 256);
@@ -1278,6 +1333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
             // D(t) drained; the next pair's encoding of tile t goes in (half t's rows)
             if (next < npairs && hc == t) store_pe_row(pe, a_pe, r);
             release(t);
+            if (tr) ODC_TRACE(ti, l, 10 + t);
           }
         }
       }

@@ -58,6 +58,16 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Relaxed remote arrive.  A release.cluster arrive compiles to MEMBAR.ALL.GPU
+// + ERRBAR (~600 ns on the critical path).  Use only where the data the
+// arrive publishes is already complete in shared memory: bulk-copy data
+// observed through complete_tx, or generic stores that their writers fenced
+// (fence.proxy.async) and released at CTA scope before this thread acquired
+// them -- shared memory is not cached, so a performed store is what the
+// peer's tensor-core read sees.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"

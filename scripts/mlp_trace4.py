@@ -28,6 +28,9 @@ for ti in range(2):
         print(f"{ti:4d} {l:5d} " + " ".join(f"{x:8.0f}" for x in row))
 ww = tr[256:320].reshape(2, 8, 4)
 print("weight waits [pair][layer][k]:", ww.tolist())
+print("layer 7 head done (rel. e_ok):", [[t[i, 7, 12 + u] - t[i, 7, 8 + u] for u in range(2)] for i in range(2)],
+      "released:", [[t[i, 7, 10 + u] - t[i, 7, 8 + u] for u in range(2)] for i in range(2)])
+print("epilogue sched_get cycles per pair:", tr[320:328].tolist())
 print("piece ends:", [[t[i, l, 14] - (t[i, l, 11]) for l in range(1, 7)] for i in range(2)])
 per = [t[0, l + 1, 0] - t[0, l, 0] for l in range(1, 6)]
 print(f"mean layer period {np.mean(per):.0f} cycles; pair {t[1, 0, 0] - t[0, 0, 0]:.0f}; kernel {tr[-1] / 1e6:.3f} ms")
