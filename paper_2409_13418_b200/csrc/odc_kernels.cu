@@ -21,8 +21,30 @@ namespace odc {
 
 namespace {
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
-__device__ __forceinline__ void atomic_max_nonneg_double(unsigned long long* a, double v) {
-  atomicMax(a, (unsigned long long)__double_as_longlong(v));
+// Statistics counters: one atomic per warp (the sum over the active lanes)
+// instead of one per thread -- a million same-address atomics serialise in
+// L2 (k_s2_finish spent 0.7 ms on them).  Call with the warp converged.
+__device__ __forceinline__ void warp_count(unsigned long long* p, unsigned v) {
+  const unsigned m = __activemask();
+  const unsigned s = __reduce_add_sync(m, v);
+  if ((int)(threadIdx.x & 31) == __ffs(m) - 1 && s) atomicAdd(p, (unsigned long long)s);
+}
+// bins[b] += 1 for this lane's bin b (0..3) when on
+__device__ __forceinline__ void warp_count4(unsigned long long* bins, int b, bool on) {
+#pragma unroll
+  for (int v = 0; v < 4; v++) warp_count(&bins[v], on && b == v ? 1u : 0u);
+}
+// max over the active lanes of non-negative doubles (ordered as bits)
+__device__ __forceinline__ void warp_max_nonneg_double(unsigned long long* p, double v) {
+  const unsigned m = __activemask();
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const unsigned hi = (unsigned)(bits >> 32);
+  const unsigned top = __reduce_max_sync(m, hi);
+  const unsigned m2 = __ballot_sync(m, hi == top);
+  if (hi == top) {
+    const unsigned lo = __reduce_max_sync(m2, (unsigned)bits);
+    if ((int)(threadIdx.x & 31) == __ffs(m2) - 1 && (top | lo)) atomicMax(p, ((unsigned long long)top << 32) | lo);
+  }
 }
 }  // namespace
 
@@ -51,19 +73,26 @@ void launch_labels_analytic(const GridP& g, const FieldP& f, uint32_t* L, cudaSt
   k_labels_analytic<<<grid_for(n, 256), 256, 0, s>>>(g, f, L);
 }
 
-__global__ void k_pack_labels(GridP g, const uint8_t* __restrict__ bytes, uint32_t* __restrict__ L) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t rowbits = g.W * 32;
-  const int64_t row = idiv(gid, rowbits);  // window-local row; bytes are window-local flat
+// one warp per label row: lane j of word w reads byte 32 w + j (coalesced),
+// a ballot makes the word -- no per-element 64-bit division
+__global__ void __launch_bounds__(256) k_pack_labels(GridP g, const uint8_t* __restrict__ bytes,
+                                                     uint32_t* __restrict__ L) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= g.nz * g.S) return;
-  const int64_t x = gid - row * rowbits;
-  uint32_t lab = x < g.S ? (uint32_t)(bytes[row * g.S + x] != 0) : 0u;
-  const uint32_t w = __ballot_sync(0xffffffffu, lab);
-  if ((threadIdx.x & 31) == 0) L[row * g.W + (x >> 5)] = w;
+  const int lane = threadIdx.x & 31;
+  const uint8_t* src = bytes + row * g.S;
+  uint32_t* dst = L + row * g.W;
+  const int S = (int)g.S;
+  for (int w = 0; w < (int)g.W; w++) {
+    const int x = 32 * w + lane;
+    const uint32_t lab = x < S ? (uint32_t)(src[x] != 0) : 0u;
+    const uint32_t bits = __ballot_sync(0xffffffffu, lab);
+    if (lane == 0) dst[w] = bits;
+  }
 }
 void launch_pack_labels(const GridP& g, const uint8_t* bytes, uint32_t* L, cudaStream_t s) {
-  int64_t n = g.nz * g.S * g.W * 32;
-  k_pack_labels<<<grid_for(n, 256), 256, 0, s>>>(g, bytes, L);
+  const int64_t rows = g.nz * g.S;
+  if (rows) k_pack_labels<<<grid_for(rows, 8), 256, 0, s>>>(g, bytes, L);
 }
 
 __global__ void k_unpack_labels(GridP g, const uint32_t* __restrict__ L, uint8_t* __restrict__ bytes) {
@@ -763,7 +792,7 @@ __global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, Op
   }
   if (out.status) out.status[q] = status;
   if (out.mid) out.mid[q] = (uint8_t)mid_label;
-  if (q >= st_lo && q < st_hi) atomicAdd(&st->status[status], 1ull);
+  warp_count4(st->status, status, q >= st_lo && q < st_hi);
 }
 
 void launch_search2d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
@@ -1137,7 +1166,7 @@ __global__ void k_s2_finish(GridP g, OptP o, const uint32_t* __restrict__ L, con
   }
   if (out.status) out.status[q] = status;
   if (out.mid) out.mid[q] = s.mid_label;
-  if (q >= st_lo && q < st_hi) atomicAdd(&st->status[status], 1ull);
+  warp_count4(st->status, status, q >= st_lo && q < st_hi);
 }
 
 void launch_search2d_lockstep_init(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
@@ -1229,7 +1258,7 @@ __global__ void k_fd_normals(GridP g, double step, const uint32_t* __restrict__ 
   if (einsum3(n, e.span) < 0.0)
     for (int c = 0; c < 3; c++) n[c] = -n[c];
   for (int c = 0; c < 3; c++) nrm[3 * k + c] = n[c];
-  if (bad && k >= st_lo && k < st_hi) atomicAdd(&st->normal_fallbacks, 1ull);
+  warp_count(&st->normal_fallbacks, bad && k >= st_lo && k < st_hi ? 1u : 0u);
 }
 void launch_fd_normals(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* edge_key, int64_t K,
                        const double* raw, double* edge_normals, DevStats* st, int64_t st_lo, int64_t st_hi,
@@ -1363,6 +1392,8 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
   hmin = hmin < g.h[2] ? hmin : g.h[2];
   const int64_t cc[3] = {imod(cell, g.R), imod(idiv(cell, g.R), g.R), idiv(cell, g.R * g.R)};
   uint32_t nfb = 0;
+  uint32_t rank_cnt = 0;  // 8-bit count per QEF rank 0..3
+  double max_res = 0.0;
   int slot = 0;
   for (int k = 0; k < T.ncyc; k++) {
     const int len = (T.lens >> (4 * k)) & 15;
@@ -1473,12 +1504,16 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
     if (out.rank) out.rank[pid] = rank;
     if (out.resid) out.resid[pid] = res;
     if (ci >= st_lo && ci < st_hi) {
-      atomicAdd(&st->rank[rank], 1ull);
-      atomic_max_nonneg_double(&st->max_resid_bits, res);
+      rank_cnt += 1u << (8 * rank);  // (partitions per cell <= 4: bytes never carry)
+      max_res = !(res <= max_res) ? res : max_res;  // NaN wins, as it did under atomicMax of the bits
     }
     slot += len;
   }
-  if (nfb && ci >= st_lo && ci < st_hi) atomicAdd(&st->normal_fallbacks, (unsigned long long)nfb);
+  const bool own = ci >= st_lo && ci < st_hi;
+#pragma unroll
+  for (int v = 0; v < 4; v++) warp_count(&st->rank[v], own ? (rank_cnt >> (8 * v)) & 255u : 0u);
+  warp_max_nonneg_double(&st->max_resid_bits, own ? max_res : 0.0);
+  warp_count(&st->normal_fallbacks, own ? (unsigned)nfb : 0u);
 }
 
 void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec, const int64_t* cell_id,
@@ -1623,7 +1658,7 @@ __global__ void __launch_bounds__(128) k_poly_classify(GridP g, OptP o, const ui
   kase[k] = (uint8_t)cs;
   ntri[k] = cs == 3 ? 4u : 2u;
   nfan[k] = cs == 3 ? 1u : 0u;
-  atomicAdd(&st->split[cs], 1ull);
+  warp_count4(st->split, cs, true);
 }
 
 void launch_poly_classify(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
