@@ -1257,8 +1257,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
     uint32_t af[2] = {0, 0};
     uint32_t pe[32];
     PePiece pes;
+    // The previous pair's labels are finished in the slack of layers 2 (tile
+    // 0) and 3 (tile 1) of the next pair: the column halves' head partials
+    // meet in s_part there, away from the pair boundary where the epilogue is
+    // the critical path.  dot = partial(cols 0..127) + partial(cols 128..255).
     int64_t p_prev = -1;
-    float dot_prev[2] = {0.f, 0.f};
+    float part_prev[2] = {0.f, 0.f};
+    auto finish_tile = [&](int t) {
+      if (hc == 1) s_part[r] = part_prev[t];
+      named_bar_sync(1, 256);
+      if (hc == 0) finish_label(m, src, n, p_prev + 256 * t, part_prev[t] + s_part[r], labels, raw);
+      named_bar_sync(1, 256);  // s_part reusable
+    };
     const bool tr = r == 0 && crank == 0 && hc == 0;
     int64_t pr = sched_get(0);
     if (pr < npairs) {
@@ -1269,17 +1279,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
       release(1);
     }
     for (int ti = 0; pr < npairs; ti++) {
-      const long long sg0 = m.trace ? clock64() : 0;
-      const int64_t next = sched_get((uint32_t)ti + 1);  // its encoding goes in during this pair
-      if (m.trace && tr && ti < 8) m.trace[320 + ti] = (unsigned long long)(clock64() - sg0);
-      float dot[2] = {0.f, 0.f};
+      int64_t next = npairs;  // the following pair: taken from the ring in layer 1's slack
+      float part[2] = {0.f, 0.f};
       for (int l = 0; l < kDepth; l++) {
         const float* bl = m.bias + l * kWidth + hc * 128;
-        if (l == 1 && hc == 0) {  // the previous pair's labels, in this layer's slack
-          finish_label(m, src, n, p_prev, dot_prev[0], labels, raw);
-          if (p_prev >= 0) finish_label(m, src, n, p_prev + 256, dot_prev[1], labels, raw);
-          p_prev = -1;
-        }
 #pragma unroll
         for (int t = 0; t < 2; t++) {
           const uint32_t a_t = smem_u32(A0 + t * tc4::kTileABytes);
@@ -1305,46 +1308,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
             }
             release(t);
             if (tr) ODC_TRACE(ti, l, 10 + t);
-            // slack until the next layer: one piece of the next pair's encoding
-            if (t == 1 && next < npairs) {
-              const int64_t pn = next * 512 + hc * 256 + crank * 128 + r;
-              if (src.petab) {  // grid points: table lookups, in one layer's slack
-                if (l == kDepth - 2) pe_from_table(src, n, pn, pe);
-              } else if (l >= 1) {  // explicit points: one frequency per layer
-                pe_piece(src, n, pn, l - 1, pes, pe);
+            // slack until the next layer's tile 0
+            if (t == 1) {
+              if (l == 1) {
+                const long long sg0 = m.trace ? clock64() : 0;
+                next = sched_get((uint32_t)ti + 1);
+                if (m.trace && tr && ti < 8) m.trace[320 + ti] = (unsigned long long)(clock64() - sg0);
+              }
+              if (l == 2 && p_prev >= 0) finish_tile(0);
+              if (l == 3 && p_prev >= 0) finish_tile(1);
+              if (l >= 1 && next < npairs) {  // one piece of the next pair's encoding
+                const int64_t pn = next * 512 + hc * 256 + crank * 128 + r;
+                if (src.petab) {  // grid points: table lookups, in one layer's slack
+                  if (l == kDepth - 2) pe_from_table(src, n, pn, pe);
+                } else {  // explicit points: one frequency per layer
+                  pe_piece(src, n, pn, l - 1, pes, pe);
+                }
               }
               if (tr) ODC_TRACE(ti, l, 14);
             }
           } else {
+            // layer 7 consumed A(t): the next pair's encoding of tile t goes in
+            // first (half t's rows), then the head drains D(t)
+            if (next < npairs && hc == t) store_pe_row(pe, a_pe, r);
             float d = 0.f;
 #pragma unroll
-            for (int gk = 0; gk < 4; gk++) {
-              uint32_t v[32];
-              ODC_TMEM_LD32(dcol + 32 * gk, v);
+            for (int gk = 0; gk < 4; gk += 2) {
+              uint32_t v0[32], v1[32];
+              ODC_TMEM_LD32(dcol + 32 * gk, v0);
+              ODC_TMEM_LD32(dcol + 32 * gk + 32, v1);
               tmem_ld_wait();
-              d = head32<kBias>(v, bl + 32 * gk, s_head + hc * 128 + 32 * gk, d);
+              d = head32<kBias>(v0, bl + 32 * gk, s_head + hc * 128 + 32 * gk, d);
+              d = head32<kBias>(v1, bl + 32 * gk + 32, s_head + hc * 128 + 32 * gk + 32, d);
             }
+            part[t] = d;
             if (tr) ODC_TRACE(ti, l, 12 + t);
-            // halves meet in shared memory (the 8 warps are on the same tile)
-            if (hc == 1) s_part[r] = d;
-            named_bar_sync(1, 256);
-            if (hc == 0) dot[t] = d + s_part[r];
-            named_bar_sync(1, 256);
-            // D(t) drained; the next pair's encoding of tile t goes in (half t's rows)
-            if (next < npairs && hc == t) store_pe_row(pe, a_pe, r);
             release(t);
             if (tr) ODC_TRACE(ti, l, 10 + t);
           }
         }
       }
       p_prev = pr * 512 + crank * 128 + r;  // tile 0 row; tile 1 row = +256
-      dot_prev[0] = dot[0];
-      dot_prev[1] = dot[1];
+      part_prev[0] = part[0];
+      part_prev[1] = part[1];
       pr = next;
     }
-    if (hc == 0 && p_prev >= 0) {
-      finish_label(m, src, n, p_prev, dot_prev[0], labels, raw);
-      finish_label(m, src, n, p_prev + 256, dot_prev[1], labels, raw);
+    if (p_prev >= 0) {
+      finish_tile(0);
+      finish_tile(1);
     }
   }
   tc_fence_before();
