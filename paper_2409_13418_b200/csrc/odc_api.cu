@@ -119,7 +119,7 @@ struct odc_ctx {
   CellTabEntry* table = nullptr;
   unsigned long long* h_pinned = nullptr;  // small readback buffer
   unsigned int* d_fail = nullptr;          // device flag: a winding query stayed on the surface
-  unsigned long long* d_sched = nullptr;   // MLP evaluator's pair counter (only grows)
+  unsigned long long* d_sched = nullptr;   // MLP evaluator's pair counters: [0] only grows, [1] compacted batches
   unsigned long long sched_next = 0;       // its value when the next launch starts
   char* h_stage = nullptr;  // grow-only pinned staging for mesh copy-back
   // mesh validation (its own workspace: the last extraction stays valid)
@@ -207,13 +207,17 @@ void check_status(odc_ctx* c, DevStatus* dst) {
 }
 
 // One MLP evaluator launch on this context's stream and pair counter.
+// With src.n_dev (a compacted batch, count known only on the device) the
+// launch uses a second pair counter that the producing kernel resets to 0.
 void run_mlp(odc_ctx* c, const odc_field* f, const PointSrc& src, int64_t n, uint8_t* lab, double* raw,
              cudaStream_t s, const MlpDev* override_md = nullptr) {
   MlpDev md = override_md ? *override_md : f->mlp;
   if (!override_md) md.impl = c->mlp_impl;
-  md.sched = c->d_sched;
-  if (mlp_eval(md, src, n, lab, raw, s, &c->sched_next) != 0)
-    throw OdcError{ODC_E_CUDA, "MLP evaluator: no pair counter on this context"};
+  unsigned long long base0 = 0;
+  md.sched = src.n_dev ? c->d_sched + 1 : c->d_sched;
+  if (mlp_eval(md, src, n, lab, raw, s, src.n_dev ? &base0 : &c->sched_next) != 0)
+    throw OdcError{ODC_E_CUDA, "MLP evaluator: no pair counter on this context, or a compacted batch on an "
+                               "evaluator other than mlp_impl 3"};
 }
 
 // Evaluate labels (and optionally raw) of n points through the field.
@@ -247,7 +251,8 @@ void ensure_mlp_format(odc_ctx* c, const odc_field* fc) {
   }
 }
 
-void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* lab, double* raw) {
+void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* lab, double* raw,
+                 const int64_t* n_dev = nullptr, const int32_t* out_map = nullptr) {
   if (n == 0) return;
   if (f->kind == 0) {
     FieldP fp{f->nodes, f->n_nodes, 0, f->iso};
@@ -261,6 +266,8 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
   } else {
     ensure_mlp_format(c, f);
     PointSrc src{pts, GridP{}, 0};
+    src.n_dev = n_dev;
+    src.out_map = out_map;
     run_mlp(c, f, src, n, lab, raw, c->stream);
   }
   check_launch(c);
@@ -745,10 +752,22 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       const int nsteps = search2d_num_steps(op);
       int64_t M = launch_search2d_lockstep_points(g, op, c->inst_key, Q, 0, state, pts, s);
       check_launch(c);
+      // linear-scan steps evaluate only the instances (rays) still scanning
+      // (CTA-pair evaluator only: it takes the count on the device)
+      const bool compact = f->kind == 1 && c->mlp_impl == 3;
+      int32_t* map = compact ? need(c->arena.get<int32_t>(2 * Q)) : nullptr;
+      int64_t* cnt2 = compact ? need(c->arena.get<int64_t>(2)) : nullptr;
+      bool packed = false;  // this step's points are compacted
       for (int step = 0; step < nsteps; step++) {
-        eval_points(c, f, pts, M, lab, nullptr);
+        if (packed) eval_points(c, f, pts, M, lab, nullptr, cnt2 + (step & 1), map);
+        else eval_points(c, f, pts, M, lab, nullptr);
         if (step + 1 < nsteps) {  // update + the next step's points in one pass
-          M = launch_search2d_lockstep_step(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, pts, s);
+          const bool was = packed;
+          // the first step of each linear scan still has every instance scanning
+          packed = compact && search2d_step_is_linear(op, step + 1) && search2d_step_is_linear(op, step);
+          if (packed && !was) CUDA_TRY(cudaMemsetAsync(cnt2, 0, 2 * sizeof(int64_t), s));  // a run starts
+          M = launch_search2d_lockstep_step(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, pts, s,
+                                            packed ? map : nullptr, cnt2, c->d_sched + 1);
         } else {
           launch_search2d_lockstep_update(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, s);
         }
@@ -921,7 +940,7 @@ int odc_create(int device, odc_ctx** out) {
   if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess || cudaEventCreate(&c->ev0) != cudaSuccess ||
       cudaEventCreate(&c->ev1) != cudaSuccess || cudaMallocHost(&c->h_pinned, 4096) != cudaSuccess ||
       cudaMalloc(&c->d_fail, 4) != cudaSuccess || cudaMemset(c->d_fail, 0, 4) != cudaSuccess ||
-      cudaMalloc(&c->d_sched, 8) != cudaSuccess || cudaMemset(c->d_sched, 0, 8) != cudaSuccess) {
+      cudaMalloc(&c->d_sched, 16) != cudaSuccess || cudaMemset(c->d_sched, 0, 16) != cudaSuccess) {
     delete c;
     return ODC_E_CUDA;
   }

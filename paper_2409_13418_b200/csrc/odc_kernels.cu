@@ -1101,12 +1101,29 @@ __global__ void k_s2_update(GridP g, OptP o, const uint32_t* __restrict__ L, con
 // per lock-step instead of two.  PH = phase of ``step`` (0 midpoint probe,
 // 1 step-1 ray, 2 step-2 rays), so the loads of fields the phase never reads
 // compile away.
+//
+// Compacted next step (cmp.map != nullptr; the next step is a linear scan):
+// an instance (ray) whose scan already flipped cannot change its state, so
+// only the others get a query point -- packed at slots taken from cmp.cnt
+// (one atomic per warp), with map[slot] = its label slot.  The evaluator
+// reads the count on the device (PointSrc::n_dev) and writes labels through
+// the map; the eval accounting keeps the reference's logical counts.
+struct S2Compact {
+  int32_t* map;
+  int64_t* cnt;                 // count of the step being produced (zero on entry)
+  int64_t* cnt_clear;           // the previous step's count: reset here for the step after
+  unsigned long long* sched;    // the evaluator's pair counter for compacted batches: reset here
+};
 template <int PH>
 __global__ void __launch_bounds__(256) k_s2_step(GridP g, OptP o, const uint32_t* __restrict__ L,
                                                  const int64_t* __restrict__ inst_key, int64_t Q, int step,
                                                  const uint8_t* __restrict__ lab, S2View S, DevStatus* dst,
-                                                 double* __restrict__ pts) {
+                                                 double* __restrict__ pts, S2Compact cmp) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cmp.map && q == 0) {
+    *cmp.cnt_clear = 0;
+    *cmp.sched = 0ull;
+  }
   if (q >= Q) return;
   Search2DState s = s2_load(S, q);
   if (PH == 0) {  // fields not yet written (init leaves them zero); keep them out of the load
@@ -1127,7 +1144,20 @@ __global__ void __launch_bounds__(256) k_s2_step(GridP g, OptP o, const uint32_t
       double u, v, p[3];
       s2_point_uv(o, I, s, next, r, u, v);
       lift(I, u, v, p);
-      const int64_t m = q + r * Q;
+      int64_t m = q + r * Q;
+      if (cmp.map) {
+        const bool act = nr == 1 ? !s.found1 : !(r == 0 ? s.found2[0] : s.found2[1]);
+        const unsigned am = __activemask();
+        const unsigned b = __ballot_sync(am, act);
+        const int lane = threadIdx.x & 31, lead = __ffs(am) - 1;
+        int64_t base = 0;
+        if (lane == lead && b) base = (int64_t)atomicAdd((unsigned long long*)cmp.cnt, (unsigned long long)__popc(b));
+        base = __shfl_sync(am, base, lead);
+        if (!act) continue;
+        const int64_t slot = base + __popc(b & ((1u << lane) - 1u));
+        cmp.map[slot] = (int32_t)m;
+        m = slot;
+      }
       pts[3 * m] = p[0];
       pts[3 * m + 1] = p[1];
       pts[3 * m + 2] = p[2];
@@ -1187,15 +1217,23 @@ void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32
                                      cudaStream_t s) {
   if (Q) k_s2_update<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, inst_key, Q, step, lab, s2_view(state, Q), dst);
 }
+bool search2d_step_is_linear(const OptP& o, int step) {
+  const int n1 = o.s1_lin + o.s1_bin;
+  return (step >= 1 && step <= o.s1_lin) || (step > n1 && step - n1 <= o.s2_lin);
+}
 int64_t launch_search2d_lockstep_step(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
                                       int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
-                                      double* pts, cudaStream_t s) {
+                                      double* pts, cudaStream_t s, int32_t* map, int64_t* cnt2,
+                                      unsigned long long* sched) {
   if (Q) {
     const int ph = step == 0 ? 0 : step <= o.s1_lin + o.s1_bin ? 1 : 2;
     const S2View v = s2_view(state, Q);
-    if (ph == 0) k_s2_step<0><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts);
-    else if (ph == 1) k_s2_step<1><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts);
-    else k_s2_step<2><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts);
+    S2Compact cmp{};
+    if (map) cmp = S2Compact{map, cnt2 + ((step + 1) & 1), cnt2 + (step & 1), sched};
+    if (ph == 0) k_s2_step<0><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts, cmp);
+    else if (ph == 1)
+      k_s2_step<1><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts, cmp);
+    else k_s2_step<2><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts, cmp);
   }
   return step + 1 > o.s1_lin + o.s1_bin ? 2 * Q : Q;
 }

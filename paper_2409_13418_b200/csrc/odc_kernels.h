@@ -101,9 +101,16 @@ void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32
                                      const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,
                                      Stage2D out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s);
 // fused: fold the labels of ``step`` in and write the points of step + 1; returns their count
+// step's labels in, the query points of step + 1 out.  With map != nullptr
+// (only when step + 1 is a linear scan step) the points are compacted to the
+// instances/rays still scanning: count in cnt2[(step + 1) & 1] (cnt2 is two
+// int64, zero before the first step), label slot of point i in map[i]; the
+// kernel also resets cnt2[step & 1] and the evaluator's pair counter sched.
+bool search2d_step_is_linear(const OptP& o, int step);
 int64_t launch_search2d_lockstep_step(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
                                       int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
-                                      double* pts, cudaStream_t s);
+                                      double* pts, cudaStream_t s, int32_t* map = nullptr, int64_t* cnt2 = nullptr,
+                                      unsigned long long* sched = nullptr);
 int search2d_num_steps(const OptP& o);
 
 // fd-gradient normals (pipeline.py:126-151): 6K raw samples

@@ -234,6 +234,7 @@ __device__ __forceinline__ void grid_coords_fast(const PointSrc& src, int64_t p,
 __device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& src, int64_t n, int64_t p, float dot,
                                              uint8_t* __restrict__ labels, double* __restrict__ raw) {
   if (p < 0 || p >= n) return;
+  const int64_t o = src.out_map ? (int64_t)src.out_map[p] : p;  // output slot
   if (!raw) {
     // labels only: the sign of the logit in fp32 (short dependent chains
     // instead of fp64 divide / sqrt / exp).  Its error is < 1e-4 for these
@@ -265,7 +266,7 @@ __device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& sr
     }
     const float lg = (float)m.amplitude * (dot + m.b_head) - (float)m.prior_scale * (sqrtf(d2) - (float)m.prior_radius);
     if (fabsf(lg) > 1e-3f) {
-      labels[p] = lg > 0.f ? 1 : 0;
+      labels[o] = lg > 0.f ? 1 : 0;
       return;
     }
   }
@@ -276,8 +277,8 @@ __device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& sr
   const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
   const double logit = m.amplitude * mlp - m.prior_scale * (dist - m.prior_radius);
   const double rv = 1.0 / (1.0 + exp(-logit));
-  labels[p] = rv > 0.5 ? 1 : 0;
-  if (raw) raw[p] = rv;
+  labels[o] = rv > 0.5 ? 1 : 0;
+  if (raw) raw[o] = rv;
 }
 
 template <bool kBias, bool kTrace>
@@ -992,7 +993,7 @@ __device__ __forceinline__ void umma_ss2(uint32_t d_tmem, uint64_t a, uint64_t b
 
 template <bool kBias>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
-    k_mlp_tc4(MlpDev m, PointSrc src, int64_t n, uint8_t* __restrict__ labels, double* __restrict__ raw) {
+    k_mlp_tc4(MlpDev m, PointSrc src, int64_t n_launch, uint8_t* __restrict__ labels, double* __restrict__ raw) {
   using namespace tc;
   using tc2::cluster_ctarank;
   using tc2::cluster_sync;
@@ -1022,6 +1023,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
+  const int64_t n = src.n_dev ? *src.n_dev : n_launch;  // compacted batch: count from the producer kernel
   const int64_t npairs = (n + 511) / 512;
 
   if (m.trace && threadIdx.x == 0 && blockIdx.x < 300) m.trace[400 + 2 * blockIdx.x] = globaltimer_ns();
@@ -1394,6 +1396,7 @@ int mlp_eval(const MlpDev& m_in, const PointSrc& src, int64_t n, uint8_t* labels
   });
   const int g_num_sms = num_sms[dev];
   const int64_t ntiles = (n + 255) / 256;
+  if ((src.n_dev || src.out_map) && m.impl != 3) return -2;  // compacted batches: impl 3 only
   if (m.impl == 3) {
     const int64_t np4 = (n + 511) / 512;
     const int64_t pairs = (g_num_sms / 2) < np4 ? (g_num_sms / 2) : np4;

@@ -45,6 +45,11 @@ struct PointSrc {
   // cos_k of every coordinate index, 16 floats per row) and a fast divisor by S
   const float* petab;
   uint32_t fd_m, fd_s;
+  // compacted batches (mlp_impl 3 only): the point count is read on the
+  // device (n is then only the launch's upper bound) and label/raw i goes
+  // to out_map[i]
+  const int64_t* n_dev;
+  const int32_t* out_map;
 };
 
 size_t mlp_packed_weight_elems();
