@@ -56,12 +56,15 @@ def test_tc_vs_numpy_fp32_label_agreement():
     assert np.mean(a == c) > 0.995
 
 
-def test_tc_batch_invariance():
+@pytest.mark.parametrize("impl", [0, 3])
+def test_tc_batch_invariance(impl):
+    """A point's value does not depend on its batch or position in it (the
+    shared-field oracle evaluates other batches than the pipeline)."""
     field = MlpField(seed=3, amplitude=2.0)
     rng = np.random.default_rng(1)
     pts = rng.uniform(0, 1, size=(5000, 3))
-    full = device_raw(field, pts, 0)
-    part = np.concatenate([device_raw(field, pts[:1234], 0), device_raw(field, pts[1234:], 0)])
+    full = device_raw(field, pts, impl)
+    part = np.concatenate([device_raw(field, pts[:1234], impl), device_raw(field, pts[1234:], impl)])
     assert np.array_equal(full, part)
-    rev = device_raw(field, pts[::-1].copy(), 0)[::-1]
+    rev = device_raw(field, pts[::-1].copy(), impl)[::-1]
     assert np.array_equal(full, rev)
