@@ -145,7 +145,9 @@ int odc_version(void);
 int odc_create(int device, odc_ctx** out);
 void odc_destroy(odc_ctx* ctx);
 const char* odc_last_error(const odc_ctx* ctx);
-/* stream: a cudaStream_t passed as void* (NULL = the context's own stream) */
+/* stream: a cudaStream_t passed as void* (NULL = the context's own stream).
+ * Synchronises the previous stream first: a context's launches stay ordered
+ * (its MLP evaluator takes work from a per-context device counter). */
 int odc_set_stream(odc_ctx* ctx, void* stream);
 /* tuning/testing knobs: "mlp_impl" = 3 CTA-pair N=256 tile ping-pong tcgen05
  * evaluator (default), 2 single-CTA tcgen05, 0 CTA-pair with A in TMEM, 1 SIMT
