@@ -208,6 +208,12 @@ int odc_mesh_finish(odc_ctx* ctx, const double* vertices, int64_t n_vertices, co
 /* which: 0 = repaired mesh, 1 = raw (pre-repair) mesh.  Buffers sized from stats. */
 int odc_copy_mesh(odc_ctx* ctx, int32_t which, double* vertices, int64_t* triangles, int64_t* prov_kind,
                   int64_t* prov_ref);
+/* the repaired mesh and the raw mesh's triangles in one pipelined transfer
+ * (ContourResult.mesh + raw_mesh when repair added vertices: the raw mesh's
+ * vertices/provenance are the first raw_n_vertices rows of the repaired one,
+ * its triangles differ).  raw_triangles: (raw_n_triangles, 3), may be NULL. */
+int odc_copy_mesh_pair(odc_ctx* ctx, double* vertices, int64_t* triangles, int64_t* prov_kind, int64_t* prov_ref,
+                       int64_t* raw_triangles);
 /* zero-copy device view of the last mesh: vertices (V,3) f64, triangles (T,3) i32 */
 int odc_mesh_device(odc_ctx* ctx, int32_t which, const double** vertices, const int32_t** triangles,
                     int64_t* n_vertices, int64_t* n_triangles);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -127,6 +128,7 @@ struct odc_ctx {
   std::vector<int64_t> v_edges, v_pinched, v_isolated;
   std::vector<int64_t> v_si_pairs;
   size_t h_stage_bytes = 0;
+  std::vector<cudaEvent_t> copy_evs;       // one per staged piece of a mesh copy
   std::string err;
   int launches = 0;
   // odc_set_param("mlp_impl"): 3 CTA-pair N=256 ping-pong tcgen05 (default,
@@ -980,6 +982,7 @@ void odc_destroy(odc_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->d_fail) cudaFree(c->d_fail);
   if (c->d_sched) cudaFree(c->d_sched);
+  for (auto e : c->copy_evs) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (auto& e : c->evs)
@@ -1360,22 +1363,96 @@ int odc_mesh_finish(odc_ctx* c, const double* vertices, int64_t V, const int32_t
   }, &a);
 }
 
+// Device arrays -> the caller's host buffers, pipelined: each segment is
+// split into ~4 MB pieces, every piece is copied D2H into pinned staging at
+// full link speed and recorded with an event, and host threads spread the
+// pieces into the (pageable, first-touch) destinations as soon as their
+// event completes -- the D2H of later pieces overlaps the host copies of
+// earlier ones.
+struct CopySeg {
+  const void* dev;
+  void* host;
+  size_t bytes;
+};
+void copy_out_pipelined(odc_ctx* cc, const std::vector<CopySeg>& segs) {
+  cudaStream_t s = cc->stream;
+  struct Piece {
+    const void* dev;
+    char* stage;
+    char* dst;
+    size_t n;
+  };
+  const size_t chunk = 4u << 20;
+  size_t total = 0;
+  for (const CopySeg& g : segs)
+    if (g.host && g.bytes) total += (g.bytes + 255) & ~(size_t)255;
+  if (!total) return;
+  if (total > cc->h_stage_bytes) {
+    if (cc->h_stage) cudaFreeHost(cc->h_stage);
+    cc->h_stage = nullptr;
+    cc->h_stage_bytes = 0;
+    const size_t want = total + total / 4;
+    CUDA_TRY(cudaHostAlloc((void**)&cc->h_stage, want, cudaHostAllocDefault));
+    cc->h_stage_bytes = want;
+  }
+  std::vector<Piece> pieces;
+  size_t off = 0;
+  for (const CopySeg& g : segs) {
+    if (!g.host || !g.bytes) continue;
+    for (size_t o = 0; o < g.bytes; o += chunk)
+      pieces.push_back({(const char*)g.dev + o, cc->h_stage + off + o, (char*)g.host + o, std::min(chunk, g.bytes - o)});
+    off += (g.bytes + 255) & ~(size_t)255;
+  }
+  while (cc->copy_evs.size() < pieces.size()) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cc->copy_evs.push_back(e);
+  }
+  for (size_t i = 0; i < pieces.size(); i++) {
+    CUDA_TRY(cudaMemcpyAsync(pieces[i].stage, pieces[i].dev, pieces[i].n, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(cc->copy_evs[i], s));
+  }
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nthr = std::min<size_t>({(size_t)8, (size_t)hw, pieces.size()});
+  std::atomic<int> bad{0};
+  auto work = [&](size_t t) {
+    for (size_t i = t; i < pieces.size(); i += nthr) {
+      if (cudaEventSynchronize(cc->copy_evs[i]) != cudaSuccess) {
+        bad = 1;
+        return;
+      }
+      std::memcpy(pieces[i].dst, pieces[i].stage, pieces[i].n);
+    }
+  };
+  if (nthr <= 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (size_t t = 1; t < nthr; t++) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+  }
+  if (bad) throw OdcError{ODC_E_CUDA, "mesh copy failed"};
+}
+
 struct CopyMeshArgs {
   int32_t which;
   double* v;
   int64_t* t;
   int64_t* kind;
   int64_t* ref;
+  int64_t* raw_t;  // odc_copy_mesh_pair: the pre-repair triangles too
 };
 
-int odc_copy_mesh(odc_ctx* c, int32_t which, double* vertices, int64_t* triangles, int64_t* prov_kind,
-                  int64_t* prov_ref) {
+// Everything is produced in its final host type on the device (triangles
+// widened to int64, duplicate provenance filled in) and copied out with
+// copy_out_pipelined.
+int copy_mesh_impl(odc_ctx* c, CopyMeshArgs* a) {
   if (!c) return ODC_E_ARG;
   if (!c->valid) {
     c->err = "no extraction result";
     return ODC_E_ARG;
   }
-  CopyMeshArgs a{which, vertices, triangles, prov_kind, prov_ref};
   cudaSetDevice(c->device);
   return guard(c, [](odc_ctx* cc, void* p) {
     CopyMeshArgs* x = (CopyMeshArgs*)p;
@@ -1384,28 +1461,12 @@ int odc_copy_mesh(odc_ctx* c, int32_t which, double* vertices, int64_t* triangle
     const double* dv = raw ? cc->verts0 : cc->verts1;
     const int32_t* dt = raw ? cc->tris0 : cc->tris1;
     cudaStream_t s = cc->stream;
-    // Everything is produced in its final host type on the device (triangles
-    // widened to int64, duplicate provenance filled in), copied with one D2H
-    // per array into pinned staging at full link speed, then spread into the
-    // caller's (pageable, first-touch) buffers by several host threads.
-    struct Seg {
-      const void* dev;
-      void* host;
-      size_t bytes;
-      size_t off;
-    };
-    std::vector<Seg> segs;
-    size_t total = 0;
-    auto add = [&](const void* dev, void* host, size_t bytes) {
-      if (!host || !bytes) return;
-      segs.push_back({dev, host, bytes, total});
-      total += (bytes + 255) & ~(size_t)255;
-    };
-    add(dv, x->v, sizeof(double) * 3 * V);
+    std::vector<CopySeg> segs;
+    segs.push_back({dv, x->v, sizeof(double) * 3 * V});
     if (x->t && T) {
       int64_t* t64 = need(cc->arena.get<int64_t>(3 * T));
       launch_widen_i32(dt, t64, 3 * T, s);
-      add(t64, x->t, sizeof(int64_t) * 3 * T);
+      segs.push_back({t64, x->t, sizeof(int64_t) * 3 * T});
     }
     if ((x->kind || x->ref) && V) {
       int64_t* dk = need(cc->arena.get<int64_t>(V));
@@ -1416,46 +1477,30 @@ int odc_copy_mesh(odc_ctx* c, int32_t which, double* vertices, int64_t* triangle
       else
         launch_provenance(V0, cc->P, cc->src0, cc->cells.part_cell, cc->cells.part_index, cc->fan_edge, dk, dr, s);
       launch_dup_provenance(V0, V, dk, dr, s);
-      add(dk, x->kind, sizeof(int64_t) * V);
-      add(dr, x->ref, sizeof(int64_t) * 2 * V);
+      segs.push_back({dk, x->kind, sizeof(int64_t) * V});
+      segs.push_back({dr, x->ref, sizeof(int64_t) * 2 * V});
+    }
+    if (x->raw_t && T) {  // pre-repair triangles (same count, corners not renamed)
+      int64_t* r64 = need(cc->arena.get<int64_t>(3 * T));
+      launch_widen_i32(cc->tris0, r64, 3 * T, s);
+      segs.push_back({r64, x->raw_t, sizeof(int64_t) * 3 * T});
     }
     CUDA_TRY(cudaGetLastError());
-    if (total > cc->h_stage_bytes) {
-      if (cc->h_stage) cudaFreeHost(cc->h_stage);
-      cc->h_stage = nullptr;
-      cc->h_stage_bytes = 0;
-      const size_t want = total + total / 4;
-      CUDA_TRY(cudaHostAlloc((void**)&cc->h_stage, want, cudaHostAllocDefault));
-      cc->h_stage_bytes = want;
-    }
-    for (const Seg& g : segs)
-      CUDA_TRY(cudaMemcpyAsync(cc->h_stage + g.off, g.dev, g.bytes, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    // parallel spread: chunks of ~4 MB over up to 8 threads
-    const size_t chunk = 4u << 20;
-    struct Piece {
-      const char* src;
-      char* dst;
-      size_t n;
-    };
-    std::vector<Piece> pieces;
-    for (const Seg& g : segs)
-      for (size_t o = 0; o < g.bytes; o += chunk)
-        pieces.push_back({cc->h_stage + g.off + o, (char*)g.host + o, std::min(chunk, g.bytes - o)});
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t nthr = std::min<size_t>({(size_t)8, (size_t)hw, pieces.size()});
-    if (nthr <= 1) {
-      for (const Piece& q : pieces) std::memcpy(q.dst, q.src, q.n);
-    } else {
-      std::vector<std::thread> pool;
-      for (size_t t = 0; t < nthr; t++)
-        pool.emplace_back([&pieces, t, nthr]() {
-          for (size_t i = t; i < pieces.size(); i += nthr) std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].n);
-        });
-      for (auto& th : pool) th.join();
-    }
+    copy_out_pipelined(cc, segs);
     return (int)ODC_OK;
-  }, &a);
+  }, a);
+}
+
+int odc_copy_mesh(odc_ctx* c, int32_t which, double* vertices, int64_t* triangles, int64_t* prov_kind,
+                  int64_t* prov_ref) {
+  CopyMeshArgs a{which, vertices, triangles, prov_kind, prov_ref, nullptr};
+  return copy_mesh_impl(c, &a);
+}
+
+int odc_copy_mesh_pair(odc_ctx* c, double* vertices, int64_t* triangles, int64_t* prov_kind, int64_t* prov_ref,
+                       int64_t* raw_triangles) {
+  CopyMeshArgs a{0, vertices, triangles, prov_kind, prov_ref, raw_triangles};
+  return copy_mesh_impl(c, &a);
 }
 
 struct ValidateArgs {

@@ -216,6 +216,31 @@ def _copy_mesh(ctx, which, st, provenance=True):
     return TriangleMesh.trusted(v, t, kind, ref)
 
 
+def _copy_meshes(ctx, st, provenance=True):
+    """(mesh, raw_mesh) in one pipelined device-to-host transfer.  Repair
+    only appends duplicates of existing vertices and renames triangle corners
+    to them (polygonize.py:348-373), so the raw mesh's vertices and
+    provenance are views of the repaired mesh's first rows and only its
+    triangles are copied."""
+    if st.repair_added_vertices == 0:
+        mesh = _copy_mesh(ctx, 0, st, provenance)
+        return mesh, mesh
+    V, T, V0, T0 = int(st.n_vertices), int(st.n_triangles), int(st.raw_n_vertices), int(st.raw_n_triangles)
+    v = np.empty((V, 3), dtype=np.float64)
+    t = np.empty((T, 3), dtype=np.int64)
+    rt = np.empty((T0, 3), dtype=np.int64)
+    kind = np.empty(V, dtype=np.int64) if provenance else None
+    ref = np.empty((V, 2), dtype=np.int64) if provenance else None
+    ptr = lambda a: a.ctypes.data if a is not None and a.size else None  # noqa: E731
+    rc = _lib.load().odc_copy_mesh_pair(ctx.handle, ptr(v), ptr(t), ptr(kind), ptr(ref), ptr(rt))
+    if rc != _lib.ODC_OK:
+        _raise(rc, ctx)
+    mesh = TriangleMesh.trusted(v, t, kind, ref)
+    raw = TriangleMesh.trusted(v[:V0], rt, kind[:V0] if kind is not None else None,
+                               ref[:V0] if ref is not None else None)
+    return mesh, raw
+
+
 def _raw_from_repaired(ctx, mesh, st):
     """The pre-repair mesh: repair only appends duplicates of existing
     vertices and renames triangle corners to them (polygonize.py:348-373), so
@@ -299,8 +324,7 @@ def contour(field, grid, options=None, counter=None, *, device=0, provenance=Tru
         empty = TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64))
         mesh = raw_mesh = empty
     else:
-        mesh = _copy_mesh(ctx, 0, st, provenance)
-        raw_mesh = mesh if st.repair_added_vertices == 0 else _raw_from_repaired(ctx, mesh, st)
+        mesh, raw_mesh = _copy_meshes(ctx, st, provenance)
     record_counts(counter, st)
     stats["wall_time_s"] = time.perf_counter() - t0
     stats["eval_counts"] = counter.snapshot()
