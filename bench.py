@@ -370,10 +370,12 @@ def run_gpu_batch(args, rank, world, dist):
     opts = make_options(ContourOptions())
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
 
-    def worker(idx):
-        ctx = _lib.context(device)
+    ctxs = [_lib.Context(device) for _ in range(workers)]  # worker w always on ctxs[w]
+
+    def worker(w):
+        ctx = ctxs[w]
         out = []
-        for j in idx:
+        for j in parts[w]:
             f, g = mine[j]
             with DeviceField(ctx, f) as df:
                 st = _lib.Stats()
@@ -386,10 +388,12 @@ def run_gpu_batch(args, rank, world, dist):
         return out
 
     parts = [list(range(w, len(mine), workers)) for w in range(workers)]
+    # one pool for the whole run: libodc contexts are per host thread, so the
+    # same threads keep their contexts (workspace, streams) across steps
+    pool = ThreadPoolExecutor(max_workers=workers)
 
     def run_all():
-        with ThreadPoolExecutor(max_workers=workers) as pool:
-            return sum(sum(x) for x in pool.map(worker, parts))
+        return sum(sum(x) for x in pool.map(worker, range(workers)))
 
     for _ in range(args.warmup):
         run_all()

@@ -9,9 +9,26 @@ and deterministic).
 
 from __future__ import annotations
 
+import threading
 from concurrent.futures import ThreadPoolExecutor
 
+from . import _lib
 from .pipeline import contour
+
+# Worker w of a batch always runs jobs w, w + W, w + 2W, ... on its own
+# persistent libodc context, so each context's workspace settles at the size
+# of the same shapes on every call (no re-allocation, deterministic).
+_state: dict = {}
+_state_lock = threading.Lock()
+
+
+def _workers(device, workers):
+    with _state_lock:
+        key = (device, workers)
+        if key not in _state:
+            _state[key] = (ThreadPoolExecutor(max_workers=workers, thread_name_prefix=f"odc{device}"),
+                           [_lib.Context(device) for _ in range(workers)])
+        return _state[key]
 
 
 def contour_batch(jobs, options=None, *, workers=8, device=0, provenance=True):
@@ -19,10 +36,14 @@ def contour_batch(jobs, options=None, *, workers=8, device=0, provenance=True):
     jobs = list(jobs)
     if not jobs:
         return []
+    W = max(1, min(workers, len(jobs)))
+    pool, ctxs = _workers(device, W)
 
-    def run(job):
-        field, grid = job
-        return contour(field, grid, options, device=device, provenance=provenance)
+    def run(w):
+        return [contour(f, g, options, device=device, provenance=provenance, _ctx=ctxs[w]) for f, g in jobs[w::W]]
 
-    with ThreadPoolExecutor(max_workers=max(1, min(workers, len(jobs)))) as pool:
-        return list(pool.map(run, jobs))
+    parts = list(pool.map(run, range(W)))
+    out = [None] * len(jobs)
+    for w, res in enumerate(parts):
+        out[w::W] = res
+    return out

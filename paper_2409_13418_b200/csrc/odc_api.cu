@@ -1405,7 +1405,9 @@ void copy_out_pipelined(odc_ctx* cc, const std::vector<CopySeg>& segs) {
   }
   while (cc->copy_evs.size() < pieces.size()) {
     cudaEvent_t e;
-    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // blocking sync: the copy threads sleep until their piece lands instead
+    // of spinning (several contexts copy at once in batch mode)
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
     cc->copy_evs.push_back(e);
   }
   for (size_t i = 0; i < pieces.size(); i++) {

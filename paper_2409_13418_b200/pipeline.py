@@ -299,7 +299,7 @@ def _grid_args(grid):
 
 
 def contour(field, grid, options=None, counter=None, *, device=0, provenance=True, keep_intermediates=False,
-            return_context=False):
+            return_context=False, _ctx=None):
     """Run the dual contouring pipeline on the GPU and return the repaired mesh.
 
     Signature and result follow occmesh.pipeline.contour (pipeline.py:154);
@@ -308,7 +308,7 @@ def contour(field, grid, options=None, counter=None, *, device=0, provenance=Tru
     options.validate()
     counter = counter or EvalCounter(field)
     t0 = time.perf_counter()
-    ctx = _lib.context(device)
+    ctx = _ctx if _ctx is not None else _lib.context(device)  # _ctx: contour_batch's own contexts
     L = _lib.load()
     st = _lib.Stats()
     lo, hi, R = _grid_args(grid)
