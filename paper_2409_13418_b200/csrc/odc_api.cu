@@ -735,6 +735,12 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   c->inst_edges = c->keep ? need(c->arena.get<int64_t>(2 * Q)) : nullptr;
   c->s2 = Stage2D{};
   if (op.normals == ODC_NORMALS_2D) {
+    // line_binary_search_batch (search.py:116-127) with n_linear == 0
+    // divides by zero: its bracket is [-inf, nan], the next query is
+    // non-finite and eval_labels raises (fields.py:42-45)
+    const bool nan1 = op.s1_lin == 0 && (op.s1_bin > 0 || op.s2_lin + op.s2_bin > 0);
+    const bool nan2 = op.s2_lin == 0 && op.s2_bin > 0;
+    if (Q > 0 && (nan1 || nan2)) throw OdcError{ODC_E_VALUE, "non-finite query point at index 0"};
     c->s2.pos3 = need(c->arena.get<double>(3 * Q));
     if (c->keep) {
       c->s2.pos2 = need(c->arena.get<double>(2 * Q));

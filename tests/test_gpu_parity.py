@@ -160,6 +160,34 @@ def test_gpu_mlp_shared_field_64():
     assert res.stats["repair_added_vertices"] == len(o["vertices"]) - len(o["raw_vertices"])
 
 
+@pytest.mark.parametrize("s1,s2", [((2, 5, 0.8), (1, 6, 0.7)), ((6, 3, 0.9), (5, 4, 0.6)), ((1, 8, 0.8), (2, 7, 0.7))])
+def test_gpu_mlp_search_budgets(s1, s2):
+    """Lock-step 2D search on the MLP evaluator with other line budgets: the
+    compacted linear-scan steps (only rays still scanning are evaluated) must
+    leave every stage identical to the oracle, which evaluates every ray."""
+    from paper_2409_13418_b200.pipeline import LineBudget, SearchBudget
+
+    opts = ContourOptions(budget=SearchBudget(iters_1d=12, step1=LineBudget(*s1), step2=LineBudget(*s2)))
+    field = MlpField(seed=1, amplitude=3.0)
+    res, arrs = gpu_run(field, (0, 0, 0), (1, 1, 1), 40, opts)
+    o = oracle_run(field, (0, 0, 0), (1, 1, 1), 40, opts)
+    compare(res, arrs, o)
+
+
+@pytest.mark.parametrize("s1,s2", [((0, 8, 0.8), (3, 12, 0.7)), ((4, 11, 0.8), (0, 7, 0.7))])
+def test_gpu_zero_linear_budget_raises(s1, s2):
+    """n_linear == 0 makes the reference's bracket [-inf, nan] (a division by
+    zero, search.py:124-125), so its next query is non-finite and eval_labels
+    raises ValueError (fields.py:42-45); the device path raises the same."""
+    from paper_2409_13418_b200 import SphereField
+    from paper_2409_13418_b200.pipeline import LineBudget, SearchBudget
+
+    opts = ContourOptions(budget=SearchBudget(step1=LineBudget(*s1), step2=LineBudget(*s2)))
+    for field in (SphereField((0.5, 0.5, 0.5), 0.3), MlpField(seed=0)):
+        with pytest.raises(ValueError, match="non-finite query point"):
+            contour(field, GridSpec((0, 0, 0), (1, 1, 1), 16), opts)
+
+
 def test_gpu_errors():
     from paper_2409_13418_b200 import ConfigurationError, SphereField
 
