@@ -158,7 +158,7 @@ def check(rc, ctx=None):
     raise OdcFailure(rc, msg)
 
 
-_contexts = {}
+_local = threading.local()  # per host thread: {device: Context}; freed with the thread
 
 
 class Context:
@@ -183,9 +183,13 @@ class Context:
 
 
 def context(device=0):
-    key = (device, threading.get_ident())
-    ctx = _contexts.get(key)
+    """This host thread's context on ``device`` (created on first use; it is
+    destroyed when the thread's locals are, so short-lived threads do not
+    accumulate device workspaces)."""
+    ctxs = getattr(_local, "ctxs", None)
+    if ctxs is None:
+        ctxs = _local.ctxs = {}
+    ctx = ctxs.get(device)
     if ctx is None:
-        ctx = Context(device)
-        _contexts[key] = ctx
+        ctx = ctxs[device] = Context(device)
     return ctx
