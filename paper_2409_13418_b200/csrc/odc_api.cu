@@ -1104,6 +1104,7 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
     if (d->biases[i] != 0.f) f->mlp.has_bias = 1;
   f->mlp.bias = f->bias;
   f->mlp.w_head = f->w_head;
+  for (int i = 0; i < 256; i++) f->mlp.w_head_k[i] = d->w_head[i];
   f->mlp.b_head = (float)d->b_head;
   f->mlp.amplitude = d->amplitude;
   f->mlp.prior_scale = d->prior_scale;

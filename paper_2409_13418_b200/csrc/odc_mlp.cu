@@ -220,6 +220,44 @@ __device__ __forceinline__ float head32(const uint32_t (&v)[32], const float* __
   return dot;
 }
 
+// The CTA-pair evaluator's head: relu(acc) . w over 32 columns with packed
+// FFMA2 (even and odd columns in the two lanes of a 64-bit accumulator;
+// the head is ALU-issue-bound on the pair boundary's critical path)
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t pack_f2(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ float2 unpack_f2(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return make_float2(lo, hi);
+}
+// sw: head weights in kernel-parameter space at a compile-time offset (the
+// caller branches on the column half), so no shared-memory load competes
+// with the tensor core's operand reads
+template <bool kBias>
+__device__ __forceinline__ uint64_t head32x2(const uint32_t (&v)[32], const float* __restrict__ sb,
+                                             const float* sw, uint64_t acc) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    float a = __uint_as_float(v[j]), b = __uint_as_float(v[j + 1]);
+    if (kBias) {
+      a += sb[j];
+      b += sb[j + 1];
+    }
+    a = a > 0.f ? a : 0.f;
+    b = b > 0.f ? b : 0.f;
+    acc = ffma2(pack_f2(a, b), pack_f2(sw[j], sw[j + 1]), acc);
+  }
+  return acc;
+}
+
 // grid vertex -> (x, y, z) with the precomputed divisor by S (vids < 2^31)
 __device__ __forceinline__ void grid_coords_fast(const PointSrc& src, int64_t p, uint32_t c[3]) {
   const uint32_t S = (uint32_t)src.grid.S;
@@ -1018,8 +1056,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
   uint64_t* sched_empty = bars + 28;           // [4] peer: all 22 reader warps took slot s
   int64_t* sched_pr = (int64_t*)(bars + 32);   // [4] ring of pair indices (>= npairs: no more work)
   uint64_t* a_loc = bars + 36;                 // [2] peer: its 8 epilogue warps released A(t)
-  float* s_head = (float*)(bars + 48);         // (256)
-  float* s_part = s_head + kWidth;             // (128) head partials of columns 128..255
+  float* s_part = (float*)(bars + 48) + kWidth;  // (128) head partials of columns 128..255 (the head's
+                                                 // weights are kernel parameters, m.w_head_k)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
@@ -1044,7 +1082,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = threadIdx.x; i < kWidth; i += blockDim.x) s_head[i] = m.w_head[i];
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -1333,17 +1370,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
             // layer 7 consumed A(t): the next pair's encoding of tile t goes in
             // first (half t's rows), then the head drains D(t)
             if (next < npairs && hc == t) store_pe_row(pe, a_pe, r);
-            float d = 0.f;
+            auto head = [&](auto hcc) {
+              constexpr int H = decltype(hcc)::value;
+              uint64_t acc = 0;  // (+0.f, +0.f)
 #pragma unroll
-            for (int gk = 0; gk < 4; gk += 2) {
-              uint32_t v0[32], v1[32];
-              ODC_TMEM_LD32(dcol + 32 * gk, v0);
-              ODC_TMEM_LD32(dcol + 32 * gk + 32, v1);
-              tmem_ld_wait();
-              d = head32<kBias>(v0, bl + 32 * gk, s_head + hc * 128 + 32 * gk, d);
-              d = head32<kBias>(v1, bl + 32 * gk + 32, s_head + hc * 128 + 32 * gk + 32, d);
-            }
-            part[t] = d;
+              for (int gk = 0; gk < 4; gk += 2) {
+                uint32_t v0[32], v1[32];
+                ODC_TMEM_LD32(dcol + 32 * gk, v0);
+                ODC_TMEM_LD32(dcol + 32 * gk + 32, v1);
+                tmem_ld_wait();
+                acc = head32x2<kBias>(v0, bl + 32 * gk, m.w_head_k + H * 128 + 32 * gk, acc);
+                acc = head32x2<kBias>(v1, bl + 32 * gk + 32, m.w_head_k + H * 128 + 32 * gk + 32, acc);
+              }
+              const float2 e = unpack_f2(acc);
+              return e.x + e.y;
+            };
+            part[t] = hc == 0 ? head(std::integral_constant<int, 0>{}) : head(std::integral_constant<int, 1>{});
             if (tr) ODC_TRACE(ti, l, 12 + t);
             release(t);
             if (tr) ODC_TRACE(ti, l, 10 + t);

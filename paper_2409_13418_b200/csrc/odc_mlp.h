@@ -31,6 +31,8 @@ struct MlpDev {
   unsigned long long sched_base;
   const float* bias;         // (8, 256)
   const float* w_head;       // (256)
+  float w_head_k[256];       // the same by value: kernel-parameter (constant) space, so the
+                             // CTA-pair head's uniform weight reads are FFMA constant operands
   float b_head;
   double amplitude, prior_scale, prior_radius;
   double prior_center[3];
