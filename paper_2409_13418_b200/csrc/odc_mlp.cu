@@ -136,20 +136,32 @@ size_t mlp_tc_weight_elems() { return (size_t)tc::kChunksPerPair * 128 * 64; }
 // chunk order = MMA consumption order: for l: for nh: for kc.  Each chunk is
 // the smem image of B rows n = 128 nh + r (K-major), k = 64 kc + j, swizzled.
 void mlp_pack_weights_tc(const float* w0, int d_in, const float* w_hidden, uint16_t* out) {
+  // 8 x 8 blocks: 8 rows k (8 contiguous n each) in, transposed, 8 contiguous
+  // 16-byte units (8 consecutive k of one row n) out
   size_t ci = 0;
   for (int l = 0; l < kDepth; l++) {
     const int nkc = l == 0 ? 1 : 4;
     for (int nh = 0; nh < 2; nh++)
       for (int kc = 0; kc < nkc; kc++, ci++) {
         uint16_t* img = out + ci * 128 * 64;
-        for (int r = 0; r < 128; r++)
-          for (int j = 0; j < 64; j++) {
-            const int n = 128 * nh + r, k = 64 * kc + j;
-            float v;
-            if (l == 0) v = k < d_in ? w0[(size_t)k * kWidth + n] : 0.f;
-            else v = w_hidden[((size_t)(l - 1) * kWidth + k) * kWidth + n];
-            const size_t byte = (size_t)((r >> 3) * 1024 + (r & 7) * 128 + (((j >> 3) ^ (r & 7)) << 4) + (j & 7) * 2);
-            img[byte / 2] = f2bf(v);
+        for (int g = 0; g < 8; g++)      // k = 64 kc + 8 g + i
+          for (int rb = 0; rb < 16; rb++) {  // r = 8 rb + c
+            float blk[8][8];  // [i][c]
+            for (int i = 0; i < 8; i++) {
+              const int k = 64 * kc + 8 * g + i;
+              const int n0 = 128 * nh + 8 * rb;
+              if (l == 0) {
+                for (int c = 0; c < 8; c++) blk[i][c] = k < d_in ? w0[(size_t)k * kWidth + n0 + c] : 0.f;
+              } else {
+                const float* row = w_hidden + ((size_t)(l - 1) * kWidth + k) * kWidth + n0;
+                for (int c = 0; c < 8; c++) blk[i][c] = row[c];
+              }
+            }
+            for (int c = 0; c < 8; c++) {
+              const int r = 8 * rb + c;
+              uint16_t* unit = img + ((r >> 3) * 1024 + (r & 7) * 128 + ((g ^ (r & 7)) << 4)) / 2;
+              for (int i = 0; i < 8; i++) unit[i] = f2bf(blk[i][c]);
+            }
           }
       }
   }
