@@ -91,6 +91,7 @@ struct odc_field {
   int kind;  // 0 analytic, 1 MLP
   odc_node* nodes = nullptr;
   int32_t n_nodes = 0;
+  FieldP fp{};  // the kernels' by-value view (fast-path parameters included)
   int32_t continuous = 0;
   double iso = 0.5;
   // MLP
@@ -257,7 +258,10 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
                  const int64_t* n_dev = nullptr, const int32_t* out_map = nullptr) {
   if (n == 0) return;
   if (f->kind == 0) {
-    FieldP fp{f->nodes, f->n_nodes, 0, f->iso};
+    FieldP fp = f->fp;
+    fp.nodes = f->nodes;
+    fp.n_nodes = f->n_nodes;
+    fp.iso = f->iso;
     launch_eval_raw_analytic(fp, pts, n, raw, lab, c->stream);
   } else if (f->kind == 2) {
     PointSrc src{pts, GridP{}, 0};
@@ -463,7 +467,11 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   }
   c->g = g;
   const OptP op = make_opt(o, f->continuous);
-  const FieldP fp{f->nodes, f->n_nodes, f->kind, f->iso};
+  FieldP fp = f->fp;  // analytic: nodes + fast-path parameters (odc_field_analytic)
+  fp.nodes = f->nodes;
+  fp.n_nodes = f->n_nodes;
+  fp.kind = f->kind;
+  fp.iso = f->iso;
   const bool mlp = f->kind != 0;  // fields evaluated in lock-step batches (MLP, mesh winding)
 
   DevStats* dst = need(c->arena.get<DevStats>(1));
@@ -1056,6 +1064,11 @@ int odc_field_analytic(odc_ctx* c, const odc_node* nodes, int32_t n_nodes, int32
     delete f;
     return ODC_E_CUDA;
   }
+  f->fp.nodes = f->nodes;
+  f->fp.n_nodes = n_nodes;
+  f->fp.kind = 0;
+  f->fp.iso = iso;
+  fieldp_set_fast(f->fp, nodes, n_nodes);
   *out = f;
   return ODC_OK;
 }

@@ -128,7 +128,38 @@ struct FieldP {
   int32_t n_nodes;
   int32_t kind;  // 0 analytic program, 1 MLP
   double iso;
+  // Fast paths, by value (kernel-parameter space: uniform constant-bank
+  // reads instead of per-thread global loads, which bound the label kernel
+  // on L1 throughput).  fast: 0 none (interpreter), 1 prim -> sd2raw,
+  // 2 prim -> smooth(k), 3 prim, sd2raw, prim, sd2raw, raw op fop[2].
+  int32_t fast = 0;
+  int32_t fop[3] = {0, 0, 0};
+  double fq[2][16] = {};
+  double fk = 0.0;
 };
+// host: classify a program for FieldP's fast paths (same patterns as field_raw)
+inline void fieldp_set_fast(FieldP& f, const odc_node* h, int32_t n) {
+  auto prim = [](int op) {
+    return op == ODC_OP_SPHERE_SD || op == ODC_OP_BOX_SD || op == ODC_OP_TORUS_SD || op == ODC_OP_PLANE_SD;
+  };
+  f.fast = 0;
+  if (n == 2 && prim(h[0].op) && (h[1].op == ODC_OP_SD2RAW || h[1].op == ODC_OP_SMOOTH)) {
+    f.fast = h[1].op == ODC_OP_SD2RAW ? 1 : 2;
+    f.fop[0] = h[0].op;
+    for (int i = 0; i < 16; i++) f.fq[0][i] = h[0].p[i];
+    f.fk = h[1].p[0];
+  } else if (n == 5 && prim(h[0].op) && h[1].op == ODC_OP_SD2RAW && prim(h[2].op) && h[3].op == ODC_OP_SD2RAW &&
+             (h[4].op == ODC_OP_RAW_MAX || h[4].op == ODC_OP_RAW_MIN || h[4].op == ODC_OP_RAW_DIFF)) {
+    f.fast = 3;
+    f.fop[0] = h[0].op;
+    f.fop[1] = h[2].op;
+    f.fop[2] = h[4].op;
+    for (int i = 0; i < 16; i++) {
+      f.fq[0][i] = h[0].p[i];
+      f.fq[1][i] = h[2].p[i];
+    }
+  }
+}
 
 // glibc 2.39 hypot (x86-64 baseline build): Borges' corrected sqrt kernel,
 // reproduced bit-for-bit (checked on 2e7 random pairs against libm).
@@ -175,22 +206,22 @@ __device__ __forceinline__ void rot_rows(const double l[3], const double* R, dou
 
 // signed distance of one primitive node at p (fields.py:75-139); shared by
 // the interpreter and the fast paths so both give identical bits
-__device__ __forceinline__ double prim_sd(int op, const double* __restrict__ q, const double p[3]) {
+__device__ __forceinline__ double prim_sd(int op, const double* q, const double p[3]) {
   if (op == ODC_OP_SPHERE_SD) {  // fields.py:80-82
-    double d[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
-    return __dsub_rn(norm3(d), __ldg(q + 3));
+    double d[3] = {__dsub_rn(p[0], q[0]), __dsub_rn(p[1], q[1]), __dsub_rn(p[2], q[2])};
+    return __dsub_rn(norm3(d), q[3]);
   }
   if (op == ODC_OP_BOX_SD) {  // fields.py:103-111
-    double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
-    if (__ldg(q + 6) != 0.0) {
+    double l[3] = {__dsub_rn(p[0], q[0]), __dsub_rn(p[1], q[1]), __dsub_rn(p[2], q[2])};
+    if (q[6] != 0.0) {
       double R[9], o[3];
-      for (int j = 0; j < 9; j++) R[j] = __ldg(q + 7 + j);
+      for (int j = 0; j < 9; j++) R[j] = q[7 + j];
       rot_rows(l, R, o);
       l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
     }
     double qq[3], mq[3];
     for (int a = 0; a < 3; a++) {
-      qq[a] = __dsub_rn(fabs(l[a]), __ldg(q + 3 + a));
+      qq[a] = __dsub_rn(fabs(l[a]), q[3 + a]);
       mq[a] = qq[a] > 0.0 ? qq[a] : 0.0;
     }
     const double outside = norm3(mq);
@@ -201,29 +232,47 @@ __device__ __forceinline__ double prim_sd(int op, const double* __restrict__ q, 
     return __dadd_rn(outside, inside);
   }
   if (op == ODC_OP_TORUS_SD) {  // fields.py:122-126
-    double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
-    const double ring = __dsub_rn(hypot_glibc(l[0], l[1]), __ldg(q + 3));
-    return __dsub_rn(hypot_glibc(ring, l[2]), __ldg(q + 4));
+    double l[3] = {__dsub_rn(p[0], q[0]), __dsub_rn(p[1], q[1]), __dsub_rn(p[2], q[2])};
+    const double ring = __dsub_rn(hypot_glibc(l[0], l[1]), q[3]);
+    return __dsub_rn(hypot_glibc(ring, l[2]), q[4]);
   }
   // ODC_OP_PLANE_SD, fields.py:138-139 (dgemv)
-  double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
-  double nn[3] = {__ldg(q + 3), __ldg(q + 4), __ldg(q + 5)};
+  double l[3] = {__dsub_rn(p[0], q[0]), __dsub_rn(p[1], q[1]), __dsub_rn(p[2], q[2])};
+  double nn[3] = {q[3], q[4], q[5]};
   return dot3_fma(l, nn);
 }
 // sd < 0 for one primitive.  For a box, sd = |max(q, 0)| + min(max_i q_i, 0)
 // is negative exactly when every q_i < 0 (otherwise the min term is 0 and
 // the norm is >= 0), so the label needs neither the norm nor its sqrt.
-__device__ __forceinline__ bool prim_inside(int op, const double* __restrict__ q, const double p[3]) {
+//
+// Sphere: sd = sqrt_rn(s) - r with s = (x^2 + y^2) + z^2 rounded as numpy
+// does, and sd < 0 <=> sqrt_rn(s) < r.  fma(r, r, -s) has the exact sign of
+// r^2 - s: if it is <= 0, sqrt(s) >= r and so is its rounding; if it exceeds
+// 2^-50 r^2, sqrt(s) < r by more than an ulp of r and its rounding stays
+// below r.  Only the sliver in between takes the sqrt.
+__device__ __forceinline__ bool sphere_inside(const double* q, const double p[3]) {
+  const double d[3] = {__dsub_rn(p[0], q[0]), __dsub_rn(p[1], q[1]), __dsub_rn(p[2], q[2])};
+  const double s = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
+  const double r = q[3];
+  if (r > 1e-150 && r < 1e150) {
+    const double e = fma(r, r, -s);
+    if (e <= 0.0) return false;
+    if (e > 0x1p-50 * __dmul_rn(r, r)) return true;
+  }
+  return __dsub_rn(__dsqrt_rn(s), r) < 0.0;
+}
+__device__ __forceinline__ bool prim_inside(int op, const double* q, const double p[3]) {
+  if (op == ODC_OP_SPHERE_SD) return sphere_inside(q, p);
   if (op != ODC_OP_BOX_SD) return prim_sd(op, q, p) < 0.0;
-  double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
-  if (__ldg(q + 6) != 0.0) {
+  double l[3] = {__dsub_rn(p[0], q[0]), __dsub_rn(p[1], q[1]), __dsub_rn(p[2], q[2])};
+  if (q[6] != 0.0) {
     double R[9], o[3];
-    for (int j = 0; j < 9; j++) R[j] = __ldg(q + 7 + j);
+    for (int j = 0; j < 9; j++) R[j] = q[7 + j];
     rot_rows(l, R, o);
     l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
   }
   bool in = true;
-  for (int a = 0; a < 3; a++) in &= __dsub_rn(fabs(l[a]), __ldg(q + 3 + a)) < 0.0;
+  for (int a = 0; a < 3; a++) in &= __dsub_rn(fabs(l[a]), q[3 + a]) < 0.0;
   return in;
 }
 __device__ __forceinline__ bool is_prim(int op) {
@@ -305,6 +354,22 @@ static __device__ __noinline__ double field_raw_prog(const odc_node* __restrict_
 // arithmetic as the interpreter, so identical bits; anything else runs the
 // interpreter.
 __device__ __forceinline__ double field_raw(const FieldP& f, const double p[3]) {
+  if (f.fast) {  // parameters by value: copied to registers (constant indices)
+    double q0[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) q0[i] = f.fq[0][i];
+    if (f.fast == 1) return prim_inside(f.fop[0], q0, p) ? 1.0 : 0.0;
+    if (f.fast == 2) return smooth_raw(f.fk, prim_sd(f.fop[0], q0, p));
+    double q1[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) q1[i] = f.fq[1][i];
+    const double a = prim_inside(f.fop[0], q0, p) ? 1.0 : 0.0;
+    double b = prim_inside(f.fop[1], q1, p) ? 1.0 : 0.0;
+    if (f.fop[2] == ODC_OP_RAW_MAX) return (a >= b) ? a : b;
+    if (f.fop[2] == ODC_OP_RAW_MIN) return (a <= b) ? a : b;
+    b = __dsub_rn(1.0, b);
+    return (a <= b) ? a : b;
+  }
   const odc_node* nd = f.nodes;
   if (f.n_nodes == 2) {
     const int op0 = __ldg(&nd[0].op), op1 = __ldg(&nd[1].op);

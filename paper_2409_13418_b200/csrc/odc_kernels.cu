@@ -52,12 +52,13 @@ __device__ __forceinline__ void warp_max_nonneg_double(unsigned long long* p, do
 // K1: grid labels (grid.py:109-126).  One thread per (row, x) bit, ballot
 // packs 32 consecutive x into one word.  label = raw > iso (fields.py:47).
 // ===========================================================================
+// Grid: blockIdx.x = label row (z, y) of the window, blockIdx.y = 256-bit
+// chunk of the row -- the row's coordinates are block-uniform, so no
+// per-thread division.
 __global__ void __launch_bounds__(256) k_labels_analytic(GridP g, FieldP f, uint32_t* __restrict__ L) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t rowbits = g.W * 32;
-  const int64_t row = idiv(gid, rowbits);  // window-local row
-  if (row >= g.nz * g.S) return;      // whole warps (rowbits is a multiple of 32)
-  const int64_t x = gid - row * rowbits;
+  const int64_t row = blockIdx.x;  // window-local row
+  const int64_t x = (int64_t)blockIdx.y * 256 + threadIdx.x;
+  if (x >= g.W * 32) return;  // whole warps (the row's bit count is a multiple of 32)
   const int64_t y = imod(row, g.S), z = g.z0 + idiv(row, g.S);
   uint32_t lab = 0;
   if (x < g.S) {
@@ -69,8 +70,8 @@ __global__ void __launch_bounds__(256) k_labels_analytic(GridP g, FieldP f, uint
 }
 
 void launch_labels_analytic(const GridP& g, const FieldP& f, uint32_t* L, cudaStream_t s) {
-  int64_t n = g.nz * g.S * g.W * 32;
-  k_labels_analytic<<<grid_for(n, 256), 256, 0, s>>>(g, f, L);
+  const int64_t rows = g.nz * g.S;
+  if (rows) k_labels_analytic<<<dim3((unsigned)rows, grid_for(g.W * 32, 256)), 256, 0, s>>>(g, f, L);
 }
 
 // one warp per label row: lane j of word w reads byte 32 w + j (coalesced),

@@ -39,6 +39,25 @@ def test_sphere_labels_basic():
     assert eval_labels(f, (0.99, 0.5, 0.5)) == 0
 
 
+def test_sphere_labels_at_the_surface_match_the_oracle():
+    """Points within a few ulps of a sphere: the device decides most labels
+    from the exact sign of r^2 - s and takes the sqrt only in a thin band;
+    every label must equal the oracle's sqrt(s) - r < 0 (fields.py:80-82)."""
+    import oracle
+
+    rng = np.random.default_rng(5)
+    for c, r in (((0.5, 0.5, 0.5), 0.3), ((0.1, -0.2, 0.3), 1.0 / 3.0), ((0.0, 0.0, 0.0), 0.7071067811865476)):
+        u = rng.normal(size=(200_000, 3))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        rad = r + rng.integers(-6, 7, size=len(u)) * np.spacing(r) * rng.uniform(0, 1, size=len(u))
+        pts = np.asarray(c) + u * rad[:, None]
+        f = SphereField(c, r)
+        expect = (oracle.eval_raw_program(f, pts) > 0.5).astype(np.uint8)
+        got = eval_labels(f, pts)
+        assert 0 < expect.sum() < len(pts)
+        assert np.array_equal(got, expect)
+
+
 def test_union_is_max_of_children():
     a = SphereField((0.3, 0.5, 0.5), 0.1)
     b = SphereField((0.7, 0.5, 0.5), 0.1)
