@@ -137,6 +137,7 @@ struct odc_ctx {
   // 1 SIMT reference
   int mlp_impl = 3;
   int mlp_debug = 0;  // odc_set_param("mlp_debug"): profiling experiments, odc_profile_mlp only
+  const double* profile_pts = nullptr;  // odc_set_param("profile_points"): host (n,3) points for odc_profile_mlp
   // last extraction
   bool valid = false;
   GridP g{};
@@ -218,9 +219,11 @@ void run_mlp(odc_ctx* c, const odc_field* f, const PointSrc& src, int64_t n, uin
   if (!override_md) md.impl = c->mlp_impl;
   unsigned long long base0 = 0;
   md.sched = src.n_dev ? c->d_sched + 1 : c->d_sched;
-  if (mlp_eval(md, src, n, lab, raw, s, src.n_dev ? &base0 : &c->sched_next) != 0)
+  const int k = mlp_eval(md, src, n, lab, raw, s, src.n_dev ? &base0 : &c->sched_next);
+  if (k < 0)
     throw OdcError{ODC_E_CUDA, "MLP evaluator: no pair counter on this context, or a compacted batch on an "
                                "evaluator other than mlp_impl 3"};
+  if (k > 1) c->launches += k - 1;  // the caller's check_launch counts one
 }
 
 // Evaluate labels (and optionally raw) of n points through the field.
@@ -775,8 +778,22 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       int64_t* cnt2 = compact ? need(c->arena.get<int64_t>(2)) : nullptr;
       bool packed = false;  // this step's points are compacted
       for (int step = 0; step < nsteps; step++) {
+        static const bool dbg_t = getenv("ODC_DEBUG_STEPS") != nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (dbg_t) {
+          cudaEventCreate(&e0);
+          cudaEventCreate(&e1);
+          cudaEventRecord(e0, s);
+        }
         if (packed) eval_points(c, f, pts, M, lab, nullptr, cnt2 + (step & 1), map);
         else eval_points(c, f, pts, M, lab, nullptr);
+        if (dbg_t) {
+          cudaEventRecord(e1, s);
+          cudaEventSynchronize(e1);
+          float ms = 0;
+          cudaEventElapsedTime(&ms, e0, e1);
+          fprintf(stderr, "step %d M %lld mlp %.3f ms\n", step, (long long)M, ms);
+        }
         if (step + 1 < nsteps) {  // update + the next step's points in one pass
           const bool was = packed;
           // the first step of each linear scan still has every instance scanning
@@ -1011,6 +1028,10 @@ int odc_set_param(odc_ctx* c, const char* name, int64_t value) {
   if (!c || !name) return ODC_E_ARG;
   if (std::strcmp(name, "mlp_debug") == 0 && value >= 0 && value <= 255) {
     c->mlp_debug = (int)value;
+    return ODC_OK;
+  }
+  if (std::strcmp(name, "profile_points") == 0) {  // profiling only: a host pointer, 0 = generated grid points
+    c->profile_pts = (const double*)(intptr_t)value;
     return ODC_OK;
   }
   if (std::strcmp(name, "mlp_impl") == 0 && value >= 0 && value <= 3) {
@@ -1970,10 +1991,11 @@ int odc_profile_mlp(odc_ctx* c, const odc_field* f, int64_t n, int64_t* trace, i
   md.trace = (c->mlp_debug & 64) ? nullptr : dt;  // 64: time the kernel without the trace hooks
   const int64_t np = n < g.S3 ? n : g.S3;
   PointSrc src{nullptr, g, 0};
-  if (c->mlp_debug & 128) {  // 128: the same vertices as explicit points (the search batches' path)
+  if (c->mlp_debug & 128) {  // 128: explicit points (the search batches' path): the grid's, or the caller's
     double* pts = c->arena.get<double>(3 * np);
     if (!pts) return ODC_E_NOMEM;
-    launch_grid_points(g, 0, np, pts, c->stream);
+    if (c->profile_pts) cudaMemcpyAsync(pts, c->profile_pts, 24 * np, cudaMemcpyHostToDevice, c->stream);
+    else launch_grid_points(g, 0, np, pts, c->stream);
     src.pts = pts;
   }
   cudaEventRecord(c->ev0, c->stream);

@@ -281,15 +281,50 @@ __device__ __forceinline__ void grid_coords_fast(const PointSrc& src, int64_t p,
 }
 // fp64 prior + logistic of one point from its fp32 head dot product
 // (paper_2409_13418_b200/fields.py MlpField); p < 0 or p >= n: nothing to do
+// fp64 label/raw of point p from its fp32 head dot (the reference's
+// expression: sigma(A * mlp - P * (|p - c| - R)), fields.py/MlpField)
+__device__ __forceinline__ void label_fp64(const MlpDev& m, const PointSrc& src, int64_t p, int64_t o, float dot,
+                                           uint8_t* __restrict__ labels, double* __restrict__ raw) {
+  const double mlp = (double)(dot + m.b_head);
+  double pt[3];
+  point_of(src, p, pt);
+  const double d[3] = {pt[0] - m.prior_center[0], pt[1] - m.prior_center[1], pt[2] - m.prior_center[2]};
+  const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+  const double logit = m.amplitude * mlp - m.prior_scale * (dist - m.prior_radius);
+  if (!raw) {
+    // the label of sigma(logit) > 1/2 without exp and the division: logit
+    // <= 0 gives exp(-logit) >= 1, 1 + e >= 2 and sigma <= 1/2; logit >
+    // 1e-12 keeps exp(-logit) thousands of ulps below 1, so 1 + e rounds
+    // below 2 and sigma > 1/2.  Only the sliver in between (and NaN) takes
+    // the full expression.
+    if (logit <= 0.0) {
+      labels[o] = 0;
+      return;
+    }
+    if (logit > 1e-12) {
+      labels[o] = 1;
+      return;
+    }
+  }
+  const double rv = 1.0 / (1.0 + exp(-logit));
+  labels[o] = rv > 0.5 ? 1 : 0;
+  if (raw) raw[o] = rv;
+}
+
+// Label (and raw) of point p from its fp32 head dot.  Labels only: the sign
+// of the logit in fp32.  Against the fp64 logit (same fp32 dot), each fp32
+// step rounds within a few ulps of its operand (parameters rounded to fp32
+// included), |error| < 4 * 2^-24 * M with M = |A * mlp| + P * (dist + R +
+// |x|_1 + |c|_1), so a margin of 1e-6 * M (about 4x that) decides exactly.  Closer points take the fp64 expression -- inline, or, with
+// src.defer_dot (CTA-pair evaluator), deferred: label 2 and the dot are
+// written and k_mlp_fixup finishes them after the launch, keeping fp64
+// latency out of the epilogue (search points sit near the surface, where
+// this case is common).
 __device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& src, int64_t n, int64_t p, float dot,
                                              uint8_t* __restrict__ labels, double* __restrict__ raw) {
   if (p < 0 || p >= n) return;
   const int64_t o = src.out_map ? (int64_t)src.out_map[p] : p;  // output slot
   if (!raw) {
-    // labels only: the sign of the logit in fp32 (short dependent chains
-    // instead of fp64 divide / sqrt / exp).  Its error is < 1e-4 for these
-    // magnitudes, so a margin of 1e-3 decides exactly; anything closer takes
-    // the fp64 path below.
     float xf[3];
     if (src.pts) {
 #pragma unroll
@@ -314,21 +349,32 @@ __device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& sr
       const float x = xf[a] - (float)m.prior_center[a];
       d2 = fmaf(x, x, d2);
     }
-    const float lg = (float)m.amplitude * (dot + m.b_head) - (float)m.prior_scale * (sqrtf(d2) - (float)m.prior_radius);
-    if (fabsf(lg) > 1e-3f) {
+    const float am = (float)m.amplitude * (dot + m.b_head), dist = sqrtf(d2);
+    const float ps = (float)m.prior_scale, pr = (float)m.prior_radius;
+    const float lg = am - ps * (dist - pr);
+    const float mag = fabsf(am) + fabsf(ps) * (dist + fabsf(pr) + fabsf(xf[0]) + fabsf(xf[1]) + fabsf(xf[2]) +
+                                               fabsf((float)m.prior_center[0]) + fabsf((float)m.prior_center[1]) +
+                                               fabsf((float)m.prior_center[2]));
+    if ((fabsf(lg) > 1e-6f * mag + 1e-30f && !(m.debug & 4)) || (m.debug & 16)) {  // debug 16 / 4: timing only
       labels[o] = lg > 0.f ? 1 : 0;
       return;
     }
+    if (src.defer_dot) {
+      labels[o] = 2;
+      src.defer_dot[p] = dot;
+      return;
+    }
   }
-  const double mlp = (double)(dot + m.b_head);
-  double pt[3];
-  point_of(src, p, pt);
-  const double d[3] = {pt[0] - m.prior_center[0], pt[1] - m.prior_center[1], pt[2] - m.prior_center[2]};
-  const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
-  const double logit = m.amplitude * mlp - m.prior_scale * (dist - m.prior_radius);
-  const double rv = 1.0 / (1.0 + exp(-logit));
-  labels[o] = rv > 0.5 ? 1 : 0;
-  if (raw) raw[o] = rv;
+  label_fp64(m, src, p, o, dot, labels, raw);
+}
+
+// the deferred labels of one launch (finish_label with src.defer_dot)
+__global__ void k_mlp_fixup(MlpDev m, PointSrc src, int64_t n_launch, uint8_t* __restrict__ labels) {
+  const int64_t n = src.n_dev ? *src.n_dev : n_launch;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t o = src.out_map ? (int64_t)src.out_map[p] : p;
+  if (labels[o] == 2) label_fp64(m, src, p, o, src.defer_dot[p], labels, nullptr);
 }
 
 template <bool kBias, bool kTrace>
@@ -1032,7 +1078,8 @@ constexpr int kSched = 4;  // pair-index ring depth (dynamic schedule)
 constexpr uint32_t kSchedReaders = 23;  // warps that read each slot: 12 in the leader, 11 in the peer
 constexpr uint32_t kBarW = 2;              // named barriers 2..7: weight stage s ready
 constexpr uint32_t kBarA = kBarW + kStages;  // 8..9: A(t) ready
-static_assert(kBarA + 2 <= 16, "named barriers");
+constexpr uint32_t kBarX = kBarA + 2;        // 10: the label exchange's s_part was read
+static_assert(kBarX + 1 <= 16, "named barriers");
 __device__ __forceinline__ void umma_ss2(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -1314,11 +1361,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc4::kThreads, 1)
     // the critical path.  dot = partial(cols 0..127) + partial(cols 128..255).
     int64_t p_prev = -1;
     float part_prev[2] = {0.f, 0.f};
+    // tile t's labels are finished by column half t (the other half hands its
+    // partial over), so each warp finishes one label per pair.  The second
+    // barrier only waits for the finisher's read of s_part (bar.arrive), not
+    // for its label.  fp32 addition commutes: dot = d0 + d1 either way.
     auto finish_tile = [&](int t) {
-      if (hc == 1) s_part[r] = part_prev[t];
+      if (hc != t) s_part[r] = part_prev[t];
       named_bar_sync(1, 256);
-      if (hc == 0) finish_label(m, src, n, p_prev + 256 * t, part_prev[t] + s_part[r], labels, raw);
-      named_bar_sync(1, 256);  // s_part reusable
+      float dot = 0.f;
+      if (hc == t) {
+        dot = t == 0 ? part_prev[0] + s_part[r] : s_part[r] + part_prev[1];
+        named_bar_arrive(tc4::kBarX, 256);  // s_part read
+        finish_label(m, src, n, p_prev + 256 * t, dot, labels, raw);
+      } else {
+        named_bar_sync(tc4::kBarX, 256);  // s_part reusable
+      }
     };
     const bool tr = r == 0 && crank == 0 && hc == 0;
     int64_t pr = sched_get(0);
@@ -1477,12 +1534,25 @@ int mlp_eval(const MlpDev& m_in, const PointSrc& src, int64_t n, uint8_t* labels
         cudaGetLastError();
       }
     }
+    // labels of explicit (search) points: undecided fp32 labels are finished
+    // by k_mlp_fixup after the launch (stream-ordered scratch for their
+    // dots).  Grid points rarely sit within the margin of the surface, so
+    // the grid pass keeps the inline fp64 path and needs no scratch.
+    float* defer = nullptr;
+    if (!raw && src.pts) {
+      if (cudaMallocAsync((void**)&defer, sizeof(float) * n, s) == cudaSuccess) sp.defer_dot = defer;
+      else cudaGetLastError();
+    }
     if (m.has_bias)
       k_mlp_tc4<true><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, sp, n, labels, raw);
     else
       k_mlp_tc4<false><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, sp, n, labels, raw);
+    if (defer) {
+      k_mlp_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(m, sp, n, labels);
+      cudaFreeAsync(defer, s);
+    }
     if (tab) cudaFreeAsync(tab, s);
-    return 0;
+    return 1 + (defer ? 1 : 0) + (tab ? 1 : 0);  // kernels launched
   }
   if (m.impl == 0 && m.w_tc2 != nullptr) {
     const int64_t pairs = (g_num_sms / 2) < ntiles ? (g_num_sms / 2) : ntiles;

@@ -52,6 +52,9 @@ struct PointSrc {
   // to out_map[i]
   const int64_t* n_dev;
   const int32_t* out_map;
+  // set by mlp_eval (impl 3, labels only): fp32-undecided labels are written
+  // as 2 with their head dot here, and finished in fp64 by k_mlp_fixup
+  float* defer_dot;
 };
 
 size_t mlp_packed_weight_elems();
@@ -64,7 +67,9 @@ void mlp_pack_weights(const float* w0, int d_in, const float* w_hidden, uint16_t
 
 // labels (u8) and optionally raw = sigmoid(logit) (f64) for n points
 // impl 3 needs m.sched and sched_next (the host copy of the counter's value
-// at the next launch, advanced here); returns nonzero when they are missing
+// at the next launch, advanced here).  Returns the number of kernels it
+// launched (0 for n == 0), negative when the counter is missing or a
+// compacted batch meets another evaluator.
 int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s,
              unsigned long long* sched_next = nullptr);
 const char* mlp_kernel_name();

@@ -16,7 +16,7 @@ tr = np.zeros(2048, dtype=np.int64)
 dbg = int(sys.argv[1]) if len(sys.argv) > 1 else 192  # 64 no trace | 128 explicit points
 with DeviceField(ctx, MlpField()) as f:
     L.odc_set_param(ctx.handle, b"mlp_debug", dbg)
-    for _ in range(30):  # heat up to the sustained state
+    for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 30):  # heat up to the sustained state
         L.odc_profile_mlp(ctx.handle, f.handle, 8_000_000, tr.ctypes.data, len(tr))
     res = {}
     for n in (37_888, 297_647, 595_294, 1_190_588, 2_381_176, 8_000_000):
