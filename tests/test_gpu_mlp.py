@@ -68,3 +68,31 @@ def test_tc_batch_invariance(impl):
     assert np.array_equal(full, part)
     rev = device_raw(field, pts[::-1].copy(), impl)[::-1]
     assert np.array_equal(full, rev)
+
+
+@pytest.mark.parametrize("impl", [2, 3])
+def test_labels_fast_path_equals_fp64(impl):
+    """Labels-only evaluation decides most labels in fp32 within a margin
+    derived from the fp32 rounding bound, and finishes the rest in fp64
+    (deferred to a fix-up kernel on the CTA-pair evaluator).  Every label
+    must equal the fp64 expression's (raw > 1/2), on random points and on
+    points at the surface, where the fp32 test is most often undecided."""
+    from paper_2409_13418_b200 import GridSpec, contour, eval_labels
+
+    field = MlpField(seed=0, amplitude=1.0)
+    mesh = contour(field, GridSpec((0, 0, 0), (1, 1, 1), 64)).mesh
+    rng = np.random.default_rng(11)
+    near = mesh.vertices[rng.integers(0, mesh.n_vertices, 400_000)]
+    near = near + rng.normal(scale=1e-7, size=near.shape)
+    pts = np.concatenate([near, rng.uniform(0, 1, size=(400_000, 3))])
+    ctx = _lib.Context(0)
+    L = _lib.load()
+    assert L.odc_set_param(ctx.handle, b"mlp_impl", impl) == 0
+    lab = np.empty(len(pts), dtype=np.uint8)
+    raw = np.empty(len(pts))
+    pts = np.ascontiguousarray(pts)
+    with DeviceField(ctx, field) as f:
+        assert L.odc_eval_labels(ctx.handle, f.handle, pts.ctypes.data, len(pts), lab.ctypes.data) == 0
+        assert L.odc_eval_raw(ctx.handle, f.handle, pts.ctypes.data, len(pts), raw.ctypes.data) == 0
+    assert np.array_equal(lab, (raw > 0.5).astype(np.uint8))
+    assert 0.1 < lab[:400_000].mean() < 0.9  # the near set straddles the surface
