@@ -22,7 +22,9 @@ struct MlpDev {
   const uint16_t* w_tc;      // 58 chunks of 128x64 bf16 in the UMMA SWIZZLE_128B smem image (odc_mlp_tc.cuh)
   const uint16_t* w_tc2;     // the same chunks split into two 64-row halves (odc_mlp_tc2.cuh)
   int impl;                  // 3 = CTA-pair N=256 (default), 2 = single-CTA, 0 = CTA-pair TS, 1 = SIMT
-  int debug;                 // profiling only (odc_profile_mlp): 1 no weight refills, 2 no A stores, 4 no TMEM loads
+  int debug;                 // timing experiments, odc_profile_mlp only (results are wrong): impl 3 --
+                             // 1 no weight refills after the first ring, 8 static round-robin schedule,
+                             // 4 every label through fp64, 16 every label decided in fp32
   int has_bias;              // any non-zero bias (selects the bias-add epilogue)
   unsigned long long* trace; // profiling: event timeline of CTA 0 (nullptr = off)
   // impl 3 dynamic pair schedule: a per-context device counter that only
