@@ -54,21 +54,26 @@ __device__ __forceinline__ void block_exscan(const uint32_t (&v)[NCH], uint32_t 
 }
 
 // Single-block exclusive scan of tile sums (NCH channels laid out [c][ntiles]);
-// writes offsets in place and the 64-bit totals.
+// writes offsets in place and the 64-bit totals.  Each thread owns kPer
+// consecutive tiles per round (a serial sum in registers), so a round of
+// 1024 threads covers 8 K tiles and the block-wide steps run 8x less often.
 template <int NCH>
 __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t* sums, int64_t ntiles, unsigned long long* totals) {
+  constexpr int kPer = 8;
   __shared__ unsigned long long carry[NCH];
   __shared__ unsigned long long wpart[NCH][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x < NCH) carry[threadIdx.x] = 0;
   __syncthreads();
-  for (int64_t base = 0; base < ntiles; base += 1024) {
-    int64_t i = base + threadIdx.x;
-    unsigned long long v[NCH], x[NCH];
+  for (int64_t base = 0; base < ntiles; base += 1024 * kPer) {
+    const int64_t i0 = base + (int64_t)threadIdx.x * kPer;
+    unsigned long long tot[NCH], x[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; c++) {
-      v[c] = i < ntiles ? sums[c * ntiles + i] : 0ull;
-      x[c] = v[c];
+      tot[c] = 0;
+#pragma unroll
+      for (int k = 0; k < kPer; k++) tot[c] += i0 + k < ntiles ? sums[c * ntiles + i0 + k] : 0u;
+      x[c] = tot[c];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         unsigned long long y = __shfl_up_sync(0xffffffffu, x[c], o);
@@ -92,8 +97,15 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t* sums, int64_t nti
     __syncthreads();
 #pragma unroll
     for (int c = 0; c < NCH; c++) {
-      unsigned long long before = (wid == 0 ? 0ull : wpart[c][wid - 1]) + carry[c];
-      if (i < ntiles) sums[c * ntiles + i] = (uint32_t)(before + x[c] - v[c]);
+      unsigned long long run = (wid == 0 ? 0ull : wpart[c][wid - 1]) + carry[c] + x[c] - tot[c];
+#pragma unroll
+      for (int k = 0; k < kPer; k++) {
+        if (i0 + k < ntiles) {
+          const uint32_t v = sums[c * ntiles + i0 + k];
+          sums[c * ntiles + i0 + k] = (uint32_t)run;
+          run += v;
+        }
+      }
     }
     __syncthreads();
     if (threadIdx.x < NCH) carry[threadIdx.x] += wpart[threadIdx.x][31];
