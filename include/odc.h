@@ -151,7 +151,10 @@ const char* odc_last_error(const odc_ctx* ctx);
 int odc_set_stream(odc_ctx* ctx, void* stream);
 /* tuning/testing knobs: "mlp_impl" = 3 CTA-pair N=256 tile ping-pong tcgen05
  * evaluator (default), 2 single-CTA tcgen05, 0 CTA-pair with A in TMEM, 1 SIMT
- * reference evaluator (same math, CUDA cores) */
+ * reference evaluator (same math, CUDA cores).  Profiling only (they affect
+ * odc_profile_mlp, never an extraction): "mlp_debug" = timing-experiment
+ * bits, "profile_points" = a host pointer to (n, 3) f64 points that
+ * odc_profile_mlp evaluates with mlp_debug bit 128 (0 = grid points). */
 int odc_set_param(odc_ctx* ctx, const char* name, int64_t value);
 
 int odc_field_analytic(odc_ctx* ctx, const odc_node* nodes, int32_t n_nodes, int32_t continuous,
