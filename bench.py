@@ -311,6 +311,15 @@ def run_gpu(args, rank, world, dist):
             roof["traffic"] = json.loads(prof.read_text()).get(args.workload)
         except Exception:
             pass
+    # context from the committed ncu capture of the same kernel: the tensor
+    # pipe's active fraction (the utilisation behind frac > 1 against the
+    # power-capped cuBLAS figure)
+    met = REPO / "profiles" / "ncu_metrics.json"
+    if met.exists():
+        try:
+            roof.update(json.loads(met.read_text()).get(args.workload, {}))
+        except Exception:
+            pass
 
     if rank != 0:
         return
