@@ -1066,6 +1066,20 @@ __device__ __forceinline__ void pe_piece(const PointSrc& src, int64_t n, int64_t
 // B reads 128 KB, weight copies 64 KB, activation stores 128 KB of shared
 // memory traffic for 4,096 MMA cycles (tc1: 768 KB), so the tensor pipe,
 // not shared memory, sets the pace.
+//
+// Synchronisation rules that the measurements forced:
+// * the MMA issuer waits only on named barriers (an mbarrier poll there
+//   stalls the tensor pipe ~180 cycles); helper warps turn mbarrier phases
+//   into bar.arrive;
+// * no epilogue warp issues a release.cluster arrive (MEMBAR.ALL.GPU +
+//   ERRBAR, ~1,000 cycles): CTA-scope arrives, and the peer's warp 1
+//   forwards them with one relaxed remote arrive;
+// * pairs come from a device counter through a 4-slot ring (dynamic
+//   schedule), the leader's copy by st.async + complete_tx;
+// * at the pair boundary the epilogue is the critical path: the next pair's
+//   encoding goes in before the head, the head's weights are kernel
+//   parameters, and labels are finished in the slack of layers 2 and 3
+//   (fp32-undecided ones deferred to k_mlp_fixup for search batches).
 // ===========================================================================
 namespace tc4 {
 constexpr int kThreads = 384;
