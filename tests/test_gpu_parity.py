@@ -225,3 +225,21 @@ def test_gpu_mlp_determinism_repeated():
         assert np.array_equal(r.mesh.vertices, ref.mesh.vertices)
         assert np.array_equal(r.mesh.triangles, ref.mesh.triangles)
         assert np.array_equal(r.raw_mesh.triangles, ref.raw_mesh.triangles)
+
+
+def test_gpu_copy_mesh_pair_matches_single_copies():
+    """odc_copy_mesh_pair (one pipelined transfer of the repaired mesh and the
+    raw mesh's triangles) returns exactly what two odc_copy_mesh calls do."""
+    from paper_2409_13418_b200 import _lib
+    from paper_2409_13418_b200.pipeline import _copy_mesh
+
+    field = MlpField(seed=0, amplitude=4.0)
+    res, ctx, st = contour(field, GridSpec((0, 0, 0), (1, 1, 1), 48), return_context=True)
+    assert st.repair_added_vertices > 0  # the raw mesh differs from the repaired one
+    m = _copy_mesh(ctx, 0, st, True)
+    raw = _copy_mesh(ctx, 1, st, True)
+    for a, b in ((res.mesh.vertices, m.vertices), (res.mesh.triangles, m.triangles),
+                 (res.mesh.provenance_kind, m.provenance_kind), (res.mesh.provenance_ref, m.provenance_ref),
+                 (res.raw_mesh.triangles, raw.triangles), (res.raw_mesh.vertices, raw.vertices)):
+        assert np.array_equal(a, b)
+    _lib.check(0)
