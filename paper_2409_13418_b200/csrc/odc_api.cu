@@ -778,22 +778,8 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       int64_t* cnt2 = compact ? need(c->arena.get<int64_t>(2)) : nullptr;
       bool packed = false;  // this step's points are compacted
       for (int step = 0; step < nsteps; step++) {
-        static const bool dbg_t = getenv("ODC_DEBUG_STEPS") != nullptr;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (dbg_t) {
-          cudaEventCreate(&e0);
-          cudaEventCreate(&e1);
-          cudaEventRecord(e0, s);
-        }
         if (packed) eval_points(c, f, pts, M, lab, nullptr, cnt2 + (step & 1), map);
         else eval_points(c, f, pts, M, lab, nullptr);
-        if (dbg_t) {
-          cudaEventRecord(e1, s);
-          cudaEventSynchronize(e1);
-          float ms = 0;
-          cudaEventElapsedTime(&ms, e0, e1);
-          fprintf(stderr, "step %d M %lld mlp %.3f ms\n", step, (long long)M, ms);
-        }
         if (step + 1 < nsteps) {  // update + the next step's points in one pass
           const bool was = packed;
           // the first step of each linear scan still has every instance scanning
