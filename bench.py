@@ -467,7 +467,7 @@ def run_gpu_slabs(args, rank, world, dist):
 
     from paper_2409_13418_b200 import GridSpec
     from paper_2409_13418_b200.fields import is_mlp
-    from paper_2409_13418_b200.slab import contour_slab, slab_ranges
+    from paper_2409_13418_b200.slab import balanced_slab_ranges, contour_slab
 
     device = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(device)
@@ -545,7 +545,7 @@ def run_gpu_slabs(args, rank, world, dist):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16+f64" if is_mlp(field) else "f64", "data": "synthetic",
         "config": {"workload": desc, "R": R, "cells": R**3, "parallelism": f"z-slabs x{world}",
-                   "slabs": slab_ranges(R, world),
+                   "slabs": balanced_slab_ranges(field, grid, world, device),
                    "l2": "flushed (512 MiB write) before every step, outside its CUDA-event pair"},
         "e2e": {"value": R**3 / (e2e_step / 1e3), "unit": "cells/s", "ms_per_step": e2e_step,
                 "api": "paper_2409_13418_b200.slab.contour_slab(field, GridSpec, rank, world) -> TriangleMesh on rank 0",

@@ -153,3 +153,27 @@ def test_gpu_slabs_mlp_repair():
     assert ref.stats["repair_added_vertices"] > 0
     assert np.array_equal(mesh.triangles, ref.mesh.triangles)
     assert np.array_equal(mesh.vertices, ref.mesh.vertices)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 7])
+def test_gpu_balanced_slabs_equal_single_extraction(world):
+    """Work-balanced slab bounds (a coarse device probe of the crossing
+    density per z) are a valid partition, give thinner slabs where the
+    surface is, and reproduce the single-extraction mesh exactly."""
+    from paper_2409_13418_b200 import GridSpec, MlpField, contour
+    from paper_2409_13418_b200.slab import balanced_slab_ranges, contour_slabs_serial
+
+    field = MlpField(seed=0, amplitude=2.0)
+    g = GridSpec((0, 0, 0), (1, 1, 1), 64)
+    ranges = balanced_slab_ranges(field, g, world)
+    assert ranges[0][0] == 0 and ranges[-1][1] == 64
+    assert all(a < b for a, b in ranges) and all(ranges[k][1] == ranges[k + 1][0] for k in range(world - 1))
+    assert ranges == balanced_slab_ranges(field, g, world)  # deterministic: every rank agrees
+    if world == 4:  # the sphere-like surface sits in the middle: the middle slabs are thinner
+        widths = [b - a for a, b in ranges]
+        assert widths[0] > widths[1] and widths[3] > widths[2]
+    ref = contour(field, g)
+    mesh, pieces, rows = contour_slabs_serial(field, g, world, ranges=ranges)
+    assert np.array_equal(mesh.triangles, ref.mesh.triangles)
+    assert np.array_equal(mesh.vertices, ref.mesh.vertices)
