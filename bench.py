@@ -170,7 +170,7 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": value, "unit": "cells/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def estimate_mlp_evals(R):
@@ -348,7 +348,7 @@ def run_gpu(args, rank, world, dist):
         "wall_s_timed_region": t_wall,
         "mesh": {**stats_snapshot, **stats_checks},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_gpu_batch(args, rank, world, dist):
@@ -454,7 +454,7 @@ def run_gpu_batch(args, rank, world, dist):
                 "api": "paper_2409_13418_b200.batch.contour_batch(jobs) -> [ContourResult]"},
         "roofline": None, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clock,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_gpu_slabs(args, rank, world, dist):
@@ -552,7 +552,27 @@ def run_gpu_slabs(args, rank, world, dist):
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": roof, "cpu_baseline": None, "gpu_launches": launches, "clocks": clock,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
+def _protect_stdout():
+    """Libraries print to fd 1 (NCCL's version banner on init, for one): keep
+    the original stdout for the JSON line and send everything else written to
+    fd 1 to stderr, so stdout carries exactly one line."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
 
 
 def main():
@@ -568,6 +588,7 @@ def main():
     ap.add_argument("--batch-workers", type=int, default=8)
     ap.add_argument("--slabs", action="store_true", help="use the z-slab path even on one rank (testing)")
     args = ap.parse_args()
+    _protect_stdout()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist = None

@@ -55,7 +55,7 @@ WORK_PER_CROSSING_MLP = 130.0
 WORK_PER_CROSSING_ANALYTIC = 300.0
 
 
-def layer_work(field, grid, device=0, nxy=17, nz_max=129):
+def layer_work(field, grid, device=0, nxy=17, nz_max=129, dfield=None):
     """Estimated work of every cell layer, in grid-pass evaluations: S^2
     vertices per layer plus WORK_PER_CROSSING_* per crossing edge.
     Crossings per layer come from a coarse probe (nxy^2 points on up to
@@ -78,7 +78,14 @@ def layer_work(field, grid, device=0, nxy=17, nz_max=129):
     ys = np.linspace(lo[1], hi[1], nxy)
     zz = lo[2] + zi * h[2]
     Z, Y, X = np.meshgrid(zz, ys, xs, indexing="ij")
-    lab = eval_labels(field, np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1), device=device)
+    pts = np.ascontiguousarray(np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1))
+    if dfield is not None:  # the caller's upload (contour_slab): no second field upload
+        lab = np.empty(len(pts), dtype=np.uint8)
+        ctx = _lib.context(device)
+        _lib.check(_lib.load().odc_eval_labels(ctx.handle, dfield.handle, pts.ctypes.data, len(pts),
+                                               lab.ctypes.data), ctx.handle)
+    else:
+        lab = eval_labels(field, pts, device=device)
     lab = lab.reshape(len(zi), nxy, nxy)
     cx = (lab[:, :, 1:] != lab[:, :, :-1]).sum(axis=(1, 2)).astype(np.float64)
     cy = (lab[:, 1:, :] != lab[:, :-1, :]).sum(axis=(1, 2)).astype(np.float64)
@@ -97,7 +104,7 @@ def layer_work(field, grid, device=0, nxy=17, nz_max=129):
     return work
 
 
-def balanced_slab_ranges(field, grid, world, device=0):
+def balanced_slab_ranges(field, grid, world, device=0, dfield=None):
     """Owned cell layers [c0, c1) of every rank, split so that the estimated
     work (layer_work) is equal: a surface concentrated in the middle z-range
     otherwise leaves the outer slabs idle (a centred sphere-like surface:
@@ -107,7 +114,7 @@ def balanced_slab_ranges(field, grid, world, device=0):
         raise ValueError(f"cannot split {R} cell layers over {world} ranks")
     if world == 1:
         return [(0, R)]
-    w = layer_work(field, grid, device)
+    w = layer_work(field, grid, device, dfield=dfield)
     cum = np.concatenate([[0.0], np.cumsum(w)])
     b = [0]
     for k in range(1, world):
@@ -164,8 +171,11 @@ def _dev(torch, ptr, shape, typestr, device):
     return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=device).clone()
 
 
-def extract_piece(field, grid, options, c0, c1, device=0):
-    """Run libodc's slab extraction for owned cell layers [c0, c1)."""
+def extract_piece(field, grid, options, c0, c1, device=0, dfield=None):
+    """Run libodc's slab extraction for owned cell layers [c0, c1)
+    (``dfield``: an already uploaded DeviceField on this thread's context)."""
+    import contextlib
+
     import torch
 
     from .pipeline import DeviceField, _grid_args, _raise, make_options
@@ -176,7 +186,7 @@ def extract_piece(field, grid, options, c0, c1, device=0):
     info = _lib.SlabInfo()
     lo, hi, R = _grid_args(grid)
     o = make_options(options)
-    with DeviceField(ctx, field) as df:
+    with (contextlib.nullcontext(dfield) if dfield is not None else DeviceField(ctx, field)) as df:
         rc = L.odc_extract_slab(ctx.handle, df.handle, lo, hi, R, ctypes.byref(o), int(c0), int(c1), ctypes.byref(st),
                                 ctypes.byref(info))
         if rc != _lib.ODC_OK:
@@ -300,8 +310,11 @@ def contour_slab(field, grid, options=None, *, rank, world, dist, device=0, to_h
     options = options or ContourOptions()
     options.validate()
     t0 = time.perf_counter()
-    c0, c1 = balanced_slab_ranges(field, grid, world, device)[rank]
-    piece, ctx = extract_piece(field, grid, options, c0, c1, device)
+    from .pipeline import DeviceField
+
+    with DeviceField(_lib.context(device), field) as df:  # one upload for the probe and the slab
+        c0, c1 = balanced_slab_ranges(field, grid, world, device, dfield=df)[rank]
+        piece, ctx = extract_piece(field, grid, options, c0, c1, device, dfield=df)
     out = stitch(piece, rank, world, dist, torch.device("cuda", device))
     if out is None:
         return None
