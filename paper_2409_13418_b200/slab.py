@@ -118,7 +118,10 @@ def balanced_slab_ranges(field, grid, world, device=0, dfield=None):
     cum = np.concatenate([[0.0], np.cumsum(w)])
     b = [0]
     for k in range(1, world):
-        c = int(np.searchsorted(cum, cum[-1] * k / world))
+        target = cum[-1] * k / world
+        c = int(np.searchsorted(cum, target))  # first layer boundary at or past the target
+        if c > 0 and target - cum[c - 1] < cum[min(c, R)] - target:
+            c -= 1  # the nearer boundary
         b.append(min(max(c, b[-1] + 1), R - (world - k)))  # every rank keeps >= 1 layer
     b.append(R)
     return [(b[k], b[k + 1]) for k in range(world)]

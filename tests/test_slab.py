@@ -177,3 +177,27 @@ def test_gpu_balanced_slabs_equal_single_extraction(world):
     mesh, pieces, rows = contour_slabs_serial(field, g, world, ranges=ranges)
     assert np.array_equal(mesh.triangles, ref.mesh.triangles)
     assert np.array_equal(mesh.vertices, ref.mesh.vertices)
+
+
+def test_balanced_slab_split_logic(monkeypatch):
+    """The split of the cumulative work estimate (host logic; the device probe
+    is replaced by a known work profile): equal shares, every rank >= 1 layer."""
+    import paper_2409_13418_b200.slab as slab
+
+    class G:
+        resolution = 8
+
+    # heavy middle layers: the middle ranks get fewer layers
+    monkeypatch.setattr(slab, "layer_work", lambda field, grid, device=0, dfield=None:
+                        np.array([1, 1, 4, 4, 4, 4, 1, 1], dtype=np.float64))
+    assert slab.balanced_slab_ranges(None, G, 1) == [(0, 8)]
+    r2 = slab.balanced_slab_ranges(None, G, 2)
+    assert r2 == [(0, 4), (4, 8)]
+    r4 = slab.balanced_slab_ranges(None, G, 4)
+    assert r4[0][0] == 0 and r4[-1][1] == 8 and all(b > a for a, b in r4)
+    assert [b - a for a, b in r4] == [3, 1, 1, 3]
+    # more ranks than heavy layers: still one layer each at least
+    r8 = slab.balanced_slab_ranges(None, G, 8)
+    assert r8 == [(k, k + 1) for k in range(8)]
+    with pytest.raises(ValueError):
+        slab.balanced_slab_ranges(None, G, 9)
