@@ -259,6 +259,16 @@ int odc_profile_mlp(odc_ctx* ctx, const odc_field* field, int64_t n, int64_t* tr
 /* Same, labels only (u8), for host points. */
 int odc_eval_labels(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, uint8_t* labels);
 
+/* numpy.linalg.eigh of n symmetric 3x3 matrices (row-major, 9 f64 each), as
+ * solve_qef_batch calls it (dualize.py:358): LAPACK dsyevd('V', 'L') of
+ * numpy's OpenBLAS, reproduced bit for bit (odc_eigh3.cuh).  w (n,3)
+ * ascending, V (n,3,3) = numpy's v (columns are eigenvectors), info (n) =
+ * LAPACK's info.  odc_eigh3 runs on ctx's device (host buffers in and out);
+ * odc_eigh3_host runs the same code on the calling CPU thread.  The QEF
+ * kernel inlines the same solver; these are its test hooks. */
+int odc_eigh3(odc_ctx* ctx, const double* A, int64_t n, double* w, double* V, int32_t* info);
+int odc_eigh3_host(const double* A, int64_t n, double* w, double* V, int32_t* info);
+
 /* Mesh validation on the device (replaces occmesh.mesh.validate_manifold,
  * mesh.py:91-150).  Triangles are host int64 (n_triangles, 3) indexing
  * n_vertices vertices.  Counts come back in the report; the lists

@@ -179,7 +179,7 @@ def numpy_dsyevd():
     return None
 
 
-def contour_oracle(field, lo, hi, resolution, options=None, raw_fn=None, continuous=None, qef="jacobi"):
+def contour_oracle(field, lo, hi, resolution, options=None, raw_fn=None, continuous=None):
     """Run the C oracle.  ``raw_fn(points (N,3) f64, category:str) -> (N,) f64``
     evaluates non-analytic fields (MLP / shared GPU field)."""
     from paper_2409_13418_b200.fields import field_continuous, is_mlp
@@ -207,10 +207,9 @@ def contour_oracle(field, lo, hi, resolution, options=None, raw_fn=None, continu
     hi = (ctypes.c_double * 3)(*[float(v) for v in hi])
     res = _Result()
     o = _opts(options, continuous, iso)
-    if qef == "lapack":
-        o.dsyevd = numpy_dsyevd()
-        if not o.dsyevd:
-            raise RuntimeError("numpy's LAPACK dsyevd not found")
+    o.dsyevd = numpy_dsyevd()  # the QEF eigensolve is numpy's own LAPACK (dualize.py:358)
+    if not o.dsyevd:
+        raise RuntimeError("numpy's LAPACK dsyevd not found")
     rc = L.orc_contour(nodes, n, cb, None, lo, hi, int(resolution), ctypes.byref(o), ctypes.byref(res))
     try:
         if rc:

@@ -14,8 +14,10 @@
  *   - (N,3) @ (3,3) (OpenBLAS dgemm) and 1-D x @ y (ddot) = fma chain
  *     fma(a2, b2, fma(a1, b1, a0*b0));
  *   - np.add.at accumulates sequentially in index order.
- * LAPACK eigh (dualize.py:358) is replaced by a cyclic Jacobi solver, so QEF
- * positions agree with the reference to ~1e-14 h, not bit-for-bit.
+ * The QEF eigensolve (np.linalg.eigh, dualize.py:358) calls numpy's own
+ * LAPACK dsyevd through a function pointer the caller supplies, so the whole
+ * result -- positions, split cases, mesh -- is the reference's bit for bit
+ * (tests/test_oracle_golden.py).
  */
 #include "odc_oracle.h"
 
@@ -229,61 +231,8 @@ static void batch_labels(field_t* f, const double* pts, int64_t n, uint8_t* lab,
   free(raw);
 }
 
-/* ------------------------------------------------------------------------ */
-/* Jacobi eigen-solver for symmetric 3x3 (replaces LAPACK ?syevd)            */
-/* ------------------------------------------------------------------------ */
-static void jacobi3(const double Ain[9], double w[3], double V[9]) {
-  double a[3][3];
-  double v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
-  for (int i = 0; i < 3; i++)
-    for (int j = 0; j < 3; j++) a[i][j] = Ain[3 * i + j];
-  static const int PQ[3][2] = {{0, 1}, {0, 2}, {1, 2}};
-  for (int sweep = 0; sweep < 16; sweep++) {
-    double off = (a[0][1] * a[0][1] + a[0][2] * a[0][2]) + a[1][2] * a[1][2];
-    if (off == 0.0) break;
-    for (int k = 0; k < 3; k++) {
-      int p = PQ[k][0], q = PQ[k][1];
-      double apq = a[p][q];
-      if (apq == 0.0) continue;
-      double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
-      double t;
-      if (fabs(theta) > 1e150) {
-        t = 1.0 / (2.0 * theta);
-      } else {
-        t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
-        if (theta < 0.0) t = -t;
-      }
-      double c = 1.0 / sqrt(t * t + 1.0);
-      double s = t * c;
-      double tau = s / (1.0 + c);
-      double app = a[p][p], aqq = a[q][q];
-      a[p][p] = app - t * apq;
-      a[q][q] = aqq + t * apq;
-      a[p][q] = a[q][p] = 0.0;
-      int r = 3 - p - q;
-      double arp = a[r][p], arq = a[r][q];
-      a[r][p] = a[p][r] = arp - s * (arq + tau * arp);
-      a[r][q] = a[q][r] = arq + s * (arp - tau * arq);
-      for (int i = 0; i < 3; i++) {
-        double vip = v[i][p], viq = v[i][q];
-        v[i][p] = vip - s * (viq + tau * vip);
-        v[i][q] = viq + s * (vip - tau * viq);
-      }
-    }
-  }
-  /* ascending sort (LAPACK order) */
-  int idx[3] = {0, 1, 2};
-  double d[3] = {a[0][0], a[1][1], a[2][2]};
-  for (int i = 0; i < 3; i++)
-    for (int j = i + 1; j < 3; j++)
-      if (d[idx[j]] < d[idx[i]]) { int t = idx[i]; idx[i] = idx[j]; idx[j] = t; }
-  for (int k = 0; k < 3; k++) {
-    w[k] = d[idx[k]];
-    for (int i = 0; i < 3; i++) V[3 * i + k] = v[i][idx[k]];
-  }
-}
-
-/* numpy.linalg.eigh(UPLO='L') through LAPACK dsyevd (pinning only). */
+/* numpy.linalg.eigh(UPLO='L') through numpy's own LAPACK dsyevd (the call
+   solve_qef_batch makes, dualize.py:358), so QEF positions are the reference's. */
 typedef void (*dsyevd_fn)(const char*, const char*, const int64_t*, double*, const int64_t*, double*,
                           double*, const int64_t*, int64_t*, const int64_t*, int64_t*, size_t, size_t);
 static void lapack_eigh3(void* fn, const double Ain[9], double w[3], double V[9]) {
@@ -332,6 +281,7 @@ int orc_contour(const orc_node* prog, int32_t n_nodes, orc_raw_cb cb, void* user
                 const orc_options* opt, orc_result* out) {
   orc_result* r = out;
   memset(r, 0, sizeof *r);
+  if (!opt->dsyevd) return ORC_E_CONFIG; /* numpy's LAPACK dsyevd is required */
   for (int i = 0; i < ORC_N_CAT; i++) r->cat_order[i] = -1;
   field_t F = {prog, n_nodes, cb, user, opt->iso_level, r, 0};
   field_t* f = &F;
@@ -1036,8 +986,7 @@ int orc_contour(const orc_node* prog, int32_t n_nodes, orc_raw_cb cb, void* user
       for (int c = 0; c < 3; c++) b[c] += n[c] * off;
     }
     double w[3], V[9];
-    if (opt->dsyevd) lapack_eigh3(opt->dsyevd, A, w, V);
-    else jacobi3(A, w, V);
+    lapack_eigh3(opt->dsyevd, A, w, V);
     double sv[3];
     for (int k = 0; k < 3; k++) sv[k] = sqrt(w[k] > 0.0 ? w[k] : 0.0);
     double smax = sv[2];

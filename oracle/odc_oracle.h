@@ -75,9 +75,8 @@ typedef struct {
   double s1_range, s2_range;
   double qef_truncation, fd_step_factor;
   double iso_level;
-  /* optional LAPACK dsyevd (Fortran ABI, 64-bit ints) used instead of the
-     Jacobi solver -- lets the pinning tests reproduce numpy.linalg.eigh
-     (dualize.py:358) bit-for-bit with numpy's own bundled LAPACK. */
+  /* numpy's bundled LAPACK dsyevd (Fortran ABI, 64-bit ints), required: the
+     QEF eigensolve is numpy.linalg.eigh (dualize.py:358) itself. */
   void* dsyevd;
 } orc_options;
 

@@ -88,7 +88,8 @@ EXPORTS = (
     "odc_copy_array", "odc_eval_raw", "odc_eval_labels", "odc_set_param", "odc_extract_slab",
     "odc_slab_globalize", "odc_mesh_finish", "odc_profile_mlp", "odc_export_obj", "odc_export_ply",
     "odc_validate_manifold", "odc_validate_copy", "odc_count_self_intersections", "odc_self_intersection_pairs",
-    "odc_mesh_distance", "odc_triangle_areas", "odc_field_mesh", "odc_field_voxels",
+    "odc_mesh_distance", "odc_triangle_areas", "odc_field_mesh", "odc_field_voxels", "odc_eigh3",
+    "odc_eigh3_host",
 )
 
 _lib = None
@@ -129,6 +130,8 @@ def load():
         L.odc_copy_array.argtypes = [vp, i32, vp, i64, P(i64)]
         L.odc_eval_raw.argtypes = [vp, vp, vp, i64, vp]
         L.odc_eval_labels.argtypes = [vp, vp, vp, i64, vp]
+        L.odc_eigh3.argtypes = [vp, vp, i64, vp, vp, vp]
+        L.odc_eigh3_host.argtypes = [vp, i64, vp, vp, vp]
         L.odc_extract_slab.argtypes = [vp, vp, P(dbl), P(dbl), i64, P(Options), i64, i64, P(Stats), P(SlabInfo)]
         L.odc_slab_globalize.argtypes = [vp, i64, i64, i64, vp]
         L.odc_mesh_finish.argtypes = [vp, vp, i64, vp, i64, i64, vp, vp, i32, P(Stats)]

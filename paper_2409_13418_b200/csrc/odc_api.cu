@@ -2010,4 +2010,40 @@ int odc_eval_labels(odc_ctx* c, const odc_field* f, const double* pts, int64_t n
   return eval_common(c, f, pts, n, nullptr, labels);
 }
 
+struct Eigh3Args {
+  const double* A;
+  int64_t n;
+  double *w, *V;
+  int32_t* info;
+};
+int odc_eigh3(odc_ctx* c, const double* A, int64_t n, double* w, double* V, int32_t* info) {
+  if (!c || n < 0 || (n && (!A || !w || !V || !info))) return ODC_E_ARG;
+  Eigh3Args a{A, n, w, V, info};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    Eigh3Args* x = (Eigh3Args*)p;
+    if (x->n == 0) return (int)ODC_OK;
+    cc->valid = false;  // reuses the workspace
+    cc->arena.reset();
+    double* dA = need(cc->arena.get<double>(9 * x->n));
+    double* dw = need(cc->arena.get<double>(3 * x->n));
+    double* dV = need(cc->arena.get<double>(9 * x->n));
+    int32_t* di = need(cc->arena.get<int32_t>(x->n));
+    CUDA_TRY(cudaMemcpyAsync(dA, x->A, sizeof(double) * 9 * x->n, cudaMemcpyHostToDevice, cc->stream));
+    launch_eigh3_batch(dA, x->n, dw, dV, di, cc->stream);
+    cc->launches++;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(x->w, dw, sizeof(double) * 3 * x->n, cudaMemcpyDeviceToHost, cc->stream));
+    CUDA_TRY(cudaMemcpyAsync(x->V, dV, sizeof(double) * 9 * x->n, cudaMemcpyDeviceToHost, cc->stream));
+    CUDA_TRY(cudaMemcpyAsync(x->info, di, sizeof(int32_t) * x->n, cudaMemcpyDeviceToHost, cc->stream));
+    CUDA_TRY(cudaStreamSynchronize(cc->stream));
+    return (int)ODC_OK;
+  }, &a);
+}
+int odc_eigh3_host(const double* A, int64_t n, double* w, double* V, int32_t* info) {
+  if (n < 0 || (n && (!A || !w || !V || !info))) return ODC_E_ARG;
+  eigh3_host_batch(A, n, w, V, info);
+  return ODC_OK;
+}
+
 }  // extern "C"

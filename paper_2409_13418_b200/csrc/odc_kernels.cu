@@ -15,6 +15,7 @@
 #include <cstdio>
 
 #include "odc_kernels.h"
+#include "odc_eigh3.cuh"
 #include "odc_scan.cuh"
 
 namespace odc {
@@ -1353,62 +1354,6 @@ void launch_cell_config(const GridP& g, const uint32_t* L, const WordRec* rec, c
   if (C) k_cell_config<<<grid_for(C, 128), 128, 0, s>>>(g, L, rec, cell_id, C, table, cfg, ncyc, nsamp);
 }
 
-// symmetric 3x3 eigen-solver (cyclic Jacobi; the CPU oracle runs the same
-// algorithm in the same order), eigenvalues ascending like LAPACK
-static __device__ void jacobi3(const double Ain[9], double w[3], double V[9]) {
-  double a[3][3];
-  double v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
-  for (int i = 0; i < 3; i++)
-    for (int j = 0; j < 3; j++) a[i][j] = Ain[3 * i + j];
-  const int PQ[3][2] = {{0, 1}, {0, 2}, {1, 2}};
-  for (int sweep = 0; sweep < 16; sweep++) {
-    const double off = (a[0][1] * a[0][1] + a[0][2] * a[0][2]) + a[1][2] * a[1][2];
-    if (off == 0.0) break;
-    for (int k = 0; k < 3; k++) {
-      const int p = PQ[k][0], q = PQ[k][1];
-      const double apq = a[p][q];
-      if (apq == 0.0) continue;
-      const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
-      double t;
-      if (fabs(theta) > 1e150) {
-        t = 1.0 / (2.0 * theta);
-      } else {
-        t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
-        if (theta < 0.0) t = -t;
-      }
-      const double c = 1.0 / sqrt(t * t + 1.0);
-      const double s = t * c;
-      const double tau = s / (1.0 + c);
-      const double app = a[p][p], aqq = a[q][q];
-      a[p][p] = app - t * apq;
-      a[q][q] = aqq + t * apq;
-      a[p][q] = a[q][p] = 0.0;
-      const int r = 3 - p - q;
-      const double arp = a[r][p], arq = a[r][q];
-      a[r][p] = a[p][r] = arp - s * (arq + tau * arp);
-      a[r][q] = a[q][r] = arq + s * (arp - tau * arq);
-      for (int i = 0; i < 3; i++) {
-        const double vip = v[i][p], viq = v[i][q];
-        v[i][p] = vip - s * (viq + tau * vip);
-        v[i][q] = viq + s * (vip - tau * viq);
-      }
-    }
-  }
-  int idx[3] = {0, 1, 2};
-  const double d[3] = {a[0][0], a[1][1], a[2][2]};
-  for (int i = 0; i < 3; i++)
-    for (int j = i + 1; j < 3; j++)
-      if (d[idx[j]] < d[idx[i]]) {
-        int t = idx[i];
-        idx[i] = idx[j];
-        idx[j] = t;
-      }
-  for (int k = 0; k < 3; k++) {
-    w[k] = d[idx[k]];
-    for (int i = 0; i < 3; i++) V[3 * i + k] = v[i][idx[k]];
-  }
-}
-
 __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint32_t* __restrict__ L,
                                                     const WordRec* __restrict__ rec,
                                                     const int64_t* __restrict__ cell_id, int64_t C,
@@ -1505,7 +1450,7 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
       for (int c = 0; c < 3; c++) b[c] += nn[j][c] * off;
     }
     double w[3], V[9];
-    jacobi3(A, w, V);
+    odc_eigh3(A, w, V);  // np.linalg.eigh (dualize.py:358), LAPACK dsyevd bit for bit
     double sv[3];
     for (int kk = 0; kk < 3; kk++) sv[kk] = sqrt(w[kk] > 0.0 ? w[kk] : 0.0);
     const double smax = sv[2];

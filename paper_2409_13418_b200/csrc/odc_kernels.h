@@ -137,6 +137,9 @@ struct CellOut {
   double* normals;     // (Ns,3) keep only
   int64_t* cyc_len;    // (P) keep only
 };
+// numpy.linalg.eigh for a batch of symmetric 3x3 matrices (odc_eigh3.cu)
+void launch_eigh3_batch(const double* A, int64_t n, double* w, double* V, int32_t* info, cudaStream_t s);
+void eigh3_host_batch(const double* A, int64_t n, double* w, double* V, int32_t* info);
 void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec, const int64_t* cell_id,
                        int64_t C, const CellTabEntry* table, const uint16_t* cfg, const uint32_t* part_base,
                        const uint32_t* samp_base, const double* pos1d, const double* pos3, const double* edge_normals,

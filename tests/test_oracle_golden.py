@@ -1,11 +1,8 @@
 """Pin the C oracle against golden vectors from the unmodified reference.
 
-With ``qef="lapack"`` the oracle calls the same LAPACK dsyevd numpy.linalg.eigh
-uses (dualize.py:358) and must reproduce the reference bit-for-bit, mesh
-included.  With the default Jacobi QEF (the algorithm the GPU runs) every
-stage up to the QEF is still bit-exact; QEF positions agree to ~1e-14 h and
-split decisions may differ only where the reference's own concavity predicate
-(polygonize.py:47-75) is degenerate at the last ulp.
+The oracle calls the same LAPACK dsyevd numpy.linalg.eigh uses
+(dualize.py:358) and must reproduce the reference bit-for-bit, every stage
+and the mesh included.
 """
 
 import numpy as np
@@ -17,9 +14,9 @@ from golden_util import cases, field_of, index, load
 ALL = cases()
 
 
-def _run(tag, qef):
+def _run(tag):
     field, lo, hi, R = field_of(tag)
-    return oracle.contour_oracle(field, lo, hi, R, qef=qef)
+    return oracle.contour_oracle(field, lo, hi, R)
 
 
 EXACT_UPTO_QEF = ["labels", "edge_key", "v_in", "face_key", "face_n_crossing", "cells", "instance_edges",
@@ -32,28 +29,12 @@ def test_oracle_lapack_bit_exact(tag):
     if oracle.numpy_dsyevd() is None:
         pytest.skip("numpy's LAPACK not loadable")
     g = load(tag)
-    o = _run(tag, "lapack")
+    o = _run(tag)
     for k in EXACT_UPTO_QEF + ["qef_pos", "qef_rank", "split_cases", "raw_vertices", "raw_triangles",
                                "raw_kind", "raw_ref", "vertices", "triangles", "kind", "ref"]:
         assert np.array_equal(np.asarray(g[k]), np.asarray(o[k])), k
     assert o["eval_counts"] == g["eval_counts"]
     assert o["n_probes"] == g["n_probes"]
-
-
-@pytest.mark.parametrize("tag", ALL)
-def test_oracle_jacobi_matches_upto_qef(tag):
-    g = load(tag)
-    o = _run(tag, "jacobi")
-    for k in EXACT_UPTO_QEF:
-        assert np.array_equal(np.asarray(g[k]), np.asarray(o[k])), k
-    h = float(np.min(o["h"]))
-    assert np.abs(g["qef_pos"] - o["qef_pos"]).max() <= 1e-12 * h
-    assert np.array_equal(g["qef_rank"], o["qef_rank"])
-    flips = int(np.sum(g["split_cases"] != o["split_cases"]))
-    # degenerate (exactly coplanar, clamped) quads only; counted, bounded
-    assert flips <= 4, flips
-    if flips == 0:
-        assert np.array_equal(g["triangles"], o["triangles"])
 
 
 def test_known_answers():

@@ -22,7 +22,7 @@ def test_oracle_voxel_mesh_matches_reference():
     from paper_2409_13418_b200 import VoxelField
 
     f = VoxelField(G["origin"], G["spacing"], G["values"])
-    o = oracle.contour_oracle(f, tuple(G["lo"]), tuple(G["hi"]), int(G["R"]), continuous=True, qef="lapack",
+    o = oracle.contour_oracle(f, tuple(G["lo"]), tuple(G["hi"]), int(G["R"]), continuous=True,
                               raw_fn=lambda p, c: voxel_raw(G["origin"], G["spacing"], G["values"], p))
     assert np.array_equal(o["triangles"], G["mesh_t"]) and np.array_equal(o["vertices"], G["mesh_v"])
 
