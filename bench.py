@@ -117,30 +117,66 @@ class ClockSampler:
 # CPU reference arm: the oracle port (C lock-step restatement of
 # occmesh.pipeline.contour + numpy MlpField) on a bounded sample
 # ---------------------------------------------------------------------------
-def cpu_sample(field, lo, hi, R_full, full_evals, sample_R=None):
+def load_cpu_cache(workload, field, lo, hi, R):
+    """The cached full-size CPU reference run (scripts/cpu_reference_full.py),
+    if one exists for exactly this input."""
+    p = REPO / "profiles" / f"r2_cpu_reference_{workload}.json"
+    if not p.exists():
+        return None
+    rec = json.loads(p.read_text())
+    sys.path.insert(0, str(REPO / "scripts"))
+    from cpu_reference_full import input_hash
+
+    if rec.get("input_hash") != input_hash(field, lo, hi, R):
+        return None
+    rec["path"] = str(p.relative_to(REPO))
+    return rec
+
+
+def cpu_sample(field, lo, hi, R_full, full_evals, sample_R=None, cache=None):
+    """One live sample of the CPU reference (the oracle port) and the
+    full-size estimate it supports.  With a cached full-size run of this
+    exact input (``cache``) the estimate is that measured time scaled by the
+    live/cached sample ratio (host-speed correction); without one it is
+    extrapolated from the sample (by eval count for the MLP, by cells
+    otherwise) and says so."""
     import oracle
     from paper_2409_13418_b200.fields import is_mlp
 
     cores = len(os.sched_getaffinity(0))
-    if is_mlp(field):
-        sR = sample_R or 64
-        t0 = time.perf_counter()
-        o = oracle.contour_oracle(field, lo, hi, sR)
-        dt = time.perf_counter() - t0
-        ev = o["eval_counts"]["total_evals"]
-        t_full = dt * full_evals / ev
-        sample = (f"oracle pipeline (C, 1 thread) + numpy fp32 MlpField (OpenBLAS, {cores} threads) at {sR}^3: "
-                  f"{ev} evals in {dt:.2f} s; scaled by the eval count of the {R_full}^3 run ({full_evals} evals)")
-    else:
-        sR = sample_R or min(R_full, 384)  # ~10 s of C oracle work; 1024^3 would take minutes
-        t0 = time.perf_counter()
-        oracle.contour_oracle(field, lo, hi, sR)
-        dt = time.perf_counter() - t0
-        t_full = dt * (R_full / sR) ** 3
-        sample = f"oracle pipeline (C, 1 thread) at {sR}^3 in {dt:.2f} s" + (
-            "" if sR == R_full else f", scaled by cells to {R_full}^3")
+    mlp = is_mlp(field)
+    sR = (cache or {}).get("sample_r") or sample_R or (64 if mlp else min(R_full, 384))
+    t0 = time.perf_counter()
+    o = oracle.contour_oracle(field, lo, hi, sR)
+    dt = time.perf_counter() - t0
+    if not mlp:
         cores = 1
-    return R_full**3 / t_full, t_full, cores, sample, dt
+    impl = ("oracle pipeline (C, 1 thread) + numpy fp32 MlpField (OpenBLAS, %d threads)" % cores if mlp
+            else "oracle pipeline (C, 1 thread)")
+    if cache is not None:
+        ratio = dt / cache["sample_wall_s"]
+        t_full = cache["full_wall_s"] * ratio
+        info = {"extrapolated": False, "cached_full_run": cache["path"], "cached_full_wall_s": cache["full_wall_s"],
+                "cached_measured_at": cache["measured_at"], "cached_host": cache["host"],
+                "live_sample_ratio": ratio}
+        sample = (f"{impl}: full {R_full}^3 run measured once on this host class ({cache['full_wall_s']:.0f} s, "
+                  f"{cache['measured_at']}, {cache['path']}); this step re-timed the {sR}^3 sample live "
+                  f"({dt:.2f} s, x{ratio:.3f} the cached sample) and scaled the full time by that ratio")
+    elif sR == R_full:
+        t_full = dt
+        info = {"extrapolated": False}
+        sample = f"{impl} at {sR}^3 in {dt:.2f} s (full size, measured live)"
+    else:
+        if mlp:
+            ev = o["eval_counts"]["total_evals"]
+            t_full = dt * full_evals / ev
+            how = f"scaled by the eval count of the {R_full}^3 run ({full_evals} evals)"
+        else:
+            t_full = dt * (R_full / sR) ** 3
+            how = f"scaled by cells to {R_full}^3"
+        info = {"extrapolated": True}
+        sample = f"{impl} at {sR}^3: {dt:.2f} s; {how}"
+    return R_full**3 / t_full, t_full, cores, sample, dt, info
 
 
 def run_reference(args, rank, world):
@@ -149,17 +185,18 @@ def run_reference(args, rank, world):
     field, lo, hi, R, desc = workload(args.workload)
     from paper_2409_13418_b200.fields import is_mlp
 
+    cache = load_cpu_cache(args.workload, field, lo, hi, R)
     full_evals = None
-    if is_mlp(field):
-        # eval count of the full-size run (S^3 + 15K + F4 + 46Q) from the oracle's
-        # accounting formula on a CPU-cheap estimate is not possible without the
-        # surface; use the recorded count of the device run when available.
+    if is_mlp(field) and cache is None:
         full_evals = args.full_evals or estimate_mlp_evals(R)
-    vals = []
+    vals, live = [], []
+    t_run = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        v, t_full, cores, sample, dt = cpu_sample(field, lo, hi, R, full_evals, args.cpu_sample_r)
+        v, t_full, cores, sample, dt, info = cpu_sample(field, lo, hi, R, full_evals, args.cpu_sample_r, cache)
         if i >= args.warmup:
             vals.append(v)
+            live.append(dt)
+    t_run = time.perf_counter() - t_run
     value = float(np.mean(vals))
     line = {
         "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -167,8 +204,11 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f32+f64" if is_mlp(field) else "f64", "data": "synthetic",
         "config": {"workload": desc, "R": R, "cells": R**3},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": cores, "kind": "port", "sample": sample, **info},
         "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "timing": {"ms_per_step_is": "the full-size step time (cached measurement x live ratio)" if cache else
+                   ("extrapolated full-size step time" if info.get("extrapolated") else "measured"),
+                   "live_sample_s": live, "wall_s_this_run": t_run},
     }
     emit(line)
 
@@ -325,8 +365,9 @@ def run_gpu(args, rank, world, dist):
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, t_full, cores, sample, dt = cpu_sample(field, lo, hi, R, total_evals, args.cpu_sample_r)
-        cpu = {"value": v, "unit": "cells/s", "cores": cores, "kind": "port", "sample": sample}
+        cache = load_cpu_cache(args.workload, field, lo, hi, R)
+        v, t_full, cores, sample, dt, info = cpu_sample(field, lo, hi, R, total_evals, args.cpu_sample_r, cache)
+        cpu = {"value": v, "unit": "cells/s", "cores": cores, "kind": "port", "sample": sample, **info}
     stage_names = ["labels", "active_sets", "points_1d", "normals_2d", "cells_qef", "polygonize", "repair",
                    "labels_kernel"]
     line = {
@@ -439,9 +480,9 @@ def run_gpu_batch(args, rank, world, dist):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         f, g = jobs[0]
-        v, t_full, cores, sample, dt = cpu_sample(f, g.lo, g.hi, R, None, args.cpu_sample_r)
+        v, t_full, cores, sample, dt, info = cpu_sample(f, g.lo, g.hi, R, None, args.cpu_sample_r)
         cpu = {"value": v, "unit": "cells/s", "cores": cores, "kind": "port",
-               "sample": sample + " (shape 0 of the batch; per-shape throughput)"}
+               "sample": sample + " (shape 0 of the batch; per-shape throughput)", **info}
     line = {
         "metric": METRIC, "value": cells / step, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -497,14 +538,16 @@ def run_gpu_slabs(args, rank, world, dist):
 
     timed(args.warmup, False)
     launches = 0
-    k_ms = []
+    k_ms, k_ev = [], []
     with ClockSampler(device) as clocks:
         dev_ms = []
         for _ in range(args.steps):
             dev_ms += timed(1, False)
             if last["out"] is not None:  # rank 0: launches summed over ranks, slowest grid pass
                 launches += last["out"]["n_kernel_launches"]
-                k_ms.append(last["out"]["labels_kernel_ms"])
+                kr = np.asarray(last["out"]["rank_label_ms"])
+                k_ms.append(float(kr.max()))
+                k_ev.append(int(last["out"]["rank_label_evals"][int(kr.argmax())]))
     clock = clocks.summary()
     timed(args.warmup, True)
     e2e_ms = timed(args.steps, True)
@@ -514,30 +557,34 @@ def run_gpu_slabs(args, rank, world, dist):
         return
     res = last["out"]
     V, T = res.mesh.n_vertices, res.mesh.n_triangles
+    from paper_2409_13418_b200.slab import probe_bytes
+
+    p_h2d, p_d2h = probe_bytes(grid)  # balanced-bounds probe, every rank, every step
     if is_mlp(field):
-        h2d = world * ((64 * 256 + 7 * 256 * 256) * 2 + 8 * 256 * 4 + 256 * 4)
+        h2d = world * ((64 * 256 + 7 * 256 * 256) * 2 + 8 * 256 * 4 + 256 * 4 + p_h2d)
     else:
         from paper_2409_13418_b200.fields import lower_program
 
-        h2d = world * 136 * len(lower_program(field))
-    d2h = V * 24 + T * 24 + V * 24 + (T * 24 if res.raw_mesh is not res.mesh else 0)
+        h2d = world * (136 * len(lower_program(field)) + p_h2d)
+    d2h = V * 24 + T * 24 + V * 24 + (T * 24 if res.raw_mesh is not res.mesh else 0) + world * p_d2h
     roof = None
     if k_ms:
         peaks, peak_kind = load_peaks()
         km = float(np.mean(k_ms))
-        S3 = (R + 1) ** 3 / world  # the slowest rank's share of the grid, approximately
+        ev = float(np.mean(k_ev))  # the slowest rank's own grid evaluations (its slab + halo layer)
         if is_mlp(field):
             peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-            ach = float(field.flops_per_eval) * S3 / (km / 1e3) / 1e12
+            ach = float(field.flops_per_eval) * ev / (km / 1e3) / 1e12
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                    "kernel": "grid occupancy MLP of one slab (slowest rank)", "kernel_ms": km}
+                    "kernel": "grid occupancy MLP of the slowest rank's slab",
+                    "algorithmic": f"937984 FLOP/eval x {int(ev)} evals (slowest rank)", "kernel_ms": km}
         else:
             W = (R + 1 + 31) // 32
-            nbytes = (R + 1) ** 2 * W * 4 / world
+            nbytes = ev / (R + 1) * W * 4
             peak = float(peaks["hbm_gbs"])
             ach = nbytes / (km / 1e3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                    "kernel": "k_labels_analytic of one slab (slowest rank)", "kernel_ms": km}
+                    "kernel": "k_labels_analytic of the slowest rank's slab", "kernel_ms": km}
         roof["peak_source"] = f"{peak_kind} (MEASURED_PEAKS.json)" if peak_kind == "measured" else "fallback"
         roof["traffic"] = None
     line = {
@@ -575,6 +622,26 @@ def _protect_stdout():
     os.dup2(2, 1)
 
 
+def relaunch(n):
+    """``python bench.py --gpus N`` outside torchrun: re-exec under
+    torch.distributed.run with one process per GPU (the driver's own launch
+    sets WORLD_SIZE and never gets here)."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        sys.exit(f"bench.py --gpus {n}: only {have} CUDA device(s) visible")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -588,6 +655,8 @@ def main():
     ap.add_argument("--batch-workers", type=int, default=8)
     ap.add_argument("--slabs", action="store_true", help="use the z-slab path even on one rank (testing)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        relaunch(args.gpus)  # one process per GPU (does not return)
     _protect_stdout()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -156,6 +156,8 @@ class SlabPiece:
     part_index: object      # (P,) i64
     fan_edge: object        # (NF,) i64
     stats: np.ndarray       # STAT_KEYS + eval counts
+    c0: int = -1            # owned cell layers [c0, c1)
+    c1: int = -1
 
 
 class _CudaArray:
@@ -205,6 +207,7 @@ def extract_piece(field, grid, options, c0, c1, device=0, dfield=None):
         part_index=_dev(torch, info.partition_index, (P,), "<i8", dev),
         fan_edge=_dev(torch, info.fan_edge, (NF,), "<i8", dev),
         stats=stats_vector(st),
+        c0=int(c0), c1=int(c1),
     )
     return piece, ctx
 
@@ -226,45 +229,98 @@ def run_extras(rows):
     return int(rows[:, -2].sum()), float(rows[:, -1].max()) / 1e6
 
 
-def stitch(piece, rank, world, dist, device):
+def rank_label_work(rows):
+    """Per rank: (grid-label evaluations incl. the halo layer, grid-label
+    kernel ms) -- for the slowest rank's roofline."""
+    rows = np.asarray(rows)
+    nk = len(STAT_KEYS)
+    return rows[:, nk + 18].astype(np.int64), rows[:, -1].astype(np.float64) / 1e6
+
+
+def probe_bytes(grid, nxy=17, nz_max=129):
+    """Host<->device bytes of layer_work's probe per rank: (H2D points, D2H labels)."""
+    R = int(grid.resolution)
+    zs = max(1, -(-R // (nz_max - 1)))
+    nz = len(range(0, R + 1, zs)) + (0 if R % zs == 0 else 1)
+    n = nz * nxy * nxy
+    return 24 * n, n
+
+
+def check_ranges(allc, R=None):
+    """Every rank computes its slab bounds on its own; rank 0 checks that the
+    gathered [c0, c1) ranges tile [0, R) in rank order (overlaps or gaps
+    would silently corrupt the global ids)."""
+    c0, c1 = allc[:, 3], allc[:, 4]
+    ok = c0[0] == 0 and bool(np.all(c1[:-1] == c0[1:])) and bool(np.all(c1 > c0))
+    if R is not None:
+        ok = ok and c1[-1] == R
+    if not ok:
+        raise RuntimeError(f"slab ranges do not tile the grid: {list(zip(c0.tolist(), c1.tolist()))}")
+
+
+def stitch(piece, rank, world, dist, device, R=None):
     """Collectives + assembly.  Returns the assembled arrays on rank 0
     (vertices, triangles (global int32), kind, ref, n_partitions_total,
-    per-rank stats) and None elsewhere."""
+    per-rank stats) and None elsewhere.  One all-gather of the counts and
+    stats, then one grouped point-to-point exchange (every rank's six
+    payload tensors to rank 0 in a single batch_isend_irecv, i.e. one
+    ncclGroupStart/End on the NCCL backend).  With the gloo backend and
+    device tensors (several ranks sharing one GPU in the tests) the payload
+    is staged through host memory."""
     import torch
 
+    stage = dist.get_backend() == "gloo" and torch.device(device).type == "cuda"
+    wire = torch.device("cpu") if stage else device
     P, NF, T = piece.part_vertices.shape[0], piece.fan_vertices.shape[0], piece.triangles.shape[0]
-    counts = torch.tensor([P, NF, T], dtype=torch.int64, device=device)
-    gathered = [torch.zeros_like(counts) for _ in range(world)]
-    dist.all_gather(gathered, counts)
-    allc = torch.stack(gathered).cpu().numpy()
-    part_base, P_tot, fan_base = global_offsets(allc, rank)
+    head = torch.tensor([P, NF, T, piece.c0, piece.c1], dtype=torch.int64)
+    sv = torch.cat([head, torch.as_tensor(piece.stats, dtype=torch.int64)]).to(wire)
+    gathered = [torch.zeros_like(sv) for _ in range(world)]
+    dist.all_gather(gathered, sv)
+    rows = torch.stack(gathered).cpu().numpy()
+    allc, stats_rows = rows[:, :5], rows[:, 5:]
+    if rank == 0:
+        check_ranges(allc, R)
+    part_base, P_tot, fan_base = global_offsets(allc[:, :3], rank)
     tris = globalize(piece, part_base, P_tot, fan_base, device)
-    sv = torch.as_tensor(piece.stats, device=device)
-    gst = [torch.zeros_like(sv) for _ in range(world)]
-    dist.all_gather(gst, sv)
     payload = [piece.part_vertices.contiguous(), piece.fan_vertices.contiguous(), tris.contiguous(),
                piece.part_cell.contiguous(), piece.part_index.contiguous(), piece.fan_edge.contiguous()]
+    if stage and rank != 0:
+        payload = [t.cpu() for t in payload]
     if rank != 0:
-        for t in payload:
-            if t.numel():
-                dist.send(t, dst=0)
+        ops = [dist.P2POp(dist.isend, t, 0) for t in payload if t.numel()]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
         return None
     parts = [[p] for p in payload]
+    ops = []
     for r in range(1, world):
-        Pr, NFr, Tr = (int(x) for x in allc[r])
-        bufs = [torch.empty((Pr, 3), dtype=torch.float64, device=device),
-                torch.empty((NFr, 3), dtype=torch.float64, device=device),
-                torch.empty((Tr, 3), dtype=torch.int32, device=device),
-                torch.empty((Pr,), dtype=torch.int64, device=device),
-                torch.empty((Pr,), dtype=torch.int64, device=device),
-                torch.empty((NFr,), dtype=torch.int64, device=device)]
-        for b in bufs:
-            if b.numel():
-                dist.recv(b, src=r)
+        Pr, NFr, Tr = (int(x) for x in allc[r, :3])
+        bufs = [torch.empty((Pr, 3), dtype=torch.float64, device=wire),
+                torch.empty((NFr, 3), dtype=torch.float64, device=wire),
+                torch.empty((Tr, 3), dtype=torch.int32, device=wire),
+                torch.empty((Pr,), dtype=torch.int64, device=wire),
+                torch.empty((Pr,), dtype=torch.int64, device=wire),
+                torch.empty((NFr,), dtype=torch.int64, device=wire)]
+        ops += [dist.P2POp(dist.irecv, b, r) for b in bufs if b.numel()]
         for i, b in enumerate(bufs):
             parts[i].append(b)
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if stage:
+        parts = [[p[0]] + [b.to(device) for b in p[1:]] for p in parts]
     verts, tr, kind, ref = assemble([[p[r] for p in parts] for r in range(world)], device)
-    return verts, tr, kind, ref, P_tot, torch.stack(gst).cpu().numpy()
+    return verts, tr, kind, ref, P_tot, stats_rows
+
+
+def _torch_sync(device):
+    """libodc runs on its context's own stream: tensors torch just wrote (or a
+    block the caching allocator just recycled) must be complete before the
+    library touches them."""
+    import torch
+
+    torch.cuda.current_stream(device).synchronize()
 
 
 def globalize(piece, part_base, P_tot, fan_base, device):
@@ -276,6 +332,7 @@ def globalize(piece, part_base, P_tot, fan_base, device):
         return out
     if piece.triangles.is_cuda:
         ctx = _lib.context(piece.triangles.device.index or 0)
+        _torch_sync(out.device)
         rc = _lib.load().odc_slab_globalize(ctx.handle, part_base, P_tot, fan_base, out.data_ptr())
         if rc != _lib.ODC_OK:
             raise RuntimeError(_lib.load().odc_last_error(ctx.handle).decode())
@@ -318,19 +375,22 @@ def contour_slab(field, grid, options=None, *, rank, world, dist, device=0, to_h
     with DeviceField(_lib.context(device), field) as df:  # one upload for the probe and the slab
         c0, c1 = balanced_slab_ranges(field, grid, world, device, dfield=df)[rank]
         piece, ctx = extract_piece(field, grid, options, c0, c1, device, dfield=df)
-    out = stitch(piece, rank, world, dist, torch.device("cuda", device))
+    out = stitch(piece, rank, world, dist, torch.device("cuda", device), R=int(grid.resolution))
     if out is None:
         return None
     verts, tris, kind, ref, P_tot, rows = out
     L = _lib.load()
     st = _lib.Stats()
+    _torch_sync(verts.device)
     rc = L.odc_mesh_finish(ctx.handle, verts.data_ptr(), verts.shape[0], tris.data_ptr(), tris.shape[0], P_tot,
                            kind.data_ptr(), ref.data_ptr(), int(bool(options.repair)), ctypes.byref(st))
     if rc != _lib.ODC_OK:
         _raise(rc, ctx)
     if not to_host:
         launches, k_ms = run_extras(rows)
-        return {"finish": st, "n_kernel_launches": launches + int(st.n_kernel_launches), "labels_kernel_ms": k_ms}
+        ev, kms = rank_label_work(rows)
+        return {"finish": st, "n_kernel_launches": launches + int(st.n_kernel_launches), "labels_kernel_ms": k_ms,
+                "rank_label_evals": ev.tolist(), "rank_label_ms": kms.tolist()}
     mesh = _copy_mesh(ctx, 0, st) if st.n_triangles else TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), np.int64))
     raw = mesh if st.repair_added_vertices == 0 else _raw_from_repaired(ctx, mesh, st)
     stats = slab_stats(rows, options, st)
@@ -385,6 +445,7 @@ def contour_slabs_serial(field, grid, n_slabs, options=None, device=0, ranges=No
     verts, tris, kind, ref = assemble(glob, dev)
     ctx = _lib.context(device)
     st = _lib.Stats()
+    _torch_sync(dev)
     rc = _lib.load().odc_mesh_finish(ctx.handle, verts.data_ptr(), verts.shape[0], tris.data_ptr(), tris.shape[0],
                                      int(counts[:, 0].sum()), kind.data_ptr(), ref.data_ptr(),
                                      int(bool(options.repair)), ctypes.byref(st))

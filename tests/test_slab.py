@@ -81,6 +81,7 @@ def oracle_pieces(o, R, world):
             part_index=torch.as_tensor(o["part_index"][p_lo:p_hi]),
             fan_edge=torch.as_tensor(fan_edges),
             stats=np.zeros(34, np.int64),
+            c0=c0, c1=c1,
         ))
     return pieces
 
@@ -96,7 +97,7 @@ def _worker(rank, world, port, R, result_path):
         field, lo, hi = scenes.resolve(scenes.SCENES["torus"], R)
         o = oracle.contour_oracle(field, lo, hi, R)
         piece = oracle_pieces(o, R, world)[rank]
-        out = stitch(piece, rank, world, dist, torch.device("cpu"))
+        out = stitch(piece, rank, world, dist, torch.device("cpu"), R=R)
         if rank == 0:
             verts, tris, kind, ref, P_tot, rows = out
             ok = (np.array_equal(verts.numpy(), o["raw_vertices"]) and np.array_equal(tris.numpy(), o["raw_triangles"])
@@ -177,6 +178,101 @@ def test_gpu_balanced_slabs_equal_single_extraction(world):
     mesh, pieces, rows = contour_slabs_serial(field, g, world, ranges=ranges)
     assert np.array_equal(mesh.triangles, ref.mesh.triangles)
     assert np.array_equal(mesh.vertices, ref.mesh.vertices)
+
+
+def test_check_ranges_rejects_gaps_and_overlaps():
+    from paper_2409_13418_b200.slab import check_ranges
+
+    def rows(rs):
+        return np.array([[0, 0, 0, a, b] for a, b in rs])
+
+    check_ranges(rows([(0, 3), (3, 8)]), 8)
+    for bad in ([(0, 3), (4, 8)], [(0, 4), (3, 8)], [(1, 4), (4, 8)], [(0, 4), (4, 7)], [(0, 0), (0, 8)]):
+        with pytest.raises(RuntimeError, match="do not tile"):
+            check_ranges(rows(bad), 8)
+
+
+@pytest.mark.gpu
+def test_gpu_slab_globalize_device_equals_host():
+    """k_globalize_tris (odc_slab_globalize, the ids the N-GPU path writes on
+    the device) equals the host restatement globalize_ids for every slab."""
+    import torch
+
+    from paper_2409_13418_b200 import GridSpec, MlpField
+    from paper_2409_13418_b200.pipeline import ContourOptions
+    from paper_2409_13418_b200.slab import extract_piece, globalize
+
+    field = MlpField(seed=0, amplitude=3.0)
+    g = GridSpec((0, 0, 0), (1, 1, 1), 48)
+    for c0, c1 in slab_ranges(48, 4):
+        piece, _ = extract_piece(field, g, ContourOptions(), c0, c1)
+        for part_base, P_tot, fan_base in ((1000, 50000, 7), (piece.n_halo, piece.n_window + 3, 0)):
+            dev = globalize(piece, part_base, P_tot, fan_base, torch.device("cuda", 0)).cpu().numpy()
+            host = globalize_ids(piece.triangles.cpu().numpy(), piece.n_halo, piece.n_window, part_base, P_tot,
+                                 fan_base)
+            assert np.array_equal(dev, host.astype(np.int32))
+
+
+def _slab_worker(rank, world, port, backend, result_path):
+    import torch.distributed as dist
+
+    from paper_2409_13418_b200 import GridSpec, MlpField, contour
+    from paper_2409_13418_b200.slab import contour_slab
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dev = rank if backend == "nccl" else 0
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    try:
+        field = MlpField(seed=0, amplitude=3.0)
+        g = GridSpec((0, 0, 0), (1, 1, 1), 56)
+        res = contour_slab(field, g, rank=rank, world=world, dist=dist, device=dev)
+        if rank == 0:
+            ref = contour(field, g, device=dev)
+            ok = all(np.array_equal(a, b) for a, b in (
+                (res.mesh.vertices, ref.mesh.vertices), (res.mesh.triangles, ref.mesh.triangles),
+                (res.mesh.provenance_kind, ref.mesh.provenance_kind),
+                (res.mesh.provenance_ref, ref.mesh.provenance_ref),
+                (res.raw_mesh.triangles, ref.raw_mesh.triangles)))
+            ok = ok and res.stats["eval_counts"] == ref.stats["eval_counts"]
+            ok = ok and res.stats["repair_added_vertices"] == ref.stats["repair_added_vertices"]
+            np.save(result_path, np.array([int(ok)]))
+        else:
+            assert res is None
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(world, backend, tmp_path):
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = tmp_path / "ok.npy"
+    mp.spawn(_slab_worker, args=(world, port, backend, str(out)), nprocs=world, join=True)
+    assert np.load(out)[0] == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo"), (3, "gloo")])
+def test_gpu_contour_slab_processes(world, backend, tmp_path):
+    """The real multi-process path (contour_slab: balanced bounds on every
+    rank, device extraction, count all-gather, device id globalization, one
+    grouped P2P gather, odc_mesh_finish on rank 0) equals contour().  NCCL
+    with one rank per GPU; with more ranks than GPUs the ranks share GPU 0
+    and the exchange goes over gloo with host staging (each rank's kernels
+    run independently; only the host-side collectives synchronise them)."""
+    _spawn(world, backend, tmp_path)
+
+
+@pytest.mark.gpu
+def test_gpu_contour_slab_two_gpus_nccl(tmp_path):
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    _spawn(2, "nccl", tmp_path)
 
 
 def test_balanced_slab_split_logic(monkeypatch):
