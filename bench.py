@@ -246,8 +246,6 @@ def run_gpu(args, rank, world, dist):
             dist.barrier()
         torch.cuda.synchronize()
 
-    if os.environ.get("ODC_MLP_IMPL"):  # evaluator selection for experiments (default: CTA-pair N=256 tcgen05)
-        L.odc_set_param(ctx.handle, b"mlp_impl", int(os.environ["ODC_MLP_IMPL"]))
     dfield = DeviceField(ctx, field)
     st = _lib.Stats()
 

@@ -149,12 +149,12 @@ const char* odc_last_error(const odc_ctx* ctx);
  * Synchronises the previous stream first: a context's launches stay ordered
  * (its MLP evaluator takes work from a per-context device counter). */
 int odc_set_stream(odc_ctx* ctx, void* stream);
-/* tuning/testing knobs: "mlp_impl" = 3 CTA-pair N=256 tile ping-pong tcgen05
- * evaluator (default), 2 single-CTA tcgen05, 0 CTA-pair with A in TMEM, 1 SIMT
- * reference evaluator (same math, CUDA cores).  Profiling only (they affect
- * odc_profile_mlp, never an extraction): "mlp_debug" = timing-experiment
- * bits, "profile_points" = a host pointer to (n, 3) f64 points that
- * odc_profile_mlp evaluates with mlp_debug bit 128 (0 = grid points). */
+/* Parameters: "mbar_timeout_ms" -- the MLP evaluator's mbarrier waits trap
+ * (kernel error) after this long without progress, default 4000, 0 = wait
+ * forever (debuggers, MPS/preemption); device-wide.  Profiling only (they
+ * affect odc_profile_mlp, never an extraction): "mlp_debug" = timing-
+ * experiment bits, "profile_points" = a host pointer to (n, 3) f64 points
+ * that odc_profile_mlp evaluates with mlp_debug bit 128 (0 = grid points). */
 int odc_set_param(odc_ctx* ctx, const char* name, int64_t value);
 
 int odc_field_analytic(odc_ctx* ctx, const odc_node* nodes, int32_t n_nodes, int32_t continuous,
@@ -258,6 +258,12 @@ int odc_eval_raw(odc_ctx* ctx, const odc_field* field, const double* points, int
 int odc_profile_mlp(odc_ctx* ctx, const odc_field* field, int64_t n, int64_t* trace, int64_t trace_len);
 /* Same, labels only (u8), for host points. */
 int odc_eval_labels(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, uint8_t* labels);
+
+/* MLP parity hook: the fp32 head dot product h_7 . w_head (before b_head and
+ * the fp64 prior) of every point, as the tcgen05 evaluator computes it
+ * (bf16 operands, fp32 accumulation) -- compared against a bf16-emulating
+ * numpy reference in tests/test_gpu_mlp.py. */
+int odc_eval_mlp_dot(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, float* dot);
 
 /* numpy.linalg.eigh of n symmetric 3x3 matrices (row-major, 9 f64 each), as
  * solve_qef_batch calls it (dualize.py:358): LAPACK dsyevd('V', 'L') of

@@ -286,6 +286,39 @@ def mlp_logit_numpy(field, pts, chunk=1 << 16):
     return out
 
 
+def mlp_dot_bf16_numpy(field, pts, chunk=1 << 15):
+    """The head dot product h_7 . w_head as the device evaluator computes it
+    in exact arithmetic where it rounds: fp32 encoding x = (float)(p - 0.5)
+    and sin/cos(pi 2^k x) rounded to fp32, every layer input rounded to bf16
+    (RNE), products exact, sums in fp64 then rounded to fp32 (the tensor
+    core accumulates in fp32 in its own order), bias + ReLU, and the head in
+    fp32 activations (not bf16).  The device differs from this only by its
+    fp32 accumulation order and sincospif's last ulp (a bf16 rounding of an
+    activation may then fall the other way): tests/test_gpu_mlp.py bounds
+    the difference.  Test infrastructure only."""
+    from paper_2409_13418_b200.fields import bf16_round
+
+    pts = np.asarray(pts, dtype=np.float64).reshape(-1, 3)
+    out = np.empty(len(pts), dtype=np.float32)
+    W = [np.asarray(w, dtype=np.float64) for w in field.weights]
+    B = [np.asarray(b, dtype=np.float32) for b in field.biases]
+    wh = np.asarray(field.w_head, dtype=np.float64)
+    for s0 in range(0, len(pts), chunk):
+        x = (pts[s0:s0 + chunk] - 0.5).astype(np.float32)
+        feats = [x]
+        for k in range(field.n_freq):
+            arg = np.pi * (x.astype(np.float64) * (2.0**k))
+            feats.append(np.sin(arg).astype(np.float32))
+            feats.append(np.cos(arg).astype(np.float32))
+        h = bf16_round(np.concatenate(feats, axis=1)).astype(np.float64)
+        for i in range(len(W)):
+            acc = (h @ W[i]).astype(np.float32) + B[i]
+            acc = np.maximum(acc, np.float32(0))
+            h = (bf16_round(acc) if i + 1 < len(W) else acc).astype(np.float64)
+        out[s0:s0 + chunk] = (h @ wh).astype(np.float32)
+    return out
+
+
 def mlp_raw_numpy(field, pts):
     z = mlp_logit_numpy(field, pts)
     return 1.0 / (1.0 + np.exp(-np.clip(z, -500.0, 500.0)))

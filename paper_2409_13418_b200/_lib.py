@@ -89,7 +89,7 @@ EXPORTS = (
     "odc_slab_globalize", "odc_mesh_finish", "odc_profile_mlp", "odc_export_obj", "odc_export_ply",
     "odc_validate_manifold", "odc_validate_copy", "odc_count_self_intersections", "odc_self_intersection_pairs",
     "odc_mesh_distance", "odc_triangle_areas", "odc_field_mesh", "odc_field_voxels", "odc_eigh3",
-    "odc_eigh3_host",
+    "odc_eigh3_host", "odc_eval_mlp_dot",
 )
 
 _lib = None
@@ -131,6 +131,7 @@ def load():
         L.odc_eval_raw.argtypes = [vp, vp, vp, i64, vp]
         L.odc_eval_labels.argtypes = [vp, vp, vp, i64, vp]
         L.odc_eigh3.argtypes = [vp, vp, i64, vp, vp, vp]
+        L.odc_eval_mlp_dot.argtypes = [vp, vp, vp, i64, vp]
         L.odc_eigh3_host.argtypes = [vp, i64, vp, vp, vp]
         L.odc_extract_slab.argtypes = [vp, vp, P(dbl), P(dbl), i64, P(Options), i64, i64, P(Stats), P(SlabInfo)]
         L.odc_slab_globalize.argtypes = [vp, i64, i64, i64, vp]

@@ -95,16 +95,10 @@ struct odc_field {
   int32_t continuous = 0;
   double iso = 0.5;
   // MLP
-  uint16_t* w_packed = nullptr;
   uint16_t* w_tc = nullptr;
-  uint16_t* w_tc2 = nullptr;
   float* bias = nullptr;
   float* w_head = nullptr;
   MlpDev mlp{};
-  // host weights for the formats packed on first use (CTA-pair TS and SIMT evaluators)
-  std::vector<float> h_w0, h_wh;
-  int32_t h_din = 0;
-  std::mutex lazy;
   // mesh winding-number field (kind 2)
   WindDev wind{};
   void* wind_buf = nullptr;
@@ -132,10 +126,6 @@ struct odc_ctx {
   std::vector<cudaEvent_t> copy_evs;       // one per staged piece of a mesh copy
   std::string err;
   int launches = 0;
-  // odc_set_param("mlp_impl"): 3 CTA-pair N=256 ping-pong tcgen05 (default,
-  // fastest measured), 2 single-CTA tcgen05, 0 CTA-pair with A in TMEM,
-  // 1 SIMT reference
-  int mlp_impl = 3;
   int mlp_debug = 0;  // odc_set_param("mlp_debug"): profiling experiments, odc_profile_mlp only
   const double* profile_pts = nullptr;  // odc_set_param("profile_points"): host (n,3) points for odc_profile_mlp
   // last extraction
@@ -216,47 +206,15 @@ void check_status(odc_ctx* c, DevStatus* dst) {
 void run_mlp(odc_ctx* c, const odc_field* f, const PointSrc& src, int64_t n, uint8_t* lab, double* raw,
              cudaStream_t s, const MlpDev* override_md = nullptr) {
   MlpDev md = override_md ? *override_md : f->mlp;
-  if (!override_md) md.impl = c->mlp_impl;
   unsigned long long base0 = 0;
   md.sched = src.n_dev ? c->d_sched + 1 : c->d_sched;
   const int k = mlp_eval(md, src, n, lab, raw, s, src.n_dev ? &base0 : &c->sched_next);
   if (k < 0)
-    throw OdcError{ODC_E_CUDA, "MLP evaluator: no pair counter on this context, or a compacted batch on an "
-                               "evaluator other than mlp_impl 3"};
+    throw OdcError{ODC_E_CUDA, "MLP evaluator: no pair counter on this context or no weights"};
   if (k > 1) c->launches += k - 1;  // the caller's check_launch counts one
 }
 
 // Evaluate labels (and optionally raw) of n points through the field.
-// The CTA-pair TS (mlp_impl 0) and SIMT (1) evaluators read their own weight
-// layouts; those are packed and uploaded the first time a context selects
-// them (the default layout is uploaded with the field).
-void ensure_mlp_format(odc_ctx* c, const odc_field* fc) {
-  odc_field* f = const_cast<odc_field*>(fc);
-  if (f->kind != 1 || (c->mlp_impl != 0 && c->mlp_impl != 1)) return;
-  std::lock_guard<std::mutex> lock(f->lazy);
-  cudaStream_t s = c->stream;
-  if (c->mlp_impl == 0 && !f->w_tc2) {
-    std::vector<uint16_t> h(mlp_tc2_weight_elems());
-    mlp_pack_weights_tc2(f->h_w0.data(), f->h_din, f->h_wh.data(), h.data());
-    uint16_t* d = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&d, h.size() * 2, s));
-    CUDA_TRY(cudaMemcpyAsync(d, h.data(), h.size() * 2, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    f->w_tc2 = d;
-    f->mlp.w_tc2 = d;
-  }
-  if (c->mlp_impl == 1 && !f->w_packed) {
-    std::vector<uint16_t> h(mlp_packed_weight_elems());
-    mlp_pack_weights(f->h_w0.data(), f->h_din, f->h_wh.data(), h.data());
-    uint16_t* d = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&d, h.size() * 2, s));
-    CUDA_TRY(cudaMemcpyAsync(d, h.data(), h.size() * 2, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    f->w_packed = d;
-    f->mlp.w_packed = d;
-  }
-}
-
 void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* lab, double* raw,
                  const int64_t* n_dev = nullptr, const int32_t* out_map = nullptr) {
   if (n == 0) return;
@@ -273,7 +231,6 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
     PointSrc src{pts, GridP{}, 0};
     voxel_eval(f->vox, src, n, lab, raw, c->stream);
   } else {
-    ensure_mlp_format(c, f);
     PointSrc src{pts, GridP{}, 0};
     src.n_dev = n_dev;
     src.out_map = out_map;
@@ -372,6 +329,7 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
     int32_t* cur = need(c->arena.get<int32_t>(3 * T));
     CUDA_TRY(cudaMemcpyAsync(cur, tris, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
     double* cv = verts;
+    char* big = nullptr;  // scratch for fans of more than 64 triangles, allocated on first need
     int passes = 0;
     for (int pass = 0; pass < 4; pass++) {
       passes++;
@@ -389,19 +347,26 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
       scan1(c, deg, off, curV + 1, totals + 6);
       launch_vertex_fill(cur, T, off, cursor, inc, s);
       check_launch(c);
-      launch_repair_count(cv, cur, curV, off, inc, extra, dst, s);
+      launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s);
       check_launch(c);
+      if (!big) {  // fans of more than 64 triangles need global scratch: re-run with it
+        readback(c, &dst->repair_overflow, sizeof(unsigned long long));
+        if (c->h_pinned[0]) {
+          big = need(c->arena.get<char>(repair_scratch_bytes(T)));
+          CUDA_TRY(cudaMemsetAsync(&dst->repair_overflow, 0, sizeof(unsigned long long), s));
+          launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s);
+          check_launch(c);
+        }
+      }
       scan1(c, extra, eoff, curV + 1, totals + 7);
       readback(c, totals + 7, sizeof(unsigned long long));
       const int64_t E = (int64_t)c->h_pinned[0];
-      readback(c, &dst->repair_overflow, sizeof(unsigned long long));
-      if (c->h_pinned[0]) throw OdcError{ODC_E_CONTRACT, "repair: a vertex fan exceeds 64 triangles"};
       if (E == 0) break;
       int32_t* next = need(c->arena.get<int32_t>(3 * T));
       CUDA_TRY(cudaMemcpyAsync(next, cur, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
       int64_t* src_new = need(c->arena.get<int64_t>(E));
       c->dup_passes.push_back({src_new, curV, E});
-      launch_repair_apply(cv, cur, curV, off, inc, eoff, next, src_new, s);
+      launch_repair_apply(cv, cur, curV, off, inc, eoff, big, next, src_new, s);
       check_launch(c);
       double* nv = need(c->arena.get<double>(3 * (curV + E)));
       CUDA_TRY(cudaMemcpyAsync(nv, cv, sizeof(double) * 3 * curV, cudaMemcpyDeviceToDevice, s));
@@ -503,7 +468,6 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     } else if (f->kind == 3) {
       voxel_eval(f->vox, src, g.nz * g.S2, bytes, nullptr, s);
     } else {
-      ensure_mlp_format(c, f);
       run_mlp(c, f, src, g.nz * g.S2, bytes, nullptr, s);
     }
     check_launch(c);
@@ -773,7 +737,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       check_launch(c);
       // linear-scan steps evaluate only the instances (rays) still scanning
       // (CTA-pair evaluator only: it takes the count on the device)
-      const bool compact = f->kind == 1 && c->mlp_impl == 3;
+      const bool compact = f->kind == 1;
       int32_t* map = compact ? need(c->arena.get<int32_t>(2 * Q)) : nullptr;
       int64_t* cnt2 = compact ? need(c->arena.get<int64_t>(2)) : nullptr;
       bool packed = false;  // this step's points are compacted
@@ -1016,12 +980,16 @@ int odc_set_param(odc_ctx* c, const char* name, int64_t value) {
     c->mlp_debug = (int)value;
     return ODC_OK;
   }
-  if (std::strcmp(name, "profile_points") == 0) {  // profiling only: a host pointer, 0 = generated grid points
-    c->profile_pts = (const double*)(intptr_t)value;
+  if (std::strcmp(name, "mbar_timeout_ms") == 0 && value >= 0) {  // 0: the MLP evaluator's waits never trap
+    cudaSetDevice(c->device);
+    if (mlp_set_wait_timeout_ns((unsigned long long)value * 1000000ull) != 0) {
+      c->err = "mbar_timeout_ms: cudaMemcpyToSymbol failed";
+      return ODC_E_CUDA;
+    }
     return ODC_OK;
   }
-  if (std::strcmp(name, "mlp_impl") == 0 && value >= 0 && value <= 3) {
-    c->mlp_impl = (int)value;
+  if (std::strcmp(name, "profile_points") == 0) {  // profiling only: a host pointer, 0 = generated grid points
+    c->profile_pts = (const double*)(intptr_t)value;
     return ODC_OK;
   }
   c->err = std::string("unknown parameter ") + name;
@@ -1092,13 +1060,9 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
   f->kind = 1;
   f->continuous = 1;
   f->iso = 0.5;
-  // only the default evaluator's layout now; the others are packed on first use
   const size_t nt = mlp_tc_weight_elems();
   std::vector<uint16_t> packed_tc(nt);
   mlp_pack_weights_tc(d->w0, d->d_in, d->w_hidden, packed_tc.data());
-  f->h_w0.assign(d->w0, d->w0 + (size_t)d->d_in * 256);
-  f->h_wh.assign(d->w_hidden, d->w_hidden + (size_t)7 * 256 * 256);
-  f->h_din = d->d_in;
   // stream-ordered pool allocations: no driver round trip per field
   cudaStream_t s = c->stream;
   if (cudaMallocAsync((void**)&f->w_tc, nt * 2, s) != cudaSuccess ||
@@ -1116,9 +1080,7 @@ int odc_field_mlp(odc_ctx* c, const odc_mlp_desc* d, odc_field** out) {
     delete f;
     return ODC_E_CUDA;
   }
-  f->mlp.w_packed = f->w_packed;
   f->mlp.w_tc = f->w_tc;
-  f->mlp.w_tc2 = f->w_tc2;
   f->mlp.has_bias = 0;
   for (int i = 0; i < 8 * 256; i++)
     if (d->biases[i] != 0.f) f->mlp.has_bias = 1;
@@ -1244,13 +1206,13 @@ void odc_field_free(odc_ctx* c, odc_field* f) {
   if (!f) return;
   if (c) {
     cudaStreamSynchronize(c->stream);
-    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head, f->wind_buf,
+    void* bufs[] = {f->nodes, f->w_tc, f->bias, f->w_head, f->wind_buf,
                     (void*)f->vox.values};
     for (void* b : bufs)
       if (b) cudaFreeAsync(b, c->stream);  // back to the pool, no device-wide sync
   } else {
     cudaDeviceSynchronize();
-    void* bufs[] = {f->nodes, f->w_packed, f->w_tc, f->w_tc2, f->bias, f->w_head, f->wind_buf,
+    void* bufs[] = {f->nodes, f->w_tc, f->bias, f->w_head, f->wind_buf,
                     (void*)f->vox.values};
     for (void* b : bufs)
       if (b) cudaFreeAsync(b, 0);
@@ -1965,14 +1927,7 @@ int odc_profile_mlp(odc_ctx* c, const odc_field* f, int64_t n, int64_t* trace, i
     g.lo[a] = 0.0;
     g.h[a] = 1.0 / (double)g.R;
   }
-  try {
-    ensure_mlp_format(c, f);
-  } catch (const OdcError& e) {
-    c->err = e.msg;
-    return e.code;
-  }
   MlpDev md = f->mlp;
-  md.impl = c->mlp_impl;
   md.debug = c->mlp_debug & 63;
   md.trace = (c->mlp_debug & 64) ? nullptr : dt;  // 64: time the kernel without the trace hooks
   const int64_t np = n < g.S3 ? n : g.S3;
@@ -2008,6 +1963,35 @@ int odc_eval_raw(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, d
 }
 int odc_eval_labels(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* labels) {
   return eval_common(c, f, pts, n, nullptr, labels);
+}
+
+struct DotArgs {
+  const odc_field* f;
+  const double* pts;
+  int64_t n;
+  float* dot;
+};
+int odc_eval_mlp_dot(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, float* dot) {
+  if (!c || !f || f->kind != 1 || n < 0 || (n && (!pts || !dot))) return ODC_E_ARG;
+  DotArgs a{f, pts, n, dot};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    DotArgs* x = (DotArgs*)p;
+    if (x->n == 0) return (int)ODC_OK;
+    cc->valid = false;
+    cc->arena.reset();
+    double* dp = need(cc->arena.get<double>(3 * x->n));
+    uint8_t* dl = need(cc->arena.get<uint8_t>(x->n));
+    float* dd = need(cc->arena.get<float>(x->n));
+    CUDA_TRY(cudaMemcpyAsync(dp, x->pts, sizeof(double) * 3 * x->n, cudaMemcpyHostToDevice, cc->stream));
+    PointSrc src{dp, GridP{}, 0};
+    src.dot_out = dd;
+    run_mlp(cc, x->f, src, x->n, dl, nullptr, cc->stream);
+    check_launch(cc);
+    CUDA_TRY(cudaMemcpyAsync(x->dot, dd, sizeof(float) * x->n, cudaMemcpyDeviceToHost, cc->stream));
+    CUDA_TRY(cudaStreamSynchronize(cc->stream));
+    return (int)ODC_OK;
+  }, &a);
 }
 
 struct Eigh3Args {

@@ -1776,11 +1776,60 @@ void launch_vertex_fill(const int32_t* tris, int64_t T, const uint32_t* off, uin
   if (T) k_vertex_fill<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, off, cursor, inc);
 }
 
+// Scratch of one fan (nt incident triangles).  Fans of up to kMaxFan
+// triangles live in the thread's local arrays; a larger fan (no cap in the
+// reference, polygonize.py:308-358) uses a global-memory region sized by its
+// degree: the region of vertex v starts at byte kFanSlotBytes * off[v] of
+// the CSR incidence offsets, so no separate allocation pass is needed.
+constexpr int kFanSlotBytes = 72;  // 4 doubles + 9 ints + 1 bool per incident triangle, rounded to 8
+struct FanScratch {
+  double* rel;  // [3 nt]
+  double* th;   // [nt]
+  int32_t* tl;  // [nt]
+  int* parent;
+  int* mem;
+  int* order;
+  int* root_comp;
+  int* comp;
+  int32_t* nb;  // [2 nt]
+  int* pa;      // [nt / 2]
+  int* pb;      // [nt / 2]
+  bool* fwd;    // [nt]
+};
+struct FanLocal {
+  double rel[3 * kMaxFan], th[kMaxFan];
+  int32_t tl[kMaxFan];
+  int parent[kMaxFan], mem[kMaxFan], order[kMaxFan], root_comp[kMaxFan], comp[kMaxFan];
+  int32_t nb[2 * kMaxFan];
+  int pa[kMaxFan / 2], pb[kMaxFan / 2];
+  bool fwd[kMaxFan];
+  __device__ FanScratch view() { return {rel, th, tl, parent, mem, order, root_comp, comp, nb, pa, pb, fwd}; }
+};
+__device__ __forceinline__ FanScratch fan_global(char* base, uint32_t start, int nt) {
+  char* p = base + (size_t)kFanSlotBytes * start;
+  FanScratch f;
+  f.rel = (double*)p;
+  f.th = f.rel + 3 * nt;
+  int* ip = (int*)(f.th + nt);
+  f.tl = ip;
+  f.parent = ip + nt;
+  f.mem = ip + 2 * nt;
+  f.order = ip + 3 * nt;
+  f.root_comp = ip + 4 * nt;
+  f.comp = ip + 5 * nt;
+  f.nb = ip + 6 * nt;
+  f.pa = ip + 8 * nt;
+  f.pb = f.pa + nt / 2;
+  f.fwd = (bool*)(ip + 9 * nt);
+  return f;
+}
+
 // components of vertex v's fan; comp[i] in first-appearance order (= order
 // of the minimum triangle id, since tl is ascending)
 static __device__ int fan_components(const double* __restrict__ verts, const int32_t* __restrict__ tris, int32_t v,
-                              const int32_t* tl, int nt, int* comp) {
-  int parent[kMaxFan];
+                                     int nt, FanScratch& f) {
+  const int32_t* tl = f.tl;
+  int* parent = f.parent;
   for (int i = 0; i < nt; i++) parent[i] = i;
   auto find = [&](int x) {
     while (parent[x] != x) {
@@ -1794,7 +1843,7 @@ static __device__ int fan_components(const double* __restrict__ verts, const int
     if (rx != ry) parent[rx] = ry;
   };
   // neighbours u: for each, the local triangle indices containing edge (v,u)
-  int32_t nb[2 * kMaxFan];
+  int32_t* nb = f.nb;
   int nnb = 0;
   for (int i = 0; i < nt; i++) {
     const int32_t* t = tris + 3 * (int64_t)tl[i];
@@ -1804,12 +1853,12 @@ static __device__ int fan_components(const double* __restrict__ verts, const int
       bool seen = false;
       for (int j = 0; j < nnb; j++)
         if (nb[j] == u) seen = true;
-      if (!seen && nnb < 2 * kMaxFan) nb[nnb++] = u;
+      if (!seen) nb[nnb++] = u;  // at most 2 per triangle
     }
   }
+  int* mem = f.mem;
   for (int j = 0; j < nnb; j++) {
     const int32_t u = nb[j];
-    int mem[kMaxFan];
     int nm = 0;
     for (int i = 0; i < nt; i++) {
       const int32_t* t = tris + 3 * (int64_t)tl[i];
@@ -1825,8 +1874,8 @@ static __device__ int fan_components(const double* __restrict__ verts, const int
       double an = sqrt(dot3_fma(axis, axis));
       if (an == 0.0) an = 1.0;
       for (int c = 0; c < 3; c++) axis[c] /= an;
-      double rel[kMaxFan][3];
-      bool fwd[kMaxFan];
+      double* rel = f.rel;
+      bool* fwd = f.fwd;
       for (int m = 0; m < nm; m++) {
         const int32_t* t = tris + 3 * (int64_t)tl[mem[m]];
         int32_t other = -1;
@@ -1835,7 +1884,7 @@ static __device__ int fan_components(const double* __restrict__ verts, const int
         double rr[3];
         for (int c = 0; c < 3; c++) rr[c] = verts[3 * (int64_t)other + c] - verts[3 * (int64_t)a + c];
         const double pr = dot3_fma(rr, axis);
-        for (int c = 0; c < 3; c++) rel[m][c] = rr[c] - axis[c] * pr;
+        for (int c = 0; c < 3; c++) rel[3 * m + c] = rr[c] - axis[c] * pr;
         // direction of the slot holding edge (a,b): e0 < e1 (polygonize.py:229)
         bool d = false;
         for (int c = 0; c < 3; c++) {
@@ -1844,16 +1893,16 @@ static __device__ int fan_components(const double* __restrict__ verts, const int
         }
         fwd[m] = d;
       }
-      double ref[3] = {rel[0][0], rel[0][1], rel[0][2]};
+      double ref[3] = {rel[0], rel[1], rel[2]};
       double rn = sqrt(dot3_fma(ref, ref));
       if (rn == 0.0) rn = 1.0;
       for (int c = 0; c < 3; c++) ref[c] /= rn;
       double perp[3];
       cross3(axis, ref, perp);
-      double th[kMaxFan];
-      int order[kMaxFan];
+      double* th = f.th;
+      int* order = f.order;
       for (int m = 0; m < nm; m++) {
-        th[m] = atan2(dot3_fma(rel[m], perp), dot3_fma(rel[m], ref));
+        th[m] = atan2(dot3_fma(rel + 3 * m, perp), dot3_fma(rel + 3 * m, ref));
         order[m] = m;
       }
       for (int x = 1; x < nm; x++) {  // stable insertion sort
@@ -1867,7 +1916,7 @@ static __device__ int fan_components(const double* __restrict__ verts, const int
       }
       // _pair_fan_triangles (polygonize.py:233-250)
       const int np = nm / 2;
-      int pa[kMaxFan / 2], pb[kMaxFan / 2];
+      int *pa = f.pa, *pb = f.pb;
       bool done = false;
       const int nstarts = (nm % 2 == 0) ? 2 : 1;
       for (int st = 0; st < nstarts && !done; st++) {
@@ -1887,21 +1936,21 @@ static __device__ int fan_components(const double* __restrict__ verts, const int
       for (int i = 0; i < np; i++) unite(mem[pa[i]], mem[pb[i]]);
     }
   }
-  int root_comp[kMaxFan];
+  int* root_comp = f.root_comp;
   for (int i = 0; i < nt; i++) root_comp[i] = -1;
   int ncomp = 0;
   for (int i = 0; i < nt; i++) {
     const int r = find(i);
     if (root_comp[r] < 0) root_comp[r] = ncomp++;
-    comp[i] = root_comp[r];
+    f.comp[i] = root_comp[r];
   }
   return ncomp;
 }
 
+// vertex v's incident triangles, ascending, into f.tl; returns the count
 __device__ __forceinline__ int load_fan(const uint32_t* off, const int32_t* inc, int64_t v, int32_t* tl) {
   const uint32_t b = off[v], e = off[v + 1];
-  int nt = (int)(e - b);
-  if (nt > kMaxFan) return -1;
+  const int nt = (int)(e - b);
   for (int i = 0; i < nt; i++) tl[i] = inc[b + i];
   for (int x = 1; x < nt; x++) {  // ascending triangle ids
     int32_t key = tl[x];
@@ -1915,58 +1964,74 @@ __device__ __forceinline__ int load_fan(const uint32_t* off, const int32_t* inc,
   return nt;
 }
 
+// The fan of vertex v in local arrays, or (more than kMaxFan triangles) in
+// its global scratch region; returns false when the fan is large and no
+// scratch was provided (the host then re-runs with scratch).
+__device__ __forceinline__ bool fan_scratch(const uint32_t* off, int64_t v, char* big, FanLocal& loc, FanScratch& f) {
+  const int nt = (int)(off[v + 1] - off[v]);
+  if (nt <= kMaxFan) {
+    f = loc.view();
+    return true;
+  }
+  if (!big) return false;
+  f = fan_global(big, off[v], nt);
+  return true;
+}
+
 __global__ void __launch_bounds__(128) k_repair_count(const double* __restrict__ verts,
                                                       const int32_t* __restrict__ tris, int64_t V,
                                                       const uint32_t* __restrict__ off,
                                                       const int32_t* __restrict__ inc, uint32_t* __restrict__ extra,
-                                                      DevStats* st) {
+                                                      char* big, DevStats* st) {
   int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
-  int32_t tl[kMaxFan];
-  const int nt = load_fan(off, inc, v, tl);
-  uint32_t ex = 0;
-  if (nt < 0) {
+  FanLocal loc;
+  FanScratch f;
+  if (!fan_scratch(off, v, big, loc, f)) {
     atomicAdd(&st->repair_overflow, 1ull);
-  } else if (nt > 1) {
-    int comp[kMaxFan];
-    const int nc = fan_components(verts, tris, (int32_t)v, tl, nt, comp);
-    ex = (uint32_t)(nc - 1);
+    return;
   }
+  const int nt = load_fan(off, inc, v, f.tl);
+  uint32_t ex = 0;
+  if (nt > 1) ex = (uint32_t)(fan_components(verts, tris, (int32_t)v, nt, f) - 1);
   extra[v] = ex;
 }
 void launch_repair_count(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off, const int32_t* inc,
-                         uint32_t* extra, DevStats* st, cudaStream_t s) {
-  if (V) k_repair_count<<<grid_for(V, 128), 128, 0, s>>>(verts, tris, V, off, inc, extra, st);
+                         uint32_t* extra, char* big, DevStats* st, cudaStream_t s) {
+  if (V) k_repair_count<<<grid_for(V, 128), 128, 0, s>>>(verts, tris, V, off, inc, extra, big, st);
 }
+size_t repair_scratch_bytes(int64_t T) { return (size_t)kFanSlotBytes * 3 * (size_t)T; }
 
 __global__ void __launch_bounds__(128) k_repair_apply(const double* __restrict__ verts,
                                                       const int32_t* __restrict__ tris, int64_t V,
                                                       const uint32_t* __restrict__ off,
                                                       const int32_t* __restrict__ inc,
-                                                      const uint32_t* __restrict__ extra_off,
+                                                      const uint32_t* __restrict__ extra_off, char* big,
                                                       int32_t* __restrict__ tris_next,
                                                       int64_t* __restrict__ src_of_new) {
   int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
   const uint32_t e0 = extra_off[v], e1 = extra_off[v + 1];
   if (e1 == e0) return;
-  int32_t tl[kMaxFan];
-  const int nt = load_fan(off, inc, v, tl);
-  if (nt < 0) return;
-  int comp[kMaxFan];
-  fan_components(verts, tris, (int32_t)v, tl, nt, comp);
+  FanLocal loc;
+  FanScratch f;
+  if (!fan_scratch(off, v, big, loc, f)) return;  // (unreachable: count ran with the same scratch)
+  const int nt = load_fan(off, inc, v, f.tl);
+  fan_components(verts, tris, (int32_t)v, nt, f);
   for (uint32_t x = e0; x < e1; x++) src_of_new[x] = v;
   for (int i = 0; i < nt; i++) {
-    if (comp[i] == 0) continue;
-    const int32_t nv = (int32_t)(V + e0 + comp[i] - 1);
-    const int64_t t = tl[i];
+    if (f.comp[i] == 0) continue;
+    const int32_t nv = (int32_t)(V + e0 + f.comp[i] - 1);
+    const int64_t t = f.tl[i];
     for (int c = 0; c < 3; c++)
       if (tris[3 * t + c] == (int32_t)v) tris_next[3 * t + c] = nv;
   }
 }
 void launch_repair_apply(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off, const int32_t* inc,
-                         const uint32_t* extra_off, int32_t* tris_next, int64_t* src_of_new, cudaStream_t s) {
-  if (V) k_repair_apply<<<grid_for(V, 128), 128, 0, s>>>(verts, tris, V, off, inc, extra_off, tris_next, src_of_new);
+                         const uint32_t* extra_off, char* big, int32_t* tris_next, int64_t* src_of_new,
+                         cudaStream_t s) {
+  if (V) k_repair_apply<<<grid_for(V, 128), 128, 0, s>>>(verts, tris, V, off, inc, extra_off, big, tris_next,
+                                                         src_of_new);
 }
 
 __global__ void k_copy_vertices(const double* __restrict__ src, const int64_t* __restrict__ src_of, int64_t base,

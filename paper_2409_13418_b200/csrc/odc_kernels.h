@@ -162,11 +162,15 @@ void launch_interior_flags(int64_t K, const uint8_t* kase, uint32_t* flag, cudaS
 void launch_vertex_degree(const int32_t* tris, int64_t T, uint32_t* deg, cudaStream_t s);
 void launch_vertex_fill(const int32_t* tris, int64_t T, const uint32_t* off, uint32_t* cursor, int32_t* inc,
                         cudaStream_t s);
+// big: per-incidence scratch for fans of more than 64 triangles (nullptr: such
+// vertices are counted in DevStats::repair_overflow and skipped; the host
+// then re-runs with repair_scratch_bytes(T) of scratch)
 void launch_repair_count(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off,
-                         const int32_t* inc, uint32_t* extra, DevStats* st, cudaStream_t s);
+                         const int32_t* inc, uint32_t* extra, char* big, DevStats* st, cudaStream_t s);
+size_t repair_scratch_bytes(int64_t T);
 void launch_repair_apply(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off,
-                         const int32_t* inc, const uint32_t* extra_off, int32_t* tris_next, int64_t* src_of_new,
-                         cudaStream_t s);
+                         const int32_t* inc, const uint32_t* extra_off, char* big, int32_t* tris_next,
+                         int64_t* src_of_new, cudaStream_t s);
 void launch_copy_vertices(const double* src, const int64_t* src_of, int64_t base, int64_t n, double* dst,
                           cudaStream_t s);
 

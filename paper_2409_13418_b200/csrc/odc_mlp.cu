@@ -11,7 +11,7 @@
 
 #include "odc_mlp.h"
 #include "odc_mlp_tc.cuh"
-#include "odc_mlp_tc2.cuh"
+#include "odc_mlp_tc2.cuh"  // cluster helpers (mapa, named barriers, pair commits) used by k_mlp_tc4
 
 namespace odc {
 
@@ -25,27 +25,13 @@ namespace odc {
 constexpr int kWidth = 256;
 constexpr int kDepth = 8;
 constexpr int kDin = 39;
-constexpr int kDinPad = 64;
 static_assert(kDin <= 48, "tc4 skips layer-0 K-step 3 (features 48..63 are padding)");
-constexpr int kPts = 32;  // points per block (SIMT evaluator)
-
-size_t mlp_packed_weight_elems() { return (size_t)kDinPad * kWidth + (size_t)(kDepth - 1) * kWidth * kWidth; }
 
 static uint16_t f2bf(float f) {  // inputs are already bf16-representable
   uint32_t u;
   std::memcpy(&u, &f, 4);
   return (uint16_t)(u >> 16);
 }
-
-// row-major W[k][n] per layer; layer 0 zero-padded to K = 64
-void mlp_pack_weights(const float* w0, int d_in, const float* w_hidden, uint16_t* out) {
-  for (int k = 0; k < kDinPad; k++)
-    for (int n = 0; n < kWidth; n++) out[(size_t)k * kWidth + n] = k < d_in ? f2bf(w0[(size_t)k * kWidth + n]) : 0;
-  uint16_t* o = out + (size_t)kDinPad * kWidth;
-  for (size_t i = 0; i < (size_t)(kDepth - 1) * kWidth * kWidth; i++) o[i] = f2bf(w_hidden[i]);
-}
-
-__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 __device__ __forceinline__ void point_of(const PointSrc& s, int64_t i, double p[3]) {
   if (s.pts) {
@@ -54,77 +40,6 @@ __device__ __forceinline__ void point_of(const PointSrc& s, int64_t i, double p[
     p[2] = s.pts[3 * i + 2];
   } else {
     vposition(s.grid, s.begin + i, p);
-  }
-}
-
-// positional encoding gamma(p - 0.5): [x(3), sin_0(3), cos_0(3), ..., sin_5(3), cos_5(3)]
-__device__ __forceinline__ float pe_feature(const double p[3], int j) {
-  if (j >= kDin) return 0.f;
-  if (j < 3) return (float)(p[j] - 0.5);
-  const int k = (j - 3) / 6, r = (j - 3) % 6, c = r % 3;
-  const float x = (float)(p[c] - 0.5);
-  float sv, cv;
-  sincospif(x * (float)(1 << k), &sv, &cv);
-  return r < 3 ? sv : cv;
-}
-
-__global__ void __launch_bounds__(kWidth) k_mlp_simt(MlpDev m, PointSrc src, int64_t n, uint8_t* __restrict__ labels,
-                                                     double* __restrict__ raw) {
-  __shared__ float h[kPts][kWidth];
-  __shared__ float red[kPts][kWidth / 32];
-  const int64_t p0 = (int64_t)blockIdx.x * kPts;
-  const int j = threadIdx.x;
-  for (int t = j; t < kPts * kDinPad; t += kWidth) {
-    const int pi = t / kDinPad, f = t % kDinPad;
-    float v = 0.f;
-    if (p0 + pi < n) {
-      double p[3];
-      point_of(src, p0 + pi, p);
-      v = pe_feature(p, f);
-    }
-    h[pi][f] = bf16r(v);
-  }
-  __syncthreads();
-  const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(m.w_packed);
-  float acc[kPts];
-  for (int layer = 0; layer < kDepth; layer++) {
-    const int K = layer == 0 ? kDinPad : kWidth;
-    for (int pi = 0; pi < kPts; pi++) acc[pi] = 0.f;
-    for (int k = 0; k < K; k++) {
-      const float w = __bfloat162float(W[(size_t)k * kWidth + j]);
-#pragma unroll
-      for (int pi = 0; pi < kPts; pi++) acc[pi] = fmaf(h[pi][k], w, acc[pi]);
-    }
-    W += (size_t)K * kWidth;
-    const float b = m.bias[layer * kWidth + j];
-    __syncthreads();
-    for (int pi = 0; pi < kPts; pi++) {
-      float v = acc[pi] + b;
-      v = v > 0.f ? v : 0.f;
-      h[pi][j] = layer == kDepth - 1 ? v : bf16r(v);
-    }
-    __syncthreads();
-  }
-  // head: fp32 dot product, fixed order (per-warp partials then warps in order)
-  const float wh = m.w_head[j];
-  for (int pi = 0; pi < kPts; pi++) {
-    float v = h[pi][j] * wh;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if ((j & 31) == 0) red[pi][j >> 5] = v;
-  }
-  __syncthreads();
-  if (j < kPts && p0 + j < n) {
-    float s = 0.f;
-    for (int w = 0; w < kWidth / 32; w++) s += red[j][w];
-    const double mlp = (double)(s + m.b_head);
-    double p[3];
-    point_of(src, p0 + j, p);
-    double d[3] = {p[0] - m.prior_center[0], p[1] - m.prior_center[1], p[2] - m.prior_center[2]};
-    const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
-    const double logit = m.amplitude * mlp - m.prior_scale * (dist - m.prior_radius);
-    const double r = 1.0 / (1.0 + exp(-logit));
-    labels[p0 + j] = r > 0.5 ? 1 : 0;
-    if (raw) raw[p0 + j] = r;
   }
 }
 
@@ -219,19 +134,6 @@ __device__ __forceinline__ void relu_pack32(const uint32_t (&v)[32], const float
     out[j] = relu_pack(a, b);
   }
 }
-template <bool kBias>
-__device__ __forceinline__ float head32(const uint32_t (&v)[32], const float* __restrict__ sb,
-                                        const float* __restrict__ sw, float dot) {
-#pragma unroll
-  for (int j = 0; j < 32; j++) {
-    float a = __uint_as_float(v[j]);
-    if (kBias) a += sb[j];
-    a = a > 0.f ? a : 0.f;
-    dot = fmaf(a, sw[j], dot);
-  }
-  return dot;
-}
-
 // The CTA-pair evaluator's head: relu(acc) . w over 32 columns with packed
 // FFMA2 (even and odd columns in the two lanes of a 64-bit accumulator;
 // the head is ALU-issue-bound on the pair boundary's critical path)
@@ -324,6 +226,7 @@ __device__ __forceinline__ void finish_label(const MlpDev& m, const PointSrc& sr
                                              uint8_t* __restrict__ labels, double* __restrict__ raw) {
   if (p < 0 || p >= n) return;
   const int64_t o = src.out_map ? (int64_t)src.out_map[p] : p;  // output slot
+  if (src.dot_out) src.dot_out[o] = dot;  // parity hook: the fp32 head dot of every point
   if (!raw) {
     float xf[3];
     if (src.pts) {
@@ -377,569 +280,6 @@ __global__ void k_mlp_fixup(MlpDev m, PointSrc src, int64_t n_launch, uint8_t* _
   if (labels[o] == 2) label_fp64(m, src, p, o, src.defer_dot[p], labels, nullptr);
 }
 
-template <bool kBias, bool kTrace>
-__global__ void __launch_bounds__(tc::kThreads, 1) k_mlp_tc(MlpDev m, PointSrc src, int64_t n,
-                                                           uint8_t* __restrict__ labels, double* __restrict__ raw) {
-  using namespace tc;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* A0 = smem;
-  uint8_t* Wst = smem + 2 * kTileABytes;
-  uint64_t* bars = (uint64_t*)(Wst + kStages * kChunkBytes);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + kStages;
-  uint64_t* acc_full = bars + 2 * kStages;
-  uint64_t* a_ready = acc_full + 2;  // [0]: K-atom 0 of A written, D half 0 drained; [1]: K-atoms 2-3, D half 1
-  uint64_t* a_rk1 = a_ready + 2;     // K-atom 1 of A written
-  uint32_t* tmem_slot = (uint32_t*)(a_rk1 + 1);
-  float* s_bias = (float*)(Wst + kStages * kChunkBytes + 256);  // (8, 256)
-  float* s_head = s_bias + kDepth * kWidth;                      // (256)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t npairs = (n + 255) / 256;
-  const int dbg = kTrace ? m.debug : 0;  // profiling experiments only
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; s++) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(&acc_full[0], 1);
-    mbar_init(&acc_full[1], 1);
-    mbar_init(&a_ready[0], 256);
-    mbar_init(&a_ready[1], 256);
-    mbar_init(a_rk1, 256);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = threadIdx.x; i < kDepth * kWidth; i += blockDim.x) s_bias[i] = m.bias[i];
-  for (int i = threadIdx.x; i < kWidth; i += blockDim.x) s_head[i] = m.w_head[i];
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0 && !(dbg & 16)) {
-    {  // ---- weight producer (whole warp, one elected lane issues)
-      uint32_t g = 0;
-      for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x)
-        for (int i = 0; i < kChunksPerPair; i++, g++) {
-          const uint32_t s = g % kStages, ph = (g / kStages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          if (elect_one()) {
-            if ((dbg & 1) && g >= (uint32_t)kStages) {
-              mbar_arrive(&full[s]);  // experiment: stale weights, no L2 traffic
-            } else {
-              mbar_expect_tx(&full[s], kChunkBytes);
-              bulk_g2s(Wst + s * kChunkBytes, m.w_tc + (size_t)i * 128 * 64, kChunkBytes, &full[s]);
-            }
-          }
-          __syncwarp();
-        }
-    }
-  } else if (warp == 1) {
-    // ---- MMA issuer.  The whole warp walks the loop (operands stay in uniform
-    // registers); one elected lane issues.  Descriptors are built from a base
-    // low word plus compile-time offsets, so a chunk of 8 MMAs costs a handful
-    // of uniform adds -- the issue path must stay well under the 512 cycles
-    // the tensor pipe spends on a chunk.
-    const uint32_t a_lo = desc_lo(smem_u32(A0));
-    const uint32_t w_lo = desc_lo(smem_u32(Wst));
-    uint32_t s = 0, ph = 0, ra0 = 0, ra1 = 0, rk1 = 0;
-    int ti = 0;
-    auto wait_a = [&](uint64_t* bar, uint32_t& cnt) {
-      if (!(dbg & 8)) mbar_wait(bar, cnt & 1);
-      cnt++;
-      tc_fence_after();
-    };
-    // one weight chunk: 2 tiles x 4 K-steps of M128 N128 K16
-    auto chunk = [&](int nh, auto kc_c, long long& wfull) {
-      constexpr int kc = decltype(kc_c)::value;
-      const long long w0 = kTrace ? clock64() : 0;
-      if (!(dbg & 16)) mbar_wait(&full[s], ph);
-      if (kTrace) wfull += clock64() - w0;
-      const uint32_t b_lo = w_lo + s * (kChunkBytes >> 4);
-      if (elect_one()) {
-#pragma unroll
-        for (int t = 0; t < 2; t++) {
-          const uint32_t d = tmem + t * 256 + nh * 128;
-#pragma unroll
-          for (int ks = 0; ks < 4; ks++)
-            umma_bf16(d, make_desc(a_lo + ((t * kTileABytes + kc * 16384 + ks * 32) >> 4)),
-                      make_desc(b_lo + ((ks * 32) >> 4)), (kc | ks) != 0);
-        }
-        umma_commit(&empty[s]);
-      }
-      __syncwarp();
-      if (++s == kStages) {
-        s = 0;
-        ph ^= 1;
-      }
-    };
-    for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x, ti++) {
-      for (int l = 0; l < kDepth; l++) {
-        long long wfull = 0;
-#pragma unroll
-        for (int nh = 0; nh < 2; nh++) {
-          if (nh == 0) {
-            if (kTrace && lane == 0) ODC_TRACE(ti, l, 0);
-            wait_a(&a_ready[0], ra0);
-            if (kTrace && lane == 0) ODC_TRACE(ti, l, 1);
-          }
-          if (l == 0 && nh == 1 && ti > 0) wait_a(&a_ready[1], ra1);  // D half 1 drained by layer 7
-          chunk(nh, std::integral_constant<int, 0>{}, wfull);
-          if (l > 0) {
-            if (nh == 0) wait_a(a_rk1, rk1);
-            chunk(nh, std::integral_constant<int, 1>{}, wfull);
-            if (nh == 0) {
-              if (kTrace && lane == 0) ODC_TRACE(ti, l, 2);
-              wait_a(&a_ready[1], ra1);
-              if (kTrace && lane == 0) ODC_TRACE(ti, l, 3);
-            }
-            chunk(nh, std::integral_constant<int, 2>{}, wfull);
-            chunk(nh, std::integral_constant<int, 3>{}, wfull);
-          }
-          if (elect_one()) umma_commit(&acc_full[nh]);
-          __syncwarp();
-          if (kTrace && lane == 0) ODC_TRACE(ti, l, 4 + nh);
-        }
-        if (kTrace && lane == 0 && blockIdx.x == 0 && ti < 2) m.trace[(ti * 8 + l) * 16 + 12] = wfull;
-      }
-    }
-  } else if (warp >= 4 && !(dbg & 32)) {  // ---- epilogue: 2 tiles x 128 rows
-    const int et = threadIdx.x - 128;
-    const int t = et >> 7;
-    const int q = warp & 3;
-    const int r = 32 * q + lane;
-    const uint32_t a_t = smem_u32(A0 + t * kTileABytes);
-    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + t * 256;
-    uint32_t af0 = 0, af1 = 0;
-    uint32_t pe[32];
-    if ((int64_t)blockIdx.x < npairs) {
-      pe_row_packed(src, n, (int64_t)blockIdx.x * 256 + t * 128 + r, pe);
-      store_pe_row(pe, a_t, r);
-      fence_proxy_async();
-      mbar_arrive(&a_ready[0]);
-    }
-    int ti = 0;
-    const bool tr = kTrace && et == 0;
-    int64_t p_prev = -1;
-    float dot_prev = 0.f;
-    for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x, ti++) {
-      float dot = 0.f;
-      const int64_t next = pair + gridDim.x;
-      for (int l = 0; l < kDepth; l++) {
-        const float* bl = s_bias + l * kWidth;
-        if (l == kDepth - 1 && next < npairs)  // hide the next tile's encoding behind layer 7's MMAs
-          pe_row_packed(src, n, next * 256 + t * 128 + r, pe);
-        if (l == 1) {
-          if (tr) ODC_TRACE(ti, l, 13);
-          finish_label(m, src, n, p_prev, dot_prev, labels, raw);
-          p_prev = -1;
-          if (tr) ODC_TRACE(ti, l, 14);
-        }
-        if (tr) ODC_TRACE(ti, l, 6);
-        if (!(dbg & 8)) mbar_wait(&acc_full[0], af0 & 1);
-        af0++;
-        tc_fence_after();
-        if (tr) ODC_TRACE(ti, l, 8);
-        uint32_t pk[64];
-        if (l < kDepth - 1) {
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            uint32_t v[32];
-            if (dbg & 4) {
-#pragma unroll
-              for (int j = 0; j < 32; j++) v[j] = j;
-            } else {
-              ODC_TMEM_LD32(trow + 32 * i, v);
-              tmem_ld_wait();
-            }
-            relu_pack32<kBias>(v, bl + 32 * i, pk + 16 * i);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            uint32_t v[32];
-            if (dbg & 4) {
-#pragma unroll
-              for (int j = 0; j < 32; j++) v[j] = j;
-            } else {
-              ODC_TMEM_LD32(trow + 32 * i, v);
-              tmem_ld_wait();
-            }
-            dot = head32<kBias>(v, bl + 32 * i, s_head + 32 * i, dot);
-          }
-        }
-        if (tr) ODC_TRACE(ti, l, 7);
-        if (!(dbg & 8)) mbar_wait(&acc_full[1], af1 & 1);
-        af1++;
-        tc_fence_after();
-        if (tr) ODC_TRACE(ti, l, 9);
-        if (l < kDepth - 1) {
-          // half 0 -> A columns 0..127 (K-atoms 0, 1); the layer's MMAs are done
-          // half 0 -> A K-atom 0 (the next layer's first chunk), release, then K-atom 1
-          if (!(dbg & 2)) {
-#pragma unroll
-            for (int c = 0; c < 8; c++)
-              st_shared_v4(a_t + sw128_off(r, c), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-          }
-          fence_proxy_async();
-          tc_fence_before();
-          mbar_arrive(&a_ready[0]);
-          if (!(dbg & 2)) {
-#pragma unroll
-            for (int c = 8; c < 16; c++)
-              st_shared_v4(a_t + 16384 + sw128_off(r, c & 7), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-          }
-          fence_proxy_async();
-          mbar_arrive(a_rk1);
-          if (tr) ODC_TRACE(ti, l, 10);
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            uint32_t v[32];
-            if (dbg & 4) {
-#pragma unroll
-              for (int j = 0; j < 32; j++) v[j] = j;
-            } else {
-              ODC_TMEM_LD32(trow + 128 + 32 * i, v);
-              tmem_ld_wait();
-            }
-            uint32_t w[16];
-            relu_pack32<kBias>(v, bl + 128 + 32 * i, w);
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-              const int cc = 4 * i + c;  // chunk within columns 128..255
-              if (!(dbg & 2)) st_shared_v4(a_t + (2 + (cc >> 3)) * 16384 + sw128_off(r, cc & 7), w[4 * c], w[4 * c + 1],
-                           w[4 * c + 2], w[4 * c + 3]);
-            }
-          }
-          fence_proxy_async();
-          tc_fence_before();
-          mbar_arrive(&a_ready[1]);
-          if (tr) ODC_TRACE(ti, l, 11);
-        } else {
-          // layer 7: the MMAs are done with A -> the next tile pair's encoding
-          // goes in now, before the half-1 head, so its layer 0 starts at once
-          if (next < npairs) {
-            store_pe_row(pe, a_t, r);
-            fence_proxy_async();
-            tc_fence_before();
-            mbar_arrive(&a_ready[0]);
-          }
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            uint32_t v[32];
-            if (dbg & 4) {
-#pragma unroll
-              for (int j = 0; j < 32; j++) v[j] = j;
-            } else {
-              ODC_TMEM_LD32(trow + 128 + 32 * i, v);
-              tmem_ld_wait();
-            }
-            dot = head32<kBias>(v, bl + 128 + 32 * i, s_head + 128 + 32 * i, dot);
-          }
-          if (next < npairs) {  // D half 1 drained: the next pair's layer 0 may overwrite it
-            tc_fence_before();
-            mbar_arrive(&a_ready[1]);
-          }
-        }
-      }
-      // the label of this point is finished during the next pair's layer 1
-      // (the epilogue idles there while the MMAs run), keeping this pair's
-      // tail off the critical path into the next pair's layer 0
-      p_prev = pair * 256 + t * 128 + r;
-      dot_prev = dot;
-    }
-    finish_label(m, src, n, p_prev, dot_prev, labels, raw);
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-// ===========================================================================
-// CTA-pair tcgen05 evaluator (see odc_mlp_tc2.cuh)
-// ===========================================================================
-size_t mlp_tc2_weight_elems() { return (size_t)tc2::kStagesPerTile * 2 * tc2::kStageBytes / 2; }
-
-// stages (l, nh, kh) in consumption order (layer 0: kh = 0 only, K = 64);
-// CTA half r of a stage holds B rows n = 128 nh + 64 r + i and K-atoms
-// kc = 2 kh, 2 kh + 1 (k = 64 kc + j), each an 8 KB SWIZZLE_128B K-major image
-__host__ __device__ inline int tc2_stage_index(int l, int nh, int kh) { return l == 0 ? nh : 2 + (l - 1) * 4 + nh * 2 + kh; }
-void mlp_pack_weights_tc2(const float* w0, int d_in, const float* w_hidden, uint16_t* out) {
-  std::memset(out, 0, mlp_tc2_weight_elems() * 2);
-  for (int l = 0; l < kDepth; l++) {
-    const int nkc = l == 0 ? 1 : 4;
-    for (int nh = 0; nh < 2; nh++)
-      for (int kc = 0; kc < nkc; kc++)
-        for (int r = 0; r < 2; r++) {
-          const int si = tc2_stage_index(l, nh, kc >> 1);
-          uint16_t* img = out + ((size_t)(si * 2 + r) * tc2::kStageBytes + (kc & 1) * 8192) / 2;
-          for (int i = 0; i < 64; i++)
-            for (int j = 0; j < 64; j++) {
-              const int n = 128 * nh + 64 * r + i, k = 64 * kc + j;
-              float v;
-              if (l == 0) v = k < d_in ? w0[(size_t)k * kWidth + n] : 0.f;
-              else v = w_hidden[((size_t)(l - 1) * kWidth + k) * kWidth + n];
-              const size_t byte = (size_t)((i >> 3) * 1024 + (i & 7) * 128 + (((j >> 3) ^ (i & 7)) << 4) + (j & 7) * 2);
-              img[byte / 2] = f2bf(v);
-            }
-        }
-  }
-}
-
-template <bool kBias>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::kThreads, 1)
-    k_mlp_tc2(MlpDev m, PointSrc src, int64_t n, uint8_t* __restrict__ labels, double* __restrict__ raw) {
-  using namespace tc;
-  using namespace tc2;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* Wst = smem;
-  uint64_t* bars = (uint64_t*)(Wst + tc2::kStages * tc2::kStageBytes);
-  uint64_t* full = bars;                         // [kStages] local weight half landed
-  uint64_t* empty = full + tc2::kStages;         // [kStages] stage consumed (commit, both CTAs)
-  uint64_t* fullp = empty + tc2::kStages;        // [kStages] leader: peer half landed (relay)
-  uint64_t* acc_full = fullp + tc2::kStages;     // [2] accumulator half ready (commit, both CTAs)
-  uint64_t* a_ready = acc_full + 2;              // [2] leader: A half written (8 warps: 4 per CTA)
-  uint64_t* pe_ready = a_ready + 2;              // leader: next tile's encoding written (4 nh0 warps x 2)
-  uint64_t* pe_free = pe_ready + 1;              // layer 6 done: A buffer 0 may take the next encoding
-  uint32_t* tmem_slot = (uint32_t*)(pe_free + 1);
-  float* s_bias = (float*)(bars + 128);           // (8, 256)
-  float* s_head = s_bias + kDepth * kWidth;       // (256)
-  float* s_part = s_head + kWidth;                // (128) head partial sums of columns 128..255
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = cluster_ctarank();
-  const bool leader = crank == 0;
-  const int64_t ntiles = (n + 255) / 256;
-  const int64_t cluster_id = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < tc2::kStages; s++) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-      mbar_init(&fullp[s], 1);
-    }
-    mbar_init(&acc_full[0], 1);
-    mbar_init(&acc_full[1], 1);
-    mbar_init(&a_ready[0], 8);
-    mbar_init(&a_ready[1], 8);
-    mbar_init(pe_ready, 8);
-    mbar_init(pe_free, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = threadIdx.x; i < kDepth * kWidth; i += blockDim.x) s_bias[i] = m.bias[i];
-  for (int i = threadIdx.x; i < kWidth; i += blockDim.x) s_head[i] = m.w_head[i];
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    {  // ---- weight producer (own half; whole warp, one elected lane issues)
-      uint32_t g = 0;
-      for (int64_t t = cluster_id; t < ntiles; t += nclusters)
-        for (int i = 0; i < tc2::kStagesPerTile; i++, g++) {
-          const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
-          const uint32_t bytes = i < 2 ? 8192u : (uint32_t)tc2::kStageBytes;  // layer 0 stages: K = 64
-          mbar_wait(&empty[s], ph ^ 1);
-          if (elect_one()) {
-            mbar_expect_tx(&full[s], bytes);
-            bulk_g2s(Wst + s * tc2::kStageBytes, m.w_tc2 + ((size_t)i * 2 + crank) * (tc2::kStageBytes / 2), bytes,
-                     &full[s]);
-          }
-          __syncwarp();
-        }
-    }
-  } else if (warp == 3) {
-    if (!leader) {  // ---- relay: peer half landed -> leader's fullp[s]
-      uint32_t g = 0;
-      for (int64_t t = cluster_id; t < ntiles; t += nclusters)
-        for (int i = 0; i < tc2::kStagesPerTile; i++, g++) {
-          const uint32_t s = g % tc2::kStages, ph = (g / tc2::kStages) & 1;
-          mbar_wait(&full[s], ph);
-          if (elect_one()) mbar_arrive_cluster(mapa(smem_u32(&fullp[s]), 0));
-          __syncwarp();
-        }
-    }
-  } else if (warp == 1) {
-    if (leader) {  // ---- MMA issuer (whole warp keeps operands uniform; one elected lane issues)
-      uint32_t g = 0, ra0 = 0, ra1 = 0, rpe = 0;
-      bool first = true;
-      int ti = 0;
-      for (int64_t t = cluster_id; t < ntiles; t += nclusters, ti++) {
-        for (int l = 0; l < kDepth; l++) {
-          const int nkc = l == 0 ? 1 : 4;
-          const uint32_t a_buf = tmem + 256 + (l & 1) * 128;
-          ODC_TRACE(ti, l, 0);
-          for (int nh = 0; nh < 2; nh++) {
-            uint32_t s = 0, b_stage = 0;
-            for (int kc = 0; kc < nkc; kc++) {
-              if ((kc & 1) == 0) {  // a new stage holds K-atoms kc, kc + 1
-                s = g % tc2::kStages;
-                const uint32_t ph = (g / tc2::kStages) & 1;
-                mbar_wait(&full[s], ph);
-                mbar_wait(&fullp[s], ph);
-                b_stage = smem_u32(Wst + s * tc2::kStageBytes);
-              }
-              if (l == 0 && nh == 0) {  // encoding of this tile written (A buffer 0, D half 0 drained)
-                mbar_wait(pe_ready, rpe & 1);
-                rpe++;
-                tc_fence_after();
-              }
-              if (l == 0 && nh == 1 && !first) {  // D half 1 drained by the previous tile's layer 7
-                mbar_wait(&a_ready[1], ra1 & 1);
-                ra1++;
-                tc_fence_after();
-              }
-              if (l > 0 && nh == 0 && kc == 0) {
-                mbar_wait(&a_ready[0], ra0 & 1);
-                ra0++;
-                tc_fence_after();
-                ODC_TRACE(ti, l, 1);
-              }
-              if (l > 0 && nh == 0 && kc == 2) {
-                ODC_TRACE(ti, l, 2);
-                mbar_wait(&a_ready[1], ra1 & 1);
-                ra1++;
-                tc_fence_after();
-                ODC_TRACE(ti, l, 3);
-              }
-              const uint32_t b_base = b_stage + (kc & 1) * 8192;
-              const uint32_t d = tmem + nh * 128;
-              const bool last_of_stage = (kc & 1) == 1 || kc == nkc - 1;
-              if (elect_one()) {
-#pragma unroll
-                for (int ks = 0; ks < 4; ks++)
-                  umma_ts(d, a_buf + kc * 32 + ks * 8, sw128_desc(b_base + ks * 32), (kc | ks) != 0);
-                if (last_of_stage) umma_commit_pair(&empty[s]);
-              }
-              __syncwarp();
-              if (last_of_stage) g++;
-            }
-            if (elect_one()) {
-              umma_commit_pair(&acc_full[nh]);
-              if (l == kDepth - 2 && nh == 1) umma_commit_pair(pe_free);
-            }
-            __syncwarp();
-            ODC_TRACE(ti, l, 4 + nh);
-          }
-        }
-        first = false;
-      }
-    }
-  } else if (warp >= 4) {  // ---- epilogue
-    const int half = (warp - 4) >> 2;  // 0: columns 0..127, 1: columns 128..255
-    const int q = warp & 3;
-    const int r = 32 * q + lane;
-    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-    const uint32_t dcol = tmem + lane_base + half * 128;
-    const uint32_t leader_a_ready = mapa(smem_u32(&a_ready[half]), 0);
-    const uint32_t leader_pe_ready = mapa(smem_u32(pe_ready), 0);
-    uint32_t af = 0, pf = 0;
-    uint32_t pe[32];
-    const int64_t t0 = cluster_id;
-    if (half == 0 && t0 < ntiles) {
-      pe_row_packed(src, n, t0 * 256 + crank * 128 + r, pe);
-      ODC_TMEM_ST32(tmem + lane_base + 256, pe);
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(leader_pe_ready);
-    }
-    int ti = 0;
-    for (int64_t t = t0; t < ntiles; t += nclusters, ti++) {
-      const int64_t next = t + nclusters;
-      float dot = 0.f;
-      for (int l = 0; l < kDepth; l++) {
-        const float* bl = s_bias + l * kWidth + half * 128;
-        if (half == 0 && l == kDepth - 1 && next < ntiles) pe_row_packed(src, n, next * 256 + crank * 128 + r, pe);
-        if (r == 0 && crank == 0) ODC_TRACE(ti, l, 6 + half);
-        mbar_wait(&acc_full[half], af & 1);
-        af++;
-        tc_fence_after();
-        if (r == 0 && crank == 0) ODC_TRACE(ti, l, 8 + half);
-        if (l < kDepth - 1) {
-          const uint32_t a_out = tmem + lane_base + 256 + ((l + 1) & 1) * 128 + half * 64;
-#pragma unroll
-          for (int i = 0; i < 4; i += 2) {
-            uint32_t v0[32], v1[32], w[32];
-            ODC_TMEM_LD32(dcol + 32 * i, v0);
-            ODC_TMEM_LD32(dcol + 32 * i + 32, v1);
-            tmem_ld_wait();
-            relu_pack32<kBias>(v0, bl + 32 * i, w);
-            relu_pack32<kBias>(v1, bl + 32 * i + 32, w + 16);
-            ODC_TMEM_ST32(a_out + 16 * i, w);
-          }
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(leader_a_ready);
-          if (r == 0 && crank == 0) ODC_TRACE(ti, l, 10 + half);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            uint32_t v[32];
-            ODC_TMEM_LD32(dcol + 32 * i, v);
-            tmem_ld_wait();
-            dot = head32<kBias>(v, bl + 32 * i, s_head + half * 128 + 32 * i, dot);
-          }
-          if (half == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(leader_a_ready);  // D half 1 drained
-            s_part[r] = dot;
-          } else if (next < ntiles) {
-            mbar_wait(pe_free, pf & 1);  // layer 6's MMAs (readers of A buffer 0) are done
-            pf++;
-            tc_fence_after();
-            ODC_TMEM_ST32(tmem + lane_base + 256, pe);
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(leader_pe_ready);
-          }
-        }
-      }
-      if (half == 0 && next >= ntiles) {  // keep pe_free's phase in step on the last tile
-        mbar_wait(pe_free, pf & 1);
-        pf++;
-      }
-      named_bar_sync(1, 256);  // head partials of columns 128..255 visible
-      if (half == 0) {
-        dot += s_part[r];
-        const int64_t p = t * 256 + crank * 128 + r;
-        if (p < n) {
-          const double mlp = (double)(dot + m.b_head);
-          double pt[3];
-          point_of(src, p, pt);
-          const double d[3] = {pt[0] - m.prior_center[0], pt[1] - m.prior_center[1], pt[2] - m.prior_center[2]};
-          const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
-          const double logit = m.amplitude * mlp - m.prior_scale * (dist - m.prior_radius);
-          const double rv = 1.0 / (1.0 + exp(-logit));
-          labels[p] = rv > 0.5 ? 1 : 0;
-          if (raw) raw[p] = rv;
-        }
-      }
-      named_bar_sync(1, 256);  // s_part reusable
-    }
-  }
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-
-// impl: 0 = CTA-pair tcgen05 (default), 1 = SIMT reference, 2 = single-CTA tcgen05
 // Positional encoding built in pieces across the layers of the current tile
 // pair (the epilogue's slack after each layer): piece 0 = the fp64 point and
 // frequency 0, piece k = frequency k.  The packed words equal
@@ -1050,7 +390,7 @@ __device__ __forceinline__ void pe_piece(const PointSrc& src, int64_t n, int64_t
 }
 
 // ===========================================================================
-// CTA-pair, N = 256, tile ping-pong evaluator (odc_mlp_tc4: mlp_impl 3)
+// CTA-pair, N = 256, tile ping-pong evaluator (k_mlp_tc4, the MLP evaluator)
 //
 // A cluster of two CTAs (one TPC) runs 2 x 256 points through the layers.
 // Each CTA holds two 128-row activation tiles in shared memory (A, bf16,
@@ -1496,11 +836,6 @@ int mlp_eval(const MlpDev& m_in, const PointSrc& src, int64_t n, uint8_t* labels
              unsigned long long* sched_next) {
   MlpDev m = m_in;
   if (n <= 0) return 0;
-  if (m.impl == 1 || m.w_tc == nullptr) {
-    const int64_t blocks = (n + kPts - 1) / kPts;
-    k_mlp_simt<<<(unsigned)blocks, kWidth, 0, s>>>(m, src, n, labels, raw);
-    return 0;
-  }
   // kernel attributes and the SM count, once per device (thread-safe: the
   // batch mode drives one context per host thread)
   static std::once_flag once[64];
@@ -1509,80 +844,61 @@ int mlp_eval(const MlpDev& m_in, const PointSrc& src, int64_t n, uint8_t* labels
   cudaGetDevice(&dev);
   dev &= 63;
   std::call_once(once[dev], [dev]() {
-    cudaFuncSetAttribute(k_mlp_tc<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
-    cudaFuncSetAttribute(k_mlp_tc<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
-    cudaFuncSetAttribute(k_mlp_tc<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
-    cudaFuncSetAttribute(k_mlp_tc<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
-    cudaFuncSetAttribute(k_mlp_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc2::kSmemBytes);
-    cudaFuncSetAttribute(k_mlp_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc2::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc4::kSmemBytes);
     cudaFuncSetAttribute(k_mlp_tc4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc4::kSmemBytes);
     cudaDeviceGetAttribute(&num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
   });
   const int g_num_sms = num_sms[dev];
-  const int64_t ntiles = (n + 255) / 256;
-  if ((src.n_dev || src.out_map) && m.impl != 3) return -2;  // compacted batches: impl 3 only
-  if (m.impl == 3) {
-    const int64_t np4 = (n + 511) / 512;
-    const int64_t pairs = (g_num_sms / 2) < np4 ? (g_num_sms / 2) : np4;
-    if (!m.sched || !sched_next) return -1;  // the dynamic schedule needs the context's counter
-    // every cluster takes indices until one is >= np4: np4 + clusters fetches
-    m.sched_base = *sched_next;
-    *sched_next += (unsigned long long)(np4 + pairs);
-    PointSrc sp = src;
-    sp.petab = nullptr;
-    sp.fd_m = sp.fd_s = 0;
-    float* tab = nullptr;
-    if (!src.pts && src.begin + n <= INT32_MAX && src.grid.S >= 2) {
-      // grid points: per-axis encoding table + divisor by S (CUTLASS-style
-      // round-up multiplier, exact for dividends < 2^31)
-      uint32_t l2 = 0;
-      while ((1u << l2) < (uint32_t)src.grid.S) l2++;
-      const uint32_t pw = 31 + l2;
-      sp.fd_m = (uint32_t)(((1ull << pw) + (uint64_t)src.grid.S - 1) / (uint64_t)src.grid.S);
-      sp.fd_s = pw - 32;
-      if (cudaMallocAsync((void**)&tab, sizeof(float) * 16 * 3 * src.grid.S, s) == cudaSuccess) {
-        k_pe_table<<<(unsigned)((3 * src.grid.S + 127) / 128), 128, 0, s>>>(src.grid, tab);
-        sp.petab = tab;
-      } else {
-        cudaGetLastError();
-      }
+  const int64_t np4 = (n + 511) / 512;
+  const int64_t pairs = (g_num_sms / 2) < np4 ? (g_num_sms / 2) : np4;
+  if (!m.sched || !sched_next || !m.w_tc) return -1;  // the dynamic schedule needs the context's counter
+  // every cluster takes indices until one is >= np4: np4 + clusters fetches
+  m.sched_base = *sched_next;
+  *sched_next += (unsigned long long)(np4 + pairs);
+  PointSrc sp = src;
+  sp.petab = nullptr;
+  sp.fd_m = sp.fd_s = 0;
+  float* tab = nullptr;
+  if (!src.pts && src.begin + n <= INT32_MAX && src.grid.S >= 2) {
+    // grid points: per-axis encoding table + divisor by S (CUTLASS-style
+    // round-up multiplier, exact for dividends < 2^31)
+    uint32_t l2 = 0;
+    while ((1u << l2) < (uint32_t)src.grid.S) l2++;
+    const uint32_t pw = 31 + l2;
+    sp.fd_m = (uint32_t)(((1ull << pw) + (uint64_t)src.grid.S - 1) / (uint64_t)src.grid.S);
+    sp.fd_s = pw - 32;
+    if (cudaMallocAsync((void**)&tab, sizeof(float) * 16 * 3 * src.grid.S, s) == cudaSuccess) {
+      k_pe_table<<<(unsigned)((3 * src.grid.S + 127) / 128), 128, 0, s>>>(src.grid, tab);
+      sp.petab = tab;
+    } else {
+      cudaGetLastError();
     }
-    // labels of explicit (search) points: undecided fp32 labels are finished
-    // by k_mlp_fixup after the launch (stream-ordered scratch for their
-    // dots).  Grid points rarely sit within the margin of the surface, so
-    // the grid pass keeps the inline fp64 path and needs no scratch.
-    float* defer = nullptr;
-    if (!raw && src.pts) {
-      if (cudaMallocAsync((void**)&defer, sizeof(float) * n, s) == cudaSuccess) sp.defer_dot = defer;
-      else cudaGetLastError();
-    }
-    if (m.has_bias)
-      k_mlp_tc4<true><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, sp, n, labels, raw);
-    else
-      k_mlp_tc4<false><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, sp, n, labels, raw);
-    if (defer) {
-      k_mlp_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(m, sp, n, labels);
-      cudaFreeAsync(defer, s);
-    }
-    if (tab) cudaFreeAsync(tab, s);
-    return 1 + (defer ? 1 : 0) + (tab ? 1 : 0);  // kernels launched
   }
-  if (m.impl == 0 && m.w_tc2 != nullptr) {
-    const int64_t pairs = (g_num_sms / 2) < ntiles ? (g_num_sms / 2) : ntiles;
-    if (m.has_bias)
-      k_mlp_tc2<true><<<(unsigned)(2 * pairs), tc2::kThreads, tc2::kSmemBytes, s>>>(m, src, n, labels, raw);
-    else
-      k_mlp_tc2<false><<<(unsigned)(2 * pairs), tc2::kThreads, tc2::kSmemBytes, s>>>(m, src, n, labels, raw);
-    return 0;
+  // labels of explicit (search) points: undecided fp32 labels are finished
+  // by k_mlp_fixup after the launch (stream-ordered scratch for their
+  // dots).  Grid points rarely sit within the margin of the surface, so
+  // the grid pass keeps the inline fp64 path and needs no scratch.
+  float* defer = nullptr;
+  if (!raw && src.pts && !src.dot_out) {
+    if (cudaMallocAsync((void**)&defer, sizeof(float) * n, s) == cudaSuccess) sp.defer_dot = defer;
+    else cudaGetLastError();
   }
-  const int64_t grid = ntiles < g_num_sms ? ntiles : g_num_sms;
-  auto k = m.trace ? (m.has_bias ? k_mlp_tc<true, true> : k_mlp_tc<false, true>)
-                   : (m.has_bias ? k_mlp_tc<true, false> : k_mlp_tc<false, false>);
-  k<<<(unsigned)grid, tc::kThreads, tc::kSmemBytes, s>>>(m, src, n, labels, raw);
-  return 0;
+  if (m.has_bias)
+    k_mlp_tc4<true><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, sp, n, labels, raw);
+  else
+    k_mlp_tc4<false><<<(unsigned)(2 * pairs), tc4::kThreads, tc4::kSmemBytes, s>>>(m, sp, n, labels, raw);
+  if (defer) {
+    k_mlp_fixup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(m, sp, n, labels);
+    cudaFreeAsync(defer, s);
+  }
+  if (tab) cudaFreeAsync(tab, s);
+  return 1 + (defer ? 1 : 0) + (tab ? 1 : 0);  // kernels launched
 }
 
 const char* mlp_kernel_name() { return "k_mlp_tc4"; }
+
+int mlp_set_wait_timeout_ns(unsigned long long ns) {
+  return cudaMemcpyToSymbol(tc::g_mbar_timeout_ns, &ns, sizeof ns) == cudaSuccess ? 0 : -1;
+}
 
 }  // namespace odc

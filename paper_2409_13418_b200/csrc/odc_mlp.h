@@ -18,16 +18,13 @@
 namespace odc {
 
 struct MlpDev {
-  const uint16_t* w_packed;  // row-major bf16 W[k][n] per layer (layer 0 padded to K=64): SIMT evaluator
   const uint16_t* w_tc;      // 58 chunks of 128x64 bf16 in the UMMA SWIZZLE_128B smem image (odc_mlp_tc.cuh)
-  const uint16_t* w_tc2;     // the same chunks split into two 64-row halves (odc_mlp_tc2.cuh)
-  int impl;                  // 3 = CTA-pair N=256 (default), 2 = single-CTA, 0 = CTA-pair TS, 1 = SIMT
-  int debug;                 // timing experiments, odc_profile_mlp only (results are wrong): impl 3 --
+  int debug;                 // timing experiments, odc_profile_mlp only (results are wrong):
                              // 1 no weight refills after the first ring, 8 static round-robin schedule,
                              // 4 every label through fp64, 16 every label decided in fp32
   int has_bias;              // any non-zero bias (selects the bias-add epilogue)
   unsigned long long* trace; // profiling: event timeline of CTA 0 (nullptr = off)
-  // impl 3 dynamic pair schedule: a per-context device counter that only
+  // dynamic pair schedule: a per-context device counter that only
   // grows; mlp_eval() sets sched_base from *sched_next and advances it
   unsigned long long* sched;
   unsigned long long sched_base;
@@ -49,31 +46,33 @@ struct PointSrc {
   // cos_k of every coordinate index, 16 floats per row) and a fast divisor by S
   const float* petab;
   uint32_t fd_m, fd_s;
-  // compacted batches (mlp_impl 3 only): the point count is read on the
+  // compacted batches: the point count is read on the
   // device (n is then only the launch's upper bound) and label/raw i goes
   // to out_map[i]
   const int64_t* n_dev;
   const int32_t* out_map;
-  // set by mlp_eval (impl 3, labels only): fp32-undecided labels are written
+  // set by mlp_eval (labels only): fp32-undecided labels are written
   // as 2 with their head dot here, and finished in fp64 by k_mlp_fixup
   float* defer_dot;
+  // parity hook (odc_eval_mlp_dot): the fp32 head dot of every point
+  float* dot_out;
 };
 
-size_t mlp_packed_weight_elems();
+// host: pack float32 weights (already bf16-representable) into the device layout
 size_t mlp_tc_weight_elems();
 void mlp_pack_weights_tc(const float* w0, int d_in, const float* w_hidden, uint16_t* out);
-size_t mlp_tc2_weight_elems();
-void mlp_pack_weights_tc2(const float* w0, int d_in, const float* w_hidden, uint16_t* out);
-// host: pack float32 weights (already bf16-representable) into the device layout
-void mlp_pack_weights(const float* w0, int d_in, const float* w_hidden, uint16_t* out);
 
 // labels (u8) and optionally raw = sigmoid(logit) (f64) for n points
-// impl 3 needs m.sched and sched_next (the host copy of the counter's value
-// at the next launch, advanced here).  Returns the number of kernels it
-// launched (0 for n == 0), negative when the counter is missing or a
-// compacted batch meets another evaluator.
+// (k_mlp_tc4, the CTA-pair tcgen05 evaluator).  Needs m.sched and
+// sched_next (the host copy of the counter's value at the next launch,
+// advanced here).  Returns the number of kernels it launched (0 for n == 0),
+// negative when the counter or the weights are missing.
 int mlp_eval(const MlpDev& m, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s,
              unsigned long long* sched_next = nullptr);
 const char* mlp_kernel_name();
+// The evaluator's mbarrier waits trap (a kernel error instead of a hung GPU)
+// after this long without progress; 0 waits forever (debuggers, heavy
+// preemption).  Default 4 s.  Applies to the current device.
+int mlp_set_wait_timeout_ns(unsigned long long ns);
 
 }  // namespace odc

@@ -56,8 +56,19 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Bounded wait: a protocol bug traps (kernel error) after ~4 s instead of
-// hanging the GPU.
+// Bounded wait: a protocol bug traps (kernel error) after g_mbar_timeout_ns
+// (default 4 s; odc_set_param("mbar_timeout_ms"), 0 = wait forever) instead
+// of hanging the GPU.
+__device__ unsigned long long g_mbar_timeout_ns = 4000000000ull;
+__device__ __forceinline__ bool mbar_timed_out(uint64_t& t0) {
+  const uint64_t t = globaltimer_ns();
+  if (t0 == 0) {
+    t0 = t;
+    return false;
+  }
+  const unsigned long long lim = *(volatile unsigned long long*)&g_mbar_timeout_ns;
+  return lim != 0 && t - t0 > lim;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t done = 0;
@@ -69,11 +80,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
     if (done) return;
-    if ((spins & 1023) == 0) {
-      const uint64_t t = globaltimer_ns();
-      if (t0 == 0) t0 = t;
-      else if (t - t0 > 4000000000ull) __trap();
-    }
+    if ((spins & 1023) == 0 && mbar_timed_out(t0)) __trap();
   }
 }
 // mbar_wait with cluster-scope acquire: for data a peer CTA stored into this
@@ -90,11 +97,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
         : "r"(a), "r"(parity)
         : "memory");
     if (done) return;
-    if ((spins & 1023) == 0) {
-      const uint64_t t = globaltimer_ns();
-      if (t0 == 0) t0 = t;
-      else if (t - t0 > 4000000000ull) __trap();
-    }
+    if ((spins & 1023) == 0 && mbar_timed_out(t0)) __trap();
   }
 }
 // Spin on the non-blocking test_wait (no suspend); bounded like mbar_wait.
@@ -109,11 +112,7 @@ __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
     if (done) return;
-    if ((spins & 1023) == 0) {
-      const uint64_t t = globaltimer_ns();
-      if (t0 == 0) t0 = t;
-      else if (t - t0 > 4000000000ull) __trap();
-    }
+    if ((spins & 1023) == 0 && mbar_timed_out(t0)) __trap();
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
