@@ -59,6 +59,17 @@ def thin_shell(R, cells=2.5):
 
 SCENES["thin_shell"] = thin_shell(64)
 
+# Thin rotated walls (thickness < one cell at the resolutions used with
+# them): the 2D searches' step-2 arms come out parallel on some faces, so
+# these exercise the midpoint-fallback status (search.py:280-313), and the
+# second also range-exhausted searches.
+SCENES["thin_wall"] = {"field": {"type": "box", "center": [0.543211, 0.511308, 0.484636],
+                                 "half_extents": [0.209059, 0.170578, 0.009314],
+                                 "rotation_euler_deg": [50.038, 51.628, 11.843]}}
+SCENES["thin_wall_b"] = {"field": {"type": "box", "center": [0.573464, 0.526427, 0.562055],
+                                   "half_extents": [0.244974, 0.207064, 0.005822],
+                                   "rotation_euler_deg": [65.276, 58.848, 38.81]}}
+
 
 def batch_shape(s):
     """Shape s of the config-5 batch: a random sphere, torus, box or CSG pair."""

@@ -105,12 +105,19 @@ def cases():
     yield "thin_shell_64", SC.SCENES["thin_shell"], 64
     yield "mlp_amp1_32", {"field": {"type": "mlp", "seed": 0, "amplitude": 1.0}}, 32
     yield "mlp_amp4_32", {"field": {"type": "mlp", "seed": 0, "amplitude": 4.0}}, 32
+    yield "thin_wall_18", SC.SCENES["thin_wall"], 18
+    yield "thin_wall_b_29", SC.SCENES["thin_wall_b"], 29
 
 
 def main():
+    """``python make_golden.py [tag ...]``: regenerate the named cases only
+    (default: all), keeping the other fixtures and index entries."""
     HERE.mkdir(exist_ok=True)
-    index = {}
+    only = set(sys.argv[1:])
+    index = json.loads((HERE / "index.json").read_text()) if only else {}
     for tag, scene, R in cases():
+        if only and tag not in only:
+            continue
         doc = scene
         lo = tuple(doc.get("domain", {}).get("lo", (0, 0, 0)))
         hi = tuple(doc.get("domain", {}).get("hi", (1, 1, 1)))

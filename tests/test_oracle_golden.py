@@ -63,3 +63,14 @@ def test_eval_accounting():
     assert ec["probe_face_midpoint"] == {"batches": 1, "evals": Q}
     assert ec["search_2d"] == {"batches": 30, "evals": 45 * Q}
     assert ec["total_evals"] == S3 + 15 * K + F4 + 46 * Q
+
+
+def test_golden_cases_cover_every_2d_status():
+    """Every find_2d_points status (search.py:308-313) occurs in some golden
+    case, so the device's status logic is pinned branch by branch."""
+    seen = set()
+    for tag in ALL:
+        g = load(tag)
+        if "status" in g:
+            seen |= set(np.unique(g["status"]).tolist())
+    assert seen == {0, 1, 2, 3}
