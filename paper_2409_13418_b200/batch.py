@@ -27,7 +27,7 @@ def _workers(device, workers):
         key = (device, workers)
         if key not in _state:
             _state[key] = (ThreadPoolExecutor(max_workers=workers, thread_name_prefix=f"odc{device}"),
-                           [_lib.Context(device) for _ in range(workers)])
+                           [_lib.Context(device) for _ in range(workers)], threading.Lock())
         return _state[key]
 
 
@@ -37,12 +37,15 @@ def contour_batch(jobs, options=None, *, workers=8, device=0, provenance=True):
     if not jobs:
         return []
     W = max(1, min(workers, len(jobs)))
-    pool, ctxs = _workers(device, W)
+    pool, ctxs, busy = _workers(device, W)
 
     def run(w):
         return [contour(f, g, options, device=device, provenance=provenance, _ctx=ctxs[w]) for f, g in jobs[w::W]]
 
-    parts = list(pool.map(run, range(W)))
+    # the contexts (workspace, stream, pair counters) serve one call at a
+    # time: concurrent contour_batch calls on the same pool queue here
+    with busy:
+        parts = list(pool.map(run, range(W)))
     out = [None] * len(jobs)
     for w, res in enumerate(parts):
         out[w::W] = res
