@@ -391,17 +391,18 @@ def run_gpu(args, rank, world, dist):
 
 
 def run_gpu_batch(args, rank, world, dist):
-    """Config 5: 64 analytic shapes at 256^3 extracted concurrently (worker
-    threads, one libodc context + stream each).  value = cells of all grids /
-    wall time between device-wide synchronizations (fields resident);
-    e2e = the same through contour_batch (field upload + mesh copy-back)."""
+    """Config 5: 64 analytic shapes at 256^3 as ONE batched extraction
+    (odc_extract_batch: the grids stacked along z, one launch per stage over
+    all shapes).  value = cells of all grids / the batch's device time (CUDA
+    events on the library stream, fields resident); e2e = the same through
+    contour_batch (field upload + per-shape mesh copy-back)."""
     import ctypes as C
-    from concurrent.futures import ThreadPoolExecutor
 
     import torch
 
     from paper_2409_13418_b200 import GridSpec, _lib, scenes
     from paper_2409_13418_b200.batch import contour_batch
+    from paper_2409_13418_b200.fields import lower_program
     from paper_2409_13418_b200.pipeline import ContourOptions, DeviceField, make_options
 
     device = int(os.environ.get("LOCAL_RANK", "0"))
@@ -413,39 +414,27 @@ def run_gpu_batch(args, rank, world, dist):
         f, lo, hi = scenes.resolve(sc, R)
         jobs.append((f, GridSpec(lo, hi, R)))
     mine = jobs[rank::world]
-    workers = args.batch_workers
+    nb = len(mine)
     L = _lib.load()
     opts = make_options(ContourOptions())
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
+    ctx = _lib.Context(device)
+    dfields = [DeviceField(ctx, f) for f, _ in mine]
+    handles = (C.c_void_p * nb)(*[d.handle.value for d in dfields])
+    lo = np.array([g.lo for _, g in mine], dtype=np.float64)
+    hi = np.array([g.hi for _, g in mine], dtype=np.float64)
+    stats = (_lib.Stats * nb)()
 
-    ctxs = [_lib.Context(device) for _ in range(workers)]  # worker w always on ctxs[w]
-
-    def worker(w):
-        ctx = ctxs[w]
-        out = []
-        for j in parts[w]:
-            f, g = mine[j]
-            with DeviceField(ctx, f) as df:
-                st = _lib.Stats()
-                lo = (C.c_double * 3)(*g.lo)
-                hi = (C.c_double * 3)(*g.hi)
-                rc = L.odc_extract(ctx.handle, df.handle, lo, hi, R, C.byref(opts), C.byref(st))
-                if rc:
-                    raise RuntimeError(L.odc_last_error(ctx.handle).decode())
-                out.append(st.n_kernel_launches)
-        return out
-
-    parts = [list(range(w, len(mine), workers)) for w in range(workers)]
-    # one pool for the whole run: libodc contexts are per host thread, so the
-    # same threads keep their contexts (workspace, streams) across steps
-    pool = ThreadPoolExecutor(max_workers=workers)
-
-    def run_all():
-        return sum(sum(x) for x in pool.map(worker, range(workers)))
+    def step():
+        rc = L.odc_extract_batch(ctx.handle, handles, nb, lo.ctypes.data, hi.ctypes.data, R, C.byref(opts),
+                                 C.cast(stats, C.c_void_p))
+        if rc:
+            raise RuntimeError(L.odc_last_error(ctx.handle).decode())
+        return float(stats[0].device_ms), int(stats[0].n_kernel_launches)
 
     for _ in range(args.warmup):
-        run_all()
-    times, launches = [], 0
+        step()
+    times, walls, launches = [], [], 0
     with ClockSampler(device) as clocks:
         for _ in range(args.steps):
             flush.zero_()
@@ -453,45 +442,56 @@ def run_gpu_batch(args, rank, world, dist):
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            launches += run_all()
-            torch.cuda.synchronize()
-            times.append(time.perf_counter() - t0)
+            ms, k = step()
+            walls.append(time.perf_counter() - t0)
+            times.append(ms * 1e-3)
+            launches += k
     clock = clocks.summary()
+    stage_ms = [float(stats[0].stage_ms[i]) for i in range(8)]
+    for d in dfields:
+        d.free()
     e2e = []
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = contour_batch(mine, workers=workers, device=device)
+        res = contour_batch(mine, device=device)
         t1 = time.perf_counter()
         if i >= args.warmup:
             e2e.append(t1 - t0)
-    step = float(np.mean(times))
+    step_s = float(np.mean(times))
     e2e_step = float(np.mean(e2e))
     if dist is not None:
-        t = torch.tensor([step, e2e_step], device=f"cuda:{device}")
+        t = torch.tensor([step_s, e2e_step], device=f"cuda:{device}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step, e2e_step = (float(x) for x in t.tolist())
+        step_s, e2e_step = (float(x) for x in t.tolist())
     if rank != 0:
         return
     cells = n * R**3
-    d2h = sum(r.mesh.n_vertices * 48 + r.mesh.n_triangles * 12 for r in res)
+    d2h = sum(r.mesh.n_vertices * 48 + r.mesh.n_triangles * 24 * (2 if r.raw_mesh is not r.mesh else 1)
+              for r in res)
+    h2d = sum(len(lower_program(f)) * C.sizeof(_lib.Node) for f, _ in mine)  # the field programs
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         f, g = jobs[0]
         v, t_full, cores, sample, dt, info = cpu_sample(f, g.lo, g.hi, R, None, args.cpu_sample_r)
         cpu = {"value": v, "unit": "cells/s", "cores": cores, "kind": "port",
                "sample": sample + " (shape 0 of the batch; per-shape throughput)", **info}
+    names = ["labels", "active_sets", "points_1d", "normals_2d", "cells_qef", "polygonize", "repair", "labels_kernel"]
     line = {
-        "metric": METRIC, "value": cells / step, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "metric": METRIC, "value": cells / step_s, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"batch of {n} analytic shapes (scenes.batch_shapes) at {R}^3 (config 5)", "R": R,
-                   "cells": cells, "parallelism": f"{workers} concurrent contexts/streams per GPU x{world}",
-                   "l2": "flushed before every step; step timed between device-wide synchronizations"},
+                   "cells": cells, "parallelism": f"one stacked-z batched extraction per GPU x{world}",
+                   "l2": "flushed (512 MiB write) before every step, outside its CUDA-event pair"},
         "e2e": {"value": cells / e2e_step, "unit": "cells/s", "ms_per_step": e2e_step * 1e3,
-                "h2d_bytes_per_step": None, "d2h_bytes_per_step": int(d2h),
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "api": "paper_2409_13418_b200.batch.contour_batch(jobs) -> [ContourResult]"},
-        "roofline": None, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clock,
+        "roofline": None, "cpu_baseline": cpu, "gpu_launches": launches // max(1, args.steps), "clocks": clock,
+        "wall_ms_per_step": float(np.mean(walls)) * 1e3,
+        "stage_ms": dict(zip(names, stage_ms)),
+        "mesh": {"n_vertices": int(sum(r.mesh.n_vertices for r in res)),
+                 "n_triangles": int(sum(r.mesh.n_triangles for r in res))},
     }
     emit(line)
 

@@ -176,6 +176,29 @@ void odc_default_options(odc_options* o);
 int odc_extract(odc_ctx* ctx, const odc_field* field, const double lo[3], const double hi[3], int64_t resolution,
                 const odc_options* opt, odc_stats* stats);
 
+/* ---- batches (BASELINE config 5: many analytic shapes, throughput) -------
+ * nb analytic fields, shape b on the grid lo[3b..3b+2]..hi[3b..3b+2] at the
+ * common resolution R, extracted together: the shapes' grids are stacked
+ * along z, so every stage is one launch over all of them (the shape is the
+ * high part of the flat index) and the per-extraction host round trips are
+ * paid once per batch.  Each shape's result equals odc_extract of that shape
+ * alone (the reference runs the shapes one by one, pipeline.py:154-240; the
+ * elements of a shape never interact with another's, search.py:1-6).  stats:
+ * nb entries.  Dual contouring with two-d-point normals only.
+ * Replaces a host loop over occmesh.pipeline.contour (pipeline.py:154). */
+int odc_extract_batch(odc_ctx* ctx, const odc_field* const* fields, int32_t nb, const double* lo, const double* hi,
+                      int64_t resolution, const odc_options* opt, odc_stats* stats);
+/* per-shape layout of the last batch (nb + 1 starts, nb raw counts): shape b
+ * owns vertex rows [vertex_start[b], vertex_start[b+1]) (its first
+ * raw_vertices[b] rows are the raw mesh's vertices) and triangle rows
+ * [triangle_start[b], triangle_start[b+1]) */
+int odc_batch_layout(odc_ctx* ctx, int64_t* vertex_start, int64_t* raw_vertices, int64_t* triangle_start);
+/* every shape's repaired mesh (vertices, triangles with shape-local vertex
+ * ids, provenance with shape-local refs) and raw triangles, concatenated in
+ * shape order; any pointer may be NULL */
+int odc_copy_batch_meshes(odc_ctx* ctx, double* vertices, int64_t* triangles, int64_t* raw_triangles,
+                          int64_t* prov_kind, int64_t* prov_ref);
+
 /* ---- z-slab mode (multi-GPU) --------------------------------
  * A rank extracts the owned cell layers [cell_z0, cell_z1) of the global grid
  * plus a recomputed one-layer halo below (no halo data exchange).  Local

@@ -134,7 +134,8 @@ struct odc_ctx {
   int64_t K = 0, Q = 0, C = 0, F = 0, F4 = 0, P = 0, Ns = 0, NF = 0, T = 0, V0 = 0, V1 = 0, n_interior = 0;
   bool keep = false;
   uint32_t* L = nullptr;
-  WordRec* rec = nullptr;
+  RecView rec{};  // sparse word records (active words only)
+  int64_t A = 0;  // active words
   int64_t *edge_key = nullptr, *inst_key = nullptr, *cell_id = nullptr, *f4_key = nullptr, *face_key = nullptr,
           *face_nc = nullptr;
   int64_t* v_in = nullptr;
@@ -163,6 +164,16 @@ struct odc_ctx {
     int64_t base, n;
   };
   std::vector<DupPass> dup_passes;  // repair passes (polygonize.py:348-358)
+  // scans kept for the batch split
+  uint32_t *pbase = nullptr, *toff = nullptr, *frank = nullptr;
+  DevStats* dstats = nullptr;
+  // last batch extraction (odc_extract_batch): per-shape row starts
+  // (nb + 1) x kBatchCols, vertex starts of the repaired mesh, raw counts,
+  // and the stable by-shape vertex order
+  int nb = 0;
+  std::vector<int64_t> b_bounds, b_vstart, b_v0;
+  uint32_t* b_skeys = nullptr;
+  int32_t *b_perm = nullptr, *b_local = nullptr;
 };
 
 namespace {
@@ -393,8 +404,16 @@ struct Window {
   bool slab;  // stop after polygonization (offsets are assigned across ranks)
 };
 
+// batch: nb shapes of resolution R stacked along z (GridP::nb), with their
+// geometry and fields in device arrays (odc_extract_batch)
+struct BatchIn {
+  int nb;
+  const double* geo;    // device (nb, 6)
+  const FieldP* fields;  // device (nb)
+};
+
 void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi[3], int64_t R,
-             const odc_options* o, odc_stats* st, const Window& win) {
+             const odc_options* o, odc_stats* st, const Window& win, const BatchIn* bin = nullptr) {
   // ---- validation: GridSpec (grid.py:24-31), ContourOptions.validate (pipeline.py:72-78)
   if (R < 2) throw OdcError{ODC_E_VALUE, "resolution must be at least 2"};
   for (int a = 0; a < 3; a++)
@@ -433,6 +452,16 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     g.lo[a] = lo[a];
     g.h[a] = (hi[a] - lo[a]) / (double)R;  // cell_size (grid.py:37-40)
   }
+  if (bin) {  // shapes stacked along z: shape b holds layers [b S, b S + S)
+    g.nb = bin->nb;
+    g.geo = bin->geo;
+    g.z0 = 0;
+    g.nz = (int64_t)bin->nb * g.S;
+    g.own0 = 0;
+    g.own1 = g.nz;
+    g.NW = g.nz * g.S * g.W;
+  }
+  c->nb = bin ? bin->nb : 0;
   c->g = g;
   const OptP op = make_opt(o, f->continuous);
   FieldP fp = f->fp;  // analytic: nodes + fast-path parameters (odc_field_analytic)
@@ -440,12 +469,15 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   fp.n_nodes = f->n_nodes;
   fp.kind = f->kind;
   fp.iso = f->iso;
+  if (bin) fp.batch = bin->fields;
   const bool mlp = f->kind != 0;  // fields evaluated in lock-step batches (MLP, mesh winding)
 
-  DevStats* dst = need(c->arena.get<DevStats>(1));
+  const int nst = bin ? bin->nb : 1;  // statistics blocks: one per shape
+  DevStats* dst = need(c->arena.get<DevStats>(nst));
+  c->dstats = dst;
   DevStatus* dstat = need(c->arena.get<DevStatus>(1));
   unsigned long long* totals = need(c->arena.get<unsigned long long>(8));
-  CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(DevStats), s));
+  CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(DevStats) * nst, s));
   CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), s));
 
   int marks = 0;
@@ -481,54 +513,59 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   // ---- K2: extract_active (grid.py:171-296)
   mark(1);
   const int64_t nt = active_tiles(g);
-  c->rec = need(c->arena.get<WordRec>(g.NW));
-  uint32_t* tiles = need(c->arena.get<uint32_t>(5 * nt));
-  launch_active_bits(g, c->L, c->rec, tiles, dst, s);
-  launch_scan_tiles(tiles, nt, 5, totals, s);
+  uint32_t* tiles = need(c->arena.get<uint32_t>(6 * nt));
+  c->rec.occ = need(c->arena.get<uint2>(occ_words(g)));
+  launch_active_bits(g, c->L, const_cast<uint2*>(c->rec.occ), tiles, dst, s);
+  launch_scan_tiles(tiles, nt, 6, totals, s);
   check_launch(c, 2);
-  readback(c, totals, 5 * sizeof(unsigned long long));
+  readback(c, totals, 6 * sizeof(unsigned long long));
   const int64_t K = (int64_t)c->h_pinned[0], Q = (int64_t)c->h_pinned[1], C = (int64_t)c->h_pinned[2],
-                Fn = (int64_t)c->h_pinned[3], F4 = (int64_t)c->h_pinned[4];
+                Fn = (int64_t)c->h_pinned[3], F4 = (int64_t)c->h_pinned[4], A = (int64_t)c->h_pinned[5];
   if (K >= (1ll << 31) || Q >= (1ll << 31)) throw OdcError{ODC_E_VALUE, "crossing set exceeds 2^31 elements"};
   c->K = K;
   c->Q = Q;
   c->C = C;
   c->F = Fn;
   c->F4 = F4;
+  c->A = A;
+  c->rec.rec = need(c->arena.get<WordRec>(A));
   c->edge_key = need(c->arena.get<int64_t>(K));
   c->inst_key = need(c->arena.get<int64_t>(Q));
   c->cell_id = need(c->arena.get<int64_t>(C));
   c->f4_key = need(c->arena.get<int64_t>(F4));
   c->face_key = c->keep ? need(c->arena.get<int64_t>(Fn)) : nullptr;
   c->face_nc = c->keep ? need(c->arena.get<int64_t>(Fn)) : nullptr;
-  launch_active_compact(g, c->rec, tiles, c->edge_key, c->inst_key, c->cell_id, c->f4_key, c->face_key, c->face_nc,
-                        s);
+  launch_active_compact(g, c->L, c->rec, tiles, c->edge_key, c->inst_key, c->cell_id, c->f4_key, c->face_key,
+                        c->face_nc, s);
   check_launch(c);
   // owned element ranges: rows are in key order, so ownership by base layer
   // is a contiguous row range [lo, hi) read from the word ranks
   int64_t e_lo = 0, e_hi = K, q_lo = 0, q_hi = Q, c_lo = 0, c_hi = C, f_own = Fn, f4_own = F4;
-  if (win.slab || g.z0 != 0 || g.nz != g.S) {
+  if (!g.nb && (win.slab || g.z0 != 0 || g.nz != g.S)) {
     const int64_t ztop = g.z0 + g.nz - 1;
-    WordRec* h = reinterpret_cast<WordRec*>(c->h_pinned);
-    CUDA_TRY(cudaMemcpyAsync(&h[0], c->rec + (g.own0 - g.z0) * g.S * g.W, sizeof(WordRec), cudaMemcpyDeviceToHost, s));
-    if (g.own1 <= ztop)
-      CUDA_TRY(cudaMemcpyAsync(&h[1], c->rec + (g.own1 - g.z0) * g.S * g.W, sizeof(WordRec), cudaMemcpyDeviceToHost,
-                               s));
+    unsigned long long* pre = need(c->arena.get<unsigned long long>(6));
+    launch_prefix_at(c->rec, (g.own0 - g.z0) * g.S * g.W, A, totals, pre, s);
+    check_launch(c);
+    if (g.own1 <= ztop) {
+      launch_prefix_at(c->rec, (g.own1 - g.z0) * g.S * g.W, A, totals, pre + 3, s);
+      check_launch(c);
+    }
     launch_count_owned_faces(g, c->rec, dst, s);
     check_launch(c);
-    CUDA_TRY(cudaMemcpyAsync(&h[2], &dst->faces_own, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    unsigned long long* h = c->h_pinned;
+    CUDA_TRY(cudaMemcpyAsync(&h[0], pre, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&h[6], &dst->faces_own, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    e_lo = h[0].pe;
-    q_lo = h[0].pq;
-    c_lo = h[0].pc;
+    e_lo = (int64_t)h[0];
+    q_lo = (int64_t)h[1];
+    c_lo = (int64_t)h[2];
     if (g.own1 <= ztop) {
-      e_hi = h[1].pe;
-      q_hi = h[1].pq;
-      c_hi = h[1].pc;
+      e_hi = (int64_t)h[3];
+      q_hi = (int64_t)h[4];
+      c_hi = (int64_t)h[5];
     }
-    const unsigned long long* fc = reinterpret_cast<const unsigned long long*>(&h[2]);
-    f_own = (int64_t)fc[0];
-    f4_own = (int64_t)fc[1];
+    f_own = (int64_t)h[6];
+    f4_own = (int64_t)h[7];
   }
   c->e_lo = e_lo;
   c->e_hi = e_hi;
@@ -791,6 +828,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   uint32_t* ncyc = need(c->arena.get<uint32_t>(C));
   uint32_t* nsamp = need(c->arena.get<uint32_t>(C));
   uint32_t* pbase = need(c->arena.get<uint32_t>(C + 1));
+  c->pbase = pbase;
   uint32_t* sbase = need(c->arena.get<uint32_t>(C + 1));
   launch_cell_config(g, c->L, c->rec, c->cell_id, C, c->table, cfg, ncyc, nsamp, s);
   check_launch(c);
@@ -842,6 +880,8 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   uint32_t* nfan = need(c->arena.get<uint32_t>(K_own));
   uint32_t* toff = need(c->arena.get<uint32_t>(K_own));
   uint32_t* frank = need(c->arena.get<uint32_t>(K_own));
+  c->toff = toff;
+  c->frank = frank;
   launch_poly_classify(g, op, c->L, c->rec, ekey, K_own, co.pinfo, verts, pid4, c->kase, ntri, nfan, dst, s);
   check_launch(c);
   scan2(c, ntri, nfan, toff, frank, K_own, totals);
@@ -887,6 +927,103 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   mark(7);
   finish_stats();
   c->valid = true;
+}
+
+// ---- batch (odc_extract_batch): per-shape statistics and the by-shape
+// vertex order of the finished union mesh (odc_batch.cu)
+void batch_split(odc_ctx* c, const odc_options* o, const OptP& op, odc_stats* st) {
+  const int nb = c->nb;
+  cudaStream_t s = c->stream;
+  const GridP& g = c->g;
+  c->b_bounds.assign((size_t)(nb + 1) * kBatchCols, 0);
+  c->b_vstart.assign(nb + 1, 0);
+  c->b_v0.assign(nb, 0);
+  std::vector<DevStats> ds(nb);
+  CUDA_TRY(cudaMemcpyAsync(ds.data(), c->dstats, sizeof(DevStats) * nb, cudaMemcpyDeviceToHost, s));
+  if (c->K) {
+    int64_t* bd = need(c->arena.get<int64_t>((nb + 1) * kBatchCols));
+    launch_batch_bounds(g, c->rec, c->A, c->K, c->Q, c->C, c->f4_key, c->F4, c->pbase, c->P, c->toff, c->frank, c->T,
+                        c->NF, bd, s);
+    check_launch(c);
+    CUDA_TRY(cudaMemcpyAsync(c->b_bounds.data(), bd, sizeof(int64_t) * (nb + 1) * kBatchCols, cudaMemcpyDeviceToHost,
+                             s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    // by-shape vertex order of the repaired union mesh
+    const int64_t V = c->V1, V0 = c->V0, T = c->T;
+    std::vector<int64_t> tstart(nb + 1);
+    for (int b = 0; b <= nb; b++) tstart[b] = c->b_bounds[(size_t)b * kBatchCols + 5];
+    int64_t* dts = need(c->arena.get<int64_t>(nb + 1));
+    CUDA_TRY(cudaMemcpyAsync(dts, tstart.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s));
+    uint32_t* vshape = need(c->arena.get<uint32_t>(V));
+    c->b_skeys = need(c->arena.get<uint32_t>(V));
+    int32_t* iota = need(c->arena.get<int32_t>(V));
+    c->b_perm = need(c->arena.get<int32_t>(V));
+    c->b_local = need(c->arena.get<int32_t>(V));
+    unsigned long long* hist = need(c->arena.get<unsigned long long>(2 * nb));
+    size_t tmp_bytes = 0;
+    batch_sort_vertices(c->tris1, T, V, V0, dts, nb, vshape, c->b_skeys, iota, c->b_perm, nullptr, &tmp_bytes, hist,
+                        s);
+    void* tmp = need(c->arena.alloc(tmp_bytes));
+    launch_iota_i32(iota, V, s);
+    batch_sort_vertices(c->tris1, T, V, V0, dts, nb, vshape, c->b_skeys, iota, c->b_perm, tmp, &tmp_bytes, hist, s);
+    check_launch(c, 4);
+    std::vector<unsigned long long> h(2 * nb);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), hist, sizeof(unsigned long long) * 2 * nb, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int b = 0; b < nb; b++) {
+      c->b_vstart[b + 1] = c->b_vstart[b] + (int64_t)h[b];
+      c->b_v0[b] = (int64_t)h[nb + b];
+    }
+    int64_t* dvs = need(c->arena.get<int64_t>(nb + 1));
+    CUDA_TRY(cudaMemcpyAsync(dvs, c->b_vstart.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s));
+    launch_local_ids(c->b_skeys, c->b_perm, V, dvs, c->b_local, s);
+    check_launch(c);
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));
+  // per-shape statistics, in the reference's accounting (pipeline.py:160-239)
+  const float ms = st[0].device_ms;
+  const odc_stats uni = st[0];
+  for (int b = 0; b < nb; b++) {
+    odc_stats& x = st[b];
+    std::memset(&x, 0, sizeof x);
+    for (int i = 0; i < ODC_N_CAT; i++) x.cat_order[i] = -1;
+    const int64_t* lo = &c->b_bounds[(size_t)b * kBatchCols];
+    const int64_t* hi = lo + kBatchCols;
+    const int64_t K = hi[0] - lo[0], Q = hi[1] - lo[1], C = hi[2] - lo[2], F4 = hi[3] - lo[3];
+    x.n_grid_vertices = g.S3;
+    record(&x, ODC_CAT_LABELS, 1, g.S3);
+    x.boundary_inside_vertices = (int64_t)ds[b].boundary_inside;
+    x.n_crossing_edges = K;
+    x.n_crossing_cells = C;
+    x.device_ms = ms;
+    for (int i = 0; i < 8; i++) x.stage_ms[i] = uni.stage_ms[i];
+    x.n_kernel_launches = uni.n_kernel_launches;
+    if (K == 0) continue;  // pipeline.py:174-179
+    x.n_crossing_faces = Q - F4;
+    if (op.one_d == ODC_ONE_D_BINARY) record(&x, ODC_CAT_SEARCH_1D, op.iters_1d, (int64_t)op.iters_1d * K);
+    if (F4) record(&x, ODC_CAT_PROBE_FACE_CENTER, 1, F4);
+    x.n_face_center_probes = F4;
+    record(&x, ODC_CAT_PROBE_FACE_MIDPOINT, 1, Q);
+    record(&x, ODC_CAT_SEARCH_2D, op.s1_lin + op.s1_bin + op.s2_lin + op.s2_bin,
+           (int64_t)(op.s1_lin + op.s1_bin) * Q + (int64_t)(op.s2_lin + op.s2_bin) * 2 * Q);
+    x.n_2d_points = Q;
+    x.n_partitions = hi[4] - lo[4];
+    for (int i = 0; i < 4; i++) {
+      x.point2d_status_counts[i] = (int64_t)ds[b].status[i];
+      x.qef_rank_counts[i] = (int64_t)ds[b].rank[i];
+      x.split_case_counts[i] = (int64_t)ds[b].split[i];
+    }
+    std::memcpy(&x.qef_max_residual, &ds[b].max_resid_bits, 8);
+    x.normal_fallbacks = (int64_t)ds[b].normal_fallbacks;
+    x.skipped_boundary_edges = (int64_t)ds[b].skipped;
+    const int64_t Tb = hi[5] - lo[5];
+    x.raw_n_triangles = x.n_triangles = Tb;
+    x.raw_n_vertices = c->b_v0[b];
+    x.n_vertices = c->b_vstart[b + 1] - c->b_vstart[b];
+    x.repair_added_vertices = x.n_vertices - x.raw_n_vertices;
+    x.repair_passes = uni.repair_passes;
+  }
+  (void)o;
 }
 
 int guard(odc_ctx* c, int (*fn)(odc_ctx*, void*), void* arg) {
@@ -1244,6 +1381,75 @@ int odc_extract(odc_ctx* c, const odc_field* f, const double lo[3], const double
   }, &a);
 }
 
+struct BatchArgs {
+  const odc_field* const* f;
+  int32_t nb;
+  const double* lo;
+  const double* hi;
+  int64_t R;
+  const odc_options* o;
+  odc_stats* st;
+};
+
+int odc_extract_batch(odc_ctx* c, const odc_field* const* fields, int32_t nb, const double* lo, const double* hi,
+                      int64_t R, const odc_options* o, odc_stats* stats) {
+  if (!c || !fields || nb < 1 || !lo || !hi || !stats) return ODC_E_ARG;
+  odc_options def;
+  odc_default_options(&def);
+  BatchArgs a{fields, nb, lo, hi, R, o ? o : &def, stats};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    BatchArgs* x = (BatchArgs*)p;
+    const int nb = x->nb;
+    cc->nb = 0;
+    if ((int64_t)nb * (x->R + 1) * (x->R + 1) * (x->R + 1) >= (1ll << 32))
+      throw OdcError{ODC_E_VALUE, "batch exceeds 2^32 grid vertices"};
+    if (x->o->method != 0) throw OdcError{ODC_E_ARG, "batches run the dual-contouring method only"};
+    if (x->o->normals != ODC_NORMALS_2D) throw OdcError{ODC_E_ARG, "batches use two-d-point normals"};
+    std::vector<double> geo((size_t)nb * 6);
+    std::vector<FieldP> fps(nb);
+    for (int b = 0; b < nb; b++) {
+      const odc_field* f = x->f[b];
+      if (!f || f->kind != 0) throw OdcError{ODC_E_ARG, "batches take analytic fields"};
+      if (f->continuous != x->f[0]->continuous)
+        throw OdcError{ODC_E_ARG, "batch fields must all be binary or all continuous"};
+      for (int a = 0; a < 3; a++) {
+        if (!(x->hi[3 * b + a] > x->lo[3 * b + a])) throw OdcError{ODC_E_VALUE, "grid box must have positive extent"};
+        geo[6 * b + a] = x->lo[3 * b + a];
+        geo[6 * b + 3 + a] = (x->hi[3 * b + a] - x->lo[3 * b + a]) / (double)x->R;  // cell_size (grid.py:37-40)
+      }
+      FieldP fp = f->fp;
+      fp.nodes = f->nodes;
+      fp.n_nodes = f->n_nodes;
+      fp.kind = f->kind;
+      fp.iso = f->iso;
+      fps[b] = fp;
+    }
+    // the geometry and field tables live in the context's field pool (not
+    // the arena, which extract() resets)
+    cudaStream_t s = cc->stream;
+    double* dgeo = nullptr;
+    FieldP* dfp = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&dgeo, sizeof(double) * geo.size(), s));
+    CUDA_TRY(cudaMallocAsync((void**)&dfp, sizeof(FieldP) * nb, s));
+    CUDA_TRY(cudaMemcpyAsync(dgeo, geo.data(), sizeof(double) * geo.size(), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(dfp, fps.data(), sizeof(FieldP) * nb, cudaMemcpyHostToDevice, s));
+    BatchIn bin{nb, dgeo, dfp};
+    try {
+      extract(cc, x->f[0], x->lo, x->hi, x->R, x->o, x->st, Window{0, x->R, false}, &bin);
+      batch_split(cc, x->o, make_opt(x->o, x->f[0]->continuous), x->st);
+    } catch (...) {
+      cudaFreeAsync(dgeo, s);
+      cudaFreeAsync(dfp, s);
+      cc->nb = 0;
+      throw;
+    }
+    CUDA_TRY(cudaFreeAsync(dgeo, s));
+    CUDA_TRY(cudaFreeAsync(dfp, s));
+    return (int)ODC_OK;
+  }, &a);
+}
+
 struct SlabArgs {
   const odc_field* f;
   const double* lo;
@@ -1493,6 +1699,77 @@ int odc_copy_mesh_pair(odc_ctx* c, double* vertices, int64_t* triangles, int64_t
   CopyMeshArgs a{0, vertices, triangles, prov_kind, prov_ref, raw_triangles};
   return copy_mesh_impl(c, &a);
 }
+
+struct BatchCopyArgs {
+  double* v;
+  int64_t* t;
+  int64_t* raw_t;
+  int64_t* kind;
+  int64_t* ref;
+};
+
+int odc_copy_batch_meshes(odc_ctx* c, double* vertices, int64_t* triangles, int64_t* raw_triangles,
+                          int64_t* prov_kind, int64_t* prov_ref) {
+  if (!c) return ODC_E_ARG;
+  if (!c->valid || !c->nb) {
+    c->err = "no batch extraction result";
+    return ODC_E_ARG;
+  }
+  BatchCopyArgs a{vertices, triangles, raw_triangles, prov_kind, prov_ref};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    BatchCopyArgs* x = (BatchCopyArgs*)p;
+    const int64_t V = cc->V1, V0 = cc->V0, T = cc->T;
+    if (!cc->K || !V) return (int)ODC_OK;
+    cudaStream_t s = cc->stream;
+    std::vector<CopySeg> segs;
+    int64_t *dk = nullptr, *dr = nullptr, *ok = nullptr, *orf = nullptr;
+    if (x->kind || x->ref) {  // union provenance, then gathered shape by shape
+      dk = need(cc->arena.get<int64_t>(V));
+      dr = need(cc->arena.get<int64_t>(2 * V));
+      launch_provenance(V0, cc->P, cc->src0, cc->cells.part_cell, cc->cells.part_index, cc->fan_edge, dk, dr, s);
+      launch_dup_provenance(V0, V, dk, dr, s);
+      ok = need(cc->arena.get<int64_t>(V));
+      orf = need(cc->arena.get<int64_t>(2 * V));
+    }
+    double* ov = need(cc->arena.get<double>(3 * V));
+    const GridP& g = cc->g;
+    launch_batch_gather(cc->verts1, cc->b_perm, cc->b_skeys, V, dk, dr, g.S * g.R * g.R, 3 * g.S3, ov, ok, orf, s);
+    segs.push_back({ov, x->v, sizeof(double) * 3 * V});
+    if (ok) {
+      segs.push_back({ok, x->kind, sizeof(int64_t) * V});
+      segs.push_back({orf, x->ref, sizeof(int64_t) * 2 * V});
+    }
+    if (x->t && T) {
+      int64_t* t64 = need(cc->arena.get<int64_t>(3 * T));
+      launch_batch_tris(cc->tris1, T, cc->b_local, t64, s);
+      segs.push_back({t64, x->t, sizeof(int64_t) * 3 * T});
+    }
+    if (x->raw_t && T) {
+      int64_t* r64 = need(cc->arena.get<int64_t>(3 * T));
+      launch_batch_tris(cc->tris0, T, cc->b_local, r64, s);
+      segs.push_back({r64, x->raw_t, sizeof(int64_t) * 3 * T});
+    }
+    CUDA_TRY(cudaGetLastError());
+    copy_out_pipelined(cc, segs);
+    return (int)ODC_OK;
+  }, &a);
+}
+
+int odc_batch_layout(odc_ctx* c, int64_t* vertex_start, int64_t* raw_vertices, int64_t* triangle_start) {
+  if (!c || !vertex_start || !raw_vertices || !triangle_start) return ODC_E_ARG;
+  if (!c->valid || !c->nb) {
+    c->err = "no batch extraction result";
+    return ODC_E_ARG;
+  }
+  for (int b = 0; b <= c->nb; b++) {
+    vertex_start[b] = c->b_vstart.empty() ? 0 : c->b_vstart[b];
+    triangle_start[b] = c->b_bounds[(size_t)b * kBatchCols + 5];
+    if (b < c->nb) raw_vertices[b] = c->b_v0[b];
+  }
+  return ODC_OK;
+}
+
 
 struct ValidateArgs {
   const int64_t* tris;

@@ -24,17 +24,29 @@ constexpr int kMaxPointStack = 8;
 // [z0, z0 + nz) of the global grid; ids, keys and positions stay global.
 // Edges/faces/vertices with base layer in [own0, own1) are owned by this
 // extraction (the full grid: z0 = 0, nz = S, own = [0, S)).
+//
+// Batch (BASELINE config 5, odc_extract_batch): nb grids of the same R
+// stacked along z -- shape b holds global vertex layers [b S, b S + S) --
+// so every kernel runs once over all shapes and the flat index space
+// carries the shape in its high part.  Keys and ids stay global (ordered
+// shape by shape); a kernel that needs a shape's geometry calls localize()
+// with the element's z, which loads that shape's lo/h and z offset.
 struct GridP {
   int64_t R, S, S2, S3;
   int64_t W;   // words per row
   int64_t NW;  // nz*S*W words held
   int64_t z0, nz, own0, own1;
   double lo[3], h[3];
+  int64_t zoff = 0;            // z of the localized shape's layer 0 (positions use z - zoff)
+  int32_t nb = 0;              // batch: shapes stacked along z (0: one grid)
+  const double* geo = nullptr;  // batch: device (nb, 6) = lo[3], h[3] per shape
 };
 
 // Per-word record of every derived bitmap plus the exclusive ranks of the
-// word's first element (edges, 2D-point instances, cells).  One 64-byte
-// record per word: a rank lookup touches one record.
+// word's first element (edges, 2D-point instances, cells).  Records exist
+// only for ACTIVE words (any crossing edge, face or cell bit): the surface
+// touches a few percent of the grid's words, so a dense per-word array
+// (64 B for every 4 B label word) was 16x the label traffic at 1025^3.
 struct __align__(16) WordRec {
   uint32_t e[3];   // crossing edges by axis, bit at the lower vertex
   uint32_t f[3];   // crossing faces (2 or 4 crossing edges) by normal axis
@@ -44,6 +56,14 @@ struct __align__(16) WordRec {
   uint32_t pe, pq, pc;  // exclusive prefix: edges, instances, cells
 };
 static_assert(sizeof(WordRec) == 64, "WordRec must be one 64-byte record");
+
+// Sparse word records: occ[w / 32] = {bitmap of active words w' in the
+// group of 32, number of active words before the group}; the record of an
+// active word w is rec[occ.y + popc(occ.x & lowmask(w % 32))].
+struct RecView {
+  const uint2* occ;
+  WordRec* rec;
+};
 
 __device__ __forceinline__ int64_t word_of(const GridP& g, int64_t x, int64_t y, int64_t z) {
   return ((z - g.z0) * g.S + y) * g.W + (x >> 5);
@@ -72,7 +92,22 @@ __device__ __forceinline__ void vid_coords(const GridP& g, int64_t vid, int64_t 
 }
 __device__ __forceinline__ int64_t vstep(const GridP& g, int a) { return a == 0 ? 1 : (a == 1 ? g.S : g.S2); }
 __device__ __forceinline__ double gpos(const GridP& g, int a, int64_t c) {
-  return __dadd_rn(g.lo[a], __dmul_rn((double)c, g.h[a]));
+  return __dadd_rn(g.lo[a], __dmul_rn((double)(a == 2 ? c - g.zoff : c), g.h[a]));
+}
+// batch: shape of global vertex layer z (0 for one grid)
+__device__ __forceinline__ int shape_of_z(const GridP& g, int64_t z) { return g.nb ? (int)idiv(z, g.S) : 0; }
+// batch: switch g to the geometry of the shape holding layer z; returns it
+template <bool B = true>
+__device__ __forceinline__ int localize(GridP& g, int64_t z) {
+  if (!B || !g.nb) return 0;
+  const int b = (int)idiv(z, g.S);
+  g.zoff = (int64_t)b * g.S;
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    g.lo[a] = g.geo[6 * b + a];
+    g.h[a] = g.geo[6 * b + 3 + a];
+  }
+  return b;
 }
 __device__ __forceinline__ void vposition(const GridP& g, int64_t vid, double p[3]) {
   int64_t c[3];
@@ -86,25 +121,32 @@ __device__ __forceinline__ uint32_t label_at(const uint32_t* L, const GridP& g, 
   return (L[word_of(g, c[0], c[1], c[2])] >> (c[0] & 31)) & 1u;
 }
 __device__ __forceinline__ uint32_t lowmask(int bit) { return bit == 0 ? 0u : (0xffffffffu >> (32 - bit)); }
+// record of word w, or nullptr when the word has no crossing element
+__device__ __forceinline__ WordRec* rec_find(const RecView& rv, int64_t w) {
+  const uint2 o = rv.occ[w >> 5];
+  const int b = (int)(w & 31);
+  if (!((o.x >> b) & 1u)) return nullptr;
+  return rv.rec + o.y + __popc(o.x & lowmask(b));
+}
 
-// rank of crossing edge (vid, axis) in ascending edge-key order
-__device__ __forceinline__ int64_t edge_rank(const WordRec* rec, const GridP& g, int64_t vid, int axis) {
-  int64_t c[3];
-  vid_coords(g, vid, c);
-  const WordRec& r = rec[word_of(g, c[0], c[1], c[2])];
-  int bit = (int)(c[0] & 31);
+// Ranks from vertex coordinates (callers that already hold them skip the
+// vid -> (x, y, z) divisions).
+// rank of crossing edge (x, y, z, axis) in ascending edge-key order
+__device__ __forceinline__ int64_t edge_rank_c(const RecView& rec, const GridP& g, int64_t x, int64_t y, int64_t z,
+                                               int axis) {
+  const WordRec& r = *rec_find(rec, word_of(g, x, y, z));  // the element's word is active
+  int bit = (int)(x & 31);
   uint32_t m = lowmask(bit);
   int64_t k = (int64_t)r.pe + __popc(r.e[0] & m) + __popc(r.e[1] & m) + __popc(r.e[2] & m);
   for (int a = 0; a < axis; a++) k += (r.e[a] >> bit) & 1u;
   return k;
 }
-// id of the first 2D-point instance of face (vid, normal): instances are
-// numbered in face-key order, two per 4-crossing face (dualize.py:72-88)
-__device__ __forceinline__ int64_t inst_rank(const WordRec* rec, const GridP& g, int64_t vid, int n) {
-  int64_t c[3];
-  vid_coords(g, vid, c);
-  const WordRec& r = rec[word_of(g, c[0], c[1], c[2])];
-  int bit = (int)(c[0] & 31);
+// id of the first 2D-point instance of face (x, y, z, normal): instances
+// are numbered in face-key order, two per 4-crossing face (dualize.py:72-88)
+__device__ __forceinline__ int64_t inst_rank_c(const RecView& rec, const GridP& g, int64_t x, int64_t y, int64_t z,
+                                               int n) {
+  const WordRec& r = *rec_find(rec, word_of(g, x, y, z));  // the element's word is active
+  int bit = (int)(x & 31);
   uint32_t m = lowmask(bit);
   int64_t k = (int64_t)r.pq;
 #pragma unroll
@@ -112,12 +154,30 @@ __device__ __forceinline__ int64_t inst_rank(const WordRec* rec, const GridP& g,
   for (int a = 0; a < n; a++) k += ((r.f[a] >> bit) & 1u) + ((r.f4[a] >> bit) & 1u);
   return k;
 }
-__device__ __forceinline__ int64_t cell_rank(const WordRec* rec, const GridP& g, int64_t base_vid) {
+__device__ __forceinline__ int64_t edge_rank(const RecView& rec, const GridP& g, int64_t vid, int axis) {
+  int64_t c[3];
+  vid_coords(g, vid, c);
+  return edge_rank_c(rec, g, c[0], c[1], c[2], axis);
+}
+__device__ __forceinline__ int64_t inst_rank(const RecView& rec, const GridP& g, int64_t vid, int n) {
+  int64_t c[3];
+  vid_coords(g, vid, c);
+  return inst_rank_c(rec, g, c[0], c[1], c[2], n);
+}
+__device__ __forceinline__ int64_t cell_rank(const RecView& rec, const GridP& g, int64_t base_vid) {
   int64_t c[3];
   vid_coords(g, base_vid, c);
-  const WordRec& r = rec[word_of(g, c[0], c[1], c[2])];
+  const WordRec& r = *rec_find(rec, word_of(g, c[0], c[1], c[2]));  // the element's word is active
   int bit = (int)(c[0] & 31);
   return (int64_t)r.pc + __popc(r.cell & lowmask(bit));
+}
+__device__ __forceinline__ uint32_t label_c(const uint32_t* L, const GridP& g, int64_t x, int64_t y, int64_t z) {
+  return (L[word_of(g, x, y, z)] >> (x & 31)) & 1u;
+}
+__device__ __forceinline__ void vposition_c(const GridP& g, int64_t x, int64_t y, int64_t z, double p[3]) {
+  p[0] = gpos(g, 0, x);
+  p[1] = gpos(g, 1, y);
+  p[2] = gpos(g, 2, z);
 }
 
 // ---------------------------------------------------------------------------
@@ -136,7 +196,9 @@ struct FieldP {
   int32_t fop[3] = {0, 0, 0};
   double fq[2][16] = {};
   double fk = 0.0;
+  const FieldP* batch = nullptr;  // batch: device (nb) fields, one per shape
 };
+__device__ __forceinline__ const FieldP& field_of(const FieldP& f, int b) { return f.batch ? f.batch[b] : f; }
 // host: classify a program for FieldP's fast paths (same patterns as field_raw)
 inline void fieldp_set_fast(FieldP& f, const odc_node* h, int32_t n) {
   auto prim = [](int op) {
@@ -392,6 +454,207 @@ __device__ __forceinline__ double field_raw(const FieldP& f, const double p[3]) 
 }
 __device__ __forceinline__ uint32_t field_label(const FieldP& f, const double p[3]) {
   return field_raw(f, p) > f.iso ? 1u : 0u;
+}
+
+// ---------------------------------------------------------------------------
+// Label culling: a conservative bound of the field over a ball, used by the
+// grid-label pass to decide 32 vertices of a label word with one evaluation.
+//
+// Every primitive is an exact signed distance (fields.py:75-139), so it is
+// Lipschitz in the point with constant |R|_F per rotation applied (1 without)
+// and |n| for a plane; the sd-level CSG ops (min, max, negation) and the raw
+// ops (max, min, 1 - x) are monotone, so intervals propagate exactly through
+// them, and the logistic of smoothed fields (fields.py:239-242) is monotone
+// in sd.  A primitive's interval is its fp64 value at the centre widened by
+// L * radius plus an absolute margin of 1e-9 x (1 + the magnitudes involved):
+// the rounding of either evaluation is below 1e-13 of those magnitudes, so
+// the interval holds the value the per-vertex evaluation computes at every
+// grid vertex of the ball.  A word is decided only when the whole interval
+// lies on one side of iso -- the labels are then the same bits the
+// per-vertex path produces.  Returns 1 (all inside), 0 (all outside) or -1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double frob9(const double* R) {
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 9; j++) s = fma(R[j], R[j], s);
+  return sqrt(s) * (1.0 + 1e-12);
+}
+// interval [lo, hi] of one primitive's computed sd over the ball (see above)
+__device__ __forceinline__ void prim_ball(int op, const double* qq, const double p[3], double lip, double rad,
+                                          double& lo, double& hi) {
+  double L = lip;
+  if (op == ODC_OP_BOX_SD && qq[6] != 0.0) L *= frob9(qq + 7);
+  if (op == ODC_OP_PLANE_SD) L *= sqrt(qq[3] * qq[3] + qq[4] * qq[4] + qq[5] * qq[5]) * (1.0 + 1e-12);
+  const double sd = prim_sd(op, qq, p);
+  const double mag = 1.0 + fabs(p[0]) + fabs(p[1]) + fabs(p[2]) + fabs(qq[0]) + fabs(qq[1]) + fabs(qq[2]) +
+                     fabs(qq[3]) + fabs(qq[4]) + fabs(qq[5]);
+  const double m = L * rad * (1.0 + 1e-9) + 1e-9 * mag;
+  if (!(fabs(sd) < 1e300) || !(m < 1e300)) {  // undecidable: the whole real line
+    lo = -1e308;
+    hi = 1e308;
+    return;
+  }
+  lo = sd - m;
+  hi = sd + m;
+}
+// binary raw of an sd interval (SD2RAW: sd < 0 -> 1)
+__device__ __forceinline__ void sd2raw_ball(double& lo, double& hi) {
+  const double l = lo, h = hi;
+  lo = h < 0.0 ? 1.0 : 0.0;
+  hi = l >= 0.0 ? 0.0 : 1.0;
+}
+__device__ __forceinline__ int ball_decide(double lo, double hi, double iso) {
+  if (lo > iso) return 1;
+  if (hi <= iso) return 0;
+  return -1;
+}
+// Fast paths of FieldP (parameters by value, registers only): one primitive
+// -> raw or smoothed, a CSG pair of binary raws; anything else runs the
+// interval interpreter below.
+static __device__ __noinline__ int field_label_ball_prog(const odc_node* __restrict__ nodes, int n_nodes, double iso,
+                                                       double pc0, double pc1, double pc2, double rad);
+__device__ __forceinline__ int field_label_ball(const FieldP& f, const double pc[3], double rad) {
+  if (f.fast) {
+    double q0[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) q0[i] = f.fq[0][i];
+    double lo, hi;
+    prim_ball(f.fop[0], q0, pc, 1.0, rad, lo, hi);
+    if (f.fast == 1) {
+      sd2raw_ball(lo, hi);
+    } else if (f.fast == 2) {
+      const double ra = smooth_raw(f.fk, lo), rb = smooth_raw(f.fk, hi);
+      lo = fmin(ra, rb) - 1e-12;
+      hi = fmax(ra, rb) + 1e-12;
+    } else {
+      double q1[16];
+#pragma unroll
+      for (int i = 0; i < 16; i++) q1[i] = f.fq[1][i];
+      double blo, bhi;
+      prim_ball(f.fop[1], q1, pc, 1.0, rad, blo, bhi);
+      sd2raw_ball(lo, hi);
+      sd2raw_ball(blo, bhi);
+      if (f.fop[2] == ODC_OP_RAW_MAX) {
+        lo = fmax(lo, blo);
+        hi = fmax(hi, bhi);
+      } else if (f.fop[2] == ODC_OP_RAW_MIN) {
+        lo = fmin(lo, blo);
+        hi = fmin(hi, bhi);
+      } else {  // min(a, 1 - b)
+        const double t = __dsub_rn(1.0, bhi);
+        bhi = __dsub_rn(1.0, blo);
+        blo = t;
+        lo = fmin(lo, blo);
+        hi = fmin(hi, bhi);
+      }
+    }
+    return ball_decide(lo, hi, f.iso);
+  }
+  return field_label_ball_prog(f.nodes, f.n_nodes, f.iso, pc[0], pc[1], pc[2], rad);
+}
+static __device__ __noinline__ int field_label_ball_prog(const odc_node* __restrict__ nodes, int n_nodes, double iso,
+                                                       double pc0, double pc1, double pc2, double rad) {
+  constexpr int kStack = 8, kPts = 4;
+  double slo[kStack], shi[kStack];
+  double pst[kPts][4];
+  int sp = 0, pp = 0;
+  double p[3] = {pc0, pc1, pc2};
+  double lip = 1.0;
+  for (int i = 0; i < n_nodes; i++) {
+    const int op = __ldg(&nodes[i].op);
+    const double* q = nodes[i].p;
+    switch (op) {
+      case ODC_OP_SPHERE_SD:
+      case ODC_OP_BOX_SD:
+      case ODC_OP_TORUS_SD:
+      case ODC_OP_PLANE_SD: {
+        if (sp >= kStack) return -1;
+        double qq[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) qq[j] = __ldg(q + j);
+        prim_ball(op, qq, p, lip, rad, slo[sp], shi[sp]);
+        sp++;
+        break;
+      }
+      case ODC_OP_SD2RAW: {  // fields.py:70-72: sd < 0 -> 1
+        if (sp < 1) return -1;
+        sd2raw_ball(slo[sp - 1], shi[sp - 1]);
+        break;
+      }
+      case ODC_OP_RAW_MAX:
+      case ODC_OP_SD_MAX:
+      case ODC_OP_RAW_MIN:
+      case ODC_OP_SD_MIN:
+      case ODC_OP_RAW_DIFF:
+      case ODC_OP_SD_DIFF: {
+        if (sp < 2) return -1;
+        double blo = slo[--sp], bhi = shi[sp];
+        const double alo = slo[sp - 1], ahi = shi[sp - 1];
+        if (op == ODC_OP_RAW_DIFF) {  // min(a, 1 - b): 1 - x is monotone under rounding
+          const double t = __dsub_rn(1.0, bhi);
+          bhi = __dsub_rn(1.0, blo);
+          blo = t;
+        } else if (op == ODC_OP_SD_DIFF) {  // max(a, -b)
+          const double t = -bhi;
+          bhi = -blo;
+          blo = t;
+        }
+        const bool mx = op == ODC_OP_RAW_MAX || op == ODC_OP_SD_MAX || op == ODC_OP_SD_DIFF;
+        slo[sp - 1] = mx ? fmax(alo, blo) : fmin(alo, blo);
+        shi[sp - 1] = mx ? fmax(ahi, bhi) : fmin(ahi, bhi);
+        break;
+      }
+      case ODC_OP_RAW_COMPL: {
+        if (sp < 1) return -1;
+        const double t = __dsub_rn(1.0, shi[sp - 1]);
+        shi[sp - 1] = __dsub_rn(1.0, slo[sp - 1]);
+        slo[sp - 1] = t;
+        break;
+      }
+      case ODC_OP_SD_NEG: {
+        if (sp < 1) return -1;
+        const double t = -shi[sp - 1];
+        shi[sp - 1] = -slo[sp - 1];
+        slo[sp - 1] = t;
+        break;
+      }
+      case ODC_OP_XFORM_BEGIN: {  // (p - t) @ R, fields.py:176-180
+        if (pp >= kPts) return -1;
+        pst[pp][0] = p[0];
+        pst[pp][1] = p[1];
+        pst[pp][2] = p[2];
+        pst[pp][3] = lip;
+        pp++;
+        double l[3] = {__dsub_rn(p[0], __ldg(q)), __dsub_rn(p[1], __ldg(q + 1)), __dsub_rn(p[2], __ldg(q + 2))};
+        if (__ldg(q + 6) != 0.0) {
+          double R[9], o[3];
+          for (int j = 0; j < 9; j++) R[j] = __ldg(q + 7 + j);
+          rot_rows(l, R, o);
+          l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
+          lip *= frob9(R);
+        }
+        p[0] = l[0]; p[1] = l[1]; p[2] = l[2];
+        break;
+      }
+      case ODC_OP_XFORM_END:
+        if (pp < 1) return -1;
+        pp--;
+        p[0] = pst[pp][0]; p[1] = pst[pp][1]; p[2] = pst[pp][2];
+        lip = pst[pp][3];
+        break;
+      case ODC_OP_SMOOTH: {  // 1 / (1 + exp(clip(k sd))): monotone in sd
+        if (sp < 1) return -1;
+        const double k = __ldg(q);
+        const double ra = smooth_raw(k, slo[sp - 1]), rb = smooth_raw(k, shi[sp - 1]);
+        slo[sp - 1] = fmin(ra, rb) - 1e-12;
+        shi[sp - 1] = fmax(ra, rb) + 1e-12;
+        break;
+      }
+      default: return -1;
+    }
+  }
+  if (sp < 1) return -1;
+  return ball_decide(slo[sp - 1], shi[sp - 1], iso);
 }
 
 // device-side status word (errors raised inside kernels)

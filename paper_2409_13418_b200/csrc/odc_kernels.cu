@@ -5,8 +5,9 @@
 //
 // Data layout in HBM (per extraction):
 //   L       bit-packed vertex labels, rows (y,z) of W words         S^2 W x 4 B
-//   rec     WordRec per word: edge/face/4-face/centre/cell bitmaps
-//           + exclusive ranks (edges, instances, cells)             S^2 W x 64 B
+//   occ     per 32 words: active-word bitmap + active words before    S^2 W / 4 B
+//   rec     WordRec per ACTIVE word: edge/face/4-face/centre/cell
+//           bitmaps + exclusive ranks (edges, instances, cells)     A x 64 B
 //   lists   edge keys (K), instance keys (Q), cell ids (C) as int64, in
 //           the reference's ascending key order
 //   stage   t/pos1d (K), pos2/pos3/status (Q), vertices (P + fans), ...
@@ -25,19 +26,25 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 // Statistics counters: one atomic per warp (the sum over the active lanes)
 // instead of one per thread -- a million same-address atomics serialise in
 // L2 (k_s2_finish spent 0.7 ms on them).  Call with the warp converged.
+// PEER: lanes are grouped by target address (a batch warp can straddle two
+// shapes, whose counters differ).
+template <bool PEER = false>
 __device__ __forceinline__ void warp_count(unsigned long long* p, unsigned v) {
   const unsigned m = __activemask();
-  const unsigned s = __reduce_add_sync(m, v);
-  if ((int)(threadIdx.x & 31) == __ffs(m) - 1 && s) atomicAdd(p, (unsigned long long)s);
+  const unsigned peers = PEER ? __match_any_sync(m, (unsigned long long)p) : m;
+  const unsigned s = __reduce_add_sync(peers, v);
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1 && s) atomicAdd(p, (unsigned long long)s);
 }
 // bins[b] += 1 for this lane's bin b (0..3) when on
+template <bool PEER = false>
 __device__ __forceinline__ void warp_count4(unsigned long long* bins, int b, bool on) {
 #pragma unroll
-  for (int v = 0; v < 4; v++) warp_count(&bins[v], on && b == v ? 1u : 0u);
+  for (int v = 0; v < 4; v++) warp_count<PEER>(&bins[v], on && b == v ? 1u : 0u);
 }
 // max over the active lanes of non-negative doubles (ordered as bits)
+template <bool PEER = false>
 __device__ __forceinline__ void warp_max_nonneg_double(unsigned long long* p, double v) {
-  const unsigned m = __activemask();
+  const unsigned m = PEER ? __match_any_sync(__activemask(), (unsigned long long)p) : __activemask();
   const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
   const unsigned hi = (unsigned)(bits >> 32);
   const unsigned top = __reduce_max_sync(m, hi);
@@ -46,6 +53,13 @@ __device__ __forceinline__ void warp_max_nonneg_double(unsigned long long* p, do
     const unsigned lo = __reduce_max_sync(m2, (unsigned)bits);
     if ((int)(threadIdx.x & 31) == __ffs(m2) - 1 && (top | lo)) atomicMax(p, ((unsigned long long)top << 32) | lo);
   }
+}
+// bits of word wx that lie below coordinate `limit` (valid x of the row)
+__device__ __forceinline__ uint32_t bits_below(int64_t limit, int64_t wx) {
+  int64_t n = limit - wx * 32;
+  if (n <= 0) return 0u;
+  if (n >= 32) return 0xffffffffu;
+  return 0xffffffffu >> (32 - n);
 }
 }  // namespace
 
@@ -56,23 +70,55 @@ __device__ __forceinline__ void warp_max_nonneg_double(unsigned long long* p, do
 // Grid: blockIdx.x = label row (z, y) of the window, blockIdx.y = 256-bit
 // chunk of the row -- the row's coordinates are block-uniform, so no
 // per-thread division.
+// Label words decided in bulk: each lane bounds the field over the ball
+// around its word's (up to) 32 vertices (field_label_ball); the warp then
+// evaluates every vertex of each undecided word, 32 lanes per word.  Far
+// from the surface one evaluation decides 32 labels.
+template <bool B>
 __global__ void __launch_bounds__(256) k_labels_analytic(GridP g, FieldP f, uint32_t* __restrict__ L) {
-  const int64_t row = blockIdx.x;  // window-local row
-  const int64_t x = (int64_t)blockIdx.y * 256 + threadIdx.x;
-  if (x >= g.W * 32) return;  // whole warps (the row's bit count is a multiple of 32)
-  const int64_t y = imod(row, g.S), z = g.z0 + idiv(row, g.S);
-  uint32_t lab = 0;
-  if (x < g.S) {
-    double p[3] = {gpos(g, 0, x), gpos(g, 1, y), gpos(g, 2, z)};
-    lab = field_label(f, p);
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int dec = 2;  // nothing to do
+  int64_t y = 0, z = 0, wx = 0;
+  if (w < g.NW) {
+    const int64_t row = idiv(w, g.W);
+    wx = w - row * g.W;
+    y = imod(row, g.S);
+    z = g.z0 + idiv(row, g.S);
+    GridP gl = g;
+    const int b = localize<B>(gl, z);
+    const int64_t xa = wx * 32, xb = (xa + 31 < g.S - 1) ? xa + 31 : g.S - 1;
+    const double pa = gpos(gl, 0, xa), pb = gpos(gl, 0, xb);
+    const double pc[3] = {__dmul_rn(__dadd_rn(pa, pb), 0.5), gpos(gl, 1, y), gpos(gl, 2, z)};
+    const double rad = __dmul_rn(__dsub_rn(pb, pa), 0.5) * (1.0 + 1e-12) + 1e-300;
+    if constexpr (B) dec = field_label_ball(f.batch[b], pc, rad);
+    else dec = field_label_ball(f, pc, rad);
+    if (dec >= 0) L[w] = dec ? bits_below(g.S, wx) : 0u;
   }
-  const uint32_t w = __ballot_sync(0xffffffffu, lab);
-  if ((threadIdx.x & 31) == 0) L[row * g.W + (x >> 5)] = w;
+  unsigned und = __ballot_sync(0xffffffffu, dec == -1);
+  while (und) {
+    const int j = __ffs(und) - 1;
+    und &= und - 1;
+    const int64_t wj = __shfl_sync(0xffffffffu, w, j), yj = __shfl_sync(0xffffffffu, y, j),
+                  zj = __shfl_sync(0xffffffffu, z, j), wxj = __shfl_sync(0xffffffffu, wx, j);
+    const int64_t x = wxj * 32 + lane;
+    uint32_t lab = 0;
+    if (x < g.S) {
+      GridP gl = g;
+      const int b = localize<B>(gl, zj);
+      const double p[3] = {gpos(gl, 0, x), gpos(gl, 1, yj), gpos(gl, 2, zj)};
+      if constexpr (B) lab = field_label(f.batch[b], p);
+      else lab = field_label(f, p);
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, lab);
+    if (lane == 0) L[wj] = word;
+  }
 }
 
 void launch_labels_analytic(const GridP& g, const FieldP& f, uint32_t* L, cudaStream_t s) {
-  const int64_t rows = g.nz * g.S;
-  if (rows) k_labels_analytic<<<dim3((unsigned)rows, grid_for(g.W * 32, 256)), 256, 0, s>>>(g, f, L);
+  if (!g.NW) return;
+  if (g.nb) k_labels_analytic<true><<<grid_for(g.NW, 256), 256, 0, s>>>(g, f, L);
+  else k_labels_analytic<false><<<grid_for(g.NW, 256), 256, 0, s>>>(g, f, L);
 }
 
 // one warp per label row: lane j of word w reads byte 32 w + j (coalesced),
@@ -128,13 +174,15 @@ void launch_grid_points(const GridP& g, int64_t begin, int64_t n, double* pts, c
 // 2 cells, 3 faces, 4 4-crossing faces.
 // ===========================================================================
 constexpr int kActiveBlock = kScanBlock;
+constexpr int kActiveCh = 6;
+// A tile (one block, one tile-sum per channel) is kActiveGroups occupancy
+// groups of 32 words: pass 1 walks it word by word (kActiveSub sub-tiles of
+// kActiveBlock words), pass 2 group by group (a warp per group).
+constexpr int kActiveGroups = 64;
+constexpr int64_t kActiveTile = (int64_t)kActiveGroups * 32;
+constexpr int kActiveSub = (int)(kActiveTile / kActiveBlock);
+constexpr int64_t kActiveWarpGroups = 65536;  // pass 2: warp per group below this many groups
 
-__device__ __forceinline__ uint32_t bits_below(int64_t limit, int64_t wx) {
-  int64_t n = limit - wx * 32;
-  if (n <= 0) return 0u;
-  if (n >= 32) return 0xffffffffu;
-  return 0xffffffffu >> (32 - n);
-}
 
 struct ActiveBits {
   uint32_t e[3], f[3], f4[3], cell;
@@ -144,7 +192,8 @@ __device__ __forceinline__ ActiveBits compute_active(const GridP& g, const uint3
                                                      int64_t z, int64_t wx) {
   const int64_t W = g.W, S = g.S, R = g.R;
   const int64_t ztop = g.z0 + g.nz - 1;  // last layer held
-  const bool yin = y < R, zin = z < R && z < ztop;
+  const int64_t zl = g.nb ? z - idiv(z, S) * S : z;  // layer within its shape (batch)
+  const bool yin = y < R, zin = zl < R && z < ztop;
   auto ld = [&](int64_t yy, int64_t zz, int64_t ww) -> uint32_t {
     if (yy > R || zz > ztop || ww >= W) return 0u;
     return L[((zz - g.z0) * S + yy) * W + ww];
@@ -152,11 +201,21 @@ __device__ __forceinline__ ActiveBits compute_active(const GridP& g, const uint3
   const uint32_t a00 = ld(y, z, wx), a10 = ld(y + 1, z, wx), a01 = ld(y, z + 1, wx), a11 = ld(y + 1, z + 1, wx);
   const uint32_t n00 = ld(y, z, wx + 1), n10 = ld(y + 1, z, wx + 1), n01 = ld(y, z + 1, wx + 1),
                  n11 = ld(y + 1, z + 1, wx + 1);
+  ActiveBits b;
+  {  // uniform neighbourhood (all 0 or all 1 labels): nothing crosses
+    const uint32_t o = a00 | a10 | a01 | a11 | n00 | n10 | n01 | n11;
+    const uint32_t n = a00 & a10 & a01 & a11 & n00 & n10 & n01 & n11;
+    if (o == 0u || n == 0xffffffffu) {
+#pragma unroll
+      for (int a = 0; a < 3; a++) b.e[a] = b.f[a] = b.f4[a] = 0u;
+      b.cell = 0u;
+      return b;
+    }
+  }
   // label at x+1
   const uint32_t s00 = (a00 >> 1) | (n00 << 31), s10 = (a10 >> 1) | (n10 << 31);
   const uint32_t s01 = (a01 >> 1) | (n01 << 31), s11 = (a11 >> 1) | (n11 << 31);
   const uint32_t mS = bits_below(S, wx), mR = bits_below(R, wx);
-  ActiveBits b;
   b.e[0] = (a00 ^ s00) & mR;
   b.e[1] = yin ? ((a00 ^ a10) & mS) : 0u;
   b.e[2] = zin ? ((a00 ^ a01) & mS) : 0u;
@@ -188,7 +247,7 @@ __device__ __forceinline__ ActiveBits compute_active(const GridP& g, const uint3
   return b;
 }
 
-__device__ __forceinline__ void active_counts(const ActiveBits& b, uint32_t (&c)[5]) {
+__device__ __forceinline__ void active_counts(const ActiveBits& b, uint32_t (&c)[kActiveCh]) {
   uint32_t nf = __popc(b.f[0]) + __popc(b.f[1]) + __popc(b.f[2]);
   uint32_t n4 = __popc(b.f4[0]) + __popc(b.f4[1]) + __popc(b.f4[2]);
   c[0] = __popc(b.e[0]) + __popc(b.e[1]) + __popc(b.e[2]);
@@ -198,116 +257,138 @@ __device__ __forceinline__ void active_counts(const ActiveBits& b, uint32_t (&c)
   c[4] = n4;
 }
 
+// Pass 1: per-tile counts only (6 channels: edges, instances, cells, faces,
+// 4-crossing faces, active words); nothing per word is written.
+__device__ __forceinline__ bool word_active(const ActiveBits& b) {
+  return (b.e[0] | b.e[1] | b.e[2] | b.f[0] | b.f[1] | b.f[2] | b.cell) != 0u;  // f4 is a subset of f
+}
+
+template <bool B>
 __global__ void __launch_bounds__(kActiveBlock) k_active_bits(GridP g, const uint32_t* __restrict__ L,
-                                                              WordRec* __restrict__ rec, uint32_t* __restrict__ sums,
+                                                              uint2* __restrict__ occ, uint32_t* __restrict__ sums,
                                                               int64_t ntiles, DevStats* st) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t c[5] = {0, 0, 0, 0, 0};
+  __shared__ uint32_t part[kActiveBlock / 32][kActiveCh];
+  uint32_t c[kActiveCh] = {0, 0, 0, 0, 0, 0};
   uint32_t shell = 0;
-  if (idx < g.NW) {
+  for (int j = 0; j < kActiveSub; j++) {
+    const int64_t idx = (int64_t)blockIdx.x * kActiveTile + j * kActiveBlock + threadIdx.x;
+    if (idx >= g.NW) break;
     const int64_t row = idiv(idx, g.W), wx = idx - row * g.W;
     const int64_t y = imod(row, g.S), z = g.z0 + idiv(row, g.S);
-    ActiveBits b = compute_active(g, L, y, z, wx);
-    WordRec r;
-    for (int a = 0; a < 3; a++) {
-      r.e[a] = b.e[a];
-      r.f[a] = b.f[a];
-      r.f4[a] = b.f4[a];
-      r.cf[a] = 0u;
-    }
-    r.cell = b.cell;
-    r.pe = r.pq = r.pc = 0u;
-    rec[idx] = r;
-    active_counts(b, c);
+    const ActiveBits b = compute_active(g, L, y, z, wx);
+    uint32_t cw[kActiveCh];
+    active_counts(b, cw);
+    cw[5] = word_active(b) ? 1u : 0u;
+    // occupancy bitmap of the warp's 32 consecutive words
+    const uint32_t act = __ballot_sync(__activemask(), cw[5] != 0u);
+    if ((threadIdx.x & 31) == 0) occ[idx >> 5].x = act;
+#pragma unroll
+    for (int ch = 0; ch < kActiveCh; ch++) c[ch] += cw[ch];
     // boundary_inside_count (grid.py:102-106)
     const uint32_t lab = (z >= g.own0 && z < g.own1) ? (L[idx] & bits_below(g.S, wx)) : 0u;
-    if (y == 0 || y == g.R || z == 0 || z == g.R) {
-      shell = __popc(lab);
+    const int64_t zl = z - (int64_t)shape_of_z(g, z) * g.S;
+    uint32_t sh;
+    if (y == 0 || y == g.R || zl == 0 || zl == g.R) {
+      sh = __popc(lab);
     } else {
       uint32_t m = 0u;
       if (wx == 0) m |= 1u;
       if ((g.R >> 5) == wx) m |= 1u << (g.R & 31);
-      shell = __popc(lab & m);
+      sh = __popc(lab & m);
     }
+    if constexpr (B) warp_count<true>(&st[shape_of_z(g, z)].boundary_inside, sh);  // per shape
+    else shell += sh;
   }
-  uint32_t ex[5], tot[5];
-  block_exscan<5>(c, ex, tot);
-  if (threadIdx.x == 0)
-    for (int ch = 0; ch < 5; ch++) sums[ch * ntiles + blockIdx.x] = tot[ch];
-  // reduce shell count
-  for (int o = 16; o > 0; o >>= 1) shell += __shfl_xor_sync(0xffffffffu, shell, o);
-  if ((threadIdx.x & 31) == 0 && shell) atomicAdd(&st->boundary_inside, (unsigned long long)shell);
+  // tile totals: warp sums, then one thread over the warps (no scan needed)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int ch = 0; ch < kActiveCh; ch++) {
+    const uint32_t v = __reduce_add_sync(0xffffffffu, c[ch]);
+    if (lane == 0) part[wid][ch] = v;
+  }
+  shell = __reduce_add_sync(0xffffffffu, shell);
+  if (lane == 0 && shell) atomicAdd(&st->boundary_inside, (unsigned long long)shell);
+  __syncthreads();
+  if (threadIdx.x < kActiveCh) {
+    uint32_t t = 0;
+    for (int w = 0; w < kActiveBlock / 32; w++) t += part[w][threadIdx.x];
+    sums[threadIdx.x * ntiles + blockIdx.x] = t;
+  }
 }
 
-int64_t active_tiles(const GridP& g) { return (g.NW + kActiveBlock - 1) / kActiveBlock; }
+int64_t active_tiles(const GridP& g) { return (g.NW + kActiveTile - 1) / kActiveTile; }
+int64_t occ_words(const GridP& g) { return (g.NW + 31) / 32; }
 
-void launch_active_bits(const GridP& g, const uint32_t* L, WordRec* rec, uint32_t* tile_sums, DevStats* st,
+void launch_active_bits(const GridP& g, const uint32_t* L, uint2* occ, uint32_t* tile_sums, DevStats* st,
                         cudaStream_t s) {
   int64_t nt = active_tiles(g);
-  k_active_bits<<<(unsigned)nt, kActiveBlock, 0, s>>>(g, L, rec, tile_sums, nt, st);
+  if (g.nb) k_active_bits<true><<<(unsigned)nt, kActiveBlock, 0, s>>>(g, L, occ, tile_sums, nt, st);
+  else k_active_bits<false><<<(unsigned)nt, kActiveBlock, 0, s>>>(g, L, occ, tile_sums, nt, st);
 }
 
 void launch_scan_tiles(uint32_t* sums, int64_t ntiles, int nch, unsigned long long* totals, cudaStream_t s) {
   switch (nch) {
     case 1: k_scan_tiles<1><<<1, 1024, 0, s>>>(sums, ntiles, totals); break;
     case 2: k_scan_tiles<2><<<1, 1024, 0, s>>>(sums, ntiles, totals); break;
+    case 6: k_scan_tiles<6><<<1, 1024, 0, s>>>(sums, ntiles, totals); break;
     default: k_scan_tiles<5><<<1, 1024, 0, s>>>(sums, ntiles, totals); break;
   }
 }
 
-__global__ void __launch_bounds__(kActiveBlock) k_active_compact(GridP g, WordRec* __restrict__ rec,
-                                                                 const uint32_t* __restrict__ sums, int64_t ntiles,
-                                                                 int64_t* __restrict__ edge_key,
-                                                                 int64_t* __restrict__ inst_key,
-                                                                 int64_t* __restrict__ cell_id,
-                                                                 int64_t* __restrict__ f4_key,
-                                                                 int64_t* __restrict__ face_key,
-                                                                 int64_t* __restrict__ face_nc) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Pass 2, per tile of kActiveGroups occupancy groups (32 words each, pass 1
+// wrote their bitmaps): (a) a warp per group sums the counts of its active
+// words (one lane per word), (b) six warps scan the groups' totals (one
+// channel each), (c) a warp per non-empty group recomputes its active words,
+// scans them across lanes and writes the records, the group prefix and the
+// key lists.  Inactive words -- most of the grid -- cost one bitmap read.
+__device__ __forceinline__ ActiveBits active_word(const GridP& g, const uint32_t* __restrict__ L, int64_t w,
+                                                  int64_t& y, int64_t& z, int64_t& wx) {
+  const int64_t row = idiv(w, g.W);
+  wx = w - row * g.W;
+  y = imod(row, g.S);
+  z = g.z0 + idiv(row, g.S);
+  return compute_active(g, L, y, z, wx);
+}
+
+// write the record of active word (y, z, wx) and its keys at positions pos
+__device__ __forceinline__ void emit_word(const GridP& g, const ActiveBits& b, int64_t y, int64_t z, int64_t wx,
+                                          const uint32_t (&pos)[kActiveCh], WordRec* __restrict__ recs,
+                                          int64_t* __restrict__ edge_key, int64_t* __restrict__ inst_key,
+                                          int64_t* __restrict__ cell_id, int64_t* __restrict__ f4_key,
+                                          int64_t* __restrict__ face_key, int64_t* __restrict__ face_nc) {
   WordRec r;
-  uint32_t c[5] = {0, 0, 0, 0, 0};
-  if (idx < g.NW) {
-    r = rec[idx];
-    ActiveBits b;
-    for (int a = 0; a < 3; a++) {
-      b.e[a] = r.e[a];
-      b.f[a] = r.f[a];
-      b.f4[a] = r.f4[a];
-    }
-    b.cell = r.cell;
-    active_counts(b, c);
+  for (int a = 0; a < 3; a++) {
+    r.e[a] = b.e[a];
+    r.f[a] = b.f[a];
+    r.f4[a] = b.f4[a];
+    r.cf[a] = 0u;
   }
-  uint32_t ex[5], tot[5];
-  block_exscan<5>(c, ex, tot);
-  if (idx >= g.NW) return;
-  uint32_t pos[5];
-  for (int ch = 0; ch < 5; ch++) pos[ch] = sums[ch * ntiles + blockIdx.x] + ex[ch];
-  rec[idx].pe = pos[0];
-  rec[idx].pq = pos[1];
-  rec[idx].pc = pos[2];
-  const int64_t row = idiv(idx, g.W), wx = idx - row * g.W;
-  const int64_t y = imod(row, g.S), z = g.z0 + idiv(row, g.S);
+  r.cell = b.cell;
+  r.pe = pos[0];
+  r.pq = pos[1];
+  r.pc = pos[2];
+  recs[pos[5]] = r;
   const int64_t vbase = (z * g.S + y) * g.S + wx * 32;  // global vertex id of bit 0 (x = 32 wx)
   // edges: ascending vertex, then axis (edge key = vid*3 + axis)
-  uint32_t any = r.e[0] | r.e[1] | r.e[2];
+  uint32_t any = b.e[0] | b.e[1] | b.e[2];
   uint32_t pe = pos[0];
   while (any) {
     int bit = __ffs(any) - 1;
     any &= any - 1;
     int64_t vid = vbase + bit;
     for (int a = 0; a < 3; a++)
-      if ((r.e[a] >> bit) & 1u) edge_key[pe++] = vid * 3 + a;
+      if ((b.e[a] >> bit) & 1u) edge_key[pe++] = vid * 3 + a;
   }
-  uint32_t anyf = r.f[0] | r.f[1] | r.f[2];
+  uint32_t anyf = b.f[0] | b.f[1] | b.f[2];
   uint32_t pq = pos[1], pf = pos[3], p4 = pos[4];
   while (anyf) {
     int bit = __ffs(anyf) - 1;
     anyf &= anyf - 1;
     int64_t vid = vbase + bit;
     for (int n = 0; n < 3; n++) {
-      if (!((r.f[n] >> bit) & 1u)) continue;
+      if (!((b.f[n] >> bit) & 1u)) continue;
       const int64_t fk = vid * 3 + n;
-      const bool four = (r.f4[n] >> bit) & 1u;
+      const bool four = (b.f4[n] >> bit) & 1u;
       inst_key[pq++] = fk * 2;
       if (four) {
         inst_key[pq++] = fk * 2 + 1;
@@ -320,7 +401,7 @@ __global__ void __launch_bounds__(kActiveBlock) k_active_compact(GridP g, WordRe
       pf++;
     }
   }
-  uint32_t cl = r.cell;
+  uint32_t cl = b.cell;
   uint32_t pc = pos[2];
   while (cl) {
     int bit = __ffs(cl) - 1;
@@ -330,12 +411,163 @@ __global__ void __launch_bounds__(kActiveBlock) k_active_compact(GridP g, WordRe
   }
 }
 
-void launch_active_compact(const GridP& g, WordRec* rec, const uint32_t* tile_sums, int64_t* edge_key,
-                           int64_t* inst_key, int64_t* cell_id, int64_t* f4_key, int64_t* face_key,
+__global__ void __launch_bounds__(kActiveBlock) k_active_compact_wpg(GridP g, const uint32_t* __restrict__ L,
+                                                                 uint2* __restrict__ occ, WordRec* __restrict__ recs,
+                                                                 const uint32_t* __restrict__ sums, int64_t ntiles,
+                                                                 int64_t* __restrict__ edge_key,
+                                                                 int64_t* __restrict__ inst_key,
+                                                                 int64_t* __restrict__ cell_id,
+                                                                 int64_t* __restrict__ f4_key,
+                                                                 int64_t* __restrict__ face_key,
+                                                                 int64_t* __restrict__ face_nc) {
+  static_assert(kActiveGroups == 64 && kActiveCh <= kActiveBlock / 32, "tile scan: 2 groups per lane, a warp per channel");
+  __shared__ uint32_t gt[kActiveGroups][kActiveCh];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int kWarps = kActiveBlock / 32;
+  const int64_t ngrp = (g.NW + 31) >> 5;
+  const int64_t g0 = (int64_t)blockIdx.x * kActiveGroups;
+  // (a) group totals
+  for (int i = wid; i < kActiveGroups; i += kWarps) {
+    const int64_t grp = g0 + i;
+    const uint32_t bits = grp < ngrp ? occ[grp].x : 0u;
+    uint32_t c[kActiveCh] = {0, 0, 0, 0, 0, 0};
+    if (bits) {  // warp-uniform
+      if ((bits >> lane) & 1u) {
+        int64_t y, z, wx;
+        active_counts(active_word(g, L, grp * 32 + lane, y, z, wx), c);
+        c[5] = 1u;
+      }
+#pragma unroll
+      for (int ch = 0; ch < kActiveCh; ch++) c[ch] = __reduce_add_sync(0xffffffffu, c[ch]);
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int ch = 0; ch < kActiveCh; ch++) gt[i][ch] = c[ch];
+  }
+  __syncthreads();
+  // (b) exclusive group prefixes (tile offset included), one warp per channel
+  if (wid < kActiveCh) {
+    const uint32_t v0 = gt[2 * lane][wid], v1 = gt[2 * lane + 1][wid];
+    uint32_t x = v0 + v1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    const uint32_t ex = x - v0 - v1 + sums[wid * ntiles + blockIdx.x];
+    gt[2 * lane][wid] = ex;
+    gt[2 * lane + 1][wid] = ex + v0;
+  }
+  __syncthreads();
+  // (c) records and keys
+  for (int i = wid; i < kActiveGroups; i += kWarps) {
+    const int64_t grp = g0 + i;
+    if (grp >= ngrp) break;  // warp-uniform
+    const uint32_t bits = occ[grp].x;
+    if (lane == 0) occ[grp].y = gt[i][5];
+    if (!bits) continue;
+    const bool act = (bits >> lane) & 1u;
+    ActiveBits b{};
+    uint32_t c[kActiveCh] = {0, 0, 0, 0, 0, 0};
+    int64_t y = 0, z = 0, wx = 0;
+    if (act) {
+      b = active_word(g, L, grp * 32 + lane, y, z, wx);
+      active_counts(b, c);
+      c[5] = 1u;
+    }
+    uint32_t pos[kActiveCh];
+#pragma unroll
+    for (int ch = 0; ch < kActiveCh; ch++) {
+      uint32_t x = c[ch];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      pos[ch] = gt[i][ch] + x - c[ch];
+    }
+    if (!act) continue;
+    emit_word(g, b, y, z, wx, pos, recs, edge_key, inst_key, cell_id, f4_key, face_key, face_nc);
+  }
+}
+
+// Thread per group (large grids: many groups, few active words each)
+__global__ void __launch_bounds__(kActiveGroups) k_active_compact_tpg(GridP g, const uint32_t* __restrict__ L,
+                                                                      uint2* __restrict__ occ,
+                                                                      WordRec* __restrict__ recs,
+                                                                      const uint32_t* __restrict__ sums,
+                                                                      int64_t ntiles, int64_t* __restrict__ edge_key,
+                                                                      int64_t* __restrict__ inst_key,
+                                                                      int64_t* __restrict__ cell_id,
+                                                                      int64_t* __restrict__ f4_key,
+                                                                      int64_t* __restrict__ face_key,
+                                                                      int64_t* __restrict__ face_nc) {
+  const int64_t grp = (int64_t)blockIdx.x * kActiveGroups + threadIdx.x;
+  const int64_t ngrp = (g.NW + 31) >> 5;
+  const uint32_t bits = grp < ngrp ? occ[grp].x : 0u;
+  uint32_t c[kActiveCh] = {0, 0, 0, 0, 0, 0};
+  for (uint32_t m = bits; m; m &= m - 1) {
+    int64_t y, z, wx;
+    uint32_t cw[kActiveCh];
+    active_counts(active_word(g, L, grp * 32 + __ffs(m) - 1, y, z, wx), cw);
+#pragma unroll
+    for (int ch = 0; ch < 5; ch++) c[ch] += cw[ch];
+  }
+  c[5] = __popc(bits);
+  uint32_t ex[kActiveCh], tot[kActiveCh];
+  block_exscan<kActiveCh, kActiveGroups>(c, ex, tot);
+  if (grp >= ngrp) return;
+  uint32_t pos[kActiveCh];
+#pragma unroll
+  for (int ch = 0; ch < kActiveCh; ch++) pos[ch] = sums[ch * ntiles + blockIdx.x] + ex[ch];
+  occ[grp].y = pos[5];
+  for (uint32_t m = bits; m; m &= m - 1) {
+    int64_t y, z, wx;
+    const ActiveBits b = active_word(g, L, grp * 32 + __ffs(m) - 1, y, z, wx);
+    uint32_t cw[kActiveCh];
+    active_counts(b, cw);
+    cw[5] = 1u;
+    emit_word(g, b, y, z, wx, pos, recs, edge_key, inst_key, cell_id, f4_key, face_key, face_nc);
+#pragma unroll
+    for (int ch = 0; ch < kActiveCh; ch++) pos[ch] += cw[ch];
+  }
+}
+
+void launch_active_compact(const GridP& g, const uint32_t* L, RecView rec, const uint32_t* tile_sums,
+                           int64_t* edge_key, int64_t* inst_key, int64_t* cell_id, int64_t* f4_key, int64_t* face_key,
                            int64_t* face_nc, cudaStream_t s) {
   int64_t nt = active_tiles(g);
-  k_active_compact<<<(unsigned)nt, kActiveBlock, 0, s>>>(g, rec, tile_sums, nt, edge_key, inst_key, cell_id, f4_key,
-                                                          face_key, face_nc);
+  // a warp per group while groups are few (latency: a thread would walk its
+  // group's active words serially), a thread per group on large grids
+  if ((g.NW + 31) / 32 < kActiveWarpGroups)
+    k_active_compact_wpg<<<(unsigned)nt, kActiveBlock, 0, s>>>(g, L, const_cast<uint2*>(rec.occ), rec.rec, tile_sums,
+                                                                nt, edge_key, inst_key, cell_id, f4_key, face_key,
+                                                                face_nc);
+  else
+    k_active_compact_tpg<<<(unsigned)nt, kActiveGroups, 0, s>>>(g, L, const_cast<uint2*>(rec.occ), rec.rec, tile_sums,
+                                                                 nt, edge_key, inst_key, cell_id, f4_key, face_key,
+                                                                 face_nc);
+}
+
+// exclusive element prefixes (edges, instances, cells) at word w: the ranks
+// stored in the first active record at or after w, else the totals
+__global__ void k_prefix_at(RecView rv, int64_t w, int64_t A, const unsigned long long* __restrict__ totals,
+                            unsigned long long* __restrict__ out) {
+  const uint2 o = rv.occ[w >> 5];
+  const int64_t a = (int64_t)o.y + __popc(o.x & lowmask((int)(w & 31)));
+  if (a < A) {
+    out[0] = rv.rec[a].pe;
+    out[1] = rv.rec[a].pq;
+    out[2] = rv.rec[a].pc;
+  } else {
+    out[0] = totals[0];
+    out[1] = totals[1];
+    out[2] = totals[2];
+  }
+}
+void launch_prefix_at(RecView rv, int64_t w, int64_t A, const unsigned long long* totals, unsigned long long* out,
+                      cudaStream_t s) {
+  k_prefix_at<<<1, 1, 0, s>>>(rv, w, A, totals, out);
 }
 
 // ===========================================================================
@@ -348,12 +580,12 @@ __device__ __forceinline__ void face_center(const GridP& g, int64_t fk, double p
   p[b] = p[b] + 0.5 * g.h[b];
   p[c] = p[c] + 0.5 * g.h[c];
 }
-__device__ __forceinline__ void set_center_bit(const GridP& g, WordRec* rec, int64_t fk) {
+__device__ __forceinline__ void set_center_bit(const GridP& g, const RecView& rec, int64_t fk) {
   int64_t vid = fk / 3;
   int n = (int)(fk % 3);
   int64_t c[3];
   vid_coords(g, vid, c);
-  atomicOr(&rec[word_of(g, c[0], c[1], c[2])].cf[n], 1u << (c[0] & 31));
+  atomicOr(&rec_find(rec, word_of(g, c[0], c[1], c[2]))->cf[n], 1u << (c[0] & 31));  // a 4-crossing face's word is active
 }
 
 __global__ void k_face_center_points(GridP g, const int64_t* __restrict__ f4, int64_t n, double* __restrict__ pts) {
@@ -369,27 +601,36 @@ void launch_face_center_points(const GridP& g, const int64_t* f4_key, int64_t n,
   if (n) k_face_center_points<<<grid_for(n, 128), 128, 0, s>>>(g, f4_key, n, pts);
 }
 
+template <bool B>
 __global__ void k_face_center_analytic(GridP g, FieldP f, const int64_t* __restrict__ f4, int64_t n,
-                                       WordRec* __restrict__ rec) {
+                                       RecView rec) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double p[3];
-  face_center(g, f4[i], p);
-  if (field_label(f, p)) set_center_bit(g, rec, f4[i]);
+  GridP gl = g;
+  int b = 0;
+  if constexpr (B) b = localize<B>(gl, idiv(f4[i] / 3, g.S2));
+  face_center(gl, f4[i], p);
+  uint32_t lab;
+  if constexpr (B) lab = field_label(f.batch[b], p);
+  else lab = field_label(f, p);
+  if (lab) set_center_bit(g, rec, f4[i]);
 }
-void launch_face_center_analytic(const GridP& g, const FieldP& f, const int64_t* f4_key, int64_t n, WordRec* rec,
+void launch_face_center_analytic(const GridP& g, const FieldP& f, const int64_t* f4_key, int64_t n, RecView rec,
                                  cudaStream_t s) {
-  if (n) k_face_center_analytic<<<grid_for(n, 128), 128, 0, s>>>(g, f, f4_key, n, rec);
+  if (!n) return;
+  if (g.nb) k_face_center_analytic<true><<<grid_for(n, 128), 128, 0, s>>>(g, f, f4_key, n, rec);
+  else k_face_center_analytic<false><<<grid_for(n, 128), 128, 0, s>>>(g, f, f4_key, n, rec);
 }
 
 __global__ void k_face_center_scatter(GridP g, const int64_t* __restrict__ f4, const uint8_t* __restrict__ lab,
-                                      int64_t n, WordRec* __restrict__ rec) {
+                                      int64_t n, RecView rec) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (lab[i]) set_center_bit(g, rec, f4[i]);
 }
 void launch_face_center_scatter(const GridP& g, const int64_t* f4_key, const uint8_t* labels, int64_t n,
-                                WordRec* rec, cudaStream_t s) {
+                                RecView rec, cudaStream_t s) {
   if (n) k_face_center_scatter<<<grid_for(n, 128), 128, 0, s>>>(g, f4_key, labels, n, rec);
 }
 
@@ -431,12 +672,10 @@ __device__ __forceinline__ double linear_t(double ri, double ro, double iso) {
   return t > 1.0 ? 1.0 : t;
 }
 
-__global__ void __launch_bounds__(128) k_search1d_analytic(GridP g, FieldP f, OptP o, const uint32_t* __restrict__ L,
-                                                           const int64_t* __restrict__ edge_key, int64_t K,
-                                                           double* __restrict__ tout, double* __restrict__ pos,
-                                                           int64_t* __restrict__ vin_out) {
-  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
+__device__ __forceinline__ void search1d_one(const GridP& g, const FieldP& f, const OptP& o,
+                                             const uint32_t* __restrict__ L, const int64_t* __restrict__ edge_key,
+                                             int64_t k, double* __restrict__ tout, double* __restrict__ pos,
+                                             int64_t* __restrict__ vin_out) {
   EdgeGeom e = edge_geom(g, L, edge_key[k]);
   double t;
   if (o.one_d == ODC_ONE_D_BINARY) {
@@ -468,10 +707,28 @@ __global__ void __launch_bounds__(128) k_search1d_analytic(GridP g, FieldP f, Op
   if (vin_out) vin_out[k] = e.vin;
 }
 
+template <bool B>
+__global__ void __launch_bounds__(128) k_search1d_analytic(GridP g, FieldP f, OptP o, const uint32_t* __restrict__ L,
+                                                           const int64_t* __restrict__ edge_key, int64_t K,
+                                                           double* __restrict__ tout, double* __restrict__ pos,
+                                                           int64_t* __restrict__ vin_out) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  if constexpr (B) {
+    GridP gl = g;
+    const int sb = localize<B>(gl, idiv(edge_key[k] / 3, g.S2));
+    search1d_one(gl, f.batch[sb], o, L, edge_key, k, tout, pos, vin_out);
+  } else {
+    search1d_one(g, f, o, L, edge_key, k, tout, pos, vin_out);
+  }
+}
+
 void launch_search1d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
                               const int64_t* edge_key, int64_t K, double* t, double* pos, int64_t* v_in,
                               cudaStream_t s) {
-  if (K) k_search1d_analytic<<<grid_for(K, 128), 128, 0, s>>>(g, f, o, L, edge_key, K, t, pos, v_in);
+  if (!K) return;
+  if (g.nb) k_search1d_analytic<true><<<grid_for(K, 128), 128, 0, s>>>(g, f, o, L, edge_key, K, t, pos, v_in);
+  else k_search1d_analytic<false><<<grid_for(K, 128), 128, 0, s>>>(g, f, o, L, edge_key, K, t, pos, v_in);
 }
 
 // lock-step form (batched fields): lo/hi state, points, update, finish
@@ -559,7 +816,7 @@ struct Inst2D {
 
 // Decode an instance key (face_key*2 + slot): corner labels, the slot's edge
 // pair (dualize.py:37-48, :72-88) and the two 1D points in face coordinates.
-__device__ __forceinline__ bool decode_instance(const GridP& g, const uint32_t* L, const WordRec* rec,
+__device__ __forceinline__ bool decode_instance(const GridP& g, const uint32_t* L, RecView rec,
                                                 int64_t ikey, const double* pos1d, Inst2D& I, int64_t pair[2]) {
   const int64_t fk = ikey >> 1;
   const int slot = (int)(ikey & 1);
@@ -589,7 +846,7 @@ __device__ __forceinline__ bool decode_instance(const GridP& g, const uint32_t* 
   } else {
     int64_t cc[3];
     vid_coords(g, vid, cc);
-    const uint32_t centre = (rec[word_of(g, cc[0], cc[1], cc[2])].cf[n] >> (cc[0] & 31)) & 1u;
+    const uint32_t centre = (rec_find(rec, word_of(g, cc[0], cc[1], cc[2]))->cf[n] >> (cc[0] & 31)) & 1u;
     if (centre == I.cl[0]) {
       a0 = slot ? ek[2] : ek[0];
       a1 = slot ? ek[3] : ek[1];
@@ -744,14 +1001,13 @@ __device__ __forceinline__ void line_binary(const FieldP& f, const Inst2D& I, co
   a_out = a;
 }
 
-__global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, OptP o, const uint32_t* __restrict__ L,
-                                                           const WordRec* __restrict__ rec,
-                                                           const int64_t* __restrict__ inst_key, int64_t Q,
-                                                           const double* __restrict__ pos1d, Stage2D out,
-                                                           int64_t* __restrict__ inst_edges, DevStats* st,
-                                                           DevStatus* dst, int64_t st_lo, int64_t st_hi) {
-  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= Q) return;
+template <bool B>
+__device__ __forceinline__ void search2d_one(const GridP& g, const FieldP& f, const OptP& o,
+                                             const uint32_t* __restrict__ L, const RecView& rec,
+                                             const int64_t* __restrict__ inst_key, int64_t q,
+                                             const double* __restrict__ pos1d, const Stage2D& out,
+                                             int64_t* __restrict__ inst_edges, DevStats* st, DevStatus* dst,
+                                             int64_t st_lo, int64_t st_hi) {
   Inst2D I;
   int64_t pair[2];
   decode_instance(g, L, rec, inst_key[q], pos1d, I, pair);
@@ -794,16 +1050,38 @@ __global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, Op
   }
   if (out.status) out.status[q] = status;
   if (out.mid) out.mid[q] = (uint8_t)mid_label;
-  warp_count4(st->status, status, q >= st_lo && q < st_hi);
+  warp_count4<B>(st->status, status, q >= st_lo && q < st_hi);
+}
+
+template <bool B>
+__global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, OptP o, const uint32_t* __restrict__ L,
+                                                           RecView rec,
+                                                           const int64_t* __restrict__ inst_key, int64_t Q,
+                                                           const double* __restrict__ pos1d, Stage2D out,
+                                                           int64_t* __restrict__ inst_edges, DevStats* st,
+                                                           DevStatus* dst, int64_t st_lo, int64_t st_hi) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  if constexpr (B) {
+    GridP gl = g;
+    const int sb = localize<B>(gl, idiv((inst_key[q] >> 1) / 3, g.S2));
+    search2d_one<B>(gl, f.batch[sb], o, L, rec, inst_key, q, pos1d, out, inst_edges, st + sb, dst, st_lo, st_hi);
+  } else {
+    search2d_one<B>(g, f, o, L, rec, inst_key, q, pos1d, out, inst_edges, st, dst, st_lo, st_hi);
+  }
 }
 
 void launch_search2d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
-                              const WordRec* rec, const int64_t* inst_key, int64_t Q, const double* pos1d,
+                              RecView rec, const int64_t* inst_key, int64_t Q, const double* pos1d,
                               Stage2D out, int64_t* inst_edges, DevStats* st, DevStatus* dst, int64_t st_lo,
                               int64_t st_hi, cudaStream_t s) {
-  if (Q)
-    k_search2d_analytic<<<grid_for(Q, 128), 128, 0, s>>>(g, f, o, L, rec, inst_key, Q, pos1d, out, inst_edges, st,
-                                                         dst, st_lo, st_hi);
+  if (!Q) return;
+  if (g.nb)
+    k_search2d_analytic<true><<<grid_for(Q, 128), 128, 0, s>>>(g, f, o, L, rec, inst_key, Q, pos1d, out, inst_edges,
+                                                               st, dst, st_lo, st_hi);
+  else
+    k_search2d_analytic<false><<<grid_for(Q, 128), 128, 0, s>>>(g, f, o, L, rec, inst_key, Q, pos1d, out, inst_edges,
+                                                                st, dst, st_lo, st_hi);
 }
 
 // ---- lock-step 2D search (batched fields) --------------------------------
@@ -910,7 +1188,7 @@ int search2d_num_steps(const OptP& o) { return 1 + o.s1_lin + o.s1_bin + o.s2_li
 
 // instance pairs only (face_pairings, dualize.py:72-88) -- the fd-gradient
 // mode has no 2D search to write them
-__global__ void k_instance_edges(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+__global__ void k_instance_edges(GridP g, const uint32_t* __restrict__ L, RecView rec,
                                  const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
                                  int64_t* __restrict__ inst_edges) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -921,12 +1199,12 @@ __global__ void k_instance_edges(GridP g, const uint32_t* __restrict__ L, const 
   inst_edges[2 * q] = pair[0];
   inst_edges[2 * q + 1] = pair[1];
 }
-void launch_instance_edges(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* inst_key, int64_t Q,
+void launch_instance_edges(const GridP& g, const uint32_t* L, RecView rec, const int64_t* inst_key, int64_t Q,
                            const double* pos1d, int64_t* inst_edges, cudaStream_t s) {
   if (Q) k_instance_edges<<<grid_for(Q, 128), 128, 0, s>>>(g, L, rec, inst_key, Q, pos1d, inst_edges);
 }
 
-__global__ void k_s2_init(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+__global__ void k_s2_init(GridP g, const uint32_t* __restrict__ L, RecView rec,
                           const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
                           S2View S, int64_t* __restrict__ inst_edges) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1016,7 +1294,7 @@ template <int PH>
 __device__ __forceinline__ unsigned s2_apply(const GridP& g, const OptP& o, const uint32_t* __restrict__ L,
                                              const int64_t* __restrict__ inst_key, int64_t Q, int64_t q, int step,
                                              const uint8_t* __restrict__ lab, Inst2D& I, Search2DState& s,
-                                             DevStatus* dst) {
+                                             DevStatus* dst, int64_t q_base) {
   const int n1 = o.s1_lin + o.s1_bin;
   if (PH == 0 || (PH < 0 && step == 0)) {
     s.mid_label = lab[q];
@@ -1034,7 +1312,7 @@ __device__ __forceinline__ unsigned s2_apply(const GridP& g, const OptP& o, cons
     ch.dl[0] = s.dl[0];
     ch.dl[1] = s.dl[1];
     ch.degen = s.degen;
-    if (!ray_direction(I, ch, s.mid_label, s.ray)) raise_status(dst, ODC_E_ASSERT, q);
+    if (!ray_direction(I, ch, s.mid_label, s.ray)) raise_status(dst, ODC_E_ASSERT, q + q_base);
     s.first1 = o.s1_lin;
     s.found1 = 0;
     return W_RAY | W_INT;
@@ -1089,13 +1367,14 @@ __device__ __forceinline__ unsigned s2_apply(const GridP& g, const OptP& o, cons
 }
 
 __global__ void k_s2_update(GridP g, OptP o, const uint32_t* __restrict__ L, const int64_t* __restrict__ inst_key,
-                            int64_t Q, int step, const uint8_t* __restrict__ lab, S2View S, DevStatus* dst) {
+                            int64_t Q, int step, const uint8_t* __restrict__ lab, S2View S, DevStatus* dst,
+                            int64_t q_base) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= Q) return;
   Search2DState s = s2_load(S, q);
   Inst2D I;
   s2_frame(g, inst_key[q], I);
-  s2_store(S, q, s, s2_apply<-1>(g, o, L, inst_key, Q, q, step, lab, I, s, dst));
+  s2_store(S, q, s, s2_apply<-1>(g, o, L, inst_key, Q, q, step, lab, I, s, dst, q_base));
 }
 
 // update with the labels of ``step`` and emit the query points of step + 1
@@ -1120,7 +1399,7 @@ template <int PH>
 __global__ void __launch_bounds__(256) k_s2_step(GridP g, OptP o, const uint32_t* __restrict__ L,
                                                  const int64_t* __restrict__ inst_key, int64_t Q, int step,
                                                  const uint8_t* __restrict__ lab, S2View S, DevStatus* dst,
-                                                 double* __restrict__ pts, S2Compact cmp) {
+                                                 double* __restrict__ pts, S2Compact cmp, int64_t q_base) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (cmp.map && q == 0) {
     *cmp.cnt_clear = 0;
@@ -1137,7 +1416,7 @@ __global__ void __launch_bounds__(256) k_s2_step(GridP g, OptP o, const uint32_t
   }
   Inst2D I;
   s2_frame(g, inst_key[q], I);
-  s2_store(S, q, s, s2_apply<PH>(g, o, L, inst_key, Q, q, step, lab, I, s, dst));
+  s2_store(S, q, s, s2_apply<PH>(g, o, L, inst_key, Q, q, step, lab, I, s, dst, q_base));
   const int next = step + 1;
   const int nr = next > o.s1_lin + o.s1_bin ? 2 : 1;
 #pragma unroll
@@ -1167,7 +1446,7 @@ __global__ void __launch_bounds__(256) k_s2_step(GridP g, OptP o, const uint32_t
   }
 }
 
-__global__ void k_s2_finish(GridP g, OptP o, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+__global__ void k_s2_finish(GridP g, OptP o, const uint32_t* __restrict__ L, RecView rec,
                             const int64_t* __restrict__ inst_key, int64_t Q, const double* __restrict__ pos1d,
                             S2View S, Stage2D out, DevStats* st, int64_t st_lo, int64_t st_hi) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1201,7 +1480,7 @@ __global__ void k_s2_finish(GridP g, OptP o, const uint32_t* __restrict__ L, con
   warp_count4(st->status, status, q >= st_lo && q < st_hi);
 }
 
-void launch_search2d_lockstep_init(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+void launch_search2d_lockstep_init(const GridP& g, const OptP& o, const uint32_t* L, RecView rec,
                                    const int64_t* inst_key, int64_t Q, const double* pos1d, void* state,
                                    int64_t* inst_edges, cudaStream_t s) {
   (void)o;
@@ -1216,8 +1495,9 @@ int64_t launch_search2d_lockstep_points(const GridP& g, const OptP& o, const int
 }
 void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
                                      int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
-                                     cudaStream_t s) {
-  if (Q) k_s2_update<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, inst_key, Q, step, lab, s2_view(state, Q), dst);
+                                     cudaStream_t s, int64_t q_base) {
+  if (Q)
+    k_s2_update<<<grid_for(Q, 128), 128, 0, s>>>(g, o, L, inst_key, Q, step, lab, s2_view(state, Q), dst, q_base);
 }
 bool search2d_step_is_linear(const OptP& o, int step) {
   const int n1 = o.s1_lin + o.s1_bin;
@@ -1226,20 +1506,20 @@ bool search2d_step_is_linear(const OptP& o, int step) {
 int64_t launch_search2d_lockstep_step(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
                                       int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
                                       double* pts, cudaStream_t s, int32_t* map, int64_t* cnt2,
-                                      unsigned long long* sched) {
+                                      unsigned long long* sched, int64_t q_base) {
   if (Q) {
     const int ph = step == 0 ? 0 : step <= o.s1_lin + o.s1_bin ? 1 : 2;
     const S2View v = s2_view(state, Q);
     S2Compact cmp{};
     if (map) cmp = S2Compact{map, cnt2 + ((step + 1) & 1), cnt2 + (step & 1), sched};
-    if (ph == 0) k_s2_step<0><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts, cmp);
+    if (ph == 0) k_s2_step<0><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts, cmp, q_base);
     else if (ph == 1)
-      k_s2_step<1><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts, cmp);
-    else k_s2_step<2><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts, cmp);
+      k_s2_step<1><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts, cmp, q_base);
+    else k_s2_step<2><<<grid_for(Q, 256), 256, 0, s>>>(g, o, L, inst_key, Q, step, lab, v, dst, pts, cmp, q_base);
   }
   return step + 1 > o.s1_lin + o.s1_bin ? 2 * Q : Q;
 }
-void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, RecView rec,
                                      const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,
                                      Stage2D out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s) {
   if (Q)
@@ -1326,21 +1606,24 @@ __device__ __forceinline__ int64_t corner_off(const GridP& g, int c) {
   return (int64_t)(c & 1) + ((c >> 1) & 1) * g.S + ((c >> 2) & 1) * g.S2;
 }
 
-__global__ void k_cell_config(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+__global__ void k_cell_config(GridP g, const uint32_t* __restrict__ L, RecView rec,
                               const int64_t* __restrict__ cell_id, int64_t C, const CellTabEntry* __restrict__ table,
                               uint16_t* __restrict__ cfg_out, uint32_t* __restrict__ ncyc,
                               uint32_t* __restrict__ nsamp) {
   int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (ci >= C) return;
-  const int64_t base = cell_base_vid(g, cell_id[ci]);
+  const int64_t cell = cell_id[ci];
+  const int64_t x = imod(cell, g.R), y = imod(idiv(cell, g.R), g.R), z = idiv(cell, g.R * g.R);
   uint32_t cfg = 0;
-  for (int i = 0; i < 8; i++) cfg |= label_at(L, g, base + corner_off(g, i)) << i;
+#pragma unroll
+  for (int i = 0; i < 8; i++) cfg |= label_c(L, g, x + (i & 1), y + ((i >> 1) & 1), z + ((i >> 2) & 1)) << i;
   uint32_t cm = 0;
+#pragma unroll
   for (int f = 0; f < 6; f++) {
-    const int64_t v = base + corner_off(g, c_LF_CORNER[f]);
-    int64_t c[3];
-    vid_coords(g, v, c);
-    cm |= ((rec[word_of(g, c[0], c[1], c[2])].cf[c_LF_NORMAL[f]] >> (c[0] & 31)) & 1u) << f;
+    const int fc = f < 3 ? 0 : (f == 3 ? 1 : (f == 4 ? 2 : 4));  // c_LF_CORNER
+    const int64_t cx = x + (fc & 1);
+    const WordRec* r = rec_find(rec, word_of(g, cx, y + ((fc >> 1) & 1), z + ((fc >> 2) & 1)));
+    if (r) cm |= ((r->cf[f % 3] >> (cx & 31)) & 1u) << f;  // inactive word: no 4-crossing face
   }
   const uint32_t idx = (cfg << 6) | cm;
   const CellTabEntry& T = table[idx];
@@ -1349,13 +1632,15 @@ __global__ void k_cell_config(GridP g, const uint32_t* __restrict__ L, const Wor
   nsamp[ci] = T.nedge;
 }
 
-void launch_cell_config(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* cell_id, int64_t C,
+void launch_cell_config(const GridP& g, const uint32_t* L, RecView rec, const int64_t* cell_id, int64_t C,
                         const CellTabEntry* table, uint16_t* cfg, uint32_t* ncyc, uint32_t* nsamp, cudaStream_t s) {
   if (C) k_cell_config<<<grid_for(C, 128), 128, 0, s>>>(g, L, rec, cell_id, C, table, cfg, ncyc, nsamp);
 }
 
-__global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint32_t* __restrict__ L,
-                                                    const WordRec* __restrict__ rec,
+constexpr int kSolveBlock = 128;
+template <bool B>
+__global__ void __launch_bounds__(kSolveBlock) k_cell_solve(GridP g, OptP o, const uint32_t* __restrict__ L,
+                                                    RecView rec,
                                                     const int64_t* __restrict__ cell_id, int64_t C,
                                                     const CellTabEntry* __restrict__ table,
                                                     const uint16_t* __restrict__ cfg,
@@ -1364,56 +1649,67 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
                                                     const double* __restrict__ pos1d, const double* __restrict__ pos3,
                                                     const double* __restrict__ edge_normals, CellOut out,
                                                     DevStats* st, int64_t st_lo, int64_t st_hi) {
+  // a cycle's samples (<= 12 edges): normals, 1D-point rows (positions are
+  // re-read from pos1d through L1) and instance ids, in per-thread arrays
+  double xn[36];
+  int32_t xi[24];
+#define NN(j, c) xn[(j) * 3 + (c)]
+#define IID(j) xi[(j)]
+#define ROW(j) xi[12 + (j)]
+#define PE(j, c) __ldg(pos1d + 3 * (int64_t)ROW(j) + (c))
   int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (ci >= C) return;
   const int64_t cell = cell_id[ci];
-  const int64_t base = cell_base_vid(g, cell);
+  const int64_t cc[3] = {imod(cell, g.R), imod(idiv(cell, g.R), g.R), idiv(cell, g.R * g.R)};
+  if constexpr (B) st += localize<B>(g, cc[2]);  // batch: this cell's shape geometry (g is the kernel's copy)
   const CellTabEntry T = table[cfg[ci]];
   const int64_t pbase = part_base[ci];
   const int64_t sbase = samp_base[ci];
   out.pinfo[ci] = ((uint64_t)pbase << 24) | T.cyc_of_edge;
   double hmin = g.h[0] < g.h[1] ? g.h[0] : g.h[1];
   hmin = hmin < g.h[2] ? hmin : g.h[2];
-  const int64_t cc[3] = {imod(cell, g.R), imod(idiv(cell, g.R), g.R), idiv(cell, g.R * g.R)};
   uint32_t nfb = 0;
   uint32_t rank_cnt = 0;  // 8-bit count per QEF rank 0..3
   double max_res = 0.0;
   int slot = 0;
   for (int k = 0; k < T.ncyc; k++) {
     const int len = (T.lens >> (4 * k)) & 15;
-    double pe[12][3], nn[12][3];
-    int64_t iid[12];
     // instance ids of the cycle (instance j joins edge j and j+1)
     for (int j = 0; j < len; j++) {
       const int code = (int)((T.insts >> (4 * (slot + j))) & 15);
       const int f = code >> 1, s = code & 1;
-      iid[j] = inst_rank(rec, g, base + corner_off(g, c_LF_CORNER[f]), c_LF_NORMAL[f]) + s;
+      const int fc = c_LF_CORNER[f];
+      IID(j) = (int32_t)(inst_rank_c(rec, g, cc[0] + (fc & 1), cc[1] + ((fc >> 1) & 1), cc[2] + ((fc >> 2) & 1),
+                                     c_LF_NORMAL[f]) + s);
     }
     for (int j = 0; j < len; j++) {
       const int le = (int)((T.edges >> (4 * (slot + j))) & 15);
-      const int64_t ev = base + corner_off(g, c_LE_CORNER[le]);
+      const int ec = c_LE_CORNER[le];
       const int ax = c_LE_AXIS[le];
-      const int64_t row = edge_rank(rec, g, ev, ax);
-      for (int c = 0; c < 3; c++) pe[j][c] = pos1d[3 * row + c];
+      const int64_t ex = cc[0] + (ec & 1), ey = cc[1] + ((ec >> 1) & 1), ez = cc[2] + ((ec >> 2) & 1);
+      const int64_t row = edge_rank_c(rec, g, ex, ey, ez, ax);
+      double pj[3];
+      ROW(j) = (int32_t)row;
+      for (int c = 0; c < 3; c++) pj[c] = pos1d[3 * row + c];
       if (out.cyc_edges) {
-        out.cyc_edges[sbase + slot + j] = ev * 3 + ax;
-        out.cyc_insts[sbase + slot + j] = iid[j];
+        out.cyc_edges[sbase + slot + j] = (ex + ey * g.S + ez * g.S2) * 3 + ax;
+        out.cyc_insts[sbase + slot + j] = IID(j);
       }
       // edge direction p_out - p_in (dualize.py:421-423)
       double pi[3], po[3], ed[3];
-      const int64_t other = ev + vstep(g, ax);
-      const bool base_in = label_at(L, g, ev) == 1u;
-      vposition(g, base_in ? ev : other, pi);
-      vposition(g, base_in ? other : ev, po);
+      const bool base_in = label_c(L, g, ex, ey, ez) == 1u;
+      const int64_t ox = ex + (ax == 0), oy = ey + (ax == 1), oz = ez + (ax == 2);  // the edge's other end
+      vposition_c(g, base_in ? ex : ox, base_in ? ey : oy, base_in ? ez : oz, pi);
+      vposition_c(g, base_in ? ox : ex, base_in ? oy : ey, base_in ? oz : ez, po);
       for (int c = 0; c < 3; c++) ed[c] = po[c] - pi[c];
       double n[3];
       if (o.normals == ODC_NORMALS_2D) {
         // estimate_normals (dualize.py:299-317)
-        const int64_t ia = iid[(j - 1 + len) % len], ib = iid[j];
+        const int64_t ia = IID((j - 1 + len) % len), ib = IID(j);
         double da[3], db[3];
         for (int c = 0; c < 3; c++) {
-          da[c] = pos3[3 * ia + c] - pe[j][c];
-          db[c] = pos3[3 * ib + c] - pe[j][c];
+          da[c] = pos3[3 * ia + c] - pj[c];
+          db[c] = pos3[3 * ib + c] - pj[c];
         }
         cross3(da, db, n);
         const double nr = norm3(n);
@@ -1430,7 +1726,7 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
       } else {
         for (int c = 0; c < 3; c++) n[c] = edge_normals[3 * row + c];
       }
-      for (int c = 0; c < 3; c++) nn[j][c] = n[c];
+      for (int c = 0; c < 3; c++) NN(j, c) = n[c];
       if (out.normals)
         for (int c = 0; c < 3; c++) out.normals[3 * (sbase + slot + j) + c] = n[c];
     }
@@ -1438,16 +1734,19 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
     const double cnt = (double)(len < 1 ? 1 : len);
     double cen[3] = {0.0, 0.0, 0.0};
     for (int j = 0; j < len; j++)
-      for (int c = 0; c < 3; c++) cen[c] += pe[j][c];
+      for (int c = 0; c < 3; c++) cen[c] += PE(j, c);
     for (int c = 0; c < 3; c++) cen[c] /= cnt;
     double A[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, b[3] = {0.0, 0.0, 0.0};
-    for (int j = 0; j < len; j++)
-      for (int r = 0; r < 3; r++)
-        for (int c = 0; c < 3; c++) A[3 * r + c] += nn[j][r] * nn[j][c];
     for (int j = 0; j < len; j++) {
-      const double d[3] = {pe[j][0] - cen[0], pe[j][1] - cen[1], pe[j][2] - cen[2]};
-      const double off = einsum3(nn[j], d);
-      for (int c = 0; c < 3; c++) b[c] += nn[j][c] * off;
+      const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
+      for (int r = 0; r < 3; r++)
+        for (int c = 0; c < 3; c++) A[3 * r + c] += nj[r] * nj[c];
+    }
+    for (int j = 0; j < len; j++) {
+      const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
+      const double d[3] = {PE(j, 0) - cen[0], PE(j, 1) - cen[1], PE(j, 2) - cen[2]};
+      const double off = einsum3(nj, d);
+      for (int c = 0; c < 3; c++) b[c] += nj[c] * off;
     }
     double w[3], V[9];
     odc_eigh3(A, w, V);  // np.linalg.eigh (dualize.py:358), LAPACK dsyevd bit for bit
@@ -1467,7 +1766,7 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
     for (int i = 0; i < 3; i++) sol[i] = (V[3 * i] * y[0] + V[3 * i + 2] * y[2]) + V[3 * i + 1] * y[1];
     double pos[3];
     for (int c = 0; c < 3; c++) {
-      const double blo = g.lo[c] + (double)cc[c] * g.h[c];  // cell_bounds (grid.py:89-91)
+      const double blo = gpos(g, c, cc[c]);  // cell_bounds (grid.py:89-91): lo + i h
       const double bhi = blo + g.h[c];
       double x = cen[c] + sol[c];
       x = x > blo ? x : blo;  // np.clip
@@ -1476,8 +1775,9 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
     }
     double res = 0.0;
     for (int j = 0; j < len; j++) {
-      const double d[3] = {pos[0] - pe[j][0], pos[1] - pe[j][1], pos[2] - pe[j][2]};
-      const double e = einsum3(nn[j], d);
+      const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
+      const double d[3] = {pos[0] - PE(j, 0), pos[1] - PE(j, 1), pos[2] - PE(j, 2)};
+      const double e = einsum3(nj, d);
       res += e * e;
     }
     const int64_t pid = pbase + k;
@@ -1495,18 +1795,26 @@ __global__ void __launch_bounds__(128) k_cell_solve(GridP g, OptP o, const uint3
   }
   const bool own = ci >= st_lo && ci < st_hi;
 #pragma unroll
-  for (int v = 0; v < 4; v++) warp_count(&st->rank[v], own ? (rank_cnt >> (8 * v)) & 255u : 0u);
-  warp_max_nonneg_double(&st->max_resid_bits, own ? max_res : 0.0);
-  warp_count(&st->normal_fallbacks, own ? (unsigned)nfb : 0u);
+  for (int v = 0; v < 4; v++) warp_count<B>(&st->rank[v], own ? (rank_cnt >> (8 * v)) & 255u : 0u);
+  warp_max_nonneg_double<B>(&st->max_resid_bits, own ? max_res : 0.0);
+  warp_count<B>(&st->normal_fallbacks, own ? (unsigned)nfb : 0u);
 }
+#undef PE
+#undef NN
+#undef IID
+#undef ROW
 
-void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec, const int64_t* cell_id,
+void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, RecView rec, const int64_t* cell_id,
                        int64_t C, const CellTabEntry* table, const uint16_t* cfg, const uint32_t* part_base,
                        const uint32_t* samp_base, const double* pos1d, const double* pos3, const double* edge_normals,
                        CellOut out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s) {
-  if (C)
-    k_cell_solve<<<grid_for(C, 128), 128, 0, s>>>(g, o, L, rec, cell_id, C, table, cfg, part_base, samp_base, pos1d,
-                                                  pos3, edge_normals, out, st, st_lo, st_hi);
+  if (!C) return;
+  if (g.nb)
+    k_cell_solve<true><<<grid_for(C, kSolveBlock), kSolveBlock, 0, s>>>(
+        g, o, L, rec, cell_id, C, table, cfg, part_base, samp_base, pos1d, pos3, edge_normals, out, st, st_lo, st_hi);
+  else
+    k_cell_solve<false><<<grid_for(C, kSolveBlock), kSolveBlock, 0, s>>>(
+        g, o, L, rec, cell_id, C, table, cfg, part_base, samp_base, pos1d, pos3, edge_normals, out, st, st_lo, st_hi);
 }
 
 // generic multi-channel exclusive scan over u32 arrays (<= 2 channels)
@@ -1562,8 +1870,9 @@ void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, i
 __constant__ int8_t c_le_of[8][3] = {{0, 1, 2}, {-1, 3, 4}, {5, -1, 6}, {-1, -1, 7},
                                      {8, 9, -1}, {-1, 10, -1}, {11, -1, -1}, {-1, -1, -1}};
 
+template <bool B>
 __global__ void __launch_bounds__(128) k_poly_classify(GridP g, OptP o, const uint32_t* __restrict__ L,
-                                                       const WordRec* __restrict__ rec,
+                                                       RecView rec,
                                                        const int64_t* __restrict__ edge_key, int64_t K,
                                                        const uint64_t* __restrict__ pinfo,
                                                        const double* __restrict__ verts, int4* __restrict__ pid4,
@@ -1575,6 +1884,7 @@ __global__ void __launch_bounds__(128) k_poly_classify(GridP g, OptP o, const ui
   const int a = (int)(key % 3), b = (a + 1) % 3, c = (a + 2) % 3;
   int64_t vc[3];
   vid_coords(g, vid, vc);
+  if constexpr (B) st += localize<B>(g, vc[2]);  // batch: this edge's shape (g is the kernel's copy)
   const bool fwd = label_at(L, g, vid) == 1u;  // v_in == edge_vertex
   const int RING[4][2] = {{-1, -1}, {0, -1}, {0, 0}, {-1, 0}};
   int pid[4];
@@ -1585,7 +1895,7 @@ __global__ void __launch_bounds__(128) k_poly_classify(GridP g, OptP o, const ui
     cc[b] += RING[rj][0];
     cc[c] += RING[rj][1];
     for (int t = 0; t < 3; t++)
-      if (cc[t] < 0 || cc[t] >= g.R) ok = false;
+      if ((t == 2 && B ? cc[t] - g.zoff : cc[t]) < 0 || (t == 2 && B ? cc[t] - g.zoff : cc[t]) >= g.R) ok = false;
     if (!ok) break;
     const int64_t cbase = cc[0] + cc[1] * g.S + cc[2] * g.S2;
     const int64_t crow = cell_rank(rec, g, cbase);
@@ -1642,15 +1952,19 @@ __global__ void __launch_bounds__(128) k_poly_classify(GridP g, OptP o, const ui
   kase[k] = (uint8_t)cs;
   ntri[k] = cs == 3 ? 4u : 2u;
   nfan[k] = cs == 3 ? 1u : 0u;
-  warp_count4(st->split, cs, true);
+  warp_count4<B>(st->split, cs, true);
 }
 
-void launch_poly_classify(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+void launch_poly_classify(const GridP& g, const OptP& o, const uint32_t* L, RecView rec,
                           const int64_t* edge_key, int64_t K, const uint64_t* pinfo, const double* verts, int4* pid4,
                           uint8_t* kase, uint32_t* ntri, uint32_t* nfan, DevStats* st, cudaStream_t s) {
-  if (K)
-    k_poly_classify<<<grid_for(K, 128), 128, 0, s>>>(g, o, L, rec, edge_key, K, pinfo, verts, pid4, kase, ntri, nfan,
-                                                     st);
+  if (!K) return;
+  if (g.nb)
+    k_poly_classify<true><<<grid_for(K, 128), 128, 0, s>>>(g, o, L, rec, edge_key, K, pinfo, verts, pid4, kase, ntri,
+                                                           nfan, st);
+  else
+    k_poly_classify<false><<<grid_for(K, 128), 128, 0, s>>>(g, o, L, rec, edge_key, K, pinfo, verts, pid4, kase, ntri,
+                                                            nfan, st);
 }
 
 __global__ void k_poly_emit(int64_t K, int64_t P, const int64_t* __restrict__ edge_key, const int4* __restrict__ pid4,
@@ -1978,6 +2292,65 @@ __device__ __forceinline__ bool fan_scratch(const uint32_t* off, int64_t v, char
   return true;
 }
 
+// Registers-only test for the common vertex: its fan is one disc.  With
+// the two other vertices (a_i, b_i) of each of its nt <= kDiscMax incident
+// triangles, walk from triangle 0 across b_0, each step to the other
+// triangle holding the shared neighbour; the fan is one closed disc exactly
+// when every neighbour met on the walk sits in exactly two triangles and the
+// walk returns to triangle 0 after nt steps (then every edge (v,u) has two
+// triangles -- no sheet pairing, polygonize.py:279-305 -- and the union-find
+// of polygonize.py:308-347 finds one component: no new vertex).  Anything
+// else (boundary, >2-triangle edges, several components, degenerate
+// triangles) takes the general path.
+constexpr int kDiscMax = 12;
+__device__ __forceinline__ bool fan_is_disc(const int32_t* __restrict__ tris, const uint32_t* __restrict__ off,
+                                            const int32_t* __restrict__ inc, int64_t v) {
+  const uint32_t b0 = off[v];
+  const int nt = (int)(off[v + 1] - b0);
+  if (nt < 3 || nt > kDiscMax) return false;
+  const int32_t vv = (int32_t)v;
+  int32_t A[kDiscMax], B[kDiscMax];
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < kDiscMax; i++) {
+    A[i] = -1 - 2 * i;  // sentinels: negative, pairwise distinct
+    B[i] = -2 - 2 * i;
+    if (i < nt) {
+      const int64_t t = inc[b0 + i];
+      const int32_t t0 = tris[3 * t], t1 = tris[3 * t + 1], t2 = tris[3 * t + 2];
+      const int hits = (t0 == vv) + (t1 == vv) + (t2 == vv);
+      ok &= hits == 1;
+      A[i] = t0 == vv ? t1 : (t1 == vv ? t2 : t0);
+      B[i] = t0 == vv ? t2 : (t1 == vv ? t0 : t1);
+      ok &= A[i] != B[i];
+    }
+  }
+  if (!ok) return false;
+  int cur = 0;
+  int32_t via = B[0];
+#pragma unroll
+  for (int step = 0; step < kDiscMax; step++) {
+    if (step < nt) {
+      int cnt = 0, nxt = -1;
+      int32_t nvia = 0;
+#pragma unroll
+      for (int j = 0; j < kDiscMax; j++) {
+        const bool ia = A[j] == via, ib = B[j] == via;
+        cnt += (int)ia + (int)ib;
+        if (j != cur && (ia || ib)) {
+          nxt = j;
+          nvia = ia ? B[j] : A[j];
+        }
+      }
+      if (cnt != 2 || nxt < 0) return false;
+      if (nxt == 0 && step != nt - 1) return false;  // a shorter cycle: several components
+      cur = nxt;
+      via = nvia;
+    }
+  }
+  return cur == 0;
+}
+
 __global__ void __launch_bounds__(128) k_repair_count(const double* __restrict__ verts,
                                                       const int32_t* __restrict__ tris, int64_t V,
                                                       const uint32_t* __restrict__ off,
@@ -1985,6 +2358,10 @@ __global__ void __launch_bounds__(128) k_repair_count(const double* __restrict__
                                                       char* big, DevStats* st) {
   int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
+  if (fan_is_disc(tris, off, inc, v)) {
+    extra[v] = 0u;
+    return;
+  }
   FanLocal loc;
   FanScratch f;
   if (!fan_scratch(off, v, big, loc, f)) {
@@ -2049,17 +2426,18 @@ void launch_copy_vertices(const double* src, const int64_t* src_of, int64_t base
 // ===========================================================================
 // slab mode helpers
 // ===========================================================================
-__global__ void k_count_owned_faces(GridP g, const WordRec* __restrict__ rec, DevStats* st) {
+__global__ void k_count_owned_faces(GridP g, RecView rec, DevStats* st) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t nf = 0, n4 = 0;
   if (idx < g.NW) {
     const int64_t z = g.z0 + idiv(idiv(idx, g.W), g.S);
     if (z >= g.own0 && z < g.own1) {
-      const WordRec& r = rec[idx];
-      for (int a = 0; a < 3; a++) {
-        nf += __popc(r.f[a]);
-        n4 += __popc(r.f4[a]);
-      }
+      const WordRec* r = rec_find(rec, idx);
+      if (r)
+        for (int a = 0; a < 3; a++) {
+          nf += __popc(r->f[a]);
+          n4 += __popc(r->f4[a]);
+        }
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -2071,7 +2449,7 @@ __global__ void k_count_owned_faces(GridP g, const WordRec* __restrict__ rec, De
     if (n4) atomicAdd(&st->faces4_own, (unsigned long long)n4);
   }
 }
-void launch_count_owned_faces(const GridP& g, const WordRec* rec, DevStats* st, cudaStream_t s) {
+void launch_count_owned_faces(const GridP& g, RecView rec, DevStats* st, cudaStream_t s) {
   k_count_owned_faces<<<grid_for(g.NW, 256), 256, 0, s>>>(g, rec, st);
 }
 
@@ -2203,7 +2581,7 @@ void launch_mc_count(int64_t C, const uint32_t* ncyc, const uint32_t* nedge, uin
   if (C) k_mc_count<<<grid_for(C, 256), 256, 0, s>>>(C, ncyc, nedge, ntri);
 }
 
-__global__ void k_mc_fans(GridP g, const uint32_t* __restrict__ L, const WordRec* __restrict__ rec,
+__global__ void k_mc_fans(GridP g, const uint32_t* __restrict__ L, RecView rec,
                           const int64_t* __restrict__ cell_id, int64_t C, const CellTabEntry* __restrict__ table,
                           const uint16_t* __restrict__ cfg, const uint32_t* __restrict__ tri_off,
                           const double* __restrict__ pos, int32_t* __restrict__ tris, uint8_t* __restrict__ used) {
@@ -2250,7 +2628,7 @@ __global__ void k_mc_fans(GridP g, const uint32_t* __restrict__ L, const WordRec
     for (int j = 0; j < len; j++) used[rows[j]] = 1;
   }
 }
-void launch_mc_fans(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* cell_id, int64_t C,
+void launch_mc_fans(const GridP& g, const uint32_t* L, RecView rec, const int64_t* cell_id, int64_t C,
                     const CellTabEntry* table, const uint16_t* cfg, const uint32_t* tri_off, const double* pos,
                     int32_t* tris, uint8_t* used, cudaStream_t s) {
   if (C) k_mc_fans<<<grid_for(C, 128), 128, 0, s>>>(g, L, rec, cell_id, C, table, cfg, tri_off, pos, tris, used);

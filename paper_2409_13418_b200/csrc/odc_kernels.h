@@ -48,19 +48,23 @@ void launch_grid_points(const GridP& g, int64_t begin, int64_t n, double* pts, c
 
 // K2: crossing edges / faces / cells + ranks + compaction (grid.py:171-296)
 int64_t active_tiles(const GridP& g);
-void launch_active_bits(const GridP& g, const uint32_t* L, WordRec* rec, uint32_t* tile_sums, DevStats* st,
+int64_t occ_words(const GridP& g);  // uint2 occupancy words of the sparse records
+void launch_active_bits(const GridP& g, const uint32_t* L, uint2* occ, uint32_t* tile_sums, DevStats* st,
                         cudaStream_t s);
 void launch_scan_tiles(uint32_t* sums, int64_t ntiles, int nch, unsigned long long* totals, cudaStream_t s);
-void launch_active_compact(const GridP& g, WordRec* rec, const uint32_t* tile_sums, int64_t* edge_key,
-                           int64_t* inst_key, int64_t* cell_id, int64_t* f4_key, int64_t* face_key,
+void launch_active_compact(const GridP& g, const uint32_t* L, RecView rec, const uint32_t* tile_sums,
+                           int64_t* edge_key, int64_t* inst_key, int64_t* cell_id, int64_t* f4_key, int64_t* face_key,
                            int64_t* face_nc, cudaStream_t s);
+// (pe, pq, pc) at word w (any word): slab ownership ranges
+void launch_prefix_at(RecView rv, int64_t w, int64_t A, const unsigned long long* totals, unsigned long long* out,
+                      cudaStream_t s);
 
 // face-centre probes for 4-crossing faces (dualize.py:59-70)
 void launch_face_center_points(const GridP& g, const int64_t* f4_key, int64_t n, double* pts, cudaStream_t s);
-void launch_face_center_analytic(const GridP& g, const FieldP& f, const int64_t* f4_key, int64_t n, WordRec* rec,
+void launch_face_center_analytic(const GridP& g, const FieldP& f, const int64_t* f4_key, int64_t n, RecView rec,
                                  cudaStream_t s);
 void launch_face_center_scatter(const GridP& g, const int64_t* f4_key, const uint8_t* labels, int64_t n,
-                                WordRec* rec, cudaStream_t s);
+                                RecView rec, cudaStream_t s);
 
 // K3: 1D points (search.py:71-94; pipeline.py:94-123)
 void launch_search1d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
@@ -82,13 +86,13 @@ void launch_edge_endpoints(const GridP& g, const uint32_t* L, const int64_t* edg
 
 // K5: 2D points (dualize.py:97-129 + search.py:194-322)
 void launch_search2d_analytic(const GridP& g, const FieldP& f, const OptP& o, const uint32_t* L,
-                              const WordRec* rec, const int64_t* inst_key, int64_t Q, const double* pos1d,
+                              RecView rec, const int64_t* inst_key, int64_t Q, const double* pos1d,
                               Stage2D out, int64_t* inst_edges, DevStats* st, DevStatus* dst, int64_t st_lo,
                               int64_t st_hi, cudaStream_t s);
 // lock-step form: 31 batches (1 midpoint + s1_lin + s1_bin + s2_lin + s2_bin)
 struct Search2DState;
 size_t search2d_state_bytes(int64_t Q);
-void launch_search2d_lockstep_init(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+void launch_search2d_lockstep_init(const GridP& g, const OptP& o, const uint32_t* L, RecView rec,
                                    const int64_t* inst_key, int64_t Q, const double* pos1d, void* state,
                                    int64_t* inst_edges, cudaStream_t s);
 // step: 0 = midpoint probe, then step-1 linear/binary, then step-2; returns number of points (Q or 2Q)
@@ -96,8 +100,8 @@ int64_t launch_search2d_lockstep_points(const GridP& g, const OptP& o, const int
                                         int step, const void* state, double* pts, cudaStream_t s);
 void launch_search2d_lockstep_update(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
                                      int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
-                                     cudaStream_t s);
-void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+                                     cudaStream_t s, int64_t q_base = 0);
+void launch_search2d_lockstep_finish(const GridP& g, const OptP& o, const uint32_t* L, RecView rec,
                                      const int64_t* inst_key, int64_t Q, const double* pos1d, const void* state,
                                      Stage2D out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s);
 // fused: fold the labels of ``step`` in and write the points of step + 1; returns their count
@@ -110,7 +114,8 @@ bool search2d_step_is_linear(const OptP& o, int step);
 int64_t launch_search2d_lockstep_step(const GridP& g, const OptP& o, const uint32_t* L, const int64_t* inst_key,
                                       int64_t Q, int step, const uint8_t* lab, void* state, DevStatus* dst,
                                       double* pts, cudaStream_t s, int32_t* map = nullptr, int64_t* cnt2 = nullptr,
-                                      unsigned long long* sched = nullptr);
+                                      unsigned long long* sched = nullptr, int64_t q_base = 0);
+// (q_base: index of the first instance of this batch, for error reports)
 int search2d_num_steps(const OptP& o);
 
 // fd-gradient normals (pipeline.py:126-151): 6K raw samples
@@ -121,7 +126,7 @@ void launch_fd_normals(const GridP& g, const OptP& o, const uint32_t* L, const i
                        cudaStream_t s);
 
 // K6: per-cell partitions, plane samples, QEF (dualize.py:194-444)
-void launch_cell_config(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* cell_id, int64_t C,
+void launch_cell_config(const GridP& g, const uint32_t* L, RecView rec, const int64_t* cell_id, int64_t C,
                         const CellTabEntry* table, uint16_t* cfg, uint32_t* ncyc, uint32_t* nsamp, cudaStream_t s);
 void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
                      unsigned long long* totals, cudaStream_t s);
@@ -140,13 +145,13 @@ struct CellOut {
 // numpy.linalg.eigh for a batch of symmetric 3x3 matrices (odc_eigh3.cu)
 void launch_eigh3_batch(const double* A, int64_t n, double* w, double* V, int32_t* info, cudaStream_t s);
 void eigh3_host_batch(const double* A, int64_t n, double* w, double* V, int32_t* info);
-void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec, const int64_t* cell_id,
+void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, RecView rec, const int64_t* cell_id,
                        int64_t C, const CellTabEntry* table, const uint16_t* cfg, const uint32_t* part_base,
                        const uint32_t* samp_base, const double* pos1d, const double* pos3, const double* edge_normals,
                        CellOut out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s);
 
 // K7: polygonization (polygonize.py:110-217)
-void launch_poly_classify(const GridP& g, const OptP& o, const uint32_t* L, const WordRec* rec,
+void launch_poly_classify(const GridP& g, const OptP& o, const uint32_t* L, RecView rec,
                           const int64_t* edge_key, int64_t K, const uint64_t* pinfo, const double* verts,
                           int4* pid4, uint8_t* kase, uint32_t* ntri, uint32_t* nfan, DevStats* st, cudaStream_t s);
 void launch_poly_emit(int64_t K, int64_t P, const int64_t* edge_key, const int4* pid4, const uint8_t* kase,
@@ -175,7 +180,7 @@ void launch_copy_vertices(const double* src, const int64_t* src_of, int64_t base
                           cudaStream_t s);
 
 // slab mode
-void launch_count_owned_faces(const GridP& g, const WordRec* rec, DevStats* st, cudaStream_t s);
+void launch_count_owned_faces(const GridP& g, RecView rec, DevStats* st, cudaStream_t s);
 void launch_globalize_tris(const int32_t* tris, int64_t T, int64_t P_halo, int64_t P_window, int64_t part_base,
                            int64_t P_total, int64_t fan_base, int32_t* out, cudaStream_t s);
 void launch_mark_used(const int32_t* tris, int64_t T, uint8_t* used, cudaStream_t s);
@@ -211,14 +216,14 @@ struct VoxDev {
 };
 void voxel_eval(const VoxDev& w, const PointSrc& src, int64_t n, uint8_t* labels, double* raw, cudaStream_t s);
 
-void launch_instance_edges(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* inst_key, int64_t Q,
+void launch_instance_edges(const GridP& g, const uint32_t* L, RecView rec, const int64_t* inst_key, int64_t Q,
                            const double* pos1d, int64_t* inst_edges, cudaStream_t s);
 
 // marching-cubes baseline (baseline.py:48-127)
 void launch_mc_points(const GridP& g, const uint32_t* L, const int64_t* edge_key, int64_t K, const double* raw_in,
                       const double* raw_out, double iso, double* pos, cudaStream_t s);
 void launch_mc_count(int64_t C, const uint32_t* ncyc, const uint32_t* nedge, uint32_t* ntri, cudaStream_t s);
-void launch_mc_fans(const GridP& g, const uint32_t* L, const WordRec* rec, const int64_t* cell_id, int64_t C,
+void launch_mc_fans(const GridP& g, const uint32_t* L, RecView rec, const int64_t* cell_id, int64_t C,
                     const CellTabEntry* table, const uint16_t* cfg, const uint32_t* tri_off, const double* pos,
                     int32_t* tris, uint8_t* used, cudaStream_t s);
 
@@ -250,5 +255,23 @@ void launch_provenance(int64_t V, int64_t P, const int64_t* src_of, const int64_
 // shared-field hook
 void launch_eval_raw_analytic(const FieldP& f, const double* pts, int64_t n, double* raw, uint8_t* lab,
                               cudaStream_t s);
+
+// ---- batch split (odc_batch.cu): per-shape ranges of a stacked-z batch
+constexpr int kBatchCols = 7;  // edges, instances, cells, 4-faces, partitions, triangles, fans
+void launch_batch_bounds(const GridP& g, RecView rec, int64_t A, int64_t K, int64_t Q, int64_t C,
+                         const int64_t* f4_key, int64_t F4, const uint32_t* pbase, int64_t P, const uint32_t* toff,
+                         const uint32_t* frank, int64_t T, int64_t NF, int64_t* out, cudaStream_t s);
+// vshape + per-shape histogram (hist: 2 nb, all / below V0) + stable sort
+// by shape (tmp == nullptr: size query into *tmp_bytes)
+void batch_sort_vertices(const int32_t* tris, int64_t T, int64_t V, int64_t V0, const int64_t* t_start, int nb,
+                         uint32_t* vshape, uint32_t* skeys, int32_t* iota, int32_t* perm, void* tmp, size_t* tmp_bytes,
+                         unsigned long long* hist, cudaStream_t s);
+void launch_iota_i32(int32_t* a, int64_t n, cudaStream_t s);
+void launch_local_ids(const uint32_t* skeys, const int32_t* perm, int64_t V, const int64_t* v_start, int32_t* local,
+                      cudaStream_t s);
+void launch_batch_gather(const double* verts, const int32_t* perm, const uint32_t* skeys, int64_t V,
+                         const int64_t* kind_in, const int64_t* ref_in, int64_t cell_per_shape,
+                         int64_t key_per_shape, double* vout, int64_t* kout, int64_t* rout, cudaStream_t s);
+void launch_batch_tris(const int32_t* tris, int64_t T, const int32_t* local, int64_t* out, cudaStream_t s);
 
 }  // namespace odc

@@ -13,10 +13,11 @@ constexpr int kScanBlock = 256;
 
 // Block-wide exclusive scan of NCH channels; returns per-thread exclusive
 // prefix and (to all threads) the block total.
-template <int NCH>
+template <int NCH, int BLOCK = kScanBlock>
 __device__ __forceinline__ void block_exscan(const uint32_t (&v)[NCH], uint32_t (&excl)[NCH],
                                              uint32_t (&total)[NCH]) {
-  __shared__ uint32_t wsum[NCH][kScanBlock / 32];
+  static_assert(BLOCK % 32 == 0 && BLOCK <= 1024, "block of whole warps");
+  __shared__ uint32_t wsum[NCH][BLOCK / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t incl[NCH];
 #pragma unroll
@@ -34,13 +35,13 @@ __device__ __forceinline__ void block_exscan(const uint32_t (&v)[NCH], uint32_t 
   if (wid == 0) {
 #pragma unroll
     for (int c = 0; c < NCH; c++) {
-      uint32_t x = lane < kScanBlock / 32 ? wsum[c][lane] : 0u;
+      uint32_t x = lane < BLOCK / 32 ? wsum[c][lane] : 0u;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
-      if (lane < kScanBlock / 32) wsum[c][lane] = x;  // inclusive over warps
+      if (lane < BLOCK / 32) wsum[c][lane] = x;  // inclusive over warps
     }
   }
   __syncthreads();
@@ -48,7 +49,7 @@ __device__ __forceinline__ void block_exscan(const uint32_t (&v)[NCH], uint32_t 
   for (int c = 0; c < NCH; c++) {
     uint32_t before = wid == 0 ? 0u : wsum[c][wid - 1];
     excl[c] = before + incl[c] - v[c];
-    total[c] = wsum[c][kScanBlock / 32 - 1];
+    total[c] = wsum[c][BLOCK / 32 - 1];
   }
   __syncthreads();
 }

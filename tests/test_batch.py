@@ -43,3 +43,74 @@ def test_gpu_batch_shapes_match_oracle():
         o = oracle.contour_oracle(f, lo, hi, 40)
         assert np.array_equal(r.mesh.triangles, o["triangles"])
         assert np.abs(r.mesh.vertices - o["vertices"]).max(initial=0) <= 1e-4 / 40
+
+
+def _stacked_jobs(n, R, extra=()):
+    jobs = []
+    for s in list(scenes.batch_shapes(n)) + list(extra):
+        f, lo, hi = scenes.resolve(s, R)
+        jobs.append((f, GridSpec(lo, hi, R)))
+    return jobs
+
+
+# two boxes sharing an edge (a non-manifold seam the repair splits) and a
+# shape entirely outside the domain (an empty extraction inside the batch)
+_EDGE_BOXES = {"field": {"type": "csg", "op": "union", "children": [
+    {"type": "box", "center": [0.3125, 0.3125, 0.5], "half_extents": [0.1875, 0.1875, 0.3]},
+    {"type": "box", "center": [0.6875, 0.6875, 0.5], "half_extents": [0.1875, 0.1875, 0.3]}]}}
+_OUTSIDE = {"field": {"type": "sphere", "center": [3.0, 3.0, 3.0], "radius": 0.5}}
+
+
+def test_batchable_rules():
+    from paper_2409_13418_b200 import ContourOptions, MlpField
+    from paper_2409_13418_b200.batch import batchable
+
+    jobs = _stacked_jobs(3, 16)
+    assert batchable(jobs, ContourOptions())
+    assert not batchable(jobs[:1], ContourOptions())
+    assert not batchable(jobs, ContourOptions(normals="fd-gradient"))
+    f, lo, hi = scenes.resolve(scenes.batch_shape(0), 20)
+    assert not batchable(jobs + [(f, GridSpec(lo, hi, 20))], ContourOptions())  # mixed resolution
+    assert not batchable(jobs + [(MlpField(seed=0), GridSpec((0, 0, 0), (1, 1, 1), 16))], ContourOptions())
+
+
+def _same(a, b):
+    for m, n in ((a.mesh, b.mesh), (a.raw_mesh, b.raw_mesh)):
+        assert np.array_equal(m.vertices, n.vertices)
+        assert np.array_equal(m.triangles, n.triangles)
+        for x, y in ((m.provenance_kind, n.provenance_kind), (m.provenance_ref, n.provenance_ref)):
+            assert (x is None and y is None) or np.array_equal(np.asarray(x).reshape(-1), np.asarray(y).reshape(-1))
+    assert a.stats["eval_counts"] == b.stats["eval_counts"]
+    for k in ("n_crossing_edges", "n_crossing_cells", "n_partitions", "n_2d_points", "point2d_status_counts",
+              "normal_fallbacks", "qef_rank_counts", "split_case_counts", "skipped_boundary_edges",
+              "repair_added_vertices", "boundary_inside_vertices", "open_boundary"):
+        assert a.stats.get(k) == b.stats.get(k), k
+    if "qef_max_residual" in a.stats:
+        assert a.stats["qef_max_residual"] == b.stats["qef_max_residual"]
+
+
+@pytest.mark.gpu
+def test_gpu_stacked_batch_equals_sequential():
+    """One odc_extract_batch over 24 shapes (incl. a repaired seam and an
+    empty shape) equals contour() of each shape alone: meshes, raw meshes,
+    provenance, statistics and eval accounting."""
+    jobs = _stacked_jobs(22, 48, extra=(_EDGE_BOXES, _OUTSIDE))
+    seq = [contour(f, g) for f, g in jobs]
+    bat = contour_batch(jobs)
+    assert all(r.stats.get("batch_size") == len(jobs) for r in bat)
+    for a, b in zip(seq, bat):
+        _same(a, b)
+    assert seq[-1].mesh.n_vertices == 0
+    print("repair in batch:", [r.stats["repair_added_vertices"] for r in seq if r.stats.get("repair_added_vertices")])
+
+
+@pytest.mark.gpu
+def test_gpu_stacked_batch_matches_oracle():
+    import oracle
+
+    jobs = _stacked_jobs(10, 40, extra=(_EDGE_BOXES,))
+    for (f, g), r in zip(jobs, contour_batch(jobs)):
+        o = oracle.contour_oracle(f, g.lo, g.hi, 40)
+        assert np.array_equal(r.mesh.triangles, o["triangles"])
+        assert np.array_equal(r.mesh.vertices, o["vertices"])
+        assert r.stats["eval_counts"] == o["eval_counts"]
