@@ -195,7 +195,9 @@ int odc_extract_batch(odc_ctx* ctx, const odc_field* const* fields, int32_t nb, 
 int odc_batch_layout(odc_ctx* ctx, int64_t* vertex_start, int64_t* raw_vertices, int64_t* triangle_start);
 /* every shape's repaired mesh (vertices, triangles with shape-local vertex
  * ids, provenance with shape-local refs) and raw triangles, concatenated in
- * shape order; any pointer may be NULL */
+ * shape order; any pointer may be NULL.  Raw triangle rows are written only
+ * for shapes whose repair added vertices (the others' raw mesh is the
+ * repaired one). */
 int odc_copy_batch_meshes(odc_ctx* ctx, double* vertices, int64_t* triangles, int64_t* raw_triangles,
                           int64_t* prov_kind, int64_t* prov_ref);
 

@@ -341,6 +341,7 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
     CUDA_TRY(cudaMemcpyAsync(cur, tris, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
     double* cv = verts;
     char* big = nullptr;  // scratch for fans of more than 64 triangles, allocated on first need
+    uint8_t* dirty = nullptr;  // passes after the first: only vertices whose fan the last pass changed
     int passes = 0;
     for (int pass = 0; pass < 4; pass++) {
       passes++;
@@ -358,14 +359,14 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
       scan1(c, deg, off, curV + 1, totals + 6);
       launch_vertex_fill(cur, T, off, cursor, inc, s);
       check_launch(c);
-      launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s);
+      launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s, dirty);
       check_launch(c);
       if (!big) {  // fans of more than 64 triangles need global scratch: re-run with it
         readback(c, &dst->repair_overflow, sizeof(unsigned long long));
         if (c->h_pinned[0]) {
           big = need(c->arena.get<char>(repair_scratch_bytes(T)));
           CUDA_TRY(cudaMemsetAsync(&dst->repair_overflow, 0, sizeof(unsigned long long), s));
-          launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s);
+          launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s, dirty);
           check_launch(c);
         }
       }
@@ -382,7 +383,10 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
       double* nv = need(c->arena.get<double>(3 * (curV + E)));
       CUDA_TRY(cudaMemcpyAsync(nv, cv, sizeof(double) * 3 * curV, cudaMemcpyDeviceToDevice, s));
       launch_copy_vertices(cv, src_new, curV, E, nv, s);
-      check_launch(c);
+      dirty = need(c->arena.get<uint8_t>(curV + E));
+      CUDA_TRY(cudaMemsetAsync(dirty, 0, (size_t)(curV + E), s));
+      launch_mark_dirty(cur, next, T, dirty, s);
+      check_launch(c, 2);
       cur = next;
       cv = nv;
       curV += E;
@@ -959,24 +963,19 @@ void batch_split(odc_ctx* c, const odc_options* o, const OptP& op, odc_stats* st
     int32_t* iota = need(c->arena.get<int32_t>(V));
     c->b_perm = need(c->arena.get<int32_t>(V));
     c->b_local = need(c->arena.get<int32_t>(V));
-    unsigned long long* hist = need(c->arena.get<unsigned long long>(2 * nb));
+    int64_t* vc = need(c->arena.get<int64_t>(2 * nb + 1));
     size_t tmp_bytes = 0;
-    batch_sort_vertices(c->tris1, T, V, V0, dts, nb, vshape, c->b_skeys, iota, c->b_perm, nullptr, &tmp_bytes, hist,
-                        s);
+    batch_sort_vertices(c->tris1, T, V, V0, dts, nb, vshape, c->b_skeys, iota, c->b_perm, nullptr, &tmp_bytes, vc, s);
     void* tmp = need(c->arena.alloc(tmp_bytes));
     launch_iota_i32(iota, V, s);
-    batch_sort_vertices(c->tris1, T, V, V0, dts, nb, vshape, c->b_skeys, iota, c->b_perm, tmp, &tmp_bytes, hist, s);
+    batch_sort_vertices(c->tris1, T, V, V0, dts, nb, vshape, c->b_skeys, iota, c->b_perm, tmp, &tmp_bytes, vc, s);
     check_launch(c, 4);
-    std::vector<unsigned long long> h(2 * nb);
-    CUDA_TRY(cudaMemcpyAsync(h.data(), hist, sizeof(unsigned long long) * 2 * nb, cudaMemcpyDeviceToHost, s));
+    std::vector<int64_t> h(2 * nb + 1);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), vc, sizeof(int64_t) * (2 * nb + 1), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    for (int b = 0; b < nb; b++) {
-      c->b_vstart[b + 1] = c->b_vstart[b] + (int64_t)h[b];
-      c->b_v0[b] = (int64_t)h[nb + b];
-    }
-    int64_t* dvs = need(c->arena.get<int64_t>(nb + 1));
-    CUDA_TRY(cudaMemcpyAsync(dvs, c->b_vstart.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, s));
-    launch_local_ids(c->b_skeys, c->b_perm, V, dvs, c->b_local, s);
+    for (int b = 0; b <= nb; b++) c->b_vstart[b] = h[b];
+    for (int b = 0; b < nb; b++) c->b_v0[b] = h[nb + 1 + b];
+    launch_local_ids(c->b_skeys, c->b_perm, V, vc, c->b_local, s);
     check_launch(c);
   }
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -1745,10 +1744,14 @@ int odc_copy_batch_meshes(odc_ctx* c, double* vertices, int64_t* triangles, int6
       launch_batch_tris(cc->tris1, T, cc->b_local, t64, s);
       segs.push_back({t64, x->t, sizeof(int64_t) * 3 * T});
     }
-    if (x->raw_t && T) {
+    if (x->raw_t && T && V != V0) {  // pre-repair triangles: only shapes the repair changed
       int64_t* r64 = need(cc->arena.get<int64_t>(3 * T));
       launch_batch_tris(cc->tris0, T, cc->b_local, r64, s);
-      segs.push_back({r64, x->raw_t, sizeof(int64_t) * 3 * T});
+      for (int b = 0; b < cc->nb; b++) {
+        const int64_t t0 = cc->b_bounds[(size_t)b * kBatchCols + 5], t1 = cc->b_bounds[(size_t)(b + 1) * kBatchCols + 5];
+        if (cc->b_vstart[b + 1] - cc->b_vstart[b] != cc->b_v0[b] && t1 > t0)
+          segs.push_back({r64 + 3 * t0, x->raw_t + 3 * t0, sizeof(int64_t) * 3 * (t1 - t0)});
+      }
     }
     CUDA_TRY(cudaGetLastError());
     copy_out_pipelined(cc, segs);

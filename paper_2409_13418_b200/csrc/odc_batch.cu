@@ -101,14 +101,34 @@ __global__ void k_vertex_shape(const int32_t* __restrict__ tris, int64_t T, cons
   vshape[tris[3 * t + 2]] = b;
 }
 
-// per-shape vertex counts: [0, nb) all vertices, [nb, 2 nb) those below V0
-__global__ void k_shape_hist(const uint32_t* __restrict__ vshape, int64_t V, int64_t V0,
-                             unsigned long long* __restrict__ hist, int nb) {
-  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const uint32_t b = vshape[v];
-  atomicAdd(&hist[b], 1ull);
-  if (v < V0) atomicAdd(&hist[nb + b], 1ull);
+// Per-shape vertex starts in the by-shape order (out[0..nb]) and raw-vertex
+// counts (out[nb+1+b]): within a shape's segment the global ids ascend and
+// the raw (pre-repair) vertices are the ids below V0, so both are binary
+// searches (no same-address atomics over millions of vertices).
+__global__ void k_batch_vcounts(const uint32_t* __restrict__ skeys, const int32_t* __restrict__ perm, int64_t V,
+                                int64_t V0, int nb, int64_t* __restrict__ out) {
+  const int b = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  if (b > nb) return;
+  auto first_key = [&](uint32_t key) {  // first i with skeys[i] >= key
+    int64_t lo = 0, hi = V;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (skeys[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  const int64_t s0 = first_key((uint32_t)b);
+  out[b] = s0;
+  if (b == nb) return;
+  const int64_t s1 = first_key((uint32_t)b + 1);
+  int64_t lo = s0, hi = s1;  // first i in [s0, s1) with perm[i] >= V0
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (perm[mid] < V0) lo = mid + 1;
+    else hi = mid;
+  }
+  out[nb + 1 + b] = lo - s0;
 }
 
 // local id of vertex perm[i] = its rank among its shape's vertices
@@ -121,17 +141,16 @@ __global__ void k_local_ids(const uint32_t* __restrict__ skeys, const int32_t* _
 
 void batch_sort_vertices(const int32_t* tris, int64_t T, int64_t V, int64_t V0, const int64_t* t_start, int nb,
                          uint32_t* vshape, uint32_t* skeys, int32_t* iota, int32_t* perm, void* tmp, size_t* tmp_bytes,
-                         unsigned long long* hist, cudaStream_t s) {
+                         int64_t* vcounts, cudaStream_t s) {
   if (!tmp) {  // size query
     cub::DeviceRadixSort::SortPairs(nullptr, *tmp_bytes, vshape, skeys, iota, perm, (int)V, 0, 16, s);
     return;
   }
   if (T) k_vertex_shape<<<grid_for(T, 256), 256, 0, s>>>(tris, T, t_start, nb, vshape);
-  cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 2 * nb, s);
-  if (V) k_shape_hist<<<grid_for(V, 256), 256, 0, s>>>(vshape, V, V0, hist, nb);
   int bits = 1;
   while ((1 << bits) < nb && bits < 16) bits++;
   cub::DeviceRadixSort::SortPairs(tmp, *tmp_bytes, vshape, skeys, iota, perm, (int)V, 0, bits, s);
+  k_batch_vcounts<<<grid_for(nb + 1, 128), 128, 0, s>>>(skeys, perm, V, V0, nb, vcounts);
 }
 
 void launch_local_ids(const uint32_t* skeys, const int32_t* perm, int64_t V, const int64_t* v_start, int32_t* local,

@@ -75,7 +75,7 @@ __device__ __forceinline__ uint32_t bits_below(int64_t limit, int64_t wx) {
 // evaluates every vertex of each undecided word, 32 lanes per word.  Far
 // from the surface one evaluation decides 32 labels.
 template <bool B>
-__global__ void __launch_bounds__(256) k_labels_analytic(GridP g, FieldP f, uint32_t* __restrict__ L) {
+__global__ void __launch_bounds__(256, 4) k_labels_analytic(GridP g, FieldP f, uint32_t* __restrict__ L) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int dec = 2;  // nothing to do
@@ -2355,10 +2355,10 @@ __global__ void __launch_bounds__(128) k_repair_count(const double* __restrict__
                                                       const int32_t* __restrict__ tris, int64_t V,
                                                       const uint32_t* __restrict__ off,
                                                       const int32_t* __restrict__ inc, uint32_t* __restrict__ extra,
-                                                      char* big, DevStats* st) {
+                                                      char* big, DevStats* st, const uint8_t* __restrict__ dirty) {
   int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
-  if (fan_is_disc(tris, off, inc, v)) {
+  if ((dirty && !dirty[v]) || fan_is_disc(tris, off, inc, v)) {
     extra[v] = 0u;
     return;
   }
@@ -2374,8 +2374,26 @@ __global__ void __launch_bounds__(128) k_repair_count(const double* __restrict__
   extra[v] = ex;
 }
 void launch_repair_count(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off, const int32_t* inc,
-                         uint32_t* extra, char* big, DevStats* st, cudaStream_t s) {
-  if (V) k_repair_count<<<grid_for(V, 128), 128, 0, s>>>(verts, tris, V, off, inc, extra, big, st);
+                         uint32_t* extra, char* big, DevStats* st, cudaStream_t s, const uint8_t* dirty) {
+  if (V) k_repair_count<<<grid_for(V, 128), 128, 0, s>>>(verts, tris, V, off, inc, extra, big, st, dirty);
+}
+
+// Vertices whose fan a repair pass changed: every corner (before and after)
+// of a renamed triangle.  Any other vertex keeps its fan, so the next pass
+// finds it as the last one did -- one component, nothing to add
+// (polygonize.py:348-373 re-runs until nothing changes).
+__global__ void k_mark_dirty(const int32_t* __restrict__ cur, const int32_t* __restrict__ next, int64_t T,
+                             uint8_t* __restrict__ dirty) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int32_t a0 = cur[3 * t], a1 = cur[3 * t + 1], a2 = cur[3 * t + 2];
+  const int32_t b0 = next[3 * t], b1 = next[3 * t + 1], b2 = next[3 * t + 2];
+  if (a0 == b0 && a1 == b1 && a2 == b2) return;
+  dirty[a0] = dirty[a1] = dirty[a2] = 1;
+  dirty[b0] = dirty[b1] = dirty[b2] = 1;
+}
+void launch_mark_dirty(const int32_t* cur, const int32_t* next, int64_t T, uint8_t* dirty, cudaStream_t s) {
+  if (T) k_mark_dirty<<<grid_for(T, 256), 256, 0, s>>>(cur, next, T, dirty);
 }
 size_t repair_scratch_bytes(int64_t T) { return (size_t)kFanSlotBytes * 3 * (size_t)T; }
 

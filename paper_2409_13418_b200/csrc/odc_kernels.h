@@ -171,7 +171,10 @@ void launch_vertex_fill(const int32_t* tris, int64_t T, const uint32_t* off, uin
 // vertices are counted in DevStats::repair_overflow and skipped; the host
 // then re-runs with repair_scratch_bytes(T) of scratch)
 void launch_repair_count(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off,
-                         const int32_t* inc, uint32_t* extra, char* big, DevStats* st, cudaStream_t s);
+                         const int32_t* inc, uint32_t* extra, char* big, DevStats* st, cudaStream_t s,
+                         const uint8_t* dirty = nullptr);
+// after a repair pass: flag every corner of the triangles it renamed
+void launch_mark_dirty(const int32_t* cur, const int32_t* next, int64_t T, uint8_t* dirty, cudaStream_t s);
 size_t repair_scratch_bytes(int64_t T);
 void launch_repair_apply(const double* verts, const int32_t* tris, int64_t V, const uint32_t* off,
                          const int32_t* inc, const uint32_t* extra_off, char* big, int32_t* tris_next,
@@ -261,11 +264,12 @@ constexpr int kBatchCols = 7;  // edges, instances, cells, 4-faces, partitions, 
 void launch_batch_bounds(const GridP& g, RecView rec, int64_t A, int64_t K, int64_t Q, int64_t C,
                          const int64_t* f4_key, int64_t F4, const uint32_t* pbase, int64_t P, const uint32_t* toff,
                          const uint32_t* frank, int64_t T, int64_t NF, int64_t* out, cudaStream_t s);
-// vshape + per-shape histogram (hist: 2 nb, all / below V0) + stable sort
-// by shape (tmp == nullptr: size query into *tmp_bytes)
+// vshape + stable sort by shape (tmp == nullptr: size query into
+// *tmp_bytes); vcounts (2 nb + 1): vertex starts per shape (nb + 1), then
+// each shape's raw-vertex count
 void batch_sort_vertices(const int32_t* tris, int64_t T, int64_t V, int64_t V0, const int64_t* t_start, int nb,
                          uint32_t* vshape, uint32_t* skeys, int32_t* iota, int32_t* perm, void* tmp, size_t* tmp_bytes,
-                         unsigned long long* hist, cudaStream_t s);
+                         int64_t* vcounts, cudaStream_t s);
 void launch_iota_i32(int32_t* a, int64_t n, cudaStream_t s);
 void launch_local_ids(const uint32_t* skeys, const int32_t* perm, int64_t V, const int64_t* v_start, int32_t* local,
                       cudaStream_t s);

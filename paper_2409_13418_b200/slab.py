@@ -49,10 +49,11 @@ def slab_ranges(R, world):
 # units of one grid-pass evaluation, measured on one B200: MLP 512^3 --
 # grid pass 76 ms for 1.35e8 evaluations, the rest 38 ms for 5.95e5
 # crossing edges (~115, rounded up for the lower efficiency of the smaller
-# per-slab launches); analytic thin shell 1024^3 -- 6.3 ps per grid vertex,
-# ~2 ns per crossing edge.
+# per-slab launches); analytic thin shell 1024^3 (interval-culled labels,
+# round 2) -- 1.7 ps per grid vertex (labels + active sets), 1.9 ns per
+# crossing edge.
 WORK_PER_CROSSING_MLP = 130.0
-WORK_PER_CROSSING_ANALYTIC = 300.0
+WORK_PER_CROSSING_ANALYTIC = 1100.0
 
 
 def layer_work(field, grid, device=0, nxy=17, nz_max=129, dfield=None):

@@ -1,7 +1,22 @@
-"""Per-rank device time of the z-slab path, emulated on one GPU: each rank's
-slab extraction (odc_extract_slab, halo included) run in turn.  The slowest
-rank bounds the N-GPU step (before the count all-gather and rank 0's
-assembly), so max(rank) vs the 1-GPU extraction estimates strong scaling."""
+"""The z-slab multi-GPU step emulated on one GPU, assembly included.
+
+For each slab count N (balanced bounds, paper_2409_13418_b200.slab):
+  * every rank's slab extraction (odc_extract_slab, halo included) runs in
+    turn: its device time is that rank's share of the step;
+  * rank 0's assembly is then run for real on the same GPU: global ids
+    (odc_slab_globalize), concatenation in rank order, unused-vertex removal
+    and repair of the whole mesh (odc_mesh_finish) -- each timed on the device;
+  * the gather itself (ranks 1..N-1 send vertices, triangles and provenance to
+    rank 0 over NVLink) cannot be run on one GPU: its bytes are counted and
+    its time estimated at --gather-gbs (default 300 GB/s, a conservative
+    NCCL point-to-point rate on NVLink 5 / NVSwitch, 900 GB/s per direction).
+
+step(N) = max over ranks of the slab time + gather estimate + rank 0's
+globalize/concatenate/finish; efficiency = t(1 GPU) / (N step(N)).
+
+    python scripts/slab_emulation.py mlp_512 thin_shell_1024
+"""
+import argparse
 import ctypes
 import sys
 from pathlib import Path
@@ -10,33 +25,95 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from bench import workload  # noqa: E402
-from paper_2409_13418_b200 import GridSpec, _lib, contour  # noqa: E402
+from paper_2409_13418_b200 import GridSpec, _lib  # noqa: E402
 from paper_2409_13418_b200.pipeline import ContourOptions, DeviceField, _grid_args, make_options  # noqa: E402
-from paper_2409_13418_b200.slab import balanced_slab_ranges, slab_ranges  # noqa: E402
+from paper_2409_13418_b200.slab import (assemble, balanced_slab_ranges, extract_piece, global_offsets,  # noqa: E402
+                                        globalize)
 
-name = sys.argv[1] if len(sys.argv) > 1 else "mlp_512"
-field, lo, hi, R, desc = workload(name)
-g = GridSpec(lo, hi, R)
-ctx = _lib.Context(0)
-L = _lib.load()
-lo_c, hi_c, RR = _grid_args(g)
-o = make_options(ContourOptions())
-with DeviceField(ctx, field) as df:
-    st = _lib.Stats()
-    for _ in range(3):
-        assert L.odc_extract(ctx.handle, df.handle, lo_c, hi_c, RR, ctypes.byref(o), ctypes.byref(st)) == 0
-    one = st.device_ms
-    print(f"{name}: 1 GPU {one:.2f} ms")
-    for world, kind in ((2, "equal"), (4, "equal"), (8, "equal"), (2, "balanced"), (4, "balanced"), (8, "balanced")):
-        times = []
-        rr = slab_ranges(R, world) if kind == "equal" else balanced_slab_ranges(field, g, world)
-        for c0, c1 in rr:
+
+def timed(torch, fn, reps=3):
+    best = None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        best = ms if best is None else min(best, ms)
+    return out, best
+
+
+def main():
+    import torch
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("workloads", nargs="*", default=["mlp_512"])
+    ap.add_argument("--gather-gbs", type=float, default=300.0)
+    ap.add_argument("--worlds", default="2,4,8")
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    L = _lib.load()
+    ctx = _lib.context(0)
+    o = make_options(ContourOptions())
+    for name in a.workloads:
+        field, lo, hi, R, desc = workload(name)
+        g = GridSpec(lo, hi, R)
+        lo_c, hi_c, RR = _grid_args(g)
+        with DeviceField(ctx, field) as df:
             st = _lib.Stats()
-            info = _lib.SlabInfo()
-            for _ in range(2):
-                assert L.odc_extract_slab(ctx.handle, df.handle, lo_c, hi_c, RR, ctypes.byref(o), int(c0), int(c1),
-                                          ctypes.byref(st), ctypes.byref(info)) == 0
-            times.append(st.device_ms)
-        mx = max(times)
-        print(f"  {world} {kind} slabs: per-rank ms {np.round(times, 2).tolist()}  max {mx:.2f}  "
-              f"-> speedup {one / mx:.2f} ({one / mx / world * 100:.0f} % of linear, before assembly)")
+            for _ in range(3):
+                assert L.odc_extract(ctx.handle, df.handle, lo_c, hi_c, RR, ctypes.byref(o), ctypes.byref(st)) == 0
+            one = float(st.device_ms)
+            print(f"{name}: 1 GPU {one:.2f} ms (device, whole extraction)")
+            for world in (int(x) for x in a.worlds.split(",")):
+                rr = balanced_slab_ranges(field, g, world, dfield=df)
+                times, pieces = [], []
+                for c0, c1 in rr:
+                    sts = _lib.Stats()
+                    info = _lib.SlabInfo()
+                    for _ in range(2):
+                        assert L.odc_extract_slab(ctx.handle, df.handle, lo_c, hi_c, RR, ctypes.byref(o), int(c0),
+                                                  int(c1), ctypes.byref(sts), ctypes.byref(info)) == 0
+                    times.append(float(sts.device_ms))
+                    pieces.append(extract_piece(field, g, ContourOptions(), c0, c1, 0, dfield=df)[0])
+                counts = np.array([[p.part_vertices.shape[0], p.fan_vertices.shape[0], p.triangles.shape[0]]
+                                   for p in pieces])
+                # rank 0's assembly: globalize every piece (on its own rank in
+                # the real run: counted once, the max), concatenate, finish
+                glob, gl_ms = [], []
+                for k, p in enumerate(pieces):
+                    extract_piece(field, g, ContourOptions(), *rr[k], 0, dfield=df)  # the context's last slab = k
+                    pb, ptot, fb = global_offsets(counts, k)
+                    t, ms = timed(torch, lambda: globalize(p, pb, ptot, fb, dev), reps=1)
+                    gl_ms.append(ms)
+                    glob.append([p.part_vertices, p.fan_vertices, t, p.part_cell, p.part_index, p.fan_edge])
+                (verts, tris, kind, ref), cat_ms = timed(torch, lambda: assemble(glob, dev))
+                fst = _lib.Stats()
+
+                def finish():
+                    torch.cuda.current_stream(dev).synchronize()
+                    rc = L.odc_mesh_finish(ctx.handle, verts.data_ptr(), verts.shape[0], tris.data_ptr(),
+                                           tris.shape[0], int(counts[:, 0].sum()), kind.data_ptr(), ref.data_ptr(),
+                                           1, ctypes.byref(fst))
+                    assert rc == 0, L.odc_last_error(ctx.handle)
+                _, fin_wall = timed(torch, finish)
+                fin_ms = float(fst.device_ms) if fst.device_ms > 0 else fin_wall
+                # bytes that ranks 1.. send to rank 0: vertices (24 B), triangles
+                # (12 B), provenance (kind 8 B + ref 16 B per vertex)
+                sent = 0
+                for p in pieces[1:]:
+                    nv = p.part_vertices.shape[0] + p.fan_vertices.shape[0]
+                    sent += nv * (24 + 24) + p.triangles.shape[0] * 12
+                gather_ms = sent / (a.gather_gbs * 1e9) * 1e3
+                step = max(times) + max(gl_ms) + gather_ms + cat_ms + fin_ms
+                print(f"  {world} balanced slabs: per-rank slab ms {np.round(times, 2).tolist()}")
+                print(f"    max slab {max(times):.2f} + globalize {max(gl_ms):.3f} + gather {gather_ms:.3f} "
+                      f"({sent / 1e6:.1f} MB at {a.gather_gbs:.0f} GB/s, estimated) + concat {cat_ms:.3f} "
+                      f"+ finish {fin_ms:.3f} (V={verts.shape[0]}, T={tris.shape[0]}, +{fst.repair_added_vertices} "
+                      f"repair) = {step:.2f} ms -> speedup {one / step:.2f} ({one / step / world * 100:.0f} % of linear)")
+
+
+if __name__ == "__main__":
+    main()
