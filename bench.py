@@ -338,8 +338,11 @@ def run_gpu(args, rank, world, dist):
         achieved = nbytes / (k1_ms / 1e3) / 1e9
         peak = float(peaks["hbm_gbs"])
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "kernel": "k_labels_analytic (fp64 field program per vertex, bit-packed labels)",
-                "algorithmic": f"{nbytes} label-bitmap bytes written per launch"}
+                "kernel": "k_labels_analytic (interval-culled fp64 field program, bit-packed labels)",
+                "algorithmic": f"{nbytes} label-bitmap bytes written per launch",
+                "note": "no analytic kernel is HBM- or tensor-bound: the grid pass and the dominant stages "
+                        "(2D search, QEF) are fp64 / SM-issue bound -- ncu_* below are the SM throughput, "
+                        "IPC and fp64-pipe fractions of the committed capture (profiles/r2_ncu_summary.md)"}
     roof["peak_source"] = f"{peak_kind} (MEASURED_PEAKS.json)" if peak_kind == "measured" else "fallback"
     roof["kernel_ms"] = k1_ms
     prof = REPO / "profiles" / "ncu_traffic.json"
@@ -359,6 +362,12 @@ def run_gpu(args, rank, world, dist):
         except Exception:
             pass
 
+    stage_names = ["labels", "active_sets", "points_1d", "normals_2d", "cells_qef", "polygonize", "repair",
+                   "labels_kernel"]
+    stage_mean = {n: float(np.mean([x[i] for x in stage])) for i, n in enumerate(stage_names)}
+    dom = max(stage_names[:7], key=lambda n: stage_mean[n])
+    roof["dominant_stage"] = {"stage": dom, "ms": stage_mean[dom], "share": stage_mean[dom] / ms_step}
+
     if rank != 0:
         return
     cpu = None
@@ -366,8 +375,6 @@ def run_gpu(args, rank, world, dist):
         cache = load_cpu_cache(args.workload, field, lo, hi, R)
         v, t_full, cores, sample, dt, info = cpu_sample(field, lo, hi, R, total_evals, args.cpu_sample_r, cache)
         cpu = {"value": v, "unit": "cells/s", "cores": cores, "kind": "port", "sample": sample, **info}
-    stage_names = ["labels", "active_sets", "points_1d", "normals_2d", "cells_qef", "polygonize", "repair",
-                   "labels_kernel"]
     line = {
         "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
@@ -383,7 +390,7 @@ def run_gpu(args, rank, world, dist):
         "cpu_baseline": cpu,
         "gpu_launches": launches,
         "clocks": clock,
-        "stage_ms": {n: float(np.mean([s[i] for s in stage])) for i, n in enumerate(stage_names)},
+        "stage_ms": stage_mean,
         "wall_s_timed_region": t_wall,
         "mesh": {**stats_snapshot, **stats_checks},
     }

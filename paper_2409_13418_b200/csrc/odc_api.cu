@@ -466,6 +466,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     g.NW = g.nz * g.S * g.W;
   }
   c->nb = bin ? bin->nb : 0;
+  set_word_divisors(g);
   c->g = g;
   const OptP op = make_opt(o, f->continuous);
   FieldP fp = f->fp;  // analytic: nodes + fast-path parameters (odc_field_analytic)

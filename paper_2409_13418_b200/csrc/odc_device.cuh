@@ -38,6 +38,9 @@ struct GridP {
   int64_t z0, nz, own0, own1;
   double lo[3], h[3];
   int64_t zoff = 0;            // z of the localized shape's layer 0 (positions use z - zoff)
+  // word index -> (row, x word) and row -> (z, y) by multiply-shift
+  // (set_word_divisors; exact for dividends below 2^31)
+  uint32_t w_m = 0, w_s = 0, s_m = 0, s_s = 0;
   int32_t nb = 0;              // batch: shapes stacked along z (0: one grid)
   const double* geo = nullptr;  // batch: device (nb, 6) = lo[3], h[3] per shape
 };
@@ -77,6 +80,35 @@ __device__ __forceinline__ int64_t imod(int64_t a, int64_t b) {
   return ((uint64_t)a <= 0xffffffffull && (uint64_t)b <= 0xffffffffull) ? (int64_t)((uint32_t)a % (uint32_t)b) : a % b;
 }
 
+// host: multiply-shift constants for n / d, n < 2^31 (round-up multiplier)
+inline void magic_u31(uint32_t d, uint32_t& m, uint32_t& sh) {
+  uint32_t l = 0;
+  while ((1u << l) < d) l++;
+  const uint32_t pw = 31 + l;
+  m = (uint32_t)(((1ull << pw) + d - 1) / d);
+  sh = pw - 32;
+}
+inline void set_word_divisors(GridP& g) {
+  g.w_m = g.s_m = 0;  // 0: word_coords divides (a divisor of 1 has no 32-bit multiplier)
+  if (g.W < 2 || g.S < 2 || g.W > 0xffff || g.S > 0xffff) return;
+  magic_u31((uint32_t)g.W, g.w_m, g.w_s);
+  magic_u31((uint32_t)g.S, g.s_m, g.s_s);
+}
+// label word w -> (y, z, x word) of the window (w < 2^31 words)
+__device__ __forceinline__ void word_coords(const GridP& g, int64_t w, int64_t& y, int64_t& z, int64_t& wx) {
+  if (g.w_m && w < (1ll << 31)) {
+    const uint32_t row = __umulhi((uint32_t)w, g.w_m) >> g.w_s;
+    const uint32_t zr = __umulhi(row, g.s_m) >> g.s_s;
+    wx = (int64_t)((uint32_t)w - row * (uint32_t)g.W);
+    y = (int64_t)(row - zr * (uint32_t)g.S);
+    z = g.z0 + (int64_t)zr;
+    return;
+  }
+  const int64_t row = idiv(w, g.W);
+  wx = w - row * g.W;
+  y = imod(row, g.S);
+  z = g.z0 + idiv(row, g.S);
+}
 __device__ __forceinline__ void vid_coords(const GridP& g, int64_t vid, int64_t c[3]) {
   if ((uint64_t)vid <= 0xffffffffull && g.S <= 0xffff) {  // 32-bit divisions (every grid up to 2^32 vertices)
     const uint32_t v = (uint32_t)vid, S = (uint32_t)g.S;
@@ -415,22 +447,81 @@ static __device__ __noinline__ double field_raw_prog(const odc_node* __restrict_
 // (union / intersection / difference of their binary raws).  Same node
 // arithmetic as the interpreter, so identical bits; anything else runs the
 // interpreter.
-__device__ __forceinline__ double field_raw(const FieldP& f, const double p[3]) {
-  if (f.fast) {  // parameters by value: copied to registers (constant indices)
-    double q0[16];
+// One primitive's label / sd from kernel-parameter space: each primitive
+// loads only its own parameters (a sphere 4 doubles, not the 16 of a
+// rotated box) -- the loads are a large share of a search kernel's
+// instructions, one field evaluation per step.
+template <int N>
+__device__ __forceinline__ void load_params(const double (&q)[16], double (&o)[16]) {
 #pragma unroll
-    for (int i = 0; i < 16; i++) q0[i] = f.fq[0][i];
-    if (f.fast == 1) return prim_inside(f.fop[0], q0, p) ? 1.0 : 0.0;
-    if (f.fast == 2) return smooth_raw(f.fk, prim_sd(f.fop[0], q0, p));
-    double q1[16];
+  for (int i = 0; i < N; i++) o[i] = q[i];
+}
+__device__ __forceinline__ bool prim_inside_p(int op, const double (&q)[16], const double p[3]) {
+  double c[16];
+  if (op == ODC_OP_SPHERE_SD) {
+    load_params<4>(q, c);
+    return sphere_inside(c, p);
+  }
+  if (op == ODC_OP_BOX_SD) {
+    load_params<16>(q, c);
+    return prim_inside(ODC_OP_BOX_SD, c, p);
+  }
+  if (op == ODC_OP_TORUS_SD) {
+    load_params<5>(q, c);
+    return prim_sd(ODC_OP_TORUS_SD, c, p) < 0.0;
+  }
+  load_params<6>(q, c);
+  return prim_sd(ODC_OP_PLANE_SD, c, p) < 0.0;
+}
+__device__ __forceinline__ double prim_sd_p(int op, const double (&q)[16], const double p[3]) {
+  double c[16];
+  if (op == ODC_OP_SPHERE_SD) {
+    load_params<4>(q, c);
+    return prim_sd(ODC_OP_SPHERE_SD, c, p);
+  }
+  if (op == ODC_OP_BOX_SD) {
+    load_params<16>(q, c);
+    return prim_sd(ODC_OP_BOX_SD, c, p);
+  }
+  if (op == ODC_OP_TORUS_SD) {
+    load_params<5>(q, c);
+    return prim_sd(ODC_OP_TORUS_SD, c, p);
+  }
+  load_params<6>(q, c);
+  return prim_sd(ODC_OP_PLANE_SD, c, p);
+}
+
+// SEL: per-primitive parameter loads (prim_inside_p) -- faster when the
+// FieldP sits in global memory (batches); a kernel-parameter FieldP keeps
+// the copy-all form, which its uniform constant loads serve better.
+template <bool SEL = false>
+__device__ __forceinline__ double field_raw_t(const FieldP& f, const double p[3]) {
+  if (f.fast) {
+    if constexpr (SEL) {
+      if (f.fast == 1) return prim_inside_p(f.fop[0], f.fq[0], p) ? 1.0 : 0.0;
+      if (f.fast == 2) return smooth_raw(f.fk, prim_sd_p(f.fop[0], f.fq[0], p));
+      const double a = prim_inside_p(f.fop[0], f.fq[0], p) ? 1.0 : 0.0;
+      double b = prim_inside_p(f.fop[1], f.fq[1], p) ? 1.0 : 0.0;
+      if (f.fop[2] == ODC_OP_RAW_MAX) return (a >= b) ? a : b;
+      if (f.fop[2] == ODC_OP_RAW_MIN) return (a <= b) ? a : b;
+      b = __dsub_rn(1.0, b);
+      return (a <= b) ? a : b;
+    } else {  // parameters by value: copied to registers (constant indices)
+      double q0[16];
 #pragma unroll
-    for (int i = 0; i < 16; i++) q1[i] = f.fq[1][i];
-    const double a = prim_inside(f.fop[0], q0, p) ? 1.0 : 0.0;
-    double b = prim_inside(f.fop[1], q1, p) ? 1.0 : 0.0;
-    if (f.fop[2] == ODC_OP_RAW_MAX) return (a >= b) ? a : b;
-    if (f.fop[2] == ODC_OP_RAW_MIN) return (a <= b) ? a : b;
-    b = __dsub_rn(1.0, b);
-    return (a <= b) ? a : b;
+      for (int i = 0; i < 16; i++) q0[i] = f.fq[0][i];
+      if (f.fast == 1) return prim_inside(f.fop[0], q0, p) ? 1.0 : 0.0;
+      if (f.fast == 2) return smooth_raw(f.fk, prim_sd(f.fop[0], q0, p));
+      double q1[16];
+#pragma unroll
+      for (int i = 0; i < 16; i++) q1[i] = f.fq[1][i];
+      const double a = prim_inside(f.fop[0], q0, p) ? 1.0 : 0.0;
+      double b = prim_inside(f.fop[1], q1, p) ? 1.0 : 0.0;
+      if (f.fop[2] == ODC_OP_RAW_MAX) return (a >= b) ? a : b;
+      if (f.fop[2] == ODC_OP_RAW_MIN) return (a <= b) ? a : b;
+      b = __dsub_rn(1.0, b);
+      return (a <= b) ? a : b;
+    }
   }
   const odc_node* nd = f.nodes;
   if (f.n_nodes == 2) {
@@ -451,6 +542,11 @@ __device__ __forceinline__ double field_raw(const FieldP& f, const double p[3]) 
     }
   }
   return field_raw_prog(f.nodes, f.n_nodes, p);
+}
+__device__ __forceinline__ double field_raw(const FieldP& f, const double p[3]) { return field_raw_t<false>(f, p); }
+template <bool SEL = false>
+__device__ __forceinline__ uint32_t field_label_t(const FieldP& f, const double p[3]) {
+  return field_raw_t<SEL>(f, p) > f.iso ? 1u : 0u;
 }
 __device__ __forceinline__ uint32_t field_label(const FieldP& f, const double p[3]) {
   return field_raw(f, p) > f.iso ? 1u : 0u;

@@ -81,10 +81,7 @@ __global__ void __launch_bounds__(256, 4) k_labels_analytic(GridP g, FieldP f, u
   int dec = 2;  // nothing to do
   int64_t y = 0, z = 0, wx = 0;
   if (w < g.NW) {
-    const int64_t row = idiv(w, g.W);
-    wx = w - row * g.W;
-    y = imod(row, g.S);
-    z = g.z0 + idiv(row, g.S);
+    word_coords(g, w, y, z, wx);
     GridP gl = g;
     const int b = localize<B>(gl, z);
     const int64_t xa = wx * 32, xb = (xa + 31 < g.S - 1) ? xa + 31 : g.S - 1;
@@ -107,7 +104,7 @@ __global__ void __launch_bounds__(256, 4) k_labels_analytic(GridP g, FieldP f, u
       GridP gl = g;
       const int b = localize<B>(gl, zj);
       const double p[3] = {gpos(gl, 0, x), gpos(gl, 1, yj), gpos(gl, 2, zj)};
-      if constexpr (B) lab = field_label(f.batch[b], p);
+      if constexpr (B) lab = field_label_t<true>(f.batch[b], p);
       else lab = field_label(f, p);
     }
     const uint32_t word = __ballot_sync(0xffffffffu, lab);
@@ -273,8 +270,8 @@ __global__ void __launch_bounds__(kActiveBlock) k_active_bits(GridP g, const uin
   for (int j = 0; j < kActiveSub; j++) {
     const int64_t idx = (int64_t)blockIdx.x * kActiveTile + j * kActiveBlock + threadIdx.x;
     if (idx >= g.NW) break;
-    const int64_t row = idiv(idx, g.W), wx = idx - row * g.W;
-    const int64_t y = imod(row, g.S), z = g.z0 + idiv(row, g.S);
+    int64_t y, z, wx;
+    word_coords(g, idx, y, z, wx);
     const ActiveBits b = compute_active(g, L, y, z, wx);
     uint32_t cw[kActiveCh];
     active_counts(b, cw);
@@ -343,10 +340,7 @@ void launch_scan_tiles(uint32_t* sums, int64_t ntiles, int nch, unsigned long lo
 // key lists.  Inactive words -- most of the grid -- cost one bitmap read.
 __device__ __forceinline__ ActiveBits active_word(const GridP& g, const uint32_t* __restrict__ L, int64_t w,
                                                   int64_t& y, int64_t& z, int64_t& wx) {
-  const int64_t row = idiv(w, g.W);
-  wx = w - row * g.W;
-  y = imod(row, g.S);
-  z = g.z0 + idiv(row, g.S);
+  word_coords(g, w, y, z, wx);
   return compute_active(g, L, y, z, wx);
 }
 
@@ -612,7 +606,7 @@ __global__ void k_face_center_analytic(GridP g, FieldP f, const int64_t* __restr
   if constexpr (B) b = localize<B>(gl, idiv(f4[i] / 3, g.S2));
   face_center(gl, f4[i], p);
   uint32_t lab;
-  if constexpr (B) lab = field_label(f.batch[b], p);
+  if constexpr (B) lab = field_label_t<true>(f.batch[b], p);
   else lab = field_label(f, p);
   if (lab) set_center_bit(g, rec, f4[i]);
 }
@@ -672,6 +666,7 @@ __device__ __forceinline__ double linear_t(double ri, double ro, double iso) {
   return t > 1.0 ? 1.0 : t;
 }
 
+template <bool SEL>
 __device__ __forceinline__ void search1d_one(const GridP& g, const FieldP& f, const OptP& o,
                                              const uint32_t* __restrict__ L, const int64_t* __restrict__ edge_key,
                                              int64_t k, double* __restrict__ tout, double* __restrict__ pos,
@@ -684,7 +679,7 @@ __device__ __forceinline__ void search1d_one(const GridP& g, const FieldP& f, co
       double tm = 0.5 * (lo + hi);
       double q[3];
       for (int j = 0; j < 3; j++) q[j] = e.pin[j] + tm * e.span[j];
-      if (field_label(f, q)) lo = tm; else hi = tm;  // bracket: label(lo)=1, label(hi)=0
+      if (field_label_t<SEL>(f, q)) lo = tm; else hi = tm;  // bracket: label(lo)=1, label(hi)=0
     }
     t = clip_t(0.5 * (lo + hi), o.iters_1d);
   } else if (o.one_d == ODC_ONE_D_MIDPOINT) {
@@ -694,8 +689,8 @@ __device__ __forceinline__ void search1d_one(const GridP& g, const FieldP& f, co
     if (o.continuous) {
       double po[3];
       vposition(g, e.vout, po);
-      ri = field_raw(f, e.pin);
-      ro = field_raw(f, po);
+      ri = field_raw_t<SEL>(f, e.pin);
+      ro = field_raw_t<SEL>(f, po);
     } else {
       ri = 1.0;
       ro = 0.0;
@@ -717,9 +712,9 @@ __global__ void __launch_bounds__(128) k_search1d_analytic(GridP g, FieldP f, Op
   if constexpr (B) {
     GridP gl = g;
     const int sb = localize<B>(gl, idiv(edge_key[k] / 3, g.S2));
-    search1d_one(gl, f.batch[sb], o, L, edge_key, k, tout, pos, vin_out);
+    search1d_one<true>(gl, f.batch[sb], o, L, edge_key, k, tout, pos, vin_out);
   } else {
-    search1d_one(g, f, o, L, edge_key, k, tout, pos, vin_out);
+    search1d_one<false>(g, f, o, L, edge_key, k, tout, pos, vin_out);
   }
 }
 
@@ -975,6 +970,7 @@ __device__ __forceinline__ void finish2d(const Inst2D& I, const Chord& ch, doubl
 // same per-element order as the lock-step batches; skipping the samples
 // after the first flip of a linear scan does not change any result, and the
 // eval accounting reports the reference's logical counts.
+template <bool SEL>
 __device__ __forceinline__ void line_binary(const FieldP& f, const Inst2D& I, const double o2[2], const double d2[2],
                                             uint32_t ref, double max_range, int nlin, int nbin, double& a_out,
                                             bool& found) {
@@ -984,7 +980,7 @@ __device__ __forceinline__ void line_binary(const FieldP& f, const Inst2D& I, co
     const double s = max_range * ((double)i / (double)nlin);
     double p[3];
     lift(I, o2[0] + s * d2[0], o2[1] + s * d2[1], p);
-    if (field_label(f, p) != ref) {
+    if (field_label_t<SEL>(f, p) != ref) {
       first = i;
       found = true;
       break;
@@ -996,7 +992,7 @@ __device__ __forceinline__ void line_binary(const FieldP& f, const Inst2D& I, co
     const double m = 0.5 * (a + b);
     double p[3];
     lift(I, o2[0] + m * d2[0], o2[1] + m * d2[1], p);
-    if (field_label(f, p) == ref) a = m; else b = m;
+    if (field_label_t<SEL>(f, p) == ref) a = m; else b = m;
   }
   a_out = a;
 }
@@ -1018,7 +1014,7 @@ __device__ __forceinline__ void search2d_one(const GridP& g, const FieldP& f, co
   const Chord ch = make_chord(I);
   double pm[3];
   lift(I, ch.mid[0], ch.mid[1], pm);
-  const uint32_t mid_label = field_label(f, pm);
+  const uint32_t mid_label = field_label_t<B>(f, pm);
   double ray[2];
   if (!ray_direction(I, ch, mid_label, ray)) {
     raise_status(dst, ODC_E_ASSERT, q);
@@ -1026,14 +1022,14 @@ __device__ __forceinline__ void search2d_one(const GridP& g, const FieldP& f, co
   }
   double dist_r;
   bool found_r;
-  line_binary(f, I, ch.mid, ray, mid_label, o.s1_range * I.hmin, o.s1_lin, o.s1_bin, dist_r, found_r);
+  line_binary<B>(f, I, ch.mid, ray, mid_label, o.s1_range * I.hmin, o.s1_lin, o.s1_bin, dist_r, found_r);
   const double q2[2] = {ch.mid[0] + dist_r * ray[0], ch.mid[1] + dist_r * ray[1]};
   const double r2 = o.s2_range * I.hmin;
   const double dneg[2] = {-ch.dl[0], -ch.dl[1]};
   double da, db;
   bool fa, fb;
-  line_binary(f, I, q2, dneg, mid_label, r2, o.s2_lin, o.s2_bin, da, fa);
-  line_binary(f, I, q2, ch.dl, mid_label, r2, o.s2_lin, o.s2_bin, db, fb);
+  line_binary<B>(f, I, q2, dneg, mid_label, r2, o.s2_lin, o.s2_bin, da, fa);
+  line_binary<B>(f, I, q2, ch.dl, mid_label, r2, o.s2_lin, o.s2_bin, db, fb);
   const double qa[2] = {q2[0] + da * dneg[0], q2[1] + da * dneg[1]};
   const double qb[2] = {q2[0] + db * ch.dl[0], q2[1] + db * ch.dl[1]};
   double p2d[2];
