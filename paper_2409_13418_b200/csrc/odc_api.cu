@@ -1610,7 +1610,9 @@ void copy_out_pipelined(odc_ctx* cc, const std::vector<CopySeg>& segs) {
     CUDA_TRY(cudaEventRecord(cc->copy_evs[i], s));
   }
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const size_t nthr = std::min<size_t>({(size_t)8, (size_t)hw, pieces.size()});
+  // the host side is first-touch page faults into fresh numpy buffers (the
+  // kernel zero-fills ~10 GB/s per thread): as many threads as cores
+  const size_t nthr = std::min<size_t>({(size_t)32, (size_t)hw, pieces.size()});
   std::atomic<int> bad{0};
   auto work = [&](size_t t) {
     for (size_t i = t; i < pieces.size(); i += nthr) {

@@ -26,7 +26,7 @@ def test_gpu_batch_equals_sequential():
         f, lo, hi = scenes.resolve(s, 48)
         jobs.append((f, GridSpec(lo, hi, 48)))
     seq = [contour(f, g) for f, g in jobs]
-    par = contour_batch(jobs, workers=4)
+    par = contour_batch(jobs, workers=4, batched=False)  # the threaded path (non-batchable jobs take it)
     for a, b in zip(seq, par):
         assert np.array_equal(a.mesh.triangles, b.mesh.triangles)
         assert np.array_equal(a.mesh.vertices, b.mesh.vertices)
@@ -114,3 +114,16 @@ def test_gpu_stacked_batch_matches_oracle():
         assert np.array_equal(r.mesh.triangles, o["triangles"])
         assert np.array_equal(r.mesh.vertices, o["vertices"])
         assert r.stats["eval_counts"] == o["eval_counts"]
+
+
+@pytest.mark.gpu
+def test_gpu_batch_with_mlp_takes_the_threaded_path():
+    from paper_2409_13418_b200 import MlpField
+
+    jobs = _stacked_jobs(3, 24) + [(MlpField(seed=1, amplitude=2.0), GridSpec((0, 0, 0), (1, 1, 1), 24))]
+    res = contour_batch(jobs, workers=2)
+    assert all("batch_size" not in r.stats for r in res)  # not stacked
+    for (f, g), r in zip(jobs, res):
+        s = contour(f, g)
+        assert np.array_equal(s.mesh.triangles, r.mesh.triangles)
+        assert np.array_equal(s.mesh.vertices, r.mesh.vertices)
