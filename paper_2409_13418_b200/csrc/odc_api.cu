@@ -354,10 +354,10 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
       CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (curV + 1), s));
       CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * curV, s));
       CUDA_TRY(cudaMemsetAsync(extra, 0, sizeof(uint32_t) * (curV + 1), s));
-      launch_vertex_degree(cur, T, deg, s);
+      launch_vertex_degree(cur, T, deg, s, dirty);
       check_launch(c);
       scan1(c, deg, off, curV + 1, totals + 6);
-      launch_vertex_fill(cur, T, off, cursor, inc, s);
+      launch_vertex_fill(cur, T, off, cursor, inc, s, dirty);
       check_launch(c);
       launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s, dirty);
       check_launch(c);

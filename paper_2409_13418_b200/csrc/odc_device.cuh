@@ -609,13 +609,30 @@ __device__ __forceinline__ int ball_decide(double lo, double hi, double iso) {
 // interval interpreter below.
 static __device__ __noinline__ int field_label_ball_prog(const odc_node* __restrict__ nodes, int n_nodes, double iso,
                                                        double pc0, double pc1, double pc2, double rad);
+// SEL: load only the primitive's own parameters (the rest are zero in the
+// node; batches read the FieldP from global memory, see field_raw_t)
+template <bool SEL>
+__device__ __forceinline__ void prim_ball_fp(int op, const double (&q)[16], const double pc[3], double rad,
+                                             double& lo, double& hi) {
+  double c[16];
+  if constexpr (SEL) {
+#pragma unroll
+    for (int i = 0; i < 16; i++) c[i] = 0.0;
+    if (op == ODC_OP_SPHERE_SD) load_params<4>(q, c);
+    else if (op == ODC_OP_TORUS_SD) load_params<5>(q, c);
+    else if (op == ODC_OP_PLANE_SD) load_params<6>(q, c);
+    else load_params<16>(q, c);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; i++) c[i] = q[i];
+  }
+  prim_ball(op, c, pc, 1.0, rad, lo, hi);
+}
+template <bool SEL = false>
 __device__ __forceinline__ int field_label_ball(const FieldP& f, const double pc[3], double rad) {
   if (f.fast) {
-    double q0[16];
-#pragma unroll
-    for (int i = 0; i < 16; i++) q0[i] = f.fq[0][i];
     double lo, hi;
-    prim_ball(f.fop[0], q0, pc, 1.0, rad, lo, hi);
+    prim_ball_fp<SEL>(f.fop[0], f.fq[0], pc, rad, lo, hi);
     if (f.fast == 1) {
       sd2raw_ball(lo, hi);
     } else if (f.fast == 2) {
@@ -623,11 +640,8 @@ __device__ __forceinline__ int field_label_ball(const FieldP& f, const double pc
       lo = fmin(ra, rb) - 1e-12;
       hi = fmax(ra, rb) + 1e-12;
     } else {
-      double q1[16];
-#pragma unroll
-      for (int i = 0; i < 16; i++) q1[i] = f.fq[1][i];
       double blo, bhi;
-      prim_ball(f.fop[1], q1, pc, 1.0, rad, blo, bhi);
+      prim_ball_fp<SEL>(f.fop[1], f.fq[1], pc, rad, blo, bhi);
       sd2raw_ball(lo, hi);
       sd2raw_ball(blo, bhi);
       if (f.fop[2] == ODC_OP_RAW_MAX) {

@@ -13,6 +13,7 @@
 //   stage   t/pos1d (K), pos2/pos3/status (Q), vertices (P + fans), ...
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "odc_kernels.h"
@@ -1818,24 +1819,55 @@ struct ScanPtrs {
   const uint32_t* in[2];
   uint32_t* out[2];
 };
+// Reduce-then-scan over tiles of kScanPer x kScanBlock elements: each
+// thread owns kScanPer consecutive elements (a serial prefix in registers),
+// so the single-block tile scan sees 8x fewer tiles.
+constexpr int kScanPer = 8;
+constexpr int64_t kScanTile = (int64_t)kScanBlock * kScanPer;
 template <int NCH>
 __global__ void __launch_bounds__(kScanBlock) k_reduce_u32(ScanPtrs p, int64_t n, uint32_t* sums, int64_t ntiles) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t v[NCH], ex[NCH], tot[NCH];
-  for (int c = 0; c < NCH; c++) v[c] = i < n ? p.in[c][i] : 0u;
-  block_exscan<NCH>(v, ex, tot);
-  if (threadIdx.x == 0)
-    for (int c = 0; c < NCH; c++) sums[c * ntiles + blockIdx.x] = tot[c];
+  __shared__ uint32_t part[NCH][kScanBlock / 32];
+  const int64_t i0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPer;
+  uint32_t v[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    v[c] = 0u;
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) v[c] += i0 + k < n ? p.in[c][i0 + k] : 0u;
+    v[c] = __reduce_add_sync(0xffffffffu, v[c]);
+    if ((threadIdx.x & 31) == 0) part[c][threadIdx.x >> 5] = v[c];
+  }
+  __syncthreads();
+  if (threadIdx.x < NCH) {
+    uint32_t t = 0;
+    for (int w = 0; w < kScanBlock / 32; w++) t += part[threadIdx.x][w];
+    sums[threadIdx.x * ntiles + blockIdx.x] = t;
+  }
 }
 template <int NCH>
 __global__ void __launch_bounds__(kScanBlock) k_apply_u32(ScanPtrs p, int64_t n, const uint32_t* sums,
                                                           int64_t ntiles) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t v[NCH], ex[NCH], tot[NCH];
-  for (int c = 0; c < NCH; c++) v[c] = i < n ? p.in[c][i] : 0u;
+  const int64_t i0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPer;
+  uint32_t x[NCH][kScanPer], v[NCH], ex[NCH], tot[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    v[c] = 0u;
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      x[c][k] = i0 + k < n ? p.in[c][i0 + k] : 0u;
+      v[c] += x[c][k];
+    }
+  }
   block_exscan<NCH>(v, ex, tot);
-  if (i < n)
-    for (int c = 0; c < NCH; c++) p.out[c][i] = sums[c * ntiles + blockIdx.x] + ex[c];
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    uint32_t run = sums[c * ntiles + blockIdx.x] + ex[c];
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      if (i0 + k < n) p.out[c][i0 + k] = run;
+      run += x[c][k];
+    }
+  }
 }
 void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
                      unsigned long long* totals, cudaStream_t s) {
@@ -1844,7 +1876,7 @@ void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, i
     p.in[c] = in[c];
     p.out[c] = out[c];
   }
-  const int64_t nt = (n + kScanBlock - 1) / kScanBlock;
+  const int64_t nt = (n + kScanTile - 1) / kScanTile;
   if (nt == 0) {
     cudaMemsetAsync(totals, 0, sizeof(unsigned long long) * nch, s);
     return;
@@ -2006,14 +2038,35 @@ void launch_poly_emit(int64_t K, int64_t P, const int64_t* edge_key, const int4*
                                                  fan_edge, used);
 }
 
-__global__ void k_count_used(const uint8_t* __restrict__ used, int64_t P, DevStats* st) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t v = (i < P && used[i]) ? 1u : 0u;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&st->used_partitions, (unsigned long long)v);
+// used flags are 0/1 bytes: 16 per thread per step (the arena aligns to
+// 256 B), one atomic per block (a same-address atomic per warp serialised
+// in L2: 75 us for 3.5 M flags)
+__global__ void __launch_bounds__(256) k_count_used(const uint8_t* __restrict__ used, int64_t P, DevStats* st) {
+  __shared__ uint32_t part[8];
+  uint32_t v = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 16;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; i < P; i += stride) {
+    if (i + 16 <= P) {
+      const uint4 w = *reinterpret_cast<const uint4*>(used + i);
+      v += __popc(w.x & 0x01010101u) + __popc(w.y & 0x01010101u) + __popc(w.z & 0x01010101u) +
+           __popc(w.w & 0x01010101u);
+    } else {
+      for (int64_t j = i; j < P; j++) v += used[j] ? 1u : 0u;
+    }
+  }
+  v = __reduce_add_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < 8; w++) t += part[w];
+    if (t) atomicAdd(&st->used_partitions, (unsigned long long)t);
+  }
 }
 void launch_count_used(const uint8_t* used, int64_t P, DevStats* st, cudaStream_t s) {
-  if (P) k_count_used<<<grid_for(P, 256), 256, 0, s>>>(used, P, st);
+  if (!P) return;
+  const int64_t blocks = std::min<int64_t>((P + 256 * 16 - 1) / (256 * 16), 148 * 8);
+  k_count_used<<<(unsigned)blocks, 256, 0, s>>>(used, P, st);
 }
 
 // drop unreferenced partition vertices (polygonize.py:199-209)
@@ -2065,25 +2118,31 @@ void launch_interior_flags(int64_t K, const uint8_t* kase, uint32_t* flag, cudaS
 // ===========================================================================
 constexpr int kMaxFan = 64;
 
-__global__ void k_vertex_degree(const int32_t* __restrict__ tris, int64_t T, uint32_t* __restrict__ deg) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 3 * T) return;
-  atomicAdd(&deg[tris[i]], 1u);
-}
-void launch_vertex_degree(const int32_t* tris, int64_t T, uint32_t* deg, cudaStream_t s) {
-  if (T) k_vertex_degree<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, deg);
-}
-__global__ void k_vertex_fill(const int32_t* __restrict__ tris, int64_t T, const uint32_t* __restrict__ off,
-                              uint32_t* __restrict__ cursor, int32_t* __restrict__ inc) {
+// Vertex -> incident-triangle CSR.  dirty (repair passes after the first):
+// only the fans of flagged vertices, the only ones the pass examines.
+__global__ void k_vertex_degree(const int32_t* __restrict__ tris, int64_t T, uint32_t* __restrict__ deg,
+                                const uint8_t* __restrict__ dirty) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 3 * T) return;
   const int32_t v = tris[i];
+  if (!dirty || dirty[v]) atomicAdd(&deg[v], 1u);
+}
+void launch_vertex_degree(const int32_t* tris, int64_t T, uint32_t* deg, cudaStream_t s, const uint8_t* dirty) {
+  if (T) k_vertex_degree<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, deg, dirty);
+}
+__global__ void k_vertex_fill(const int32_t* __restrict__ tris, int64_t T, const uint32_t* __restrict__ off,
+                              uint32_t* __restrict__ cursor, int32_t* __restrict__ inc,
+                              const uint8_t* __restrict__ dirty) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * T) return;
+  const int32_t v = tris[i];
+  if (dirty && !dirty[v]) return;
   const uint32_t slot = atomicAdd(&cursor[v], 1u);
   inc[off[v] + slot] = (int32_t)(i / 3);
 }
 void launch_vertex_fill(const int32_t* tris, int64_t T, const uint32_t* off, uint32_t* cursor, int32_t* inc,
-                        cudaStream_t s) {
-  if (T) k_vertex_fill<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, off, cursor, inc);
+                        cudaStream_t s, const uint8_t* dirty) {
+  if (T) k_vertex_fill<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, off, cursor, inc, dirty);
 }
 
 // Scratch of one fan (nt incident triangles).  Fans of up to kMaxFan
