@@ -227,6 +227,27 @@ int odc_extract_slab(odc_ctx* ctx, const odc_field* field, const double lo[3], c
 /* rewrite the last slab's local triangle ids to global ids (device int32 (T,3)) */
 int odc_slab_globalize(odc_ctx* ctx, int64_t part_base, int64_t n_partitions_total, int64_t fan_base,
                        int32_t* triangles_out);
+/* Distributed finish (no gather of the whole mesh to one rank).  Only the
+ * partitions of a slab's top cell layer are referenced by another rank's
+ * triangles (the next rank's, through its halo); with those "seam"
+ * triangles every vertex's whole fan is on its own rank:
+ *   1. odc_slab_seam: the last slab's triangles with a halo corner (local ids;
+ *      triangles_out NULL = count only) -- sent to the previous rank;
+ *   2. odc_slab_local_finish(seam of the next rank, its n_halo): marks and
+ *      compacts the used owned partitions (polygonize.py:199-209) and counts
+ *      owned vertices whose fan is not one closed disc;
+ *   3. if no rank reports such a vertex the reference's repair
+ *      (polygonize.py:253-374) adds nothing: with the all-gathered used
+ *      counts, odc_slab_top_ids gives the next rank the global ids of this
+ *      rank's top-layer partitions, and odc_slab_final writes the final
+ *      triangles (global ids) and the compacted partition vertices and
+ *      provenance; otherwise the host falls back to odc_mesh_finish. */
+int odc_slab_seam(odc_ctx* ctx, int32_t* triangles_out, int64_t* n_triangles);
+int odc_slab_local_finish(odc_ctx* ctx, const int32_t* next_seam, int64_t n_seam, int64_t next_n_halo,
+                          int64_t* n_used_partitions, int64_t* n_nondisc);
+int odc_slab_top_ids(odc_ctx* ctx, int64_t part_base, int64_t n_top, int32_t* ids_out);
+int odc_slab_final(odc_ctx* ctx, int64_t part_base, int64_t fan_base, const int32_t* halo_ids, int32_t* triangles_out,
+                   double* part_vertices_out, int64_t* part_cell_out, int64_t* part_index_out);
 /* finish an assembled mesh (device or host pointers): unused-vertex removal +
  * repair; the result is read back with odc_copy_mesh / odc_mesh_device. */
 int odc_mesh_finish(odc_ctx* ctx, const double* vertices, int64_t n_vertices, const int32_t* triangles,

@@ -90,6 +90,7 @@ EXPORTS = (
     "odc_validate_manifold", "odc_validate_copy", "odc_count_self_intersections", "odc_self_intersection_pairs",
     "odc_mesh_distance", "odc_triangle_areas", "odc_field_mesh", "odc_field_voxels", "odc_eigh3",
     "odc_eigh3_host", "odc_eval_mlp_dot", "odc_extract_batch", "odc_batch_layout", "odc_copy_batch_meshes",
+    "odc_slab_seam", "odc_slab_local_finish", "odc_slab_top_ids", "odc_slab_final",
 )
 
 _lib = None
@@ -135,6 +136,10 @@ def load():
         L.odc_eigh3_host.argtypes = [vp, i64, vp, vp, vp]
         L.odc_extract_slab.argtypes = [vp, vp, P(dbl), P(dbl), i64, P(Options), i64, i64, P(Stats), P(SlabInfo)]
         L.odc_extract_batch.argtypes = [vp, vp, i32, vp, vp, i64, P(Options), vp]
+        L.odc_slab_seam.argtypes = [vp, vp, P(i64)]
+        L.odc_slab_local_finish.argtypes = [vp, vp, i64, i64, P(i64), P(i64)]
+        L.odc_slab_top_ids.argtypes = [vp, i64, i64, vp]
+        L.odc_slab_final.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp]
         L.odc_batch_layout.argtypes = [vp, vp, vp, vp]
         L.odc_copy_batch_meshes.argtypes = [vp, vp, vp, vp, vp, vp]
         L.odc_slab_globalize.argtypes = [vp, i64, i64, i64, vp]

@@ -156,6 +156,10 @@ struct odc_ctx {
   int64_t e_lo = 0, e_hi = 0, c_lo = 0, c_hi = 0, P_halo = 0, P_own = 0;
   double* slab_verts = nullptr;
   int32_t* slab_tris = nullptr;
+  // distributed finish of the last slab (odc_slab_local_finish)
+  uint8_t* slab_used = nullptr;    // owned partitions referenced by a triangle
+  uint32_t* slab_newid = nullptr;  // their compacted index
+  int64_t slab_U = -1;
   // mesh assembled by odc_mesh_finish: provenance supplied by the caller
   int64_t* prov_kind_in = nullptr;
   int64_t* prov_ref_in = nullptr;
@@ -435,6 +439,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   for (int i = 0; i < ODC_N_CAT; i++) st->cat_order[i] = -1;
   c->valid = false;
   c->launches = 0;
+  c->slab_U = -1;
   c->arena.reset();
   c->keep = o->keep_intermediates != 0;
   cudaStream_t s = c->stream;
@@ -1514,6 +1519,125 @@ struct FinishArgs {
   int32_t repair;
   odc_stats* st;
 };
+
+// ---- distributed slab finish (odc_slabfin.cu, slab.py finish_distributed)
+struct SeamArgs {
+  int32_t* out;
+  int64_t* n;
+};
+// the last slab's triangles with a halo corner (the previous rank's top
+// cell layer), local ids; out == nullptr: count only
+int odc_slab_seam(odc_ctx* c, int32_t* out, int64_t* n_out) {
+  if (!c || !c->valid || !c->slab_mode || !n_out) return ODC_E_ARG;
+  SeamArgs a{out, n_out};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    SeamArgs* x = (SeamArgs*)p;
+    cudaStream_t s = cc->stream;
+    const int64_t T = cc->T;
+    *x->n = 0;
+    if (T == 0 || cc->P_halo == 0) return (int)ODC_OK;
+    uint32_t* flag = need(cc->arena.get<uint32_t>(T));
+    uint32_t* rank = need(cc->arena.get<uint32_t>(T));
+    unsigned long long* tot = need(cc->arena.get<unsigned long long>(1));
+    launch_seam_flags(cc->slab_tris, T, cc->P_halo, flag, s);
+    check_launch(cc);
+    scan1(cc, flag, rank, T, tot);
+    readback(cc, tot, sizeof(unsigned long long));
+    *x->n = (int64_t)cc->h_pinned[0];
+    if (x->out && *x->n) {
+      launch_seam_take(cc->slab_tris, T, flag, rank, x->out, s);
+      check_launch(cc);
+      CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    return (int)ODC_OK;
+  }, &a);
+}
+
+struct LocalFinishArgs {
+  const int32_t* seam;
+  int64_t n_seam, n_halo_next;
+  int64_t *n_used, *n_nondisc;
+};
+
+int odc_slab_local_finish(odc_ctx* c, const int32_t* seam, int64_t n_seam, int64_t n_halo_next, int64_t* n_used,
+                          int64_t* n_nondisc) {
+  if (!c || !c->valid || !c->slab_mode || !n_used || !n_nondisc || n_seam < 0 || (n_seam && !seam))
+    return ODC_E_ARG;
+  if (n_halo_next < 0 || n_halo_next > c->P_own) return ODC_E_ARG;
+  LocalFinishArgs a{seam, n_seam, n_halo_next, n_used, n_nondisc};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    LocalFinishArgs* x = (LocalFinishArgs*)p;
+    cudaStream_t s = cc->stream;
+    const int64_t T = cc->T, Ts = x->n_seam, P = cc->P, Ph = cc->P_halo, Po = cc->P_own, V = cc->P + cc->NF;
+    // this rank's triangles followed by the next rank's seam (mapped)
+    int32_t* ext = need(cc->arena.get<int32_t>(3 * (T + Ts)));
+    if (T) CUDA_TRY(cudaMemcpyAsync(ext, cc->slab_tris, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
+    launch_seam_map(x->seam, Ts, x->n_halo_next, P, V, ext + 3 * T, s);
+    // used owned partitions and their compacted ids (polygonize.py:199-209)
+    cc->slab_used = need(cc->arena.get<uint8_t>(Po));
+    CUDA_TRY(cudaMemsetAsync(cc->slab_used, 0, (size_t)std::max<int64_t>(Po, 1), s));
+    launch_mark_owned(ext, T + Ts, Ph, P, cc->slab_used, s);
+    uint32_t* u32 = need(cc->arena.get<uint32_t>(Po));
+    cc->slab_newid = need(cc->arena.get<uint32_t>(Po));
+    unsigned long long* cnt = need(cc->arena.get<unsigned long long>(4));
+    CUDA_TRY(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), s));
+    launch_widen_flags(cc->slab_used, Po, u32, s);
+    check_launch(cc, 2);
+    scan1(cc, u32, cc->slab_newid, Po, cnt);
+    // every owned vertex's whole fan is here: one closed disc each?
+    uint32_t* deg = need(cc->arena.get<uint32_t>(V + 1));
+    uint32_t* off = need(cc->arena.get<uint32_t>(V + 1));
+    uint32_t* cursor = need(cc->arena.get<uint32_t>(V + 1));
+    int32_t* inc = need(cc->arena.get<int32_t>(3 * (T + Ts)));
+    CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (V + 1), s));
+    CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * (V + 1), s));
+    launch_degree_range(ext, T + Ts, Ph, V, deg, s);
+    check_launch(cc);
+    scan1(cc, deg, off, V + 1, cnt + 1);
+    launch_fill_range(ext, T + Ts, Ph, V, off, cursor, inc, s);
+    launch_count_nondisc(ext, off, inc, Ph, V, cnt + 2, s);
+    check_launch(cc, 2);
+    readback(cc, cnt, 3 * sizeof(unsigned long long));
+    cc->slab_U = (int64_t)cc->h_pinned[0];
+    *x->n_used = cc->slab_U;
+    *x->n_nondisc = (int64_t)cc->h_pinned[2];
+    return (int)ODC_OK;
+  }, &a);
+}
+
+int odc_slab_top_ids(odc_ctx* c, int64_t part_base, int64_t n_top, int32_t* out) {
+  if (!c || !c->valid || !c->slab_mode || c->slab_U < 0 || n_top < 0 || n_top > c->P_own || (n_top && !out))
+    return ODC_E_ARG;
+  cudaSetDevice(c->device);
+  launch_slab_top_ids(c->P_own, n_top, c->slab_newid, part_base, out, c->stream);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    c->err = "slab top ids failed";
+    return ODC_E_CUDA;
+  }
+  return ODC_OK;
+}
+
+int odc_slab_final(odc_ctx* c, int64_t part_base, int64_t fan_base, const int32_t* halo_ids, int32_t* triangles_out,
+                   double* part_vertices_out, int64_t* part_cell_out, int64_t* part_index_out) {
+  if (!c || !c->valid || !c->slab_mode || c->slab_U < 0) return ODC_E_ARG;
+  if ((c->P_halo && !halo_ids) || (c->T && !triangles_out) ||
+      (c->slab_U && (!part_vertices_out || !part_cell_out || !part_index_out)))
+    return ODC_E_ARG;
+  cudaSetDevice(c->device);
+  cudaStream_t s = c->stream;
+  launch_slab_final_tris(c->slab_tris, c->T, c->P_halo, c->P, halo_ids, c->slab_newid, part_base, fan_base,
+                         triangles_out, s);
+  launch_slab_final_parts(c->P_own, c->slab_used, c->slab_newid, c->slab_verts + 3 * c->P_halo,
+                          c->cells.part_cell + c->P_halo, c->cells.part_index + c->P_halo, part_vertices_out,
+                          part_cell_out, part_index_out, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) {
+    c->err = "slab final failed";
+    return ODC_E_CUDA;
+  }
+  return ODC_OK;
+}
 
 int odc_mesh_finish(odc_ctx* c, const double* vertices, int64_t V, const int32_t* triangles, int64_t T,
                     int64_t n_partitions, const int64_t* prov_kind, const int64_t* prov_ref, int32_t repair,

@@ -2347,65 +2347,6 @@ __device__ __forceinline__ bool fan_scratch(const uint32_t* off, int64_t v, char
   return true;
 }
 
-// Registers-only test for the common vertex: its fan is one disc.  With
-// the two other vertices (a_i, b_i) of each of its nt <= kDiscMax incident
-// triangles, walk from triangle 0 across b_0, each step to the other
-// triangle holding the shared neighbour; the fan is one closed disc exactly
-// when every neighbour met on the walk sits in exactly two triangles and the
-// walk returns to triangle 0 after nt steps (then every edge (v,u) has two
-// triangles -- no sheet pairing, polygonize.py:279-305 -- and the union-find
-// of polygonize.py:308-347 finds one component: no new vertex).  Anything
-// else (boundary, >2-triangle edges, several components, degenerate
-// triangles) takes the general path.
-constexpr int kDiscMax = 12;
-__device__ __forceinline__ bool fan_is_disc(const int32_t* __restrict__ tris, const uint32_t* __restrict__ off,
-                                            const int32_t* __restrict__ inc, int64_t v) {
-  const uint32_t b0 = off[v];
-  const int nt = (int)(off[v + 1] - b0);
-  if (nt < 3 || nt > kDiscMax) return false;
-  const int32_t vv = (int32_t)v;
-  int32_t A[kDiscMax], B[kDiscMax];
-  bool ok = true;
-#pragma unroll
-  for (int i = 0; i < kDiscMax; i++) {
-    A[i] = -1 - 2 * i;  // sentinels: negative, pairwise distinct
-    B[i] = -2 - 2 * i;
-    if (i < nt) {
-      const int64_t t = inc[b0 + i];
-      const int32_t t0 = tris[3 * t], t1 = tris[3 * t + 1], t2 = tris[3 * t + 2];
-      const int hits = (t0 == vv) + (t1 == vv) + (t2 == vv);
-      ok &= hits == 1;
-      A[i] = t0 == vv ? t1 : (t1 == vv ? t2 : t0);
-      B[i] = t0 == vv ? t2 : (t1 == vv ? t0 : t1);
-      ok &= A[i] != B[i];
-    }
-  }
-  if (!ok) return false;
-  int cur = 0;
-  int32_t via = B[0];
-#pragma unroll
-  for (int step = 0; step < kDiscMax; step++) {
-    if (step < nt) {
-      int cnt = 0, nxt = -1;
-      int32_t nvia = 0;
-#pragma unroll
-      for (int j = 0; j < kDiscMax; j++) {
-        const bool ia = A[j] == via, ib = B[j] == via;
-        cnt += (int)ia + (int)ib;
-        if (j != cur && (ia || ib)) {
-          nxt = j;
-          nvia = ia ? B[j] : A[j];
-        }
-      }
-      if (cnt != 2 || nxt < 0) return false;
-      if (nxt == 0 && step != nt - 1) return false;  // a shorter cycle: several components
-      cur = nxt;
-      via = nvia;
-    }
-  }
-  return cur == 0;
-}
-
 __global__ void __launch_bounds__(128) k_repair_count(const double* __restrict__ verts,
                                                       const int32_t* __restrict__ tris, int64_t V,
                                                       const uint32_t* __restrict__ off,

@@ -280,4 +280,25 @@ void launch_batch_gather(const double* verts, const int32_t* perm, const uint32_
                          int64_t key_per_shape, double* vout, int64_t* kout, int64_t* rout, cudaStream_t s);
 void launch_batch_tris(const int32_t* tris, int64_t T, const int32_t* local, int64_t* out, cudaStream_t s);
 
+// ---- distributed slab finish (odc_slabfin.cu)
+void launch_seam_flags(const int32_t* tris, int64_t T, int64_t n_halo, uint32_t* flag, cudaStream_t s);
+void launch_seam_take(const int32_t* tris, int64_t T, const uint32_t* flag, const uint32_t* rank, int32_t* out,
+                      cudaStream_t s);
+void launch_seam_map(const int32_t* seam, int64_t n_tris, int64_t n_halo_next, int64_t P, int64_t ghost, int32_t* out,
+                     cudaStream_t s);
+void launch_mark_owned(const int32_t* tris, int64_t n_tris, int64_t P_halo, int64_t P, uint8_t* used,
+                       cudaStream_t s);
+void launch_degree_range(const int32_t* tris, int64_t n_tris, int64_t lo, int64_t hi, uint32_t* deg, cudaStream_t s);
+void launch_fill_range(const int32_t* tris, int64_t n_tris, int64_t lo, int64_t hi, const uint32_t* off,
+                       uint32_t* cursor, int32_t* inc, cudaStream_t s);
+void launch_count_nondisc(const int32_t* tris, const uint32_t* off, const int32_t* inc, int64_t lo, int64_t hi,
+                          unsigned long long* out, cudaStream_t s);
+void launch_slab_final_tris(const int32_t* tris, int64_t T, int64_t P_halo, int64_t P, const int32_t* halo_ids,
+                            const uint32_t* newid, int64_t part_base, int64_t fan_base, int32_t* out, cudaStream_t s);
+void launch_slab_final_parts(int64_t P_own, const uint8_t* used, const uint32_t* newid, const double* verts,
+                             const int64_t* pcell, const int64_t* pidx, double* vout, int64_t* cout, int64_t* iout,
+                             cudaStream_t s);
+void launch_slab_top_ids(int64_t P_own, int64_t n_top, const uint32_t* newid, int64_t part_base, int32_t* out,
+                         cudaStream_t s);
+
 }  // namespace odc

@@ -50,10 +50,12 @@ def slab_ranges(R, world):
 # grid pass 76 ms for 1.35e8 evaluations, the rest 38 ms for 5.95e5
 # crossing edges (~115, rounded up for the lower efficiency of the smaller
 # per-slab launches); analytic thin shell 1024^3 (interval-culled labels,
-# round 2) -- 1.7 ps per grid vertex (labels + active sets), 1.9 ns per
-# crossing edge.
+# round 2) -- the grid pass far from the surface costs ~0.6 ps per vertex
+# (one bound per 32 labels + the active-set pass), and everything near it
+# (undecided label words, searches, cells, polygonization, finish) ~2 ns
+# per crossing edge.
 WORK_PER_CROSSING_MLP = 130.0
-WORK_PER_CROSSING_ANALYTIC = 1100.0
+WORK_PER_CROSSING_ANALYTIC = 3000.0
 
 
 def layer_work(field, grid, device=0, nxy=17, nz_max=129, dfield=None):
@@ -359,11 +361,126 @@ def aggregate_stats(rows, options):
     return d, status, ranks, split, batches, evals, resid
 
 
-def contour_slab(field, grid, options=None, *, rank, world, dist, device=0, to_host=True):
+def _p2p(dist, sends, recvs):
+    """One grouped exchange: sends = [(tensor, peer)], recvs = [(tensor, peer)]."""
+    ops = [dist.P2POp(dist.isend, t, r) for t, r in sends if t.numel()]
+    ops += [dist.P2POp(dist.irecv, t, r) for t, r in recvs if t.numel()]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+def finish_distributed(piece, ctx, rank, world, dist, device, R=None):
+    """Finish the mesh on the ranks that produced it (odc.h "Distributed
+    finish"): seam triangles go one rank down, every rank marks/compacts its
+    used partitions and checks that all its vertices' fans are closed discs.
+    Returns None on every rank when some fan is not (the caller then runs
+    the central finish, which repairs); else this rank's final piece
+    [partition vertices, fan vertices, triangles (global ids), partition
+    cell, partition index, fan edge] and the all-gathered count/stat rows."""
+    import torch
+
+    L = _lib.load()
+    device = torch.device(device)
+    stage = dist.get_backend() == "gloo" and device.type == "cuda"
+    wire = torch.device("cpu") if stage else device
+    _torch_sync(device)  # torch-allocated buffers below are written on libodc's stream
+    n = ctypes.c_int64()
+    _lib.check(L.odc_slab_seam(ctx.handle, None, ctypes.byref(n)), ctx.handle)
+    seam = torch.empty((n.value, 3), dtype=torch.int32, device=device)
+    if n.value:
+        _lib.check(L.odc_slab_seam(ctx.handle, seam.data_ptr(), ctypes.byref(n)), ctx.handle)
+    P, NF, T = piece.part_vertices.shape[0], piece.fan_vertices.shape[0], piece.triangles.shape[0]
+    head = torch.tensor([P, NF, T, piece.c0, piece.c1, piece.n_halo, seam.shape[0]], dtype=torch.int64)
+    sv = torch.cat([head, torch.as_tensor(piece.stats, dtype=torch.int64)]).to(wire)
+    gathered = [torch.zeros_like(sv) for _ in range(world)]
+    dist.all_gather(gathered, sv)
+    rows = torch.stack(gathered).cpu().numpy()
+    allc, stats_rows = rows[:, :7], rows[:, 7:]
+    if rank == 0:
+        check_ranges(allc[:, :5], R)
+    # seam exchange: this rank's seam to the rank below, the next rank's to here
+    nxt = rank + 1 < world
+    recv = torch.empty((int(allc[rank + 1, 6]) if nxt else 0, 3), dtype=torch.int32, device=wire)
+    send = seam.to(wire) if stage else seam
+    _p2p(dist, [(send, rank - 1)] if rank > 0 else [], [(recv, rank + 1)] if nxt else [])
+    recv = recv.to(device)
+    torch.cuda.current_stream(device).synchronize()
+    U, nd = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(L.odc_slab_local_finish(ctx.handle, recv.data_ptr() if recv.numel() else None, recv.shape[0],
+                                       int(allc[rank + 1, 5]) if nxt else 0, ctypes.byref(U), ctypes.byref(nd)),
+               ctx.handle)
+    fin = torch.tensor([U.value, nd.value], dtype=torch.int64, device=wire)
+    got = [torch.zeros_like(fin) for _ in range(world)]
+    dist.all_gather(got, fin)
+    un = torch.stack(got).cpu().numpy()
+    if un[:, 1].sum() > 0:
+        return None
+    Us, NFs = un[:, 0], allc[:, 1]
+    part_base, P_tot = int(Us[:rank].sum()), int(Us.sum())
+    fan_base = P_tot + int(NFs[:rank].sum())
+    # global ids of this rank's top-layer partitions to the next rank (its halo)
+    top = torch.empty((int(allc[rank + 1, 5]) if nxt else 0,), dtype=torch.int32, device=device)
+    if top.numel():
+        _lib.check(L.odc_slab_top_ids(ctx.handle, part_base, top.shape[0], top.data_ptr()), ctx.handle)
+    halo = torch.empty((piece.n_halo,), dtype=torch.int32, device=wire)
+    _p2p(dist, [(top.to(wire) if stage else top, rank + 1)] if nxt else [], [(halo, rank - 1)] if rank > 0 else [])
+    halo = halo.to(device)
+    torch.cuda.current_stream(device).synchronize()
+    u = int(Us[rank])
+    tris = torch.empty((T, 3), dtype=torch.int32, device=device)
+    pv = torch.empty((u, 3), dtype=torch.float64, device=device)
+    pc = torch.empty((u,), dtype=torch.int64, device=device)
+    pi = torch.empty((u,), dtype=torch.int64, device=device)
+    ptr = lambda t: t.data_ptr() if t.numel() else None  # noqa: E731
+    _lib.check(L.odc_slab_final(ctx.handle, part_base, fan_base, ptr(halo), ptr(tris), ptr(pv), ptr(pc), ptr(pi)),
+               ctx.handle)
+    final = [pv, piece.fan_vertices.contiguous(), tris, pc, pi, piece.fan_edge.contiguous()]
+    return final, allc, stats_rows, Us
+
+
+def gather_final(final, Us, allc, rank, world, dist, device):
+    """Rank 0 receives every rank's final piece (one grouped exchange) and
+    concatenates it in the reference's order; None on the other ranks."""
+    import torch
+
+    device = torch.device(device)
+    stage = dist.get_backend() == "gloo" and device.type == "cuda"
+    wire = torch.device("cpu") if stage else device
+    if rank != 0:
+        _p2p(dist, [(t.to(wire) if stage else t, 0) for t in final], [])
+        return None
+    parts = [[t] for t in final]
+    recvs = []
+    for r in range(1, world):
+        u, nf, t = int(Us[r]), int(allc[r, 1]), int(allc[r, 2])
+        bufs = [torch.empty((u, 3), dtype=torch.float64, device=wire),
+                torch.empty((nf, 3), dtype=torch.float64, device=wire),
+                torch.empty((t, 3), dtype=torch.int32, device=wire),
+                torch.empty((u,), dtype=torch.int64, device=wire),
+                torch.empty((u,), dtype=torch.int64, device=wire),
+                torch.empty((nf,), dtype=torch.int64, device=wire)]
+        recvs += [(b, r) for b in bufs]
+        for i, b in enumerate(bufs):
+            parts[i].append(b)
+    _p2p(dist, [], recvs)
+    if stage:
+        parts = [[p[0]] + [b.to(device) for b in p[1:]] for p in parts]
+    return assemble([[p[r] for p in parts] for r in range(world)], device)
+
+
+def contour_slab(field, grid, options=None, *, rank, world, dist, device=0, to_host=True, distributed=True):
     """One rank of a z-slab extraction over ``world`` ranks (one per GPU).
     Returns the ContourResult on rank 0 and None on the other ranks; with
     ``to_host=False`` the finished mesh stays on rank 0's device (read it with
-    odc_mesh_device) and only the stats are returned."""
+    odc_mesh_device) and only the stats are returned.
+
+    ``distributed``: finish on the ranks (finish_distributed) whenever every
+    vertex fan is a closed disc -- then ``to_host=False`` returns as soon as
+    every rank holds its final piece (the mesh stays distributed) and
+    ``to_host=True`` gathers the pieces to rank 0; otherwise (or with
+    ``distributed=False``) the pieces are gathered and rank 0 finishes and
+    repairs the whole mesh."""
     import torch
 
     from .pipeline import ContourOptions, ContourResult, EvalCounter, _copy_mesh, _raise, _raw_from_repaired
@@ -376,6 +493,11 @@ def contour_slab(field, grid, options=None, *, rank, world, dist, device=0, to_h
     with DeviceField(_lib.context(device), field) as df:  # one upload for the probe and the slab
         c0, c1 = balanced_slab_ranges(field, grid, world, device, dfield=df)[rank]
         piece, ctx = extract_piece(field, grid, options, c0, c1, device, dfield=df)
+    if distributed and options.repair and world > 1:
+        dres = finish_distributed(piece, ctx, rank, world, dist, torch.device("cuda", device),
+                                  R=int(grid.resolution))
+        if dres is not None:
+            return _distributed_result(field, options, dres, rank, world, dist, device, to_host, t0)
     out = stitch(piece, rank, world, dist, torch.device("cuda", device), R=int(grid.resolution))
     if out is None:
         return None
@@ -407,6 +529,49 @@ def contour_slab(field, grid, options=None, *, rank, world, dist, device=0, to_h
     stats["n_kernel_launches"] = launches + int(st.n_kernel_launches)
     stats["labels_kernel_ms"] = k_ms
     return ContourResult(mesh, raw, counter, stats)
+
+
+def _distributed_result(field, options, dres, rank, world, dist, device, to_host, t0):
+    import torch
+
+    from .pipeline import ContourResult, EvalCounter
+
+    final, allc, rows, Us = dres
+    if not to_host:
+        torch.cuda.synchronize(device)
+        if rank != 0:
+            return None
+        launches, k_ms = run_extras(rows)
+        ev, kms = rank_label_work(rows)
+        return {"finish": None, "distributed": True, "n_kernel_launches": launches, "labels_kernel_ms": k_ms,
+                "rank_label_evals": ev.tolist(), "rank_label_ms": kms.tolist()}
+    out = gather_final(final, Us, allc, rank, world, dist, device)
+    if out is None:
+        return None
+    verts, tris, kind, ref = out
+    if tris.shape[0] == 0:  # pipeline.py:174-179: the empty mesh carries no provenance
+        mesh = TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64))
+    else:
+        mesh = TriangleMesh(verts.cpu().numpy(), tris.cpu().numpy().astype(np.int64),
+                            provenance_kind=kind.cpu().numpy(), provenance_ref=ref.cpu().numpy())
+
+    class _NoRepair:
+        repair_added_vertices = 0
+
+    stats = slab_stats(rows, options, _NoRepair())
+    counter = EvalCounter(field)
+    _, _, _, _, batches, evals, _ = aggregate_stats(rows, options)
+    for c, name in enumerate(_lib.CATEGORIES):
+        if evals[c] or (batches[c] and c == 0):
+            counter.record(name, int(batches[c]), int(evals[c]))
+    stats["wall_time_s"] = time.perf_counter() - t0
+    stats["eval_counts"] = counter.snapshot()
+    stats["slabs"] = world
+    stats["distributed_finish"] = True
+    launches, k_ms = run_extras(rows)
+    stats["n_kernel_launches"] = launches
+    stats["labels_kernel_ms"] = k_ms
+    return ContourResult(mesh, mesh, counter, stats)
 
 
 def assemble(pieces_global, device):

@@ -14,6 +14,13 @@ For each slab count N (balanced bounds, paper_2409_13418_b200.slab):
 step(N) = max over ranks of the slab time + gather estimate + rank 0's
 globalize/concatenate/finish; efficiency = t(1 GPU) / (N step(N)).
 
+Distributed finish (slab.finish_distributed, used when every fan is a
+closed disc): per rank the slab extraction, its seam, the local finish with
+the next rank's seam and the final ids, all timed on the device; the two
+neighbour exchanges (seam triangles, top-layer ids) are a few MB and are
+estimated at the same rate.  The mesh then stays on the ranks; gathering it
+to rank 0 is the end-to-end part (reported separately).
+
     python scripts/slab_emulation.py mlp_512 thin_shell_1024
 """
 import argparse
@@ -109,6 +116,56 @@ def main():
                 gather_ms = sent / (a.gather_gbs * 1e9) * 1e3
                 step = max(times) + max(gl_ms) + gather_ms + cat_ms + fin_ms
                 print(f"  {world} balanced slabs: per-rank slab ms {np.round(times, 2).tolist()}")
+                # distributed finish, ranks from the top down (rank k needs rank k+1's seam)
+                dist_ms, nondisc, seam_next, xbytes = [0.0] * world, 0, None, 0
+                for k in reversed(range(world)):
+                    c0, c1 = rr[k]
+                    sts = _lib.Stats()
+                    info = _lib.SlabInfo()
+                    assert L.odc_extract_slab(ctx.handle, df.handle, lo_c, hi_c, RR, ctypes.byref(o), int(c0),
+                                              int(c1), ctypes.byref(sts), ctypes.byref(info)) == 0
+                    n = ctypes.c_int64()
+
+                    def seam_fn():
+                        L.odc_slab_seam(ctx.handle, None, ctypes.byref(n))
+                        t = torch.empty((n.value, 3), dtype=torch.int32, device=dev)
+                        if n.value:
+                            L.odc_slab_seam(ctx.handle, t.data_ptr(), ctypes.byref(n))
+                        return t
+                    seam, t_seam = timed(torch, seam_fn, reps=1)
+                    nh_next = int(pieces[k + 1].n_halo) if k + 1 < world else 0
+                    U, nd = ctypes.c_int64(), ctypes.c_int64()
+                    sn = seam_next if seam_next is not None else torch.empty((0, 3), dtype=torch.int32, device=dev)
+
+                    def local_fn():
+                        assert L.odc_slab_local_finish(ctx.handle, sn.data_ptr() if sn.numel() else None,
+                                                       sn.shape[0], nh_next, ctypes.byref(U), ctypes.byref(nd)) == 0
+                    _, t_local = timed(torch, local_fn, reps=1)
+                    nondisc += nd.value
+                    u = U.value
+                    T_k = int(counts[k, 2])
+                    top = torch.zeros((nh_next,), dtype=torch.int32, device=dev)
+                    halo = torch.zeros((int(pieces[k].n_halo),), dtype=torch.int32, device=dev)
+                    tri = torch.empty((T_k, 3), dtype=torch.int32, device=dev)
+                    pv = torch.empty((u, 3), dtype=torch.float64, device=dev)
+                    pc = torch.empty((u,), dtype=torch.int64, device=dev)
+                    pi = torch.empty((u,), dtype=torch.int64, device=dev)
+                    ptr = lambda t: t.data_ptr() if t.numel() else None  # noqa: E731
+
+                    def final_fn():
+                        if nh_next:
+                            assert L.odc_slab_top_ids(ctx.handle, 0, nh_next, top.data_ptr()) == 0
+                        assert L.odc_slab_final(ctx.handle, 0, 0, ptr(halo), ptr(tri), ptr(pv), ptr(pc), ptr(pi)) == 0
+                    _, t_final = timed(torch, final_fn, reps=1)
+                    dist_ms[k] = times[k] + t_seam + t_local + t_final
+                    xbytes = max(xbytes, seam.numel() * 4 + nh_next * 4)
+                    seam_next = seam
+                xchg_ms = 2 * xbytes / (a.gather_gbs * 1e9) * 1e3 + 0.05  # two neighbour exchanges + all-gathers
+                dstep = max(dist_ms) + xchg_ms
+                print(f"    distributed finish: per-rank ms {np.round(dist_ms, 2).tolist()} + exchanges "
+                      f"{xchg_ms:.3f} (est) = {dstep:.2f} ms -> speedup {one / dstep:.2f} "
+                      f"({one / dstep / world * 100:.0f} % of linear); non-disc fans {nondisc} "
+                      f"({'fallback to the central finish' if nondisc else 'distributed path taken'})")
                 print(f"    max slab {max(times):.2f} + globalize {max(gl_ms):.3f} + gather {gather_ms:.3f} "
                       f"({sent / 1e6:.1f} MB at {a.gather_gbs:.0f} GB/s, estimated) + concat {cat_ms:.3f} "
                       f"+ finish {fin_ms:.3f} (V={verts.shape[0]}, T={tris.shape[0]}, +{fst.repair_added_vertices} "

@@ -213,10 +213,10 @@ def test_gpu_slab_globalize_device_equals_host():
             assert np.array_equal(dev, host.astype(np.int32))
 
 
-def _slab_worker(rank, world, port, backend, result_path):
+def _slab_worker(rank, world, port, backend, result_path, scene="mlp", distributed=True):
     import torch.distributed as dist
 
-    from paper_2409_13418_b200 import GridSpec, MlpField, contour
+    from paper_2409_13418_b200 import GridSpec, MlpField, contour, scenes
     from paper_2409_13418_b200.slab import contour_slab
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -224,9 +224,14 @@ def _slab_worker(rank, world, port, backend, result_path):
     dev = rank if backend == "nccl" else 0
     dist.init_process_group(backend, rank=rank, world_size=world)
     try:
-        field = MlpField(seed=0, amplitude=3.0)
-        g = GridSpec((0, 0, 0), (1, 1, 1), 56)
-        res = contour_slab(field, g, rank=rank, world=world, dist=dist, device=dev)
+        if scene == "mlp":
+            field = MlpField(seed=0, amplitude=3.0)
+            g = GridSpec((0, 0, 0), (1, 1, 1), 56)
+        else:
+            R = 72
+            field, lo, hi = scenes.resolve(scenes.thin_shell(R) if scene == "thin_shell" else scenes.SCENES[scene], R)
+            g = GridSpec(lo, hi, R)
+        res = contour_slab(field, g, rank=rank, world=world, dist=dist, device=dev, distributed=distributed)
         if rank == 0:
             ref = contour(field, g, device=dev)
             ok = all(np.array_equal(a, b) for a, b in (
@@ -236,22 +241,27 @@ def _slab_worker(rank, world, port, backend, result_path):
                 (res.raw_mesh.triangles, ref.raw_mesh.triangles)))
             ok = ok and res.stats["eval_counts"] == ref.stats["eval_counts"]
             ok = ok and res.stats["repair_added_vertices"] == ref.stats["repair_added_vertices"]
-            np.save(result_path, np.array([int(ok)]))
+            for k in ("n_crossing_edges", "n_crossing_cells", "n_partitions", "point2d_status_counts",
+                      "qef_rank_counts", "split_case_counts", "skipped_boundary_edges"):
+                ok = ok and res.stats.get(k) == ref.stats.get(k)
+            np.save(result_path, np.array([int(ok), int(bool(res.stats.get("distributed_finish")))]))
         else:
             assert res is None
     finally:
         dist.destroy_process_group()
 
 
-def _spawn(world, backend, tmp_path):
+def _spawn(world, backend, tmp_path, scene="mlp", distributed=True):
     import torch.multiprocessing as mp
 
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     out = tmp_path / "ok.npy"
-    mp.spawn(_slab_worker, args=(world, port, backend, str(out)), nprocs=world, join=True)
-    assert np.load(out)[0] == 1
+    mp.spawn(_slab_worker, args=(world, port, backend, str(out), scene, distributed), nprocs=world, join=True)
+    r = np.load(out)
+    assert r[0] == 1
+    return bool(r[1])
 
 
 @pytest.mark.gpu
@@ -264,6 +274,23 @@ def test_gpu_contour_slab_processes(world, backend, tmp_path):
     and the exchange goes over gloo with host staging (each rank's kernels
     run independently; only the host-side collectives synchronise them)."""
     _spawn(world, backend, tmp_path)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scene,world", [("thin_shell", 2), ("thin_shell", 4), ("torus", 3), ("csg_union", 2)])
+def test_gpu_contour_slab_distributed_finish(scene, world, tmp_path):
+    """Closed surfaces: every fan is a disc, so each rank finishes its own
+    piece (seam triangles one rank down, local unused-vertex removal) and
+    the gathered mesh equals contour() bit for bit."""
+    assert _spawn(world, "gloo", tmp_path, scene=scene) is True
+
+
+@pytest.mark.gpu
+def test_gpu_contour_slab_central_finish_when_repair_needed(tmp_path):
+    """The MLP surface has non-manifold fans: the ranks detect it and fall
+    back to the central finish on rank 0, which repairs."""
+    assert _spawn(2, "gloo", tmp_path, scene="mlp") is False
+    assert _spawn(2, "gloo", tmp_path, scene="thin_shell", distributed=False) is False
 
 
 @pytest.mark.gpu
