@@ -505,10 +505,13 @@ def run_gpu_batch(args, rank, world, dist):
 
 def run_gpu_slabs(args, rank, world, dist):
     """N > 1: the workload's grid is split into N z-slabs, one per GPU
-    (paper_2409_13418_b200.slab): total work fixed (strong scaling); the step
-    covers the slab extraction, the count all-gather, the NCCL gather of
-    every slab's vertices/triangles to rank 0 and the finish (unused-vertex
-    removal + repair) there.  Time = max over ranks of CUDA-event time."""
+    (paper_2409_13418_b200.slab): total work fixed (strong scaling).  The
+    step covers the slab extraction and the finish: distributed (seam
+    exchange, per-rank unused-vertex removal, closed-disc check, global ids;
+    the mesh ends distributed over the ranks) when every fan is a disc, else
+    the NCCL gather of every slab to rank 0 and the central finish (unused-
+    vertex removal + repair) there.  e2e adds the gather of the mesh to rank
+    0's host.  Time = max over ranks of CUDA-event time."""
     import torch
 
     from paper_2409_13418_b200 import GridSpec
@@ -543,6 +546,7 @@ def run_gpu_slabs(args, rank, world, dist):
 
     timed(args.warmup, False)
     launches = 0
+    finish_kind = None
     k_ms, k_ev = [], []
     with ClockSampler(device) as clocks:
         dev_ms = []
@@ -550,6 +554,7 @@ def run_gpu_slabs(args, rank, world, dist):
             dev_ms += timed(1, False)
             if last["out"] is not None:  # rank 0: launches summed over ranks, slowest grid pass
                 launches += last["out"]["n_kernel_launches"]
+                finish_kind = "distributed" if last["out"].get("distributed") else "central (rank 0, repair)"
                 kr = np.asarray(last["out"]["rank_label_ms"])
                 k_ms.append(float(kr.max()))
                 k_ev.append(int(last["out"]["rank_label_evals"][int(kr.argmax())]))
@@ -597,7 +602,7 @@ def run_gpu_slabs(args, rank, world, dist):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16+f64" if is_mlp(field) else "f64", "data": "synthetic",
         "config": {"workload": desc, "R": R, "cells": R**3, "parallelism": f"z-slabs x{world}",
-                   "slabs": balanced_slab_ranges(field, grid, world, device),
+                   "slabs": balanced_slab_ranges(field, grid, world, device), "finish": finish_kind,
                    "l2": "flushed (512 MiB write) before every step, outside its CUDA-event pair"},
         "e2e": {"value": R**3 / (e2e_step / 1e3), "unit": "cells/s", "ms_per_step": e2e_step,
                 "api": "paper_2409_13418_b200.slab.contour_slab(field, GridSpec, rank, world) -> TriangleMesh on rank 0",
