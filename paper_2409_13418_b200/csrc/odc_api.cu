@@ -209,9 +209,28 @@ void check_status(odc_ctx* c, DevStatus* dst) {
   readback(c, dst, sizeof(DevStatus));
   DevStatus s;
   std::memcpy(&s, c->h_pinned, sizeof s);
-  if (s.code == ODC_E_ASSERT)
-    throw OdcError{ODC_E_ASSERT, "2D search instance " + std::to_string(s.detail) +
+  if (s.code == ODC_E_ASSERT) {
+    int64_t q = s.detail;
+    std::string where;
+    if (c->nb) {  // batch: the shape whose own extraction raises, and its instance index
+      unsigned long long* pre = need(c->arena.get<unsigned long long>(3 * (c->nb + 1)));
+      unsigned long long* tot = need(c->arena.get<unsigned long long>(3));
+      const unsigned long long t3[3] = {(unsigned long long)c->K, (unsigned long long)c->Q, (unsigned long long)c->C};
+      CUDA_TRY(cudaMemcpyAsync(tot, t3, sizeof t3, cudaMemcpyHostToDevice, c->stream));
+      for (int b = 0; b < c->nb; b++)
+        launch_prefix_at(c->rec, (int64_t)b * c->g.S * c->g.S * c->g.W, c->A, tot, pre + 3 * b, c->stream);
+      std::vector<unsigned long long> h(3 * c->nb);
+      CUDA_TRY(cudaMemcpyAsync(h.data(), pre, sizeof(unsigned long long) * 3 * c->nb, cudaMemcpyDeviceToHost,
+                               c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      int b = 0;
+      while (b + 1 < c->nb && (int64_t)h[3 * (b + 1) + 1] <= q) b++;
+      q -= (int64_t)h[3 * b + 1];
+      where = "shape " + std::to_string(b) + ": ";
+    }
+    throw OdcError{ODC_E_ASSERT, where + "2D search instance " + std::to_string(q) +
                                      ": no corner label differs from the midpoint"};
+  }
   if (s.code) throw OdcError{s.code, "device status " + std::to_string(s.code)};
 }
 
@@ -489,6 +508,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   unsigned long long* totals = need(c->arena.get<unsigned long long>(8));
   CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(DevStats) * nst, s));
   CUDA_TRY(cudaMemsetAsync(dstat, 0, sizeof(DevStatus), s));
+  CUDA_TRY(cudaMemsetAsync(&dstat->detail, 0x7f, sizeof(int64_t), s));  // ~INT64_MAX: min over reporters
 
   int marks = 0;
   auto mark = [&](int i) {

@@ -832,8 +832,12 @@ struct DevStatus {
   int32_t pad;
   int64_t detail;   // offending element
 };
+// The reference raises at the first offending element in index order
+// (numpy finds the first), so the detail is the smallest index reported
+// (detail starts at INT64_MAX, see extract()).
 __device__ __forceinline__ void raise_status(DevStatus* st, int code, int64_t detail) {
-  if (atomicCAS(&st->code, 0, code) == 0) st->detail = detail;
+  atomicCAS(&st->code, 0, code);
+  atomicMin(reinterpret_cast<unsigned long long*>(&st->detail), (unsigned long long)detail);
 }
 
 }  // namespace odc

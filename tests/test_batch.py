@@ -127,3 +127,44 @@ def test_gpu_batch_with_mlp_takes_the_threaded_path():
         s = contour(f, g)
         assert np.array_equal(s.mesh.triangles, r.mesh.triangles)
         assert np.array_equal(s.mesh.vertices, r.mesh.vertices)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("opts", [dict(one_d="midpoint", split="mdc"), dict(one_d="linear-interp", repair=False),
+                                  dict(split="mdc", repair=False)])
+def test_gpu_stacked_batch_option_variants(opts):
+    """The stacked batch under non-default options (1D mode, split mode,
+    repair off) equals contour() of each shape alone."""
+    from paper_2409_13418_b200 import ContourOptions
+
+    options = ContourOptions(**opts)
+    jobs = _stacked_jobs(8, 32, extra=(_EDGE_BOXES,))
+    bat = contour_batch(jobs, options)
+    assert all(r.stats.get("batch_size") == len(jobs) for r in bat)
+    for (f, g), b in zip(jobs, bat):
+        _same(contour(f, g, options), b)
+
+
+@pytest.mark.gpu
+def test_gpu_stacked_batch_smoothed_fields():
+    """Continuous (smoothed) analytic shapes batch together; where a shape's
+    own extraction raises (the reference raises AssertionError at 2D
+    instance 856 for this smoothed sphere with linear-interp 1D points,
+    search.py:248-256 -- checked against the reference in this repo's
+    history), the batch raises the same error naming that shape."""
+    from paper_2409_13418_b200 import ContourOptions, SmoothedOccupancy, SphereField, TorusField
+
+    S = SmoothedOccupancy(SphereField((0.5, 0.45, 0.5), 0.3), 40.0)
+    Tr = SmoothedOccupancy(TorusField((0.5, 0.5, 0.5), 0.25, 0.08), 60.0)
+    g = GridSpec((0, 0, 0), (1, 1, 1), 40)
+    jobs = [(S, g), (Tr, g)]
+    bat = contour_batch(jobs)
+    assert all(r.stats.get("batch_size") == 2 for r in bat)
+    for (f, gg), b in zip(jobs, bat):
+        _same(contour(f, gg), b)
+    lin = ContourOptions(one_d="linear-interp")
+    with pytest.raises(AssertionError, match="2D search instance 856:"):
+        contour(S, g, lin)
+    with pytest.raises(AssertionError, match="shape 1: 2D search instance 856:"):
+        contour_batch([(Tr, g), (S, g)], lin)
+    _same(contour(Tr, g, lin), contour_batch([(Tr, g), (Tr, g)], lin)[1])
