@@ -61,3 +61,56 @@ def test_random_scene_matches_oracle(seed):
     assert np.array_equal(res.mesh.triangles, o["triangles"])
     assert np.array_equal(res.mesh.vertices, o["vertices"])
     assert res.stats["eval_counts"] == o["eval_counts"]
+
+
+def _options(rng, continuous):
+    from paper_2409_13418_b200 import ContourOptions
+    from paper_2409_13418_b200.pipeline import LineBudget, SearchBudget
+
+    one_d = ["midpoint", "linear-interp", "binary-search"][rng.integers(3)]
+    normals = "fd-gradient" if continuous and rng.random() < 0.4 else "two-d-points"
+    budget = SearchBudget(iters_1d=int(rng.integers(4, 16)),
+                          step1=LineBudget(int(rng.integers(1, 6)), int(rng.integers(0, 12)), float(rng.uniform(0.4, 1.0))),
+                          step2=LineBudget(int(rng.integers(1, 5)), int(rng.integers(0, 13)), float(rng.uniform(0.3, 0.9))))
+    return ContourOptions(one_d=one_d, normals=normals, split=["mdc", "ic"][rng.integers(2)],
+                          repair=bool(rng.random() < 0.8), budget=budget)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_scene_and_options_match_oracle(seed):
+    """Random scenes (some smoothed) under random options and search budgets:
+    either both the GPU and the oracle raise the same error, or every label,
+    crossing set and triangle is equal (vertices bit-equal for binary
+    fields; within 1e-9 h for smoothed ones, whose raw values use the device
+    exp)."""
+    from paper_2409_13418_b200 import SmoothedOccupancy
+
+    rng = np.random.default_rng(5000 + seed)
+    field = _field(rng)
+    smooth = rng.random() < 0.4
+    if smooth:  # SmoothedOccupancy needs a signed distance: a primitive
+        field = SmoothedOccupancy(_prim(rng), float(rng.uniform(20, 80)))
+    opts = _options(rng, smooth)
+    R = int(rng.choice([16, 21, 29, 36]))
+    lo, hi = (0.0, 0.0, 0.0), (1.0, 1.0, 1.0)
+    gpu_err = ref_err = None
+    try:
+        res, ctx, st = contour(field, GridSpec(lo, hi, R), opts, keep_intermediates=True, return_context=True)
+    except Exception as e:  # noqa: BLE001
+        gpu_err = e
+    try:
+        o = oracle.contour_oracle(field, lo, hi, R, options=opts)
+    except Exception as e:  # noqa: BLE001
+        ref_err = e
+    if ref_err is not None or gpu_err is not None:
+        assert type(gpu_err) is type(ref_err), (gpu_err, ref_err)
+        assert str(gpu_err) == str(ref_err)
+        return
+    arrs = stage_arrays(ctx, ["labels", "edge_key", "cells"])
+    assert np.array_equal(arrs["labels"], o["labels"])
+    assert np.array_equal(arrs["edge_key"], o["edge_key"])
+    assert np.array_equal(arrs["cells"], o["cells"])
+    assert np.array_equal(res.mesh.triangles, o["triangles"])
+    tol = 1e-9 / R if smooth else 0.0
+    assert np.abs(res.mesh.vertices - o["vertices"]).max(initial=0.0) <= tol
+    assert res.stats["eval_counts"] == o["eval_counts"]
