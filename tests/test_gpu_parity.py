@@ -177,6 +177,32 @@ def test_gpu_mlp_search_budgets(s1, s2):
     compare(res, arrs, o)
 
 
+@pytest.mark.parametrize("opts", [dict(one_d="midpoint"), dict(one_d="linear-interp"),
+                                  dict(normals="fd-gradient"), dict(split="mdc", repair=False),
+                                  dict(one_d="linear-interp", normals="fd-gradient", split="mdc")])
+def test_gpu_mlp_option_variants(opts):
+    """The MLP field (continuous) under the other pipeline modes: linear-interp
+    1D points from the raw grid values (lock-step endpoint evaluations) and
+    fd-gradient normals (6 raw evaluations per edge, pipeline.py:126-151) run
+    through the CTA-pair evaluator with raw output; every stage equals the
+    shared-field oracle or both raise the same error."""
+    options = ContourOptions(**opts)
+    field = MlpField(seed=2, amplitude=3.0)
+    gpu_err = ref_err = None
+    try:
+        res, arrs = gpu_run(field, (0, 0, 0), (1, 1, 1), 36, options)
+    except Exception as e:  # noqa: BLE001
+        gpu_err = e
+    try:
+        o = oracle_run(field, (0, 0, 0), (1, 1, 1), 36, options)
+    except Exception as e:  # noqa: BLE001
+        ref_err = e
+    if gpu_err or ref_err:
+        assert type(gpu_err) is type(ref_err) and str(gpu_err) == str(ref_err), (gpu_err, ref_err)
+        return
+    compare(res, arrs, o)
+
+
 @pytest.mark.parametrize("s1,s2", [((0, 8, 0.8), (3, 12, 0.7)), ((4, 11, 0.8), (0, 7, 0.7))])
 def test_gpu_zero_linear_budget_raises(s1, s2):
     """n_linear == 0 makes the reference's bracket [-inf, nan] (a division by
