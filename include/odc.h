@@ -51,6 +51,7 @@ extern "C" {
 #define ODC_E_CUDA 5     /* CUDA runtime failure                                   */
 #define ODC_E_NOMEM 6    /* device allocation failure                              */
 #define ODC_E_ARG 7      /* bad argument to the C-ABI                              */
+#define ODC_E_CALLBACK 8 /* a callback field's function failed (its own exception)  */
 
 /* field program opcodes (postfix; lowering in paper_2409_13418_b200/fields.py) */
 #define ODC_OP_END 0
@@ -170,6 +171,18 @@ int odc_field_mesh(odc_ctx* ctx, const double* vertices, int64_t n_vertices, con
  * continuous, label = raw > 1/2. */
 int odc_field_voxels(odc_ctx* ctx, const double origin[3], const double spacing[3], const double* values, int64_t nx,
                      int64_t ny, int64_t nz, odc_field** out);
+/* Any other occupancy function (the reference's field duck type: an object
+ * with eval_raw, fields.py:51-61): the pipeline runs on the device and calls
+ * fn(user, points, n, labels, raw, stream) for every batch of query points
+ * it would pass to eval_raw -- the grid (in chunks), the 1D bisection steps,
+ * the face probes, the 2D search steps.  points: device (n,3) f64, complete
+ * when fn is called; fn writes labels (device u8, raw > iso) and, when raw is
+ * not NULL, raw (device f64), complete when it returns.  Return 0 on
+ * success; non-zero aborts the extraction with ODC_E_CALLBACK.  stream is
+ * the context's cudaStream_t (fn may enqueue on it and synchronise). */
+typedef int (*odc_eval_fn)(void* user, const double* points, int64_t n, uint8_t* labels, double* raw, void* stream);
+int odc_field_callback(odc_ctx* ctx, odc_eval_fn fn, void* user, int32_t continuous, double iso_level,
+                       odc_field** out);
 void odc_field_free(odc_ctx* ctx, odc_field* f);
 
 void odc_default_options(odc_options* o);

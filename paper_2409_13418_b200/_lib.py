@@ -12,7 +12,10 @@ import numpy as np
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libodc.so"
 
-ODC_OK, ODC_E_ASSERT, ODC_E_CONTRACT, ODC_E_CONFIG, ODC_E_VALUE, ODC_E_CUDA, ODC_E_NOMEM, ODC_E_ARG = range(8)
+ODC_OK, ODC_E_ASSERT, ODC_E_CONTRACT, ODC_E_CONFIG, ODC_E_VALUE, ODC_E_CUDA, ODC_E_NOMEM, ODC_E_ARG, ODC_E_CALLBACK = range(9)
+# int fn(void* user, const double* points, int64_t n, uint8_t* labels, double* raw, void* stream)
+EVAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p)
 ODC_N_CAT = 6
 CATEGORIES = ("labels", "search_1d", "probe_face_center", "probe_face_midpoint", "search_2d", "fd_gradient")
 
@@ -90,7 +93,7 @@ EXPORTS = (
     "odc_validate_manifold", "odc_validate_copy", "odc_count_self_intersections", "odc_self_intersection_pairs",
     "odc_mesh_distance", "odc_triangle_areas", "odc_field_mesh", "odc_field_voxels", "odc_eigh3",
     "odc_eigh3_host", "odc_eval_mlp_dot", "odc_extract_batch", "odc_batch_layout", "odc_copy_batch_meshes",
-    "odc_slab_seam", "odc_slab_local_finish", "odc_slab_top_ids", "odc_slab_final",
+    "odc_slab_seam", "odc_slab_local_finish", "odc_slab_top_ids", "odc_slab_final", "odc_field_callback",
 )
 
 _lib = None
@@ -121,6 +124,7 @@ def load():
         L.odc_field_mesh.argtypes = [vp, vp, i64, vp, i64, P(vp)]
         L.odc_field_voxels.argtypes = [vp, P(dbl), P(dbl), vp, i64, i64, i64, P(vp)]
         L.odc_field_free.argtypes = [vp, vp]
+        L.odc_field_callback.argtypes = [vp, EVAL_FN, vp, i32, dbl, P(vp)]
         L.odc_field_free.restype = None
         L.odc_default_options.argtypes = [P(Options)]
         L.odc_default_options.restype = None

@@ -58,7 +58,7 @@ def marching_cubes(field, grid, mode="binary", counter=None, *, device=0):
     with DeviceField(ctx, field) as dfield:
         rc = L.odc_extract(ctx.handle, dfield.handle, lo, hi, R, ctypes.byref(o), ctypes.byref(st))
         if rc != _lib.ODC_OK:
-            _raise(rc, ctx)
+            _raise(rc, ctx, dfield)
     bi = int(st.boundary_inside_vertices)
     stats["boundary_inside_vertices"] = bi
     if bi:

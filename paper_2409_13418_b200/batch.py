@@ -24,7 +24,7 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 
 from . import _lib
-from .fields import field_continuous, is_mesh_winding, is_mlp, is_voxels
+from .fields import LoweringError, field_continuous, is_mesh_winding, is_mlp, is_voxels, lower_program
 from .mesh import TriangleMesh
 from .pipeline import (ContourOptions, ContourResult, DeviceField, EvalCounter, _grid_args, _raise, contour,
                        make_options, record_counts, stats_dict)
@@ -62,6 +62,10 @@ def batchable(jobs, options):
     cont = None
     for f, g in jobs:
         if int(g.resolution) != R or is_mlp(f) or is_mesh_winding(f) or is_voxels(f):
+            return False
+        try:
+            lower_program(f)  # a device program (callback fields run through the threaded path)
+        except LoweringError:
             return False
         c = bool(field_continuous(f))
         if cont is not None and c != cont:

@@ -104,6 +104,9 @@ struct odc_field {
   void* wind_buf = nullptr;
   // voxel field (kind 3)
   VoxDev vox{};
+  // host callback field (kind 4): the caller's own occupancy function
+  odc_eval_fn cb = nullptr;
+  void* cb_user = nullptr;
 };
 
 struct odc_ctx {
@@ -249,6 +252,16 @@ void run_mlp(odc_ctx* c, const odc_field* f, const PointSrc& src, int64_t n, uin
 }
 
 // Evaluate labels (and optionally raw) of n points through the field.
+// A callback field: the device points are complete when the caller's
+// function runs (stream synchronised), and its labels/raw are complete when
+// it returns (its contract), so the pipeline's ordering holds.
+void eval_callback(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* lab, double* raw) {
+  if (n == 0) return;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const int rc = f->cb(f->cb_user, pts, n, lab, raw, (void*)c->stream);
+  if (rc) throw OdcError{ODC_E_CALLBACK, "the field's evaluation callback failed (" + std::to_string(rc) + ")"};
+}
+
 void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* lab, double* raw,
                  const int64_t* n_dev = nullptr, const int32_t* out_map = nullptr) {
   if (n == 0) return;
@@ -264,6 +277,9 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
   } else if (f->kind == 3) {
     PointSrc src{pts, GridP{}, 0};
     voxel_eval(f->vox, src, n, lab, raw, c->stream);
+  } else if (f->kind == 4) {
+    eval_callback(c, f, pts, n, lab, raw);
+    return;
   } else {
     PointSrc src{pts, GridP{}, 0};
     src.n_dev = n_dev;
@@ -529,6 +545,15 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       winding_eval(f->wind, src, g.nz * g.S2, bytes, nullptr, c->d_fail, s);
     } else if (f->kind == 3) {
       voxel_eval(f->vox, src, g.nz * g.S2, bytes, nullptr, s);
+    } else if (f->kind == 4) {  // the grid's points in flat vertex order, a few million at a time
+      const int64_t nall = g.nz * g.S2, chunk = std::min<int64_t>(nall, 1 << 22);
+      double* gp = need(c->arena.get<double>(3 * chunk));
+      for (int64_t b0 = 0; b0 < nall; b0 += chunk) {
+        const int64_t nb = std::min(chunk, nall - b0);
+        launch_grid_points(g, g.z0 * g.S2 + b0, nb, gp, s);
+        check_launch(c);
+        eval_callback(c, f, gp, nb, bytes + b0, nullptr);
+      }
     } else {
       run_mlp(c, f, src, g.nz * g.S2, bytes, nullptr, s);
     }
@@ -1360,6 +1385,21 @@ int odc_field_voxels(odc_ctx* c, const double origin[3], const double spacing[3]
     f->vox.origin[a] = origin[a];
     f->vox.spacing[a] = spacing[a];
   }
+  *out = f;
+  return ODC_OK;
+}
+
+int odc_field_callback(odc_ctx* c, odc_eval_fn fn, void* user, int32_t continuous, double iso, odc_field** out) {
+  if (!c || !fn || !out) return ODC_E_ARG;
+  odc_field* f = new (std::nothrow) odc_field();
+  if (!f) return ODC_E_NOMEM;
+  f->kind = 4;
+  f->cb = fn;
+  f->cb_user = user;
+  f->continuous = continuous;
+  f->iso = iso;
+  f->fp.kind = 4;
+  f->fp.iso = iso;
   *out = f;
   return ODC_OK;
 }

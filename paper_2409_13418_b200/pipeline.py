@@ -17,7 +17,8 @@ from dataclasses import dataclass, field as dc_field
 import numpy as np
 
 from . import _lib
-from .fields import SurfaceCoincidenceError, field_continuous, is_mesh_winding, is_mlp, is_voxels, lower_program
+from .fields import (LoweringError, SurfaceCoincidenceError, field_continuous, is_mesh_winding, is_mlp, is_voxels,
+                     lower_program)
 from .mesh import GridSpec, TriangleMesh
 
 ONE_D_MODES = ("midpoint", "linear-interp", "binary-search")
@@ -121,20 +122,71 @@ _ERRORS = {
 }
 
 
-def _raise(rc, ctx):
+def _raise(rc, ctx, dfield=None):
+    if dfield is not None and dfield.error is not None:  # the field's own exception (callback fields)
+        err, dfield.error = dfield.error, None
+        raise err
     msg = _lib.load().odc_last_error(ctx.handle).decode()
     if rc == _lib.ODC_E_VALUE and "off the surface" in msg:
         raise SurfaceCoincidenceError(msg)
     raise _ERRORS.get(rc, RuntimeError)(msg)
 
 
+class _CudaView:
+    """Zero-copy view of a device buffer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _make_callback(dfield, field):
+    """The evaluation callback of a field the device cannot run itself (the
+    reference's duck type: an object with ``eval_raw``, fields.py:51-61).
+    The pipeline still runs on the device; for every batch of query points
+    it would pass to eval_raw it calls the field: ``eval_raw_torch(points)``
+    (a CUDA tensor in, a tensor out: the points never leave the device) when
+    the field has one, else ``eval_raw`` on a host copy of the points, as
+    the reference does.  label = raw > iso_level (fields.py:35-48).  An
+    exception inside the field is kept and re-raised by the caller."""
+    import torch
+
+    iso = float(getattr(field, "iso_level", 0.5))
+    torch_fn = getattr(field, "eval_raw_torch", None)
+    dev = torch.device("cuda", dfield.ctx.device)
+
+    def cb(user, pts_ptr, n, lab_ptr, raw_ptr, stream):
+        try:
+            with torch.cuda.device(dev):
+                pts = torch.as_tensor(_CudaView(pts_ptr, (n, 3), "<f8"), device=dev)
+                if torch_fn is not None:
+                    raw = torch.as_tensor(torch_fn(pts), device=dev).to(torch.float64).reshape(-1)
+                else:
+                    host = np.asarray(field.eval_raw(pts.cpu().numpy()), dtype=np.float64).reshape(-1)
+                    raw = torch.from_numpy(host).to(dev)
+                if raw.shape[0] != n:
+                    raise ValueError(f"eval_raw returned {raw.shape[0]} values for {n} points")
+                torch.as_tensor(_CudaView(lab_ptr, (n,), "|u1"), device=dev).copy_((raw > iso).to(torch.uint8))
+                if raw_ptr:
+                    torch.as_tensor(_CudaView(raw_ptr, (n,), "<f8"), device=dev).copy_(raw)
+                torch.cuda.synchronize(dev)
+            return 0
+        except BaseException as e:  # noqa: BLE001 -- re-raised by _raise via dfield.error
+            dfield.error = e
+            return 1
+
+    return cb
+
+
 class DeviceField:
-    """A field uploaded to one libodc context (program or MLP weights)."""
+    """A field uploaded to one libodc context (program, MLP weights, mesh,
+    voxels) or, for any other occupancy function, a callback field."""
 
     def __init__(self, ctx, field):
         L = _lib.load()
         self.ctx = ctx
         self.handle = ctypes.c_void_p()
+        self.error = None
         self.continuous = field_continuous(field)
         if is_mlp(field):
             keep = [
@@ -163,11 +215,21 @@ class DeviceField:
             rc = L.odc_field_mesh(ctx.handle, v.ctypes.data if len(v) else None, len(v),
                                   t.ctypes.data if len(t) else None, len(t), ctypes.byref(self.handle))
         else:
-            prog = lower_program(field)
-            nodes = np.ascontiguousarray(prog)
-            rc = L.odc_field_analytic(ctx.handle, nodes.ctypes.data_as(ctypes.POINTER(_lib.Node)), len(nodes),
-                                      int(self.continuous), float(getattr(field, "iso_level", 0.5)),
-                                      ctypes.byref(self.handle))
+            try:
+                prog = lower_program(field)
+            except LoweringError:
+                if not (hasattr(field, "eval_raw") or hasattr(field, "eval_raw_torch")):
+                    raise
+                prog = None
+            if prog is None:  # any other occupancy function: a callback field
+                self._fn = _lib.EVAL_FN(_make_callback(self, field))
+                rc = L.odc_field_callback(ctx.handle, self._fn, None, int(self.continuous),
+                                          float(getattr(field, "iso_level", 0.5)), ctypes.byref(self.handle))
+            else:
+                nodes = np.ascontiguousarray(prog)
+                rc = L.odc_field_analytic(ctx.handle, nodes.ctypes.data_as(ctypes.POINTER(_lib.Node)), len(nodes),
+                                          int(self.continuous), float(getattr(field, "iso_level", 0.5)),
+                                          ctypes.byref(self.handle))
         if rc != _lib.ODC_OK:
             _raise(rc, ctx)
 
@@ -318,7 +380,7 @@ def contour(field, grid, options=None, counter=None, *, device=0, provenance=Tru
     with DeviceField(ctx, field) as dfield:
         rc = L.odc_extract(ctx.handle, dfield.handle, lo, hi, R, ctypes.byref(o), ctypes.byref(st))
         if rc != _lib.ODC_OK:
-            _raise(rc, ctx)
+            _raise(rc, ctx, dfield)
     stats = stats_dict(st, options)
     if st.n_crossing_edges == 0:
         empty = TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64))
@@ -362,7 +424,7 @@ def eval_raw(field, points, device=0):
     with DeviceField(ctx, field) as f:
         rc = _lib.load().odc_eval_raw(ctx.handle, f.handle, pts.ctypes.data, len(pts), out.ctypes.data)
         if rc != _lib.ODC_OK:
-            _raise(rc, ctx)
+            _raise(rc, ctx, f)
     return out
 
 
@@ -376,7 +438,7 @@ def eval_labels(field, points, device=0):
     with DeviceField(ctx, field) as f:
         rc = _lib.load().odc_eval_labels(ctx.handle, f.handle, pts.ctypes.data, len(pts), out.ctypes.data)
         if rc != _lib.ODC_OK:
-            _raise(rc, ctx)
+            _raise(rc, ctx, f)
     return out[0] if squeeze else out
 
 
@@ -396,7 +458,7 @@ class SharedField:
         out = np.empty(len(pts))
         rc = _lib.load().odc_eval_raw(self.ctx.handle, self.dev.handle, pts.ctypes.data, len(pts), out.ctypes.data)
         if rc != _lib.ODC_OK:
-            _raise(rc, self.ctx)
+            _raise(rc, self.ctx, self.dev)
         return out
 
     def close(self):

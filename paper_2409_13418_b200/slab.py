@@ -198,7 +198,7 @@ def extract_piece(field, grid, options, c0, c1, device=0, dfield=None):
         rc = L.odc_extract_slab(ctx.handle, df.handle, lo, hi, R, ctypes.byref(o), int(c0), int(c1), ctypes.byref(st),
                                 ctypes.byref(info))
         if rc != _lib.ODC_OK:
-            _raise(rc, ctx)
+            _raise(rc, ctx, df)
     dev = torch.device("cuda", device)
     P, NF, T = info.n_partitions, info.n_fans, info.n_triangles
     piece = SlabPiece(
