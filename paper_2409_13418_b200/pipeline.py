@@ -132,6 +132,10 @@ def _raise(rc, ctx, dfield=None):
     raise _ERRORS.get(rc, RuntimeError)(msg)
 
 
+_DEVICE_KINDS = {"SphereField", "BoxField", "TorusField", "PlaneField", "CsgField", "SmoothedOccupancy",
+                 "MlpField", "VoxelField", "MeshWindingField"}
+
+
 class _CudaView:
     """Zero-copy view of a device buffer (__cuda_array_interface__)."""
 
@@ -218,7 +222,10 @@ class DeviceField:
             try:
                 prog = lower_program(field)
             except LoweringError:
-                if not (hasattr(field, "eval_raw") or hasattr(field, "eval_raw_torch")):
+                # the reference's own field types always lower (a failure there is
+                # a bug to surface, never a silent switch to host evaluation)
+                if type(field).__name__ in _DEVICE_KINDS or not (hasattr(field, "eval_raw")
+                                                                 or hasattr(field, "eval_raw_torch")):
                     raise
                 prog = None
             if prog is None:  # any other occupancy function: a callback field

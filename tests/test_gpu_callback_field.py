@@ -115,3 +115,14 @@ def test_user_field_wrong_length_raises():
 
     with pytest.raises(ValueError, match="values for"):
         contour(Short(), GridSpec((0, 0, 0), (1, 1, 1), 16))
+
+
+def test_reference_field_types_never_become_callbacks():
+    """A CsgField with a child the device cannot lower raises LoweringError
+    rather than silently evaluating on the host."""
+    from paper_2409_13418_b200 import CsgField, SphereField
+    from paper_2409_13418_b200.fields import LoweringError
+
+    f = CsgField("union", [SphereField((0.5, 0.5, 0.5), 0.2), Gyroid()])
+    with pytest.raises(LoweringError):
+        contour(f, GridSpec((0, 0, 0), (1, 1, 1), 16))
