@@ -494,10 +494,45 @@ __device__ __forceinline__ double prim_sd_p(int op, const double (&q)[16], const
 // SEL: per-primitive parameter loads (prim_inside_p) -- faster when the
 // FieldP sits in global memory (batches); a kernel-parameter FieldP keeps
 // the copy-all form, which its uniform constant loads serve better.
-template <bool SEL = false>
+// Evaluation modes: 0 kernel-parameter FieldP (copy its parameters), 1
+// per-primitive loads (FieldP in global memory: batches), and kernels
+// specialised for the commonest fast paths (the host picks them from the
+// FieldP): one sphere / box / torus, a CSG pair of spheres.
+enum { EV_PARAM = 0, EV_SEL = 1, EV_SPHERE = 2, EV_BOX = 3, EV_TORUS = 4, EV_SPHERE2 = 5 };
+__host__ __device__ inline int ev_mode_of(const FieldP& f) {
+  if (f.fast == 1 && f.fop[0] == ODC_OP_SPHERE_SD) return EV_SPHERE;
+  if (f.fast == 1 && f.fop[0] == ODC_OP_BOX_SD) return EV_BOX;
+  if (f.fast == 1 && f.fop[0] == ODC_OP_TORUS_SD) return EV_TORUS;
+  if (f.fast == 3 && f.fop[0] == ODC_OP_SPHERE_SD && f.fop[1] == ODC_OP_SPHERE_SD) return EV_SPHERE2;
+  return EV_PARAM;
+}
+template <int SEL = EV_PARAM>
 __device__ __forceinline__ double field_raw_t(const FieldP& f, const double p[3]) {
+  if constexpr (SEL == EV_SPHERE) {
+    double c[16];
+    load_params<4>(f.fq[0], c);
+    return sphere_inside(c, p) ? 1.0 : 0.0;
+  } else if constexpr (SEL == EV_BOX) {
+    double c[16];
+    load_params<16>(f.fq[0], c);
+    return prim_inside(ODC_OP_BOX_SD, c, p) ? 1.0 : 0.0;
+  } else if constexpr (SEL == EV_TORUS) {
+    double c[16];
+    load_params<5>(f.fq[0], c);
+    return prim_sd(ODC_OP_TORUS_SD, c, p) < 0.0 ? 1.0 : 0.0;
+  } else if constexpr (SEL == EV_SPHERE2) {
+    double c0[16], c1[16];
+    load_params<4>(f.fq[0], c0);
+    load_params<4>(f.fq[1], c1);
+    const double a = sphere_inside(c0, p) ? 1.0 : 0.0;
+    double b = sphere_inside(c1, p) ? 1.0 : 0.0;
+    if (f.fop[2] == ODC_OP_RAW_MAX) return (a >= b) ? a : b;
+    if (f.fop[2] == ODC_OP_RAW_MIN) return (a <= b) ? a : b;
+    b = __dsub_rn(1.0, b);
+    return (a <= b) ? a : b;
+  }
   if (f.fast) {
-    if constexpr (SEL) {
+    if constexpr (SEL == EV_SEL) {
       if (f.fast == 1) return prim_inside_p(f.fop[0], f.fq[0], p) ? 1.0 : 0.0;
       if (f.fast == 2) return smooth_raw(f.fk, prim_sd_p(f.fop[0], f.fq[0], p));
       const double a = prim_inside_p(f.fop[0], f.fq[0], p) ? 1.0 : 0.0;
@@ -543,8 +578,8 @@ __device__ __forceinline__ double field_raw_t(const FieldP& f, const double p[3]
   }
   return field_raw_prog(f.nodes, f.n_nodes, p);
 }
-__device__ __forceinline__ double field_raw(const FieldP& f, const double p[3]) { return field_raw_t<false>(f, p); }
-template <bool SEL = false>
+__device__ __forceinline__ double field_raw(const FieldP& f, const double p[3]) { return field_raw_t<EV_PARAM>(f, p); }
+template <int SEL = EV_PARAM>
 __device__ __forceinline__ uint32_t field_label_t(const FieldP& f, const double p[3]) {
   return field_raw_t<SEL>(f, p) > f.iso ? 1u : 0u;
 }

@@ -75,7 +75,7 @@ __device__ __forceinline__ uint32_t bits_below(int64_t limit, int64_t wx) {
 // around its word's (up to) 32 vertices (field_label_ball); the warp then
 // evaluates every vertex of each undecided word, 32 lanes per word.  Far
 // from the surface one evaluation decides 32 labels.
-template <bool B>
+template <bool B, int EV>
 __global__ void __launch_bounds__(256, 4) k_labels_analytic(GridP g, FieldP f, uint32_t* __restrict__ L) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256, 4) k_labels_analytic(GridP g, FieldP f, u
       const int b = localize<B>(gl, zj);
       const double p[3] = {gpos(gl, 0, x), gpos(gl, 1, yj), gpos(gl, 2, zj)};
       if constexpr (B) lab = field_label_t<true>(f.batch[b], p);
-      else lab = field_label(f, p);
+      else lab = field_label_t<EV>(f, p);
     }
     const uint32_t word = __ballot_sync(0xffffffffu, lab);
     if (lane == 0) L[wj] = word;
@@ -115,8 +115,18 @@ __global__ void __launch_bounds__(256, 4) k_labels_analytic(GridP g, FieldP f, u
 
 void launch_labels_analytic(const GridP& g, const FieldP& f, uint32_t* L, cudaStream_t s) {
   if (!g.NW) return;
-  if (g.nb) k_labels_analytic<true><<<grid_for(g.NW, 256), 256, 0, s>>>(g, f, L);
-  else k_labels_analytic<false><<<grid_for(g.NW, 256), 256, 0, s>>>(g, f, L);
+  const unsigned grid = grid_for(g.NW, 256);
+  if (g.nb) {
+    k_labels_analytic<true, EV_SEL><<<grid, 256, 0, s>>>(g, f, L);
+    return;
+  }
+  switch (ev_mode_of(f)) {  // the per-vertex evaluations of undecided words, specialised
+    case EV_SPHERE: k_labels_analytic<false, EV_SPHERE><<<grid, 256, 0, s>>>(g, f, L); break;
+    case EV_BOX: k_labels_analytic<false, EV_BOX><<<grid, 256, 0, s>>>(g, f, L); break;
+    case EV_TORUS: k_labels_analytic<false, EV_TORUS><<<grid, 256, 0, s>>>(g, f, L); break;
+    case EV_SPHERE2: k_labels_analytic<false, EV_SPHERE2><<<grid, 256, 0, s>>>(g, f, L); break;
+    default: k_labels_analytic<false, EV_PARAM><<<grid, 256, 0, s>>>(g, f, L); break;
+  }
 }
 
 // one warp per label row: lane j of word w reads byte 32 w + j (coalesced),
@@ -667,7 +677,7 @@ __device__ __forceinline__ double linear_t(double ri, double ro, double iso) {
   return t > 1.0 ? 1.0 : t;
 }
 
-template <bool SEL>
+template <int SEL>
 __device__ __forceinline__ void search1d_one(const GridP& g, const FieldP& f, const OptP& o,
                                              const uint32_t* __restrict__ L, const int64_t* __restrict__ edge_key,
                                              int64_t k, double* __restrict__ tout, double* __restrict__ pos,
@@ -703,7 +713,7 @@ __device__ __forceinline__ void search1d_one(const GridP& g, const FieldP& f, co
   if (vin_out) vin_out[k] = e.vin;
 }
 
-template <bool B>
+template <bool B, int EV>
 __global__ void __launch_bounds__(128) k_search1d_analytic(GridP g, FieldP f, OptP o, const uint32_t* __restrict__ L,
                                                            const int64_t* __restrict__ edge_key, int64_t K,
                                                            double* __restrict__ tout, double* __restrict__ pos,
@@ -713,9 +723,9 @@ __global__ void __launch_bounds__(128) k_search1d_analytic(GridP g, FieldP f, Op
   if constexpr (B) {
     GridP gl = g;
     const int sb = localize<B>(gl, idiv(edge_key[k] / 3, g.S2));
-    search1d_one<true>(gl, f.batch[sb], o, L, edge_key, k, tout, pos, vin_out);
+    search1d_one<EV_SEL>(gl, f.batch[sb], o, L, edge_key, k, tout, pos, vin_out);
   } else {
-    search1d_one<false>(g, f, o, L, edge_key, k, tout, pos, vin_out);
+    search1d_one<EV>(g, f, o, L, edge_key, k, tout, pos, vin_out);
   }
 }
 
@@ -723,8 +733,20 @@ void launch_search1d_analytic(const GridP& g, const FieldP& f, const OptP& o, co
                               const int64_t* edge_key, int64_t K, double* t, double* pos, int64_t* v_in,
                               cudaStream_t s) {
   if (!K) return;
-  if (g.nb) k_search1d_analytic<true><<<grid_for(K, 128), 128, 0, s>>>(g, f, o, L, edge_key, K, t, pos, v_in);
-  else k_search1d_analytic<false><<<grid_for(K, 128), 128, 0, s>>>(g, f, o, L, edge_key, K, t, pos, v_in);
+  const unsigned grid = grid_for(K, 128);
+#define S1A(BB, EVV) k_search1d_analytic<BB, EVV><<<grid, 128, 0, s>>>(g, f, o, L, edge_key, K, t, pos, v_in)
+  if (g.nb) {
+    S1A(true, EV_SEL);
+    return;
+  }
+  switch (ev_mode_of(f)) {
+    case EV_SPHERE: S1A(false, EV_SPHERE); break;
+    case EV_BOX: S1A(false, EV_BOX); break;
+    case EV_TORUS: S1A(false, EV_TORUS); break;
+    case EV_SPHERE2: S1A(false, EV_SPHERE2); break;
+    default: S1A(false, EV_PARAM); break;
+  }
+#undef S1A
 }
 
 // lock-step form (batched fields): lo/hi state, points, update, finish
@@ -971,7 +993,7 @@ __device__ __forceinline__ void finish2d(const Inst2D& I, const Chord& ch, doubl
 // same per-element order as the lock-step batches; skipping the samples
 // after the first flip of a linear scan does not change any result, and the
 // eval accounting reports the reference's logical counts.
-template <bool SEL>
+template <int SEL>
 __device__ __forceinline__ void line_binary(const FieldP& f, const Inst2D& I, const double o2[2], const double d2[2],
                                             uint32_t ref, double max_range, int nlin, int nbin, double& a_out,
                                             bool& found) {
@@ -998,7 +1020,7 @@ __device__ __forceinline__ void line_binary(const FieldP& f, const Inst2D& I, co
   a_out = a;
 }
 
-template <bool B>
+template <bool B, int EV>
 __device__ __forceinline__ void search2d_one(const GridP& g, const FieldP& f, const OptP& o,
                                              const uint32_t* __restrict__ L, const RecView& rec,
                                              const int64_t* __restrict__ inst_key, int64_t q,
@@ -1015,7 +1037,7 @@ __device__ __forceinline__ void search2d_one(const GridP& g, const FieldP& f, co
   const Chord ch = make_chord(I);
   double pm[3];
   lift(I, ch.mid[0], ch.mid[1], pm);
-  const uint32_t mid_label = field_label_t<B>(f, pm);
+  const uint32_t mid_label = field_label_t<EV>(f, pm);
   double ray[2];
   if (!ray_direction(I, ch, mid_label, ray)) {
     raise_status(dst, ODC_E_ASSERT, q);
@@ -1023,14 +1045,14 @@ __device__ __forceinline__ void search2d_one(const GridP& g, const FieldP& f, co
   }
   double dist_r;
   bool found_r;
-  line_binary<B>(f, I, ch.mid, ray, mid_label, o.s1_range * I.hmin, o.s1_lin, o.s1_bin, dist_r, found_r);
+  line_binary<EV>(f, I, ch.mid, ray, mid_label, o.s1_range * I.hmin, o.s1_lin, o.s1_bin, dist_r, found_r);
   const double q2[2] = {ch.mid[0] + dist_r * ray[0], ch.mid[1] + dist_r * ray[1]};
   const double r2 = o.s2_range * I.hmin;
   const double dneg[2] = {-ch.dl[0], -ch.dl[1]};
   double da, db;
   bool fa, fb;
-  line_binary<B>(f, I, q2, dneg, mid_label, r2, o.s2_lin, o.s2_bin, da, fa);
-  line_binary<B>(f, I, q2, ch.dl, mid_label, r2, o.s2_lin, o.s2_bin, db, fb);
+  line_binary<EV>(f, I, q2, dneg, mid_label, r2, o.s2_lin, o.s2_bin, da, fa);
+  line_binary<EV>(f, I, q2, ch.dl, mid_label, r2, o.s2_lin, o.s2_bin, db, fb);
   const double qa[2] = {q2[0] + da * dneg[0], q2[1] + da * dneg[1]};
   const double qb[2] = {q2[0] + db * ch.dl[0], q2[1] + db * ch.dl[1]};
   double p2d[2];
@@ -1050,7 +1072,7 @@ __device__ __forceinline__ void search2d_one(const GridP& g, const FieldP& f, co
   warp_count4<B>(st->status, status, q >= st_lo && q < st_hi);
 }
 
-template <bool B>
+template <bool B, int EV>
 __global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, OptP o, const uint32_t* __restrict__ L,
                                                            RecView rec,
                                                            const int64_t* __restrict__ inst_key, int64_t Q,
@@ -1062,9 +1084,10 @@ __global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, Op
   if constexpr (B) {
     GridP gl = g;
     const int sb = localize<B>(gl, idiv((inst_key[q] >> 1) / 3, g.S2));
-    search2d_one<B>(gl, f.batch[sb], o, L, rec, inst_key, q, pos1d, out, inst_edges, st + sb, dst, st_lo, st_hi);
+    search2d_one<B, EV_SEL>(gl, f.batch[sb], o, L, rec, inst_key, q, pos1d, out, inst_edges, st + sb, dst, st_lo,
+                            st_hi);
   } else {
-    search2d_one<B>(g, f, o, L, rec, inst_key, q, pos1d, out, inst_edges, st, dst, st_lo, st_hi);
+    search2d_one<B, EV>(g, f, o, L, rec, inst_key, q, pos1d, out, inst_edges, st, dst, st_lo, st_hi);
   }
 }
 
@@ -1073,12 +1096,21 @@ void launch_search2d_analytic(const GridP& g, const FieldP& f, const OptP& o, co
                               Stage2D out, int64_t* inst_edges, DevStats* st, DevStatus* dst, int64_t st_lo,
                               int64_t st_hi, cudaStream_t s) {
   if (!Q) return;
-  if (g.nb)
-    k_search2d_analytic<true><<<grid_for(Q, 128), 128, 0, s>>>(g, f, o, L, rec, inst_key, Q, pos1d, out, inst_edges,
-                                                               st, dst, st_lo, st_hi);
-  else
-    k_search2d_analytic<false><<<grid_for(Q, 128), 128, 0, s>>>(g, f, o, L, rec, inst_key, Q, pos1d, out, inst_edges,
-                                                                st, dst, st_lo, st_hi);
+  const dim3 grid(grid_for(Q, 128));
+#define S2A(BB, EVV) k_search2d_analytic<BB, EVV><<<grid, 128, 0, s>>>(g, f, o, L, rec, inst_key, Q, pos1d, out, \
+                                                                      inst_edges, st, dst, st_lo, st_hi)
+  if (g.nb) {
+    S2A(true, EV_SEL);
+    return;
+  }
+  switch (ev_mode_of(f)) {  // kernels specialised for the commonest fast paths
+    case EV_SPHERE: S2A(false, EV_SPHERE); break;
+    case EV_BOX: S2A(false, EV_BOX); break;
+    case EV_TORUS: S2A(false, EV_TORUS); break;
+    case EV_SPHERE2: S2A(false, EV_SPHERE2); break;
+    default: S2A(false, EV_PARAM); break;
+  }
+#undef S2A
 }
 
 // ---- lock-step 2D search (batched fields) --------------------------------
