@@ -498,12 +498,20 @@ __device__ __forceinline__ double prim_sd_p(int op, const double (&q)[16], const
 // per-primitive loads (FieldP in global memory: batches), and kernels
 // specialised for the commonest fast paths (the host picks them from the
 // FieldP): one sphere / box / torus, a CSG pair of spheres.
-enum { EV_PARAM = 0, EV_SEL = 1, EV_SPHERE = 2, EV_BOX = 3, EV_TORUS = 4, EV_SPHERE2 = 5 };
+// EV_BOX2F: a CSG pair of boxes in the same frame (bitwise-equal centre and
+// rotation, e.g. a hollow box): the rotated local point is computed once.
+enum { EV_PARAM = 0, EV_SEL = 1, EV_SPHERE = 2, EV_BOX = 3, EV_TORUS = 4, EV_SPHERE2 = 5, EV_BOX2F = 6 };
 __host__ __device__ inline int ev_mode_of(const FieldP& f) {
   if (f.fast == 1 && f.fop[0] == ODC_OP_SPHERE_SD) return EV_SPHERE;
   if (f.fast == 1 && f.fop[0] == ODC_OP_BOX_SD) return EV_BOX;
   if (f.fast == 1 && f.fop[0] == ODC_OP_TORUS_SD) return EV_TORUS;
   if (f.fast == 3 && f.fop[0] == ODC_OP_SPHERE_SD && f.fop[1] == ODC_OP_SPHERE_SD) return EV_SPHERE2;
+  if (f.fast == 3 && f.fop[0] == ODC_OP_BOX_SD && f.fop[1] == ODC_OP_BOX_SD) {
+    bool same = true;
+    for (int i = 0; i < 16; i++)
+      if (i < 3 || i > 5) same = same && f.fq[0][i] == f.fq[1][i] && ((f.fq[0][i] == 0.0) == (f.fq[1][i] == 0.0));
+    if (same) return EV_BOX2F;
+  }
   return EV_PARAM;
 }
 template <int SEL = EV_PARAM>
@@ -520,6 +528,27 @@ __device__ __forceinline__ double field_raw_t(const FieldP& f, const double p[3]
     double c[16];
     load_params<5>(f.fq[0], c);
     return prim_sd(ODC_OP_TORUS_SD, c, p) < 0.0 ? 1.0 : 0.0;
+  } else if constexpr (SEL == EV_BOX2F) {
+    // box inside test of prim_inside, the shared rotation applied once
+    double l[3] = {__dsub_rn(p[0], f.fq[0][0]), __dsub_rn(p[1], f.fq[0][1]), __dsub_rn(p[2], f.fq[0][2])};
+    if (f.fq[0][6] != 0.0) {
+      double R[9], o[3];
+      for (int j = 0; j < 9; j++) R[j] = f.fq[0][7 + j];
+      rot_rows(l, R, o);
+      l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
+    }
+    bool ia = true, ib = true;
+    for (int a = 0; a < 3; a++) {
+      const double al = fabs(l[a]);
+      ia &= __dsub_rn(al, f.fq[0][3 + a]) < 0.0;
+      ib &= __dsub_rn(al, f.fq[1][3 + a]) < 0.0;
+    }
+    const double A = ia ? 1.0 : 0.0;
+    double B = ib ? 1.0 : 0.0;
+    if (f.fop[2] == ODC_OP_RAW_MAX) return (A >= B) ? A : B;
+    if (f.fop[2] == ODC_OP_RAW_MIN) return (A <= B) ? A : B;
+    B = __dsub_rn(1.0, B);
+    return (A <= B) ? A : B;
   } else if constexpr (SEL == EV_SPHERE2) {
     double c0[16], c1[16];
     load_params<4>(f.fq[0], c0);

@@ -125,6 +125,7 @@ void launch_labels_analytic(const GridP& g, const FieldP& f, uint32_t* L, cudaSt
     case EV_BOX: k_labels_analytic<false, EV_BOX><<<grid, 256, 0, s>>>(g, f, L); break;
     case EV_TORUS: k_labels_analytic<false, EV_TORUS><<<grid, 256, 0, s>>>(g, f, L); break;
     case EV_SPHERE2: k_labels_analytic<false, EV_SPHERE2><<<grid, 256, 0, s>>>(g, f, L); break;
+    case EV_BOX2F: k_labels_analytic<false, EV_BOX2F><<<grid, 256, 0, s>>>(g, f, L); break;
     default: k_labels_analytic<false, EV_PARAM><<<grid, 256, 0, s>>>(g, f, L); break;
   }
 }
@@ -744,6 +745,7 @@ void launch_search1d_analytic(const GridP& g, const FieldP& f, const OptP& o, co
     case EV_BOX: S1A(false, EV_BOX); break;
     case EV_TORUS: S1A(false, EV_TORUS); break;
     case EV_SPHERE2: S1A(false, EV_SPHERE2); break;
+    case EV_BOX2F: S1A(false, EV_BOX2F); break;
     default: S1A(false, EV_PARAM); break;
   }
 #undef S1A
@@ -1108,6 +1110,7 @@ void launch_search2d_analytic(const GridP& g, const FieldP& f, const OptP& o, co
     case EV_BOX: S2A(false, EV_BOX); break;
     case EV_TORUS: S2A(false, EV_TORUS); break;
     case EV_SPHERE2: S2A(false, EV_SPHERE2); break;
+    case EV_BOX2F: S2A(false, EV_BOX2F); break;
     default: S2A(false, EV_PARAM); break;
   }
 #undef S2A
