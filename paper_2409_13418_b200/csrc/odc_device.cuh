@@ -692,6 +692,59 @@ __device__ __forceinline__ void prim_ball_fp(int op, const double (&q)[16], cons
   }
   prim_ball(op, c, pc, 1.0, rad, lo, hi);
 }
+// box sd (fields.py:103-111) from the box-local point: |max(q,0)| + min(max q, 0)
+__device__ __forceinline__ double box_sd_local(const double l[3], const double* h) {
+  double qq[3], mq[3];
+  for (int a = 0; a < 3; a++) {
+    qq[a] = __dsub_rn(fabs(l[a]), h[a]);
+    mq[a] = qq[a] > 0.0 ? qq[a] : 0.0;
+  }
+  const double outside = norm3(mq);
+  double mx = qq[0];
+  if (qq[1] > mx) mx = qq[1];
+  if (qq[2] > mx) mx = qq[2];
+  const double inside = mx < 0.0 ? mx : 0.0;
+  return __dadd_rn(outside, inside);
+}
+// EV_BOX2F ball (two boxes in one frame): the rotation and its norm once
+__device__ __forceinline__ int field_label_ball_box2f(const FieldP& f, const double pc[3], double rad) {
+  double l[3] = {__dsub_rn(pc[0], f.fq[0][0]), __dsub_rn(pc[1], f.fq[0][1]), __dsub_rn(pc[2], f.fq[0][2])};
+  double L = 1.0;
+  if (f.fq[0][6] != 0.0) {
+    double R[9], o[3];
+    for (int j = 0; j < 9; j++) R[j] = f.fq[0][7 + j];
+    rot_rows(l, R, o);
+    l[0] = o[0]; l[1] = o[1]; l[2] = o[2];
+    L = frob9(R);
+  }
+  const double base = 1.0 + fabs(pc[0]) + fabs(pc[1]) + fabs(pc[2]) + fabs(f.fq[0][0]) + fabs(f.fq[0][1]) +
+                      fabs(f.fq[0][2]);
+  double lo[2], hi[2];
+  for (int k = 0; k < 2; k++) {
+    const double* h = &f.fq[k][3];
+    const double sd = box_sd_local(l, h);
+    const double m = L * rad * (1.0 + 1e-9) + 1e-9 * (base + fabs(h[0]) + fabs(h[1]) + fabs(h[2]));
+    if (!(fabs(sd) < 1e300) || !(m < 1e300)) return -1;
+    lo[k] = sd - m;
+    hi[k] = sd + m;
+    sd2raw_ball(lo[k], hi[k]);
+  }
+  double a0 = lo[0], a1 = hi[0], b0 = lo[1], b1 = hi[1];
+  if (f.fop[2] == ODC_OP_RAW_MAX) {
+    a0 = fmax(a0, b0);
+    a1 = fmax(a1, b1);
+  } else if (f.fop[2] == ODC_OP_RAW_MIN) {
+    a0 = fmin(a0, b0);
+    a1 = fmin(a1, b1);
+  } else {  // min(a, 1 - b)
+    const double t = __dsub_rn(1.0, b1);
+    b1 = __dsub_rn(1.0, b0);
+    b0 = t;
+    a0 = fmin(a0, b0);
+    a1 = fmin(a1, b1);
+  }
+  return ball_decide(a0, a1, f.iso);
+}
 template <bool SEL = false>
 __device__ __forceinline__ int field_label_ball(const FieldP& f, const double pc[3], double rad) {
   if (f.fast) {

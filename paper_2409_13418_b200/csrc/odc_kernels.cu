@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(256, 4) k_labels_analytic(GridP g, FieldP f, u
     const double pc[3] = {__dmul_rn(__dadd_rn(pa, pb), 0.5), gpos(gl, 1, y), gpos(gl, 2, z)};
     const double rad = __dmul_rn(__dsub_rn(pb, pa), 0.5) * (1.0 + 1e-12) + 1e-300;
     if constexpr (B) dec = field_label_ball(f.batch[b], pc, rad);
+    else if constexpr (EV == EV_BOX2F) dec = field_label_ball_box2f(f, pc, rad);
     else dec = field_label_ball(f, pc, rad);
     if (dec >= 0) L[w] = dec ? bits_below(g.S, wx) : 0u;
   }
