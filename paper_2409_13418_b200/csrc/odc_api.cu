@@ -13,6 +13,7 @@
 #include <string>
 #include <thread>
 #include <vector>
+#include <chrono>
 
 #include "../../include/odc.h"
 #include "odc_kernels.h"
@@ -120,6 +121,11 @@ struct odc_ctx {
   unsigned int* d_fail = nullptr;          // device flag: a winding query stayed on the surface
   unsigned long long* d_sched = nullptr;   // MLP evaluator's pair counters: [0] only grows, [1] compacted batches
   unsigned long long sched_next = 0;       // its value when the next launch starts
+  // odc_set_param("step_trace"), profiling only: 1 = per-step event timings
+  // of the 2D lock-step search to stderr, 2 = also every evaluator launch's
+  // per-CTA start/end spread, 3 = 1 after a 300 ms idle (a cool GPU)
+  int step_trace = 0;
+  unsigned long long* trace_buf = nullptr;
   char* h_stage = nullptr;  // grow-only pinned staging for mesh copy-back
   // mesh validation (its own workspace: the last extraction stays valid)
   Arena varena;
@@ -245,6 +251,10 @@ void run_mlp(odc_ctx* c, const odc_field* f, const PointSrc& src, int64_t n, uin
   MlpDev md = override_md ? *override_md : f->mlp;
   unsigned long long base0 = 0;
   md.sched = src.n_dev ? c->d_sched + 1 : c->d_sched;
+  if (c->trace_buf && !override_md) {
+    CUDA_TRY(cudaMemsetAsync(c->trace_buf, 0, 8 * 2048, s));
+    md.trace = c->trace_buf;
+  }
   const int k = mlp_eval(md, src, n, lab, raw, s, src.n_dev ? &base0 : &c->sched_next);
   if (k < 0)
     throw OdcError{ODC_E_CUDA, "MLP evaluator: no pair counter on this context or no weights"};
@@ -287,6 +297,49 @@ void eval_points(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, u
     run_mlp(c, f, src, n, lab, raw, c->stream);
   }
   check_launch(c);
+}
+
+// step_trace (profiling): the evaluator launch of one lock-step -- its span
+// from the first CTA start to the last CTA end, and the spread of CTA ends
+// (the drain tail)
+void trace_spans(odc_ctx* c, int step) {
+  std::vector<unsigned long long> tb(2048);
+  CUDA_TRY(cudaMemcpyAsync(tb.data(), c->trace_buf, 8 * 2048, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+  for (int i = 0; i < 148; i++) {  // slots 400 + 2b, 401 + 2b: CTA b's start and end
+    const unsigned long long a = tb[400 + 2 * i], z = tb[401 + 2 * i];
+    if (!a || !z) continue;
+    s0 = std::min(s0, a);
+    s1 = std::max(s1, a);
+    e0 = std::min(e0, z);
+    e1 = std::max(e1, z);
+  }
+  if (s1) fprintf(stderr, "  step %2d evaluator: span %.1f us, CTA starts spread %.1f us, ends spread %.1f us\n", step,
+                  (e1 - s0) * 1e-3, (s1 - s0) * 1e-3, (e1 - e0) * 1e-3);
+}
+// step_trace: per-step evaluation (evaluator + label fix-up), update and gap times
+void trace_steps(odc_ctx* c, std::vector<cudaEvent_t>& tev) {
+  CUDA_TRY(cudaEventSynchronize(tev.back()));
+  const int nsteps = (int)tev.size() / 3;
+  double se = 0, su = 0, sg = 0;
+  for (int step = 0; step < nsteps; step++) {
+    float e = 0, u = 0, gap = 0;
+    cudaEventElapsedTime(&e, tev[3 * step], tev[3 * step + 1]);
+    cudaEventElapsedTime(&u, tev[3 * step + 1], tev[3 * step + 2]);
+    if (step + 1 < nsteps) cudaEventElapsedTime(&gap, tev[3 * step + 2], tev[3 * step + 3]);
+    se += e;
+    su += u;
+    sg += gap;
+    fprintf(stderr, "step %2d: eval %.3f ms  update %.3f ms  gap %.3f ms\n", step, e, u, gap);
+  }
+  fprintf(stderr, "2D search: eval %.3f  update %.3f  gaps %.3f ms\n", se, su, sg);
+  for (auto e : tev) cudaEventDestroy(e);
+  tev.clear();
+  if (c->trace_buf) {
+    cudaFree(c->trace_buf);
+    c->trace_buf = nullptr;
+  }
 }
 
 // MeshWindingField "perturb" mode gave up on a query (fields.py:354-355)
@@ -833,9 +886,22 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       int32_t* map = compact ? need(c->arena.get<int32_t>(2 * Q)) : nullptr;
       int64_t* cnt2 = compact ? need(c->arena.get<int64_t>(2)) : nullptr;
       bool packed = false;  // this step's points are compacted
+      std::vector<cudaEvent_t> tev;  // step_trace: eval start, eval end, step end per step
+      if (c->step_trace) {
+        if (c->step_trace == 3) {
+          CUDA_TRY(cudaStreamSynchronize(s));
+          std::this_thread::sleep_for(std::chrono::milliseconds(300));
+        }
+        if (c->step_trace == 2) CUDA_TRY(cudaMalloc(&c->trace_buf, 8 * 2048));
+        tev.resize(3 * nsteps);
+        for (auto& e : tev) CUDA_TRY(cudaEventCreate(&e));
+      }
       for (int step = 0; step < nsteps; step++) {
+        if (!tev.empty()) CUDA_TRY(cudaEventRecord(tev[3 * step], s));
         if (packed) eval_points(c, f, pts, M, lab, nullptr, cnt2 + (step & 1), map);
         else eval_points(c, f, pts, M, lab, nullptr);
+        if (!tev.empty()) CUDA_TRY(cudaEventRecord(tev[3 * step + 1], s));
+        if (c->trace_buf) trace_spans(c, step);
         if (step + 1 < nsteps) {  // update + the next step's points in one pass
           const bool was = packed;
           // the first step of each linear scan still has every instance scanning
@@ -847,7 +913,9 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
           launch_search2d_lockstep_update(g, op, c->L, c->inst_key, Q, step, lab, state, dstat, s);
         }
         check_launch(c);
+        if (!tev.empty()) CUDA_TRY(cudaEventRecord(tev[3 * step + 2], s));
       }
+      if (!tev.empty()) trace_steps(c, tev);
       launch_search2d_lockstep_finish(g, op, c->L, c->rec, c->inst_key, Q, c->pos1d, state, c->s2, dst, q_lo, q_hi,
                                       s);
       check_launch(c);
@@ -1150,6 +1218,7 @@ void odc_destroy(odc_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->d_fail) cudaFree(c->d_fail);
   if (c->d_sched) cudaFree(c->d_sched);
+  if (c->trace_buf) cudaFree(c->trace_buf);
   for (auto e : c->copy_evs) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -1165,6 +1234,10 @@ int odc_set_param(odc_ctx* c, const char* name, int64_t value) {
   if (!c || !name) return ODC_E_ARG;
   if (std::strcmp(name, "mlp_debug") == 0 && value >= 0 && value <= 255) {
     c->mlp_debug = (int)value;
+    return ODC_OK;
+  }
+  if (std::strcmp(name, "step_trace") == 0 && value >= 0 && value <= 3) {
+    c->step_trace = (int)value;
     return ODC_OK;
   }
   if (std::strcmp(name, "mbar_timeout_ms") == 0 && value >= 0) {  // 0: the MLP evaluator's waits never trap

@@ -12,7 +12,7 @@ from paper_2409_13418_b200.pipeline import DeviceField  # noqa: E402
 
 ctx = _lib.Context(0)
 L = _lib.load()
-L.odc_set_param(ctx.handle, b"mlp_impl", 3)
+
 tr = np.zeros(1024, dtype=np.int64)
 extra = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 with DeviceField(ctx, MlpField()) as f:
