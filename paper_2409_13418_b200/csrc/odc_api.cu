@@ -1304,6 +1304,7 @@ int odc_field_analytic(odc_ctx* c, const odc_node* nodes, int32_t n_nodes, int32
   f->fp.kind = 0;
   f->fp.iso = iso;
   fieldp_set_fast(f->fp, nodes, n_nodes);
+  f->fp.ev = ev_mode_of(f->fp);
   *out = f;
   return ODC_OK;
 }

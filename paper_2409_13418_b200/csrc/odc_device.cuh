@@ -229,6 +229,7 @@ struct FieldP {
   double fq[2][16] = {};
   double fk = 0.0;
   const FieldP* batch = nullptr;  // batch: device (nb) fields, one per shape
+  int32_t ev = 0;                 // evaluation mode (ev_mode_of), set by the host
 };
 __device__ __forceinline__ const FieldP& field_of(const FieldP& f, int b) { return f.batch ? f.batch[b] : f; }
 // host: classify a program for FieldP's fast paths (same patterns as field_raw)

@@ -106,8 +106,17 @@ __global__ void __launch_bounds__(256, 4) k_labels_analytic(GridP g, FieldP f, u
       GridP gl = g;
       const int b = localize<B>(gl, zj);
       const double p[3] = {gpos(gl, 0, x), gpos(gl, 1, yj), gpos(gl, 2, zj)};
-      if constexpr (B) lab = field_label_t<true>(f.batch[b], p);
-      else lab = field_label_t<EV>(f, p);
+      if constexpr (B) {  // the shape's specialised evaluation (warp-uniform: one word)
+        const FieldP& fb = f.batch[b];
+        switch (fb.ev) {
+          case EV_SPHERE: lab = field_label_t<EV_SPHERE>(fb, p); break;
+          case EV_BOX: lab = field_label_t<EV_BOX>(fb, p); break;
+          case EV_TORUS: lab = field_label_t<EV_TORUS>(fb, p); break;
+          default: lab = field_label_t<EV_SEL>(fb, p); break;
+        }
+      } else {
+        lab = field_label_t<EV>(f, p);
+      }
     }
     const uint32_t word = __ballot_sync(0xffffffffu, lab);
     if (lane == 0) L[wj] = word;
@@ -725,7 +734,13 @@ __global__ void __launch_bounds__(128) k_search1d_analytic(GridP g, FieldP f, Op
   if constexpr (B) {
     GridP gl = g;
     const int sb = localize<B>(gl, idiv(edge_key[k] / 3, g.S2));
-    search1d_one<EV_SEL>(gl, f.batch[sb], o, L, edge_key, k, tout, pos, vin_out);
+    const FieldP& fb = f.batch[sb];
+    switch (fb.ev) {  // the shape's specialised evaluation (elements are in shape order)
+      case EV_SPHERE: search1d_one<EV_SPHERE>(gl, fb, o, L, edge_key, k, tout, pos, vin_out); break;
+      case EV_BOX: search1d_one<EV_BOX>(gl, fb, o, L, edge_key, k, tout, pos, vin_out); break;
+      case EV_TORUS: search1d_one<EV_TORUS>(gl, fb, o, L, edge_key, k, tout, pos, vin_out); break;
+      default: search1d_one<EV_SEL>(gl, fb, o, L, edge_key, k, tout, pos, vin_out); break;
+    }
   } else {
     search1d_one<EV>(g, f, o, L, edge_key, k, tout, pos, vin_out);
   }
@@ -1087,8 +1102,15 @@ __global__ void __launch_bounds__(128) k_search2d_analytic(GridP g, FieldP f, Op
   if constexpr (B) {
     GridP gl = g;
     const int sb = localize<B>(gl, idiv((inst_key[q] >> 1) / 3, g.S2));
-    search2d_one<B, EV_SEL>(gl, f.batch[sb], o, L, rec, inst_key, q, pos1d, out, inst_edges, st + sb, dst, st_lo,
-                            st_hi);
+    const FieldP& fb = f.batch[sb];
+#define S2O(EVV) search2d_one<B, EVV>(gl, fb, o, L, rec, inst_key, q, pos1d, out, inst_edges, st + sb, dst, st_lo, st_hi)
+    switch (fb.ev) {  // the shape's specialised evaluation (elements are in shape order)
+      case EV_SPHERE: S2O(EV_SPHERE); break;
+      case EV_BOX: S2O(EV_BOX); break;
+      case EV_TORUS: S2O(EV_TORUS); break;
+      default: S2O(EV_SEL); break;
+    }
+#undef S2O
   } else {
     search2d_one<B, EV>(g, f, o, L, rec, inst_key, q, pos1d, out, inst_edges, st, dst, st_lo, st_hi);
   }
