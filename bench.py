@@ -317,9 +317,9 @@ def run_gpu(args, rank, world, dist):
         from paper_2409_13418_b200.fields import lower_program
 
         h2d = 136 * len(lower_program(field))
-    d2h = V * 24 + T * 24 + V * 24  # vertices f64, triangles i64 (widened on the device), provenance
+    d2h = V * 24 + T * 12 + V * 24  # vertices f64, triangles i32 (widened to i64 by the host), provenance
     if res.raw_mesh is not res.mesh:
-        d2h += T * 24  # pre-repair triangles
+        d2h += T * 12  # pre-repair triangles
 
     # ---- roofline of the dominant kernel (grid labels)
     peaks, peak_kind = load_peaks()
@@ -474,7 +474,7 @@ def run_gpu_batch(args, rank, world, dist):
     if rank != 0:
         return
     cells = n * R**3
-    d2h = sum(r.mesh.n_vertices * 48 + r.mesh.n_triangles * 24 * (2 if r.raw_mesh is not r.mesh else 1)
+    d2h = sum(r.mesh.n_vertices * 48 + r.mesh.n_triangles * 12 * (2 if r.raw_mesh is not r.mesh else 1)
               for r in res)
     h2d = sum(len(lower_program(f)) * C.sizeof(_lib.Node) for f, _ in mine)  # the field programs
     cpu = None
@@ -576,7 +576,7 @@ def run_gpu_slabs(args, rank, world, dist):
         from paper_2409_13418_b200.fields import lower_program
 
         h2d = world * (136 * len(lower_program(field)) + p_h2d)
-    d2h = V * 24 + T * 24 + V * 24 + (T * 24 if res.raw_mesh is not res.mesh else 0) + world * p_d2h
+    d2h = V * 24 + T * 12 + V * 24 + (T * 12 if res.raw_mesh is not res.mesh else 0) + world * p_d2h
     roof = None
     if k_ms:
         peaks, peak_kind = load_peaks()

@@ -1822,10 +1822,14 @@ int odc_mesh_finish(odc_ctx* c, const double* vertices, int64_t V, const int32_t
 // pieces into the (pageable, first-touch) destinations as soon as their
 // event completes -- the D2H of later pieces overlaps the host copies of
 // earlier ones.
+// One array of a copy-back: `bytes` on the device; widen = the device holds
+// int32 that the host receives as int64 (triangles: half the PCIe bytes,
+// widened by the copy threads on the way out of the staging buffer).
 struct CopySeg {
   const void* dev;
   void* host;
   size_t bytes;
+  bool widen = false;
 };
 void copy_out_pipelined(odc_ctx* cc, const std::vector<CopySeg>& segs) {
   cudaStream_t s = cc->stream;
@@ -1834,6 +1838,7 @@ void copy_out_pipelined(odc_ctx* cc, const std::vector<CopySeg>& segs) {
     char* stage;
     char* dst;
     size_t n;
+    bool widen;
   };
   const size_t chunk = 4u << 20;
   size_t total = 0;
@@ -1853,7 +1858,8 @@ void copy_out_pipelined(odc_ctx* cc, const std::vector<CopySeg>& segs) {
   for (const CopySeg& g : segs) {
     if (!g.host || !g.bytes) continue;
     for (size_t o = 0; o < g.bytes; o += chunk)
-      pieces.push_back({(const char*)g.dev + o, cc->h_stage + off + o, (char*)g.host + o, std::min(chunk, g.bytes - o)});
+      pieces.push_back({(const char*)g.dev + o, cc->h_stage + off + o, (char*)g.host + (g.widen ? 2 * o : o),
+                        std::min(chunk, g.bytes - o), g.widen});
     off += (g.bytes + 255) & ~(size_t)255;
   }
   while (cc->copy_evs.size() < pieces.size()) {
@@ -1878,7 +1884,14 @@ void copy_out_pipelined(odc_ctx* cc, const std::vector<CopySeg>& segs) {
         bad = 1;
         return;
       }
-      std::memcpy(pieces[i].dst, pieces[i].stage, pieces[i].n);
+      if (pieces[i].widen) {
+        const int32_t* a = (const int32_t*)pieces[i].stage;
+        int64_t* b = (int64_t*)pieces[i].dst;
+        const size_t m = pieces[i].n / 4;
+        for (size_t j = 0; j < m; j++) b[j] = a[j];
+      } else {
+        std::memcpy(pieces[i].dst, pieces[i].stage, pieces[i].n);
+      }
     }
   };
   if (nthr <= 1) {
@@ -1920,11 +1933,7 @@ int copy_mesh_impl(odc_ctx* c, CopyMeshArgs* a) {
     cudaStream_t s = cc->stream;
     std::vector<CopySeg> segs;
     segs.push_back({dv, x->v, sizeof(double) * 3 * V});
-    if (x->t && T) {
-      int64_t* t64 = need(cc->arena.get<int64_t>(3 * T));
-      launch_widen_i32(dt, t64, 3 * T, s);
-      segs.push_back({t64, x->t, sizeof(int64_t) * 3 * T});
-    }
+    if (x->t && T) segs.push_back({dt, x->t, sizeof(int32_t) * 3 * T, true});
     if ((x->kind || x->ref) && V) {
       int64_t* dk = need(cc->arena.get<int64_t>(V));
       int64_t* dr = need(cc->arena.get<int64_t>(2 * V));
@@ -1937,11 +1946,8 @@ int copy_mesh_impl(odc_ctx* c, CopyMeshArgs* a) {
       segs.push_back({dk, x->kind, sizeof(int64_t) * V});
       segs.push_back({dr, x->ref, sizeof(int64_t) * 2 * V});
     }
-    if (x->raw_t && T) {  // pre-repair triangles (same count, corners not renamed)
-      int64_t* r64 = need(cc->arena.get<int64_t>(3 * T));
-      launch_widen_i32(cc->tris0, r64, 3 * T, s);
-      segs.push_back({r64, x->raw_t, sizeof(int64_t) * 3 * T});
-    }
+    if (x->raw_t && T)  // pre-repair triangles (same count, corners not renamed)
+      segs.push_back({cc->tris0, x->raw_t, sizeof(int32_t) * 3 * T, true});
     CUDA_TRY(cudaGetLastError());
     copy_out_pipelined(cc, segs);
     return (int)ODC_OK;
@@ -2001,17 +2007,17 @@ int odc_copy_batch_meshes(odc_ctx* c, double* vertices, int64_t* triangles, int6
       segs.push_back({orf, x->ref, sizeof(int64_t) * 2 * V});
     }
     if (x->t && T) {
-      int64_t* t64 = need(cc->arena.get<int64_t>(3 * T));
-      launch_batch_tris(cc->tris1, T, cc->b_local, t64, s);
-      segs.push_back({t64, x->t, sizeof(int64_t) * 3 * T});
+      int32_t* t32 = need(cc->arena.get<int32_t>(3 * T));
+      launch_batch_tris(cc->tris1, T, cc->b_local, t32, s);
+      segs.push_back({t32, x->t, sizeof(int32_t) * 3 * T, true});
     }
     if (x->raw_t && T && V != V0) {  // pre-repair triangles: only shapes the repair changed
-      int64_t* r64 = need(cc->arena.get<int64_t>(3 * T));
-      launch_batch_tris(cc->tris0, T, cc->b_local, r64, s);
+      int32_t* r32 = need(cc->arena.get<int32_t>(3 * T));
+      launch_batch_tris(cc->tris0, T, cc->b_local, r32, s);
       for (int b = 0; b < cc->nb; b++) {
         const int64_t t0 = cc->b_bounds[(size_t)b * kBatchCols + 5], t1 = cc->b_bounds[(size_t)(b + 1) * kBatchCols + 5];
         if (cc->b_vstart[b + 1] - cc->b_vstart[b] != cc->b_v0[b] && t1 > t0)
-          segs.push_back({r64 + 3 * t0, x->raw_t + 3 * t0, sizeof(int64_t) * 3 * (t1 - t0)});
+          segs.push_back({r32 + 3 * t0, x->raw_t + 3 * t0, sizeof(int32_t) * 3 * (t1 - t0), true});
       }
     }
     CUDA_TRY(cudaGetLastError());

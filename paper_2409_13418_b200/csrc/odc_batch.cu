@@ -199,11 +199,11 @@ void launch_batch_gather(const double* verts, const int32_t* perm, const uint32_
 }
 
 __global__ void k_batch_tris(const int32_t* __restrict__ tris, int64_t n, const int32_t* __restrict__ local,
-                             int64_t* __restrict__ out) {
+                             int32_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = local[tris[i]];
 }
-void launch_batch_tris(const int32_t* tris, int64_t T, const int32_t* local, int64_t* out, cudaStream_t s) {
+void launch_batch_tris(const int32_t* tris, int64_t T, const int32_t* local, int32_t* out, cudaStream_t s) {
   if (T) k_batch_tris<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, 3 * T, local, out);
 }
 

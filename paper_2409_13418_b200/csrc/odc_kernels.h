@@ -278,7 +278,7 @@ void launch_local_ids(const uint32_t* skeys, const int32_t* perm, int64_t V, con
 void launch_batch_gather(const double* verts, const int32_t* perm, const uint32_t* skeys, int64_t V,
                          const int64_t* kind_in, const int64_t* ref_in, int64_t cell_per_shape,
                          int64_t key_per_shape, double* vout, int64_t* kout, int64_t* rout, cudaStream_t s);
-void launch_batch_tris(const int32_t* tris, int64_t T, const int32_t* local, int64_t* out, cudaStream_t s);
+void launch_batch_tris(const int32_t* tris, int64_t T, const int32_t* local, int32_t* out, cudaStream_t s);
 
 // ---- distributed slab finish (odc_slabfin.cu)
 void launch_seam_flags(const int32_t* tris, int64_t T, int64_t n_halo, uint32_t* flag, cudaStream_t s);

@@ -27,9 +27,8 @@ for i in range(reps):
     o = P.make_options(P.ContourOptions())
     rc = L.odc_extract(ctx.handle, df.handle, lo_c, hi_c, RR, ctypes.byref(o), ctypes.byref(st))
     t.append(time.perf_counter())
-    m = P._copy_mesh(ctx, 0, st, True)
+    m, raw = P._copy_meshes(ctx, st, True)
     t.append(time.perf_counter())
-    raw = P._raw_from_repaired(ctx, m, st) if st.repair_added_vertices else m
     t.append(time.perf_counter())
     df.free()
     t.append(time.perf_counter())
