@@ -135,6 +135,10 @@ struct odc_ctx {
   std::vector<cudaEvent_t> copy_evs;       // one per staged piece of a mesh copy
   std::string err;
   int launches = 0;
+  // the statistics block as read back with the used-partition count
+  // (finish_mesh): final by then, so finish_stats needs no readback of its own
+  DevStats h_stats{};
+  bool stats_cached = false;
   int mlp_debug = 0;  // odc_set_param("mlp_debug"): profiling experiments, odc_profile_mlp only
   const double* profile_pts = nullptr;  // odc_set_param("profile_points"): host (n,3) points for odc_profile_mlp
   // last extraction
@@ -214,10 +218,7 @@ void readback(odc_ctx* c, const void* dev, size_t bytes) {
   CUDA_TRY(cudaStreamSynchronize(c->stream));
 }
 
-void check_status(odc_ctx* c, DevStatus* dst) {
-  readback(c, dst, sizeof(DevStatus));
-  DevStatus s;
-  std::memcpy(&s, c->h_pinned, sizeof s);
+void raise_device_status(odc_ctx* c, const DevStatus& s) {
   if (s.code == ODC_E_ASSERT) {
     int64_t q = s.detail;
     std::string where;
@@ -241,6 +242,21 @@ void check_status(odc_ctx* c, DevStatus* dst) {
                                      ": no corner label differs from the midpoint"};
   }
   if (s.code) throw OdcError{s.code, "device status " + std::to_string(s.code)};
+}
+// readback of `bytes` at `dev` that also brings the device status (the 2D
+// search's assertion, raised first) in the same synchronisation
+void readback_checked(odc_ctx* c, const void* dev, size_t bytes, DevStatus* dstat) {
+  if (!dstat) {
+    readback(c, dev, bytes);
+    return;
+  }
+  char* h = reinterpret_cast<char*>(c->h_pinned);
+  CUDA_TRY(cudaMemcpyAsync(h, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(h + 2048, dstat, sizeof(DevStatus), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  DevStatus st;
+  std::memcpy(&st, h + 2048, sizeof st);
+  raise_device_status(c, st);
 }
 
 // One MLP evaluator launch on this context's stream and pair counter.
@@ -402,8 +418,12 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
   cudaStream_t s = c->stream;
   launch_count_used(used, P, dst, s);
   check_launch(c);
-  readback(c, &dst->used_partitions, sizeof(unsigned long long));
-  const int64_t used_p = (int64_t)c->h_pinned[0];
+  // every statistic but the repair's is final here: one readback serves the
+  // used-partition count and finish_stats
+  readback(c, dst, sizeof(DevStats));
+  std::memcpy(&c->h_stats, c->h_pinned, sizeof(DevStats));
+  c->stats_cached = true;
+  const int64_t used_p = (int64_t)c->h_stats.used_partitions;
   int64_t V0 = P + NF;
   c->src0 = nullptr;
   if (used_p != P) {
@@ -453,17 +473,20 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
       check_launch(c);
       launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s, dirty);
       check_launch(c);
-      if (!big) {  // fans of more than 64 triangles need global scratch: re-run with it
-        readback(c, &dst->repair_overflow, sizeof(unsigned long long));
-        if (c->h_pinned[0]) {
-          big = need(c->arena.get<char>(repair_scratch_bytes(T)));
-          CUDA_TRY(cudaMemsetAsync(&dst->repair_overflow, 0, sizeof(unsigned long long), s));
-          launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s, dirty);
-          check_launch(c);
-        }
-      }
       scan1(c, extra, eoff, curV + 1, totals + 7);
-      readback(c, totals + 7, sizeof(unsigned long long));
+      // the added-vertex total and the fan-overflow flag in one synchronisation
+      CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[0], totals + 7, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[1], &dst->repair_overflow, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      if (!big && c->h_pinned[1]) {  // fans of more than 64 triangles need global scratch: re-run with it
+        big = need(c->arena.get<char>(repair_scratch_bytes(T)));
+        CUDA_TRY(cudaMemsetAsync(&dst->repair_overflow, 0, sizeof(unsigned long long), s));
+        launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s, dirty);
+        check_launch(c);
+        scan1(c, extra, eoff, curV + 1, totals + 7);
+        readback(c, totals + 7, sizeof(unsigned long long));
+      }
       const int64_t E = (int64_t)c->h_pinned[0];
       if (E == 0) break;
       int32_t* next = need(c->arena.get<int32_t>(3 * T));
@@ -527,6 +550,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   for (int i = 0; i < ODC_N_CAT; i++) st->cat_order[i] = -1;
   c->valid = false;
   c->launches = 0;
+  c->stats_cached = false;
   c->slab_U = -1;
   c->arena.reset();
   c->keep = o->keep_intermediates != 0;
@@ -685,10 +709,14 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   st->n_crossing_cells = c_hi - c_lo;
 
   auto finish_stats = [&]() {
-    check_surface(c);
-    readback(c, dst, sizeof(DevStats));
+    if (f->kind == 2) check_surface(c);  // only the winding field raises through d_fail
     DevStats h;
-    std::memcpy(&h, c->h_pinned, sizeof h);
+    if (c->stats_cached) {
+      h = c->h_stats;
+    } else {
+      readback(c, dst, sizeof(DevStats));
+      std::memcpy(&h, c->h_pinned, sizeof h);
+    }
     st->boundary_inside_vertices = (int64_t)h.boundary_inside;
     for (int i = 0; i < 4; i++) {
       st->point2d_status_counts[i] = (int64_t)h.status[i];
@@ -852,6 +880,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   // ---- normals: 2D points (search.py:194-322) or fd gradient (pipeline.py:126-151)
   mark(3);
   double* edge_normals = nullptr;
+  DevStatus* status_pending = nullptr;
   c->inst_edges = c->keep ? need(c->arena.get<int64_t>(2 * Q)) : nullptr;
   c->s2 = Stage2D{};
   if (op.normals == ODC_NORMALS_2D) {
@@ -920,7 +949,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
                                       s);
       check_launch(c);
     }
-    check_status(c, dstat);
+    status_pending = dstat;  // raised at the next readback (partition totals), before anything uses the points
     record(st, ODC_CAT_PROBE_FACE_MIDPOINT, 1, Q_own);
     record(st, ODC_CAT_SEARCH_2D, op.s1_lin + op.s1_bin + op.s2_lin + op.s2_bin,
            (int64_t)(op.s1_lin + op.s1_bin) * Q_own + (int64_t)(op.s2_lin + op.s2_bin) * 2 * Q_own);
@@ -956,7 +985,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   launch_cell_config(g, c->L, c->rec, c->cell_id, C, c->table, cfg, ncyc, nsamp, s);
   check_launch(c);
   scan2(c, ncyc, nsamp, pbase, sbase, C, totals);
-  readback(c, totals, 2 * sizeof(unsigned long long));
+  readback_checked(c, totals, 2 * sizeof(unsigned long long), status_pending);
   const int64_t P = (int64_t)c->h_pinned[0], Ns = (int64_t)c->h_pinned[1];
   int64_t P_halo = 0, P_end = P;  // partitions of the halo cell layer come first
   if (c_lo > 0 || c_hi < C) {
