@@ -398,16 +398,14 @@ void scan1(odc_ctx* c, const uint32_t* in, uint32_t* out, int64_t n, unsigned lo
   const uint32_t* ins[1] = {in};
   uint32_t* outs[1] = {out};
   uint32_t* tiles = need(c->arena.get<uint32_t>((n + 255) / 256 + 1));
-  launch_scan_u32(ins, outs, 1, n, tiles, totals, c->stream);
-  check_launch(c, 3);
+  check_launch(c, launch_scan_u32(ins, outs, 1, n, tiles, totals, c->stream));
 }
 void scan2(odc_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* oa, uint32_t* ob, int64_t n,
            unsigned long long* totals) {
   const uint32_t* ins[2] = {a, b};
   uint32_t* outs[2] = {oa, ob};
   uint32_t* tiles = need(c->arena.get<uint32_t>(2 * ((n + 255) / 256) + 2));
-  launch_scan_u32(ins, outs, 2, n, tiles, totals, c->stream);
-  check_launch(c, 3);
+  check_launch(c, launch_scan_u32(ins, outs, 2, n, tiles, totals, c->stream));
 }
 
 // Drop unreferenced partition vertices (polygonize.py:199-209), then repair
@@ -2121,8 +2119,7 @@ int odc_validate_manifold(odc_ctx* c, const int64_t* triangles, int64_t n_triang
       const uint32_t* ins[1] = {in};
       uint32_t* outs[1] = {o};
       uint32_t* tiles = need(A.get<uint32_t>((n + 255) / 256 + 1));
-      launch_scan_u32(ins, outs, 1, n, tiles, tot, s);
-      check_launch(cc, 3);
+      check_launch(cc, launch_scan_u32(ins, outs, 1, n, tiles, tot, s));
     };
     scan(deg, off, V + 1, totals + 0);
     launch_vertex_fill(t, T, off, cursor, inc, s);

@@ -1927,8 +1927,45 @@ __global__ void __launch_bounds__(kScanBlock) k_apply_u32(ScanPtrs p, int64_t n,
     }
   }
 }
-void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
-                     unsigned long long* totals, cudaStream_t s) {
+// Small arrays (<= kScanSmallMax): one block walks the tiles in order with a
+// running carry -- one launch instead of three (what dominates the scans of
+// a small grid is launch latency, not bandwidth).
+constexpr int kScanSmallBlock = 1024;
+constexpr int64_t kScanSmallMax = 64 * 1024;
+template <int NCH>
+__global__ void __launch_bounds__(kScanSmallBlock) k_scan_small(ScanPtrs p, int64_t n, unsigned long long* totals) {
+  unsigned long long carry[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; c++) carry[c] = 0ull;
+  for (int64_t base = 0; base < n; base += (int64_t)kScanSmallBlock * kScanPer) {
+    const int64_t i0 = base + (int64_t)threadIdx.x * kScanPer;
+    uint32_t x[NCH][kScanPer], v[NCH], ex[NCH], tot[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+      v[c] = 0u;
+#pragma unroll
+      for (int k = 0; k < kScanPer; k++) {
+        x[c][k] = i0 + k < n ? p.in[c][i0 + k] : 0u;
+        v[c] += x[c][k];
+      }
+    }
+    block_exscan<NCH, kScanSmallBlock>(v, ex, tot);
+#pragma unroll
+    for (int c = 0; c < NCH; c++) {
+      uint32_t run = (uint32_t)carry[c] + ex[c];
+#pragma unroll
+      for (int k = 0; k < kScanPer; k++) {
+        if (i0 + k < n) p.out[c][i0 + k] = run;
+        run += x[c][k];
+      }
+      carry[c] += tot[c];
+    }
+  }
+  if (threadIdx.x < NCH) totals[threadIdx.x] = carry[threadIdx.x];
+}
+
+int launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
+                    unsigned long long* totals, cudaStream_t s) {
   ScanPtrs p{};
   for (int c = 0; c < nch; c++) {
     p.in[c] = in[c];
@@ -1937,7 +1974,12 @@ void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, i
   const int64_t nt = (n + kScanTile - 1) / kScanTile;
   if (nt == 0) {
     cudaMemsetAsync(totals, 0, sizeof(unsigned long long) * nch, s);
-    return;
+    return 0;
+  }
+  if (n <= kScanSmallMax) {
+    if (nch == 1) k_scan_small<1><<<1, kScanSmallBlock, 0, s>>>(p, n, totals);
+    else k_scan_small<2><<<1, kScanSmallBlock, 0, s>>>(p, n, totals);
+    return 1;
   }
   if (nch == 1) {
     k_reduce_u32<1><<<(unsigned)nt, kScanBlock, 0, s>>>(p, n, tile_buf, nt);
@@ -1948,6 +1990,7 @@ void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, i
     k_scan_tiles<2><<<1, 1024, 0, s>>>(tile_buf, nt, totals);
     k_apply_u32<2><<<(unsigned)nt, kScanBlock, 0, s>>>(p, n, tile_buf, nt);
   }
+  return 3;
 }
 
 // ===========================================================================

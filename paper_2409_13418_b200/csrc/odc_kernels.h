@@ -128,8 +128,9 @@ void launch_fd_normals(const GridP& g, const OptP& o, const uint32_t* L, const i
 // K6: per-cell partitions, plane samples, QEF (dualize.py:194-444)
 void launch_cell_config(const GridP& g, const uint32_t* L, RecView rec, const int64_t* cell_id, int64_t C,
                         const CellTabEntry* table, uint16_t* cfg, uint32_t* ncyc, uint32_t* nsamp, cudaStream_t s);
-void launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
-                     unsigned long long* totals, cudaStream_t s);
+// returns the number of kernels launched
+int launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
+                    unsigned long long* totals, cudaStream_t s);
 struct CellOut {
   double* verts;       // (P,3) partition vertices (the first P rows of the mesh)
   int64_t* part_cell;  // (P)
