@@ -569,7 +569,7 @@ def run_gpu_slabs(args, rank, world, dist):
     V, T = res.mesh.n_vertices, res.mesh.n_triangles
     from paper_2409_13418_b200.slab import probe_bytes
 
-    p_h2d, p_d2h = probe_bytes(grid)  # balanced-bounds probe, every rank, every step
+    p_h2d, p_d2h = probe_bytes(grid, analytic=not is_mlp(field))  # balanced-bounds probe, every rank, every step
     if is_mlp(field):
         h2d = world * ((64 * 256 + 7 * 256 * 256) * 2 + 8 * 256 * 4 + 256 * 4 + p_h2d)
     else:

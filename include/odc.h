@@ -318,6 +318,16 @@ int odc_profile_mlp(odc_ctx* ctx, const odc_field* field, int64_t n, int64_t* tr
 /* Same, labels only (u8), for host points. */
 int odc_eval_labels(odc_ctx* ctx, const odc_field* field, const double* points, int64_t n, uint8_t* labels);
 
+/* Slab balancing probe (SURVEY 8(e) "Balance"; no reference counterpart --
+ * the reference has no multi-GPU path): for an analytic field on the grid
+ * (lo, hi, R), the number of cubic boxes of `box` vertices per side whose
+ * interval bound (the label pass's culling test) cannot exclude the surface,
+ * per box layer along z: counts has ceil(R / box) entries.  Proportional to
+ * the surface area in each z-range, thin walls included.  ODC_E_ARG for
+ * fields without an interval bound (MLP, mesh winding, voxels, callbacks). */
+int odc_surface_probe(odc_ctx* ctx, const odc_field* field, const double lo[3], const double hi[3], int64_t R,
+                      int64_t box, int64_t* counts);
+
 /* MLP parity hook: the fp32 head dot product h_7 . w_head (before b_head and
  * the fp64 prior) of every point, as the tcgen05 evaluator computes it
  * (bf16 operands, fp32 accumulation) -- compared against a bf16-emulating

@@ -88,7 +88,7 @@ class ManifoldReport(ctypes.Structure):
 EXPORTS = (
     "odc_version", "odc_create", "odc_destroy", "odc_last_error", "odc_set_stream", "odc_field_analytic",
     "odc_field_mlp", "odc_field_free", "odc_default_options", "odc_extract", "odc_copy_mesh", "odc_copy_mesh_pair", "odc_mesh_device",
-    "odc_copy_array", "odc_eval_raw", "odc_eval_labels", "odc_set_param", "odc_extract_slab",
+    "odc_copy_array", "odc_eval_raw", "odc_eval_labels", "odc_surface_probe", "odc_set_param", "odc_extract_slab",
     "odc_slab_globalize", "odc_mesh_finish", "odc_profile_mlp", "odc_export_obj", "odc_export_ply",
     "odc_validate_manifold", "odc_validate_copy", "odc_count_self_intersections", "odc_self_intersection_pairs",
     "odc_mesh_distance", "odc_triangle_areas", "odc_field_mesh", "odc_field_voxels", "odc_eigh3",
@@ -135,6 +135,7 @@ def load():
         L.odc_copy_array.argtypes = [vp, i32, vp, i64, P(i64)]
         L.odc_eval_raw.argtypes = [vp, vp, vp, i64, vp]
         L.odc_eval_labels.argtypes = [vp, vp, vp, i64, vp]
+        L.odc_surface_probe.argtypes = [vp, vp, vp, vp, i64, i64, vp]
         L.odc_eigh3.argtypes = [vp, vp, i64, vp, vp, vp]
         L.odc_eval_mlp_dot.argtypes = [vp, vp, vp, i64, vp]
         L.odc_eigh3_host.argtypes = [vp, i64, vp, vp, vp]

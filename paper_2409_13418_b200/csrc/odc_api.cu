@@ -173,6 +173,10 @@ struct odc_ctx {
   uint8_t* slab_used = nullptr;    // owned partitions referenced by a triangle
   uint32_t* slab_newid = nullptr;  // their compacted index
   int64_t slab_U = -1;
+  // seam of the last slab (triangles with a halo corner), flagged and ranked
+  // during odc_extract_slab; odc_slab_seam only gathers them
+  uint32_t *seam_flag = nullptr, *seam_rank = nullptr;
+  int64_t seam_n = 0;
   // mesh assembled by odc_mesh_finish: provenance supplied by the caller
   int64_t* prov_kind_in = nullptr;
   int64_t* prov_ref_in = nullptr;
@@ -1064,10 +1068,23 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     c->slab_tris = tris;
     c->P_own = P_end - P_halo;
     mark(6);
+    // the seam (distributed finish): its count comes back with the statistics
+    c->seam_n = 0;
+    c->seam_flag = c->seam_rank = nullptr;
+    const bool seam = T > 0 && P_halo > 0;
+    if (seam) {
+      c->seam_flag = need(c->arena.get<uint32_t>(T));
+      c->seam_rank = need(c->arena.get<uint32_t>(T));
+      launch_seam_flags(tris, T, P_halo, c->seam_flag, s);
+      check_launch(c);
+      scan1(c, c->seam_flag, c->seam_rank, T, totals + 4);
+      CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[256], totals + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    }
     mark(7);
     c->V0 = c->V1 = 0;
     st->raw_n_triangles = st->n_triangles = T;
-    finish_stats();
+    finish_stats();  // synchronises
+    if (seam) c->seam_n = (int64_t)c->h_pinned[256];
     c->valid = true;
     return;
   }
@@ -1696,18 +1713,9 @@ int odc_slab_seam(odc_ctx* c, int32_t* out, int64_t* n_out) {
     SeamArgs* x = (SeamArgs*)p;
     cudaStream_t s = cc->stream;
     const int64_t T = cc->T;
-    *x->n = 0;
-    if (T == 0 || cc->P_halo == 0) return (int)ODC_OK;
-    uint32_t* flag = need(cc->arena.get<uint32_t>(T));
-    uint32_t* rank = need(cc->arena.get<uint32_t>(T));
-    unsigned long long* tot = need(cc->arena.get<unsigned long long>(1));
-    launch_seam_flags(cc->slab_tris, T, cc->P_halo, flag, s);
-    check_launch(cc);
-    scan1(cc, flag, rank, T, tot);
-    readback(cc, tot, sizeof(unsigned long long));
-    *x->n = (int64_t)cc->h_pinned[0];
+    *x->n = cc->seam_n;  // flagged and counted by odc_extract_slab
     if (x->out && *x->n) {
-      launch_seam_take(cc->slab_tris, T, flag, rank, x->out, s);
+      launch_seam_take(cc->slab_tris, T, cc->seam_flag, cc->seam_rank, x->out, s);
       check_launch(cc);
       CUDA_TRY(cudaStreamSynchronize(s));
     }
@@ -1736,27 +1744,23 @@ int odc_slab_local_finish(odc_ctx* c, const int32_t* seam, int64_t n_seam, int64
     int32_t* ext = need(cc->arena.get<int32_t>(3 * (T + Ts)));
     if (T) CUDA_TRY(cudaMemcpyAsync(ext, cc->slab_tris, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
     launch_seam_map(x->seam, Ts, x->n_halo_next, P, V, ext + 3 * T, s);
-    // used owned partitions and their compacted ids (polygonize.py:199-209)
-    cc->slab_used = need(cc->arena.get<uint8_t>(Po));
-    CUDA_TRY(cudaMemsetAsync(cc->slab_used, 0, (size_t)std::max<int64_t>(Po, 1), s));
-    launch_mark_owned(ext, T + Ts, Ph, P, cc->slab_used, s);
-    uint32_t* u32 = need(cc->arena.get<uint32_t>(Po));
-    cc->slab_newid = need(cc->arena.get<uint32_t>(Po));
-    unsigned long long* cnt = need(cc->arena.get<unsigned long long>(4));
-    CUDA_TRY(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), s));
-    launch_widen_flags(cc->slab_used, Po, u32, s);
-    check_launch(cc, 2);
-    scan1(cc, u32, cc->slab_newid, Po, cnt);
-    // every owned vertex's whole fan is here: one closed disc each?
-    uint32_t* deg = need(cc->arena.get<uint32_t>(V + 1));
+    // incidence of every owned vertex (its whole fan is here), and from it
+    // the used owned partitions and their compacted ids (polygonize.py:199-209)
+    uint32_t* deg = need(cc->arena.get<uint32_t>(2 * (V + 1)));  // deg, then cursor: one memset
+    uint32_t* cursor = deg + (V + 1);
     uint32_t* off = need(cc->arena.get<uint32_t>(V + 1));
-    uint32_t* cursor = need(cc->arena.get<uint32_t>(V + 1));
     int32_t* inc = need(cc->arena.get<int32_t>(3 * (T + Ts)));
-    CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (V + 1), s));
-    CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * (V + 1), s));
+    unsigned long long* cnt = need(cc->arena.get<unsigned long long>(4));
+    CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * 2 * (V + 1), s));
+    CUDA_TRY(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), s));
     launch_degree_range(ext, T + Ts, Ph, V, deg, s);
-    check_launch(cc);
-    scan1(cc, deg, off, V + 1, cnt + 1);
+    cc->slab_used = need(cc->arena.get<uint8_t>(std::max<int64_t>(Po, 1)));
+    uint32_t* u32 = need(cc->arena.get<uint32_t>(V + 1));
+    cc->slab_newid = need(cc->arena.get<uint32_t>(V + 1));
+    launch_used_from_degree(deg, Ph, Po, V + 1, cc->slab_used, u32, s);
+    check_launch(cc, 2);
+    scan2(cc, u32, deg, cc->slab_newid, off, V + 1, cnt);  // cnt[0] = used partitions
+    // every owned vertex's fan: one closed disc?
     launch_fill_range(ext, T + Ts, Ph, V, off, cursor, inc, s);
     launch_count_nondisc(ext, off, inc, Ph, V, cnt + 2, s);
     check_launch(cc, 2);
@@ -2536,6 +2540,48 @@ int odc_eval_raw(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, d
 }
 int odc_eval_labels(odc_ctx* c, const odc_field* f, const double* pts, int64_t n, uint8_t* labels) {
   return eval_common(c, f, pts, n, nullptr, labels);
+}
+
+int odc_surface_probe(odc_ctx* c, const odc_field* f, const double lo[3], const double hi[3], int64_t R,
+                      int64_t box, int64_t* counts) {
+  if (!c || !f || !lo || !hi || !counts || R < 1 || box < 1) return ODC_E_ARG;
+  if (f->kind != 0) {
+    c->err = "surface probe: only analytic fields have an interval bound";
+    return ODC_E_ARG;
+  }
+  struct A {
+    const odc_field* f;
+    const double *lo, *hi;
+    int64_t R, box;
+    int64_t* counts;
+  } a{f, lo, hi, R, box, counts};
+  cudaSetDevice(c->device);
+  return guard(c, [](odc_ctx* cc, void* p) {
+    A* x = (A*)p;
+    GridP g{};
+    g.R = x->R;
+    g.S = x->R + 1;
+    for (int k = 0; k < 3; k++) {
+      g.lo[k] = x->lo[k];
+      g.h[k] = (x->hi[k] - x->lo[k]) / (double)x->R;
+    }
+    FieldP fp = x->f->fp;
+    fp.nodes = x->f->nodes;
+    fp.n_nodes = x->f->n_nodes;
+    fp.iso = x->f->iso;
+    const int64_t nbz = (x->R + x->box - 1) / x->box;
+    // stream-ordered scratch: the last extraction's workspace stays valid
+    unsigned long long* d = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d, sizeof(unsigned long long) * nbz, cc->stream));
+    CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * nbz, cc->stream));
+    launch_surface_probe(g, fp, x->box, d, cc->stream);
+    const cudaError_t e = cudaPeekAtLastError();
+    cudaMemcpyAsync(x->counts, d, sizeof(int64_t) * nbz, cudaMemcpyDeviceToHost, cc->stream);
+    cudaFreeAsync(d, cc->stream);
+    CUDA_TRY(e);
+    CUDA_TRY(cudaStreamSynchronize(cc->stream));
+    return (int)ODC_OK;
+  }, &a);
 }
 
 struct DotArgs {

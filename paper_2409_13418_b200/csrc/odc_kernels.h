@@ -287,8 +287,8 @@ void launch_seam_take(const int32_t* tris, int64_t T, const uint32_t* flag, cons
                       cudaStream_t s);
 void launch_seam_map(const int32_t* seam, int64_t n_tris, int64_t n_halo_next, int64_t P, int64_t ghost, int32_t* out,
                      cudaStream_t s);
-void launch_mark_owned(const int32_t* tris, int64_t n_tris, int64_t P_halo, int64_t P, uint8_t* used,
-                       cudaStream_t s);
+void launch_used_from_degree(const uint32_t* deg, int64_t P_halo, int64_t P_own, int64_t n, uint8_t* used,
+                             uint32_t* u32, cudaStream_t s);
 void launch_degree_range(const int32_t* tris, int64_t n_tris, int64_t lo, int64_t hi, uint32_t* deg, cudaStream_t s);
 void launch_fill_range(const int32_t* tris, int64_t n_tris, int64_t lo, int64_t hi, const uint32_t* off,
                        uint32_t* cursor, int32_t* inc, cudaStream_t s);
@@ -301,5 +301,7 @@ void launch_slab_final_parts(int64_t P_own, const uint8_t* used, const uint32_t*
                              cudaStream_t s);
 void launch_slab_top_ids(int64_t P_own, int64_t n_top, const uint32_t* newid, int64_t part_base, int32_t* out,
                          cudaStream_t s);
+// slab balancing: undecided boxes (of `box` vertices per side) per box layer along z
+void launch_surface_probe(const GridP& g, const FieldP& f, int64_t box, unsigned long long* counts, cudaStream_t s);
 
 }  // namespace odc

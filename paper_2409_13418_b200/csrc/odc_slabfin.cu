@@ -60,17 +60,21 @@ void launch_seam_map(const int32_t* seam, int64_t n_tris, int64_t n_halo_next, i
   if (n_tris) k_seam_map<<<grid_for(3 * n_tris, 256), 256, 0, s>>>(seam, 3 * n_tris, n_halo_next, P, ghost, out);
 }
 
-// owned partitions [P_halo, P) referenced by any corner
-__global__ void k_mark_owned(const int32_t* __restrict__ tris, int64_t n, int64_t P_halo, int64_t P,
-                             uint8_t* __restrict__ used) {
+// owned partitions [P_halo, P) referenced by any corner: the incidence
+// count of the fan pass (k_degree_range over the same triangles) is
+// non-zero exactly for them.  used (u8, P_own) for odc_slab_final and its
+// u32 widening (n >= P_own entries, zero past P_own) for the compaction scan.
+__global__ void k_used_from_degree(const uint32_t* __restrict__ deg, int64_t P_halo, int64_t P_own, int64_t n,
+                                   uint8_t* __restrict__ used, uint32_t* __restrict__ u32) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int64_t v = tris[i];
-  if (v >= P_halo && v < P) used[v - P_halo] = 1;
+  const uint32_t u = i < P_own && deg[P_halo + i] > 0u ? 1u : 0u;
+  if (i < P_own) used[i] = (uint8_t)u;
+  u32[i] = u;
 }
-void launch_mark_owned(const int32_t* tris, int64_t n_tris, int64_t P_halo, int64_t P, uint8_t* used,
-                       cudaStream_t s) {
-  if (n_tris) k_mark_owned<<<grid_for(3 * n_tris, 256), 256, 0, s>>>(tris, 3 * n_tris, P_halo, P, used);
+void launch_used_from_degree(const uint32_t* deg, int64_t P_halo, int64_t P_own, int64_t n, uint8_t* used,
+                             uint32_t* u32, cudaStream_t s) {
+  if (n) k_used_from_degree<<<grid_for(n, 256), 256, 0, s>>>(deg, P_halo, P_own, n, used, u32);
 }
 
 // incidence of the vertices in [lo, hi) only
@@ -164,6 +168,46 @@ void launch_slab_final_parts(int64_t P_own, const uint8_t* used, const uint32_t*
 void launch_slab_top_ids(int64_t P_own, int64_t n_top, const uint32_t* newid, int64_t part_base, int32_t* out,
                          cudaStream_t s) {
   if (n_top) k_slab_top_ids<<<grid_for(n_top, 256), 256, 0, s>>>(P_own, n_top, newid, part_base, out);
+}
+
+// Surface probe for slab balancing (analytic fields): one thread per cubic
+// box of `box` vertices per side; the box is undecided when the label pass's
+// interval bound (field_label_ball, the culling test of k_labels_analytic)
+// cannot place the whole ball around it on one side of iso.  counts[bz] =
+// undecided boxes in box layer bz -- proportional to the surface area in
+// that z-range (thin walls included, which a label-flip probe misses).
+__global__ void k_surface_probe(GridP g, FieldP f, int64_t box, int64_t nbx, int64_t nby, int64_t nbz,
+                                unsigned long long* __restrict__ counts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = nbx * nby * nbz;
+  const int64_t bz = i < n ? i / (nbx * nby) : 0;
+  unsigned und = 0;
+  if (i < n) {
+    const int64_t r = i - bz * nbx * nby, by = r / nbx, bx = r - by * nbx;
+    const int64_t b[3] = {bx, by, bz};
+    double pc[3], r2 = 0.0;
+    for (int a = 0; a < 3; a++) {
+      const double e = 0.5 * (double)box * g.h[a];  // half extent: vertices [b box, (b + 1) box]
+      pc[a] = g.lo[a] + ((double)(b[a] * box) + 0.5 * (double)box) * g.h[a];
+      r2 += e * e;
+    }
+    und = field_label_ball(f, pc, sqrt(r2) * (1.0 + 1e-12) + 1e-300) < 0 ? 1u : 0u;
+  }
+  // warp aggregate: a warp's boxes share a box layer except at layer ends
+  const unsigned lane = threadIdx.x & 31;
+  const int64_t bz0 = __shfl_sync(0xffffffffu, bz, 0);
+  const bool same = __all_sync(0xffffffffu, bz == bz0 || i >= n);
+  if (same) {
+    const unsigned t = __reduce_add_sync(0xffffffffu, und);
+    if (lane == 0 && t) atomicAdd(&counts[bz0], (unsigned long long)t);
+  } else if (und) {
+    atomicAdd(&counts[bz], 1ull);
+  }
+}
+void launch_surface_probe(const GridP& g, const FieldP& f, int64_t box, unsigned long long* counts, cudaStream_t s) {
+  const int64_t nbx = (g.R + box - 1) / box, nby = nbx, nbz = (g.R + box - 1) / box;
+  const int64_t n = nbx * nby * nbz;
+  if (n) k_surface_probe<<<grid_for(n, 256), 256, 0, s>>>(g, f, box, nbx, nby, nbz, counts);
 }
 
 }  // namespace odc

@@ -192,6 +192,7 @@ class DeviceField:
         self.handle = ctypes.c_void_p()
         self.error = None
         self.continuous = field_continuous(field)
+        self.analytic = False  # a lowered field program (interval-boundable)
         if is_mlp(field):
             keep = [
                 np.ascontiguousarray(field.weights[0], dtype=np.float32),
@@ -233,6 +234,7 @@ class DeviceField:
                 rc = L.odc_field_callback(ctx.handle, self._fn, None, int(self.continuous),
                                           float(getattr(field, "iso_level", 0.5)), ctypes.byref(self.handle))
             else:
+                self.analytic = True
                 nodes = np.ascontiguousarray(prog)
                 rc = L.odc_field_analytic(ctx.handle, nodes.ctypes.data_as(ctypes.POINTER(_lib.Node)), len(nodes),
                                           int(self.continuous), float(getattr(field, "iso_level", 0.5)),

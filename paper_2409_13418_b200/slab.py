@@ -58,19 +58,53 @@ WORK_PER_CROSSING_MLP = 130.0
 WORK_PER_CROSSING_ANALYTIC = 3000.0
 
 
+def surface_layer_crossings(grid, dfield, device=0):
+    """Crossing edges per cell layer of an analytic field, estimated from the
+    device's surface probe (odc_surface_probe): cubic boxes of B vertices
+    whose interval bound cannot exclude the surface.  A surface patch of
+    area A leaves ~A (1 + sqrt 3) / (B h)^2 boxes undecided (the bound's
+    margin is the box's circumradius) and crosses ~1.5 A / h^2 grid edges,
+    so crossings ~ 0.55 B^2 x undecided boxes, spread over the box layer.
+    Unlike a coarse label probe this sees walls thinner than its spacing
+    (the config-4 thin shell)."""
+    R = int(grid.resolution)
+    box = max(4, R // 64)
+    nbz = -(-R // box)
+    counts = np.zeros(nbz, dtype=np.int64)
+    lo = (ctypes.c_double * 3)(*[float(x) for x in grid.lo])
+    hi = (ctypes.c_double * 3)(*[float(x) for x in grid.hi])
+    ctx = _lib.context(device)
+    _lib.check(_lib.load().odc_surface_probe(ctx.handle, dfield.handle, lo, hi, R, box, counts.ctypes.data),
+               ctx.handle)
+    k = np.zeros(R, dtype=np.float64)
+    for bz in range(nbz):
+        z0, z1 = bz * box, min(R, (bz + 1) * box)
+        k[z0:z1] = 0.55 * box * box * counts[bz] / (z1 - z0)
+    return k
+
+
 def layer_work(field, grid, device=0, nxy=17, nz_max=129, dfield=None):
     """Estimated work of every cell layer, in grid-pass evaluations: S^2
     vertices per layer plus WORK_PER_CROSSING_* per crossing edge.
-    Crossings per layer come from a coarse probe (nxy^2 points on up to
-    nz_max z-planes, evaluated on the device), scaled to the fine grid by
-    the ratio of cell areas.  Deterministic: every rank computes the same
-    estimate, so no communication is needed to agree on slab bounds."""
+    Analytic fields: crossings from the device surface probe
+    (surface_layer_crossings).  Others: crossings per layer from a coarse
+    label probe (nxy^2 points on up to nz_max z-planes, evaluated on the
+    device), scaled to the fine grid by the ratio of cell areas.
+    Deterministic: every rank computes the same estimate, so no
+    communication is needed to agree on slab bounds."""
     from .fields import is_mlp
-    from .pipeline import eval_labels
+    from .pipeline import DeviceField, eval_labels
 
     per_crossing = WORK_PER_CROSSING_MLP if is_mlp(field) else WORK_PER_CROSSING_ANALYTIC
 
     R = int(grid.resolution)
+    if not is_mlp(field):
+        if dfield is not None and getattr(dfield, "analytic", False):
+            return np.full(R, float(R + 1) ** 2) + per_crossing * surface_layer_crossings(grid, dfield, device)
+        if dfield is None:
+            with DeviceField(_lib.context(device), field) as df:
+                if df.analytic:
+                    return np.full(R, float(R + 1) ** 2) + per_crossing * surface_layer_crossings(grid, df, device)
     lo, hi = np.asarray(grid.lo, dtype=np.float64), np.asarray(grid.hi, dtype=np.float64)
     zs = max(1, -(-R // (nz_max - 1)))  # z stride in vertex layers
     zi = np.arange(0, R + 1, zs)
@@ -240,9 +274,12 @@ def rank_label_work(rows):
     return rows[:, nk + 18].astype(np.int64), rows[:, -1].astype(np.float64) / 1e6
 
 
-def probe_bytes(grid, nxy=17, nz_max=129):
-    """Host<->device bytes of layer_work's probe per rank: (H2D points, D2H labels)."""
+def probe_bytes(grid, nxy=17, nz_max=129, analytic=False):
+    """Host<->device bytes of layer_work's probe per rank: (H2D points, D2H
+    labels), or for an analytic field the surface probe's (0, its counts)."""
     R = int(grid.resolution)
+    if analytic:
+        return 0, 8 * -(-R // max(4, R // 64))
     zs = max(1, -(-R // (nz_max - 1)))
     nz = len(range(0, R + 1, zs)) + (0 if R % zs == 0 else 1)
     n = nz * nxy * nxy

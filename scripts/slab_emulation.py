@@ -118,6 +118,7 @@ def main():
                 print(f"  {world} balanced slabs: per-rank slab ms {np.round(times, 2).tolist()}")
                 # distributed finish, ranks from the top down (rank k needs rank k+1's seam)
                 dist_ms, nondisc, seam_next, xbytes = [0.0] * world, 0, None, 0
+                fin_parts = [None] * world
                 for k in reversed(range(world)):
                     c0, c1 = rr[k]
                     sts = _lib.Stats()
@@ -158,6 +159,7 @@ def main():
                         assert L.odc_slab_final(ctx.handle, 0, 0, ptr(halo), ptr(tri), ptr(pv), ptr(pc), ptr(pi)) == 0
                     _, t_final = timed(torch, final_fn, reps=1)
                     dist_ms[k] = times[k] + t_seam + t_local + t_final
+                    fin_parts[k] = (round(t_seam, 3), round(t_local, 3), round(t_final, 3))
                     xbytes = max(xbytes, seam.numel() * 4 + nh_next * 4)
                     seam_next = seam
                 xchg_ms = 2 * xbytes / (a.gather_gbs * 1e9) * 1e3 + 0.05  # two neighbour exchanges + all-gathers
@@ -166,6 +168,7 @@ def main():
                       f"{xchg_ms:.3f} (est) = {dstep:.2f} ms -> speedup {one / dstep:.2f} "
                       f"({one / dstep / world * 100:.0f} % of linear); non-disc fans {nondisc} "
                       f"({'fallback to the central finish' if nondisc else 'distributed path taken'})")
+                print(f"    per-rank finish (seam, local, final) ms: {fin_parts}")
                 print(f"    max slab {max(times):.2f} + globalize {max(gl_ms):.3f} + gather {gather_ms:.3f} "
                       f"({sent / 1e6:.1f} MB at {a.gather_gbs:.0f} GB/s, estimated) + concat {cat_ms:.3f} "
                       f"+ finish {fin_ms:.3f} (V={verts.shape[0]}, T={tris.shape[0]}, +{fst.repair_added_vertices} "

@@ -302,6 +302,61 @@ def test_gpu_contour_slab_two_gpus_nccl(tmp_path):
     _spawn(2, "nccl", tmp_path)
 
 
+@pytest.mark.gpu
+def test_gpu_surface_probe_counts_thin_walls():
+    """odc_surface_probe: the undecided boxes of the interval bound find a
+    wall 2.5 cells thick that a 17x17 label probe misses; the per-layer
+    estimate is zero away from the shell and every box layer the shell
+    spans has work; MLP fields (no interval bound) are rejected."""
+    import ctypes
+
+    from paper_2409_13418_b200 import GridSpec, MlpField, _lib
+    from paper_2409_13418_b200.pipeline import DeviceField
+    from paper_2409_13418_b200.slab import surface_layer_crossings
+
+    R = 256
+    field, lo, hi = scenes.resolve(scenes.thin_shell(R), R)
+    g = GridSpec(lo, hi, R)
+    ctx = _lib.context(0)
+    with DeviceField(ctx, field) as df:
+        assert df.analytic
+        k = surface_layer_crossings(g, df)
+    assert k.shape == (R,) and (k >= 0).all()
+    z = np.nonzero(k)[0]
+    # the rotated shell spans a z-range inside the domain, with empty layers on both sides
+    assert 0 < z[0] and z[-1] < R - 1 and (k[z[0]:z[-1] + 1] > 0).all()
+    # the estimate is within a small factor of the true crossing count
+    from paper_2409_13418_b200 import contour
+    n_true = contour(field, g).stats["n_crossing_edges"]
+    assert 0.3 < k.sum() / n_true < 3.0, (k.sum(), n_true)
+    with DeviceField(ctx, MlpField(seed=0)) as dm:
+        counts = np.zeros(4, dtype=np.int64)
+        l3 = (ctypes.c_double * 3)(0, 0, 0)
+        h3 = (ctypes.c_double * 3)(1, 1, 1)
+        assert _lib.load().odc_surface_probe(ctx.handle, dm.handle, l3, h3, 16, 4, counts.ctypes.data) == _lib.ODC_E_ARG
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [3, 8])
+def test_gpu_balanced_analytic_slabs_equal_single_extraction(world):
+    """Analytic balance (surface probe) on the thin shell: a valid partition,
+    deterministic, and the serial slab mesh equals the single extraction."""
+    from paper_2409_13418_b200 import GridSpec, contour
+    from paper_2409_13418_b200.slab import balanced_slab_ranges, contour_slabs_serial
+
+    R = 96
+    field, lo, hi = scenes.resolve(scenes.thin_shell(R), R)
+    g = GridSpec(lo, hi, R)
+    ranges = balanced_slab_ranges(field, g, world)
+    assert ranges[0][0] == 0 and ranges[-1][1] == R
+    assert all(a < b for a, b in ranges) and all(ranges[k][1] == ranges[k + 1][0] for k in range(world - 1))
+    assert ranges == balanced_slab_ranges(field, g, world)
+    ref = contour(field, g)
+    mesh, _, _ = contour_slabs_serial(field, g, world, ranges=ranges)
+    assert np.array_equal(mesh.triangles, ref.mesh.triangles)
+    assert np.array_equal(mesh.vertices, ref.mesh.vertices)
+
+
 def test_balanced_slab_split_logic(monkeypatch):
     """The split of the cumulative work estimate (host logic; the device probe
     is replaced by a known work profile): equal shares, every rank >= 1 layer."""
