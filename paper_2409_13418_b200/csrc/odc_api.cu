@@ -1019,9 +1019,12 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     co.normals = need(c->arena.get<double>(3 * Ns));
     co.cyc_len = need(c->arena.get<int64_t>(P));
   }
+  double* snorm = co.normals ? co.normals : need(c->arena.get<double>(3 * Ns));
+  int32_t* srow = need(c->arena.get<int32_t>(Ns));
+  uint32_t* psoff = need(c->arena.get<uint32_t>(P + 1));
   launch_cell_solve(g, op, c->L, c->rec, c->cell_id, C, c->table, cfg, pbase, sbase, c->pos1d, c->s2.pos3,
-                    edge_normals, co, dst, c_lo, c_hi, s);
-  check_launch(c);
+                    edge_normals, co, snorm, srow, psoff, P, dst, c_lo, c_hi, P_halo, P_end, s);
+  check_launch(c, 2);
   c->cells = co;
 
   // ---- K7: build_mesh (polygonize.py:110-217) over the owned edges

@@ -1693,25 +1693,28 @@ void launch_cell_config(const GridP& g, const uint32_t* L, RecView rec, const in
 }
 
 constexpr int kSolveBlock = 128;
+// K6 runs in two kernels.  k_cell_samples (one thread per cell) walks the
+// cell's cycles through the table and writes every plane sample's normal
+// (dualize.py:299-317) and 1D-point row, in sample order, plus each
+// partition's first sample; k_part_solve (one thread per partition) sums
+// its samples and solves the QEF (dualize.py:332-372).  One kernel holding a
+// cycle's samples in per-thread arrays kept them in local memory (≈3.9 GB of
+// DRAM traffic at 1024³) and the LAPACK restatement's divergence behind
+// them; here each sample is written once and re-read from L1/L2, and the
+// solve runs one partition per thread with no per-thread arrays.
 template <bool B>
-__global__ void __launch_bounds__(kSolveBlock) k_cell_solve(GridP g, OptP o, const uint32_t* __restrict__ L,
-                                                    RecView rec,
-                                                    const int64_t* __restrict__ cell_id, int64_t C,
-                                                    const CellTabEntry* __restrict__ table,
-                                                    const uint16_t* __restrict__ cfg,
-                                                    const uint32_t* __restrict__ part_base,
-                                                    const uint32_t* __restrict__ samp_base,
-                                                    const double* __restrict__ pos1d, const double* __restrict__ pos3,
-                                                    const double* __restrict__ edge_normals, CellOut out,
-                                                    DevStats* st, int64_t st_lo, int64_t st_hi) {
-  // a cycle's samples (<= 12 edges): normals, 1D-point rows (positions are
-  // re-read from pos1d through L1) and instance ids, in per-thread arrays
-  double xn[36];
-  int32_t xi[24];
-#define NN(j, c) xn[(j) * 3 + (c)]
-#define IID(j) xi[(j)]
-#define ROW(j) xi[12 + (j)]
-#define PE(j, c) __ldg(pos1d + 3 * (int64_t)ROW(j) + (c))
+__global__ void __launch_bounds__(kSolveBlock) k_cell_samples(GridP g, OptP o, const uint32_t* __restrict__ L,
+                                                      RecView rec, const int64_t* __restrict__ cell_id, int64_t C,
+                                                      const CellTabEntry* __restrict__ table,
+                                                      const uint16_t* __restrict__ cfg,
+                                                      const uint32_t* __restrict__ part_base,
+                                                      const uint32_t* __restrict__ samp_base,
+                                                      const double* __restrict__ pos1d,
+                                                      const double* __restrict__ pos3,
+                                                      const double* __restrict__ edge_normals, CellOut out,
+                                                      double* __restrict__ snorm, int32_t* __restrict__ srow,
+                                                      uint32_t* __restrict__ psoff, DevStats* st, int64_t st_lo,
+                                                      int64_t st_hi) {
   int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (ci >= C) return;
   const int64_t cell = cell_id[ci];
@@ -1724,43 +1727,46 @@ __global__ void __launch_bounds__(kSolveBlock) k_cell_solve(GridP g, OptP o, con
   double hmin = g.h[0] < g.h[1] ? g.h[0] : g.h[1];
   hmin = hmin < g.h[2] ? hmin : g.h[2];
   uint32_t nfb = 0;
-  uint32_t rank_cnt = 0;  // 8-bit count per QEF rank 0..3
-  double max_res = 0.0;
   int slot = 0;
+  // instance id of the cycle's j-th instance (instance j joins edge j and j+1)
+  auto iid = [&](int j) -> int64_t {
+    const int code = (int)((T.insts >> (4 * (slot + j))) & 15);
+    const int f = code >> 1, s = code & 1;
+    const int fc = c_LF_CORNER[f];
+    return inst_rank_c(rec, g, cc[0] + (fc & 1), cc[1] + ((fc >> 1) & 1), cc[2] + ((fc >> 2) & 1), c_LF_NORMAL[f]) +
+           s;
+  };
   for (int k = 0; k < T.ncyc; k++) {
     const int len = (T.lens >> (4 * k)) & 15;
-    // instance ids of the cycle (instance j joins edge j and j+1)
+    const int64_t pid = pbase + k;
+    psoff[pid] = (uint32_t)(sbase + slot);
+    out.part_cell[pid] = cell;
+    out.part_index[pid] = k;
+    if (out.cyc_len) out.cyc_len[pid] = len;
+    int64_t ia = len > 0 ? iid(len - 1) : 0;  // instance before edge 0 (cyclic)
     for (int j = 0; j < len; j++) {
-      const int code = (int)((T.insts >> (4 * (slot + j))) & 15);
-      const int f = code >> 1, s = code & 1;
-      const int fc = c_LF_CORNER[f];
-      IID(j) = (int32_t)(inst_rank_c(rec, g, cc[0] + (fc & 1), cc[1] + ((fc >> 1) & 1), cc[2] + ((fc >> 2) & 1),
-                                     c_LF_NORMAL[f]) + s);
-    }
-    for (int j = 0; j < len; j++) {
+      const int64_t ib = iid(j);
       const int le = (int)((T.edges >> (4 * (slot + j))) & 15);
       const int ec = c_LE_CORNER[le];
       const int ax = c_LE_AXIS[le];
       const int64_t ex = cc[0] + (ec & 1), ey = cc[1] + ((ec >> 1) & 1), ez = cc[2] + ((ec >> 2) & 1);
       const int64_t row = edge_rank_c(rec, g, ex, ey, ez, ax);
-      double pj[3];
-      ROW(j) = (int32_t)row;
-      for (int c = 0; c < 3; c++) pj[c] = pos1d[3 * row + c];
+      const int64_t sj = sbase + slot + j;
+      srow[sj] = (int32_t)row;
       if (out.cyc_edges) {
-        out.cyc_edges[sbase + slot + j] = (ex + ey * g.S + ez * g.S2) * 3 + ax;
-        out.cyc_insts[sbase + slot + j] = IID(j);
+        out.cyc_edges[sj] = (ex + ey * g.S + ez * g.S2) * 3 + ax;
+        out.cyc_insts[sj] = ib;
       }
-      // edge direction p_out - p_in (dualize.py:421-423)
-      double pi[3], po[3], ed[3];
-      const bool base_in = label_c(L, g, ex, ey, ez) == 1u;
-      const int64_t ox = ex + (ax == 0), oy = ey + (ax == 1), oz = ez + (ax == 2);  // the edge's other end
-      vposition_c(g, base_in ? ex : ox, base_in ? ey : oy, base_in ? ez : oz, pi);
-      vposition_c(g, base_in ? ox : ex, base_in ? oy : ey, base_in ? oz : ez, po);
-      for (int c = 0; c < 3; c++) ed[c] = po[c] - pi[c];
       double n[3];
       if (o.normals == ODC_NORMALS_2D) {
-        // estimate_normals (dualize.py:299-317)
-        const int64_t ia = IID((j - 1 + len) % len), ib = IID(j);
+        // estimate_normals (dualize.py:299-317), edge direction p_out - p_in (dualize.py:421-423)
+        double pj[3], pi[3], po[3], ed[3];
+        for (int c = 0; c < 3; c++) pj[c] = pos1d[3 * row + c];
+        const bool base_in = label_c(L, g, ex, ey, ez) == 1u;
+        const int64_t ox = ex + (ax == 0), oy = ey + (ax == 1), oz = ez + (ax == 2);  // the edge's other end
+        vposition_c(g, base_in ? ex : ox, base_in ? ey : oy, base_in ? ez : oz, pi);
+        vposition_c(g, base_in ? ox : ex, base_in ? oy : ey, base_in ? oz : ez, po);
+        for (int c = 0; c < 3; c++) ed[c] = po[c] - pi[c];
         double da[3], db[3];
         for (int c = 0; c < 3; c++) {
           da[c] = pos3[3 * ia + c] - pj[c];
@@ -1781,95 +1787,109 @@ __global__ void __launch_bounds__(kSolveBlock) k_cell_solve(GridP g, OptP o, con
       } else {
         for (int c = 0; c < 3; c++) n[c] = edge_normals[3 * row + c];
       }
-      for (int c = 0; c < 3; c++) NN(j, c) = n[c];
-      if (out.normals)
-        for (int c = 0; c < 3; c++) out.normals[3 * (sbase + slot + j) + c] = n[c];
-    }
-    // solve_qef_batch (dualize.py:332-372), sums sequential in cycle order
-    const double cnt = (double)(len < 1 ? 1 : len);
-    double cen[3] = {0.0, 0.0, 0.0};
-    for (int j = 0; j < len; j++)
-      for (int c = 0; c < 3; c++) cen[c] += PE(j, c);
-    for (int c = 0; c < 3; c++) cen[c] /= cnt;
-    double A[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, b[3] = {0.0, 0.0, 0.0};
-    for (int j = 0; j < len; j++) {
-      const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
-      for (int r = 0; r < 3; r++)
-        for (int c = 0; c < 3; c++) A[3 * r + c] += nj[r] * nj[c];
-    }
-    for (int j = 0; j < len; j++) {
-      const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
-      const double d[3] = {PE(j, 0) - cen[0], PE(j, 1) - cen[1], PE(j, 2) - cen[2]};
-      const double off = einsum3(nj, d);
-      for (int c = 0; c < 3; c++) b[c] += nj[c] * off;
-    }
-    double w[3], V[9];
-    odc_eigh3(A, w, V);  // np.linalg.eigh (dualize.py:358), LAPACK dsyevd bit for bit
-    double sv[3];
-    for (int kk = 0; kk < 3; kk++) sv[kk] = sqrt(w[kk] > 0.0 ? w[kk] : 0.0);
-    const double smax = sv[2];
-    const double thr = o.qef_trunc * (smax > 1e-300 ? smax : 1e-300);
-    bool keep[3];
-    int rank = 0;
-    for (int kk = 0; kk < 3; kk++) {
-      keep[kk] = (sv[kk] >= thr) && (smax > 0.0);
-      rank += keep[kk];
-    }
-    double coef[3], y[3], sol[3];
-    for (int j = 0; j < 3; j++) coef[j] = (V[j] * b[0] + V[3 + j] * b[1]) + V[6 + j] * b[2];
-    for (int j = 0; j < 3; j++) y[j] = keep[j] ? coef[j] / w[j] : 0.0;
-    for (int i = 0; i < 3; i++) sol[i] = (V[3 * i] * y[0] + V[3 * i + 2] * y[2]) + V[3 * i + 1] * y[1];
-    double pos[3];
-    for (int c = 0; c < 3; c++) {
-      const double blo = gpos(g, c, cc[c]);  // cell_bounds (grid.py:89-91): lo + i h
-      const double bhi = blo + g.h[c];
-      double x = cen[c] + sol[c];
-      x = x > blo ? x : blo;  // np.clip
-      x = x < bhi ? x : bhi;
-      pos[c] = x;
-    }
-    double res = 0.0;
-    for (int j = 0; j < len; j++) {
-      const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
-      const double d[3] = {pos[0] - PE(j, 0), pos[1] - PE(j, 1), pos[2] - PE(j, 2)};
-      const double e = einsum3(nj, d);
-      res += e * e;
-    }
-    const int64_t pid = pbase + k;
-    for (int c = 0; c < 3; c++) out.verts[3 * pid + c] = pos[c];
-    out.part_cell[pid] = cell;
-    out.part_index[pid] = k;
-    if (out.cyc_len) out.cyc_len[pid] = len;
-    if (out.rank) out.rank[pid] = rank;
-    if (out.resid) out.resid[pid] = res;
-    if (ci >= st_lo && ci < st_hi) {
-      rank_cnt += 1u << (8 * rank);  // (partitions per cell <= 4: bytes never carry)
-      max_res = !(res <= max_res) ? res : max_res;  // NaN wins, as it did under atomicMax of the bits
+      for (int c = 0; c < 3; c++) snorm[3 * sj + c] = n[c];
+      ia = ib;
     }
     slot += len;
   }
-  const bool own = ci >= st_lo && ci < st_hi;
-#pragma unroll
-  for (int v = 0; v < 4; v++) warp_count<B>(&st->rank[v], own ? (rank_cnt >> (8 * v)) & 255u : 0u);
-  warp_max_nonneg_double<B>(&st->max_resid_bits, own ? max_res : 0.0);
-  warp_count<B>(&st->normal_fallbacks, own ? (unsigned)nfb : 0u);
+  if (ci == C - 1) psoff[pbase + T.ncyc] = (uint32_t)(sbase + slot);  // psoff[P] = Ns
+  warp_count<B>(&st->normal_fallbacks, ci >= st_lo && ci < st_hi ? (unsigned)nfb : 0u);
 }
+
+// solve_qef_batch (dualize.py:332-372) of partition pid: sums sequential in
+// cycle order, then np.linalg.eigh (LAPACK dsyevd bit for bit), the
+// truncated pseudo-inverse, the clip to the cell, the residual
+template <bool B>
+__global__ void __launch_bounds__(kSolveBlock) k_part_solve(GridP g, OptP o, int64_t P,
+                                                    const double* __restrict__ pos1d,
+                                                    const double* __restrict__ snorm,
+                                                    const int32_t* __restrict__ srow,
+                                                    const uint32_t* __restrict__ psoff, CellOut out, DevStats* st,
+                                                    int64_t own_lo, int64_t own_hi) {
+  const int64_t pid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pid >= P) return;
+  const int64_t s0 = psoff[pid];
+  const int len = (int)(psoff[pid + 1] - s0);
+  const int64_t cell = out.part_cell[pid];
+  const int64_t cc[3] = {imod(cell, g.R), imod(idiv(cell, g.R), g.R), idiv(cell, g.R * g.R)};
+  if constexpr (B) st += localize<B>(g, cc[2]);
+#define PE(j, c) __ldg(pos1d + 3 * (int64_t)srow[s0 + (j)] + (c))
+#define NN(j, c) snorm[3 * (s0 + (j)) + (c)]
+  const double cnt = (double)(len < 1 ? 1 : len);
+  double cen[3] = {0.0, 0.0, 0.0};
+  for (int j = 0; j < len; j++)
+    for (int c = 0; c < 3; c++) cen[c] += PE(j, c);
+  for (int c = 0; c < 3; c++) cen[c] /= cnt;
+  double A[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, b[3] = {0.0, 0.0, 0.0};
+  for (int j = 0; j < len; j++) {  // A and b accumulate independently, each in cycle order
+    const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
+    for (int r = 0; r < 3; r++)
+      for (int c = 0; c < 3; c++) A[3 * r + c] += nj[r] * nj[c];
+    const double d[3] = {PE(j, 0) - cen[0], PE(j, 1) - cen[1], PE(j, 2) - cen[2]};
+    const double off = einsum3(nj, d);
+    for (int c = 0; c < 3; c++) b[c] += nj[c] * off;
+  }
+  double w[3], V[9];
+  odc_eigh3(A, w, V);  // np.linalg.eigh (dualize.py:358), LAPACK dsyevd bit for bit
+  double sv[3];
+  for (int kk = 0; kk < 3; kk++) sv[kk] = sqrt(w[kk] > 0.0 ? w[kk] : 0.0);
+  const double smax = sv[2];
+  const double thr = o.qef_trunc * (smax > 1e-300 ? smax : 1e-300);
+  bool keep[3];
+  int rank = 0;
+  for (int kk = 0; kk < 3; kk++) {
+    keep[kk] = (sv[kk] >= thr) && (smax > 0.0);
+    rank += keep[kk];
+  }
+  double coef[3], y[3], sol[3];
+  for (int j = 0; j < 3; j++) coef[j] = (V[j] * b[0] + V[3 + j] * b[1]) + V[6 + j] * b[2];
+  for (int j = 0; j < 3; j++) y[j] = keep[j] ? coef[j] / w[j] : 0.0;
+  for (int i = 0; i < 3; i++) sol[i] = (V[3 * i] * y[0] + V[3 * i + 2] * y[2]) + V[3 * i + 1] * y[1];
+  double pos[3];
+  for (int c = 0; c < 3; c++) {
+    const double blo = gpos(g, c, cc[c]);  // cell_bounds (grid.py:89-91): lo + i h
+    const double bhi = blo + g.h[c];
+    double x = cen[c] + sol[c];
+    x = x > blo ? x : blo;  // np.clip
+    x = x < bhi ? x : bhi;
+    pos[c] = x;
+  }
+  double res = 0.0;
+  for (int j = 0; j < len; j++) {
+    const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
+    const double d[3] = {pos[0] - PE(j, 0), pos[1] - PE(j, 1), pos[2] - PE(j, 2)};
+    const double e = einsum3(nj, d);
+    res += e * e;
+  }
 #undef PE
 #undef NN
-#undef IID
-#undef ROW
+  for (int c = 0; c < 3; c++) out.verts[3 * pid + c] = pos[c];
+  if (out.rank) out.rank[pid] = rank;
+  if (out.resid) out.resid[pid] = res;
+  const bool own = pid >= own_lo && pid < own_hi;
+  warp_count4<B>(st->rank, rank, own);
+  warp_max_nonneg_double<B>(&st->max_resid_bits, own && !(res <= 0.0) ? res : 0.0);  // NaN wins
+}
 
 void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, RecView rec, const int64_t* cell_id,
                        int64_t C, const CellTabEntry* table, const uint16_t* cfg, const uint32_t* part_base,
                        const uint32_t* samp_base, const double* pos1d, const double* pos3, const double* edge_normals,
-                       CellOut out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s) {
+                       CellOut out, double* snorm, int32_t* srow, uint32_t* psoff, int64_t P, DevStats* st,
+                       int64_t st_lo, int64_t st_hi, int64_t own_lo, int64_t own_hi, cudaStream_t s) {
   if (!C) return;
-  if (g.nb)
-    k_cell_solve<true><<<grid_for(C, kSolveBlock), kSolveBlock, 0, s>>>(
-        g, o, L, rec, cell_id, C, table, cfg, part_base, samp_base, pos1d, pos3, edge_normals, out, st, st_lo, st_hi);
-  else
-    k_cell_solve<false><<<grid_for(C, kSolveBlock), kSolveBlock, 0, s>>>(
-        g, o, L, rec, cell_id, C, table, cfg, part_base, samp_base, pos1d, pos3, edge_normals, out, st, st_lo, st_hi);
+  if (g.nb) {
+    k_cell_samples<true><<<grid_for(C, kSolveBlock), kSolveBlock, 0, s>>>(
+        g, o, L, rec, cell_id, C, table, cfg, part_base, samp_base, pos1d, pos3, edge_normals, out, snorm, srow,
+        psoff, st, st_lo, st_hi);
+    if (P) k_part_solve<true><<<grid_for(P, kSolveBlock), kSolveBlock, 0, s>>>(g, o, P, pos1d, snorm, srow, psoff,
+                                                                              out, st, own_lo, own_hi);
+  } else {
+    k_cell_samples<false><<<grid_for(C, kSolveBlock), kSolveBlock, 0, s>>>(
+        g, o, L, rec, cell_id, C, table, cfg, part_base, samp_base, pos1d, pos3, edge_normals, out, snorm, srow,
+        psoff, st, st_lo, st_hi);
+    if (P) k_part_solve<false><<<grid_for(P, kSolveBlock), kSolveBlock, 0, s>>>(g, o, P, pos1d, snorm, srow, psoff,
+                                                                               out, st, own_lo, own_hi);
+  }
 }
 
 // generic multi-channel exclusive scan over u32 arrays (<= 2 channels)

@@ -146,10 +146,15 @@ struct CellOut {
 // numpy.linalg.eigh for a batch of symmetric 3x3 matrices (odc_eigh3.cu)
 void launch_eigh3_batch(const double* A, int64_t n, double* w, double* V, int32_t* info, cudaStream_t s);
 void eigh3_host_batch(const double* A, int64_t n, double* w, double* V, int32_t* info);
+// K6 (two kernels, see odc_kernels.cu): snorm (Ns,3) / srow (Ns) sample
+// scratch, psoff (P + 1) first sample of every partition (psoff[P] = Ns is
+// set by the caller); statistics of cells [st_lo, st_hi) / partitions
+// [own_lo, own_hi)
 void launch_cell_solve(const GridP& g, const OptP& o, const uint32_t* L, RecView rec, const int64_t* cell_id,
                        int64_t C, const CellTabEntry* table, const uint16_t* cfg, const uint32_t* part_base,
                        const uint32_t* samp_base, const double* pos1d, const double* pos3, const double* edge_normals,
-                       CellOut out, DevStats* st, int64_t st_lo, int64_t st_hi, cudaStream_t s);
+                       CellOut out, double* snorm, int32_t* srow, uint32_t* psoff, int64_t P, DevStats* st,
+                       int64_t st_lo, int64_t st_hi, int64_t own_lo, int64_t own_hi, cudaStream_t s);
 
 // K7: polygonization (polygonize.py:110-217)
 void launch_poly_classify(const GridP& g, const OptP& o, const uint32_t* L, RecView rec,
