@@ -1800,7 +1800,7 @@ __global__ void __launch_bounds__(kSolveBlock) k_cell_samples(GridP g, OptP o, c
 // cycle order, then np.linalg.eigh (LAPACK dsyevd bit for bit), the
 // truncated pseudo-inverse, the clip to the cell, the residual
 template <bool B>
-__global__ void __launch_bounds__(kSolveBlock) k_part_solve(GridP g, OptP o, int64_t P,
+__global__ void __launch_bounds__(kSolveBlock, 8) k_part_solve(GridP g, OptP o, int64_t P,
                                                     const double* __restrict__ pos1d,
                                                     const double* __restrict__ snorm,
                                                     const int32_t* __restrict__ srow,
