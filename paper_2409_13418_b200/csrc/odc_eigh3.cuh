@@ -34,10 +34,14 @@
 #include <math.h>
 #include <stdint.h>
 
+// ODC_EIGH_COLD: out of line on the device (helpers called from several
+// sites: rotations, 2x2 eigensystems, scalings are kept once).
 #ifdef __CUDACC__
 #define ODC_EIGH_FN static __host__ __device__ __forceinline__
+#define ODC_EIGH_COLD static __host__ __device__ __noinline__
 #else
 #define ODC_EIGH_FN static inline
+#define ODC_EIGH_COLD static inline
 #endif
 
 namespace odc_eigh {
@@ -54,7 +58,7 @@ ODC_EIGH_FN double f_max(double a, double b) { return a > b ? a : b; }
 ODC_EIGH_FN double f_min(double a, double b) { return a < b ? a : b; }
 
 // dlapy2 (LAPACK 3.10+, with the NaN guards)
-ODC_EIGH_FN double dlapy2(double x, double y) {
+ODC_EIGH_COLD double dlapy2(double x, double y) {
   if (isnan(y)) return y;
   if (isnan(x)) return x;
   const double xa = fabs(x), ya = fabs(y);
@@ -65,7 +69,7 @@ ODC_EIGH_FN double dlapy2(double x, double y) {
 }
 
 // dlascl('G'): multiply n values by cto/cfrom without over/underflow
-ODC_EIGH_FN void dlascl(double cfrom, double cto, int n, double* a) {
+ODC_EIGH_COLD void dlascl(double cfrom, double cto, int n, double* a) {
   const double smlnum = kSafMin, bignum = 1.0 / smlnum;
   double cfromc = cfrom, ctoc = cto;
   bool done = false;
@@ -98,7 +102,11 @@ ODC_EIGH_FN void dlascl(double cfrom, double cto, int n, double* a) {
 }
 
 // dlartg (LAPACK 3.10+ Fortran 90 version)
-ODC_EIGH_FN void dlartg(double f, double g, double& c, double& s, double& r) {
+struct Rot {
+  double c, s, r;
+};
+ODC_EIGH_COLD Rot dlartg(double f, double g) {
+  double c, s, r;
   const double safmin = kSafMin, safmax = 1.0 / kSafMin;
   const double rtmin = sqrt(safmin), rtmax = sqrt(safmax / 2.0);
   const double f1 = fabs(f), g1 = fabs(g);
@@ -124,10 +132,15 @@ ODC_EIGH_FN void dlartg(double f, double g, double& c, double& s, double& r) {
     s = gs / r;
     r = r * u;
   }
+  return Rot{c, s, r};
 }
 
 // dlaev2: eigensystem of [[a, b], [b, c]]
-ODC_EIGH_FN void dlaev2(double a, double b, double c, double& rt1, double& rt2, double& cs1, double& sn1) {
+struct Eig2 {
+  double rt1, rt2, cs1, sn1;
+};
+ODC_EIGH_COLD Eig2 dlaev2(double a, double b, double c) {
+  double rt1, rt2, cs1, sn1;
   const double sm = a + c, df = a - c, adf = fabs(df), tb = b + b, ab = fabs(tb);
   double acmx, acmn, rt;
   if (fabs(a) > fabs(c)) {
@@ -185,11 +198,12 @@ ODC_EIGH_FN void dlaev2(double a, double b, double c, double& rt1, double& rt2, 
     cs1 = -sn1;
     sn1 = tn;
   }
+  return Eig2{rt1, rt2, cs1, sn1};
 }
 
 // dlasr('R', 'V', 'B' | 'F'): rotations (c[j], s[j]) on columns (j, j+1) of
 // the 3-row column-major block z (mm columns)
-ODC_EIGH_FN void dlasr_rv(bool backward, int mm, const double* c, const double* s, double* z) {
+ODC_EIGH_COLD void dlasr_rv(bool backward, int mm, const double* c, const double* s, double* z) {
   for (int k = 0; k < mm - 1; k++) {
     const int j = backward ? mm - 2 - k : k;
     const double ct = c[j], st = s[j];
@@ -283,7 +297,11 @@ ODC_EIGH_FN int dsteqr3(double* d, double* e, double* Z) {
           break;
         }
         if (m == l + 1) {
-          dlaev2(d[l], e[l], d[l + 1], rt1, rt2, c, s);
+          const Eig2 ev = dlaev2(d[l], e[l], d[l + 1]);
+          rt1 = ev.rt1;
+          rt2 = ev.rt2;
+          c = ev.cs1;
+          s = ev.sn1;
           wk[l] = c;
           wk[n - 1 + l] = s;
           dlasr_rv(true, 2, &wk[l], &wk[n - 1 + l], Z + 3 * (l - 1));
@@ -305,7 +323,10 @@ ODC_EIGH_FN int dsteqr3(double* d, double* e, double* Z) {
         for (int i = m - 1; i >= l; i--) {
           f = s * e[i];
           b = c * e[i];
-          dlartg(g, f, c, s, r);
+          const Rot rt = dlartg(g, f);
+          c = rt.c;
+          s = rt.s;
+          r = rt.r;
           if (i != m - 1) e[i + 1] = r;
           g = d[i + 1] - p;
           r = (d[i] - g) * s + 2.0 * c * b;
@@ -341,7 +362,11 @@ ODC_EIGH_FN int dsteqr3(double* d, double* e, double* Z) {
           break;
         }
         if (m == l - 1) {
-          dlaev2(d[l - 1], e[l - 1], d[l], rt1, rt2, c, s);
+          const Eig2 ev = dlaev2(d[l - 1], e[l - 1], d[l]);
+          rt1 = ev.rt1;
+          rt2 = ev.rt2;
+          c = ev.cs1;
+          s = ev.sn1;
           wk[m] = c;
           wk[n - 1 + m] = s;
           dlasr_rv(false, 2, &wk[m], &wk[n - 1 + m], Z + 3 * (l - 2));
@@ -363,7 +388,10 @@ ODC_EIGH_FN int dsteqr3(double* d, double* e, double* Z) {
         for (int i = m; i <= l - 1; i++) {
           f = s * e[i];
           b = c * e[i];
-          dlartg(g, f, c, s, r);
+          const Rot rt = dlartg(g, f);
+          c = rt.c;
+          s = rt.s;
+          r = rt.r;
           if (i != m) e[i - 1] = r;
           g = d[i] - p;
           r = (d[i + 1] - g) * s + 2.0 * c * b;
