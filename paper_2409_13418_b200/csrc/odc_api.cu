@@ -675,40 +675,51 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   // owned element ranges: rows are in key order, so ownership by base layer
   // is a contiguous row range [lo, hi) read from the word ranks
   int64_t e_lo = 0, e_hi = K, q_lo = 0, q_hi = Q, c_lo = 0, c_hi = C, f_own = Fn, f4_own = F4;
-  if (!g.nb && (win.slab || g.z0 != 0 || g.nz != g.S)) {
-    const int64_t ztop = g.z0 + g.nz - 1;
-    unsigned long long* pre = need(c->arena.get<unsigned long long>(6));
+  int64_t K_own = K, Q_own = Q;
+  const bool window = !g.nb && (win.slab || g.z0 != 0 || g.nz != g.S);
+  const bool win_top = g.own1 <= g.z0 + g.nz - 1;
+  unsigned long long* pre = nullptr;
+  if (window) {  // read back with the partition totals (window_ranges, one synchronisation)
+    pre = need(c->arena.get<unsigned long long>(8));
     launch_prefix_at(c->rec, (g.own0 - g.z0) * g.S * g.W, A, totals, pre, s);
     check_launch(c);
-    if (g.own1 <= ztop) {
+    if (win_top) {
       launch_prefix_at(c->rec, (g.own1 - g.z0) * g.S * g.W, A, totals, pre + 3, s);
       check_launch(c);
     }
     launch_count_owned_faces(g, c->rec, dst, s);
     check_launch(c);
-    unsigned long long* h = c->h_pinned;
-    CUDA_TRY(cudaMemcpyAsync(&h[0], pre, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(&h[6], &dst->faces_own, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    e_lo = (int64_t)h[0];
-    q_lo = (int64_t)h[1];
-    c_lo = (int64_t)h[2];
-    if (g.own1 <= ztop) {
-      e_hi = (int64_t)h[3];
-      q_hi = (int64_t)h[4];
-      c_hi = (int64_t)h[5];
-    }
-    f_own = (int64_t)h[6];
-    f4_own = (int64_t)h[7];
+    CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[300], pre, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[306], &dst->faces_own, 2 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
   }
-  c->e_lo = e_lo;
-  c->e_hi = e_hi;
-  c->c_lo = c_lo;
-  c->c_hi = c_hi;
-  const int64_t K_own = e_hi - e_lo, Q_own = q_hi - q_lo;
-  st->n_crossing_edges = K_own;
-  st->n_crossing_faces = f_own;
-  st->n_crossing_cells = c_hi - c_lo;
+  // owned element ranges: rows are in key order, so ownership by base layer
+  // is a contiguous row range [lo, hi) read from the word ranks; call after
+  // a synchronisation of the stream
+  auto window_ranges = [&]() {
+    if (window) {
+      const unsigned long long* h = c->h_pinned + 300;
+      e_lo = (int64_t)h[0];
+      q_lo = (int64_t)h[1];
+      c_lo = (int64_t)h[2];
+      if (win_top) {
+        e_hi = (int64_t)h[3];
+        q_hi = (int64_t)h[4];
+        c_hi = (int64_t)h[5];
+      }
+      f_own = (int64_t)h[6];
+      f4_own = (int64_t)h[7];
+    }
+    c->e_lo = e_lo;
+    c->e_hi = e_hi;
+    c->c_lo = c_lo;
+    c->c_hi = c_hi;
+    K_own = e_hi - e_lo;
+    Q_own = q_hi - q_lo;
+    st->n_crossing_edges = K_own;
+    st->n_crossing_faces = f_own;
+    st->n_crossing_cells = c_hi - c_lo;
+  };
 
   auto finish_stats = [&]() {
     if (f->kind == 2) check_surface(c);  // only the winding field raises through d_fail
@@ -749,6 +760,8 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   };
 
   if (K == 0) {  // pipeline.py:174-179
+    if (window) CUDA_TRY(cudaStreamSynchronize(s));
+    window_ranges();
     c->P = c->NF = c->T = c->V0 = c->V1 = c->Ns = c->n_interior = 0;
     c->P_halo = c->P_own = 0;
     c->prov_kind_in = c->prov_ref_in = nullptr;
@@ -761,8 +774,11 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   }
 
   // ---- face_pairings probes (dualize.py:59-70)
-  auto face_probes = [&]() {
-    if (F4) {
+  // run: the probes themselves (they set the 4-crossing faces' pairing bits
+  // in the word records, which the cell configurations read); rec: their
+  // eval accounting, in the reference's category order
+  auto face_probes = [&](bool run, bool rec) {
+    if (run && F4) {
       if (!mlp) {
         launch_face_center_analytic(g, fp, c->f4_key, F4, c->rec, s);
         check_launch(c);
@@ -776,11 +792,13 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
         check_launch(c);
       }
     }
+    if (!rec) return;
     if (f4_own) record(st, ODC_CAT_PROBE_FACE_CENTER, 1, f4_own);
     st->n_face_center_probes = f4_own;
   };
 
   if (o->method) {  // ---- marching-cubes baseline (baseline.py:48-127)
+    window_ranges();  // whole grid (checked above): nothing pending
     mark(2);
     double* mcpos = need(c->arena.get<double>(3 * K));
     double *raw_in = nullptr, *raw_out = nullptr;
@@ -801,7 +819,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     check_launch(c);
     c->t1d = nullptr;
     c->pos1d = mcpos;
-    face_probes();
+    face_probes(true, true);
     mark(3);
     mark(4);
     uint16_t* cfg = need(c->arena.get<uint16_t>(C));
@@ -837,6 +855,31 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
     c->valid = true;
     return;
   }
+
+  // ---- K6, first half: per-cell configurations and the partition / plane
+  // sample totals (dualize.py:194-238).  They need only the labels and the
+  // word records, so they run before the searches: their readback also
+  // brings the window's owned ranges and the halo / owned partition bounds
+  // (one synchronisation instead of three).
+  face_probes(true, false);
+  uint16_t* cfg = need(c->arena.get<uint16_t>(C));
+  uint32_t* ncyc = need(c->arena.get<uint32_t>(C));
+  uint32_t* nsamp = need(c->arena.get<uint32_t>(C));
+  uint32_t* pbase = need(c->arena.get<uint32_t>(C + 1));
+  c->pbase = pbase;
+  uint32_t* sbase = need(c->arena.get<uint32_t>(C + 1));
+  launch_cell_config(g, c->L, c->rec, c->cell_id, C, c->table, cfg, ncyc, nsamp, s);
+  check_launch(c);
+  scan2(c, ncyc, nsamp, pbase, sbase, C, totals);
+  if (window) {
+    launch_part_bounds(pbase, C, pre, win_top, totals, pre + 6, s);
+    check_launch(c);
+    CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[308], pre + 6, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  }
+  readback(c, totals, 2 * sizeof(unsigned long long));
+  const int64_t P = (int64_t)c->h_pinned[0], Ns = (int64_t)c->h_pinned[1];
+  window_ranges();
+  const int64_t P_halo = window ? (int64_t)c->h_pinned[308] : 0, P_end = window ? (int64_t)c->h_pinned[309] : P;
 
   // ---- K3: 1D points (pipeline.py:94-123, search.py:71-94)
   mark(2);
@@ -877,7 +920,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   }
   if (op.one_d == ODC_ONE_D_BINARY) record(st, ODC_CAT_SEARCH_1D, op.iters_1d, (int64_t)op.iters_1d * K_own);
 
-  face_probes();
+  face_probes(false, true);
 
   // ---- normals: 2D points (search.py:194-322) or fd gradient (pipeline.py:126-151)
   mark(3);
@@ -951,7 +994,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
                                       s);
       check_launch(c);
     }
-    status_pending = dstat;  // raised at the next readback (partition totals), before anything uses the points
+    status_pending = dstat;  // raised at the triangle-total readback, before the mesh is built
     record(st, ODC_CAT_PROBE_FACE_MIDPOINT, 1, Q_own);
     record(st, ODC_CAT_SEARCH_2D, op.s1_lin + op.s1_bin + op.s2_lin + op.s2_bin,
            (int64_t)(op.s1_lin + op.s1_bin) * Q_own + (int64_t)(op.s2_lin + op.s2_bin) * 2 * Q_own);
@@ -978,27 +1021,6 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
 
   // ---- K6: partitions + plane samples + QEF (dualize.py:194-444)
   mark(4);
-  uint16_t* cfg = need(c->arena.get<uint16_t>(C));
-  uint32_t* ncyc = need(c->arena.get<uint32_t>(C));
-  uint32_t* nsamp = need(c->arena.get<uint32_t>(C));
-  uint32_t* pbase = need(c->arena.get<uint32_t>(C + 1));
-  c->pbase = pbase;
-  uint32_t* sbase = need(c->arena.get<uint32_t>(C + 1));
-  launch_cell_config(g, c->L, c->rec, c->cell_id, C, c->table, cfg, ncyc, nsamp, s);
-  check_launch(c);
-  scan2(c, ncyc, nsamp, pbase, sbase, C, totals);
-  readback_checked(c, totals, 2 * sizeof(unsigned long long), status_pending);
-  const int64_t P = (int64_t)c->h_pinned[0], Ns = (int64_t)c->h_pinned[1];
-  int64_t P_halo = 0, P_end = P;  // partitions of the halo cell layer come first
-  if (c_lo > 0 || c_hi < C) {
-    uint32_t* hp = reinterpret_cast<uint32_t*>(c->h_pinned);
-    hp[0] = hp[1] = 0;
-    if (c_lo > 0 && c_lo < C) CUDA_TRY(cudaMemcpyAsync(&hp[0], pbase + c_lo, 4, cudaMemcpyDeviceToHost, s));
-    if (c_hi < C) CUDA_TRY(cudaMemcpyAsync(&hp[1], pbase + c_hi, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    P_halo = c_lo >= C ? P : (int64_t)hp[0];
-    P_end = c_hi < C ? (int64_t)hp[1] : P;
-  }
   c->P = P;
   c->Ns = Ns;
   c->P_halo = P_halo;
@@ -1042,7 +1064,7 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   launch_poly_classify(g, op, c->L, c->rec, ekey, K_own, co.pinfo, verts, pid4, c->kase, ntri, nfan, dst, s);
   check_launch(c);
   scan2(c, ntri, nfan, toff, frank, K_own, totals);
-  readback(c, totals, 2 * sizeof(unsigned long long));
+  readback_checked(c, totals, 2 * sizeof(unsigned long long), status_pending);  // the 2D status is raised first
   const int64_t T = (int64_t)c->h_pinned[0], NF = (int64_t)c->h_pinned[1];
   c->T = T;
   c->NF = NF;

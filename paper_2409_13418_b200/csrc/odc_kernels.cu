@@ -586,6 +586,21 @@ void launch_prefix_at(RecView rv, int64_t w, int64_t A, const unsigned long long
   k_prefix_at<<<1, 1, 0, s>>>(rv, w, A, totals, out);
 }
 
+// first partition of the window's owned cells and the end of them: pbase at
+// the owned cell rows c_lo = pre[2], c_hi = pre[5] (or C without a top
+// bound), P = the partition total past the last cell
+__global__ void k_part_bounds(const uint32_t* __restrict__ pbase, int64_t C, const unsigned long long* __restrict__ pre,
+                              int has_hi, const unsigned long long* __restrict__ totals, unsigned long long* out) {
+  const unsigned long long P = totals[0];
+  const int64_t clo = (int64_t)pre[2], chi = has_hi ? (int64_t)pre[5] : C;
+  out[0] = clo < C ? (unsigned long long)pbase[clo] : P;
+  out[1] = chi < C ? (unsigned long long)pbase[chi] : P;
+}
+void launch_part_bounds(const uint32_t* pbase, int64_t C, const unsigned long long* pre, bool has_hi,
+                        const unsigned long long* totals, unsigned long long* out, cudaStream_t s) {
+  k_part_bounds<<<1, 1, 0, s>>>(pbase, C, pre, has_hi ? 1 : 0, totals, out);
+}
+
 // ===========================================================================
 // face-centre probes (dualize.py:59-70): corner + 0.5 h along both in-plane axes
 // ===========================================================================

@@ -58,6 +58,9 @@ void launch_active_compact(const GridP& g, const uint32_t* L, RecView rec, const
 // (pe, pq, pc) at word w (any word): slab ownership ranges
 void launch_prefix_at(RecView rv, int64_t w, int64_t A, const unsigned long long* totals, unsigned long long* out,
                       cudaStream_t s);
+// pbase at the window's owned cell bounds (pre[2], pre[5]) -> out[0..1] (odc_api.cu)
+void launch_part_bounds(const uint32_t* pbase, int64_t C, const unsigned long long* pre, bool has_hi,
+                        const unsigned long long* totals, unsigned long long* out, cudaStream_t s);
 
 // face-centre probes for 4-crossing faces (dualize.py:59-70)
 void launch_face_center_points(const GridP& g, const int64_t* f4_key, int64_t n, double* pts, cudaStream_t s);
