@@ -1053,6 +1053,51 @@ __device__ __forceinline__ void line_binary(const FieldP& f, const Inst2D& I, co
   a_out = a;
 }
 
+// The two step-2 rays (search.py:266-276: -dl and +dl from the same point,
+// same budget) searched side by side: each ray's samples and bisection are
+// line_binary's, in the same order; interleaving the two independent
+// evaluation chains gives the scheduler two fp64 chains per thread.
+template <int SEL>
+__device__ __forceinline__ void line_binary2(const FieldP& f, const Inst2D& I, const double o2[2],
+                                             const double da2[2], const double db2[2], uint32_t ref, double max_range,
+                                             int nlin, int nbin, double& a_out, bool& found_a, double& b_out,
+                                             bool& found_b) {
+  int fa = nlin, fb = nlin;
+  found_a = found_b = false;
+  for (int i = 1; i <= nlin && !(found_a && found_b); i++) {
+    const double s = max_range * ((double)i / (double)nlin);
+    if (!found_a) {
+      double p[3];
+      lift(I, o2[0] + s * da2[0], o2[1] + s * da2[1], p);
+      if (field_label_t<SEL>(f, p) != ref) {
+        fa = i;
+        found_a = true;
+      }
+    }
+    if (!found_b) {
+      double p[3];
+      lift(I, o2[0] + s * db2[0], o2[1] + s * db2[1], p);
+      if (field_label_t<SEL>(f, p) != ref) {
+        fb = i;
+        found_b = true;
+      }
+    }
+  }
+  double aa = max_range * ((double)(fa - 1) / (double)nlin), ba = max_range * ((double)fa / (double)nlin);
+  double ab = max_range * ((double)(fb - 1) / (double)nlin), bb = max_range * ((double)fb / (double)nlin);
+  for (int it = 0; it < nbin; it++) {
+    const double ma = 0.5 * (aa + ba), mb = 0.5 * (ab + bb);
+    double pa[3], pb[3];
+    lift(I, o2[0] + ma * da2[0], o2[1] + ma * da2[1], pa);
+    lift(I, o2[0] + mb * db2[0], o2[1] + mb * db2[1], pb);
+    const bool sa = field_label_t<SEL>(f, pa) == ref, sb = field_label_t<SEL>(f, pb) == ref;
+    if (sa) aa = ma; else ba = ma;
+    if (sb) ab = mb; else bb = mb;
+  }
+  a_out = aa;
+  b_out = ab;
+}
+
 template <bool B, int EV>
 __device__ __forceinline__ void search2d_one(const GridP& g, const FieldP& f, const OptP& o,
                                              const uint32_t* __restrict__ L, const RecView& rec,
@@ -1084,8 +1129,7 @@ __device__ __forceinline__ void search2d_one(const GridP& g, const FieldP& f, co
   const double dneg[2] = {-ch.dl[0], -ch.dl[1]};
   double da, db;
   bool fa, fb;
-  line_binary<EV>(f, I, q2, dneg, mid_label, r2, o.s2_lin, o.s2_bin, da, fa);
-  line_binary<EV>(f, I, q2, ch.dl, mid_label, r2, o.s2_lin, o.s2_bin, db, fb);
+  line_binary2<EV>(f, I, q2, dneg, ch.dl, mid_label, r2, o.s2_lin, o.s2_bin, da, fa, db, fb);
   const double qa[2] = {q2[0] + da * dneg[0], q2[1] + da * dneg[1]};
   const double qb[2] = {q2[0] + db * ch.dl[0], q2[1] + db * ch.dl[1]};
   double p2d[2];
