@@ -117,7 +117,10 @@ struct odc_ctx {
   cudaEvent_t evs[9] = {};  // stage boundaries
   Arena arena;
   CellTabEntry* table = nullptr;
-  unsigned long long* h_pinned = nullptr;  // small readback buffer
+  // small readback buffer (4 KB): [0, 256) readback(), [256, 258) the device
+  // status (readback_checked), [300, 310) a window's owned ranges and
+  // partition bounds, [320] a slab's seam count
+  unsigned long long* h_pinned = nullptr;
   unsigned int* d_fail = nullptr;          // device flag: a winding query stayed on the surface
   unsigned long long* d_sched = nullptr;   // MLP evaluator's pair counters: [0] only grows, [1] compacted batches
   unsigned long long sched_next = 0;       // its value when the next launch starts
@@ -554,6 +557,8 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   c->launches = 0;
   c->stats_cached = false;
   c->slab_U = -1;
+  c->seam_n = 0;  // set again by a slab extraction that has triangles
+  c->seam_flag = c->seam_rank = nullptr;
   c->arena.reset();
   c->keep = o->keep_intermediates != 0;
   cudaStream_t s = c->stream;
@@ -1103,13 +1108,13 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
       launch_seam_flags(tris, T, P_halo, c->seam_flag, s);
       check_launch(c);
       scan1(c, c->seam_flag, c->seam_rank, T, totals + 4);
-      CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[256], totals + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[320], totals + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     }
     mark(7);
     c->V0 = c->V1 = 0;
     st->raw_n_triangles = st->n_triangles = T;
     finish_stats();  // synchronises
-    if (seam) c->seam_n = (int64_t)c->h_pinned[256];
+    if (seam) c->seam_n = (int64_t)c->h_pinned[320];
     c->valid = true;
     return;
   }
