@@ -357,6 +357,31 @@ def test_gpu_balanced_analytic_slabs_equal_single_extraction(world):
     assert np.array_equal(mesh.vertices, ref.mesh.vertices)
 
 
+@pytest.mark.gpu
+def test_gpu_slab_seam_counts():
+    """The seam (triangles with a halo corner, counted during the slab
+    extraction) equals the host count from the slab's own triangles, and a
+    slab without surface on the same context reports none."""
+    import ctypes
+
+    from paper_2409_13418_b200 import ContourOptions, GridSpec, _lib
+    from paper_2409_13418_b200.slab import extract_piece
+
+    R = 64
+    field, lo, hi = scenes.resolve(scenes.thin_shell(R), R)
+    g = GridSpec(lo, hi, R)
+    ctx = _lib.context(0)
+    L = _lib.load()
+    piece = extract_piece(field, g, ContourOptions(), 30, 40)[0]
+    n = ctypes.c_int64()
+    assert L.odc_slab_seam(ctx.handle, None, ctypes.byref(n)) == 0
+    tris = piece.triangles.cpu().numpy()
+    assert n.value == int((tris < piece.n_halo).any(axis=1).sum()) > 0
+    piece = extract_piece(field, g, ContourOptions(), 1, 3)[0]  # below the shell: no surface
+    assert piece.triangles.shape[0] == 0
+    assert L.odc_slab_seam(ctx.handle, None, ctypes.byref(n)) == 0 and n.value == 0
+
+
 def test_balanced_slab_split_logic(monkeypatch):
     """The split of the cumulative work estimate (host logic; the device probe
     is replaced by a known work profile): equal shares, every rank >= 1 layer."""
