@@ -26,8 +26,8 @@ import numpy as np
 from . import _lib
 from .fields import LoweringError, field_continuous, is_mesh_winding, is_mlp, is_voxels, lower_program
 from .mesh import TriangleMesh
-from .pipeline import (ContourOptions, ContourResult, DeviceField, EvalCounter, _grid_args, _raise, contour,
-                       make_options, record_counts, stats_dict)
+from .pipeline import (ContourOptions, ContourResult, DeviceField, EvalCounter, _grid_args, _host_arrays, _raise,
+                       contour, make_options, record_counts, stats_dict)
 
 # Worker w of a threaded batch always runs jobs w, w + W, w + 2W, ... on its
 # own persistent libodc context, so each context's workspace settles at the
@@ -139,11 +139,12 @@ def _contour_stacked(jobs, options, *, device, provenance):
         if rc != _lib.ODC_OK:
             _raise(rc, ctx)
         V, T = int(vstart[-1]), int(tstart[-1])
-        v = np.empty((V, 3))
-        t = np.empty((T, 3), dtype=np.int64)
-        rt = np.empty((T, 3), dtype=np.int64)
-        kind = np.empty(V, dtype=np.int64) if provenance else None
-        ref = np.empty((V, 2), dtype=np.int64) if provenance else None
+        if provenance:  # one page-locked block: libodc DMAs straight into it (pipeline._host_arrays)
+            v, t, rt, kind, ref = _host_arrays([((V, 3), np.float64), ((T, 3), np.int64), ((T, 3), np.int64),
+                                                ((V,), np.int64), ((V, 2), np.int64)])
+        else:
+            v, t, rt = _host_arrays([((V, 3), np.float64), ((T, 3), np.int64), ((T, 3), np.int64)])
+            kind = ref = None
         if V:
             ptr = lambda a: a.ctypes.data if a is not None and a.size else None  # noqa: E731
             rc = L.odc_copy_batch_meshes(ctx.handle, ptr(v), ptr(t), ptr(rt), ptr(kind), ptr(ref))

@@ -1892,8 +1892,43 @@ struct CopySeg {
   size_t bytes;
   bool widen = false;
 };
-void copy_out_pipelined(odc_ctx* cc, const std::vector<CopySeg>& segs) {
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Destinations in page-locked memory (the Python layer allocates the mesh
+// arrays from torch's caching pinned allocator) are written by DMA directly:
+// int32 triangles are widened on the device first.  Pageable destinations
+// go through the staging pipeline below, whose host side is bound by page
+// faults in fresh buffers (~9 GB/s per thread on the B200 hosts).
+void copy_out_pipelined(odc_ctx* cc, const std::vector<CopySeg>& segs_in) {
   cudaStream_t s = cc->stream;
+  std::vector<CopySeg> segs;
+  bool direct = false;
+  for (const CopySeg& g : segs_in) {
+    if (!g.host || !g.bytes) continue;
+    if (!host_pinned(g.host)) {
+      segs.push_back(g);
+      continue;
+    }
+    const void* src = g.dev;
+    if (g.widen) {
+      int64_t* w = need(cc->arena.get<int64_t>(g.bytes / 4));
+      launch_widen_i32((const int32_t*)g.dev, w, (int64_t)(g.bytes / 4), s);
+      src = w;
+    }
+    CUDA_TRY(cudaMemcpyAsync(g.host, src, g.widen ? 2 * g.bytes : g.bytes, cudaMemcpyDeviceToHost, s));
+    direct = true;
+  }
+  if (direct && segs.empty()) {
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return;
+  }
   struct Piece {
     const void* dev;
     char* stage;

@@ -10,6 +10,7 @@ C-ABI in include/odc.h.  Fields are lowered to device programs
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 import time
 from dataclasses import dataclass, field as dc_field
@@ -271,15 +272,45 @@ def make_options(options, keep_intermediates=False):
     return o
 
 
+_PINNED_OUTPUT = os.environ.get("ODC_PINNED_OUTPUT", "1") != "0"
+
+
+def _host_arrays(specs):
+    """Output arrays of a mesh copy-back, carved from one page-locked block of
+    torch's caching host allocator: libodc DMAs straight into them (no
+    staging copy), and a block freed with the caller's last array is reused
+    by the next call, so no page of it faults again -- first writes into
+    fresh numpy buffers run at ~9 GB/s per thread on the B200 hosts, against
+    56 GB/s of pinned D2H.  Falls back to plain numpy arrays.  The arrays
+    are views of the block, which lives as long as any of them."""
+    sizes = [int(np.prod(sh)) * np.dtype(dt).itemsize for sh, dt in specs]
+    offs = np.cumsum([0] + [(n + 63) // 64 * 64 for n in sizes])
+    buf = None
+    if _PINNED_OUTPUT and offs[-1] >= (1 << 20):
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                buf = torch.empty(int(offs[-1]), dtype=torch.uint8, pin_memory=True).numpy()
+        except Exception:  # no torch / no pinned memory: pageable arrays
+            buf = None
+    if buf is None:
+        return [np.empty(sh, dtype=dt) for sh, dt in specs]
+    return [np.frombuffer(buf, dtype=dt, count=int(np.prod(sh)), offset=int(o)).reshape(sh)
+            for (sh, dt), o in zip(specs, offs[:-1])]
+
+
 def _copy_mesh(ctx, which, st, provenance=True):
     L = _lib.load()
     raw = which == 1
     V = st.raw_n_vertices if raw else st.n_vertices
     T = st.raw_n_triangles if raw else st.n_triangles
-    v = np.empty((V, 3), dtype=np.float64)
-    t = np.empty((T, 3), dtype=np.int64)
-    kind = np.empty(V, dtype=np.int64) if provenance else None
-    ref = np.empty((V, 2), dtype=np.int64) if provenance else None
+    if provenance:
+        v, t, kind, ref = _host_arrays([((V, 3), np.float64), ((T, 3), np.int64), ((V,), np.int64),
+                                        ((V, 2), np.int64)])
+    else:
+        v, t = _host_arrays([((V, 3), np.float64), ((T, 3), np.int64)])
+        kind = ref = None
     ptr = lambda a: a.ctypes.data if a is not None and a.size else None  # noqa: E731
     rc = L.odc_copy_mesh(ctx.handle, which, ptr(v), ptr(t), ptr(kind), ptr(ref))
     if rc != _lib.ODC_OK:
@@ -297,11 +328,12 @@ def _copy_meshes(ctx, st, provenance=True):
         mesh = _copy_mesh(ctx, 0, st, provenance)
         return mesh, mesh
     V, T, V0, T0 = int(st.n_vertices), int(st.n_triangles), int(st.raw_n_vertices), int(st.raw_n_triangles)
-    v = np.empty((V, 3), dtype=np.float64)
-    t = np.empty((T, 3), dtype=np.int64)
-    rt = np.empty((T0, 3), dtype=np.int64)
-    kind = np.empty(V, dtype=np.int64) if provenance else None
-    ref = np.empty((V, 2), dtype=np.int64) if provenance else None
+    if provenance:
+        v, t, rt, kind, ref = _host_arrays([((V, 3), np.float64), ((T, 3), np.int64), ((T0, 3), np.int64),
+                                            ((V,), np.int64), ((V, 2), np.int64)])
+    else:
+        v, t, rt = _host_arrays([((V, 3), np.float64), ((T, 3), np.int64), ((T0, 3), np.int64)])
+        kind = ref = None
     ptr = lambda a: a.ctypes.data if a is not None and a.size else None  # noqa: E731
     rc = _lib.load().odc_copy_mesh_pair(ctx.handle, ptr(v), ptr(t), ptr(kind), ptr(ref), ptr(rt))
     if rc != _lib.ODC_OK:
