@@ -2006,11 +2006,13 @@ __global__ void __launch_bounds__(kScanBlock) k_apply_u32(ScanPtrs p, int64_t n,
     }
   }
 }
-// Small arrays (<= kScanSmallMax): one block walks the tiles in order with a
-// running carry -- one launch instead of three (what dominates the scans of
-// a small grid is launch latency, not bandwidth).
+// Small arrays (<= kScanSmallMax = one pass of 1,024 threads x 8): one block,
+// one launch instead of three -- what dominates the scans of a small grid is
+// launch latency, not bandwidth.  A single block walking more tiles with a
+// running carry is slower than the three launches (63 K elements: 48-90 us
+// against ~15 us), so larger arrays take the tiled path.
 constexpr int kScanSmallBlock = 1024;
-constexpr int64_t kScanSmallMax = 64 * 1024;
+constexpr int64_t kScanSmallMax = (int64_t)kScanSmallBlock * kScanPer;
 template <int NCH>
 __global__ void __launch_bounds__(kScanSmallBlock) k_scan_small(ScanPtrs p, int64_t n, unsigned long long* totals) {
   unsigned long long carry[NCH];
