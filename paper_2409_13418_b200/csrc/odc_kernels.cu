@@ -1876,10 +1876,12 @@ __global__ void __launch_bounds__(kSolveBlock, 8) k_part_solve(GridP g, OptP o, 
 #define NN(j, c) snorm[3 * (s0 + (j)) + (c)]
   const double cnt = (double)(len < 1 ? 1 : len);
   double cen[3] = {0.0, 0.0, 0.0};
+#pragma unroll 4
   for (int j = 0; j < len; j++)
     for (int c = 0; c < 3; c++) cen[c] += PE(j, c);
   for (int c = 0; c < 3; c++) cen[c] /= cnt;
   double A[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, b[3] = {0.0, 0.0, 0.0};
+#pragma unroll 4
   for (int j = 0; j < len; j++) {  // A and b accumulate independently, each in cycle order
     const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
     for (int r = 0; r < 3; r++)
@@ -1914,6 +1916,7 @@ __global__ void __launch_bounds__(kSolveBlock, 8) k_part_solve(GridP g, OptP o, 
     pos[c] = x;
   }
   double res = 0.0;
+#pragma unroll 4
   for (int j = 0; j < len; j++) {
     const double nj[3] = {NN(j, 0), NN(j, 1), NN(j, 2)};
     const double d[3] = {pos[0] - PE(j, 0), pos[1] - PE(j, 1), pos[2] - PE(j, 2)};
