@@ -559,6 +559,10 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   c->slab_U = -1;
   c->seam_n = 0;  // set again by a slab extraction that has triangles
   c->seam_flag = c->seam_rank = nullptr;
+  if (c->trace_buf) {  // a step trace cut short by an error: no tracing from here on
+    cudaFree(c->trace_buf);
+    c->trace_buf = nullptr;
+  }
   c->arena.reset();
   c->keep = o->keep_intermediates != 0;
   cudaStream_t s = c->stream;
