@@ -1,5 +1,5 @@
 // Batched numpy.linalg.eigh for symmetric 3x3 matrices (odc_eigh3.cuh) on
-// the device and on the host.  The QEF kernel (k_cell_solve) inlines the
+// the device and on the host.  The QEF kernel (k_part_solve) inlines the
 // same function; these entry points exist so the tests can pin the solver
 // against numpy itself on arbitrary matrices (tests/test_eigh3.py,
 // tests/test_gpu_eigh3.py).  Compiled with --fmad=false and host

@@ -1,4 +1,4 @@
-"""The QEF eigensolver (odc_eigh3.cuh, the code k_cell_solve inlines) run on
+"""The QEF eigensolver (odc_eigh3.cuh, the code k_part_solve inlines) run on
 the host through libodc's C-ABI must equal numpy.linalg.eigh -- the call
 solve_qef_batch makes (dualize.py:358) -- bit for bit, eigenvalues and
 eigenvectors.  No device needed: the header is plain IEEE fp64 with explicit

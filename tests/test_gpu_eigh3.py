@@ -1,5 +1,5 @@
 """The QEF eigensolver on the device (odc_eigh3 through libodc's C-ABI, the
-same inline code k_cell_solve runs) against numpy.linalg.eigh -- the call
+same inline code k_part_solve runs) against numpy.linalg.eigh -- the call
 solve_qef_batch makes (dualize.py:358) -- bit for bit."""
 
 import ctypes
