@@ -867,9 +867,11 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
 
   // ---- K6, first half: per-cell configurations and the partition / plane
   // sample totals (dualize.py:194-238).  They need only the labels and the
-  // word records, so they run before the searches: their readback also
-  // brings the window's owned ranges and the halo / owned partition bounds
-  // (one synchronisation instead of three).
+  // word records (with the face-centre probes' pairing bits, so the probes
+  // run first; their eval accounting stays in the reference's order below),
+  // so they run before the searches: their readback also brings the
+  // window's owned ranges and the halo / owned partition bounds (one
+  // synchronisation instead of three).
   face_probes(true, false);
   uint16_t* cfg = need(c->arena.get<uint16_t>(C));
   uint32_t* ncyc = need(c->arena.get<uint32_t>(C));
