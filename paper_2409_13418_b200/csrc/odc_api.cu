@@ -117,7 +117,8 @@ struct odc_ctx {
   cudaEvent_t evs[9] = {};  // stage boundaries
   Arena arena;
   CellTabEntry* table = nullptr;
-  // small readback buffer (4 KB): [0, 256) readback(), [256, 258) the device
+  // small readback buffer (4 KB): [0, 256) readback() ([8, 32) the
+  // statistics block of finish_mesh), [256, 258) the device
   // status (readback_checked), [300, 310) a window's owned ranges and
   // partition bounds, [320] a slab's seam count
   unsigned long long* h_pinned = nullptr;
@@ -423,15 +424,10 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
   cudaStream_t s = c->stream;
   launch_count_used(used, P, dst, s);
   check_launch(c);
-  // every statistic but the repair's is final here: one readback serves the
-  // used-partition count and finish_stats
-  readback(c, dst, sizeof(DevStats));
-  std::memcpy(&c->h_stats, c->h_pinned, sizeof(DevStats));
-  c->stats_cached = true;
-  const int64_t used_p = (int64_t)c->h_stats.used_partitions;
-  int64_t V0 = P + NF;
   c->src0 = nullptr;
-  if (used_p != P) {
+  int64_t V0 = P + NF;
+  // unused-vertex removal: drop partitions no triangle references
+  auto compact = [&](int64_t used_p) {
     uint32_t* u32 = need(c->arena.get<uint32_t>(V0));
     uint32_t* nid = need(c->arena.get<uint32_t>(V0));
     launch_widen_flags(used, V0, u32, s);
@@ -443,34 +439,45 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
     check_launch(c, 2);
     V0 = used_p + NF;
     verts = vc;
+  };
+  // Every statistic but the repair's is final here.  The used-partition
+  // count rides on the first repair pass's readback: that pass runs on the
+  // uncompacted ids (an unreferenced vertex has no fan, so it changes
+  // nothing); in the rare case that partitions are unused (open boundaries)
+  // the mesh is compacted and the repair starts over.
+  auto take_stats = [&]() {
+    std::memcpy(&c->h_stats, c->h_pinned + 8, sizeof(DevStats));
+    c->stats_cached = true;
+    return (int64_t)c->h_stats.used_partitions;
+  };
+  const bool run = repair && T > 0;
+  if (!run) {
+    CUDA_TRY(cudaMemcpyAsync(c->h_pinned + 8, dst, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const int64_t used_p = take_stats();
+    if (used_p != P) compact(used_p);
   }
-  c->verts0 = verts;
-  c->tris0 = tris;
-  c->V0 = V0;
-  st->raw_n_vertices = V0;
-  st->raw_n_triangles = T;
-  c->verts1 = verts;
-  c->dup_passes.clear();
-  c->tris1 = tris;
   int64_t curV = V0;
-  if (repair && T > 0) {
-    int32_t* cur = need(c->arena.get<int32_t>(3 * T));
-    CUDA_TRY(cudaMemcpyAsync(cur, tris, sizeof(int32_t) * 3 * T, cudaMemcpyDeviceToDevice, s));
+  int passes = 0;
+  bool stats_pending = run;
+  for (bool restart = run; restart;) {
+    restart = false;
+    c->dup_passes.clear();
+    curV = V0;
+    const int32_t* cur = tris;  // read only: each pass writes a new triangle array
     double* cv = verts;
     char* big = nullptr;  // scratch for fans of more than 64 triangles, allocated on first need
     uint8_t* dirty = nullptr;  // passes after the first: only vertices whose fan the last pass changed
-    int passes = 0;
+    passes = 0;
     for (int pass = 0; pass < 4; pass++) {
       passes++;
-      uint32_t* deg = need(c->arena.get<uint32_t>(curV + 1));
+      uint32_t* deg = need(c->arena.get<uint32_t>(3 * (curV + 1)));  // deg, cursor, extra: one memset
+      uint32_t* cursor = deg + (curV + 1);
+      uint32_t* extra = cursor + (curV + 1);
       uint32_t* off = need(c->arena.get<uint32_t>(curV + 1));
-      uint32_t* cursor = need(c->arena.get<uint32_t>(curV));
       int32_t* inc = need(c->arena.get<int32_t>(3 * T));
-      uint32_t* extra = need(c->arena.get<uint32_t>(curV + 1));
       uint32_t* eoff = need(c->arena.get<uint32_t>(curV + 1));
-      CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (curV + 1), s));
-      CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * curV, s));
-      CUDA_TRY(cudaMemsetAsync(extra, 0, sizeof(uint32_t) * (curV + 1), s));
+      CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * 3 * (curV + 1), s));
       launch_vertex_degree(cur, T, deg, s, dirty);
       check_launch(c);
       scan1(c, deg, off, curV + 1, totals + 6);
@@ -479,11 +486,24 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
       launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s, dirty);
       check_launch(c);
       scan1(c, extra, eoff, curV + 1, totals + 7);
-      // the added-vertex total and the fan-overflow flag in one synchronisation
+      // the added-vertex total, the fan-overflow flag (and, first pass, the
+      // statistics) in one synchronisation
       CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[0], totals + 7, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[1], &dst->repair_overflow, sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s));
+      if (stats_pending)
+        CUDA_TRY(cudaMemcpyAsync(c->h_pinned + 8, dst, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
+      if (stats_pending) {
+        stats_pending = false;
+        const int64_t used_p = take_stats();
+        if (used_p != P) {  // compact, then repair the compacted mesh from the start
+          CUDA_TRY(cudaMemsetAsync(&dst->repair_overflow, 0, sizeof(unsigned long long), s));
+          compact(used_p);
+          restart = true;
+          break;
+        }
+      }
       if (!big && c->h_pinned[1]) {  // fans of more than 64 triangles need global scratch: re-run with it
         big = need(c->arena.get<char>(repair_scratch_bytes(T)));
         CUDA_TRY(cudaMemsetAsync(&dst->repair_overflow, 0, sizeof(unsigned long long), s));
@@ -511,8 +531,21 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
       cv = nv;
       curV += E;
     }
-    c->verts1 = cv;
-    c->tris1 = cur;
+    if (!restart) {
+      c->verts1 = cv;
+      c->tris1 = const_cast<int32_t*>(cur);
+    }
+  }
+  c->verts0 = verts;
+  c->tris0 = tris;
+  c->V0 = V0;
+  st->raw_n_vertices = V0;
+  st->raw_n_triangles = T;
+  if (!run) {
+    c->verts1 = verts;
+    c->tris1 = tris;
+    c->dup_passes.clear();
+  } else {
     st->repair_passes = passes;
   }
   c->V1 = curV;

@@ -272,3 +272,41 @@ def test_gpu_copy_mesh_pair_matches_single_copies():
                  (res.raw_mesh.triangles, raw.triangles), (res.raw_mesh.vertices, raw.vertices)):
         assert np.array_equal(a, b)
     _lib.check(0)
+
+
+def _open_boundary_case(i):
+    """Case i of a seeded stream of shapes that leave the unit box (the
+    stream scripts/probe_unused_partitions.py searched): 4 (sphere, 20^3), 6 (plane,
+    16^3) and 7 (torus, 16^3) keep partition vertices no triangle uses."""
+    from paper_2409_13418_b200 import BoxField, PlaneField, SphereField, TorusField
+
+    rng = np.random.default_rng(0)
+    for j in range(i + 1):
+        k = j % 4
+        if k == 0:
+            f = SphereField(tuple(rng.uniform(-0.2, 1.2, 3)), float(rng.uniform(0.2, 0.9)))
+        elif k == 1:
+            f = BoxField(tuple(rng.uniform(-0.2, 1.2, 3)), tuple(rng.uniform(0.1, 0.8, 3)))
+        elif k == 2:
+            f = PlaneField(tuple(rng.uniform(0, 1, 3)), tuple(rng.normal(size=3)))
+        else:
+            f = TorusField(tuple(rng.uniform(0, 1, 3)), float(rng.uniform(0.2, 0.5)), float(rng.uniform(0.05, 0.2)))
+        R = int(rng.choice([9, 12, 16, 20]))
+    return f, R
+
+
+@pytest.mark.parametrize("i", [4, 6, 7])
+def test_gpu_open_boundary_drops_unused_partitions(i):
+    """Open boundaries: some partition vertices are referenced by no
+    triangle, and polygonize.py:204-214 drops them before the repair; the
+    device path learns that from the first repair pass's readback and
+    restarts the repair on the compacted mesh.  Mesh, raw mesh and
+    provenance equal the oracle's."""
+    field, R = _open_boundary_case(i)
+    res = contour(field, GridSpec((0, 0, 0), (1, 1, 1), R))
+    o = oracle.contour_oracle(field, (0, 0, 0), (1, 1, 1), R)
+    assert int((res.raw_mesh.provenance_kind == 0).sum()) < res.stats["n_partitions"]  # the path under test
+    assert np.array_equal(res.mesh.triangles, o["triangles"])
+    assert np.array_equal(res.mesh.vertices, o["vertices"])
+    assert np.array_equal(res.raw_mesh.triangles, o["raw_triangles"])
+    assert np.array_equal(res.raw_mesh.vertices, o["raw_vertices"])
