@@ -139,6 +139,10 @@ struct odc_ctx {
   std::vector<cudaEvent_t> copy_evs;       // one per staged piece of a mesh copy
   std::string err;
   int launches = 0;
+  // look-back scan status words (scan1 / scan2)
+  unsigned long long* scan_status = nullptr;
+  int64_t scan_status_words = 0;
+  uint32_t scan_epoch = 0;
   // the statistics block as read back with the used-partition count
   // (finish_mesh): final by then, so finish_stats needs no readback of its own
   DevStats h_stats{};
@@ -402,18 +406,49 @@ void record(odc_stats* st, int cat, int64_t batches, int64_t evals) {
   st->eval_evals[cat] += evals;
 }
 
+// The context's look-back status words (grow-only, never cleared: each
+// scan takes a new epoch, see launch_scan_lookback)
+unsigned long long* scan_status(odc_ctx* c, int64_t n) {
+  const int64_t words = 2 * scan_lookback_tiles(n);
+  if (words > c->scan_status_words) {
+    if (c->scan_status) cudaFree(c->scan_status);
+    c->scan_status = nullptr;
+    c->scan_status_words = 0;
+    const int64_t want = std::max<int64_t>(words, 4096);
+    CUDA_TRY(cudaMalloc(&c->scan_status, sizeof(unsigned long long) * want));
+    CUDA_TRY(cudaMemset(c->scan_status, 0, sizeof(unsigned long long) * want));  // epoch 0: never current
+    c->scan_status_words = want;
+  }
+  if (++c->scan_epoch >= (1u << 30)) {  // wrapped: clear so no stale word can match
+    CUDA_TRY(cudaMemsetAsync(c->scan_status, 0, sizeof(unsigned long long) * c->scan_status_words, c->stream));
+    c->scan_epoch = 1;
+  }
+  return c->scan_status;
+}
+// Scans up to kLookbackMax elements run single-pass (one launch instead of
+// three); longer chains of tiles serialise on the look-back (measured slower
+// at 0.6-4 M elements), so they keep the tiled reduce-then-scan.
+constexpr int64_t kLookbackMax = 256 * 1024;
+void scan_any(odc_ctx* c, const uint32_t* const* ins, uint32_t* const* outs, int nch, int64_t n,
+              unsigned long long* totals) {
+  if (n <= kLookbackMax) {
+    unsigned long long* status = scan_status(c, n);
+    check_launch(c, launch_scan_lookback(ins, outs, nch, n, status, c->scan_epoch, totals, c->stream));
+  } else {
+    uint32_t* tiles = need(c->arena.get<uint32_t>(nch * ((n + 255) / 256) + 2));
+    check_launch(c, launch_scan_u32(ins, outs, nch, n, tiles, totals, c->stream));
+  }
+}
 void scan1(odc_ctx* c, const uint32_t* in, uint32_t* out, int64_t n, unsigned long long* totals) {
   const uint32_t* ins[1] = {in};
   uint32_t* outs[1] = {out};
-  uint32_t* tiles = need(c->arena.get<uint32_t>((n + 255) / 256 + 1));
-  check_launch(c, launch_scan_u32(ins, outs, 1, n, tiles, totals, c->stream));
+  scan_any(c, ins, outs, 1, n, totals);
 }
 void scan2(odc_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* oa, uint32_t* ob, int64_t n,
            unsigned long long* totals) {
   const uint32_t* ins[2] = {a, b};
   uint32_t* outs[2] = {oa, ob};
-  uint32_t* tiles = need(c->arena.get<uint32_t>(2 * ((n + 255) / 256) + 2));
-  check_launch(c, launch_scan_u32(ins, outs, 2, n, tiles, totals, c->stream));
+  scan_any(c, ins, outs, 2, n, totals);
 }
 
 // Drop unreferenced partition vertices (polygonize.py:199-209), then repair
@@ -1332,6 +1367,7 @@ void odc_destroy(odc_ctx* c) {
   if (c->d_fail) cudaFree(c->d_fail);
   if (c->d_sched) cudaFree(c->d_sched);
   if (c->trace_buf) cudaFree(c->trace_buf);
+  if (c->scan_status) cudaFree(c->scan_status);
   for (auto e : c->copy_evs) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);

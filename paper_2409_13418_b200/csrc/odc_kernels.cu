@@ -2048,6 +2048,90 @@ __global__ void __launch_bounds__(kScanSmallBlock) k_scan_small(ScanPtrs p, int6
   if (threadIdx.x < NCH) totals[threadIdx.x] = carry[threadIdx.x];
 }
 
+// Single-pass scan with decoupled look-back: each tile publishes its
+// aggregate, then walks back over its predecessors' published words until
+// one carries an inclusive prefix, and publishes its own.  One word per
+// (channel, tile): epoch (30 bits) | flag (2 bits: 1 aggregate, 2 inclusive)
+// | value (32 bits -- the outputs are u32 prefixes).  The epoch is a
+// per-context counter bumped every scan, so the status array is never
+// cleared: a word from an earlier scan has another epoch and reads as "not
+// yet published".  Tiles wait only on lower-indexed tiles, which the
+// hardware dispatches first.
+template <int NCH>
+__global__ void __launch_bounds__(kScanBlock) k_scan_lookback(ScanPtrs p, int64_t n,
+                                                              unsigned long long* __restrict__ status,
+                                                              int64_t ntiles, uint32_t epoch,
+                                                              unsigned long long* __restrict__ totals) {
+  __shared__ uint32_t s_excl[NCH];
+  const int64_t t = blockIdx.x;
+  const int64_t i0 = t * kScanTile + (int64_t)threadIdx.x * kScanPer;
+  uint32_t x[NCH][kScanPer], v[NCH], ex[NCH], tot[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    v[c] = 0u;
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      x[c][k] = i0 + k < n ? p.in[c][i0 + k] : 0u;
+      v[c] += x[c][k];
+    }
+  }
+  block_exscan<NCH>(v, ex, tot);
+  if (threadIdx.x < NCH) {
+    const int c = threadIdx.x;
+    volatile unsigned long long* st = status + (int64_t)c * ntiles;
+    const unsigned long long tag = (unsigned long long)epoch << 34;
+    uint32_t excl = 0;
+    if (t == 0) {
+      st[0] = tag | (2ull << 32) | tot[c];
+    } else {
+      st[t] = tag | (1ull << 32) | tot[c];  // aggregate: the successors may start looking back
+      for (int64_t j = t - 1; j >= 0;) {
+        const unsigned long long w = st[j];
+        if ((w >> 34) != epoch || ((w >> 32) & 3ull) == 0ull) continue;  // not published yet: spin
+        excl += (uint32_t)w;
+        if (((w >> 32) & 3ull) == 2ull) break;  // inclusive prefix: done
+        j--;
+      }
+      st[t] = tag | (2ull << 32) | (uint32_t)(excl + tot[c]);
+    }
+    s_excl[c] = excl;
+    if (t == ntiles - 1) totals[c] = (unsigned long long)excl + tot[c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    uint32_t run = s_excl[c] + ex[c];
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      if (i0 + k < n) p.out[c][i0 + k] = run;
+      run += x[c][k];
+    }
+  }
+}
+
+int launch_scan_lookback(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n,
+                         unsigned long long* status, uint32_t epoch, unsigned long long* totals, cudaStream_t s) {
+  ScanPtrs p{};
+  for (int c = 0; c < nch; c++) {
+    p.in[c] = in[c];
+    p.out[c] = out[c];
+  }
+  const int64_t nt = (n + kScanTile - 1) / kScanTile;
+  if (nt == 0) {
+    cudaMemsetAsync(totals, 0, sizeof(unsigned long long) * nch, s);
+    return 0;
+  }
+  if (n <= kScanSmallMax) {
+    if (nch == 1) k_scan_small<1><<<1, kScanSmallBlock, 0, s>>>(p, n, totals);
+    else k_scan_small<2><<<1, kScanSmallBlock, 0, s>>>(p, n, totals);
+    return 1;
+  }
+  if (nch == 1) k_scan_lookback<1><<<(unsigned)nt, kScanBlock, 0, s>>>(p, n, status, nt, epoch, totals);
+  else k_scan_lookback<2><<<(unsigned)nt, kScanBlock, 0, s>>>(p, n, status, nt, epoch, totals);
+  return 1;
+}
+int64_t scan_lookback_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
+
 int launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
                     unsigned long long* totals, cudaStream_t s) {
   ScanPtrs p{};

@@ -131,6 +131,11 @@ void launch_fd_normals(const GridP& g, const OptP& o, const uint32_t* L, const i
 // K6: per-cell partitions, plane samples, QEF (dualize.py:194-444)
 void launch_cell_config(const GridP& g, const uint32_t* L, RecView rec, const int64_t* cell_id, int64_t C,
                         const CellTabEntry* table, uint16_t* cfg, uint32_t* ncyc, uint32_t* nsamp, cudaStream_t s);
+// single-pass (decoupled look-back) form: status holds 2 * scan_lookback_tiles(n)
+// words that are never cleared (epoch: a per-context counter, new per scan, >= 1)
+int launch_scan_lookback(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n,
+                         unsigned long long* status, uint32_t epoch, unsigned long long* totals, cudaStream_t s);
+int64_t scan_lookback_tiles(int64_t n);
 // returns the number of kernels launched
 int launch_scan_u32(const uint32_t* const* in, uint32_t* const* out, int nch, int64_t n, uint32_t* tile_buf,
                     unsigned long long* totals, cudaStream_t s);
