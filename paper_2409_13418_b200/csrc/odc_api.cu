@@ -425,19 +425,14 @@ unsigned long long* scan_status(odc_ctx* c, int64_t n) {
   }
   return c->scan_status;
 }
-// Scans up to kLookbackMax elements run single-pass (one launch instead of
-// three); longer chains of tiles serialise on the look-back (measured slower
-// at 0.6-4 M elements), so they keep the tiled reduce-then-scan.
-constexpr int64_t kLookbackMax = 256 * 1024;
+// The pipeline's scans run single-pass (decoupled look-back, one launch;
+// arrays up to one block pass: one block): measured against the tiled
+// reduce-then-scan (three launches), equal at 0.6-4 M elements and faster
+// below.
 void scan_any(odc_ctx* c, const uint32_t* const* ins, uint32_t* const* outs, int nch, int64_t n,
               unsigned long long* totals) {
-  if (n <= kLookbackMax) {
-    unsigned long long* status = scan_status(c, n);
-    check_launch(c, launch_scan_lookback(ins, outs, nch, n, status, c->scan_epoch, totals, c->stream));
-  } else {
-    uint32_t* tiles = need(c->arena.get<uint32_t>(nch * ((n + 255) / 256) + 2));
-    check_launch(c, launch_scan_u32(ins, outs, nch, n, tiles, totals, c->stream));
-  }
+  unsigned long long* status = scan_status(c, n);
+  check_launch(c, launch_scan_lookback(ins, outs, nch, n, status, c->scan_epoch, totals, c->stream));
 }
 void scan1(odc_ctx* c, const uint32_t* in, uint32_t* out, int64_t n, unsigned long long* totals) {
   const uint32_t* ins[1] = {in};

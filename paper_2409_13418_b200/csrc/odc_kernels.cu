@@ -2049,8 +2049,10 @@ __global__ void __launch_bounds__(kScanSmallBlock) k_scan_small(ScanPtrs p, int6
 }
 
 // Single-pass scan with decoupled look-back: each tile publishes its
-// aggregate, then walks back over its predecessors' published words until
-// one carries an inclusive prefix, and publishes its own.  One word per
+// aggregate, then one warp per channel walks back over its predecessors'
+// published words, 32 at a time, until one carries an inclusive prefix, and
+// publishes its own (a one-thread walk serialises long tile chains: 2,000
+// tiles took longer than the three-launch scan).  One word per
 // (channel, tile): epoch (30 bits) | flag (2 bits: 1 aggregate, 2 inclusive)
 // | value (32 bits -- the outputs are u32 prefixes).  The epoch is a
 // per-context counter bumped every scan, so the status array is never
@@ -2076,26 +2078,37 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_lookback(ScanPtrs p, int64_
     }
   }
   block_exscan<NCH>(v, ex, tot);
-  if (threadIdx.x < NCH) {
-    const int c = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < NCH) {  // warp c publishes channel c and looks back 32 tiles per step
+    const int c = warp;
     volatile unsigned long long* st = status + (int64_t)c * ntiles;
     const unsigned long long tag = (unsigned long long)epoch << 34;
+    if (lane == 0) st[t] = tag | ((t == 0 ? 2ull : 1ull) << 32) | tot[c];  // aggregate (tile 0: inclusive)
     uint32_t excl = 0;
-    if (t == 0) {
-      st[0] = tag | (2ull << 32) | tot[c];
-    } else {
-      st[t] = tag | (1ull << 32) | tot[c];  // aggregate: the successors may start looking back
-      for (int64_t j = t - 1; j >= 0;) {
-        const unsigned long long w = st[j];
-        if ((w >> 34) != epoch || ((w >> 32) & 3ull) == 0ull) continue;  // not published yet: spin
-        excl += (uint32_t)w;
-        if (((w >> 32) & 3ull) == 2ull) break;  // inclusive prefix: done
-        j--;
+    if (t > 0) {
+      int64_t base = t - 1;  // the predecessor lane 0 reads
+      while (true) {
+        const int64_t j = base - lane;
+        // before tile 0: an inclusive prefix of 0
+        const unsigned long long w = j >= 0 ? st[j] : (tag | (2ull << 32));
+        const unsigned flag = (w >> 34) == epoch ? (unsigned)((w >> 32) & 3ull) : 0u;
+        const unsigned pub = __ballot_sync(0xffffffffu, flag != 0u);
+        const unsigned inc = __ballot_sync(0xffffffffu, flag == 2u);
+        const int k = inc ? __ffs(inc) - 1 : 31;  // lanes 0..k are needed
+        const unsigned need = k == 31 ? 0xffffffffu : ((2u << k) - 1u);
+        if ((pub & need) != need) continue;  // a needed predecessor has not published yet
+        uint32_t val = lane <= k ? (uint32_t)w : 0u;
+        val = __reduce_add_sync(0xffffffffu, val);
+        excl += val;
+        if (inc) break;
+        base -= 32;
       }
-      st[t] = tag | (2ull << 32) | (uint32_t)(excl + tot[c]);
+      if (lane == 0) st[t] = tag | (2ull << 32) | (uint32_t)(excl + tot[c]);
     }
-    s_excl[c] = excl;
-    if (t == ntiles - 1) totals[c] = (unsigned long long)excl + tot[c];
+    if (lane == 0) {
+      s_excl[c] = excl;
+      if (t == ntiles - 1) totals[c] = (unsigned long long)excl + tot[c];
+    }
   }
   __syncthreads();
 #pragma unroll
