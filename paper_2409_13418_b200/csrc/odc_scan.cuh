@@ -1,4 +1,5 @@
-// odc_scan.cuh -- hand-written multi-channel exclusive scans (reduce-then-scan).
+// odc_scan.cuh -- hand-written multi-channel exclusive scans (block scans for
+// the single-pass look-back scan and the tiled reduce-then-scan, odc_kernels.cu).
 //
 // Every ordered output of the pipeline (edge rows, instance ids, cell rows,
 // partition ids, triangle offsets, fan-vertex ids, repair vertex ids) is an
