@@ -116,52 +116,55 @@ def main():
                 gather_ms = sent / (a.gather_gbs * 1e9) * 1e3
                 step = max(times) + max(gl_ms) + gather_ms + cat_ms + fin_ms
                 print(f"  {world} balanced slabs: per-rank slab ms {np.round(times, 2).tolist()}")
-                # distributed finish, ranks from the top down (rank k needs rank k+1's seam)
-                dist_ms, nondisc, seam_next, xbytes = [0.0] * world, 0, None, 0
-                fin_parts = [None] * world
-                for k in reversed(range(world)):
-                    c0, c1 = rr[k]
-                    sts = _lib.Stats()
-                    info = _lib.SlabInfo()
-                    assert L.odc_extract_slab(ctx.handle, df.handle, lo_c, hi_c, RR, ctypes.byref(o), int(c0),
-                                              int(c1), ctypes.byref(sts), ctypes.byref(info)) == 0
-                    n = ctypes.c_int64()
+                # distributed finish, ranks from the top down (rank k needs rank k+1's seam);
+                # run twice and keep the second (the first carries one-time allocations, like
+                # the bench's warm-up steps)
+                for _rep in range(2):
+                    dist_ms, nondisc, seam_next, xbytes = [0.0] * world, 0, None, 0
+                    fin_parts = [None] * world
+                    for k in reversed(range(world)):
+                        c0, c1 = rr[k]
+                        sts = _lib.Stats()
+                        info = _lib.SlabInfo()
+                        assert L.odc_extract_slab(ctx.handle, df.handle, lo_c, hi_c, RR, ctypes.byref(o), int(c0),
+                                                  int(c1), ctypes.byref(sts), ctypes.byref(info)) == 0
+                        n = ctypes.c_int64()
 
-                    def seam_fn():
-                        L.odc_slab_seam(ctx.handle, None, ctypes.byref(n))
-                        t = torch.empty((n.value, 3), dtype=torch.int32, device=dev)
-                        if n.value:
-                            L.odc_slab_seam(ctx.handle, t.data_ptr(), ctypes.byref(n))
-                        return t
-                    seam, t_seam = timed(torch, seam_fn, reps=1)
-                    nh_next = int(pieces[k + 1].n_halo) if k + 1 < world else 0
-                    U, nd = ctypes.c_int64(), ctypes.c_int64()
-                    sn = seam_next if seam_next is not None else torch.empty((0, 3), dtype=torch.int32, device=dev)
+                        def seam_fn():
+                            L.odc_slab_seam(ctx.handle, None, ctypes.byref(n))
+                            t = torch.empty((n.value, 3), dtype=torch.int32, device=dev)
+                            if n.value:
+                                L.odc_slab_seam(ctx.handle, t.data_ptr(), ctypes.byref(n))
+                            return t
+                        seam, t_seam = timed(torch, seam_fn, reps=1)
+                        nh_next = int(pieces[k + 1].n_halo) if k + 1 < world else 0
+                        U, nd = ctypes.c_int64(), ctypes.c_int64()
+                        sn = seam_next if seam_next is not None else torch.empty((0, 3), dtype=torch.int32, device=dev)
 
-                    def local_fn():
-                        assert L.odc_slab_local_finish(ctx.handle, sn.data_ptr() if sn.numel() else None,
-                                                       sn.shape[0], nh_next, ctypes.byref(U), ctypes.byref(nd)) == 0
-                    _, t_local = timed(torch, local_fn, reps=1)
-                    nondisc += nd.value
-                    u = U.value
-                    T_k = int(counts[k, 2])
-                    top = torch.zeros((nh_next,), dtype=torch.int32, device=dev)
-                    halo = torch.zeros((int(pieces[k].n_halo),), dtype=torch.int32, device=dev)
-                    tri = torch.empty((T_k, 3), dtype=torch.int32, device=dev)
-                    pv = torch.empty((u, 3), dtype=torch.float64, device=dev)
-                    pc = torch.empty((u,), dtype=torch.int64, device=dev)
-                    pi = torch.empty((u,), dtype=torch.int64, device=dev)
-                    ptr = lambda t: t.data_ptr() if t.numel() else None  # noqa: E731
+                        def local_fn():
+                            assert L.odc_slab_local_finish(ctx.handle, sn.data_ptr() if sn.numel() else None,
+                                                           sn.shape[0], nh_next, ctypes.byref(U), ctypes.byref(nd)) == 0
+                        _, t_local = timed(torch, local_fn, reps=1)
+                        nondisc += nd.value
+                        u = U.value
+                        T_k = int(counts[k, 2])
+                        top = torch.zeros((nh_next,), dtype=torch.int32, device=dev)
+                        halo = torch.zeros((int(pieces[k].n_halo),), dtype=torch.int32, device=dev)
+                        tri = torch.empty((T_k, 3), dtype=torch.int32, device=dev)
+                        pv = torch.empty((u, 3), dtype=torch.float64, device=dev)
+                        pc = torch.empty((u,), dtype=torch.int64, device=dev)
+                        pi = torch.empty((u,), dtype=torch.int64, device=dev)
+                        ptr = lambda t: t.data_ptr() if t.numel() else None  # noqa: E731
 
-                    def final_fn():
-                        if nh_next:
-                            assert L.odc_slab_top_ids(ctx.handle, 0, nh_next, top.data_ptr()) == 0
-                        assert L.odc_slab_final(ctx.handle, 0, 0, ptr(halo), ptr(tri), ptr(pv), ptr(pc), ptr(pi)) == 0
-                    _, t_final = timed(torch, final_fn, reps=1)
-                    dist_ms[k] = times[k] + t_seam + t_local + t_final
-                    fin_parts[k] = (round(t_seam, 3), round(t_local, 3), round(t_final, 3))
-                    xbytes = max(xbytes, seam.numel() * 4 + nh_next * 4)
-                    seam_next = seam
+                        def final_fn():
+                            if nh_next:
+                                assert L.odc_slab_top_ids(ctx.handle, 0, nh_next, top.data_ptr()) == 0
+                            assert L.odc_slab_final(ctx.handle, 0, 0, ptr(halo), ptr(tri), ptr(pv), ptr(pc), ptr(pi)) == 0
+                        _, t_final = timed(torch, final_fn, reps=1)
+                        dist_ms[k] = times[k] + t_seam + t_local + t_final
+                        fin_parts[k] = (round(t_seam, 3), round(t_local, 3), round(t_final, 3))
+                        xbytes = max(xbytes, seam.numel() * 4 + nh_next * 4)
+                        seam_next = seam
                 xchg_ms = 2 * xbytes / (a.gather_gbs * 1e9) * 1e3 + 0.05  # two neighbour exchanges + all-gathers
                 dstep = max(dist_ms) + xchg_ms
                 print(f"    distributed finish: per-rank ms {np.round(dist_ms, 2).tolist()} + exchanges "
