@@ -310,3 +310,30 @@ def test_gpu_open_boundary_drops_unused_partitions(i):
     assert np.array_equal(res.mesh.vertices, o["vertices"])
     assert np.array_equal(res.raw_mesh.triangles, o["raw_triangles"])
     assert np.array_equal(res.raw_mesh.vertices, o["raw_vertices"])
+
+
+@pytest.mark.parametrize("R", [2, 3, 5])
+def test_gpu_tiny_grids_match_oracle(R):
+    """The smallest grids (R = 2: one interior vertex, every cell on the
+    boundary) against the oracle, mesh and statistics included."""
+    from paper_2409_13418_b200 import SphereField
+
+    field = SphereField((0.45, 0.52, 0.5), 0.3)
+    res = contour(field, GridSpec((0, 0, 0), (1, 1, 1), R))
+    o = oracle.contour_oracle(field, (0, 0, 0), (1, 1, 1), R)
+    assert np.array_equal(res.mesh.triangles, o["triangles"])
+    assert np.array_equal(res.mesh.vertices, o["vertices"])
+    assert res.stats["boundary_inside_vertices"] == o["boundary_inside"]
+
+
+def test_gpu_all_inside_and_resolution_limit():
+    """A field inside everywhere: no crossing, an empty mesh and the
+    boundary warning (pipeline.py:174-179); a resolution past the 32-bit
+    vertex-index space is refused with ValueError, not truncated."""
+    from paper_2409_13418_b200 import SphereField
+
+    full = contour(SphereField((0.5, 0.5, 0.5), 5.0), GridSpec((0, 0, 0), (1, 1, 1), 16))
+    assert full.mesh.n_triangles == 0 and full.stats["boundary_inside_vertices"] > 0
+    assert any("open boundary" in w for w in full.stats["warnings"])
+    with pytest.raises(ValueError, match="1290"):
+        contour(SphereField((0.5, 0.5, 0.5), 0.3), GridSpec((0, 0, 0), (1, 1, 1), 1300))
