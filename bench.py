@@ -34,6 +34,21 @@ sys.path.insert(0, str(REPO))
 METRIC = json.loads((REPO / "BASELINE.json").read_text())["metric"]
 
 
+def tri_bytes():
+    """PCIe bytes per copied triangle: int64 when the copy-back DMAs into
+    page-locked arrays (widened on the device), int32 otherwise (widened by
+    the host copy threads)."""
+    from paper_2409_13418_b200 import pipeline
+
+    try:
+        import torch
+
+        pinned = pipeline._PINNED_OUTPUT and torch.cuda.is_available()
+    except Exception:
+        pinned = False
+    return 24 if pinned else 12
+
+
 def workload(name):
     from paper_2409_13418_b200 import MlpField, scenes
 
@@ -317,9 +332,10 @@ def run_gpu(args, rank, world, dist):
         from paper_2409_13418_b200.fields import lower_program
 
         h2d = 136 * len(lower_program(field))
-    d2h = V * 24 + T * 12 + V * 24  # vertices f64, triangles i32 (widened to i64 by the host), provenance
+    tb = tri_bytes()
+    d2h = V * 24 + T * tb + V * 24  # vertices f64, triangles, provenance
     if res.raw_mesh is not res.mesh:
-        d2h += T * 12  # pre-repair triangles
+        d2h += T * tb  # pre-repair triangles
 
     # ---- roofline of the dominant kernel (grid labels)
     peaks, peak_kind = load_peaks()
@@ -474,7 +490,7 @@ def run_gpu_batch(args, rank, world, dist):
     if rank != 0:
         return
     cells = n * R**3
-    d2h = sum(r.mesh.n_vertices * 48 + r.mesh.n_triangles * 12 * (2 if r.raw_mesh is not r.mesh else 1)
+    d2h = sum(r.mesh.n_vertices * 48 + r.mesh.n_triangles * tri_bytes() * (2 if r.raw_mesh is not r.mesh else 1)
               for r in res)
     h2d = sum(len(lower_program(f)) * C.sizeof(_lib.Node) for f, _ in mine)  # the field programs
     cpu = None
@@ -576,7 +592,9 @@ def run_gpu_slabs(args, rank, world, dist):
         from paper_2409_13418_b200.fields import lower_program
 
         h2d = world * (136 * len(lower_program(field)) + p_h2d)
-    d2h = V * 24 + T * 12 + V * 24 + (T * 12 if res.raw_mesh is not res.mesh else 0) + world * p_d2h
+    # distributed finish: int32 triangles from rank 0's device buffers; central: the pipeline's copy-back
+    tb = 12 if finish_kind == "distributed" else tri_bytes()
+    d2h = V * 24 + T * tb + V * 24 + (T * tb if res.raw_mesh is not res.mesh else 0) + world * p_d2h
     roof = None
     if k_ms:
         peaks, peak_kind = load_peaks()
