@@ -449,13 +449,38 @@ void scan2(odc_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* oa, uint3
 // Drop unreferenced partition vertices (polygonize.py:199-209), then repair
 // non-manifold fans (polygonize.py:253-374, up to 4 passes).  verts holds P
 // partition vertices followed by NF fan vertices; used marks referenced ones.
+// tn_dev (optional): the triangle and fan-vertex totals [T, NF] on the device,
+// NF and T then being only upper bounds (the caller sized the mesh without
+// reading them back); the first synchronisation here brings the exact
+// values, with the statistics and (status) the device status to raise.
+// Returns the exact T and NF through T_out / NF_out.
 void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris, int64_t T, uint8_t* used,
-                 bool repair, odc_stats* st, DevStats* dst, unsigned long long* totals) {
+                 bool repair, odc_stats* st, DevStats* dst, unsigned long long* totals,
+                 const unsigned long long* tn_dev = nullptr, DevStatus* status = nullptr, int64_t* T_out = nullptr,
+                 int64_t* NF_out = nullptr) {
   cudaStream_t s = c->stream;
   launch_count_used(used, P, dst, s);
   check_launch(c);
   c->src0 = nullptr;
   int64_t V0 = P + NF;
+  // the first synchronisation's extra payload: exact totals, device status
+  auto queue_first = [&]() {
+    if (tn_dev)
+      CUDA_TRY(cudaMemcpyAsync(c->h_pinned + 40, tn_dev, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    if (status) CUDA_TRY(cudaMemcpyAsync(c->h_pinned + 256, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  };
+  auto take_first = [&]() {
+    if (status) {
+      DevStatus ds;
+      std::memcpy(&ds, c->h_pinned + 256, sizeof ds);
+      raise_device_status(c, ds);  // before anything trusts the sizes
+    }
+    if (tn_dev) {
+      T = (int64_t)c->h_pinned[40];
+      NF = (int64_t)c->h_pinned[41];
+      V0 = P + NF;
+    }
+  };
   // unused-vertex removal: drop partitions no triangle references
   auto compact = [&](int64_t used_p) {
     uint32_t* u32 = need(c->arena.get<uint32_t>(V0));
@@ -483,7 +508,9 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
   const bool run = repair && T > 0;
   if (!run) {
     CUDA_TRY(cudaMemcpyAsync(c->h_pinned + 8, dst, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    queue_first();
     CUDA_TRY(cudaStreamSynchronize(s));
+    take_first();
     const int64_t used_p = take_stats();
     if (used_p != P) compact(used_p);
   }
@@ -508,10 +535,10 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
       int32_t* inc = need(c->arena.get<int32_t>(3 * T));
       uint32_t* eoff = need(c->arena.get<uint32_t>(curV + 1));
       CUDA_TRY(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * 3 * (curV + 1), s));
-      launch_vertex_degree(cur, T, deg, s, dirty);
+      launch_vertex_degree(cur, T, deg, s, dirty, stats_pending ? tn_dev : nullptr);
       check_launch(c);
       scan1(c, deg, off, curV + 1, totals + 6);
-      launch_vertex_fill(cur, T, off, cursor, inc, s, dirty);
+      launch_vertex_fill(cur, T, off, cursor, inc, s, dirty, stats_pending ? tn_dev : nullptr);
       check_launch(c);
       launch_repair_count(cv, cur, curV, off, inc, extra, big, dst, s, dirty);
       check_launch(c);
@@ -521,11 +548,19 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
       CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[0], totals + 7, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaMemcpyAsync(&c->h_pinned[1], &dst->repair_overflow, sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s));
-      if (stats_pending)
+      if (stats_pending) {
         CUDA_TRY(cudaMemcpyAsync(c->h_pinned + 8, dst, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+        queue_first();
+      }
       CUDA_TRY(cudaStreamSynchronize(s));
       if (stats_pending) {
         stats_pending = false;
+        take_first();  // exact T, NF: vertex ids below P + NF are the same under the bound
+        curV = V0;
+        if (T == 0) {  // no triangle after all: nothing to repair
+          passes = 0;
+          break;
+        }
         const int64_t used_p = take_stats();
         if (used_p != P) {  // compact, then repair the compacted mesh from the start
           CUDA_TRY(cudaMemsetAsync(&dst->repair_overflow, 0, sizeof(unsigned long long), s));
@@ -582,6 +617,8 @@ void finish_mesh(odc_ctx* c, double* verts, int64_t P, int64_t NF, int32_t* tris
   st->n_vertices = curV;
   st->n_triangles = T;
   st->repair_added_vertices = curV - V0;
+  if (T_out) *T_out = T;
+  if (NF_out) *NF_out = NF;
 }
 
 // z-window of one extraction: owned cell layers [c0, c1) plus a one-layer
@@ -1138,15 +1175,26 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   launch_poly_classify(g, op, c->L, c->rec, ekey, K_own, co.pinfo, verts, pid4, c->kase, ntri, nfan, dst, s);
   check_launch(c);
   scan2(c, ntri, nfan, toff, frank, K_own, totals);
-  readback_checked(c, totals, 2 * sizeof(unsigned long long), status_pending);  // the 2D status is raised first
-  const int64_t T = (int64_t)c->h_pinned[0], NF = (int64_t)c->h_pinned[1];
+  // Small whole-grid extractions size the mesh by its bounds (a crossing
+  // edge emits at most 4 triangles and 1 fan vertex) and learn the exact
+  // totals at the repair's first synchronisation (finish_mesh), one host
+  // round trip fewer.  Past ~256 K edges the bounds double the repair's
+  // first pass (vertex range P + K instead of P + NF) -- more than a round
+  // trip costs -- and slabs and keep_intermediates need the totals here.
+  const bool lazy = !win.slab && !c->keep && K_own <= (int64_t(1) << 18);
+  int64_t T = 4 * K_own, NF = K_own;
+  if (!lazy) {
+    readback_checked(c, totals, 2 * sizeof(unsigned long long), status_pending);  // the 2D status is raised first
+    T = (int64_t)c->h_pinned[0];
+    NF = (int64_t)c->h_pinned[1];
+  }
   c->T = T;
   c->NF = NF;
   int32_t* tris = need(c->arena.get<int32_t>(3 * T));
   c->fan_edge = need(c->arena.get<int64_t>(NF));
   uint8_t* used = need(c->arena.get<uint8_t>(P + NF));
-  CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)(P + NF), s));
-  if (NF) CUDA_TRY(cudaMemsetAsync(used + P, 1, (size_t)NF, s));
+  CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)P, s));
+  if (NF) CUDA_TRY(cudaMemsetAsync(used + P, 1, (size_t)NF, s));  // fan vertices are always referenced
   launch_poly_emit(K_own, P, ekey, pid4, c->kase, toff, frank, epos, verts, tris, c->fan_edge, used, s);
   check_launch(c);
   if (c->keep) {
@@ -1189,7 +1237,15 @@ void extract(odc_ctx* c, const odc_field* f, const double lo[3], const double hi
   }
   // ---- unused-vertex removal + K8 repair (polygonize.py:199-209, :253-374)
   mark(6);
-  finish_mesh(c, verts, P, NF, tris, T, used, o->repair != 0, st, dst, totals);
+  {
+    int64_t Tx = T, NFx = NF;
+    // totals[0..1] (triangle / fan totals of the scan above) are not touched by
+    // finish_mesh's scans (totals + 5..7)
+    finish_mesh(c, verts, P, NF, tris, T, used, o->repair != 0, st, dst, totals, lazy ? totals : nullptr,
+                lazy ? status_pending : nullptr, &Tx, &NFx);
+    c->T = Tx;
+    c->NF = NFx;
+  }
   mark(7);
   finish_stats();
   c->valid = true;

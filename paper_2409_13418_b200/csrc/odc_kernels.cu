@@ -2402,29 +2402,32 @@ constexpr int kMaxFan = 64;
 
 // Vertex -> incident-triangle CSR.  dirty (repair passes after the first):
 // only the fans of flagged vertices, the only ones the pass examines.
+// T_dev: the triangle count on the device (T is then only the launch's
+// upper bound: the extraction sized the mesh before reading its totals back)
 __global__ void k_vertex_degree(const int32_t* __restrict__ tris, int64_t T, uint32_t* __restrict__ deg,
-                                const uint8_t* __restrict__ dirty) {
+                                const uint8_t* __restrict__ dirty, const unsigned long long* __restrict__ T_dev) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 3 * T) return;
+  if (i >= 3 * (T_dev ? (int64_t)*T_dev : T)) return;
   const int32_t v = tris[i];
   if (!dirty || dirty[v]) atomicAdd(&deg[v], 1u);
 }
-void launch_vertex_degree(const int32_t* tris, int64_t T, uint32_t* deg, cudaStream_t s, const uint8_t* dirty) {
-  if (T) k_vertex_degree<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, deg, dirty);
+void launch_vertex_degree(const int32_t* tris, int64_t T, uint32_t* deg, cudaStream_t s, const uint8_t* dirty,
+                          const unsigned long long* T_dev) {
+  if (T) k_vertex_degree<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, deg, dirty, T_dev);
 }
 __global__ void k_vertex_fill(const int32_t* __restrict__ tris, int64_t T, const uint32_t* __restrict__ off,
                               uint32_t* __restrict__ cursor, int32_t* __restrict__ inc,
-                              const uint8_t* __restrict__ dirty) {
+                              const uint8_t* __restrict__ dirty, const unsigned long long* __restrict__ T_dev) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 3 * T) return;
+  if (i >= 3 * (T_dev ? (int64_t)*T_dev : T)) return;
   const int32_t v = tris[i];
   if (dirty && !dirty[v]) return;
   const uint32_t slot = atomicAdd(&cursor[v], 1u);
   inc[off[v] + slot] = (int32_t)(i / 3);
 }
 void launch_vertex_fill(const int32_t* tris, int64_t T, const uint32_t* off, uint32_t* cursor, int32_t* inc,
-                        cudaStream_t s, const uint8_t* dirty) {
-  if (T) k_vertex_fill<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, off, cursor, inc, dirty);
+                        cudaStream_t s, const uint8_t* dirty, const unsigned long long* T_dev) {
+  if (T) k_vertex_fill<<<grid_for(3 * T, 256), 256, 0, s>>>(tris, T, off, cursor, inc, dirty, T_dev);
 }
 
 // Scratch of one fan (nt incident triangles).  Fans of up to kMaxFan

@@ -178,11 +178,11 @@ void launch_split_cases(int64_t K, const uint8_t* kase, int64_t* out, uint32_t* 
 void launch_interior_flags(int64_t K, const uint8_t* kase, uint32_t* flag, cudaStream_t s);
 
 // K8: non-manifold repair (polygonize.py:220-374)
+// T_dev (optional): the count on the device, T then only bounds the launch
 void launch_vertex_degree(const int32_t* tris, int64_t T, uint32_t* deg, cudaStream_t s,
-                          const uint8_t* dirty = nullptr);
+                          const uint8_t* dirty = nullptr, const unsigned long long* T_dev = nullptr);
 void launch_vertex_fill(const int32_t* tris, int64_t T, const uint32_t* off, uint32_t* cursor, int32_t* inc,
-                        cudaStream_t s,
-                        const uint8_t* dirty = nullptr);
+                        cudaStream_t s, const uint8_t* dirty = nullptr, const unsigned long long* T_dev = nullptr);
 // big: per-incidence scratch for fans of more than 64 triangles (nullptr: such
 // vertices are counted in DevStats::repair_overflow and skipped; the host
 // then re-runs with repair_scratch_bytes(T) of scratch)
