@@ -337,3 +337,29 @@ def test_gpu_all_inside_and_resolution_limit():
     assert any("open boundary" in w for w in full.stats["warnings"])
     with pytest.raises(ValueError, match="1290"):
         contour(SphereField((0.5, 0.5, 0.5), 0.3), GridSpec((0, 0, 0), (1, 1, 1), 1300))
+
+
+def test_gpu_output_arrays_are_independent():
+    """The mesh arrays come from recycled page-locked blocks: results of
+    successive calls must not alias (a block is reused only after every
+    array of the previous result is gone), stay valid after later
+    extractions, and be ordinary writable numpy arrays of the reference's
+    dtypes."""
+    import gc
+
+    from paper_2409_13418_b200 import SphereField, TorusField
+
+    g = GridSpec((0, 0, 0), (1, 1, 1), 48)
+    a = contour(SphereField((0.5, 0.5, 0.5), 0.3), g)
+    va, ta = a.mesh.vertices.copy(), a.mesh.triangles.copy()
+    b = contour(TorusField((0.5, 0.5, 0.5), 0.25, 0.08), g)
+    assert not np.shares_memory(a.mesh.vertices, b.mesh.vertices)
+    assert np.array_equal(a.mesh.vertices, va) and np.array_equal(a.mesh.triangles, ta)
+    assert a.mesh.vertices.dtype == np.float64 and a.mesh.triangles.dtype == np.int64
+    assert a.mesh.provenance_kind.dtype == np.int64 and a.mesh.provenance_ref.dtype == np.int64
+    a.mesh.vertices[0, 0] += 1.0  # writable
+    del b
+    gc.collect()
+    c = contour(SphereField((0.5, 0.5, 0.5), 0.3), g)  # may reuse b's block, never a's
+    assert not np.shares_memory(a.mesh.vertices, c.mesh.vertices)
+    assert np.array_equal(c.mesh.vertices, va) and np.array_equal(c.mesh.triangles, ta)
