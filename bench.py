@@ -395,7 +395,7 @@ def run_gpu(args, rank, world, dist):
         "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16+f64" if is_mlp(field) else "f64", "data": "synthetic",
-        "config": {"workload": desc, "R": R, "cells": R**3, "parallelism": f"replicas x{world}",
+        "config": {"workload": desc, "R": R, "cells": R**3, "parallelism": f"whole-grid extraction x{world}",
                    "l2": "flushed (512 MiB write) before every step, outside its CUDA-event pair",
                    "evals_per_step": total_evals},
         "e2e": {"value": world * R**3 / (e2e_step / 1e3), "unit": "cells/s", "ms_per_step": e2e_step,
