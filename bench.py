@@ -161,9 +161,14 @@ def cpu_sample(field, lo, hi, R_full, full_evals, sample_R=None, cache=None):
     cores = len(os.sched_getaffinity(0))
     mlp = is_mlp(field)
     sR = (cache or {}).get("sample_r") or sample_R or (64 if mlp else min(R_full, 384))
-    t0 = time.perf_counter()
-    o = oracle.contour_oracle(field, lo, hi, sR)
-    dt = time.perf_counter() - t0
+    # every host core for the BLAS of the numpy MlpField, whatever the launcher
+    # set (torchrun exports OMP_NUM_THREADS=1 to each rank)
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=cores, user_api="blas"):
+        t0 = time.perf_counter()
+        o = oracle.contour_oracle(field, lo, hi, sR)
+        dt = time.perf_counter() - t0
     if not mlp:
         cores = 1
     impl = ("oracle pipeline (C, 1 thread) + numpy fp32 MlpField (OpenBLAS, %d threads)" % cores if mlp
